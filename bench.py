@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""Headline benchmark: batched incircle RayCast, SURVEY.md §8(d) config 2.
+
+Workload (BASELINE.json configs[1]): N=20,000 generators uniform in [0,1]^6
+(default_rng(0)), 1,000,000 rays per GPU.  Ray k starts at the Voronoi vertex
+reached by `descent` from generator s[p_k] (s = default_rng(1).choice(20000,
+10000), p = default_rng(2).integers), with direction default_rng(3) normal
+normalised, entering cell g = argmax_{s in sigma} u.x_s (eta = (g,)).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`ours`: one step = one fused RayCast launch (+ its exact re-check pass) over
+the rank's 1e6 HBM-resident rays; value = all ranks' rays / max-over-ranks
+device time.  `e2e` repeats the step through the public host-array API
+(pinned host rays in, idx/t/rp/flag back out, copies inside the timed region).
+`reference`: the reference's CPU algorithm (the oracle port of
+raycast_incircle, kd-tree probe as in the reference for N > 2048) on all host
+cores, on a bounded sample of the same rays per step.
+"""
+
+import os
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # CPU legs: one BLAS thread per process
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import multiprocessing as mp  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import threading  # noqa: E402
+import time  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_GEN, DIM, N_POOL, RAYS_PER_GPU = 20000, 6, 10000, 1_000_000
+METRIC = "RayCast rays/sec (config 2: d=6, N=20000)"
+FLOP_PER_PAIR = 2 * DIM + 2  # incircle-sphere test: one d-dot + one FMA per (ray, generator)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--rays", type=int, default=RAYS_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rays-per-core", type=int, default=3000)
+    return ap.parse_args()
+
+
+def generators():
+    return np.random.default_rng(0).random((N_GEN, DIM))
+
+
+def ray_recipe(n_total):
+    """Start pool indices, pool pick per ray, unit directions (first 1e6 rays
+    are exactly config 2; further ranks extend the same streams)."""
+    s = np.random.default_rng(1).choice(N_GEN, N_POOL, replace=False)
+    p = np.random.default_rng(2).integers(0, N_POOL, n_total)
+    u = np.random.default_rng(3).standard_normal((n_total, DIM))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    return s, p, u
+
+
+def assemble(pts, pool_sig, pool_r, p, u):
+    x = pool_r[p]
+    sig = pool_sig[p]
+    proj = np.einsum("kd,ksd->ks", u, pts[sig])
+    g = sig[np.arange(len(p)), np.argmax(proj, axis=1)].astype(np.int32)
+    return np.ascontiguousarray(x), np.ascontiguousarray(u), np.ascontiguousarray(g[:, None])
+
+
+# --------------------------------------------------------------------------
+# CPU legs (oracle port of the reference algorithm; test infrastructure)
+# --------------------------------------------------------------------------
+_W = {}
+
+
+def _w_init(pts):
+    from oracle import voronray_oracle as orc
+    _W["orc"] = orc
+    _W["nodes"] = orc.Nodes(pts)
+
+
+def _w_descent(start):
+    orc = _W["orc"]
+    sig, r = orc.descent(_W["nodes"], int(start), orc.stream(0, "descent", int(start)))
+    return sig, r
+
+
+def _w_rays(args):
+    x, u, g = args
+    orc = _W["orc"]
+    out = np.full(len(g), -1, dtype=np.int64)
+    for k in range(len(g)):
+        res = orc.raycast(_W["nodes"], (int(g[k]),), x[k], u[k])
+        if res is not None:
+            out[k] = [s for s in res[0] if s != int(g[k])][0]
+    return out
+
+
+def cpu_pool(pts, cores):
+    ctx = mp.get_context("fork")
+    return ctx.Pool(cores, initializer=_w_init, initargs=(pts,))
+
+
+def cpu_rays(pool, x, u, g, cores):
+    chunks = max(1, cores * 4)
+    bounds = np.linspace(0, len(g), chunks + 1).astype(int)
+    jobs = [(x[a:b], u[a:b], g[a:b, 0]) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+    t0 = time.perf_counter()
+    parts = pool.map(_w_rays, jobs)
+    return np.concatenate(parts), time.perf_counter() - t0
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md clocks line)
+# --------------------------------------------------------------------------
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.3)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+def fp64_peak(torch, L, _lib):
+    """DFMA pipe peak measured live (MEASURED_PEAKS.json has no FP64 figure)."""
+    scratch = torch.empty(16, dtype=torch.float64, device="cuda")
+    sm = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, iters = sm * 8, 4096
+    best = 0.0
+    sh = _lib.stream_handle()
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(L.vr_fma_probe(0, blocks, iters, _lib.ptr(scratch), sh))
+        e1.record()
+        e1.synchronize()
+        best = max(best, 4096.0 * iters * blocks / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    return best
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2405_10050_b200 as vb
+    from paper_2405_10050_b200 import _lib
+    from paper_2405_10050_b200.raycast import HostRaycaster, Workspace
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = _lib.lib()
+
+    pts = generators()
+    ns = vb.build_node_set(pts)
+    n = args.rays
+    s, p_all, u_all = ray_recipe(n * world)
+    lo, hi = rank * n, (rank + 1) * n
+    # vertex pool: the reference descent (same host RNG streams), run on the GPU
+    need = np.unique(p_all[lo:hi])
+    t0 = time.perf_counter()
+    sig_n, r_n = vb.descent_batch(ns, s[need], seed=0)
+    t_pool = time.perf_counter() - t0
+    pool_sig = np.zeros((N_POOL, DIM + 1), dtype=np.int32)
+    pool_r = np.zeros((N_POOL, DIM))
+    pool_sig[need], pool_r[need] = sig_n, r_n
+    x, u, g = assemble(pts, pool_sig, pool_r, p_all[lo:hi], u_all[lo:hi])
+
+    dev = torch.device("cuda", local)
+    xd, ud, gd = (torch.from_numpy(a).to(dev) for a in (x, u, g))
+    out = dict(idx=torch.empty(n, dtype=torch.int32, device=dev),
+               t=torch.empty(n, dtype=torch.float64, device=dev),
+               rp=torch.empty((n, DIM), dtype=torch.float64, device=dev),
+               flag=torch.empty(n, dtype=torch.uint8, device=dev))
+    ws = Workspace()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)]
+          for _ in range(args.warmup + args.steps)]
+
+    def step(i):
+        flush.fill_(i & 0xFF)  # L2 flush, outside the timed events
+        vb.raycast_batch(ns, xd, ud, gd, out=out, workspace=ws, events=ev[i])
+
+    for i in range(args.warmup):
+        step(i)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for i in range(args.warmup, args.warmup + args.steps):
+            step(i)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [ev[i][0].elapsed_time(ev[i][2]) for i in range(args.warmup, args.warmup + args.steps)]
+    kern_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(args.warmup, args.warmup + args.steps)]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    value = world * n * args.steps / (total_ms * 1e-3)
+
+    # correctness guard on the timed outputs (cheap, outside the timing)
+    flags = out["flag"].cpu().numpy()
+    n_deg = int((flags == 3).sum())
+    n_esc = int((flags == 1).sum())
+
+    # ---- e2e through the public host-array API ----------------------------
+    hr = HostRaycaster(ns, n, 1)
+    hx, hu, hg = (HostRaycaster.pinned(a.shape, t) for a, t in
+                  ((x, torch.float64), (u, torch.float64), (g, torch.int32)))
+    hx.copy_(torch.from_numpy(x))
+    hu.copy_(torch.from_numpy(u))
+    hg.copy_(torch.from_numpy(g))
+    hidx = HostRaycaster.pinned((n,), torch.int32)
+    ht = HostRaycaster.pinned((n,), torch.float64)
+    hrp = HostRaycaster.pinned((n, DIM), torch.float64)
+    hfl = HostRaycaster.pinned((n,), torch.uint8)
+    for _ in range(max(1, args.warmup)):
+        hr.run(hx, hu, hg, hidx, ht, hrp, hfl)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        hr.run(hx, hu, hg, hidx, ht, hrp, hfl)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = world * n * args.steps / (float(e2e_t.item()) * 1e-3)
+    assert np.array_equal(hidx.numpy(), out["idx"].cpu().numpy()), "e2e result differs"
+    h2d = x.nbytes + u.nbytes + g.nbytes
+    d2h = n * (4 + 8 + 8 * DIM + 1)
+
+    result = None
+    if rank == 0:
+        peak = fp64_peak(torch, L, _lib)
+        kms = float(np.mean(kern_ms))
+        pairs = n * N_GEN
+        achieved = pairs * FLOP_PER_PAIR / (kms * 1e-3) / 1e12
+        result = {
+            "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded config-2 recipe, SURVEY.md §8(d))",
+            "config": {"workload": "config2: batched RayCast N=20000 d=6, 1e6 rays/GPU from "
+                                   "descent vertices, eta=(g,)",
+                       "n_generators": N_GEN, "d": DIM, "rays_per_gpu": n,
+                       "parallelism": f"ray-sharded x{world}, generators replicated",
+                       "l2": "flushed between timed steps (256 MB write, untimed)"},
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                         "kernel": "k_raycast<6,3,128,128,4>", "kernel_ms": kms,
+                         "flop_per_pair": FLOP_PER_PAIR,
+                         "peak_source": "measured live: DFMA probe (vr_fma_probe), "
+                                        "MEASURED_PEAKS.json has no FP64 figure"},
+            "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "api": "HostRaycaster.run (pinned host arrays)"},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clk.summary(),
+            "checks": {"escaped": n_esc, "degenerate": n_deg, "pool_build_s": t_pool},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            cores = host_cores()
+            m = min(n, args.cpu_rays_per_core * cores)
+            pool = cpu_pool(pts, cores)
+            try:
+                cpu_idx, wall = cpu_rays(pool, x[:m], u[:m], g[:m], cores)
+            finally:
+                pool.close()
+                pool.join()
+            agree = float(np.mean(cpu_idx == out["idx"].cpu().numpy()[:m]))
+            result["cpu_baseline"] = {
+                "value": m / wall, "unit": "rays/s", "cores": cores, "kind": "port",
+                "sample": f"first {m} config-2 rays, oracle raycast (kd-tree probe loop), "
+                          f"{cores} processes", "index_agreement": agree}
+    if world > 1:
+        dist.destroy_process_group()
+    return result
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    cores = host_cores()
+    pts = generators()
+    m = min(args.rays, args.cpu_rays_per_core * cores)
+    s, p_all, u_all = ray_recipe(m * (args.warmup + args.steps))
+    pool = cpu_pool(pts, cores)
+    try:
+        need = np.unique(p_all)
+        res = pool.map(_w_descent, s[need], chunksize=max(1, len(need) // (cores * 4)))
+        pool_sig = np.zeros((N_POOL, DIM + 1), dtype=np.int32)
+        pool_r = np.zeros((N_POOL, DIM))
+        for k, (sg, r) in zip(need, res):
+            pool_sig[k], pool_r[k] = sg, r
+        times = []
+        for i in range(args.warmup + args.steps):
+            sl = slice(i * m, (i + 1) * m)
+            x, u, g = assemble(pts, pool_sig, pool_r, p_all[sl], u_all[sl])
+            _, wall = cpu_rays(pool, x, u, g, cores)
+            if i >= args.warmup:
+                times.append(wall)
+    finally:
+        pool.close()
+        pool.join()
+    value = m * args.steps / sum(times)
+    return {"metric": METRIC, "value": value, "unit": "rays/s", "impl": "reference",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded config-2 recipe)",
+            "config": {"workload": "config2: batched RayCast N=20000 d=6", "n_generators": N_GEN,
+                       "d": DIM, "rays_per_step": m},
+            "cpu_baseline": {"value": value, "unit": "rays/s", "cores": cores, "kind": "port",
+                             "sample": f"{m} config-2 rays per step, oracle restatement of "
+                                       "raycast_incircle (kd-tree probe loop, scipy cKDTree)"},
+            "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,249 @@
+/*
+ * voronray_b200.h -- C ABI of the B200-native incircle RayCast library.
+ *
+ * The reference (`voronray`, pure Python + numpy/scipy) has no FFI layer: its
+ * drop-in boundary is the public Python API (pkg/src/voronray/__init__.py:3-32).
+ * Every entry point below replaces one inner operation of that API; the
+ * reference function each one stands in for is cited per declaration.
+ *
+ * Conventions (all entry points):
+ *   - plain device pointers + sizes, no framework types;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *   - stream-ordered, reentrant across streams, no persistent allocation
+ *     (callers pass workspaces), no host synchronisation unless stated;
+ *   - return 0 (VR_OK) or a negative vr_status / -(1000 + cudaError_t).
+ *   - generator indices are 0-based int32 (reference core.py:7).
+ *
+ * Per-ray flags (uint8):  0 VR_RAY_OK, 1 VR_RAY_ESCAPED (reference: `None`,
+ *   raycast.py:190-191), 2 VR_RAY_RECHECK (internal; resolved by
+ *   vr_raycast_recheck), 3 VR_RAY_DEGENERATE (reference raises
+ *   DegenerateConfiguration, raycast.py:216-219).
+ */
+#ifndef VORONRAY_B200_H
+#define VORONRAY_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum vr_status {
+  VR_OK = 0,
+  VR_EINVAL = -1,         /* bad size / null pointer / unsupported d          */
+  VR_EDIM = -2,           /* d outside [2, 8]                                 */
+  VR_ECAPACITY = -3,      /* a caller-sized workspace / table is too small    */
+  VR_ECUDA_BASE = -1000   /* -(1000 + cudaError_t)                            */
+};
+
+enum vr_ray_flag {
+  VR_RAY_OK = 0,
+  VR_RAY_ESCAPED = 1,
+  VR_RAY_RECHECK = 2,
+  VR_RAY_DEGENERATE = 3
+};
+
+/* MC per-cell status (reference integrate_mc.py:63-64,184-187). */
+enum vr_cell_status {
+  VR_CELL_OK = 0,
+  VR_CELL_UNBOUNDED = 1,   /* reference raises UnboundedRay(cell, direction)   */
+  VR_CELL_DEGENERATE = 2,  /* reference raises DegenerateConfiguration         */
+  VR_CELL_OVERFLOW = 3     /* more distinct hit faces than area slots          */
+};
+
+int vr_abi_version(void);
+const char* vr_status_string(int status);
+
+/* Record stride (doubles) of one packed generator for dimension d:
+ * [x_0 .. x_{d-1}, |x|^2, pad] rounded up to an even count (16-B rows). */
+int vr_record_stride(int d);
+
+/* Pack an (n, d) fp64 row-major point array into 16-B aligned records
+ * [x, |x|^2, pad].  Replaces the NodeSet fp64 copy + squared norms
+ * (reference core.py:44-51).  rec must hold n * vr_record_stride(d) doubles. */
+int vr_pack_generators(const double* pts, int64_t n, int d, double* rec,
+                       double* sqmax_out /* device, 1 double */, void* stream);
+
+/* Batched incircle RayCast (reference raycast_incircle, raycast.py:154-224,
+ * with its filtered NN probe _Probe, raycast.py:85-151, core.py:62-103).
+ *
+ * Ray k starts at x[k*d..] (equidistant to its eta generators), travels along
+ * unit u[k*d..], and carries eta[k*eta_len .. +eta_len] (eta_len in [1, d]).
+ * Candidate i is valid iff u.x_i > max_{e in eta} u.x_e + 1e-12*max(1,|.|)
+ * (raycast.py:95-96, 110-117); the result is the valid i minimising
+ * t_i = (|x_i-x|^2 - |x_g-x|^2) / (2 u.(x_i-x_g)), g = eta[0] (raycast.py:203),
+ * smallest index on ties, or ESCAPED when no candidate is valid.
+ *
+ * cand (nullable, n_cand entries, ascending or not) restricts the search to a
+ * subset like the reference `candidates=` argument (raycast.py:100-102);
+ * cand_rec must then hold the packed records of exactly those generators.
+ *
+ * Outputs: out_idx (global generator index, -1 on escape), out_t (ray
+ * parameter from the reference's centred formula), out_rp (nullable; x+t*u),
+ * out_flag.  Rays left in VR_RAY_RECHECK must be passed through
+ * vr_raycast_recheck (done internally by vr_raycast_resolve).
+ * recheck_list/recheck_count: workspace (n_rays int32 + 1 int32, device),
+ * receives the ids of RECHECK rays (the count is zeroed on `stream` first);
+ * may be NULL if the caller does not resolve. */
+int vr_raycast_batch(const double* rec, int64_t n_gen, int d, double sqmax,
+                     const double* cand_rec, const int32_t* cand, int64_t n_cand,
+                     const double* x, const double* u,
+                     const int32_t* eta, int eta_len, int64_t n_rays,
+                     int32_t* out_idx, double* out_t, double* out_rp,
+                     uint8_t* out_flag, int32_t* recheck_list,
+                     int32_t* recheck_count, void* stream);
+
+/* Exact re-evaluation of the rays listed in recheck_list[0 .. *count)
+ * (count read on device): centred t for every candidate, argmin with the
+ * smallest-index tie-break, then the reference's runner-up degeneracy band
+ * second < radius*(1+1e-10) (raycast.py:211-219).  max_list bounds the
+ * launch (pass n_rays). */
+int vr_raycast_recheck(const double* rec, int64_t n_gen, int d,
+                       const double* cand_rec, const int32_t* cand, int64_t n_cand,
+                       const double* x, const double* u,
+                       const int32_t* eta, int eta_len,
+                       const int32_t* recheck_list, const int32_t* recheck_count,
+                       int64_t max_list,
+                       int32_t* out_idx, double* out_t, double* out_rp,
+                       uint8_t* out_flag, void* stream);
+
+/* Filtered nearest neighbour for a batch of queries (reference
+ * NodeSet.nearest / nearest2, core.py:62-142): smallest squared distance
+ * (expanded form, smallest index on ties, core.py:81-90), skip mask per
+ * generator (nullable, uint8, 1 = excluded).  out_d1/out_d2 are the clean
+ * Euclidean distances of the nearest and second-nearest (inf if absent),
+ * out_idx -1 when every generator is skipped. */
+int vr_nearest_batch(const double* rec, int64_t n_gen, int d,
+                     const double* q, int64_t n_q, const uint8_t* skip,
+                     int32_t* out_idx, double* out_d1, double* out_d2,
+                     void* stream);
+
+/* Vertex invariants (reference verify_vertex, core.py:279-296) for a batch:
+ * equidistance within tol*rad and no foreign generator closer than
+ * rad*(1-tol).  sigma is (n_v, d+1) int32, r is (n_v, d) fp64.
+ * out_ok[v] = 1 when both hold. */
+int vr_verify_vertices(const double* rec, int64_t n_gen, int d,
+                       const int32_t* sigma, const double* r, int64_t n_v,
+                       double tol, uint8_t* out_ok, void* stream);
+
+/* fp64 circumcentres of generator tuples (reference graph.py:163-171 and
+ * SURVEY.md §8(c) rule 3): solve 2(x_s - x_s0).y = |x_s - x_s0|^2 with
+ * partial-pivot LU in registers, r = x_s0 + y.  out_ok = 0 when singular. */
+int vr_circumcenters(const double* rec, int d, const int32_t* sigma,
+                     int64_t n_v, double* out_r, uint8_t* out_ok, void* stream);
+
+/* Outward edge directions of vertices (reference _vertex_directions,
+ * raycast.py:345-378): column k-1 of -D^{-1} (k>0) or the row sums of D^{-1}
+ * (k=0), D rows x_s - x_s0, normalised.  out_u is (n_v, d+1, d);
+ * out_ok[v*(d+1)+k] = 0 on a singular / non-finite direction. */
+int vr_vertex_directions(const double* rec, int d, const int32_t* sigma,
+                         int64_t n_v, double* out_u, uint8_t* out_ok,
+                         void* stream);
+
+/* ---- Monte-Carlo cell volumes / interface areas (reference mc_areas_only,
+ *      integrate_mc.py:124-161, _mc_areas_batch :164-197) -------------------
+ *
+ * Rays: n_cells cells (cells[c] = generator index) x rays_per_cell rays.
+ * Directions come either from `dirs` ((n_cells*rays_per_cell, d) fp64, raw
+ * Gaussian draws normalised on device exactly as sample_unit_sphere,
+ * integrate_mc.py:51-56) or, when dirs == NULL, from the Philox4x32-10
+ * stream keyed by `seed` with counter (ray, cell, block) + Box-Muller.
+ *
+ * vr_mc_rays writes per-ray hit index / t / flag (same meaning as the
+ * RayCast outputs).  vr_mc_reduce then forms, per cell, in ray order:
+ *   length = |(x_c + t y) - x_c|, w = length^(d-1)/cos(n_cj, y),
+ *   area[j] = sum w * S_{d-1}/n, volume = sum length^d * S_{d-1}/(d n)
+ * (integrate_mc.py:150-160), with areas as a per-cell list of (j, area)
+ * sorted by j in slots [c*max_faces, c*max_faces + out_nfaces[c]).
+ * out_status[c] / out_first_bad[c] report the first escaping (UnboundedRay)
+ * or degenerate ray of the cell in ray order; degenerate rays count only when
+ * degenerate_is_error (the per-ray path raises, the neighbour-batch path
+ * _mc_areas_batch takes the plain argmin).  surf = S_{d-1} as computed by the
+ * caller (integrate_mc.py:44-48); max_faces <= 512. */
+int vr_mc_rays(const double* rec, int64_t n_gen, int d, double sqmax,
+               const double* cand_rec, const int32_t* cand, int64_t n_cand,
+               const int32_t* cells, int64_t n_cells, int64_t rays_per_cell,
+               const double* dirs, uint64_t seed,
+               int32_t* out_idx, double* out_t, uint8_t* out_flag,
+               int32_t* recheck_list, int32_t* recheck_count, void* stream);
+
+int vr_mc_recheck(const double* rec, int64_t n_gen, int d,
+                  const double* cand_rec, const int32_t* cand, int64_t n_cand,
+                  const int32_t* cells, int64_t rays_per_cell,
+                  const double* dirs, uint64_t seed,
+                  const int32_t* recheck_list, const int32_t* recheck_count,
+                  int64_t max_list, int32_t* out_idx, double* out_t,
+                  uint8_t* out_flag, void* stream);
+
+int vr_mc_reduce(const double* rec, int d, const int32_t* cells,
+                 int64_t n_cells, int64_t rays_per_cell, const double* dirs,
+                 uint64_t seed, const int32_t* ray_idx, const double* ray_t,
+                 const uint8_t* ray_flag, int max_faces,
+                 int degenerate_is_error, double surf,
+                 double* out_volume, int32_t* out_face_j, double* out_face_area,
+                 int32_t* out_nfaces, int32_t* out_status,
+                 int64_t* out_first_bad, double* out_samples /* nullable */,
+                 void* stream);
+
+/* Export the unit directions the Philox path uses (for RNG replay into the
+ * reference, SURVEY.md §8(c) rule 4): raw Gaussian draws z, (n, d) fp64. */
+int vr_mc_directions(int d, int64_t n_cells, const int32_t* cells,
+                     int64_t rays_per_cell, uint64_t seed, double* out_z,
+                     void* stream);
+
+/* ---- Level-synchronous traversal (reference voronoi_graph DFS,
+ *      graph.py:88-146, reformulated per SURVEY.md §7 K2) -------------------
+ * Tables are open-addressed on the device; capacities are powers of two. */
+typedef struct vr_traverse_tables {
+  int32_t* vkeys;   /* vcap * (d+1) sorted sigma keys                        */
+  int32_t* vstate;  /* vcap: 0 empty, 1 writing, 2 ready                     */
+  int32_t* vval;    /* vcap: winning ray id of the current level / vertex id */
+  int64_t vcap;
+  int32_t* ekeys;   /* ecap * d sorted eta keys                              */
+  int32_t* estate;  /* ecap                                                  */
+  int32_t* ecount;  /* ecap: number of discovered incident vertices          */
+  int64_t ecap;
+  int32_t* overflow;/* 1 int32: set when a probe sequence exhausts a table   */
+} vr_traverse_tables;
+
+/* Register vertices (sigma (n_v, d+1) sorted, ids base_id..) in the vertex
+ * table and bump the edge counters of their d+1 edges (graph.py:115-120). */
+int vr_trav_insert_vertices(const vr_traverse_tables* tab, int d,
+                            const int32_t* sigma, int64_t n_v, int32_t base_id,
+                            void* stream);
+
+/* Expand a frontier: for every vertex and position k whose edge
+ * sigma\sigma[k] has count < 2 (graph.py:127-135), emit one ray
+ * (x = r, u = direction, eta = sigma\sigma[k]).  Writes per-(vertex,k) open
+ * flags to open_mask (n_v*(d+1) uint8); rays are compacted by the caller
+ * (prefix sum) and emitted by vr_trav_emit_rays. */
+int vr_trav_open_edges(const vr_traverse_tables* tab, int d,
+                       const int32_t* sigma, int64_t n_v, uint8_t* open_mask,
+                       void* stream);
+
+int vr_trav_emit_rays(const double* rec, int d, const int32_t* sigma,
+                      const double* r, int64_t n_v, const uint8_t* open_mask,
+                      const int64_t* open_offset, double* ray_x,
+                      double* ray_u, int32_t* ray_eta, int32_t* ray_parent,
+                      uint8_t* ray_ok, void* stream);
+
+/* Claim new vertices: for each ray with a hit, sigma' = sorted(eta + {i});
+ * insert-or-find in the vertex table and keep the smallest ray id per new
+ * key (deterministic winner).  new_flag[k] = 1 iff ray k is the winner of a
+ * key that was absent before this level.  out_sigma receives sigma'. */
+int vr_trav_claim(const vr_traverse_tables* tab, int d, const int32_t* ray_eta,
+                  const int32_t* hit_idx, const uint8_t* hit_flag,
+                  int64_t n_rays, int32_t level_tag, int32_t* out_sigma,
+                  int32_t* out_slot, uint8_t* new_flag, void* stream);
+
+/* Roofline probe: `blocks` x 256 threads x iters x 8 independent FMA chains
+ * (dtype 0 = fp64 DFMA, 1 = fp32 FFMA); flops = 4096 * iters * blocks.  Used
+ * by bench.py to measure the FP64/FP32 pipe peaks live (MEASURED_PEAKS.json
+ * has only HBM and bf16). */
+int vr_fma_probe(int dtype, int blocks, int iters, void* scratch, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VORONRAY_B200_H */

@@ -1,0 +1,32 @@
+"""B200-native incircle RayCast, traversal and Monte-Carlo integration.
+
+Drop-in for the hot path of the reference package ``voronray``
+(pkg/src/voronray/__init__.py:3-32): the RayCast, full-diagram traversal and
+MC volume/area entry points keep their names, arguments, return types and
+exceptions, and run as hand-written sm_100a kernels behind a C-ABI library
+(include/voronray_b200.h) loaded with ctypes.  There is no CPU fallback.
+"""
+
+from . import errors, rng
+from .core import (TOL_VERTEX, TOL_DEGENERATE, HALFSPACE_SLACK, BoundaryRay, Mesh, NodeSet,
+                   VertexRecord, build_node_set, edge_keys, nearest_neighbor, verify_vertex,
+                   verify_vertices)
+from .raycast import (RayQuery, RaycastBatch, RaycastStats, initial_heuristic, project_t,
+                      raycast_batch, raycast_incircle, search_direction, vertex_directions_batch)
+from .graph import (DESCENT_RETRIES, VerifyReport, brute_force_vertices, circumcenters, descent,
+                    descent_batch, edge_set, verify_mesh, voronoi_graph)
+from .integrate_mc import (CellIntegrals, Integrand, MCResult, mc_areas_only, mc_cells,
+                           mc_directions, sample_unit_sphere, sphere_surface_area)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Mesh", "NodeSet", "VertexRecord", "BoundaryRay", "build_node_set", "nearest_neighbor",
+    "verify_vertex", "verify_vertices", "TOL_VERTEX", "TOL_DEGENERATE", "HALFSPACE_SLACK",
+    "edge_keys", "RayQuery", "RaycastStats", "RaycastBatch", "project_t", "initial_heuristic",
+    "raycast_incircle", "raycast_batch", "search_direction", "vertex_directions_batch",
+    "edge_set", "descent", "descent_batch", "voronoi_graph", "verify_mesh", "VerifyReport",
+    "brute_force_vertices", "circumcenters", "DESCENT_RETRIES", "CellIntegrals", "Integrand",
+    "MCResult", "sample_unit_sphere", "sphere_surface_area", "mc_areas_only", "mc_cells",
+    "mc_directions", "errors", "rng",
+]

@@ -1,0 +1,94 @@
+"""ctypes binding of the C-ABI library (include/voronray_b200.h).
+
+This is the one place that touches the native library.  There is no CPU
+fallback: importing the compute entry points without the built ``.so`` or
+without a CUDA device raises :class:`~.errors.DeviceUnavailable`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from ._build import LIB_PATH
+from .errors import DeviceUnavailable
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+_dbl = ctypes.c_double
+_u64 = ctypes.c_uint64
+
+# name -> argtypes (all return int status)
+_SIGNATURES = {
+    "vr_abi_version": [],
+    "vr_record_stride": [_int],
+    "vr_pack_generators": [_vp, _i64, _int, _vp, _vp, _vp],
+    "vr_raycast_batch": [_vp, _i64, _int, _dbl, _vp, _vp, _i64, _vp, _vp, _vp, _int, _i64,
+                         _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "vr_raycast_recheck": [_vp, _i64, _int, _vp, _vp, _i64, _vp, _vp, _vp, _int, _vp, _vp, _i64,
+                           _vp, _vp, _vp, _vp, _vp],
+    "vr_nearest_batch": [_vp, _i64, _int, _vp, _i64, _vp, _vp, _vp, _vp, _vp],
+    "vr_verify_vertices": [_vp, _i64, _int, _vp, _vp, _i64, _dbl, _vp, _vp],
+    "vr_circumcenters": [_vp, _int, _vp, _i64, _vp, _vp, _vp],
+    "vr_vertex_directions": [_vp, _int, _vp, _i64, _vp, _vp, _vp],
+    "vr_mc_rays": [_vp, _i64, _int, _dbl, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _u64,
+                   _vp, _vp, _vp, _vp, _vp, _vp],
+    "vr_mc_recheck": [_vp, _i64, _int, _vp, _vp, _i64, _vp, _i64, _vp, _u64, _vp, _vp, _i64,
+                      _vp, _vp, _vp, _vp],
+    "vr_mc_reduce": [_vp, _int, _vp, _i64, _i64, _vp, _u64, _vp, _vp, _vp, _int, _int, _dbl,
+                     _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "vr_mc_directions": [_int, _i64, _vp, _i64, _u64, _vp, _vp],
+    "vr_fma_probe": [_int, _int, _int, _vp, _vp],
+}
+
+# Symbols declared in include/voronray_b200.h that the .so must export.
+EXPORTED = tuple(_SIGNATURES) + ("vr_status_string",)
+
+_LIB = None
+
+
+def load_library():
+    """Load the shared library (no device needed); raises if it was not built."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise DeviceUnavailable(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, argtypes in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = ctypes.c_int
+    lib.vr_status_string.argtypes = [_int]
+    lib.vr_status_string.restype = ctypes.c_char_p
+    _LIB = lib
+    return lib
+
+
+def lib():
+    """The library, after checking that a CUDA device is present."""
+    L = load_library()
+    if not torch.cuda.is_available():
+        raise DeviceUnavailable("no CUDA device: the B200 kernels have no CPU fallback")
+    return L
+
+
+def check(status, what=""):
+    if status != 0:
+        msg = load_library().vr_status_string(int(status)).decode()
+        raise RuntimeError(f"{what or 'voronray_b200'} failed: {msg} (status {status})")
+
+
+def ptr(t):
+    """Raw device pointer of a tensor (or None)."""
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def stream_handle(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)

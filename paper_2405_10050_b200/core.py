@@ -1,0 +1,369 @@
+"""Generators, mesh types and vertex checks (drop-in for voronray.core).
+
+Mirrors pkg/src/voronray/core.py: ``NodeSet`` / ``build_node_set`` keep the
+reference constructor, validation and errors (core.py:35-57, 145-169); the
+nearest-neighbour query (core.py:62-142) and ``verify_vertex``
+(core.py:279-296) run on the B200 through the C-ABI library.  The generator
+set lives in HBM as 16-B aligned records [x, |x|^2, pad] (one copy per
+device, packed on first use).
+
+``Mesh`` is array-backed: the traversal returns sigma /
+coordinate / edge / boundary arrays and the reference's dict views
+(``vertices``, ``edge_counts``, ``boundary``) are materialised lazily.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from itertools import combinations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DimensionMismatch, DuplicatePoint
+
+# Reference tolerances (core.py:24-32).
+TOL_VERTEX = 1e-8
+TOL_DEGENERATE = 1e-10
+HALFSPACE_SLACK = 1e-12
+_SCAN_MAX = 2048
+
+MIN_DIM, MAX_DIM = 2, 8
+
+
+def _device(device=None):
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    if device.type != "cuda":
+        raise ValueError("the B200 kernels need a CUDA device")
+    if device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    return device
+
+
+class NodeSet:
+    """Immutable generator points, resident in HBM as packed records.
+
+    ``backend`` is accepted for API compatibility ("scan", "kdtree", "auto",
+    core.py:52-57); every query is a brute-force scan on the GPU, which is
+    the reference's semantic contract (exact equivalence with a linear scan,
+    smallest index on ties, core.py:36-42).
+    """
+
+    def __init__(self, points, backend="auto"):
+        pts = np.array(points, dtype=float, copy=True)
+        if pts.ndim != 2:
+            raise DimensionMismatch("points must form a 2-d array of shape (n, d)")
+        self.points = np.ascontiguousarray(pts)
+        self.points.setflags(write=False)
+        self.n, self.dim = self.points.shape
+        if not MIN_DIM <= self.dim <= MAX_DIM:
+            raise DimensionMismatch(
+                f"the B200 kernels support {MIN_DIM} <= d <= {MAX_DIM}, got d={self.dim}")
+        self._sq = np.einsum("ij,ij->i", self.points, self.points)
+        if backend == "auto":
+            backend = "scan" if self.n <= _SCAN_MAX else "kdtree"
+        if backend not in ("scan", "kdtree"):
+            raise ValueError(f"unknown backend {backend!r}")
+        self.backend = backend
+        self._dev = {}
+
+    def __len__(self):
+        return self.n
+
+    @property
+    def stride(self):
+        return (self.dim + 2) & ~1
+
+    def device_records(self, device=None):
+        """(records tensor (n, stride) fp64 on `device`, max |x|^2 as float)."""
+        dev = _device(device)
+        hit = self._dev.get(dev.index)
+        if hit is not None:
+            return hit
+        L = _lib.lib()
+        with torch.cuda.device(dev):
+            pts = torch.from_numpy(self.points).to(dev)
+            rec = torch.empty((self.n, self.stride), dtype=torch.float64, device=dev)
+            sqmax = torch.zeros(1, dtype=torch.float64, device=dev)
+            _lib.check(L.vr_pack_generators(_lib.ptr(pts), self.n, self.dim, _lib.ptr(rec),
+                                            _lib.ptr(sqmax), _lib.stream_handle()),
+                       "vr_pack_generators")
+            entry = (rec, float(sqmax.item()))
+        self._dev[dev.index] = entry
+        return entry
+
+    # -- filtered nearest neighbour (core.py:62-142) -------------------------
+    def _skip_mask(self, skip):
+        if skip is None:
+            return None
+        if callable(skip):
+            return np.fromiter((bool(skip(i)) for i in range(self.n)), dtype=bool, count=self.n)
+        return np.asarray(skip, dtype=bool)
+
+    def _nearest_dev(self, q, skip):
+        rec, _ = self.device_records()
+        dev = rec.device
+        L = _lib.lib()
+        qd = torch.as_tensor(np.asarray(q, dtype=float).reshape(-1, self.dim), device=dev)
+        mask = self._skip_mask(skip)
+        md = None if mask is None else torch.as_tensor(mask.astype(np.uint8), device=dev)
+        nq = qd.shape[0]
+        idx = torch.empty(nq, dtype=torch.int32, device=dev)
+        d1 = torch.empty(nq, dtype=torch.float64, device=dev)
+        d2 = torch.empty(nq, dtype=torch.float64, device=dev)
+        _lib.check(L.vr_nearest_batch(_lib.ptr(rec), self.n, self.dim, _lib.ptr(qd), nq,
+                                      _lib.ptr(md), _lib.ptr(idx), _lib.ptr(d1), _lib.ptr(d2),
+                                      _lib.stream_handle()), "vr_nearest_batch")
+        return idx.cpu().numpy(), d1.cpu().numpy(), d2.cpu().numpy()
+
+    def nearest(self, q, skip=None):
+        """``(index, distance)`` of the nearest non-skipped point, or None."""
+        idx, d1, _ = self._nearest_dev(q, skip)
+        if idx[0] < 0:
+            return None
+        return int(idx[0]), float(d1[0])
+
+    def nearest2(self, q, skip=None):
+        """``((i, dist_i), dist_second)`` or None (core.py:105-142)."""
+        idx, d1, d2 = self._nearest_dev(q, skip)
+        if idx[0] < 0:
+            return None
+        return (int(idx[0]), float(d1[0])), float(d2[0])
+
+
+def build_node_set(points, backend="auto"):
+    """Validate raw coordinates and build a :class:`NodeSet` (core.py:145-169)."""
+    rows = [np.asarray(p, dtype=float) for p in points]
+    if not rows:
+        raise DimensionMismatch("empty point set")
+    d = rows[0].shape[-1] if rows[0].ndim else 0
+    for p in rows:
+        if p.ndim != 1 or p.shape[0] != d:
+            raise DimensionMismatch("all points must share one dimension")
+    if d < 2:
+        raise DimensionMismatch("dimension must be at least 2")
+    if len(rows) < d + 1:
+        raise DimensionMismatch(f"need at least d+1={d + 1} points, got {len(rows)}")
+    arr = np.vstack(rows)
+    # exact duplicates: identical byte rows (core.py:163-168), vectorised
+    _, first = np.unique(arr.view(np.dtype((np.void, arr.dtype.itemsize * d))).ravel(),
+                         return_index=True)
+    if first.size != arr.shape[0]:
+        dup_mask = np.ones(arr.shape[0], dtype=bool)
+        dup_mask[first] = False
+        raise DuplicatePoint(f"duplicate coordinates {arr[np.argmax(dup_mask)].tolist()}")
+    return NodeSet(arr, backend=backend)
+
+
+def nearest_neighbor(ns: NodeSet, q, skip=None):
+    """Nearest node to ``q`` among non-skipped indices (core.py:172-181)."""
+    q = np.asarray(q, dtype=float)
+    if q.shape != (ns.dim,):
+        raise DimensionMismatch(f"query must have length {ns.dim}")
+    return ns.nearest(q, skip)
+
+
+@dataclass(frozen=True)
+class VertexRecord:
+    """A Voronoi vertex: sorted generator indices plus its coordinate."""
+
+    sigma: tuple
+    r: np.ndarray
+
+
+@dataclass(frozen=True)
+class BoundaryRay:
+    """An unbounded edge anchored at vertex ``sigma`` with direction ``u``."""
+
+    sigma: tuple
+    u: np.ndarray
+
+
+def edge_keys(sigma):
+    """All d-subsets of the sorted (d+1)-tuple ``sigma`` (core.py:200-202)."""
+    return [sigma[:k] + sigma[k + 1:] for k in range(len(sigma))]
+
+
+class Mesh:
+    """Traversal output with array storage and lazy reference-style views.
+
+    Constructed either like the reference dataclass
+    ``Mesh(nodes, vertices, edge_counts, boundary)`` (core.py:205-221) or from
+    device-produced arrays via :meth:`from_arrays`.
+    """
+
+    def __init__(self, nodes, vertices=None, edge_counts=None, boundary=None):
+        self.nodes = nodes
+        self._vertices = vertices
+        self._edge_counts = edge_counts
+        self._boundary = boundary
+        self._arr = None
+        self._cell_csr = None
+        self._neighbors = {}
+        self._unbounded = None
+        self._unbounded_faces = None
+
+    # -- array form -------------------------------------------------------
+    @classmethod
+    def from_arrays(cls, nodes, sigma, r, edge_key, edge_count, boundary_sigma, boundary_u):
+        m = cls(nodes)
+        m._arr = dict(sigma=np.ascontiguousarray(sigma, dtype=np.int32),
+                      r=np.ascontiguousarray(r, dtype=np.float64),
+                      edge_key=np.ascontiguousarray(edge_key, dtype=np.int32),
+                      edge_count=np.ascontiguousarray(edge_count, dtype=np.int32),
+                      boundary_sigma=np.ascontiguousarray(boundary_sigma, dtype=np.int32),
+                      boundary_u=np.ascontiguousarray(boundary_u, dtype=np.float64))
+        return m
+
+    def arrays(self):
+        """sigma (V, d+1) int32, r (V, d), edge_key (E, d), edge_count (E,),
+        boundary_sigma (B, d+1), boundary_u (B, d)."""
+        if self._arr is None:
+            d = self.nodes.dim
+            verts = list(self._vertices.values()) if self._vertices else []
+            sig = np.array([v.sigma for v in verts], dtype=np.int32).reshape(-1, d + 1)
+            r = np.array([v.r for v in verts], dtype=np.float64).reshape(-1, d)
+            ek = np.array(list(self._edge_counts.keys()) if self._edge_counts else [],
+                          dtype=np.int32).reshape(-1, d)
+            ec = np.array(list(self._edge_counts.values()) if self._edge_counts else [],
+                          dtype=np.int32)
+            bl = self._boundary or []
+            bs = np.array([b.sigma for b in bl], dtype=np.int32).reshape(-1, d + 1)
+            bu = np.array([b.u for b in bl], dtype=np.float64).reshape(-1, d)
+            self._arr = dict(sigma=sig, r=r, edge_key=ek, edge_count=ec,
+                             boundary_sigma=bs, boundary_u=bu)
+        return self._arr
+
+    @property
+    def n_vertices(self):
+        return self.arrays()["sigma"].shape[0]
+
+    @property
+    def vertices(self):
+        if self._vertices is None:
+            a = self.arrays()
+            self._vertices = {tuple(int(x) for x in s): VertexRecord(tuple(int(x) for x in s), r)
+                              for s, r in zip(a["sigma"], a["r"])}
+        return self._vertices
+
+    @vertices.setter
+    def vertices(self, value):
+        self._vertices = value
+        self._arr = None
+
+    @property
+    def edge_counts(self):
+        if self._edge_counts is None:
+            a = self.arrays()
+            self._edge_counts = {tuple(int(x) for x in k): int(c)
+                                 for k, c in zip(a["edge_key"], a["edge_count"])}
+        return self._edge_counts
+
+    @property
+    def boundary(self):
+        if self._boundary is None:
+            a = self.arrays()
+            self._boundary = [BoundaryRay(tuple(int(x) for x in s), u)
+                              for s, u in zip(a["boundary_sigma"], a["boundary_u"])]
+        return self._boundary
+
+    # -- cell maps (core.py:223-276) ---------------------------------------
+    def _csr(self):
+        if self._cell_csr is None:
+            sig = self.arrays()["sigma"] if self._vertices is None else None
+            if sig is None:
+                keys = list(self._vertices.keys())
+                sig = np.array(keys, dtype=np.int32).reshape(-1, self.nodes.dim + 1)
+                self._vlist = [self._vertices[k] for k in keys]
+            else:
+                self._vlist = None
+            flat = sig.ravel()
+            vid = np.repeat(np.arange(sig.shape[0]), sig.shape[1])
+            order = np.argsort(flat, kind="stable")
+            counts = np.bincount(flat, minlength=self.nodes.n)
+            off = np.zeros(self.nodes.n + 1, dtype=np.int64)
+            np.cumsum(counts, out=off[1:])
+            self._cell_csr = (off, vid[order], sig)
+        return self._cell_csr
+
+    def _vertex(self, v):
+        if getattr(self, "_vlist", None) is not None:
+            return self._vlist[v]
+        a = self.arrays()
+        s = tuple(int(x) for x in a["sigma"][v])
+        return self.vertices[s]
+
+    def cell_vertices(self, i):
+        off, vids, _ = self._csr()
+        if i < 0 or i >= self.nodes.n:
+            return []
+        return [self._vertex(int(v)) for v in vids[off[i]:off[i + 1]]]
+
+    def neighbors(self, i):
+        hit = self._neighbors.get(i)
+        if hit is None:
+            off, vids, sig = self._csr()
+            if 0 <= i < self.nodes.n and off[i + 1] > off[i]:
+                s = np.unique(sig[vids[off[i]:off[i + 1]]])
+                hit = tuple(int(x) for x in s if x != i)
+            else:
+                hit = ()
+            self._neighbors[i] = hit
+        return hit
+
+    def unbounded_cells(self):
+        if self._unbounded is None:
+            out = set()
+            for eta, c in self.edge_counts.items():
+                if c == 1:
+                    out.update(eta)
+            self._unbounded = frozenset(out)
+        return self._unbounded
+
+    def bounded_cells(self):
+        unb = self.unbounded_cells()
+        off, _, _ = self._csr()
+        return [i for i in range(self.nodes.n) if i not in unb and off[i + 1] > off[i]]
+
+    def face_vertices(self, i, j):
+        return [v for v in self.cell_vertices(i) if j in v.sigma]
+
+    def face_is_unbounded(self, i, j):
+        if self._unbounded_faces is None:
+            pairs = set()
+            for eta, c in self.edge_counts.items():
+                if c == 1:
+                    pairs.update(combinations(eta, 2))
+            self._unbounded_faces = frozenset(pairs)
+        key = (i, j) if i < j else (j, i)
+        return key in self._unbounded_faces
+
+
+def verify_vertices(ns: NodeSet, sigma, r, tol: float = TOL_VERTEX):
+    """Batched verify_vertex on the GPU: bool array, one per vertex."""
+    sigma = np.ascontiguousarray(sigma, dtype=np.int32).reshape(-1, ns.dim + 1)
+    r = np.ascontiguousarray(r, dtype=np.float64).reshape(-1, ns.dim)
+    if sigma.shape[0] == 0:
+        return np.zeros(0, dtype=bool)
+    rec, _ = ns.device_records()
+    dev = rec.device
+    L = _lib.lib()
+    sd = torch.from_numpy(sigma).to(dev)
+    rd = torch.from_numpy(r).to(dev)
+    ok = torch.empty(sigma.shape[0], dtype=torch.uint8, device=dev)
+    _lib.check(L.vr_verify_vertices(_lib.ptr(rec), ns.n, ns.dim, _lib.ptr(sd), _lib.ptr(rd),
+                                    sigma.shape[0], float(tol), _lib.ptr(ok),
+                                    _lib.stream_handle()), "vr_verify_vertices")
+    return ok.cpu().numpy().astype(bool)
+
+
+def verify_vertex(mesh: Mesh, v: VertexRecord, tol: float = TOL_VERTEX) -> bool:
+    """Equidistance + incircle invariants of one vertex (core.py:279-296)."""
+    ns = mesh.nodes
+    sig = list(v.sigma)
+    if len(sig) != ns.dim + 1 or len(set(sig)) != len(sig):
+        return False
+    return bool(verify_vertices(ns, np.array([sig]), np.asarray(v.r)[None], tol)[0])

@@ -1,0 +1,244 @@
+// Generator packing, filtered nearest neighbour, vertex verification,
+// circumcentres and vertex edge directions (include/voronray_b200.h).
+#include "common.cuh"
+
+namespace {
+
+template <int D>
+__global__ void k_pack(const double* __restrict__ pts, int64_t n, double* __restrict__ rec,
+                       unsigned long long* __restrict__ sqmax) {
+  constexpr int S = rec_stride(D);
+  double local = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double sq = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const double v = pts[i * D + k];
+      rec[i * S + k] = v;
+      sq = fma(v, v, sq);
+    }
+    rec[i * S + D] = sq;
+#pragma unroll
+    for (int k = D + 1; k < S; ++k) rec[i * S + k] = 0.0;
+    local = fmax(local, sq);
+  }
+  // non-negative doubles order like their bit patterns
+  for (int off = 16; off > 0; off >>= 1) local = fmax(local, __shfl_xor_sync(0xffffffffu, local, off));
+  if ((threadIdx.x & 31) == 0 && sqmax) atomicMax(sqmax, (unsigned long long)__double_as_longlong(local));
+}
+
+// Nearest / second nearest by the expanded squared distance with the
+// smallest index on ties (core.py:81-90, 131-142); clean distances after.
+template <int D>
+__global__ void k_nearest(const double* __restrict__ rec, int64_t n, const double* __restrict__ q,
+                          int64_t nq, const uint8_t* __restrict__ skip, int32_t* out_idx,
+                          double* out_d1, double* out_d2) {
+  constexpr int S = rec_stride(D);
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= nq) return;
+  double qq[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) qq[j] = q[k * D + j];
+  double b1 = CUDART_INF, b2 = CUDART_INF;
+  int i1 = -1, i2 = -1;
+  for (int64_t i = 0; i < n; ++i) {
+    if (skip && skip[i]) continue;
+    const double* x = rec + i * S;
+    double p = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) p = fma(qq[j], x[j], p);
+    const double d2 = fma(-2.0, p, x[D]);
+    if (d2 < b1) { b2 = b1; i2 = i1; b1 = d2; i1 = (int)i; }
+    else if (d2 < b2) { b2 = d2; i2 = (int)i; }
+  }
+  out_idx[k] = i1;
+  auto clean = [&](int i) {
+    if (i < 0) return CUDART_INF;
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) { const double a = rec[(int64_t)i * S + j] - qq[j]; s = fma(a, a, s); }
+    return sqrt(s);
+  };
+  if (out_d1) out_d1[k] = clean(i1);
+  if (out_d2) out_d2[k] = clean(i2);
+}
+
+// verify_vertex (core.py:279-296) for a batch of vertices.
+template <int D>
+__global__ void k_verify(const double* __restrict__ rec, int64_t n, const int32_t* __restrict__ sigma,
+                         const double* __restrict__ r, int64_t nv, double tol, uint8_t* ok) {
+  constexpr int S = rec_stride(D);
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  double rr[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) rr[j] = r[v * D + j];
+  int sig[D + 1];
+  bool good = true;
+#pragma unroll
+  for (int a = 0; a <= D; ++a) {
+    sig[a] = sigma[v * (D + 1) + a];
+    if (sig[a] < 0 || sig[a] >= n) good = false;
+  }
+#pragma unroll
+  for (int a = 0; a <= D; ++a)
+#pragma unroll
+    for (int b = a + 1; b <= D; ++b)
+      if (sig[a] == sig[b]) good = false;
+  if (!good) { ok[v] = 0; return; }
+  auto dist = [&](int64_t i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) { const double a = rec[i * S + j] - rr[j]; s = fma(a, a, s); }
+    return sqrt(s);
+  };
+  const double rad = dist(sig[0]);
+  double dev = 0.0;
+#pragma unroll
+  for (int a = 1; a <= D; ++a) dev = fmax(dev, fabs(dist(sig[a]) - rad));
+  if (!(rad > 0.0) || dev > tol * rad) { ok[v] = 0; return; }
+  double mn = CUDART_INF;
+  for (int64_t i = 0; i < n; ++i) {
+    bool own = false;
+#pragma unroll
+    for (int a = 0; a <= D; ++a) own |= (sig[a] == i);
+    if (!own) mn = fmin(mn, dist(i));
+  }
+  ok[v] = (mn >= rad * (1.0 - tol)) ? 1 : 0;
+}
+
+template <int D>
+__global__ void k_circumcenters(const double* __restrict__ rec, const int32_t* __restrict__ sigma,
+                                int64_t nv, double* out_r, uint8_t* out_ok) {
+  constexpr int S = rec_stride(D);
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const double* x0 = rec + (int64_t)sigma[v * (D + 1)] * S;
+  double A[D][D], b[D];
+  int piv[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const double* xa = rec + (int64_t)sigma[v * (D + 1) + a + 1] * S;
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double e = xa[j] - x0[j];
+      A[a][j] = 2.0 * e;
+      s = fma(e, e, s);
+    }
+    b[a] = s;
+  }
+  const bool ok = lu_factor<D>(A, piv);
+  if (ok) lu_solve<D>(A, piv, b);
+#pragma unroll
+  for (int j = 0; j < D; ++j) out_r[v * D + j] = ok ? x0[j] + b[j] : CUDART_NAN;
+  if (out_ok) out_ok[v] = ok ? 1 : 0;
+}
+
+// _vertex_directions (raycast.py:345-378): rows of D are x_s - x_s0.
+template <int D>
+__device__ void vertex_dirs(const double* __restrict__ rec, const int32_t* sig, double* out_u,
+                            uint8_t* out_ok) {
+  constexpr int S = rec_stride(D);
+  const double* x0 = rec + (int64_t)sig[0] * S;
+  double A[D][D];
+  int piv[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const double* xa = rec + (int64_t)sig[a + 1] * S;
+#pragma unroll
+    for (int j = 0; j < D; ++j) A[a][j] = xa[j] - x0[j];
+  }
+  const bool ok = lu_factor<D>(A, piv);
+  for (int k = 0; k <= D; ++k) {
+    double v[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) v[j] = (k == 0) ? 1.0 : (j == k - 1 ? 1.0 : 0.0);
+    bool good = ok;
+    if (ok) lu_solve<D>(A, piv, v);
+    const double sgn = (k == 0) ? 1.0 : -1.0;
+    double nn = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) nn = fma(v[j], v[j], nn);
+    const double nrm = sqrt(nn);
+    good = good && nrm > 0.0 && isfinite(nrm);
+#pragma unroll
+    for (int j = 0; j < D; ++j) out_u[k * D + j] = good ? sgn * v[j] / nrm : CUDART_NAN;
+    if (out_ok) out_ok[k] = good ? 1 : 0;
+  }
+}
+
+template <int D>
+__global__ void k_vertex_dirs(const double* __restrict__ rec, const int32_t* __restrict__ sigma,
+                              int64_t nv, double* out_u, uint8_t* out_ok) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  vertex_dirs<D>(rec, sigma + v * (D + 1), out_u + v * (D + 1) * D,
+                 out_ok ? out_ok + v * (D + 1) : nullptr);
+}
+
+inline unsigned blocks_for(int64_t n, int nt) { return (unsigned)((n + nt - 1) / nt); }
+
+}  // namespace
+
+extern "C" int vr_pack_generators(const double* pts, int64_t n, int d, double* rec,
+                                  double* sqmax_out, void* stream) {
+  if (!pts || !rec || n <= 0) return VR_EINVAL;
+  cudaStream_t st = as_stream(stream);
+  if (sqmax_out) {
+    cudaError_t e = cudaMemsetAsync(sqmax_out, 0, sizeof(double), st);
+    if (e != cudaSuccess) return vr_cuda_status(e);
+  }
+  const unsigned nb = blocks_for(n, 256) < 4096 ? blocks_for(n, 256) : 4096;
+  VR_DISPATCH_D(d, {
+    k_pack<D><<<nb, 256, 0, st>>>(pts, n, rec, reinterpret_cast<unsigned long long*>(sqmax_out));
+  });
+  VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_nearest_batch(const double* rec, int64_t n_gen, int d, const double* q,
+                                int64_t n_q, const uint8_t* skip, int32_t* out_idx,
+                                double* out_d1, double* out_d2, void* stream) {
+  if (!rec || !q || !out_idx || n_gen <= 0) return VR_EINVAL;
+  if (n_q <= 0) return VR_OK;
+  VR_DISPATCH_D(d, {
+    k_nearest<D><<<blocks_for(n_q, 128), 128, 0, as_stream(stream)>>>(rec, n_gen, q, n_q, skip,
+                                                                        out_idx, out_d1, out_d2);
+  });
+  VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_verify_vertices(const double* rec, int64_t n_gen, int d, const int32_t* sigma,
+                                  const double* r, int64_t n_v, double tol, uint8_t* out_ok,
+                                  void* stream) {
+  if (!rec || !sigma || !r || !out_ok) return VR_EINVAL;
+  if (n_v <= 0) return VR_OK;
+  VR_DISPATCH_D(d, {
+    k_verify<D><<<blocks_for(n_v, 128), 128, 0, as_stream(stream)>>>(rec, n_gen, sigma, r, n_v,
+                                                                       tol, out_ok);
+  });
+  VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_circumcenters(const double* rec, int d, const int32_t* sigma, int64_t n_v,
+                                double* out_r, uint8_t* out_ok, void* stream) {
+  if (!rec || !sigma || !out_r) return VR_EINVAL;
+  if (n_v <= 0) return VR_OK;
+  VR_DISPATCH_D(d, {
+    k_circumcenters<D><<<blocks_for(n_v, 128), 128, 0, as_stream(stream)>>>(rec, sigma, n_v,
+                                                                              out_r, out_ok);
+  });
+  VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_vertex_directions(const double* rec, int d, const int32_t* sigma, int64_t n_v,
+                                    double* out_u, uint8_t* out_ok, void* stream) {
+  if (!rec || !sigma || !out_u) return VR_EINVAL;
+  if (n_v <= 0) return VR_OK;
+  VR_DISPATCH_D(d, {
+    k_vertex_dirs<D><<<blocks_for(n_v, 128), 128, 0, as_stream(stream)>>>(rec, sigma, n_v, out_u,
+                                                                            out_ok);
+  });
+  VR_RETURN_LAUNCH();
+}

@@ -1,0 +1,235 @@
+// Monte-Carlo cell volumes and interface areas:
+// Philox directions -> fused RayCast -> per-cell segmented reduction in ray
+// order (reference integrate_mc.py:124-197).
+#include "raycast_core.cuh"
+
+using namespace vr;
+
+namespace {
+
+constexpr int RED_NT = 256;
+constexpr int RED_CHUNK = 1024;   // rays per reduction chunk (4 per thread)
+constexpr int RED_MAPCAP = 1024;  // smem face map capacity (max_faces <= 512)
+
+__device__ __forceinline__ void bitonic_sort_u64(unsigned long long* keys, int n) {
+  // n is a power of two; ascending.
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long a = keys[i], b = keys[l];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) { keys[i] = b; keys[l] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(RED_NT)
+    k_mc_reduce(SrcMC<D> src, const int32_t* __restrict__ ray_idx, const double* __restrict__ ray_t,
+                const uint8_t* __restrict__ ray_flag, int max_faces, int degenerate_is_error,
+                double surf, double* out_volume, int32_t* out_face_j, double* out_face_area,
+                int32_t* out_nfaces, int32_t* out_status, int64_t* out_first_bad,
+                double* out_samples) {
+  constexpr int S = rec_stride(D);
+  __shared__ unsigned long long keys[RED_CHUNK];
+  __shared__ double wv[RED_CHUNK];
+  __shared__ double lv[RED_CHUNK];
+  __shared__ int mkey[RED_MAPCAP];
+  __shared__ double macc[RED_MAPCAP];
+  __shared__ unsigned long long first_bad;  // (ray << 2) | kind
+  __shared__ int nused;
+
+  const int64_t c = blockIdx.x;
+  const int64_t per = src.per;
+  const double* xc = src.grec + (int64_t)src.cells[c] * S;
+  for (int i = threadIdx.x; i < RED_MAPCAP; i += RED_NT) { mkey[i] = -1; macc[i] = 0.0; }
+  if (threadIdx.x == 0) { first_bad = ~0ull; nused = 0; }
+  double vol = 0.0;  // thread 0 only: sequential sum in ray order (integrate_mc.py:155)
+  __syncthreads();
+
+  for (int64_t start = 0; start < per; start += RED_CHUNK) {
+    const int cnt = (int)min((int64_t)RED_CHUNK, per - start);
+    for (int s = threadIdx.x; s < RED_CHUNK; s += RED_NT) {
+      unsigned long long key = ~0ull;
+      double w = 0.0, ld = 0.0;
+      if (s < cnt) {
+        const int64_t r = start + s;
+        const int64_t k = c * per + r;
+        const uint8_t fl = ray_flag[k];
+        const bool bad = fl == VR_RAY_ESCAPED || (fl == VR_RAY_DEGENERATE && degenerate_is_error);
+        if (bad) {
+          atomicMin(&first_bad, ((unsigned long long)r << 2) | (fl == VR_RAY_ESCAPED ? 1ull : 2ull));
+        } else {
+          const int32_t j = ray_idx[k];
+          const double t = ray_t[k];
+          double y[D];
+          src.direction(k, y);
+          const double* xj = src.grec + (int64_t)j * S;
+          double ss = 0.0, nd = 0.0, nn = 0.0;
+#pragma unroll
+          for (int q = 0; q < D; ++q) {
+            const double rp = fma(t, y[q], xc[q]);  // rp = xi + t y  (raycast.py:210)
+            const double seg = rp - xc[q];           // integrate_mc.py:151
+            ss = fma(seg, seg, ss);
+            const double nij = xj[q] - xc[q];
+            nd = fma(nij, y[q], nd);
+            nn = fma(nij, nij, nn);
+          }
+          const double length = sqrt(ss);
+          const double cosang = nd / sqrt(nn);
+          double p = 1.0;
+#pragma unroll
+          for (int q = 0; q < D - 1; ++q) p *= length;
+          w = p / cosang;          // length^(d-1) / cos
+          ld = p * length;         // length^d
+          key = ((unsigned long long)(uint32_t)j << 32) | (unsigned)s;
+          if (out_samples) out_samples[k] = ld;
+        }
+      }
+      keys[s] = key;
+      wv[s] = w;
+      lv[s] = ld;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < cnt; ++s) vol += lv[s];
+    }
+    bitonic_sort_u64(keys, RED_CHUNK);
+    for (int p = threadIdx.x; p < RED_CHUNK; p += RED_NT) {
+      const unsigned long long key = keys[p];
+      if (key == ~0ull) continue;
+      const uint32_t j = (uint32_t)(key >> 32);
+      if (p > 0 && (uint32_t)(keys[p - 1] >> 32) == j) continue;  // not a segment head
+      double sum = 0.0;  // ray order inside the segment (keys sorted by (j, ray))
+      for (int q = p; q < RED_CHUNK && keys[q] != ~0ull && (uint32_t)(keys[q] >> 32) == j; ++q)
+        sum += wv[keys[q] & 0xffffffffu];
+      unsigned h = (j * 2654435761u) & (RED_MAPCAP - 1);
+      bool placed = false;
+      for (int probe = 0; probe < RED_MAPCAP; ++probe) {
+        const int prev = atomicCAS(&mkey[h], -1, (int)j);
+        if (prev == -1) { atomicAdd(&nused, 1); placed = true; break; }
+        if (prev == (int)j) { placed = true; break; }
+        h = (h + 1) & (RED_MAPCAP - 1);
+      }
+      if (placed) macc[h] += sum;  // one head per face per chunk: single writer
+      else atomicAdd(&nused, RED_MAPCAP);  // map full: reported as OVERFLOW
+    }
+    __syncthreads();
+  }
+
+  // Emit faces sorted by neighbour index.
+  for (int i = threadIdx.x; i < RED_MAPCAP; i += RED_NT)
+    keys[i] = mkey[i] < 0 ? ~0ull : (((unsigned long long)(uint32_t)mkey[i] << 32) | (unsigned)i);
+  __syncthreads();
+  bitonic_sort_u64(keys, RED_MAPCAP);
+  const int nf = nused;
+  const double scale = surf / (double)per;  // integrate_mc.py:157-158
+  for (int p = threadIdx.x; p < nf && p < max_faces; p += RED_NT) {
+    const unsigned long long key = keys[p];
+    out_face_j[c * max_faces + p] = (int32_t)(key >> 32);
+    out_face_area[c * max_faces + p] = macc[key & 0xffffffffu] * scale;
+  }
+  if (threadIdx.x == 0) {
+    out_volume[c] = vol * surf / (double)((int64_t)D * per);  // integrate_mc.py:159
+    out_nfaces[c] = nf < max_faces ? nf : max_faces;
+    int status = VR_CELL_OK;
+    int64_t fb = -1;
+    if (first_bad != ~0ull) {
+      fb = (int64_t)(first_bad >> 2);
+      status = (first_bad & 3ull) == 1ull ? VR_CELL_UNBOUNDED : VR_CELL_DEGENERATE;
+    } else if (nf > max_faces) {
+      status = VR_CELL_OVERFLOW;
+    }
+    out_status[c] = status;
+    out_first_bad[c] = fb;
+  }
+}
+
+template <int D>
+__global__ void k_mc_dirs(SrcMC<D> src, double* out_z) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= src.n) return;
+  const int64_t c = k / src.per;
+  double z[D];
+  philox_normals<D>(src.seed, src.cells[c], k - c * src.per, z);
+#pragma unroll
+  for (int j = 0; j < D; ++j) out_z[k * D + j] = z[j];
+}
+
+}  // namespace
+
+extern "C" int vr_mc_rays(const double* rec, int64_t n_gen, int d, double sqmax,
+                          const double* cand_rec, const int32_t* cand, int64_t n_cand,
+                          const int32_t* cells, int64_t n_cells, int64_t rays_per_cell,
+                          const double* dirs, uint64_t seed, int32_t* out_idx, double* out_t,
+                          uint8_t* out_flag, int32_t* recheck_list, int32_t* recheck_count,
+                          void* stream) {
+  if (!rec || !cells || !out_idx || !out_t || !out_flag || rays_per_cell <= 0) return VR_EINVAL;
+  const double* crec = cand ? cand_rec : rec;
+  const int64_t nc = cand ? n_cand : n_gen;
+  if (!crec || nc <= 0) return VR_EINVAL;
+  const int64_t n = n_cells * rays_per_cell;
+  RayOut out{out_idx, out_t, nullptr, out_flag, recheck_list, recheck_count};
+  VR_DISPATCH_D(d, {
+    SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n};
+    return launch_raycast<D>(src, n, crec, cand, nc, sqmax, out, as_stream(stream));
+  });
+  return VR_OK;
+}
+
+extern "C" int vr_mc_recheck(const double* rec, int64_t n_gen, int d, const double* cand_rec,
+                             const int32_t* cand, int64_t n_cand, const int32_t* cells,
+                             int64_t rays_per_cell, const double* dirs, uint64_t seed,
+                             const int32_t* recheck_list, const int32_t* recheck_count,
+                             int64_t max_list, int32_t* out_idx, double* out_t, uint8_t* out_flag,
+                             void* stream) {
+  if (!rec || !cells || !recheck_list || !recheck_count) return VR_EINVAL;
+  const double* crec = cand ? cand_rec : rec;
+  const int64_t nc = cand ? n_cand : n_gen;
+  RayOut out{out_idx, out_t, nullptr, out_flag, nullptr, nullptr};
+  VR_DISPATCH_D(d, {
+    SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, INT64_MAX};
+    return launch_recheck<D>(src, max_list, crec, cand, nc, recheck_list, recheck_count, out,
+                             as_stream(stream));
+  });
+  return VR_OK;
+}
+
+extern "C" int vr_mc_reduce(const double* rec, int d, const int32_t* cells, int64_t n_cells,
+                            int64_t rays_per_cell, const double* dirs, uint64_t seed,
+                            const int32_t* ray_idx, const double* ray_t, const uint8_t* ray_flag,
+                            int max_faces, int degenerate_is_error, double surf,
+                            double* out_volume, int32_t* out_face_j, double* out_face_area,
+                            int32_t* out_nfaces, int32_t* out_status, int64_t* out_first_bad,
+                            double* out_samples, void* stream) {
+  if (!rec || !cells || !ray_idx || !ray_t || !ray_flag || !out_volume || !out_face_j ||
+      !out_face_area || !out_nfaces || !out_status || !out_first_bad)
+    return VR_EINVAL;
+  if (max_faces <= 0 || max_faces > RED_MAPCAP / 2) return VR_EINVAL;
+  if (n_cells <= 0) return VR_OK;
+  VR_DISPATCH_D(d, {
+    SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n_cells * rays_per_cell};
+    k_mc_reduce<D><<<(unsigned)n_cells, RED_NT, 0, as_stream(stream)>>>(
+        src, ray_idx, ray_t, ray_flag, max_faces, degenerate_is_error, surf, out_volume,
+        out_face_j, out_face_area, out_nfaces, out_status, out_first_bad, out_samples);
+  });
+  VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_mc_directions(int d, int64_t n_cells, const int32_t* cells,
+                                int64_t rays_per_cell, uint64_t seed, double* out_z,
+                                void* stream) {
+  if (!cells || !out_z || rays_per_cell <= 0) return VR_EINVAL;
+  const int64_t n = n_cells * rays_per_cell;
+  if (n <= 0) return VR_OK;
+  VR_DISPATCH_D(d, {
+    SrcMC<D> src{nullptr, cells, rays_per_cell, nullptr, seed, n};
+    k_mc_dirs<D><<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(src, out_z);
+  });
+  VR_RETURN_LAUNCH();
+}

@@ -1,0 +1,61 @@
+// C-ABI entry points for the batched incircle RayCast (include/voronray_b200.h).
+#include "raycast_core.cuh"
+
+using namespace vr;
+
+extern "C" int vr_abi_version(void) { return 1; }
+
+extern "C" const char* vr_status_string(int status) {
+  switch (status) {
+    case VR_OK: return "ok";
+    case VR_EINVAL: return "invalid argument";
+    case VR_EDIM: return "dimension outside [2, 8]";
+    case VR_ECAPACITY: return "workspace or table capacity exceeded";
+    default: break;
+  }
+  if (status <= VR_ECUDA_BASE) return cudaGetErrorString((cudaError_t)(VR_ECUDA_BASE - status));
+  return "unknown status";
+}
+
+extern "C" int vr_record_stride(int d) {
+  if (d < VR_MIN_D || d > VR_MAX_D) return VR_EDIM;
+  return rec_stride(d);
+}
+
+extern "C" int vr_raycast_batch(const double* rec, int64_t n_gen, int d, double sqmax,
+                                const double* cand_rec, const int32_t* cand, int64_t n_cand,
+                                const double* x, const double* u, const int32_t* eta, int eta_len,
+                                int64_t n_rays, int32_t* out_idx, double* out_t, double* out_rp,
+                                uint8_t* out_flag, int32_t* recheck_list, int32_t* recheck_count,
+                                void* stream) {
+  if (!rec || n_gen <= 0 || !x || !u || !eta || !out_idx || !out_t || !out_flag) return VR_EINVAL;
+  if (eta_len < 1 || eta_len > d) return VR_EINVAL;
+  if ((recheck_list == nullptr) != (recheck_count == nullptr)) return VR_EINVAL;
+  const double* crec = cand ? cand_rec : rec;
+  const int64_t nc = cand ? n_cand : n_gen;
+  if (!crec || nc <= 0) return VR_EINVAL;
+  RayOut out{out_idx, out_t, out_rp, out_flag, recheck_list, recheck_count};
+  VR_DISPATCH_D(d, {
+    SrcExplicit<D> src{x, u, eta, eta_len, rec, n_rays};
+    return launch_raycast<D>(src, n_rays, crec, cand, nc, sqmax, out, as_stream(stream));
+  });
+  return VR_OK;
+}
+
+extern "C" int vr_raycast_recheck(const double* rec, int64_t n_gen, int d, const double* cand_rec,
+                                  const int32_t* cand, int64_t n_cand, const double* x,
+                                  const double* u, const int32_t* eta, int eta_len,
+                                  const int32_t* recheck_list, const int32_t* recheck_count,
+                                  int64_t max_list, int32_t* out_idx, double* out_t,
+                                  double* out_rp, uint8_t* out_flag, void* stream) {
+  if (!rec || !x || !u || !eta || !recheck_list || !recheck_count) return VR_EINVAL;
+  const double* crec = cand ? cand_rec : rec;
+  const int64_t nc = cand ? n_cand : n_gen;
+  RayOut out{out_idx, out_t, out_rp, out_flag, nullptr, nullptr};
+  VR_DISPATCH_D(d, {
+    SrcExplicit<D> src{x, u, eta, eta_len, rec, INT64_MAX};
+    return launch_recheck<D>(src, max_list, crec, cand, nc, recheck_list, recheck_count, out,
+                             as_stream(stream));
+  });
+  return VR_OK;
+}

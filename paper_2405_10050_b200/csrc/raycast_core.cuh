@@ -1,0 +1,511 @@
+// Fused rays x generators incircle RayCast.
+//
+// Reference semantics (pkg/src/voronray/raycast.py:154-224): the converged
+// incircle loop returns the valid generator i (u.x_i > thr, raycast.py:95-96,
+// 110-117) with the smallest crossing parameter
+//     t_i = (|x_i - x|^2 - |x_g - x|^2) / (2 (u.x_i - u.x_g)),   g = eta[0]
+// (raycast.py:203; SURVEY.md §8 proves argmin-t == the probe loop).
+//
+// B200 formulation.  Each thread owns R rays and streams every generator
+// through registers; generator tiles are staged in shared memory by TMA bulk
+// copies (cp.async.bulk + mbarrier ring).  Instead of evaluating t_i for every
+// pair, the kernel keeps the CURRENT best vertex z = x + t_best u and its
+// circumsphere radius rho, and runs the incircle test
+//     f_i = |x_i|^2 - 2 z.x_i  <  rho^2 - |z|^2                        (*)
+// (the power of x_i w.r.t. the current sphere is negative  <=>  t_i < t_best
+// for a valid i).  (*) costs one length-d dot product + one FMA per pair,
+// i.e. d+2 FP64 pipe ops (2d+2 flops) instead of the 4d+3 of the t form.
+// Candidates that pass (*) (or fall inside its rounding band) take the rare
+// path: the halfspace test, the reference's centred t formula, and the
+// sphere update.  Candidates inside the band +-delta (reference degeneracy
+// band 1e-10 plus a rigorous rounding bound) mark the ray RECHECK; such rays
+// are re-evaluated exactly by k_raycast_recheck, which also applies the
+// reference's runner-up degeneracy test (raycast.py:211-219).
+#pragma once
+
+#include "common.cuh"
+
+namespace vr {
+
+// Candidate records as seen by the kernel: `rec` packed [x, |x|^2, pad].
+template <int D>
+struct RayState {
+  double x[D], u[D], z[D];
+  double hi;    // lim + dlt  (screening bound; +inf before the first hit)
+  double lim;   // rho^2 - |z|^2 of the current sphere
+  double dlt;   // band half-width (degeneracy band + rounding bound)
+  double thr;   // halfspace threshold incl. slack
+  double s;     // u . x_g
+  double base;  // |x - x_g|^2
+  double bu;    // u . (x - x_g)
+  double tb;    // current best t
+  double denb;  // u.(x_best - x_g) of the current best
+  int ib;       // current best (local candidate index), -1 = none
+  int near;     // 1 -> needs exact re-check
+};
+
+// Fill the per-ray constants from origin x, direction u and the eta
+// generators (global records).  Mirrors _Probe.__init__ (raycast.py:93-96)
+// and raycast_incircle's loop constants (raycast.py:178,186-189).
+template <int D>
+__device__ __forceinline__ void ray_setup(RayState<D>& r, const double* __restrict__ grec,
+                                          const int32_t* eta, int eta_len) {
+  constexpr int S = rec_stride(D);
+  const double* xg = grec + (int64_t)eta[0] * S;
+  double thr = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) thr = fma(xg[k], r.u[k], thr);
+  r.s = thr;
+  for (int e = 1; e < eta_len; ++e) {
+    const double* xe = grec + (int64_t)eta[e] * S;
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) v = fma(xe[k], r.u[k], v);
+    thr = fmax(thr, v);
+  }
+  r.thr = thr + VR_HALFSPACE_SLACK * fmax(1.0, fabs(thr));
+  double base = 0.0, bu = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    double b = r.x[k] - xg[k];
+    base = fma(b, b, base);
+    bu = fma(r.u[k], b, bu);
+  }
+  r.base = base;
+  r.bu = bu;
+#pragma unroll
+  for (int k = 0; k < D; ++k) r.z[k] = r.x[k];
+  r.hi = CUDART_INF;
+  r.lim = CUDART_INF;
+  r.dlt = 0.0;
+  r.tb = CUDART_INF;
+  r.denb = 0.0;
+  r.ib = -1;
+  r.near = 0;
+}
+
+// Move the screening sphere to the new best crossing t.
+template <int D>
+__device__ __forceinline__ void ray_set_best(RayState<D>& r, double t, double den, int i,
+                                             double sqmax) {
+  double zz = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    r.z[k] = fma(t, r.u[k], r.x[k]);
+    zz = fma(r.z[k], r.z[k], zz);
+  }
+  const double tq = t * fma(2.0, fabs(r.bu), fabs(t));
+  const double rho2 = fma(t, fma(2.0, r.bu, t), r.base);  // raycast.py:212
+  const double scale = zz + sqmax + r.base + tq + fabs(rho2);
+  const double err = 16.0 * (D + 4) * 2.220446049250313e-16 * scale;
+  const double dlt = 2.1e-10 * fmax(r.base, rho2) + err;
+  r.lim = rho2 - zz;
+  r.dlt = dlt;
+  r.hi = r.lim + dlt;
+  r.tb = t;
+  r.denb = den;
+  r.ib = i;
+}
+
+// Rare path: candidate i passed the screening bound.
+template <int D>
+__device__ __forceinline__ void ray_rare(RayState<D>& r, const double (&xi)[D], double fp, int i,
+                                      double sqmax) {
+  double q = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) q = fma(r.u[k], xi[k], q);
+  if (!(q > r.thr)) return;  // outside the forward halfspace (raycast.py:110-117)
+  const bool have = r.ib >= 0;
+  if (have && fp >= r.lim - r.dlt) r.near = 1;
+  if (have && !(fp < r.lim)) return;
+  // reference centred crossing (raycast.py:201-203)
+  double aa = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    double a = r.x[k] - xi[k];
+    aa = fma(a, a, aa);
+  }
+  const double den = q - r.s;
+  const double t = (aa - r.base) / (2.0 * den);
+  const double told = r.tb, denold = r.denb;
+  ray_set_best<D>(r, t, den, i, sqmax);
+  // power of the previous best w.r.t. the new sphere
+  if (have && 2.0 * denold * (told - t) < r.dlt) r.near = 1;
+}
+
+template <int D>
+__device__ __forceinline__ void ray_screen(RayState<D>& r, const double (&xi)[D], double sq,
+                                           int i, double sqmax) {
+  double h0 = 0.0, h1 = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; k += 2) h0 = fma(r.z[k], xi[k], h0);
+#pragma unroll
+  for (int k = 1; k < D; k += 2) h1 = fma(r.z[k], xi[k], h1);
+  const double fp = fma(-2.0, h0 + h1, sq);
+  if (fp < r.hi) ray_rare<D>(r, xi, fp, i, sqmax);
+}
+
+// ---------------------------------------------------------------------------
+// Ray sources.  load() fills x, u and calls ray_setup; returns false for
+// padding lanes (k >= n).
+// ---------------------------------------------------------------------------
+template <int D>
+struct SrcExplicit {
+  const double* x;
+  const double* u;
+  const int32_t* eta;
+  int eta_len;
+  const double* grec;
+  int64_t n;
+  __device__ __forceinline__ bool load(int64_t k, RayState<D>& r) const {
+    if (k >= n) return false;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      r.x[j] = x[k * D + j];
+      r.u[j] = u[k * D + j];
+    }
+    ray_setup<D>(r, grec, eta + k * eta_len, eta_len);
+    return true;
+  }
+};
+
+// Philox4x32-10 (Salmon et al. 2011) -- counter-based, so every (seed, cell,
+// ray) direction is independent of the launch shape and of the GPU count.
+__device__ __forceinline__ void philox4x32_10(uint32_t (&c)[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int rnd = 0; rnd < 10; ++rnd) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+// D standard normals for ray `ray` of generator `cell`: Philox counter
+// (ray, cell, pair, 0x4D43), Box-Muller on 53-bit uniforms.
+template <int D>
+__device__ __forceinline__ void philox_normals(uint64_t seed, int64_t cell, int64_t ray,
+                                               double (&z)[D]) {
+#pragma unroll
+  for (int p = 0; p < (D + 1) / 2; ++p) {
+    uint32_t c[4] = {(uint32_t)ray, (uint32_t)cell, (uint32_t)p | ((uint32_t)(ray >> 32) << 8),
+                     0x4D430000u | (uint32_t)((cell >> 32) & 0xFFFF)};
+    philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const uint64_t a = ((((uint64_t)c[0]) << 32) | c[1]) >> 11;
+    const uint64_t b = ((((uint64_t)c[2]) << 32) | c[3]) >> 11;
+    const double u1 = (double)(a + 1) * 0x1.0p-53;  // (0, 1]
+    const double u2 = (double)b * 0x1.0p-53;        // [0, 1)
+    const double rad = sqrt(-2.0 * log(u1));
+    double sn, cs;
+    sincos(6.283185307179586 * u2, &sn, &cs);
+    z[2 * p] = rad * cs;
+    if (2 * p + 1 < D) z[2 * p + 1] = rad * sn;
+  }
+}
+
+// Unit direction exactly as sample_unit_sphere (integrate_mc.py:51-56):
+// y = z / sqrt(z.z).
+template <int D>
+__device__ __forceinline__ void normalise(const double (&z)[D], double (&y)[D]) {
+  double zz = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) zz = fma(z[k], z[k], zz);
+  const double nrm = sqrt(zz);
+#pragma unroll
+  for (int k = 0; k < D; ++k) y[k] = z[k] / nrm;
+}
+
+template <int D>
+struct SrcMC {
+  const double* grec;
+  const int32_t* cells;
+  int64_t per;    // rays per cell
+  const double* dirs;  // nullable: raw Gaussian draws (n, D)
+  uint64_t seed;
+  int64_t n;      // total rays
+  __device__ __forceinline__ void direction(int64_t k, double (&y)[D]) const {
+    double z[D];
+    if (dirs) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) z[j] = dirs[k * D + j];
+    } else {
+      const int64_t c = k / per;
+      philox_normals<D>(seed, cells[c], k - c * per, z);
+    }
+    normalise<D>(z, y);
+  }
+  __device__ __forceinline__ bool load(int64_t k, RayState<D>& r) const {
+    if (k >= n) return false;
+    const int32_t cell = cells[k / per];
+    const double* xc = grec + (int64_t)cell * rec_stride(D);
+#pragma unroll
+    for (int j = 0; j < D; ++j) r.x[j] = xc[j];
+    direction(k, r.u);
+    ray_setup<D>(r, grec, &cell, 1);
+    return true;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Outputs.
+// ---------------------------------------------------------------------------
+struct RayOut {
+  int32_t* idx;
+  double* t;
+  double* rp;  // nullable
+  uint8_t* flag;
+  int32_t* recheck_list;   // nullable
+  int32_t* recheck_count;  // nullable
+};
+
+template <int D>
+__device__ __forceinline__ void ray_store(const RayState<D>& r, int64_t k,
+                                          const int32_t* __restrict__ cand, const RayOut& o) {
+  if (r.ib < 0) {
+    o.idx[k] = -1;
+    o.t[k] = CUDART_INF;
+    o.flag[k] = VR_RAY_ESCAPED;
+    if (o.rp) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) o.rp[k * D + j] = CUDART_NAN;
+    }
+    return;
+  }
+  o.idx[k] = cand ? cand[r.ib] : r.ib;
+  o.t[k] = r.tb;
+  if (o.rp) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) o.rp[k * D + j] = fma(r.tb, r.u[j], r.x[j]);  // raycast.py:210
+  }
+  if (r.near) {
+    o.flag[k] = VR_RAY_RECHECK;
+    if (o.recheck_list) {
+      int slot = atomicAdd(o.recheck_count, 1);
+      o.recheck_list[slot] = (int32_t)k;
+    }
+  } else {
+    o.flag[k] = VR_RAY_OK;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Main kernel: NT threads x R rays, generator tiles of TILE records through a
+// STAGES-deep TMA ring.
+// ---------------------------------------------------------------------------
+template <int D, int R, int NT, int TILE, int STAGES, class Src>
+__global__ void __launch_bounds__(NT, 1)
+    k_raycast(Src src, const double* __restrict__ crec, const int32_t* __restrict__ cand,
+              int64_t n_cand, double sqmax, RayOut out) {
+  constexpr int S = rec_stride(D);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* tiles = reinterpret_cast<double*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)STAGES * TILE * S * sizeof(double));
+
+  const int tid = threadIdx.x;
+  const int64_t ntiles = (n_cand + TILE - 1) / TILE;
+  auto issue = [&](int64_t t) {
+    const int st = (int)(t % STAGES);
+    const int64_t cnt = min((int64_t)TILE, n_cand - t * TILE);
+    const uint32_t bytes = (uint32_t)(cnt * S * sizeof(double));
+    mbar_arrive_expect_tx(&full[st], bytes);
+    bulk_g2s(tiles + (size_t)st * TILE * S, crec + t * TILE * S, bytes, &full[st]);
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int64_t t = 0; t < ntiles && t < STAGES; ++t) issue(t);
+  }
+
+  RayState<D> ray[R];
+  bool act[R];
+  const int64_t k0 = (int64_t)blockIdx.x * NT * R + tid;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    act[j] = src.load(k0 + (int64_t)j * NT, ray[j]);
+    if (!act[j]) {  // padding lane: never passes the screen
+      ray[j].hi = -CUDART_INF;
+#pragma unroll
+      for (int k = 0; k < D; ++k) ray[j].z[k] = 0.0;
+    }
+  }
+
+  for (int64_t t = 0; t < ntiles; ++t) {
+    const int st = (int)(t % STAGES);
+    mbar_wait(&full[st], (uint32_t)((t / STAGES) & 1));
+    const double* tile = tiles + (size_t)st * TILE * S;
+    const int cnt = (int)min((int64_t)TILE, n_cand - t * TILE);
+    const int gbase = (int)(t * TILE);
+#pragma unroll 2
+    for (int c = 0; c < cnt; ++c) {
+      double xi[D];
+      const double2* p2 = reinterpret_cast<const double2*>(tile + c * S);
+#pragma unroll
+      for (int k = 0; k < S / 2; ++k) {
+        const double2 v = p2[k];
+        if (2 * k < D) xi[2 * k] = v.x;
+        if (2 * k + 1 < D) xi[2 * k + 1] = v.y;
+      }
+      const double sq = tile[c * S + D];
+#pragma unroll
+      for (int j = 0; j < R; ++j) ray_screen<D>(ray[j], xi, sq, gbase + c, sqmax);
+    }
+    __syncthreads();
+    if (tid == 0 && t + STAGES < ntiles) issue(t + STAGES);
+  }
+
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+    if (act[j]) ray_store<D>(ray[j], k0 + (int64_t)j * NT, cand, out);
+}
+
+// ---------------------------------------------------------------------------
+// Exact re-check: one CTA per listed ray.  Pass 1: centred t for every valid
+// candidate, lexicographic (t, index) argmin.  Pass 2: runner-up distance at
+// the winner's vertex; DEGENERATE when second < radius (1 + 1e-10)
+// (raycast.py:211-219).
+// ---------------------------------------------------------------------------
+template <int NT>
+__device__ __forceinline__ void block_argmin(double& t, int& i, double* sh_t, int* sh_i) {
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ot = __shfl_xor_sync(0xffffffffu, t, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, i, off);
+    if (ot < t || (ot == t && (unsigned)oi < (unsigned)i)) { t = ot; i = oi; }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) { sh_t[w] = t; sh_i[w] = i; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < NT / 32; ++k) {
+      if (sh_t[k] < t || (sh_t[k] == t && (unsigned)sh_i[k] < (unsigned)i)) { t = sh_t[k]; i = sh_i[k]; }
+    }
+    sh_t[0] = t;
+    sh_i[0] = i;
+  }
+  __syncthreads();
+  t = sh_t[0];
+  i = sh_i[0];
+}
+
+template <int D, int NT, class Src>
+__global__ void __launch_bounds__(NT)
+    k_raycast_recheck(Src src, const double* __restrict__ crec, const int32_t* __restrict__ cand,
+                      int64_t n_cand, const int32_t* __restrict__ list,
+                      const int32_t* __restrict__ count, RayOut out) {
+  constexpr int S = rec_stride(D);
+  __shared__ double sh_t[NT / 32];
+  __shared__ int sh_i[NT / 32];
+  const int cntl = *count;
+  for (int li = blockIdx.x; li < cntl; li += gridDim.x) {
+    const int64_t k = list[li];
+    RayState<D> r;
+    src.load(k, r);
+    double best = CUDART_INF;
+    int bi = -1;
+    for (int64_t c = threadIdx.x; c < n_cand; c += NT) {
+      const double* xc = crec + c * S;
+      double q = 0.0, aa = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        q = fma(r.u[j], xc[j], q);
+        const double a = r.x[j] - xc[j];
+        aa = fma(a, a, aa);
+      }
+      if (q > r.thr) {
+        const double t = (aa - r.base) / (2.0 * (q - r.s));
+        if (t < best) { best = t; bi = (int)c; }  // ascending c per thread: keeps smallest index
+      }
+    }
+    if (bi < 0) best = CUDART_INF;
+    block_argmin<NT>(best, bi, sh_t, sh_i);
+    if (bi < 0 || !(best < CUDART_INF)) {
+      if (threadIdx.x == 0) {
+        out.idx[k] = -1;
+        out.t[k] = CUDART_INF;
+        out.flag[k] = VR_RAY_ESCAPED;
+        if (out.rp)
+          for (int j = 0; j < D; ++j) out.rp[k * D + j] = CUDART_NAN;
+      }
+      continue;
+    }
+    double rp[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) rp[j] = fma(best, r.u[j], r.x[j]);
+    const double radius = sqrt(fmax(fma(best, fma(2.0, r.bu, best), r.base), 0.0));
+    double second = CUDART_INF;
+    for (int64_t c = threadIdx.x; c < n_cand; c += NT) {
+      if ((int)c == bi) continue;
+      const double* xc = crec + c * S;
+      double q = 0.0, dd = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        q = fma(r.u[j], xc[j], q);
+        const double a = rp[j] - xc[j];
+        dd = fma(a, a, dd);
+      }
+      if (q > r.thr) second = fmin(second, sqrt(dd));
+    }
+    int dummy = 0;
+    block_argmin<NT>(second, dummy, sh_t, sh_i);
+    if (threadIdx.x == 0) {
+      out.idx[k] = cand ? cand[bi] : bi;
+      out.t[k] = best;
+      if (out.rp)
+        for (int j = 0; j < D; ++j) out.rp[k * D + j] = rp[j];
+      out.flag[k] = (second < radius * (1.0 + VR_TOL_DEGENERATE)) ? VR_RAY_DEGENERATE : VR_RAY_OK;
+    }
+  }
+}
+
+// Host-side launch helpers -------------------------------------------------
+template <int D>
+struct RaycastCfg {
+  static constexpr int NT = 128;
+  static constexpr int R = (D <= 4) ? 4 : (D <= 6 ? 3 : 2);
+  static constexpr int TILE = 128;
+  static constexpr int STAGES = 4;
+  static size_t smem() {
+    return (size_t)STAGES * TILE * rec_stride(D) * sizeof(double) + STAGES * sizeof(uint64_t);
+  }
+};
+
+template <int D, class Src>
+int launch_raycast(const Src& src, int64_t n_rays, const double* crec, const int32_t* cand,
+                   int64_t n_cand, double sqmax, const RayOut& out, cudaStream_t st) {
+  using C = RaycastCfg<D>;
+  if (n_rays <= 0) return VR_OK;
+  auto kern = k_raycast<D, C::R, C::NT, C::TILE, C::STAGES, Src>;
+  const size_t sm = C::smem();
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int64_t per_block = (int64_t)C::NT * C::R;
+  const int64_t grid = (n_rays + per_block - 1) / per_block;
+  if (n_cand <= 0) return VR_EINVAL;
+  if (out.recheck_count) {  // the re-check list is rebuilt by every launch
+    cudaError_t e = cudaMemsetAsync(out.recheck_count, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return vr_cuda_status(e);
+  }
+  kern<<<(unsigned)grid, C::NT, sm, st>>>(src, crec, cand, n_cand, sqmax, out);
+  VR_RETURN_LAUNCH();
+}
+
+template <int D, class Src>
+int launch_recheck(const Src& src, int64_t max_list, const double* crec, const int32_t* cand,
+                   int64_t n_cand, const int32_t* list, const int32_t* count, const RayOut& out,
+                   cudaStream_t st) {
+  if (max_list <= 0) return VR_OK;
+  const int64_t grid = max_list < 4096 ? max_list : 4096;
+  k_raycast_recheck<D, 256, Src><<<(unsigned)grid, 256, 0, st>>>(src, crec, cand, n_cand, list,
+                                                                 count, out);
+  VR_RETURN_LAUNCH();
+}
+
+}  // namespace vr

@@ -1,0 +1,239 @@
+"""Monte-Carlo cell volumes and interface areas on the B200.
+
+Drop-in for pkg/src/voronray/integrate_mc.py.  Every ray is the RayCast from
+the cell generator with eta = (i,) (integrate_mc.py:60-67); the per-cell sums
+of l^d and l^(d-1)/cos(n_ij, y) (integrate_mc.py:147-160) are formed on the
+device in ray order by vr_mc_reduce.
+
+Two direction sources:
+
+* ``mc_areas_only(ns, i, n, rng)`` -- the reference signature: directions are
+  drawn from the caller's ``rng`` on the host in the reference order
+  (``rng.standard_normal((n, d))`` == n draws of ``(d,)``), so results agree
+  with the reference to floating-point roundoff;
+* ``mc_cells(ns, cells, n, seed)`` -- the throughput path: Philox4x32-10
+  directions generated inside the kernel, keyed by (seed, cell, ray), so the
+  result does not depend on launch shape or GPU count.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import NodeSet
+from .errors import DegenerateConfiguration, UnboundedRay
+from .raycast import RaycastStats, Workspace, candidate_records
+
+Integrand = Callable[[np.ndarray], float]
+
+CELL_OK, CELL_UNBOUNDED, CELL_DEGENERATE, CELL_OVERFLOW = 0, 1, 2, 3
+MAX_FACES_LIMIT = 512
+
+
+@dataclass
+class CellIntegrals:
+    """Per-cell results (integrate_mc.py:27-41)."""
+
+    volume: float = 0.0
+    area: dict = field(default_factory=dict)
+    surface_integral: dict = field(default_factory=dict)
+    volume_integral: float = 0.0
+    n_rays: int = 0
+    m_subsamples: int = 0
+
+
+def sphere_surface_area(d: int) -> float:
+    """2 pi^(d/2) / Gamma(d/2) (integrate_mc.py:44-48)."""
+    if d < 1:
+        raise ValueError("dimension must be positive")
+    return 2.0 * math.pi ** (d / 2.0) / math.gamma(d / 2.0)
+
+
+def sample_unit_sphere(d: int, rng) -> np.ndarray:
+    """Uniform direction by normalising a Gaussian draw (integrate_mc.py:51-56)."""
+    while True:
+        y = rng.standard_normal(d)
+        norm = math.sqrt(float(y @ y))
+        if norm > 0.0:
+            return y / norm
+
+
+@dataclass
+class MCResult:
+    """Batched MC output for cells[c]: volume, faces sorted by neighbour."""
+
+    cells: np.ndarray
+    volume: np.ndarray
+    face_offsets: np.ndarray
+    face_j: np.ndarray
+    face_area: np.ndarray
+    status: np.ndarray
+    first_bad: np.ndarray
+    samples: np.ndarray = None
+
+    def areas(self, c):
+        lo, hi = self.face_offsets[c], self.face_offsets[c + 1]
+        return {int(j): float(a) for j, a in zip(self.face_j[lo:hi], self.face_area[lo:hi])}
+
+
+def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_faces=256,
+               degenerate_is_error=True, want_samples=False, workspace=None, stats=None):
+    """Run rays + recheck + reduce for len(cells) cells x n rays; device tensors out."""
+    rec, sqmax = ns.device_records()
+    dev = rec.device
+    L = _lib.lib()
+    d = ns.dim
+    cells_d = torch.as_tensor(np.ascontiguousarray(cells, dtype=np.int32), device=dev) \
+        if not isinstance(cells, torch.Tensor) else cells.to(device=dev, dtype=torch.int32).contiguous()
+    nc = cells_d.shape[0]
+    total = nc * n
+    ws = workspace or Workspace()
+    dd = None
+    if dirs is not None:
+        dd = dirs if isinstance(dirs, torch.Tensor) else torch.as_tensor(
+            np.ascontiguousarray(dirs, dtype=np.float64))
+        dd = dd.to(device=dev, dtype=torch.float64).contiguous().view(total, d)
+    cand = crec = None
+    n_cand = 0
+    if candidates is not None:
+        cand, crec = candidate_records(ns, candidates, dev)
+        n_cand = cand.shape[0]
+    idx = ws.get("mc_idx", (total,), torch.int32, dev)
+    t = ws.get("mc_t", (total,), torch.float64, dev)
+    flag = ws.get("mc_flag", (total,), torch.uint8, dev)
+    rl = ws.get("mc_rl", (total,), torch.int32, dev)
+    rc = ws.get("mc_rc", (1,), torch.int32, dev)
+    sh = _lib.stream_handle()
+    seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    _lib.check(L.vr_mc_rays(_lib.ptr(rec), ns.n, d, sqmax, _lib.ptr(crec), _lib.ptr(cand), n_cand,
+                            _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed, _lib.ptr(idx),
+                            _lib.ptr(t), _lib.ptr(flag), _lib.ptr(rl), _lib.ptr(rc), sh),
+               "vr_mc_rays")
+    _lib.check(L.vr_mc_recheck(_lib.ptr(rec), ns.n, d, _lib.ptr(crec), _lib.ptr(cand), n_cand,
+                               _lib.ptr(cells_d), n, _lib.ptr(dd), seed, _lib.ptr(rl),
+                               _lib.ptr(rc), total, _lib.ptr(idx), _lib.ptr(t), _lib.ptr(flag),
+                               sh), "vr_mc_recheck")
+    vol = torch.empty(nc, dtype=torch.float64, device=dev)
+    fj = torch.empty((nc, max_faces), dtype=torch.int32, device=dev)
+    fa = torch.empty((nc, max_faces), dtype=torch.float64, device=dev)
+    nf = torch.empty(nc, dtype=torch.int32, device=dev)
+    st = torch.empty(nc, dtype=torch.int32, device=dev)
+    fb = torch.empty(nc, dtype=torch.int64, device=dev)
+    smp = torch.empty(total, dtype=torch.float64, device=dev) if want_samples else None
+    _lib.check(L.vr_mc_reduce(_lib.ptr(rec), d, _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed,
+                              _lib.ptr(idx), _lib.ptr(t), _lib.ptr(flag), max_faces,
+                              1 if degenerate_is_error else 0, sphere_surface_area(d),
+                              _lib.ptr(vol), _lib.ptr(fj), _lib.ptr(fa), _lib.ptr(nf),
+                              _lib.ptr(st), _lib.ptr(fb), _lib.ptr(smp), sh), "vr_mc_reduce")
+    if stats is not None:
+        stats.add(total)
+    return dict(volume=vol, face_j=fj, face_area=fa, nfaces=nf, status=st, first_bad=fb,
+                samples=smp, ray_idx=idx, ray_t=t, ray_flag=flag)
+
+
+def _collect(cells, out, want_samples):
+    vol = out["volume"].cpu().numpy()
+    nf = out["nfaces"].cpu().numpy()
+    fj = out["face_j"].cpu().numpy()
+    fa = out["face_area"].cpu().numpy()
+    off = np.zeros(len(nf) + 1, dtype=np.int64)
+    np.cumsum(nf, out=off[1:])
+    mask = np.arange(fj.shape[1])[None, :] < nf[:, None]
+    return MCResult(cells=np.asarray(cells), volume=vol, face_offsets=off, face_j=fj[mask],
+                    face_area=fa[mask], status=out["status"].cpu().numpy(),
+                    first_bad=out["first_bad"].cpu().numpy(),
+                    samples=out["samples"].cpu().numpy() if want_samples else None)
+
+
+def mc_cells(ns: NodeSet, cells, n: int, seed: int = 0, max_faces: int = 256,
+             want_samples=False, stats: RaycastStats = None, chunk_rays: int = 1 << 26):
+    """Batched device MC (Philox directions) over many cells.
+
+    Returns an :class:`MCResult`; cells whose status is not CELL_OK are the
+    ones the reference would reject (UnboundedRay / DegenerateConfiguration).
+    Work is split into chunks of at most ``chunk_rays`` rays.
+    """
+    if n < 1:
+        raise ValueError("need n >= 1 rays")
+    if not 1 <= max_faces <= MAX_FACES_LIMIT:
+        raise ValueError(f"max_faces must be in [1, {MAX_FACES_LIMIT}]")
+    cells = np.ascontiguousarray(cells, dtype=np.int32)
+    per_chunk = max(1, chunk_rays // n)
+    parts = []
+    ws = Workspace()
+    for lo in range(0, len(cells), per_chunk):
+        sub = cells[lo:lo + per_chunk]
+        out = _mc_device(ns, sub, n, seed=seed, max_faces=max_faces, want_samples=want_samples,
+                         workspace=ws, stats=stats)
+        parts.append(_collect(sub, out, want_samples))
+    if len(parts) == 1:
+        return parts[0]
+    off = [np.zeros(1, dtype=np.int64)]
+    base = 0
+    for p in parts:
+        off.append(p.face_offsets[1:] + base)
+        base += p.face_offsets[-1]
+    return MCResult(cells=cells, volume=np.concatenate([p.volume for p in parts]),
+                    face_offsets=np.concatenate(off),
+                    face_j=np.concatenate([p.face_j for p in parts]),
+                    face_area=np.concatenate([p.face_area for p in parts]),
+                    status=np.concatenate([p.status for p in parts]),
+                    first_bad=np.concatenate([p.first_bad for p in parts]),
+                    samples=np.concatenate([p.samples for p in parts]) if want_samples else None)
+
+
+def mc_directions(ns_dim: int, cells, n: int, seed: int = 0, device=None):
+    """The raw Gaussian draws the Philox path uses for (cells x n) rays,
+    shape (len(cells) * n, d) -- for replay into a host consumer."""
+    L = _lib.lib()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    cd = torch.as_tensor(np.ascontiguousarray(cells, dtype=np.int32), device=dev)
+    out = torch.empty((len(cells) * n, ns_dim), dtype=torch.float64, device=dev)
+    _lib.check(L.vr_mc_directions(ns_dim, len(cells), _lib.ptr(cd), n,
+                                  int(seed) & 0xFFFFFFFFFFFFFFFF, _lib.ptr(out),
+                                  _lib.stream_handle()), "vr_mc_directions")
+    return out.cpu().numpy()
+
+
+def _max_faces_for(ns, n, neighbors):
+    if neighbors is not None:
+        return max(1, min(MAX_FACES_LIMIT, len(neighbors), n))
+    return max(1, min(MAX_FACES_LIMIT, n, ns.n - 1))
+
+
+def mc_areas_only(ns: NodeSet, i: int, n: int, rng, neighbors=None,
+                  stats: RaycastStats = None, return_samples: bool = False):
+    """Face areas and volume of cell i (integrate_mc.py:124-161).
+
+    Returns ``(areas, volume)`` or ``(areas, volume, samples)``.  Raises
+    :class:`UnboundedRay` (with the unit direction of the first escaping ray)
+    or :class:`DegenerateConfiguration` like the reference per-ray path; with
+    ``neighbors`` the degeneracy band is not checked, like _mc_areas_batch.
+    """
+    if n < 1:
+        raise ValueError("need n >= 1 rays")
+    d = ns.dim
+    z = np.asarray(rng.standard_normal((n, d)), dtype=np.float64).reshape(n, d)
+    use_nb = neighbors is not None and len(neighbors) > 0
+    max_faces = _max_faces_for(ns, n, neighbors if use_nb else None)
+    out = _mc_device(ns, [int(i)], n, dirs=z, candidates=neighbors if use_nb else None,
+                     max_faces=max_faces, degenerate_is_error=not use_nb,
+                     want_samples=True, stats=stats)
+    res = _collect([i], out, True)
+    st = int(res.status[0])
+    if st == CELL_UNBOUNDED:
+        y = z[int(res.first_bad[0])]
+        raise UnboundedRay(i, y / math.sqrt(float(y @ y)))
+    if st == CELL_DEGENERATE:
+        raise DegenerateConfiguration(f"a foreign generator lies on a circumsphere of cell {i}")
+    if st == CELL_OVERFLOW:
+        raise RuntimeError(f"cell {i} hit more than {max_faces} faces")
+    areas = res.areas(0)
+    volume = float(res.volume[0])
+    return (areas, volume, res.samples) if return_samples else (areas, volume)

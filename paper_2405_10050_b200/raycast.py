@@ -1,0 +1,367 @@
+"""Incircle RayCast on the B200 (drop-in for voronray.raycast).
+
+``raycast_batch`` is the real entry point: one fused sm_100a kernel over
+rays x generators (csrc/raycast_core.cuh) computes, for every ray, the
+converged answer of the reference's incircle probe loop
+(pkg/src/voronray/raycast.py:154-224) -- the valid generator with the
+smallest crossing parameter -- plus the exact re-check pass for rays whose
+decision lies inside the degeneracy / rounding band.  ``raycast_incircle``
+keeps the reference signature, return type and exceptions on top of it.
+
+The small helpers (``project_t``, ``initial_heuristic``, ``search_direction``,
+``_vertex_directions``, Gram-Schmidt) are host-side scalar geometry with the
+reference semantics (raycast.py:49-82, 295-378); they are not on the hot path.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import NodeSet
+from .errors import DegenerateConfiguration, ParallelGenerator
+
+PARALLEL_TOL = 1e-14
+RANK_TOL = 1e-10
+
+RAY_OK, RAY_ESCAPED, RAY_RECHECK, RAY_DEGENERATE = 0, 1, 2, 3
+
+
+@dataclass(slots=True)
+class RayQuery:
+    """Edge/face ray: generator indices ``eta``, anchor ``r``, direction ``u``."""
+
+    eta: tuple
+    r: np.ndarray
+    u: np.ndarray
+
+
+@dataclass
+class RaycastStats:
+    """Counters (raycast.py:40-46).  On the GPU one fused candidate scan
+    replaces the whole probe loop, so each raycast counts one ``nn_calls``
+    and one ``iterations``."""
+
+    nn_calls: int = 0
+    iterations: int = 0
+    raycasts: int = 0
+
+    def add(self, n):
+        self.raycasts += n
+        self.nn_calls += n
+        self.iterations += n
+
+
+def project_t(r, u, x0, x):
+    """Ray parameter of the point equidistant to ``x0`` and ``x`` (raycast.py:49-65)."""
+    dx = x - x0
+    denom = float(np.dot(u, dx))
+    scale = float(np.linalg.norm(dx))
+    if abs(denom) < PARALLEL_TOL * scale:
+        raise ParallelGenerator("candidate generator lies in the search hyperplane")
+    a = r - x
+    b = r - x0
+    return (float(a @ a) - float(b @ b)) / (2.0 * denom)
+
+
+def initial_heuristic(q: RayQuery, x):
+    """Regular-simplex warm start (raycast.py:68-82).  Result-neutral: the GPU
+    kernel scans every candidate, so it is provided for API parity only."""
+    k = len(q.eta)
+    if k < 2:
+        raise ValueError("heuristic needs at least two known generators")
+    rp = q.r + q.u * float(q.u @ (x - q.r))
+    rx = rp - x
+    radius = math.sqrt(float(rx @ rx))
+    return rp + q.u * (radius / math.sqrt((k - 1) * (k + 1)))
+
+
+def _as_dev(a, dev, dtype):
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=dtype).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device=dev)
+
+
+class RaycastBatch:
+    """Device-resident results of one batched RayCast.
+
+    idx (int32, -1 = escaped), t (fp64), rp (fp64 (n, d) or None),
+    flag (uint8: 0 ok, 1 escaped, 3 degenerate).
+    """
+
+    def __init__(self, idx, t, rp, flag):
+        self.idx, self.t, self.rp, self.flag = idx, t, rp, flag
+
+    def to_host(self):
+        return (self.idx.cpu().numpy(), self.t.cpu().numpy(),
+                None if self.rp is None else self.rp.cpu().numpy(), self.flag.cpu().numpy())
+
+
+class Workspace:
+    """Reusable device buffers for repeated batches of the same size."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def get(self, name, shape, dtype, dev):
+        t = self._bufs.get(name)
+        n = int(np.prod(shape))
+        if t is None or t.numel() < n or t.dtype != dtype or t.device != dev:
+            t = torch.empty(max(n, 1), dtype=dtype, device=dev)
+            self._bufs[name] = t
+        return t[:n].view(shape)
+
+
+def candidate_records(ns: NodeSet, candidates, dev):
+    """Packed records of a candidate subset (raycast.py:100-102)."""
+    rec, _ = ns.device_records(dev)
+    cand = _as_dev(np.asarray(candidates, dtype=np.int64).ravel(), dev, torch.int64)
+    crec = rec.index_select(0, cand).contiguous()
+    return cand.to(torch.int32).contiguous(), crec
+
+
+def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=None,
+                  workspace=None, out=None, stream=None, events=None) -> RaycastBatch:
+    """Batched incircle RayCast on the current CUDA device.
+
+    Args:
+        ns: node set.
+        x: (n, d) ray origins, equidistant to their eta generators.
+        u: (n, d) unit directions.
+        eta: (n, k) generator indices per ray (1 <= k <= d); eta[:, 0] is the
+            reference generator x0 of the crossing formula (raycast.py:182).
+        candidates: optional index subset restricting the search.
+        want_rp: also return the new vertex coordinates x + t u.
+        out: optional dict of preallocated output tensors (idx, t, rp, flag).
+        events: optional three CUDA events recorded before the fused kernel,
+            between it and the re-check pass, and after (kernel timing).
+
+    Stream-ordered; no host synchronisation.
+    """
+    rec, sqmax = ns.device_records()
+    dev = rec.device
+    L = _lib.lib()
+    d = ns.dim
+    xd = _as_dev(x, dev, torch.float64).view(-1, d)
+    ud = _as_dev(u, dev, torch.float64).view(-1, d)
+    n = xd.shape[0]
+    ed = _as_dev(eta, dev, torch.int32)
+    if ed.dim() == 1:
+        ed = ed.view(n, -1) if n else ed.view(0, 1)
+    k = ed.shape[1] if ed.dim() == 2 else 1
+    if not 1 <= k <= d:
+        raise ValueError(f"eta must hold between 1 and d={d} generators, got {k}")
+    if ud.shape[0] != n or ed.shape[0] != n:
+        raise ValueError("x, u and eta must describe the same number of rays")
+    ws = workspace or Workspace()
+    if out is None:
+        out = {}
+    idx = out.get("idx") if out.get("idx") is not None else torch.empty(n, dtype=torch.int32, device=dev)
+    t = out.get("t") if out.get("t") is not None else torch.empty(n, dtype=torch.float64, device=dev)
+    flag = out.get("flag") if out.get("flag") is not None else torch.empty(n, dtype=torch.uint8, device=dev)
+    rp = None
+    if want_rp:
+        rp = out.get("rp") if out.get("rp") is not None else torch.empty((n, d), dtype=torch.float64, device=dev)
+    if stats is not None:
+        stats.add(n)
+    if n == 0:
+        return RaycastBatch(idx, t, rp, flag)
+    cand = crec = None
+    n_cand = 0
+    if candidates is not None:
+        cand, crec = candidate_records(ns, candidates, dev)
+        n_cand = cand.shape[0]
+        if n_cand == 0:
+            raise ValueError("empty candidate set")
+    rl = ws.get("recheck_list", (n,), torch.int32, dev)
+    rc = ws.get("recheck_count", (1,), torch.int32, dev)
+    sh = _lib.stream_handle(stream)
+    if events is not None:
+        events[0].record(stream)
+    _lib.check(L.vr_raycast_batch(_lib.ptr(rec), ns.n, d, sqmax, _lib.ptr(crec), _lib.ptr(cand),
+                                  n_cand, _lib.ptr(xd), _lib.ptr(ud), _lib.ptr(ed), k, n,
+                                  _lib.ptr(idx), _lib.ptr(t), _lib.ptr(rp), _lib.ptr(flag),
+                                  _lib.ptr(rl), _lib.ptr(rc), sh), "vr_raycast_batch")
+    if events is not None:
+        events[1].record(stream)
+    _lib.check(L.vr_raycast_recheck(_lib.ptr(rec), ns.n, d, _lib.ptr(crec), _lib.ptr(cand),
+                                    n_cand, _lib.ptr(xd), _lib.ptr(ud), _lib.ptr(ed), k,
+                                    _lib.ptr(rl), _lib.ptr(rc), n, _lib.ptr(idx), _lib.ptr(t),
+                                    _lib.ptr(rp), _lib.ptr(flag), sh), "vr_raycast_recheck")
+    if events is not None:
+        events[2].record(stream)
+    return RaycastBatch(idx, t, rp, flag)
+
+
+class HostRaycaster:
+    """Batched RayCast on host (pinned) arrays, pipelined over two streams:
+    the H2D copy of chunk c+1 and the D2H copy of chunk c-1 overlap the
+    kernel of chunk c.  The end-to-end public entry point for callers whose
+    rays live in host memory."""
+
+    def __init__(self, ns: NodeSet, n_max: int, eta_len: int, chunk: int = 1 << 17):
+        rec, _ = ns.device_records()
+        self.ns, self.dev, self.chunk, self.k = ns, rec.device, int(chunk), int(eta_len)
+        d = ns.dim
+        c = self.chunk
+        self.copy_stream = torch.cuda.Stream(self.dev)
+        self.comp_stream = torch.cuda.Stream(self.dev)
+        self.buf = [dict(x=torch.empty((c, d), dtype=torch.float64, device=self.dev),
+                         u=torch.empty((c, d), dtype=torch.float64, device=self.dev),
+                         eta=torch.empty((c, self.k), dtype=torch.int32, device=self.dev),
+                         idx=torch.empty(c, dtype=torch.int32, device=self.dev),
+                         t=torch.empty(c, dtype=torch.float64, device=self.dev),
+                         rp=torch.empty((c, d), dtype=torch.float64, device=self.dev),
+                         flag=torch.empty(c, dtype=torch.uint8, device=self.dev),
+                         h2d=torch.cuda.Event(), done=torch.cuda.Event(), d2h=torch.cuda.Event())
+                    for _ in range(2)]
+        self.ws = [Workspace(), Workspace()]
+
+    @staticmethod
+    def pinned(shape, dtype):
+        return torch.empty(shape, dtype=dtype, pin_memory=True)
+
+    def run(self, hx, hu, heta, hidx, ht, hrp, hflag, stats=None):
+        """hx, hu (n, d) f64, heta (n, k) i32 pinned inputs; outputs pinned
+        hidx (n,) i32, ht (n,) f64, hrp (n, d) f64, hflag (n,) u8.  Returns
+        after the last D2H copy has completed."""
+        n = hx.shape[0]
+        c = self.chunk
+        nchunks = (n + c - 1) // c
+        for ci in range(nchunks):
+            b = self.buf[ci & 1]
+            lo, hi = ci * c, min(n, (ci + 1) * c)
+            m = hi - lo
+            with torch.cuda.stream(self.copy_stream):
+                self.copy_stream.wait_event(b["d2h"])  # buffer free again
+                b["x"][:m].copy_(hx[lo:hi], non_blocking=True)
+                b["u"][:m].copy_(hu[lo:hi], non_blocking=True)
+                b["eta"][:m].copy_(heta[lo:hi], non_blocking=True)
+                b["h2d"].record(self.copy_stream)
+            with torch.cuda.stream(self.comp_stream):
+                self.comp_stream.wait_event(b["h2d"])
+                raycast_batch(self.ns, b["x"][:m], b["u"][:m], b["eta"][:m],
+                              out=dict(idx=b["idx"][:m], t=b["t"][:m], rp=b["rp"][:m],
+                                       flag=b["flag"][:m]),
+                              workspace=self.ws[ci & 1], stats=stats,
+                              stream=self.comp_stream)
+                b["done"].record(self.comp_stream)
+            with torch.cuda.stream(self.copy_stream):
+                self.copy_stream.wait_event(b["done"])
+                hidx[lo:hi].copy_(b["idx"][:m], non_blocking=True)
+                ht[lo:hi].copy_(b["t"][:m], non_blocking=True)
+                hrp[lo:hi].copy_(b["rp"][:m], non_blocking=True)
+                hflag[lo:hi].copy_(b["flag"][:m], non_blocking=True)
+                b["d2h"].record(self.copy_stream)
+        self.copy_stream.synchronize()
+
+
+def raycast_incircle(ns: NodeSet, q: RayQuery, stats: RaycastStats = None,
+                     heuristic: bool = True, candidates=None):
+    """Exact first Voronoi object hit by the ray, or None if it escapes.
+
+    Drop-in for raycast.py:154-224: returns ``(tuple(sorted(eta + (i,))), rp)``
+    or ``None``; raises :class:`DegenerateConfiguration` when a foreign
+    generator lies within the reference's 1e-10 band of the circumsphere.
+    ``heuristic`` is result-neutral in the reference and ignored here.
+    """
+    if stats is None:
+        stats = RaycastStats()
+    eta = tuple(int(e) for e in q.eta)
+    res = raycast_batch(ns, np.asarray(q.r, dtype=float)[None], np.asarray(q.u, dtype=float)[None],
+                        np.asarray([eta], dtype=np.int32), candidates=candidates, stats=stats)
+    idx, _, rp, flag = res.to_host()
+    f = int(flag[0])
+    if f == RAY_ESCAPED:
+        return None
+    if f == RAY_DEGENERATE:
+        raise DegenerateConfiguration(
+            f"a foreign generator lies on the circumsphere of {(*eta, int(idx[0]))}")
+    return tuple(sorted((*eta, int(idx[0])))), rp[0]
+
+
+# --- host-side direction helpers (raycast.py:295-378) ----------------------
+
+def _orthonormal_rows(diffs):
+    """Modified Gram-Schmidt, two passes (raycast.py:295-308)."""
+    out = []
+    for row in np.atleast_2d(diffs) if len(diffs) else []:
+        v = np.array(row, dtype=float)
+        norm0 = math.sqrt(float(v @ v))
+        for _ in range(2):
+            for qv in out:
+                v -= (qv @ v) * qv
+        norm = math.sqrt(float(v @ v))
+        if norm < RANK_TOL * max(norm0, 1.0):
+            raise DegenerateConfiguration("generators are affinely dependent")
+        out.append(v / norm)
+    return out
+
+
+def _project_out(w, basis):
+    """Component of ``w`` orthogonal to orthonormal rows (raycast.py:311-317)."""
+    v = np.array(w, dtype=float)
+    for _ in range(2):
+        for qv in basis:
+            v -= (qv @ v) * qv
+    return v
+
+
+def _search_direction(pts, eta, missing):
+    sub = pts[list(eta)]
+    basis = _orthonormal_rows(sub[1:] - sub[0]) if len(eta) > 1 else []
+    w = sub.sum(axis=0) * (1.0 / len(eta)) - pts[missing]
+    v = _project_out(w, basis)
+    norm = math.sqrt(float(v @ v))
+    if norm < RANK_TOL * max(math.sqrt(float(w @ w)), 1.0):
+        raise DegenerateConfiguration(f"generator {missing} lies in the affine span of {eta}")
+    return v / norm
+
+
+def search_direction(ns: NodeSet, sigma, eta):
+    """Outward direction of edge ``eta`` of vertex ``sigma`` (raycast.py:320-342)."""
+    extra = set(sigma) - set(eta)
+    if len(extra) != 1 or not set(eta) <= set(sigma):
+        raise ValueError("eta must be sigma minus exactly one generator")
+    return _search_direction(ns.points, tuple(eta), extra.pop())
+
+
+def vertex_directions_batch(ns: NodeSet, sigma):
+    """All d+1 edge directions of many vertices on the GPU (vr_vertex_directions).
+
+    Returns (u (V, d+1, d) device tensor, ok (V, d+1) uint8 device tensor)."""
+    rec, _ = ns.device_records()
+    dev = rec.device
+    L = _lib.lib()
+    sd = _as_dev(np.asarray(sigma), dev, torch.int32).view(-1, ns.dim + 1)
+    nv = sd.shape[0]
+    u = torch.empty((nv, ns.dim + 1, ns.dim), dtype=torch.float64, device=dev)
+    ok = torch.empty((nv, ns.dim + 1), dtype=torch.uint8, device=dev)
+    _lib.check(L.vr_vertex_directions(_lib.ptr(rec), ns.dim, _lib.ptr(sd), nv, _lib.ptr(u),
+                                      _lib.ptr(ok), _lib.stream_handle()), "vr_vertex_directions")
+    return u, ok
+
+
+def _vertex_directions(pts, sigma, positions):
+    """Outward directions for several edges of one vertex (raycast.py:345-378).
+
+    Host fp64 inverse with the reference's column convention; the traversal
+    itself uses the batched device kernel (vr_vertex_directions)."""
+    sub = pts[list(sigma)]
+    diffs = sub[1:] - sub[0]
+    try:
+        inv = np.linalg.inv(diffs)
+    except np.linalg.LinAlgError:
+        raise DegenerateConfiguration(f"generators of {sigma} are affinely dependent") from None
+    out = {}
+    for k in positions:
+        v = inv.sum(axis=1) if k == 0 else -inv[:, k - 1]
+        norm = math.sqrt(float(v @ v))
+        if not norm > 0.0 or not math.isfinite(norm):
+            raise DegenerateConfiguration(f"generators of {sigma} are affinely dependent")
+        out[k] = v / norm
+    return out

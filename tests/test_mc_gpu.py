@@ -1,0 +1,126 @@
+"""B200 Monte-Carlo parity (SURVEY.md §8(c) rule 4): with the same normals
+(replayed), the device MC equals the reference's mc_areas_only -- per-face
+areas and volume within 1e-12 relative, identical face sets."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import UNIT_SQUARE_POINTS, golden
+
+pytestmark = pytest.mark.gpu
+
+import paper_2405_10050_b200 as vb  # noqa: E402
+from paper_2405_10050_b200.errors import UnboundedRay  # noqa: E402
+from paper_2405_10050_b200.rng import ReplayNormals  # noqa: E402
+from oracle import voronray_oracle as orc  # noqa: E402
+
+REL = 1e-12
+
+
+def _close(a, b, rel=REL):
+    return abs(a - b) <= rel * max(abs(a), abs(b), 1e-300)
+
+
+def _cmp_areas(got, want_j, want_a, rel=REL):
+    assert sorted(got) == [int(j) for j in want_j]
+    for j, a in zip(want_j, want_a):
+        assert _close(got[int(j)], float(a), rel), (j, got[int(j)], a)
+
+
+def test_config4_cells_replayed_normals():
+    gz = golden("mc_golden.npz")
+    pts = np.random.default_rng(0).random((100000, 4))
+    ns = vb.NodeSet(pts)
+    z = gz["c4_z"]
+    off = gz["c4_face_off"]
+    for m, c in enumerate(gz["c4_cells"]):
+        areas, vol = vb.mc_areas_only(ns, int(c), 1000, ReplayNormals(z[m * 1000:(m + 1) * 1000]))
+        assert _close(vol, float(gz["c4_volume"][m]))
+        _cmp_areas(areas, gz["c4_face_j"][off[m]:off[m + 1]], gz["c4_face_area"][off[m]:off[m + 1]])
+
+
+def test_batched_philox_equals_replay_of_its_own_directions():
+    pts = np.random.default_rng(0).random((100000, 4))
+    ns = vb.NodeSet(pts)
+    gz = golden("mc_golden.npz")
+    cells = gz["c4_cells"]
+    res = vb.mc_cells(ns, cells, 1000, seed=0)
+    z = vb.mc_directions(4, cells, 1000, seed=0)
+    # device Philox normals == the numpy port of the same stream (libm vs CUDA
+    # log/sincos differ in the last ulp only)
+    zp = orc.philox_normals(0, cells, 1000, 4)
+    assert np.max(np.abs(z - zp)) <= 1e-13 * max(1.0, np.max(np.abs(zp)))
+    nodes = orc.Nodes(pts)
+    for m, c in enumerate(cells[:3]):
+        areas, vol, _ = orc.mc_areas(nodes, int(c), 1000, orc.Replay(z[m * 1000:(m + 1) * 1000]))
+        assert res.status[m] == 0
+        assert _close(float(res.volume[m]), vol)
+        got = res.areas(m)
+        assert sorted(got) == sorted(areas)
+        for j in areas:
+            assert _close(got[j], areas[j])
+
+
+def test_unit_square_reference_stream():
+    # reference test stream (test_integrate_mc.py:63-67) drawn on the host
+    gz = golden("mc_golden.npz")
+    ns = vb.build_node_set(UNIT_SQUARE_POINTS)
+    areas, vol, smp = vb.mc_areas_only(ns, 0, 20000, vb.rng.stream(2024, "test", 4),
+                                       return_samples=True)
+    assert _close(vol, float(gz["usq_volume"]), 1e-11)
+    _cmp_areas(areas, gz["usq_face_j"], gz["usq_face_area"], 1e-11)
+    assert np.allclose(smp, gz["usq_samples"], rtol=1e-12, atol=0)
+    # the reference's statistical contract (test_integrate_mc.py:56-67)
+    areas, vol = vb.mc_areas_only(ns, 0, 100_000, vb.rng.stream(2024, "test", 3))
+    assert vol == pytest.approx(1.0, rel=0.01)
+    assert sum(areas.values()) == pytest.approx(4.0, rel=0.015)
+    assert set(areas) == {1, 2, 3, 4}
+
+
+def test_neighbour_restricted_batch_path():
+    gz = golden("mc_golden.npz")
+    pts = np.random.default_rng(1234).random((120, 2))
+    ns = vb.build_node_set(pts)
+    i = int(gz["m2_cell"])
+    areas, vol = vb.mc_areas_only(ns, i, 3000, vb.rng.stream(2024, "test", 20),
+                                  neighbors=gz["m2_neighbors"])
+    assert _close(vol, float(gz["m2_volume"]), 1e-11)
+    _cmp_areas(areas, gz["m2_face_j"], gz["m2_face_area"], 1e-11)
+    # full search with the same stream: same answer (test_integrate_mc.py:118-128)
+    a2, v2 = vb.mc_areas_only(ns, i, 3000, vb.rng.stream(2024, "test", 20))
+    assert _close(v2, vol, 1e-11)
+
+
+def test_unbounded_cell_raises_with_direction():
+    gz = golden("mc_golden.npz")
+    ns = vb.build_node_set(UNIT_SQUARE_POINTS)
+    with pytest.raises(UnboundedRay) as info:
+        vb.mc_areas_only(ns, 1, 2000, vb.rng.stream(2024, "test", 8))
+    assert info.value.cell == 1
+    assert info.value.direction.shape == (2,)
+    assert np.allclose(info.value.direction, gz["unb_dir"], rtol=0, atol=1e-15)
+
+
+def test_unbiased_over_repetitions():
+    ns = vb.build_node_set(UNIT_SQUARE_POINTS)
+    est = np.array([vb.mc_areas_only(ns, 0, 2000, vb.rng.stream(2024, "test", 100 + k))[1]
+                    for k in range(50)])
+    se = est.std(ddof=1) / math.sqrt(len(est))
+    assert abs(est.mean() - 1.0) <= 3 * se
+
+
+def test_batched_cells_status_unbounded():
+    # hull cells of a small uniform set are unbounded -> status UNBOUNDED
+    pts = np.random.default_rng(3).random((400, 3))
+    ns = vb.NodeSet(pts)
+    res = vb.mc_cells(ns, np.arange(400), 200, seed=7)
+    c = int(np.argmin(pts[:, 0]))
+    assert res.status[c] == 1
+    assert (res.status == 0).sum() > 100
+    ok = np.nonzero(res.status == 0)[0][:5]
+    z = vb.mc_directions(3, ok, 200, seed=7)
+    nodes = orc.Nodes(pts)
+    for m, c in enumerate(ok):
+        areas, vol, _ = orc.mc_areas(nodes, int(c), 200, orc.Replay(z[m * 200:(m + 1) * 200]))
+        assert _close(float(res.volume[c]), vol)

@@ -1,0 +1,200 @@
+"""B200 RayCast parity: CUDA path (through the C-ABI) vs the reference's
+golden vectors and the CPU oracle.  Bar: bit-exact generator indices and
+escape status; coordinates within 1e-9 * max(1, |r'|)."""
+import numpy as np
+import pytest
+
+from conftest import config2_rays, golden
+
+pytestmark = pytest.mark.gpu
+
+import paper_2405_10050_b200 as vb  # noqa: E402
+from paper_2405_10050_b200.errors import DegenerateConfiguration  # noqa: E402
+from oracle import voronray_oracle as orc  # noqa: E402
+
+COORD_TOL = 1e-9
+
+
+def _arr(*xs):
+    return np.asarray(xs, dtype=float)
+
+
+def triangle_ns():
+    return vb.build_node_set([(0.0, 0.0), (1.0, 0.0), (0.0, 1.0)])
+
+
+def test_triangle_finds_circumcenter():
+    # reference test_raycast.py:102-110
+    stats = vb.RaycastStats()
+    res = vb.raycast_incircle(triangle_ns(), vb.RayQuery((0, 1), _arr(0.5, 0.0), _arr(0.0, 1.0)), stats)
+    sigma, rp = res
+    assert sigma == (0, 1, 2)
+    assert np.allclose(rp, [0.5, 0.5], atol=1e-12)
+    assert stats.nn_calls >= 1 and stats.raycasts == 1
+
+
+def test_triangle_escapes_downward():
+    # test_raycast.py:113-116
+    assert vb.raycast_incircle(triangle_ns(), vb.RayQuery((0, 1), _arr(0.5, 0.0), _arr(0.0, -1.0))) is None
+
+
+def test_cocircular_square_raises_degenerate():
+    # test_raycast.py:145-148: exact tie -> recheck -> runner-up band
+    ns = vb.build_node_set([(0.0, 0.0), (1.0, 0.0), (1.0, 1.0), (0.0, 1.0)])
+    with pytest.raises(DegenerateConfiguration):
+        vb.raycast_incircle(ns, vb.RayQuery((0, 1), _arr(0.5, 0.0), _arr(0.0, 1.0)))
+
+
+def test_near_degenerate_goes_through_recheck():
+    # a fifth point 1e-13 outside the square's circumcircle: the screening
+    # band flags the ray, the exact pass applies the reference band test
+    c = np.array([0.5, 0.5])
+    rad = np.sqrt(0.5)
+    p5 = c + (rad * (1 + 1e-13)) * np.array([np.cos(1.0), np.sin(1.0)])
+    ns = vb.build_node_set([(0.0, 0.0), (1.0, 0.0), (1.0, 1.0), tuple(p5)])
+    with pytest.raises(DegenerateConfiguration):
+        vb.raycast_incircle(ns, vb.RayQuery((0, 1), _arr(0.5, 0.0), _arr(0.0, 1.0)))
+    # moved well outside the band: a regular hit
+    p5 = c + (rad * 1.01) * np.array([np.cos(1.0), np.sin(1.0)])
+    ns = vb.build_node_set([(0.0, 0.0), (1.0, 0.0), (1.0, 1.0), tuple(p5)])
+    sigma, rp = vb.raycast_incircle(ns, vb.RayQuery((0, 1), _arr(0.5, 0.0), _arr(0.0, 1.0)))
+    assert sigma == (0, 1, 2)
+
+
+def _check_against(ns, x, u, eta, status, idx, rp):
+    res = vb.raycast_batch(ns, x, u, eta)
+    gi, gt, grp, gf = res.to_host()
+    ok = status == 0
+    assert np.array_equal(gf[status == 1], np.ones(int((status == 1).sum()), dtype=np.uint8))
+    assert np.array_equal(gi[ok], idx[ok])
+    scale = np.maximum(1.0, np.linalg.norm(rp[ok], axis=1))
+    err = np.linalg.norm(grp[ok] - rp[ok], axis=1) / scale
+    assert err.max(initial=0.0) <= COORD_TOL, err.max()
+    assert np.all(gf[ok] == 0)
+    return gi, grp, gf
+
+
+def test_config2_golden_rays():
+    """First 4000 canonical config-2 rays vs the unmodified reference."""
+    gz = golden("config2_sample.npz")
+    pts = np.random.default_rng(0).random((20000, 6))
+    ns = vb.build_node_set(pts)
+    pos = {int(p): m for m, p in enumerate(gz["pool_p"])}
+    x = np.array([gz["pool_r"][pos[int(p)]] for p in gz["ray_p"]])
+    _check_against(ns, x, gz["u"], gz["g"][:, None], gz["status"], gz["idx"], gz["rp"])
+
+
+def test_config2_descent_vertices_match_reference():
+    gz = golden("config2_sample.npz")
+    pts = np.random.default_rng(0).random((20000, 6))
+    ns = vb.build_node_set(pts)
+    starts = gz["pool_start"][:300]
+    sig, r = vb.descent_batch(ns, starts, seed=0)
+    assert np.array_equal(sig, gz["pool_sigma"][:300])
+    err = np.linalg.norm(r - gz["pool_r"][:300], axis=1) / np.maximum(1, np.linalg.norm(r, axis=1))
+    assert err.max() <= COORD_TOL
+    # single-start drop-in agrees with the batched form
+    v = vb.descent(ns, int(starts[0]), vb.rng.stream(0, "descent", int(starts[0])))
+    assert v.sigma == tuple(int(s) for s in gz["pool_sigma"][0])
+
+
+def test_config5_golden_rays():
+    """N=1e6, d=8 (fp32-upcast generators): generator-start and edge rays."""
+    gz = golden("config5_sample.npz")
+    pts = np.random.default_rng(0).random((10 ** 6, 8)).astype(np.float32).astype(np.float64)
+    ns = vb.NodeSet(pts)
+    g = gz["gen_g"]
+    _check_against(ns, pts[g], gz["gen_u"], g[:, None], gz["gen_status"], gz["gen_idx"], gz["gen_rp"])
+    _check_against(ns, gz["edge_x"], gz["edge_u"], gz["edge_eta"], gz["edge_status"],
+                   gz["edge_idx"], gz["edge_rp"])
+
+
+@pytest.mark.parametrize("d", [2, 3, 4, 5, 6, 7, 8])
+def test_random_rays_vs_oracle_all_dims(d):
+    rng = np.random.default_rng(100 + d)
+    n = 3000 if d <= 5 else 6000
+    pts = rng.random((n, d))
+    ns = vb.build_node_set(pts)
+    m = 700
+    g = rng.integers(0, n, m)
+    u = rng.standard_normal((m, d))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    want_idx, want_t = orc.raycast_argmin(pts, pts[g], u, g[:, None])
+    res = vb.raycast_batch(ns, pts[g], u, g[:, None])
+    gi, gt, grp, gf = res.to_host()
+    assert np.array_equal(gi, np.where(want_idx >= 0, want_idx, -1))
+    assert np.array_equal(gf == 1, want_idx < 0)
+    ok = want_idx >= 0
+    assert np.allclose(gt[ok], want_t[ok], rtol=1e-12, atol=0)
+    # iterative probe loop (the reference algorithm itself) on a subset
+    nodes = orc.Nodes(pts)
+    for k in range(0, m, 35):
+        r = orc.raycast(nodes, (int(g[k]),), pts[g[k]], u[k])
+        if r is None:
+            assert gi[k] == -1
+        else:
+            assert tuple(sorted((int(g[k]), int(gi[k])))) == r[0]
+            assert np.linalg.norm(grp[k] - r[1]) <= COORD_TOL * max(1, np.linalg.norm(r[1]))
+
+
+def test_candidate_restriction_matches_full_search():
+    # reference test_raycast.py:151-164 on a cell's Voronoi neighbours
+    gz = golden("meshes_small.npz")
+    pts = np.random.default_rng(1234).random((120, 2))
+    ns = vb.build_node_set(pts)
+    sig = gz["mesh_2d__sigma"]
+    i = 57
+    nb = np.unique(sig[(sig == i).any(axis=1)])
+    nb = nb[nb != i]
+    rng = np.random.default_rng(0)
+    y = rng.standard_normal((50, 2))
+    y /= np.linalg.norm(y, axis=1, keepdims=True)
+    full = vb.raycast_batch(ns, np.repeat(pts[i:i + 1], 50, 0), y, np.full((50, 1), i)).to_host()
+    rest = vb.raycast_batch(ns, np.repeat(pts[i:i + 1], 50, 0), y, np.full((50, 1), i),
+                            candidates=nb).to_host()
+    assert np.array_equal(full[0], rest[0])
+    assert np.array_equal(full[2], rest[2])
+
+
+def test_edge_cases_sizes():
+    ns = vb.build_node_set([(0.0, 0.0), (1.0, 0.0), (0.0, 1.0)])
+    # zero rays
+    res = vb.raycast_batch(ns, np.zeros((0, 2)), np.zeros((0, 2)), np.zeros((0, 1), dtype=np.int32))
+    assert res.idx.shape[0] == 0
+    # rays not a multiple of the CTA ray block, N = d + 1
+    rng = np.random.default_rng(5)
+    u = rng.standard_normal((1000, 2))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    gi, _, _, gf = vb.raycast_batch(ns, np.zeros((1000, 2)), u, np.zeros((1000, 1), dtype=np.int32)).to_host()
+    want, _ = orc.raycast_argmin(ns.points, np.zeros((1000, 2)), u, np.zeros((1000, 1), dtype=int))
+    assert np.array_equal(gi, want)
+
+
+def test_vertex_directions_match_reference_helper():
+    gz = golden("meshes_small.npz")
+    pts = np.random.default_rng(999).random((90, 3))
+    ns = vb.build_node_set(pts)
+    sig = gz["mesh_3d__sigma"][:40]
+    u, ok = vb.vertex_directions_batch(ns, sig)
+    u = u.cpu().numpy()
+    assert ok.cpu().numpy().all()
+    for v in range(len(sig)):
+        want = orc.vertex_directions(pts, tuple(sig[v]), range(4))
+        for k in range(4):
+            assert float(u[v, k] @ want[k]) >= 1.0 - 1e-12
+
+
+def test_nearest_and_verify():
+    rng = np.random.default_rng(7)
+    pts = rng.random((60, 3))
+    ns = vb.NodeSet(pts)
+    q = rng.random(3)
+    skip = lambda i: i % 3 == 0  # noqa: E731
+    (i1, d1), d2 = ns.nearest2(q, skip)
+    dists = sorted((float(np.linalg.norm(p - q)), i) for i, p in enumerate(pts) if i % 3 != 0)
+    assert i1 == dists[0][1]
+    assert d1 == pytest.approx(dists[0][0])
+    assert d2 == pytest.approx(dists[1][0])
+    assert vb.nearest_neighbor(ns, q, skip=lambda i: True) is None
+    tie = vb.NodeSet([(1.0, 0.0), (-1.0, 0.0), (0.0, 3.0)])
+    assert tie.nearest(np.zeros(2))[0] == 0
