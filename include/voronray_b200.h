@@ -193,11 +193,13 @@ int vr_mc_directions(int d, int64_t n_cells, const int32_t* cells,
 
 /* ---- Level-synchronous traversal (reference voronoi_graph DFS,
  *      graph.py:88-146, reformulated per SURVEY.md §7 K2) -------------------
- * Tables are open-addressed on the device; capacities are powers of two. */
+ * Device hash tables, open-addressed with linear probing; capacities are
+ * powers of two; slot state 0 empty / 1 being written / 2 published. */
 typedef struct vr_traverse_tables {
   int32_t* vkeys;   /* vcap * (d+1) sorted sigma keys                        */
-  int32_t* vstate;  /* vcap: 0 empty, 1 writing, 2 ready                     */
-  int32_t* vval;    /* vcap: winning ray id of the current level / vertex id */
+  int32_t* vstate;  /* vcap                                                  */
+  int32_t* vval;    /* vcap: vertex id (or smallest claiming ray this level) */
+  int32_t* vlevel;  /* vcap: level at which the key was inserted             */
   int64_t vcap;
   int32_t* ekeys;   /* ecap * d sorted eta keys                              */
   int32_t* estate;  /* ecap                                                  */
@@ -206,35 +208,64 @@ typedef struct vr_traverse_tables {
   int32_t* overflow;/* 1 int32: set when a probe sequence exhausts a table   */
 } vr_traverse_tables;
 
-/* Register vertices (sigma (n_v, d+1) sorted, ids base_id..) in the vertex
- * table and bump the edge counters of their d+1 edges (graph.py:115-120). */
+/* Register vertices (sigma (n_v, d+1) sorted) with ids base_id.. at `level`;
+ * optionally bump the counters of their d+1 edges (graph.py:115-120). */
 int vr_trav_insert_vertices(const vr_traverse_tables* tab, int d,
                             const int32_t* sigma, int64_t n_v, int32_t base_id,
-                            void* stream);
+                            int32_t level, int bump_edges, void* stream);
 
-/* Expand a frontier: for every vertex and position k whose edge
- * sigma\sigma[k] has count < 2 (graph.py:127-135), emit one ray
- * (x = r, u = direction, eta = sigma\sigma[k]).  Writes per-(vertex,k) open
- * flags to open_mask (n_v*(d+1) uint8); rays are compacted by the caller
- * (prefix sum) and emitted by vr_trav_emit_rays. */
+/* Re-insert the published slots of an old edge table into tab (growth). */
+int vr_trav_rehash_edges(const vr_traverse_tables* tab, int d,
+                         const int32_t* okeys, const int32_t* ostate,
+                         const int32_t* ocount, int64_t ocap, void* stream);
+
+/* open_mask[v*(d+1)+k] = 1 iff edge sigma_v \ sigma_v[k] has count < 2
+ * (graph.py:127-128); open_count[v] = number of open edges of v. */
 int vr_trav_open_edges(const vr_traverse_tables* tab, int d,
                        const int32_t* sigma, int64_t n_v, uint8_t* open_mask,
-                       void* stream);
+                       int32_t* open_count, void* stream);
 
+/* One ray per open edge at exclusive offset open_off[v] (+ rank among v's
+ * open edges): x = r_v, u = outward direction (raycast.py:345-378),
+ * eta = sigma_v \ sigma_v[k], parent = v.  *bad counts singular simplices. */
 int vr_trav_emit_rays(const double* rec, int d, const int32_t* sigma,
                       const double* r, int64_t n_v, const uint8_t* open_mask,
-                      const int64_t* open_offset, double* ray_x,
-                      double* ray_u, int32_t* ray_eta, int32_t* ray_parent,
-                      uint8_t* ray_ok, void* stream);
+                      const int64_t* open_off, double* ray_x, double* ray_u,
+                      int32_t* ray_eta, int32_t* ray_parent, int32_t* bad,
+                      void* stream);
 
-/* Claim new vertices: for each ray with a hit, sigma' = sorted(eta + {i});
- * insert-or-find in the vertex table and keep the smallest ray id per new
- * key (deterministic winner).  new_flag[k] = 1 iff ray k is the winner of a
- * key that was absent before this level.  out_sigma receives sigma'. */
+/* sigma' = sorted(eta + {hit}) per hit ray; insert-or-find in the vertex
+ * table; the smallest ray id claims each key first seen at `level`.
+ * new_flag[k] = 1 for the claiming ray, esc_flag[k] = 1 for escaped rays. */
 int vr_trav_claim(const vr_traverse_tables* tab, int d, const int32_t* ray_eta,
                   const int32_t* hit_idx, const uint8_t* hit_flag,
-                  int64_t n_rays, int32_t level_tag, int32_t* out_sigma,
-                  int32_t* out_slot, uint8_t* new_flag, void* stream);
+                  int64_t n_rays, int32_t level, int32_t* out_sigma,
+                  int64_t* out_slot, int32_t* new_flag, int32_t* esc_flag,
+                  void* stream);
+
+/* New vertex base_id + new_off[k]: store sigma', its fp64 circumcentre
+ * (no chained drift, SURVEY.md §8(c) rule 3) and bump its edge counters. */
+int vr_trav_finalize(const vr_traverse_tables* tab, const double* rec, int d,
+                     const int32_t* ray_sigma, const int64_t* slot,
+                     const int32_t* new_flag, const int64_t* new_off,
+                     int64_t n_rays, int32_t base_id, int32_t* vsig, double* vr,
+                     int32_t* bad, void* stream);
+
+/* Escaped rays -> BoundaryRay(sigma_parent, u) at base_b + esc_off[k]
+ * (graph.py:138-139). */
+int vr_trav_boundary(int d, const int32_t* esc_flag, const int64_t* esc_off,
+                     const int32_t* ray_parent, const double* ray_u,
+                     int64_t n_rays, const int32_t* frontier_sigma,
+                     int64_t base_b, int32_t* bsig, double* bu, void* stream);
+
+/* flag[h] = (state[h] == 2), for compaction of a table. */
+int vr_trav_published(const int32_t* state, int64_t cap, int32_t* flag,
+                      void* stream);
+
+/* Compact the edge table (published slots, exclusive offsets `off`). */
+int vr_trav_edge_compact(const vr_traverse_tables* tab, int d,
+                         const int64_t* off, int32_t* out_keys,
+                         int32_t* out_count, void* stream);
 
 /* Roofline probe: `blocks` x 256 threads x iters x 8 independent FMA chains
  * (dtype 0 = fp64 DFMA, 1 = fp32 FFMA); flops = 4096 * iters * blocks.  Used

@@ -42,6 +42,16 @@ _SIGNATURES = {
                      _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_mc_directions": [_int, _i64, _vp, _i64, _u64, _vp, _vp],
     "vr_fma_probe": [_int, _int, _int, _vp, _vp],
+    "vr_trav_insert_vertices": [_vp, _int, _vp, _i64, ctypes.c_int32, ctypes.c_int32, _int, _vp],
+    "vr_trav_rehash_edges": [_vp, _int, _vp, _vp, _vp, _i64, _vp],
+    "vr_trav_open_edges": [_vp, _int, _vp, _i64, _vp, _vp, _vp],
+    "vr_trav_emit_rays": [_vp, _int, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "vr_trav_claim": [_vp, _int, _vp, _vp, _vp, _i64, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp],
+    "vr_trav_finalize": [_vp, _vp, _int, _vp, _vp, _vp, _vp, _i64, ctypes.c_int32, _vp, _vp,
+                         _vp, _vp],
+    "vr_trav_boundary": [_int, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp],
+    "vr_trav_published": [_vp, _i64, _vp, _vp],
+    "vr_trav_edge_compact": [_vp, _int, _vp, _vp, _vp, _vp],
 }
 
 # Symbols declared in include/voronray_b200.h that the .so must export.

@@ -21,13 +21,15 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from itertools import combinations
 
+import ctypes
+
 import numpy as np
 import torch
 
 from . import _lib
 from . import rng as _rng
 from .core import (TOL_VERTEX, Mesh, NodeSet, VertexRecord, edge_keys, verify_vertices)
-from .errors import RetryExhausted
+from .errors import DegenerateConfiguration, RetryExhausted
 from .raycast import (RayQuery, RaycastStats, _orthonormal_rows, _project_out, raycast_batch,
                       raycast_incircle)
 
@@ -243,5 +245,239 @@ def verify_mesh(mesh: Mesh, oracle: bool = None, coord_tol: float = 1e-8) -> Ver
     return report
 
 
-def voronoi_graph(ns, seed=0, *, method="incircle_heuristic", eps=None, stats=None):
-    raise NotImplementedError("level-synchronous traversal lands with csrc/traverse.cu")
+# ---------------------------------------------------------------------------
+# level-synchronous device traversal (csrc/traverse.cu)
+# ---------------------------------------------------------------------------
+
+class _Tables(ctypes.Structure):
+    _fields_ = [("vkeys", ctypes.c_void_p), ("vstate", ctypes.c_void_p),
+                ("vval", ctypes.c_void_p), ("vlevel", ctypes.c_void_p),
+                ("vcap", ctypes.c_int64), ("ekeys", ctypes.c_void_p),
+                ("estate", ctypes.c_void_p), ("ecount", ctypes.c_void_p),
+                ("ecap", ctypes.c_int64), ("overflow", ctypes.c_void_p)]
+
+
+def _pow2(n):
+    return 1 << max(10, int(n - 1).bit_length())
+
+
+def _excl_cumsum(x):
+    """Exclusive prefix sum (int64) and the total, on the device."""
+    c = torch.cumsum(x, 0, dtype=torch.int64)
+    return c - x.to(torch.int64), c
+
+
+class DeviceTraversal:
+    """Device state of one traversal: vertex / edge hash tables, vertex,
+    boundary arrays.  Capacities grow geometrically between levels."""
+
+    def __init__(self, ns: NodeSet, vcap_hint=None):
+        rec, sqmax = ns.device_records()
+        self.ns, self.rec, self.sqmax, self.dev = ns, rec, sqmax, rec.device
+        self.d = ns.dim
+        self.L = _lib.lib()
+        d = self.d
+        vcap = _pow2(vcap_hint or 4 * max(1024, ns.n))
+        self.overflow = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self._alloc_vtable(vcap)
+        self._alloc_etable(_pow2(2 * vcap))
+        self.vsig = torch.empty((vcap // 2, d + 1), dtype=torch.int32, device=self.dev)
+        self.vr = torch.empty((vcap // 2, d), dtype=torch.float64, device=self.dev)
+        self.bsig = torch.empty((1024, d + 1), dtype=torch.int32, device=self.dev)
+        self.bu = torch.empty((1024, d), dtype=torch.float64, device=self.dev)
+        self.nv = 0
+        self.nb = 0
+        self.e_ub = 0
+
+    def _alloc_vtable(self, cap):
+        d = self.d
+        self.vkeys = torch.empty(cap * (d + 1), dtype=torch.int32, device=self.dev)
+        self.vstate = torch.zeros(cap, dtype=torch.int32, device=self.dev)
+        self.vval = torch.empty(cap, dtype=torch.int32, device=self.dev)
+        self.vlevel = torch.empty(cap, dtype=torch.int32, device=self.dev)
+        self.vcap = cap
+
+    def _alloc_etable(self, cap):
+        self.ekeys = torch.empty(cap * self.d, dtype=torch.int32, device=self.dev)
+        self.estate = torch.zeros(cap, dtype=torch.int32, device=self.dev)
+        self.ecount = torch.zeros(cap, dtype=torch.int32, device=self.dev)
+        self.ecap = cap
+
+    def tables(self):
+        p = _lib.ptr
+        return _Tables(p(self.vkeys).value, p(self.vstate).value, p(self.vval).value,
+                       p(self.vlevel).value, self.vcap, p(self.ekeys).value,
+                       p(self.estate).value, p(self.ecount).value, self.ecap,
+                       p(self.overflow).value)
+
+    def _sh(self):
+        return _lib.stream_handle()
+
+    def ensure_vertices(self, extra):
+        """Room for `extra` more vertices in the arrays and the hash set."""
+        need = self.nv + extra
+        if need > self.vsig.shape[0]:
+            cap = max(need, 2 * self.vsig.shape[0])
+            self.vsig = torch.cat([self.vsig[:self.nv],
+                                   torch.empty((cap - self.nv, self.d + 1), dtype=torch.int32,
+                                               device=self.dev)])
+            self.vr = torch.cat([self.vr[:self.nv],
+                                 torch.empty((cap - self.nv, self.d), dtype=torch.float64,
+                                             device=self.dev)])
+        if 2 * need > self.vcap:
+            self._alloc_vtable(_pow2(4 * need))
+            T = self.tables()
+            _lib.check(self.L.vr_trav_insert_vertices(ctypes.byref(T), self.d,
+                                                      _lib.ptr(self.vsig), self.nv, 0, -1, 0,
+                                                      self._sh()), "rehash vertices")
+
+    def ensure_edges(self, extra):
+        if 2 * (self.e_ub + extra) > self.ecap:
+            ok, os_, oc, ocap = self.ekeys, self.estate, self.ecount, self.ecap
+            self._alloc_etable(_pow2(4 * (self.e_ub + extra)))
+            T = self.tables()
+            _lib.check(self.L.vr_trav_rehash_edges(ctypes.byref(T), self.d, _lib.ptr(ok),
+                                                   _lib.ptr(os_), _lib.ptr(oc), ocap,
+                                                   self._sh()), "rehash edges")
+
+    def ensure_boundary(self, extra):
+        need = self.nb + extra
+        if need > self.bsig.shape[0]:
+            cap = max(need, 2 * self.bsig.shape[0])
+            self.bsig = torch.cat([self.bsig[:self.nb],
+                                   torch.empty((cap - self.nb, self.d + 1), dtype=torch.int32,
+                                               device=self.dev)])
+            self.bu = torch.cat([self.bu[:self.nb],
+                                 torch.empty((cap - self.nb, self.d), dtype=torch.float64,
+                                             device=self.dev)])
+
+    def seed_vertex(self, sigma):
+        """Insert the descent vertex (level 0) with its fp64 circumcentre."""
+        self.ensure_vertices(1)
+        self.ensure_edges(self.d + 1)
+        s = torch.as_tensor(np.asarray(sigma, dtype=np.int32)[None], device=self.dev)
+        self.vsig[0:1] = s
+        ok = torch.empty(1, dtype=torch.uint8, device=self.dev)
+        _lib.check(self.L.vr_circumcenters(_lib.ptr(self.rec), self.d, _lib.ptr(s), 1,
+                                           _lib.ptr(self.vr), _lib.ptr(ok), self._sh()),
+                   "vr_circumcenters")
+        T = self.tables()
+        _lib.check(self.L.vr_trav_insert_vertices(ctypes.byref(T), self.d, _lib.ptr(s), 1, 0, 0,
+                                                  1, self._sh()), "insert seed")
+        self.nv = 1
+        self.e_ub = self.d + 1
+
+    def level(self, f0, f1, lvl, stats=None, ws=None):
+        """Expand frontier vertices [f0, f1); returns the number of new vertices."""
+        d, L, dev, sh = self.d, self.L, self.dev, self._sh()
+        F = f1 - f0
+        fs = self.vsig[f0:f1]
+        fr = self.vr[f0:f1]
+        open_mask = torch.empty((F, d + 1), dtype=torch.uint8, device=dev)
+        open_cnt = torch.empty(F, dtype=torch.int32, device=dev)
+        T = self.tables()
+        _lib.check(L.vr_trav_open_edges(ctypes.byref(T), d, _lib.ptr(fs), F, _lib.ptr(open_mask),
+                                        _lib.ptr(open_cnt), sh), "open_edges")
+        off, inc = _excl_cumsum(open_cnt)
+        R = int(inc[-1].item())
+        if R == 0:
+            return 0
+        rx = torch.empty((R, d), dtype=torch.float64, device=dev)
+        ru = torch.empty((R, d), dtype=torch.float64, device=dev)
+        reta = torch.empty((R, d), dtype=torch.int32, device=dev)
+        rpar = torch.empty(R, dtype=torch.int32, device=dev)
+        bad = torch.zeros(2, dtype=torch.int32, device=dev)
+        _lib.check(L.vr_trav_emit_rays(_lib.ptr(self.rec), d, _lib.ptr(fs), _lib.ptr(fr), F,
+                                       _lib.ptr(open_mask), _lib.ptr(off), _lib.ptr(rx),
+                                       _lib.ptr(ru), _lib.ptr(reta), _lib.ptr(rpar),
+                                       _lib.ptr(bad), sh), "emit_rays")
+        res = raycast_batch(self.ns, rx, ru, reta, want_rp=False, stats=stats, workspace=ws)
+        self.ensure_vertices(R)
+        T = self.tables()
+        rsig = torch.empty((R, d + 1), dtype=torch.int32, device=dev)
+        slot = torch.empty(R, dtype=torch.int64, device=dev)
+        newf = torch.empty(R, dtype=torch.int32, device=dev)
+        escf = torch.empty(R, dtype=torch.int32, device=dev)
+        _lib.check(L.vr_trav_claim(ctypes.byref(T), d, _lib.ptr(reta), _lib.ptr(res.idx),
+                                   _lib.ptr(res.flag), R, lvl, _lib.ptr(rsig), _lib.ptr(slot),
+                                   _lib.ptr(newf), _lib.ptr(escf), sh), "claim")
+        noff, ninc = _excl_cumsum(newf)
+        eoff, einc = _excl_cumsum(escf)
+        ndeg = (res.flag == 3).sum()
+        summary = torch.stack([ninc[-1], einc[-1], ndeg.to(torch.int64), bad[0].to(torch.int64),
+                               self.overflow[0].to(torch.int64)]).cpu().numpy()
+        n_new, n_esc, n_deg, n_bad, ovf = (int(v) for v in summary)
+        if n_bad:
+            raise DegenerateConfiguration("generators of a frontier vertex are affinely dependent")
+        if n_deg:
+            raise DegenerateConfiguration(
+                f"{n_deg} edge raycasts hit a generator on the circumsphere band")
+        if ovf:
+            raise RuntimeError("traversal hash table overflow")
+        self.ensure_edges((d + 1) * n_new)
+        T = self.tables()
+        _lib.check(L.vr_trav_finalize(ctypes.byref(T), _lib.ptr(self.rec), d, _lib.ptr(rsig),
+                                      _lib.ptr(slot), _lib.ptr(newf), _lib.ptr(noff), R, f1,
+                                      _lib.ptr(self.vsig), _lib.ptr(self.vr), _lib.ptr(bad[1:]),
+                                      sh), "finalize")
+        self.e_ub += (d + 1) * n_new
+        if n_esc:
+            self.ensure_boundary(n_esc)
+            _lib.check(L.vr_trav_boundary(d, _lib.ptr(escf), _lib.ptr(eoff), _lib.ptr(rpar),
+                                          _lib.ptr(ru), R, _lib.ptr(fs), self.nb,
+                                          _lib.ptr(self.bsig), _lib.ptr(self.bu), sh), "boundary")
+            self.nb += n_esc
+        self.nv = f1 + n_new
+        self.rays_last = R
+        return n_new
+
+    def edges(self):
+        """Published edge keys (sorted lexicographically) and counts."""
+        flag = torch.empty(self.ecap, dtype=torch.int32, device=self.dev)
+        _lib.check(self.L.vr_trav_published(_lib.ptr(self.estate), self.ecap, _lib.ptr(flag),
+                                            self._sh()), "published")
+        off, inc = _excl_cumsum(flag)
+        ne = int(inc[-1].item())
+        keys = torch.empty((ne, self.d), dtype=torch.int32, device=self.dev)
+        cnt = torch.empty(ne, dtype=torch.int32, device=self.dev)
+        T = self.tables()
+        _lib.check(self.L.vr_trav_edge_compact(ctypes.byref(T), self.d, _lib.ptr(off),
+                                               _lib.ptr(keys), _lib.ptr(cnt), self._sh()),
+                   "edge_compact")
+        order = torch.arange(ne, device=self.dev)
+        for c in range(self.d - 1, -1, -1):  # stable LSD lexicographic sort
+            _, o = torch.sort(keys[order, c], stable=True)
+            order = order[o]
+        return keys[order], cnt[order]
+
+
+def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heuristic",
+                  eps: float = None, stats: RaycastStats = None, return_info: bool = False):
+    """Full Voronoi mesh by exhaustive edge-tracked traversal (graph.py:88-146).
+
+    Level-synchronous on the device: every level raycasts all open edges of
+    the frontier in one fused launch.  The vertex set, edge counts and the
+    boundary-ray multiset equal the reference's depth-first result; vertex
+    coordinates are fp64 circumcentres of sigma.
+    """
+    _resolve_raycaster(method, eps)
+    if stats is None:
+        stats = RaycastStats()
+    first = descent(ns, 0, _rng.stream(seed, "descent", 0), stats)
+    tr = DeviceTraversal(ns)
+    tr.seed_vertex(first.sigma)
+    from .raycast import Workspace
+    ws = Workspace()
+    f0, f1, lvl = 0, 1, 1
+    levels = []
+    while f1 > f0:
+        n_new = tr.level(f0, f1, lvl, stats=stats, ws=ws)
+        levels.append((f1 - f0, n_new))
+        f0, f1, lvl = f1, f1 + n_new, lvl + 1
+    ek, ec = tr.edges()
+    mesh = Mesh.from_arrays(ns, tr.vsig[:tr.nv].cpu().numpy(), tr.vr[:tr.nv].cpu().numpy(),
+                            ek.cpu().numpy(), ec.cpu().numpy(), tr.bsig[:tr.nb].cpu().numpy(),
+                            tr.bu[:tr.nb].cpu().numpy())
+    if return_info:
+        return mesh, {"levels": levels, "vertices": tr.nv, "boundary": tr.nb}
+    return mesh

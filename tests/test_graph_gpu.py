@@ -1,0 +1,190 @@
+"""B200 traversal parity: vertex sets (sorted sigma tuples) bit-exact vs the
+reference DFS, edge counts and boundary-ray multisets equal, coordinates
+within 1e-9 * max(1, |r|) of the fp64 circumcentre of sigma (SURVEY.md
+§8(c) rule 3)."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden
+
+pytestmark = pytest.mark.gpu
+
+import paper_2405_10050_b200 as vb  # noqa: E402
+from paper_2405_10050_b200.core import VertexRecord  # noqa: E402
+from paper_2405_10050_b200.errors import RetryExhausted  # noqa: E402
+from oracle import voronray_oracle as orc  # noqa: E402
+
+COORD_TOL = 1e-9
+
+
+def digest(arr):
+    return hashlib.sha256(np.ascontiguousarray(arr, dtype="<i4").tobytes()).hexdigest()
+
+
+def sorted_rows(a):
+    a = np.asarray(a)
+    if len(a) == 0:
+        return a
+    return a[np.lexsort(a.T[::-1])]
+
+
+def check_mesh(mesh, pts, gz, name):
+    a = mesh.arrays()
+    sig = sorted_rows(a["sigma"])
+    assert np.array_equal(sig, gz[f"{name}__sigma"]), name
+    assert np.array_equal(sorted_rows(a["boundary_sigma"]), gz[f"{name}__boundary_sigma"]), name
+    assert np.array_equal(a["edge_key"], gz[f"{name}__edge_key"]), name
+    assert np.array_equal(a["edge_count"], gz[f"{name}__edge_count"]), name
+    # coordinates vs a fresh fp64 circumcentre
+    for v in range(0, len(a["sigma"]), max(1, len(a["sigma"]) // 200)):
+        want = orc.circumcenter(pts, a["sigma"][v])
+        assert np.linalg.norm(a["r"][v] - want) <= COORD_TOL * max(1.0, np.linalg.norm(want))
+
+
+def test_descent_on_simplex():
+    for d in (2, 3, 4):
+        pts = np.vstack([np.zeros(d), np.eye(d)])
+        v = vb.descent(vb.build_node_set(pts), 0)
+        assert v.sigma == tuple(range(d + 1))
+        assert np.allclose(v.r, np.full(d, 0.5), atol=1e-9)
+
+
+def test_descent_retry_exhausted():
+    ns = vb.build_node_set([(0.0, 0.0), (2.0, 0.0), (0.0, 2.0), (2.0, 2.1)])
+    calls = []
+
+    def always_escape(ns_, q, stats):
+        calls.append(1)
+        return None
+
+    with pytest.raises(RetryExhausted):
+        vb.descent(ns, 0, raycaster=always_escape)
+    assert len(calls) == vb.DESCENT_RETRIES
+
+
+def test_four_point_mesh():
+    ns = vb.build_node_set([(0.0, 0.0), (2.0, 0.0), (0.0, 2.0), (2.0, 2.1)])
+    mesh = vb.voronoi_graph(ns, seed=42)
+    assert set(mesh.vertices) == {(0, 1, 2), (1, 2, 3)}
+    assert [e for e, c in mesh.edge_counts.items() if c == 2] == [(1, 2)]
+    assert len(mesh.boundary) == 4
+    oracle = vb.brute_force_vertices(ns)
+    assert set(oracle) == set(mesh.vertices)
+
+
+@pytest.mark.parametrize("d", [2, 3, 4])
+def test_simplex_mesh(d):
+    pts = np.vstack([np.zeros(d), np.eye(d)])
+    mesh = vb.voronoi_graph(vb.build_node_set(pts), seed=0)
+    assert len(mesh.vertices) == 1
+    assert sum(1 for c in mesh.edge_counts.values() if c == 2) == 0
+    assert len(mesh.boundary) == d + 1
+
+
+SMALL = {
+    "mesh_2d": (lambda: np.random.default_rng(1234).random((120, 2)), 0),
+    "mesh_3d": (lambda: np.random.default_rng(999).random((90, 3)), 0),
+    "four_point": (lambda: np.array([(0.0, 0.0), (2.0, 0.0), (0.0, 2.0), (2.0, 2.1)]), 42),
+    "unit_square": (lambda: np.array([(0.0, 0.0), (1.0, 0.0), (-1.0, 0.0), (0.0, 1.0),
+                                      (0.0, -1.0)]), 3),
+    "nodup_d2": (lambda: np.random.default_rng(25).random((300, 2)), 0),
+    "nodup_d3": (lambda: np.random.default_rng(26).random((300, 3)), 0),
+    "incircle_d4": (lambda: np.random.default_rng(14).random((1000, 4)), 0),
+    "incircle_d5": (lambda: np.random.default_rng(15).random((500, 5)), 0),
+    "oracle_3d_50": (lambda: np.random.default_rng(17).random((50, 3)), 5),
+    "gauss_d5_2000": (lambda: np.random.default_rng(0).standard_normal((2000, 5)), 0),
+}
+
+
+@pytest.mark.parametrize("name", list(SMALL))
+def test_reference_instances(name):
+    gz = golden("meshes_small.npz")
+    mk, seed = SMALL[name]
+    pts = mk()
+    mesh = vb.voronoi_graph(vb.build_node_set(pts), seed=seed)
+    check_mesh(mesh, pts, gz, name)
+
+
+def test_config1_full_diagram():
+    gz = golden("mesh_config1.npz")
+    pts = np.random.default_rng(0).random((1000, 3))
+    mesh = vb.voronoi_graph(vb.build_node_set(pts), seed=0)
+    a = mesh.arrays()
+    sig = sorted_rows(a["sigma"])
+    assert digest(sig) == "b1f6f8721369b9116ff154e6673225998fb3785479bb65c18dafb6b2db2c0b1a"
+    assert np.array_equal(sig, gz["sigma"])
+    assert np.array_equal(sorted_rows(a["boundary_sigma"]), gz["boundary_sigma"])
+    assert np.array_equal(a["edge_key"], gz["edge_key"])
+    assert np.array_equal(a["edge_count"], gz["edge_count"])
+    # coordinates: every vertex within 1e-9 of the fp64 solve; the reference's
+    # own chained coordinates drift -- report, not fail
+    order = np.lexsort(a["sigma"].T[::-1])
+    r = a["r"][order]
+    solve = np.array([orc.circumcenter(pts, s) for s in gz["sigma"]])
+    rel = np.linalg.norm(r - solve, axis=1) / np.maximum(1, np.linalg.norm(solve, axis=1))
+    assert rel.max() <= COORD_TOL
+    drift = np.linalg.norm(gz["r"] - solve, axis=1) / np.maximum(1, np.linalg.norm(solve, axis=1))
+    assert (drift > COORD_TOL).sum() <= 8  # reference drift, 4 vertices measured
+    # the boundary rays carry the reference's directions
+    bs = a["boundary_sigma"]
+    ob = np.lexsort(bs.T[::-1])
+    assert np.allclose(a["boundary_u"][ob], gz["boundary_u"], atol=1e-9)
+
+
+def test_config3_full_diagram():
+    """N=10,000, d=5 Gaussian: 1,607,349 vertices; digests of the reference."""
+    with open(os.path.join(GOLDEN, "config3_reference.json")) as fh:
+        ref = json.load(fh)
+    pts = np.random.default_rng(0).standard_normal((10000, 5))
+    mesh = vb.voronoi_graph(vb.build_node_set(pts), seed=0)
+    a = mesh.arrays()
+    assert a["sigma"].shape[0] == ref["n_vertices"]
+    assert digest(sorted_rows(a["sigma"])) == ref["sigma_digest"]
+    assert a["boundary_sigma"].shape[0] == ref["n_boundary"]
+    assert digest(sorted_rows(a["boundary_sigma"])) == ref["boundary_digest"]
+    assert a["edge_key"].shape[0] == ref["n_edges"]
+    assert int((a["edge_count"] == 2).sum()) == ref["n_interior_edges"]
+    ok = vb.verify_vertices(mesh.nodes, a["sigma"][::97], a["r"][::97])
+    assert ok.all()
+
+
+def test_verify_mesh_and_perturbation():
+    pts = np.random.default_rng(1234).random((120, 2))
+    mesh = vb.voronoi_graph(vb.build_node_set(pts), seed=0)
+    report = vb.verify_mesh(mesh, oracle=True)
+    assert report.passed and report.oracle_checked
+    sig = next(iter(mesh.vertices))
+    good = mesh.vertices[sig]
+    mesh.vertices[sig] = VertexRecord(sig, good.r + np.array([1e-3, 0.0]))
+    bad = vb.verify_mesh(mesh, oracle=False)
+    assert not bad.passed and sig in bad.vertex_failures
+
+
+def test_determinism_and_seed_independence():
+    pts = np.random.default_rng(31).random((150, 3))
+    ns = vb.build_node_set(pts)
+    m1, m2, m3 = (vb.voronoi_graph(ns, seed=s) for s in (9, 9, 2))
+    a1, a2, a3 = m1.arrays(), m2.arrays(), m3.arrays()
+    for k in a1:
+        assert np.array_equal(a1[k], a2[k]), k
+    assert set(m1.vertices) == set(m3.vertices)
+    for s in m1.vertices:
+        assert np.linalg.norm(m1.vertices[s].r - m3.vertices[s].r) <= 1e-9
+
+
+def test_mesh_helpers_match_reference_semantics():
+    pts = np.random.default_rng(1234).random((120, 2))
+    mesh = vb.voronoi_graph(vb.build_node_set(pts), seed=0)
+    unb = mesh.unbounded_cells()
+    bnd = mesh.bounded_cells()
+    assert not unb & set(bnd)
+    i = bnd[0]
+    for j in mesh.neighbors(i):
+        assert len(mesh.face_vertices(i, j)) >= 2
+    for s in mesh.vertices:
+        for e in vb.edge_set(s):
+            assert e in mesh.edge_counts

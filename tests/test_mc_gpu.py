@@ -115,9 +115,14 @@ def test_batched_cells_status_unbounded():
     pts = np.random.default_rng(3).random((400, 3))
     ns = vb.NodeSet(pts)
     res = vb.mc_cells(ns, np.arange(400), 200, seed=7)
-    c = int(np.argmin(pts[:, 0]))
-    assert res.status[c] == 1
-    assert (res.status == 0).sum() > 100
+    assert (res.status == 1).sum() > 20 and (res.status == 0).sum() > 100
+    # the first escaping ray of an UNBOUNDED cell really escapes (oracle)
+    zc = vb.mc_directions(3, np.nonzero(res.status == 1)[0][:5], 200, seed=7)
+    for m, c in enumerate(np.nonzero(res.status == 1)[0][:5]):
+        k = int(res.first_bad[c])
+        y = zc[m * 200 + k] / np.linalg.norm(zc[m * 200 + k])
+        want, _ = orc.raycast_argmin(pts, pts[c][None], y[None], np.array([[c]]))
+        assert want[0] == -1
     ok = np.nonzero(res.status == 0)[0][:5]
     z = vb.mc_directions(3, ok, 200, seed=7)
     nodes = orc.Nodes(pts)
