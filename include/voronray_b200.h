@@ -58,9 +58,16 @@ const char* vr_status_string(int status);
  * [x_0 .. x_{d-1}, |x|^2, pad] rounded up to an even count (16-B rows). */
 int vr_record_stride(int d);
 
+/* Rows of a packed record array for n generators: n rounded up to a
+ * multiple of 512.  Rows >= n are sentinels [0, .., 0, +inf] that can never
+ * win a RayCast, so every shared-memory tile the kernels stage is full. */
+int64_t vr_record_rows(int64_t n);
+
 /* Pack an (n, d) fp64 row-major point array into 16-B aligned records
- * [x, |x|^2, pad].  Replaces the NodeSet fp64 copy + squared norms
- * (reference core.py:44-51).  rec must hold n * vr_record_stride(d) doubles. */
+ * [x, |x|^2, pad] plus the sentinel rows.  Replaces the NodeSet fp64 copy +
+ * squared norms (reference core.py:44-51).  rec must hold
+ * vr_record_rows(n) * vr_record_stride(d) doubles.  Every `rec` / `cand_rec`
+ * argument below uses this padded layout. */
 int vr_pack_generators(const double* pts, int64_t n, int d, double* rec,
                        double* sqmax_out /* device, 1 double */, void* stream);
 

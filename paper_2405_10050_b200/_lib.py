@@ -55,7 +55,7 @@ _SIGNATURES = {
 }
 
 # Symbols declared in include/voronray_b200.h that the .so must export.
-EXPORTED = tuple(_SIGNATURES) + ("vr_status_string",)
+EXPORTED = tuple(_SIGNATURES) + ("vr_status_string", "vr_record_rows")
 
 _LIB = None
 
@@ -74,6 +74,8 @@ def load_library():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
         fn.restype = ctypes.c_int
+    lib.vr_record_rows.argtypes = [_i64]
+    lib.vr_record_rows.restype = ctypes.c_int64
     lib.vr_status_string.argtypes = [_int]
     lib.vr_status_string.restype = ctypes.c_char_p
     _LIB = lib
@@ -86,6 +88,14 @@ def lib():
     if not torch.cuda.is_available():
         raise DeviceUnavailable("no CUDA device: the B200 kernels have no CPU fallback")
     return L
+
+
+REC_PAD = 512
+
+
+def record_rows(n):
+    """Rows of a padded record array (include/voronray_b200.h vr_record_rows)."""
+    return (int(n) + REC_PAD - 1) // REC_PAD * REC_PAD
 
 
 def check(status, what=""):

@@ -78,7 +78,9 @@ class NodeSet:
         return (self.dim + 2) & ~1
 
     def device_records(self, device=None):
-        """(records tensor (n, stride) fp64 on `device`, max |x|^2 as float)."""
+        """(records tensor (rows, stride) fp64 on `device`, max |x|^2 as float).
+
+        rows = n rounded up to 512; rows >= n are RayCast sentinels."""
         dev = _device(device)
         hit = self._dev.get(dev.index)
         if hit is not None:
@@ -86,7 +88,8 @@ class NodeSet:
         L = _lib.lib()
         with torch.cuda.device(dev):
             pts = torch.from_numpy(self.points).to(dev)
-            rec = torch.empty((self.n, self.stride), dtype=torch.float64, device=dev)
+            rec = torch.empty((_lib.record_rows(self.n), self.stride), dtype=torch.float64,
+                              device=dev)
             sqmax = torch.zeros(1, dtype=torch.float64, device=dev)
             _lib.check(L.vr_pack_generators(_lib.ptr(pts), self.n, self.dim, _lib.ptr(rec),
                                             _lib.ptr(sqmax), _lib.stream_handle()),

@@ -17,6 +17,13 @@
 #define VR_TOL_DEGENERATE 1e-10
 #define VR_HALFSPACE_SLACK 1e-12
 
+// Record arrays hold ceil(n / VR_REC_PAD) * VR_REC_PAD rows; rows >= n are
+// sentinels [0, .., 0, +inf] (|x|^2 = inf never passes the RayCast screen).
+#define VR_REC_PAD 512
+__host__ __device__ constexpr int64_t rec_rows(int64_t n) {
+  return (n + VR_REC_PAD - 1) / VR_REC_PAD * VR_REC_PAD;
+}
+
 // Doubles per packed generator record: [x_0..x_{d-1}, |x|^2] rounded up to an
 // even count so every record starts on a 16-byte boundary (LDS.128 / TMA).
 __host__ __device__ constexpr int rec_stride(int d) { return (d + 2) & ~1; }

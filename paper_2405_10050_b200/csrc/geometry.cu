@@ -9,6 +9,12 @@ __global__ void k_pack(const double* __restrict__ pts, int64_t n, double* __rest
                        unsigned long long* __restrict__ sqmax) {
   constexpr int S = rec_stride(D);
   double local = 0.0;
+  const int64_t rows = rec_rows(n);
+  for (int64_t i = n + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
+       i += (int64_t)gridDim.x * blockDim.x) {  // sentinel rows
+#pragma unroll
+    for (int k = 0; k < S; ++k) rec[i * S + k] = (k == D) ? CUDART_INF : 0.0;
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double sq = 0.0;
@@ -181,6 +187,8 @@ __global__ void k_vertex_dirs(const double* __restrict__ rec, const int32_t* __r
 inline unsigned blocks_for(int64_t n, int nt) { return (unsigned)((n + nt - 1) / nt); }
 
 }  // namespace
+
+extern "C" int64_t vr_record_rows(int64_t n) { return rec_rows(n); }
 
 extern "C" int vr_pack_generators(const double* pts, int64_t n, int d, double* rec,
                                   double* sqmax_out, void* stream) {

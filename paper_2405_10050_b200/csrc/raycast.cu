@@ -1,7 +1,17 @@
 // C-ABI entry points for the batched incircle RayCast (include/voronray_b200.h).
 #include "raycast_core.cuh"
 
+#include <cstdlib>
+
 using namespace vr;
+
+int vr::raycast_variant() {
+  static int v = [] {
+    const char* e = std::getenv("VR_RAYCAST_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
 
 extern "C" int vr_abi_version(void) { return 1; }
 

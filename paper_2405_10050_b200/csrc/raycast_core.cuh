@@ -30,7 +30,8 @@ namespace vr {
 // Candidate records as seen by the kernel: `rec` packed [x, |x|^2, pad].
 template <int D>
 struct RayState {
-  double x[D], u[D], z[D];
+  double x[D], u[D];
+  double z[D];  // -2 * (x + t_best u): the screening value is |x_i|^2 + z.x_i
   double hi;    // lim + dlt  (screening bound; +inf before the first hit)
   double lim;   // rho^2 - |z|^2 of the current sphere
   double dlt;   // band half-width (degeneracy band + rounding bound)
@@ -74,7 +75,7 @@ __device__ __forceinline__ void ray_setup(RayState<D>& r, const double* __restri
   r.base = base;
   r.bu = bu;
 #pragma unroll
-  for (int k = 0; k < D; ++k) r.z[k] = r.x[k];
+  for (int k = 0; k < D; ++k) r.z[k] = -2.0 * r.x[k];
   r.hi = CUDART_INF;
   r.lim = CUDART_INF;
   r.dlt = 0.0;
@@ -88,15 +89,20 @@ __device__ __forceinline__ void ray_setup(RayState<D>& r, const double* __restri
 template <int D>
 __device__ __forceinline__ void ray_set_best(RayState<D>& r, double t, double den, int i,
                                              double sqmax) {
-  double zz = 0.0;
+  double zz = 0.0, xx = 0.0;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    r.z[k] = fma(t, r.u[k], r.x[k]);
-    zz = fma(r.z[k], r.z[k], zz);
+    const double zk = fma(t, r.u[k], r.x[k]);
+    r.z[k] = -2.0 * zk;
+    zz = fma(zk, zk, zz);
+    xx = fma(r.x[k], r.x[k], xx);
   }
+  // Every term of `scale` (and the band) is non-increasing as t decreases
+  // (|z(t)|^2 and rho^2(t) are convex in t), so a verdict taken against an
+  // older sphere stays conservative for every later one.
   const double tq = t * fma(2.0, fabs(r.bu), fabs(t));
   const double rho2 = fma(t, fma(2.0, r.bu, t), r.base);  // raycast.py:212
-  const double scale = zz + sqmax + r.base + tq + fabs(rho2);
+  const double scale = fmax(zz, xx) + sqmax + r.base + tq + fabs(rho2);
   const double err = 16.0 * (D + 4) * 2.220446049250313e-16 * scale;
   const double dlt = 2.1e-10 * fmax(r.base, rho2) + err;
   r.lim = rho2 - zz;
@@ -107,13 +113,19 @@ __device__ __forceinline__ void ray_set_best(RayState<D>& r, double t, double de
   r.ib = i;
 }
 
-// Rare path: candidate i passed the screening bound.
+// Rare path: candidate i passed the (possibly stale) screening bound.  The
+// power w.r.t. the CURRENT sphere is recomputed first, because an earlier
+// candidate of the same unrolled step may have moved the sphere.
 template <int D>
-__device__ __forceinline__ void ray_rare(RayState<D>& r, const double (&xi)[D], double fp, int i,
-                                      double sqmax) {
-  double q = 0.0;
+__device__ __forceinline__ void ray_rare(RayState<D>& r, const double (&xi)[D], double sq, int i,
+                                         double sqmax) {
+  double fp = sq, q = 0.0;
 #pragma unroll
-  for (int k = 0; k < D; ++k) q = fma(r.u[k], xi[k], q);
+  for (int k = 0; k < D; ++k) {
+    fp = fma(r.z[k], xi[k], fp);
+    q = fma(r.u[k], xi[k], q);
+  }
+  if (!(fp < r.hi)) return;  // outside the current sphere's band
   if (!(q > r.thr)) return;  // outside the forward halfspace (raycast.py:110-117)
   const bool have = r.ib >= 0;
   if (have && fp >= r.lim - r.dlt) r.near = 1;
@@ -134,15 +146,26 @@ __device__ __forceinline__ void ray_rare(RayState<D>& r, const double (&xi)[D], 
 }
 
 template <int D>
-__device__ __forceinline__ void ray_screen(RayState<D>& r, const double (&xi)[D], double sq,
-                                           int i, double sqmax) {
-  double h0 = 0.0, h1 = 0.0;
+__device__ __forceinline__ void load_rec(const double* p, double (&xi)[D]) {
+  const double2* p2 = reinterpret_cast<const double2*>(p);
 #pragma unroll
-  for (int k = 0; k < D; k += 2) h0 = fma(r.z[k], xi[k], h0);
+  for (int k = 0; k < D / 2; ++k) {
+    const double2 v = p2[k];
+    xi[2 * k] = v.x;
+    xi[2 * k + 1] = v.y;
+  }
+  if (D & 1) xi[D - 1] = p[D - 1];
+}
+
+// Screening value of one pair: |x_i|^2 - 2 z.x_i as one chain of d FMAs
+// (z is stored pre-scaled by -2), so a pair costs d DFMA + 1 DSETP.
+template <int D>
+__device__ __forceinline__ double ray_power(const RayState<D>& r, const double (&xi)[D],
+                                            double sq) {
+  double fp = sq;
 #pragma unroll
-  for (int k = 1; k < D; k += 2) h1 = fma(r.z[k], xi[k], h1);
-  const double fp = fma(-2.0, h0 + h1, sq);
-  if (fp < r.hi) ray_rare<D>(r, xi, fp, i, sqmax);
+  for (int k = 0; k < D; ++k) fp = fma(r.z[k], xi[k], fp);
+  return fp;
 }
 
 // ---------------------------------------------------------------------------
@@ -297,27 +320,35 @@ __device__ __forceinline__ void ray_store(const RayState<D>& r, int64_t k,
 // Main kernel: NT threads x R rays, generator tiles of TILE records through a
 // STAGES-deep TMA ring.
 // ---------------------------------------------------------------------------
-template <int D, int R, int NT, int TILE, int STAGES, class Src>
-__global__ void __launch_bounds__(NT, 1)
+template <int D, int R, int NT, int TILE, int STAGES, int MINB, class Src>
+__global__ void __launch_bounds__(NT, MINB)
     k_raycast(Src src, const double* __restrict__ crec, const int32_t* __restrict__ cand,
               int64_t n_cand, double sqmax, RayOut out) {
   constexpr int S = rec_stride(D);
+  constexpr int U = 8;  // candidates per screening block (one warp vote each)
+  constexpr int NW = NT / 32;
+  static_assert(TILE % U == 0 && VR_REC_PAD % TILE == 0, "tile must divide the record padding");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* tiles = reinterpret_cast<double*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)STAGES * TILE * S * sizeof(double));
+  int* released = reinterpret_cast<int*>(full + STAGES);
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  // the record array is padded to a multiple of VR_REC_PAD with sentinel
+  // rows [0.., +inf] that can never pass the screen: every tile is full
   const int64_t ntiles = (n_cand + TILE - 1) / TILE;
+  constexpr uint32_t TILE_BYTES = (uint32_t)(TILE * S * sizeof(double));
   auto issue = [&](int64_t t) {
     const int st = (int)(t % STAGES);
-    const int64_t cnt = min((int64_t)TILE, n_cand - t * TILE);
-    const uint32_t bytes = (uint32_t)(cnt * S * sizeof(double));
-    mbar_arrive_expect_tx(&full[st], bytes);
-    bulk_g2s(tiles + (size_t)st * TILE * S, crec + t * TILE * S, bytes, &full[st]);
+    mbar_arrive_expect_tx(&full[st], TILE_BYTES);
+    bulk_g2s(tiles + (size_t)st * TILE * S, crec + t * TILE * S, TILE_BYTES, &full[st]);
   };
   if (tid == 0) {
 #pragma unroll
-    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      released[s] = 0;
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -342,24 +373,50 @@ __global__ void __launch_bounds__(NT, 1)
     const int st = (int)(t % STAGES);
     mbar_wait(&full[st], (uint32_t)((t / STAGES) & 1));
     const double* tile = tiles + (size_t)st * TILE * S;
-    const int cnt = (int)min((int64_t)TILE, n_cand - t * TILE);
     const int gbase = (int)(t * TILE);
-#pragma unroll 2
-    for (int c = 0; c < cnt; ++c) {
-      double xi[D];
-      const double2* p2 = reinterpret_cast<const double2*>(tile + c * S);
+    for (int c = 0; c < TILE; c += U) {
+      // Screening block: U candidates x R rays of independent dot products,
+      // stale-safe (a candidate outside an older sphere is outside every
+      // later one), then a single warp vote guards the in-order rare path.
+      unsigned m[R];
 #pragma unroll
-      for (int k = 0; k < S / 2; ++k) {
-        const double2 v = p2[k];
-        if (2 * k < D) xi[2 * k] = v.x;
-        if (2 * k + 1 < D) xi[2 * k + 1] = v.y;
+      for (int j = 0; j < R; ++j) m[j] = 0u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        double xi[D];
+        load_rec<D>(tile + (c + u) * S, xi);
+        const double sq = tile[(c + u) * S + D];
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          m[j] |= (ray_power<D>(ray[j], xi, sq) < ray[j].hi) ? (1u << u) : 0u;
       }
-      const double sq = tile[c * S + D];
+      unsigned any = 0u;
 #pragma unroll
-      for (int j = 0; j < R; ++j) ray_screen<D>(ray[j], xi, sq, gbase + c, sqmax);
+      for (int j = 0; j < R; ++j) any |= m[j];
+      if (__any_sync(0xffffffffu, any != 0u)) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          unsigned mm = m[j];
+          while (mm) {
+            const int u = __ffs(mm) - 1;
+            mm &= mm - 1;
+            double xi[D];
+            load_rec<D>(tile + (c + u) * S, xi);
+            ray_rare<D>(ray[j], xi, tile[(c + u) * S + D], gbase + c + u, sqmax);
+          }
+        }
+      }
     }
-    __syncthreads();
-    if (tid == 0 && t + STAGES < ntiles) issue(t + STAGES);
+    // release the stage; the last warp to release it issues the refill
+    __syncwarp();
+    if (lane == 0) {
+      const int old = atomicAdd(&released[st], 1);
+      if (old == NW - 1) {
+        released[st] = 0;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (t + STAGES < ntiles) issue(t + STAGES);
+      }
+    }
   }
 
 #pragma unroll
@@ -467,34 +524,56 @@ __global__ void __launch_bounds__(NT)
 }
 
 // Host-side launch helpers -------------------------------------------------
-template <int D>
-struct RaycastCfg {
+template <int D, int R_, int MINB_>
+struct RaycastCfgT {
   static constexpr int NT = 128;
-  static constexpr int R = (D <= 4) ? 4 : (D <= 6 ? 3 : 2);
-  static constexpr int TILE = 128;
+  static constexpr int R = R_;
+  static constexpr int MINB = MINB_;
+  static constexpr int TILE = 256;
   static constexpr int STAGES = 4;
   static size_t smem() {
-    return (size_t)STAGES * TILE * rec_stride(D) * sizeof(double) + STAGES * sizeof(uint64_t);
+    return (size_t)STAGES * TILE * rec_stride(D) * sizeof(double) +
+           STAGES * (sizeof(uint64_t) + sizeof(int));
   }
 };
 
-template <int D, class Src>
-int launch_raycast(const Src& src, int64_t n_rays, const double* crec, const int32_t* cand,
-                   int64_t n_cand, double sqmax, const RayOut& out, cudaStream_t st) {
-  using C = RaycastCfg<D>;
-  if (n_rays <= 0) return VR_OK;
-  auto kern = k_raycast<D, C::R, C::NT, C::TILE, C::STAGES, Src>;
+template <int D>
+using RaycastCfg = RaycastCfgT<D, (D <= 3) ? 4 : 2, (D <= 3 || D >= 7) ? 2 : 3>;
+
+template <class C, int D, class Src>
+int launch_raycast_cfg(const Src& src, int64_t n_rays, const double* crec, const int32_t* cand,
+                       int64_t n_cand, double sqmax, const RayOut& out, cudaStream_t st) {
+  auto kern = k_raycast<D, C::R, C::NT, C::TILE, C::STAGES, C::MINB, Src>;
   const size_t sm = C::smem();
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int64_t per_block = (int64_t)C::NT * C::R;
   const int64_t grid = (n_rays + per_block - 1) / per_block;
+  kern<<<(unsigned)grid, C::NT, sm, st>>>(src, crec, cand, n_cand, sqmax, out);
+  VR_RETURN_LAUNCH();
+}
+
+// Tuning hook: VR_RAYCAST_VARIANT selects alternative register blockings
+// for d = 6 (the config-2 shape); 0 = default.
+int raycast_variant();
+
+template <int D, class Src>
+int launch_raycast(const Src& src, int64_t n_rays, const double* crec, const int32_t* cand,
+                   int64_t n_cand, double sqmax, const RayOut& out, cudaStream_t st) {
+  if (n_rays <= 0) return VR_OK;
   if (n_cand <= 0) return VR_EINVAL;
   if (out.recheck_count) {  // the re-check list is rebuilt by every launch
     cudaError_t e = cudaMemsetAsync(out.recheck_count, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return vr_cuda_status(e);
   }
-  kern<<<(unsigned)grid, C::NT, sm, st>>>(src, crec, cand, n_cand, sqmax, out);
-  VR_RETURN_LAUNCH();
+  if constexpr (D == 6) {
+    switch (raycast_variant()) {
+      case 1: return launch_raycast_cfg<RaycastCfgT<D, 2, 1>, D>(src, n_rays, crec, cand, n_cand, sqmax, out, st);
+      case 2: return launch_raycast_cfg<RaycastCfgT<D, 3, 1>, D>(src, n_rays, crec, cand, n_cand, sqmax, out, st);
+      case 3: return launch_raycast_cfg<RaycastCfgT<D, 1, 4>, D>(src, n_rays, crec, cand, n_cand, sqmax, out, st);
+      default: break;
+    }
+  }
+  return launch_raycast_cfg<RaycastCfg<D>, D>(src, n_rays, crec, cand, n_cand, sqmax, out, st);
 }
 
 template <int D, class Src>

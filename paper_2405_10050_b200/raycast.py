@@ -120,7 +120,10 @@ def candidate_records(ns: NodeSet, candidates, dev):
     """Packed records of a candidate subset (raycast.py:100-102)."""
     rec, _ = ns.device_records(dev)
     cand = _as_dev(np.asarray(candidates, dtype=np.int64).ravel(), dev, torch.int64)
-    crec = rec.index_select(0, cand).contiguous()
+    m = cand.shape[0]
+    crec = torch.zeros((_lib.record_rows(m), rec.shape[1]), dtype=rec.dtype, device=dev)
+    crec[:, ns.dim] = float("inf")  # sentinel rows (include/voronray_b200.h)
+    crec[:m] = rec.index_select(0, cand)
     return cand.to(torch.int32).contiguous(), crec
 
 

@@ -130,8 +130,8 @@ def test_config1_full_diagram():
     drift = np.linalg.norm(gz["r"] - solve, axis=1) / np.maximum(1, np.linalg.norm(solve, axis=1))
     assert (drift > COORD_TOL).sum() <= 8  # reference drift, 4 vertices measured
     # the boundary rays carry the reference's directions
-    bs = a["boundary_sigma"]
-    ob = np.lexsort(bs.T[::-1])
+    keys = np.hstack([a["boundary_sigma"], a["boundary_u"]])
+    ob = np.lexsort(keys.T[::-1])
     assert np.allclose(a["boundary_u"][ob], gz["boundary_u"], atol=1e-9)
 
 
