@@ -81,6 +81,7 @@ class NodeSet:
         """(records tensor (rows, stride) fp64 on `device`, max |x|^2 as float).
 
         rows = n rounded up to 512; rows >= n are RayCast sentinels."""
+        _lib.lib()  # raises DeviceUnavailable without the library or a GPU
         dev = _device(device)
         hit = self._dev.get(dev.index)
         if hit is not None:

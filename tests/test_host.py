@@ -1,0 +1,115 @@
+"""Host-side logic of the drop-in API that needs no GPU: input validation,
+error types, RNG streams, geometry helpers and the array-backed Mesh."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+import paper_2405_10050_b200 as vb
+from paper_2405_10050_b200.errors import DimensionMismatch, DuplicatePoint, ParallelGenerator
+from paper_2405_10050_b200.raycast import _orthonormal_rows, _project_out, _vertex_directions
+from oracle import voronray_oracle as orc
+
+
+def test_build_validation():
+    # reference test_core.py:21-50
+    ns = vb.build_node_set([(0, 0), (1, 0), (0, 1)])
+    assert ns.n == 3 and ns.dim == 2
+    with pytest.raises(DimensionMismatch):
+        vb.build_node_set([(0, 0), (1, 0, 0)])
+    with pytest.raises(DuplicatePoint):
+        vb.build_node_set([(0, 0), (1, 1), (0, 0)])
+    with pytest.raises(DimensionMismatch):
+        vb.build_node_set([(0, 0, 0), (1, 0, 0)])
+    with pytest.raises(DimensionMismatch):
+        vb.build_node_set([(0.0,), (1.0,), (2.0,)])
+    with pytest.raises(DimensionMismatch):
+        vb.build_node_set(np.random.default_rng(0).random((20, 9)))
+    with pytest.raises(ValueError):
+        vb.NodeSet(np.random.default_rng(0).random((5, 2)), backend="octree")
+    with pytest.raises(ValueError):
+        ns.points[0, 0] = 5.0
+    with pytest.raises(DimensionMismatch):
+        vb.nearest_neighbor(ns, (0.0, 0.0, 0.0))
+
+
+def test_edge_sets():
+    assert vb.edge_set((1, 2, 3)) == {(1, 2), (1, 3), (2, 3)}
+    for d in range(2, 8):
+        sigma = tuple(sorted(np.random.default_rng(d).choice(100, d + 1, replace=False)))
+        edges = vb.edge_set(sigma)
+        assert len(edges) == d + 1 and all(len(e) == d for e in edges)
+
+
+def test_rng_and_replay():
+    a = vb.rng.stream(3, "mc", 9).standard_normal((4, 3))
+    b = orc.stream(3, "mc", 9).standard_normal((4, 3))
+    assert np.array_equal(a, b)
+    rp = vb.rng.ReplayNormals(np.arange(10.0))
+    assert np.array_equal(rp.standard_normal(3), [0.0, 1.0, 2.0])
+    assert np.array_equal(rp.standard_normal((2, 2)), [[3.0, 4.0], [5.0, 6.0]])
+    assert rp.remaining == 3
+    with pytest.raises(IndexError):
+        rp.standard_normal(4)
+
+
+def test_sphere_area_and_sampling():
+    assert vb.sphere_surface_area(2) == pytest.approx(2 * math.pi, rel=1e-14)
+    assert vb.sphere_surface_area(3) == pytest.approx(4 * math.pi, rel=1e-14)
+    assert vb.sphere_surface_area(5) == pytest.approx(8 * math.pi ** 2 / 3, rel=1e-12)
+    rng = vb.rng.stream(2024, "test", 0)
+    for d in (2, 3, 5):
+        assert abs(np.linalg.norm(vb.sample_unit_sphere(d, rng)) - 1.0) <= 1e-12
+
+
+def test_project_t_and_heuristic():
+    t = vb.project_t(np.array([0.0, 0]), np.array([1.0, 0]), np.array([0.0, 1]), np.array([2.0, 1]))
+    assert t == pytest.approx(1.0, abs=1e-14)
+    with pytest.raises(ParallelGenerator):
+        vb.project_t(np.array([0.0, 0]), np.array([1.0, 0]), np.array([0.0, 1]), np.array([0.0, 3]))
+    q = vb.RayQuery((0, 1), np.array([0.5, 0.0]), np.array([0.0, 1.0]))
+    g = vb.initial_heuristic(q, np.array([0.0, 0.0]))
+    assert np.allclose(g, [0.5, 0.5 / math.sqrt(3.0)], atol=1e-14)
+
+
+def test_direction_helpers_match_oracle():
+    rng = np.random.default_rng(5)
+    pts = rng.random((6, 5))
+    sig = (0, 1, 2, 3, 4, 5)
+    got = _vertex_directions(pts, sig, range(6))
+    want = orc.vertex_directions(pts, sig, range(6))
+    for k in range(6):
+        assert np.allclose(got[k], want[k], atol=1e-14)
+    basis = _orthonormal_rows(pts[1:4] - pts[0])
+    v = _project_out(rng.standard_normal(5), basis)
+    for row in pts[1:4] - pts[0]:
+        assert abs(float(v @ row)) <= 1e-12
+
+
+def test_array_mesh_helpers():
+    gz = golden("meshes_small.npz")
+    pts = np.random.default_rng(1234).random((120, 2))
+    ns = vb.NodeSet(pts)
+    sig = gz["mesh_2d__sigma"]
+    m = vb.Mesh.from_arrays(ns, sig, gz["mesh_2d__r"], gz["mesh_2d__edge_key"],
+                            gz["mesh_2d__edge_count"], gz["mesh_2d__boundary_sigma"],
+                            np.zeros((len(gz["mesh_2d__boundary_sigma"]), 2)))
+    assert len(m.vertices) == len(sig)
+    # neighbours from the dict semantics of the reference (core.py:223-246)
+    neigh = {}
+    for s in sig:
+        for i in s:
+            neigh.setdefault(int(i), set()).update(int(x) for x in s)
+    for i in range(120):
+        want = tuple(sorted(neigh.get(i, {i}) - {i}))
+        assert m.neighbors(i) == want
+    unb = m.unbounded_cells()
+    assert unb and not unb & set(m.bounded_cells())
+    i = m.bounded_cells()[0]
+    for j in m.neighbors(i):
+        assert len(m.face_vertices(i, j)) >= 2
+    # dict-constructed mesh (reference constructor shape) round-trips to arrays
+    m2 = vb.Mesh(ns, dict(m.vertices), dict(m.edge_counts), list(m.boundary))
+    assert m2.arrays()["sigma"].shape == sig.shape
