@@ -100,6 +100,37 @@ int vr_raycast_batch(const double* rec, int64_t n_gen, int d, double sqmax,
                      uint8_t* out_flag, int32_t* recheck_list,
                      int32_t* recheck_count, void* stream);
 
+/* ---- Exact candidate pruning ---------------------
+ * Generators reordered by a balanced kd partition into tiles of
+ * VR_PRUNE_TILE records (padded with sentinels), each tile with an
+ * axis-aligned bounding box, tiles grouped in blocks of VR_PRUNE_BLOCK tiles
+ * with their own boxes.  A warp of spatially coherent rays skips a block /
+ * tile only when, for every one of its rays, the box lies behind the ray's
+ * forward halfspace or outside its current candidate sphere plus the
+ * degeneracy/rounding band -- a certificate that no skipped generator could
+ * change the result, so the output equals vr_raycast_batch's. */
+#define VR_PRUNE_TILE 64
+#define VR_PRUNE_BLOCK 32
+typedef struct vr_prune_index {
+  const double* rec;       /* kd-ordered records, vr_record_rows(n) rows       */
+  const int32_t* perm;     /* kd position -> generator index (n)               */
+  const int32_t* inv_perm; /* generator index -> kd position (n)               */
+  const double* tile_box;  /* ceil(n/64) x 2d, [lo_0..lo_{d-1}, hi_0..]        */
+  const double* block_box; /* ceil(ceil(n/64)/32) x 2d                         */
+  int64_t n;
+} vr_prune_index;
+
+/* vr_raycast_batch through the pruned index.  `order` (nullable, n_rays
+ * int32) is the processing order: slot k handles ray order[k]; callers sort
+ * rays by the kd position of eta[0] so that a warp's rays are spatially
+ * coherent.  Outputs are written at the ray's own index. */
+int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
+                      const vr_prune_index* ix, const double* x, const double* u,
+                      const int32_t* eta, int eta_len, int64_t n_rays,
+                      const int32_t* order, int32_t* out_idx, double* out_t,
+                      double* out_rp, uint8_t* out_flag, int32_t* recheck_list,
+                      int32_t* recheck_count, void* stream);
+
 /* Exact re-evaluation of the rays listed in recheck_list[0 .. *count)
  * (count read on device): centred t for every candidate, argmin with the
  * smallest-index tie-break, then the reference's runner-up degeneracy band
@@ -173,6 +204,14 @@ int vr_mc_rays(const double* rec, int64_t n_gen, int d, double sqmax,
                const double* dirs, uint64_t seed,
                int32_t* out_idx, double* out_t, uint8_t* out_flag,
                int32_t* recheck_list, int32_t* recheck_count, void* stream);
+
+/* vr_mc_rays through the pruned index (rays of one cell are coherent). */
+int vr_mc_rays_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
+                      const vr_prune_index* ix, const int32_t* cells,
+                      int64_t n_cells, int64_t rays_per_cell, const double* dirs,
+                      uint64_t seed, int32_t* out_idx, double* out_t,
+                      uint8_t* out_flag, int32_t* recheck_list,
+                      int32_t* recheck_count, void* stream);
 
 int vr_mc_recheck(const double* rec, int64_t n_gen, int d,
                   const double* cand_rec, const int32_t* cand, int64_t n_cand,

@@ -14,6 +14,7 @@ coordinate / edge / boundary arrays and the reference's dict views
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 from itertools import combinations
 
@@ -69,6 +70,7 @@ class NodeSet:
             raise ValueError(f"unknown backend {backend!r}")
         self.backend = backend
         self._dev = {}
+        self._prune = {}
 
     def __len__(self):
         return self.n
@@ -98,6 +100,18 @@ class NodeSet:
             entry = (rec, float(sqmax.item()))
         self._dev[dev.index] = entry
         return entry
+
+    def prune_index(self, device=None):
+        """kd-ordered records + tile / block bounding boxes for the pruned
+        RayCast (include/voronray_b200.h vr_prune_index); built once per
+        device on the GPU."""
+        dev = _device(device)
+        hit = self._prune.get(dev.index)
+        if hit is None:
+            rec, _ = self.device_records(dev)
+            hit = PruneIndex(rec, self.n, self.dim)
+            self._prune[dev.index] = hit
+        return hit
 
     # -- filtered nearest neighbour (core.py:62-142) -------------------------
     def _skip_mask(self, skip):
@@ -136,6 +150,93 @@ class NodeSet:
         if idx[0] < 0:
             return None
         return (int(idx[0]), float(d1[0])), float(d2[0])
+
+
+PRUNE_TILE, PRUNE_BLOCK = 64, 32
+
+
+class _PruneStruct(ctypes.Structure):
+    _fields_ = [("rec", ctypes.c_void_p), ("perm", ctypes.c_void_p),
+                ("inv_perm", ctypes.c_void_p), ("tile_box", ctypes.c_void_p),
+                ("block_box", ctypes.c_void_p), ("n", ctypes.c_int64)]
+
+
+def kd_order(P, tile=PRUNE_TILE):
+    """Balanced kd partition on the device: returns the permutation (int64)
+    placing generators so that every leaf occupies whole tiles of `tile`
+    rows (only the last tile is partial).  Each split sorts a segment along
+    its widest extent and cuts after floor(tiles/2) full tiles."""
+    n, d = P.shape
+    dev = P.device
+    order = torch.arange(n, device=dev)
+    seg_start = torch.zeros(1, dtype=torch.int64, device=dev)
+    seg_len = torch.full((1,), n, dtype=torch.int64, device=dev)
+    seg_of = torch.zeros(n, dtype=torch.int64, device=dev)
+    pos = torch.arange(n, device=dev)
+    inf = float("inf")
+    while True:
+        split = seg_len > tile
+        if not bool(split.any()):
+            break
+        X = P[order]
+        nseg = seg_start.numel()
+        idx = seg_of[:, None].expand(n, d)
+        mn = torch.full((nseg, d), inf, dtype=P.dtype, device=dev).scatter_reduce(
+            0, idx, X, "amin", include_self=True)
+        mx = torch.full((nseg, d), -inf, dtype=P.dtype, device=dev).scatter_reduce(
+            0, idx, X, "amax", include_self=True)
+        dim = (mx - mn).argmax(1)
+        key = X.gather(1, dim[seg_of][:, None]).squeeze(1)
+        key = torch.where(split[seg_of], key, torch.zeros_like(key))
+        o1 = torch.sort(key, stable=True).indices
+        o2 = torch.sort(seg_of[o1], stable=True).indices
+        order = order[o1[o2]]
+        nt = (seg_len + tile - 1) // tile
+        left = torch.where(split, (nt // 2) * tile, seg_len)
+        rel = pos - seg_start[seg_of]
+        is_right = split[seg_of] & (rel >= left[seg_of])
+        # children ids: left = 2s, right = 2s+1, compacted to existing ones
+        exists = torch.stack([torch.ones_like(split), split], 1).reshape(-1)
+        new_id = torch.cumsum(exists.to(torch.int64), 0) - 1
+        seg_of = new_id[2 * seg_of + is_right.to(torch.int64)]
+        starts = torch.stack([seg_start, seg_start + left], 1).reshape(-1)
+        lens = torch.stack([left, seg_len - left], 1).reshape(-1)
+        seg_start, seg_len = starts[exists], lens[exists]
+    return order
+
+
+class PruneIndex:
+    """Device tensors of one vr_prune_index."""
+
+    def __init__(self, rec, n, d):
+        dev = rec.device
+        pts = rec[:n, :d]
+        perm = kd_order(pts)
+        rows = rec.shape[0]
+        crec = torch.zeros_like(rec)
+        crec[:, d] = float("inf")
+        crec[:n] = rec[perm]
+        self.perm = perm.to(torch.int32).contiguous()
+        inv = torch.empty(n, dtype=torch.int64, device=dev)
+        inv[perm] = torch.arange(n, device=dev)
+        self.inv_perm = inv.to(torch.int32).contiguous()
+        nt = (n + PRUNE_TILE - 1) // PRUNE_TILE
+        X = crec[:nt * PRUNE_TILE, :d].view(nt, PRUNE_TILE, d)
+        valid = (torch.arange(nt * PRUNE_TILE, device=dev) < n).view(nt, PRUNE_TILE, 1)
+        lo = torch.where(valid, X, torch.full_like(X, float("inf"))).amin(1)
+        hi = torch.where(valid, X, torch.full_like(X, float("-inf"))).amax(1)
+        self.tile_box = torch.cat([lo, hi], 1).contiguous()
+        nb = (nt + PRUNE_BLOCK - 1) // PRUNE_BLOCK
+        pad = nb * PRUNE_BLOCK - nt
+        blo = torch.cat([lo, lo[-1:].expand(pad, d)]).view(nb, PRUNE_BLOCK, d).amin(1)
+        bhi = torch.cat([hi, hi[-1:].expand(pad, d)]).view(nb, PRUNE_BLOCK, d).amax(1)
+        self.block_box = torch.cat([blo, bhi], 1).contiguous()
+        self.rec = crec
+        self.n = n
+        self.rows = rows
+        p = lambda t: t.data_ptr()  # noqa: E731
+        self.struct = _PruneStruct(p(crec), p(self.perm), p(self.inv_perm), p(self.tile_box),
+                                   p(self.block_box), n)
 
 
 def build_node_set(points, backend="auto"):

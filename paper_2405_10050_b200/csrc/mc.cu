@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(RED_NT)
         const bool bad = fl == VR_RAY_ESCAPED || (fl == VR_RAY_DEGENERATE && degenerate_is_error);
         if (bad) {
           atomicMin(&first_bad, ((unsigned long long)r << 2) | (fl == VR_RAY_ESCAPED ? 1ull : 2ull));
+          if (out_samples) out_samples[k] = CUDART_NAN;
         } else {
           const int32_t j = ray_idx[k];
           const double t = ray_t[k];
@@ -232,4 +233,22 @@ extern "C" int vr_mc_directions(int d, int64_t n_cells, const int32_t* cells,
     k_mc_dirs<D><<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(src, out_z);
   });
   VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_mc_rays_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
+                                 const vr_prune_index* ix, const int32_t* cells, int64_t n_cells,
+                                 int64_t rays_per_cell, const double* dirs, uint64_t seed,
+                                 int32_t* out_idx, double* out_t, uint8_t* out_flag,
+                                 int32_t* recheck_list, int32_t* recheck_count, void* stream) {
+  if (!rec || !ix || !ix->rec || !cells || !out_idx || !out_t || !out_flag || rays_per_cell <= 0 ||
+      ix->n != n_gen)
+    return VR_EINVAL;
+  const int64_t n = n_cells * rays_per_cell;
+  RayOut out{out_idx, out_t, nullptr, out_flag, recheck_list, recheck_count};
+  PrunedIndex pi{ix->rec, ix->perm, ix->inv_perm, ix->tile_box, ix->block_box, ix->n};
+  VR_DISPATCH_D(d, {
+    SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n};
+    return launch_raycast_pruned<D>(src, n, pi, sqmax, out, as_stream(stream));
+  });
+  return VR_OK;
 }

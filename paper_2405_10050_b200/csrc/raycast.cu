@@ -69,3 +69,23 @@ extern "C" int vr_raycast_recheck(const double* rec, int64_t n_gen, int d, const
   });
   return VR_OK;
 }
+
+extern "C" int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
+                                 const vr_prune_index* ix, const double* x, const double* u,
+                                 const int32_t* eta, int eta_len, int64_t n_rays,
+                                 const int32_t* order, int32_t* out_idx, double* out_t,
+                                 double* out_rp, uint8_t* out_flag, int32_t* recheck_list,
+                                 int32_t* recheck_count, void* stream) {
+  if (!rec || !ix || !ix->rec || !ix->perm || !ix->inv_perm || !ix->tile_box || !ix->block_box ||
+      !x || !u || !eta || !out_idx || !out_t || !out_flag)
+    return VR_EINVAL;
+  if (eta_len < 1 || eta_len > d || ix->n != n_gen) return VR_EINVAL;
+  if ((recheck_list == nullptr) != (recheck_count == nullptr)) return VR_EINVAL;
+  RayOut out{out_idx, out_t, out_rp, out_flag, recheck_list, recheck_count};
+  PrunedIndex pi{ix->rec, ix->perm, ix->inv_perm, ix->tile_box, ix->block_box, ix->n};
+  VR_DISPATCH_D(d, {
+    SrcExplicit<D> src{x, u, eta, eta_len, rec, n_rays, order};
+    return launch_raycast_pruned<D>(src, n_rays, pi, sqmax, out, as_stream(stream));
+  });
+  return VR_OK;
+}

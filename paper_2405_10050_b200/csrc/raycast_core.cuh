@@ -41,6 +41,7 @@ struct RayState {
   double bu;    // u . (x - x_g)
   double tb;    // current best t
   double denb;  // u.(x_best - x_g) of the current best
+  double rho2;  // radius^2 of the current sphere (+inf before the first hit)
   int ib;       // current best (local candidate index), -1 = none
   int near;     // 1 -> needs exact re-check
 };
@@ -81,6 +82,7 @@ __device__ __forceinline__ void ray_setup(RayState<D>& r, const double* __restri
   r.dlt = 0.0;
   r.tb = CUDART_INF;
   r.denb = 0.0;
+  r.rho2 = CUDART_INF;
   r.ib = -1;
   r.near = 0;
 }
@@ -110,6 +112,7 @@ __device__ __forceinline__ void ray_set_best(RayState<D>& r, double t, double de
   r.hi = r.lim + dlt;
   r.tb = t;
   r.denb = den;
+  r.rho2 = rho2;
   r.ib = i;
 }
 
@@ -157,6 +160,18 @@ __device__ __forceinline__ void load_rec(const double* p, double (&xi)[D]) {
   if (D & 1) xi[D - 1] = p[D - 1];
 }
 
+template <int D>
+__device__ __forceinline__ void load_rec_g(const double* p, double (&xi)[D]) {
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int k = 0; k < D / 2; ++k) {
+    const double2 v = __ldg(p2 + k);
+    xi[2 * k] = v.x;
+    xi[2 * k + 1] = v.y;
+  }
+  if (D & 1) xi[D - 1] = __ldg(p + D - 1);
+}
+
 // Screening value of one pair: |x_i|^2 - 2 z.x_i as one chain of d FMAs
 // (z is stored pre-scaled by -2), so a pair costs d DFMA + 1 DSETP.
 template <int D>
@@ -180,8 +195,12 @@ struct SrcExplicit {
   int eta_len;
   const double* grec;
   int64_t n;
+  const int32_t* order = nullptr;  // optional processing order (slot -> ray id)
+  __device__ __forceinline__ int64_t id(int64_t k) const { return order ? order[k] : k; }
+  __device__ __forceinline__ int32_t gen(int64_t k) const { return eta[id(k) * eta_len]; }
   __device__ __forceinline__ bool load(int64_t k, RayState<D>& r) const {
     if (k >= n) return false;
+    k = id(k);
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       r.x[j] = x[k * D + j];
@@ -262,6 +281,8 @@ struct SrcMC {
     }
     normalise<D>(z, y);
   }
+  __device__ __forceinline__ int64_t id(int64_t k) const { return k; }
+  __device__ __forceinline__ int32_t gen(int64_t k) const { return cells[k / per]; }
   __device__ __forceinline__ bool load(int64_t k, RayState<D>& r) const {
     if (k >= n) return false;
     const int32_t cell = cells[k / per];
@@ -421,7 +442,125 @@ __global__ void __launch_bounds__(NT, MINB)
 
 #pragma unroll
   for (int j = 0; j < R; ++j)
-    if (act[j]) ray_store<D>(ray[j], k0 + (int64_t)j * NT, cand, out);
+    if (act[j]) ray_store<D>(ray[j], src.id(k0 + (int64_t)j * NT), cand, out);
+}
+
+// ---------------------------------------------------------------------------
+// Pruned RayCast: generators in kd-order, grouped in
+// tiles of PT records with axis-aligned bounding boxes, tiles grouped in
+// blocks of PB tiles with their own boxes.  A warp (32 lanes x R rays,
+// spatially coherent) skips a block / tile when for EVERY ray of the warp the
+// box is either entirely behind the ray's halfspace or certifiably outside
+// its current sphere plus band -- such a tile holds no candidate that could
+// improve the ray or fall in its degeneracy band, now or for any later
+// (smaller) sphere.  Everything not skipped goes through exactly the same
+// screening / rare path as the exhaustive kernel, so results are identical.
+// ---------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ bool ray_needs_box(const RayState<D>& r, const double* __restrict__ box) {
+  // box = [lo_0..lo_{D-1}, hi_0..hi_{D-1}]
+  double umax = 0.0, d2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const double lo = __ldg(box + k), hi = __ldg(box + D + k);
+    umax = fma(r.u[k], r.u[k] > 0.0 ? hi : lo, umax);
+    const double zc = -0.5 * r.z[k];
+    const double e = fmax(fmax(lo - zc, zc - hi), 0.0);
+    d2 = fma(e, e, d2);
+  }
+  // every candidate of the box is behind the forward halfspace
+  if (umax + 1e-13 * (fabs(umax) + 1.0) <= r.thr) return false;
+  if (r.ib < 0) return true;  // no sphere yet
+  // power of any box point w.r.t. the sphere >= d2 - rho2
+  return d2 < r.rho2 + r.dlt + 1e-12 * (r.rho2 + d2);
+}
+
+template <int D, int R, int PT, int PB, int NT, int MINB, class Src>
+__global__ void __launch_bounds__(NT, MINB)
+    k_raycast_pruned(Src src, const double* __restrict__ crec, const int32_t* __restrict__ perm,
+                     const int32_t* __restrict__ inv_perm, int64_t n_cand,
+                     const double* __restrict__ tile_box, const double* __restrict__ block_box,
+                     double sqmax, RayOut out) {
+  constexpr int S = rec_stride(D);
+  constexpr int U = 8;
+  static_assert(PT % U == 0 && VR_REC_PAD % PT == 0, "tile must divide the record padding");
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)NT + threadIdx.x) >> 5;
+  const int64_t ntiles = (n_cand + PT - 1) / PT;
+  const int64_t nblocks = (ntiles + PB - 1) / PB;
+
+  RayState<D> ray[R];
+  bool act[R];
+  const int64_t k0 = warp * 32 * R + lane;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    act[j] = src.load(k0 + (int64_t)j * 32, ray[j]);
+    if (!act[j]) {
+      ray[j].hi = -CUDART_INF;
+      ray[j].thr = CUDART_INF;  // never needs a box
+#pragma unroll
+      for (int k = 0; k < D; ++k) ray[j].z[k] = 0.0;
+    }
+  }
+  if (!__any_sync(0xffffffffu, act[0])) return;
+  // start where lane 0's first ray lives in kd-order
+  int64_t st = 0;
+  if (lane == 0) st = inv_perm[src.gen(k0)] / PT;
+  st = __shfl_sync(0xffffffffu, st, 0);
+  const int64_t sb = st / PB;
+
+  for (int64_t bi = 0; bi < nblocks; ++bi) {
+    const int64_t b = (sb + bi) % nblocks;
+    bool need = false;
+#pragma unroll
+    for (int j = 0; j < R; ++j) need |= ray_needs_box<D>(ray[j], block_box + b * 2 * D);
+    if (!__any_sync(0xffffffffu, need)) continue;
+    const int64_t t_lo = b * PB, t_hi = min(ntiles, t_lo + PB);
+    const int64_t tstart = (b == sb) ? st : t_lo;
+    for (int64_t ti = 0; ti < t_hi - t_lo; ++ti) {
+      int64_t t = tstart + ti;
+      if (t >= t_hi) t -= (t_hi - t_lo);
+      bool tneed = false;
+#pragma unroll
+      for (int j = 0; j < R; ++j) tneed |= ray_needs_box<D>(ray[j], tile_box + t * 2 * D);
+      if (!__any_sync(0xffffffffu, tneed)) continue;
+      const double* tile = crec + t * PT * S;
+      const int gbase = (int)(t * PT);
+      for (int c = 0; c < PT; c += U) {
+        unsigned m[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) m[j] = 0u;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          double xi[D];
+          load_rec_g<D>(tile + (c + u) * S, xi);
+          const double sq = __ldg(tile + (c + u) * S + D);
+#pragma unroll
+          for (int j = 0; j < R; ++j)
+            m[j] |= (ray_power<D>(ray[j], xi, sq) < ray[j].hi) ? (1u << u) : 0u;
+        }
+        unsigned any = 0u;
+#pragma unroll
+        for (int j = 0; j < R; ++j) any |= m[j];
+        if (__any_sync(0xffffffffu, any != 0u)) {
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            unsigned mm = m[j];
+            while (mm) {
+              const int u = __ffs(mm) - 1;
+              mm &= mm - 1;
+              double xi[D];
+              load_rec_g<D>(tile + (c + u) * S, xi);
+              ray_rare<D>(ray[j], xi, __ldg(tile + (c + u) * S + D), gbase + c + u, sqmax);
+            }
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+    if (act[j]) ray_store<D>(ray[j], src.id(k0 + (int64_t)j * 32), perm, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -574,6 +713,37 @@ int launch_raycast(const Src& src, int64_t n_rays, const double* crec, const int
     }
   }
   return launch_raycast_cfg<RaycastCfg<D>, D>(src, n_rays, crec, cand, n_cand, sqmax, out, st);
+}
+
+struct PrunedIndex {
+  const double* crec;      // records in kd-order (padded)
+  const int32_t* perm;     // kd position -> generator index
+  const int32_t* inv_perm; // generator index -> kd position
+  const double* tile_box;  // ntiles x 2D
+  const double* block_box; // nblocks x 2D
+  int64_t n;
+};
+
+constexpr int PRUNE_TILE = 64;
+constexpr int PRUNE_BLOCK = 32;
+
+template <int D, class Src>
+int launch_raycast_pruned(const Src& src, int64_t n_rays, const PrunedIndex& ix, double sqmax,
+                          const RayOut& out, cudaStream_t st) {
+  if (n_rays <= 0) return VR_OK;
+  if (ix.n <= 0) return VR_EINVAL;
+  if (out.recheck_count) {
+    cudaError_t e = cudaMemsetAsync(out.recheck_count, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return vr_cuda_status(e);
+  }
+  constexpr int NT = 128;
+  constexpr int R = (D <= 3) ? 4 : 2;
+  constexpr int MINB = (D <= 3 || D >= 7) ? 2 : 3;
+  const int64_t per_block = (int64_t)NT * R;
+  const int64_t grid = (n_rays + per_block - 1) / per_block;
+  k_raycast_pruned<D, R, PRUNE_TILE, PRUNE_BLOCK, NT, MINB, Src><<<(unsigned)grid, NT, 0, st>>>(
+      src, ix.crec, ix.perm, ix.inv_perm, ix.n, ix.tile_box, ix.block_box, sqmax, out);
+  VR_RETURN_LAUNCH();
 }
 
 template <int D, class Src>

@@ -18,6 +18,7 @@ Two direction sources:
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field
 from typing import Callable
@@ -28,7 +29,7 @@ import torch
 from . import _lib
 from .core import NodeSet
 from .errors import DegenerateConfiguration, UnboundedRay
-from .raycast import RaycastStats, Workspace, candidate_records
+from .raycast import RaycastStats, Workspace, _use_pruned, candidate_records
 
 Integrand = Callable[[np.ndarray], float]
 
@@ -83,7 +84,8 @@ class MCResult:
 
 
 def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_faces=256,
-               degenerate_is_error=True, want_samples=False, workspace=None, stats=None):
+               degenerate_is_error=True, want_samples=False, workspace=None, stats=None,
+               mode="auto"):
     """Run rays + recheck + reduce for len(cells) cells x n rays; device tensors out."""
     rec, sqmax = ns.device_records()
     dev = rec.device
@@ -111,10 +113,17 @@ def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_fa
     rc = ws.get("mc_rc", (1,), torch.int32, dev)
     sh = _lib.stream_handle()
     seed = int(seed) & 0xFFFFFFFFFFFFFFFF
-    _lib.check(L.vr_mc_rays(_lib.ptr(rec), ns.n, d, sqmax, _lib.ptr(crec), _lib.ptr(cand), n_cand,
-                            _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed, _lib.ptr(idx),
-                            _lib.ptr(t), _lib.ptr(flag), _lib.ptr(rl), _lib.ptr(rc), sh),
-               "vr_mc_rays")
+    if _use_pruned(ns, candidates, mode):
+        ix = ns.prune_index(dev)
+        _lib.check(L.vr_mc_rays_pruned(_lib.ptr(rec), ns.n, d, sqmax, ctypes.byref(ix.struct),
+                                       _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed,
+                                       _lib.ptr(idx), _lib.ptr(t), _lib.ptr(flag), _lib.ptr(rl),
+                                       _lib.ptr(rc), sh), "vr_mc_rays_pruned")
+    else:
+        _lib.check(L.vr_mc_rays(_lib.ptr(rec), ns.n, d, sqmax, _lib.ptr(crec), _lib.ptr(cand),
+                                n_cand, _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed,
+                                _lib.ptr(idx), _lib.ptr(t), _lib.ptr(flag), _lib.ptr(rl),
+                                _lib.ptr(rc), sh), "vr_mc_rays")
     _lib.check(L.vr_mc_recheck(_lib.ptr(rec), ns.n, d, _lib.ptr(crec), _lib.ptr(cand), n_cand,
                                _lib.ptr(cells_d), n, _lib.ptr(dd), seed, _lib.ptr(rl),
                                _lib.ptr(rc), total, _lib.ptr(idx), _lib.ptr(t), _lib.ptr(flag),
@@ -152,7 +161,8 @@ def _collect(cells, out, want_samples):
 
 
 def mc_cells(ns: NodeSet, cells, n: int, seed: int = 0, max_faces: int = 256,
-             want_samples=False, stats: RaycastStats = None, chunk_rays: int = 1 << 26):
+             want_samples=False, stats: RaycastStats = None, chunk_rays: int = 1 << 26,
+             mode="auto"):
     """Batched device MC (Philox directions) over many cells.
 
     Returns an :class:`MCResult`; cells whose status is not CELL_OK are the
@@ -170,7 +180,7 @@ def mc_cells(ns: NodeSet, cells, n: int, seed: int = 0, max_faces: int = 256,
     for lo in range(0, len(cells), per_chunk):
         sub = cells[lo:lo + per_chunk]
         out = _mc_device(ns, sub, n, seed=seed, max_faces=max_faces, want_samples=want_samples,
-                         workspace=ws, stats=stats)
+                         workspace=ws, stats=stats, mode=mode)
         parts.append(_collect(sub, out, want_samples))
     if len(parts) == 1:
         return parts[0]

@@ -15,6 +15,7 @@ reference semantics (raycast.py:49-82, 295-378); they are not on the hot path.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -127,8 +128,20 @@ def candidate_records(ns: NodeSet, candidates, dev):
     return cand.to(torch.int32).contiguous(), crec
 
 
+PRUNE_MIN_GENERATORS = 1024
+
+
+def _use_pruned(ns, candidates, mode):
+    if mode not in ("auto", "pruned", "exhaustive"):
+        raise ValueError(f"unknown mode {mode!r}")
+    if candidates is not None or mode == "exhaustive":
+        return False
+    return mode == "pruned" or ns.n >= PRUNE_MIN_GENERATORS
+
+
 def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=None,
-                  workspace=None, out=None, stream=None, events=None) -> RaycastBatch:
+                  workspace=None, out=None, stream=None, events=None,
+                  mode="auto") -> RaycastBatch:
     """Batched incircle RayCast on the current CUDA device.
 
     Args:
@@ -142,6 +155,9 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
         out: optional dict of preallocated output tensors (idx, t, rp, flag).
         events: optional three CUDA events recorded before the fused kernel,
             between it and the re-check pass, and after (kernel timing).
+        mode: "exhaustive" scans every generator (TMA-staged tiles);
+            "pruned" skips kd tiles with a certificate (identical results);
+            "auto" prunes when N >= 1024 and no candidate subset is given.
 
     Stream-ordered; no host synchronisation.
     """
@@ -183,12 +199,27 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
     rl = ws.get("recheck_list", (n,), torch.int32, dev)
     rc = ws.get("recheck_count", (1,), torch.int32, dev)
     sh = _lib.stream_handle(stream)
+    pruned = _use_pruned(ns, candidates, mode)
     if events is not None:
         events[0].record(stream)
-    _lib.check(L.vr_raycast_batch(_lib.ptr(rec), ns.n, d, sqmax, _lib.ptr(crec), _lib.ptr(cand),
-                                  n_cand, _lib.ptr(xd), _lib.ptr(ud), _lib.ptr(ed), k, n,
-                                  _lib.ptr(idx), _lib.ptr(t), _lib.ptr(rp), _lib.ptr(flag),
-                                  _lib.ptr(rl), _lib.ptr(rc), sh), "vr_raycast_batch")
+    if pruned:
+        ix = ns.prune_index(dev)
+        cur = torch.cuda.current_stream() if stream is None else stream
+        with torch.cuda.stream(cur):
+            # warp-coherent processing order: rays sorted by the kd position of eta[0]
+            key = ix.inv_perm.index_select(0, ed[:, 0].to(torch.int64))
+            order = torch.sort(key, stable=True).indices.to(torch.int32)
+        _lib.check(L.vr_raycast_pruned(_lib.ptr(rec), ns.n, d, sqmax, ctypes.byref(ix.struct),
+                                       _lib.ptr(xd), _lib.ptr(ud), _lib.ptr(ed), k, n,
+                                       _lib.ptr(order), _lib.ptr(idx), _lib.ptr(t),
+                                       _lib.ptr(rp), _lib.ptr(flag), _lib.ptr(rl), _lib.ptr(rc),
+                                       sh), "vr_raycast_pruned")
+    else:
+        _lib.check(L.vr_raycast_batch(_lib.ptr(rec), ns.n, d, sqmax, _lib.ptr(crec),
+                                      _lib.ptr(cand), n_cand, _lib.ptr(xd), _lib.ptr(ud),
+                                      _lib.ptr(ed), k, n, _lib.ptr(idx), _lib.ptr(t),
+                                      _lib.ptr(rp), _lib.ptr(flag), _lib.ptr(rl), _lib.ptr(rc),
+                                      sh), "vr_raycast_batch")
     if events is not None:
         events[1].record(stream)
     _lib.check(L.vr_raycast_recheck(_lib.ptr(rec), ns.n, d, _lib.ptr(crec), _lib.ptr(cand),
@@ -228,7 +259,7 @@ class HostRaycaster:
     def pinned(shape, dtype):
         return torch.empty(shape, dtype=dtype, pin_memory=True)
 
-    def run(self, hx, hu, heta, hidx, ht, hrp, hflag, stats=None):
+    def run(self, hx, hu, heta, hidx, ht, hrp, hflag, stats=None, mode="auto"):
         """hx, hu (n, d) f64, heta (n, k) i32 pinned inputs; outputs pinned
         hidx (n,) i32, ht (n,) f64, hrp (n, d) f64, hflag (n,) u8.  Returns
         after the last D2H copy has completed."""
@@ -251,7 +282,7 @@ class HostRaycaster:
                               out=dict(idx=b["idx"][:m], t=b["t"][:m], rp=b["rp"][:m],
                                        flag=b["flag"][:m]),
                               workspace=self.ws[ci & 1], stats=stats,
-                              stream=self.comp_stream)
+                              stream=self.comp_stream, mode=mode)
                 b["done"].record(self.comp_stream)
             with torch.cuda.stream(self.copy_stream):
                 self.copy_stream.wait_event(b["done"])

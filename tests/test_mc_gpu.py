@@ -129,3 +129,32 @@ def test_batched_cells_status_unbounded():
     for m, c in enumerate(ok):
         areas, vol, _ = orc.mc_areas(nodes, int(c), 200, orc.Replay(z[m * 200:(m + 1) * 200]))
         assert _close(float(res.volume[c]), vol)
+
+
+def test_mc_pruned_equals_exhaustive():
+    pts = np.random.default_rng(0).random((100000, 4))
+    ns = vb.NodeSet(pts)
+    cells = np.random.default_rng(9).choice(100000, 300, replace=False)
+    a = vb.mc_cells(ns, cells, 500, seed=3, mode="exhaustive", want_samples=True)
+    b = vb.mc_cells(ns, cells, 500, seed=3, mode="pruned", want_samples=True)
+    for f in ("volume", "face_offsets", "face_j", "face_area", "status", "first_bad", "samples"):
+        assert np.array_equal(getattr(a, f), getattr(b, f), equal_nan=True), f
+
+
+def test_config4_subset_vs_exact_volumes():
+    """SURVEY §8(c) rule 5: >= 95% of the 2,000 central cells within 4 SE of
+    the exact (Leibniz, reference integrate_cell_poly) volume."""
+    gz = golden("config4_exact.npz")
+    pts = np.random.default_rng(0).random((100000, 4))
+    ns = vb.NodeSet(pts)
+    cells = gz["cells"]
+    res = vb.mc_cells(ns, cells, 1000, seed=0, want_samples=True)
+    assert (res.status == 0).all()
+    surf = vb.sphere_surface_area(4)
+    smp = res.samples.reshape(len(cells), 1000)
+    se = surf * smp.std(axis=1, ddof=1) / (4 * np.sqrt(1000))
+    dev = np.abs(res.volume - gz["volume"])
+    frac = float(np.mean(dev <= 4 * se))
+    assert frac >= 0.95, frac
+    # unbiased in aggregate
+    assert abs(np.mean((res.volume - gz["volume"]) / se)) < 0.2

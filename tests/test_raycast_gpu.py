@@ -198,3 +198,30 @@ def test_nearest_and_verify():
     assert vb.nearest_neighbor(ns, q, skip=lambda i: True) is None
     tie = vb.NodeSet([(1.0, 0.0), (-1.0, 0.0), (0.0, 3.0)])
     assert tie.nearest(np.zeros(2))[0] == 0
+
+
+@pytest.mark.parametrize("d", [2, 3, 4, 5, 6, 7, 8])
+def test_pruned_equals_exhaustive(d):
+    """The kd-tile pruning certificate never changes a result (bitwise)."""
+    rng = np.random.default_rng(300 + d)
+    n = 20000 if d <= 6 else 50000
+    pts = rng.random((n, d)) if d % 2 else rng.standard_normal((n, d))
+    ns = vb.build_node_set(pts)
+    m = 20000
+    g = rng.integers(0, n, m)
+    u = rng.standard_normal((m, d))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    a = vb.raycast_batch(ns, pts[g], u, g[:, None], mode="exhaustive").to_host()
+    b = vb.raycast_batch(ns, pts[g], u, g[:, None], mode="pruned").to_host()
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y, equal_nan=True)
+    # edge rays with |eta| = d from descent vertices
+    sig, r = vb.descent_batch(ns, rng.choice(n, 200, replace=False), seed=1)
+    uu, ok = vb.vertex_directions_batch(ns, sig)
+    uu = uu.cpu().numpy().reshape(-1, d)
+    xs = np.repeat(r, d + 1, axis=0)
+    eta = np.array([[s[j] for j in range(d + 1) if j != k] for s in sig for k in range(d + 1)])
+    a = vb.raycast_batch(ns, xs, uu, eta, mode="exhaustive").to_host()
+    b = vb.raycast_batch(ns, xs, uu, eta, mode="pruned").to_host()
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y, equal_nan=True)
