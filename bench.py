@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--rays", type=int, default=RAYS_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rays-per-core", type=int, default=3000)
+    ap.add_argument("--mode", choices=["pruned", "exhaustive"], default="pruned")
     return ap.parse_args()
 
 
@@ -238,10 +239,13 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)]
           for _ in range(args.warmup + args.steps)]
+    work = torch.zeros(1, dtype=torch.int64, device=dev)
+    ns.prune_index()  # kd index built once per NodeSet, outside the timing
 
-    def step(i):
+    def step(i, mode=args.mode, events=None):
         flush.fill_(i & 0xFF)  # L2 flush, outside the timed events
-        vb.raycast_batch(ns, xd, ud, gd, out=out, workspace=ws, events=ev[i])
+        vb.raycast_batch(ns, xd, ud, gd, out=out, workspace=ws, events=events or ev[i],
+                         mode=mode, work=work if mode == "pruned" else None)
 
     for i in range(args.warmup):
         step(i)
@@ -256,6 +260,13 @@ def run_ours(args):
         dist.barrier()
     step_ms = [ev[i][0].elapsed_time(ev[i][2]) for i in range(args.warmup, args.warmup + args.steps)]
     kern_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(args.warmup, args.warmup + args.steps)]
+    screened = int(work.item()) / (args.warmup + args.steps) if args.mode == "pruned" else None
+    # the exhaustive (TMA-staged, unpruned) kernel on the same rays, for its roofline
+    ex_ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    step(0, mode="exhaustive")
+    step(1, mode="exhaustive", events=ex_ev)
+    torch.cuda.synchronize()
+    ex_ms = ex_ev[0].elapsed_time(ex_ev[1])
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -279,7 +290,7 @@ def run_ours(args):
     hrp = HostRaycaster.pinned((n, DIM), torch.float64)
     hfl = HostRaycaster.pinned((n,), torch.uint8)
     for _ in range(max(1, args.warmup)):
-        hr.run(hx, hu, hg, hidx, ht, hrp, hfl)
+        hr.run(hx, hu, hg, hidx, ht, hrp, hfl, mode=args.mode)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -288,7 +299,7 @@ def run_ours(args):
         flush.fill_(1)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        hr.run(hx, hu, hg, hidx, ht, hrp, hfl)
+        hr.run(hx, hu, hg, hidx, ht, hrp, hfl, mode=args.mode)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -302,8 +313,9 @@ def run_ours(args):
     if rank == 0:
         peak = fp64_peak(torch, L, _lib)
         kms = float(np.mean(kern_ms))
-        pairs = n * N_GEN
+        pairs = screened if screened is not None else n * N_GEN
         achieved = pairs * FLOP_PER_PAIR / (kms * 1e-3) / 1e12
+        ex_achieved = n * N_GEN * FLOP_PER_PAIR / (ex_ms * 1e-3) / 1e12
         result = {
             "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -316,13 +328,20 @@ def run_ours(args):
                        "l2": "flushed between timed steps (256 MB write, untimed)"},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                         "kernel": "k_raycast<6,3,128,128,4>", "kernel_ms": kms,
-                         "flop_per_pair": FLOP_PER_PAIR,
+                         "kernel": ("k_raycast_pruned<6,2,64,32,10>" if args.mode == "pruned"
+                                    else "k_raycast<6,2,128,256,4,3>"),
+                         "kernel_ms": kms, "flop_per_pair": FLOP_PER_PAIR,
+                         "pairs_per_launch": pairs, "pairs_per_ray": pairs / n,
                          "peak_source": "measured live: DFMA probe (vr_fma_probe), "
                                         "MEASURED_PEAKS.json has no FP64 figure"},
+            "roofline_exhaustive": {"bound": "fp64", "kernel": "k_raycast<6,2,128,256,4,3>",
+                                    "kernel_ms": ex_ms, "achieved": ex_achieved, "peak": peak,
+                                    "unit": "TFLOP/s", "frac": ex_achieved / peak,
+                                    "pairs_per_launch": n * N_GEN,
+                                    "rays_per_s": n / (ex_ms * 1e-3)},
             "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "HostRaycaster.run (pinned host arrays)"},
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": 2 * args.steps,  # fused RayCast + exact re-check per step
             "clocks": clk.summary(),
             "checks": {"escaped": n_esc, "degenerate": n_deg, "pool_build_s": t_pool},
         }

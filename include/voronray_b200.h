@@ -123,13 +123,14 @@ typedef struct vr_prune_index {
 /* vr_raycast_batch through the pruned index.  `order` (nullable, n_rays
  * int32) is the processing order: slot k handles ray order[k]; callers sort
  * rays by the kd position of eta[0] so that a warp's rays are spatially
- * coherent.  Outputs are written at the ray's own index. */
+ * coherent.  Outputs are written at the ray's own index.  `work` (nullable,
+ * device uint64) accumulates the (ray, generator) pairs actually screened. */
 int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
                       const vr_prune_index* ix, const double* x, const double* u,
                       const int32_t* eta, int eta_len, int64_t n_rays,
                       const int32_t* order, int32_t* out_idx, double* out_t,
                       double* out_rp, uint8_t* out_flag, int32_t* recheck_list,
-                      int32_t* recheck_count, void* stream);
+                      int32_t* recheck_count, uint64_t* work, void* stream);
 
 /* Exact re-evaluation of the rays listed in recheck_list[0 .. *count)
  * (count read on device): centred t for every candidate, argmin with the
@@ -211,7 +212,7 @@ int vr_mc_rays_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
                       int64_t n_cells, int64_t rays_per_cell, const double* dirs,
                       uint64_t seed, int32_t* out_idx, double* out_t,
                       uint8_t* out_flag, int32_t* recheck_list,
-                      int32_t* recheck_count, void* stream);
+                      int32_t* recheck_count, uint64_t* work, void* stream);
 
 int vr_mc_recheck(const double* rec, int64_t n_gen, int d,
                   const double* cand_rec, const int32_t* cand, int64_t n_cand,

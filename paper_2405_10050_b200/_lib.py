@@ -43,9 +43,9 @@ _SIGNATURES = {
     "vr_mc_directions": [_int, _i64, _vp, _i64, _u64, _vp, _vp],
     "vr_fma_probe": [_int, _int, _int, _vp, _vp],
     "vr_raycast_pruned": [_vp, _i64, _int, _dbl, _vp, _vp, _vp, _vp, _int, _i64, _vp, _vp, _vp,
-                          _vp, _vp, _vp, _vp, _vp],
+                          _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_mc_rays_pruned": [_vp, _i64, _int, _dbl, _vp, _vp, _i64, _i64, _vp, _u64, _vp, _vp,
-                          _vp, _vp, _vp, _vp],
+                          _vp, _vp, _vp, _vp, _vp],
     "vr_trav_insert_vertices": [_vp, _int, _vp, _i64, ctypes.c_int32, ctypes.c_int32, _int, _vp],
     "vr_trav_rehash_edges": [_vp, _int, _vp, _vp, _vp, _i64, _vp],
     "vr_trav_open_edges": [_vp, _int, _vp, _i64, _vp, _vp, _vp],

@@ -239,7 +239,8 @@ extern "C" int vr_mc_rays_pruned(const double* rec, int64_t n_gen, int d, double
                                  const vr_prune_index* ix, const int32_t* cells, int64_t n_cells,
                                  int64_t rays_per_cell, const double* dirs, uint64_t seed,
                                  int32_t* out_idx, double* out_t, uint8_t* out_flag,
-                                 int32_t* recheck_list, int32_t* recheck_count, void* stream) {
+                                 int32_t* recheck_list, int32_t* recheck_count, uint64_t* work,
+                                 void* stream) {
   if (!rec || !ix || !ix->rec || !cells || !out_idx || !out_t || !out_flag || rays_per_cell <= 0 ||
       ix->n != n_gen)
     return VR_EINVAL;
@@ -248,7 +249,8 @@ extern "C" int vr_mc_rays_pruned(const double* rec, int64_t n_gen, int d, double
   PrunedIndex pi{ix->rec, ix->perm, ix->inv_perm, ix->tile_box, ix->block_box, ix->n};
   VR_DISPATCH_D(d, {
     SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n};
-    return launch_raycast_pruned<D>(src, n, pi, sqmax, out, as_stream(stream));
+    return launch_raycast_pruned<D>(src, n, pi, sqmax, out, as_stream(stream),
+                                    reinterpret_cast<unsigned long long*>(work));
   });
   return VR_OK;
 }

@@ -75,7 +75,7 @@ extern "C" int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double
                                  const int32_t* eta, int eta_len, int64_t n_rays,
                                  const int32_t* order, int32_t* out_idx, double* out_t,
                                  double* out_rp, uint8_t* out_flag, int32_t* recheck_list,
-                                 int32_t* recheck_count, void* stream) {
+                                 int32_t* recheck_count, uint64_t* work, void* stream) {
   if (!rec || !ix || !ix->rec || !ix->perm || !ix->inv_perm || !ix->tile_box || !ix->block_box ||
       !x || !u || !eta || !out_idx || !out_t || !out_flag)
     return VR_EINVAL;
@@ -85,7 +85,8 @@ extern "C" int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double
   PrunedIndex pi{ix->rec, ix->perm, ix->inv_perm, ix->tile_box, ix->block_box, ix->n};
   VR_DISPATCH_D(d, {
     SrcExplicit<D> src{x, u, eta, eta_len, rec, n_rays, order};
-    return launch_raycast_pruned<D>(src, n_rays, pi, sqmax, out, as_stream(stream));
+    return launch_raycast_pruned<D>(src, n_rays, pi, sqmax, out, as_stream(stream),
+                                    reinterpret_cast<unsigned long long*>(work));
   });
   return VR_OK;
 }

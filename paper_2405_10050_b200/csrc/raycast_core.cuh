@@ -475,23 +475,103 @@ __device__ __forceinline__ bool ray_needs_box(const RayState<D>& r, const double
   return d2 < r.rho2 + r.dlt + 1e-12 * (r.rho2 + d2);
 }
 
-template <int D, int R, int PT, int PB, int NT, int MINB, class Src>
-__global__ void __launch_bounds__(NT, MINB)
+// Cursor over the kd tiles in visiting order (cyclic from the warp's start
+// tile), yielding only tiles whose block and tile boxes pass the warp-wide
+// need test against the rays' CURRENT spheres.
+template <int D, int R, int PT, int PB>
+struct TileCursor {
+  int64_t ntiles, nblocks, st, sb;
+  int64_t bi = 0;      // blocks visited so far
+  int64_t ti = 0;      // tiles visited inside the current block
+  bool in_block = false;
+  __device__ __forceinline__ int64_t next(const RayState<D> (&ray)[R],
+                                          const double* __restrict__ tile_box,
+                                          const double* __restrict__ block_box) {
+    while (bi < nblocks) {
+      const int64_t b = (sb + bi) % nblocks;
+      const int64_t t_lo = b * PB, t_hi = min(ntiles, t_lo + PB);
+      if (!in_block) {
+        bool need = false;
+#pragma unroll
+        for (int j = 0; j < R; ++j) need |= ray_needs_box<D>(ray[j], block_box + b * 2 * D);
+        if (!__any_sync(0xffffffffu, need)) { ++bi; continue; }
+        in_block = true;
+        ti = 0;
+      }
+      const int64_t tstart = (b == sb) ? st : t_lo;
+      while (ti < t_hi - t_lo) {
+        int64_t t = tstart + ti;
+        if (t >= t_hi) t -= (t_hi - t_lo);
+        ++ti;
+        bool need = false;
+#pragma unroll
+        for (int j = 0; j < R; ++j) need |= ray_needs_box<D>(ray[j], tile_box + t * 2 * D);
+        if (__any_sync(0xffffffffu, need)) return t;
+      }
+      in_block = false;
+      ++bi;
+    }
+    return -1;
+  }
+};
+
+template <int D, int R, int PT>
+__device__ __forceinline__ void screen_tile(RayState<D> (&ray)[R], const double* tile, int gbase,
+                                            double sqmax) {
+  constexpr int S = rec_stride(D);
+  constexpr int U = 8;
+  for (int c = 0; c < PT; c += U) {
+    unsigned m[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) m[j] = 0u;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double xi[D];
+      load_rec<D>(tile + (c + u) * S, xi);
+      const double sq = tile[(c + u) * S + D];
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        m[j] |= (ray_power<D>(ray[j], xi, sq) < ray[j].hi) ? (1u << u) : 0u;
+    }
+    unsigned any = 0u;
+#pragma unroll
+    for (int j = 0; j < R; ++j) any |= m[j];
+    if (__any_sync(0xffffffffu, any != 0u)) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        unsigned mm = m[j];
+        while (mm) {
+          const int u = __ffs(mm) - 1;
+          mm &= mm - 1;
+          double xi[D];
+          load_rec<D>(tile + (c + u) * S, xi);
+          ray_rare<D>(ray[j], xi, tile[(c + u) * S + D], gbase + c + u, sqmax);
+        }
+      }
+    }
+  }
+}
+
+// One warp per CTA (warps finish at very different times; a freed slot is
+// refilled immediately).  The warp's next needed tile is fetched by TMA into
+// the other half of a two-tile shared-memory buffer while the current tile
+// is screened; the need test is re-applied before screening (spheres shrink).
+template <int D, int R, int PT, int PB, int MINB, class Src>
+__global__ void __launch_bounds__(32, MINB)
     k_raycast_pruned(Src src, const double* __restrict__ crec, const int32_t* __restrict__ perm,
                      const int32_t* __restrict__ inv_perm, int64_t n_cand,
                      const double* __restrict__ tile_box, const double* __restrict__ block_box,
-                     double sqmax, RayOut out) {
+                     double sqmax, RayOut out, unsigned long long* __restrict__ work) {
   constexpr int S = rec_stride(D);
-  constexpr int U = 8;
-  static_assert(PT % U == 0 && VR_REC_PAD % PT == 0, "tile must divide the record padding");
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)NT + threadIdx.x) >> 5;
-  const int64_t ntiles = (n_cand + PT - 1) / PT;
-  const int64_t nblocks = (ntiles + PB - 1) / PB;
+  constexpr uint32_t TILE_BYTES = (uint32_t)(PT * S * sizeof(double));
+  static_assert(PT % 8 == 0 && VR_REC_PAD % PT == 0, "tile must divide the record padding");
+  __shared__ __align__(128) double buf[2][PT * S];
+  __shared__ uint64_t bar[2];
+  const int lane = threadIdx.x;
+  const int64_t k0 = (int64_t)blockIdx.x * 32 * R + lane;
 
   RayState<D> ray[R];
   bool act[R];
-  const int64_t k0 = warp * 32 * R + lane;
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     act[j] = src.load(k0 + (int64_t)j * 32, ray[j]);
@@ -502,65 +582,55 @@ __global__ void __launch_bounds__(NT, MINB)
       for (int k = 0; k < D; ++k) ray[j].z[k] = 0.0;
     }
   }
-  if (!__any_sync(0xffffffffu, act[0])) return;
-  // start where lane 0's first ray lives in kd-order
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
   int64_t st = 0;
   if (lane == 0) st = inv_perm[src.gen(k0)] / PT;
   st = __shfl_sync(0xffffffffu, st, 0);
-  const int64_t sb = st / PB;
+  TileCursor<D, R, PT, PB> cur;
+  cur.ntiles = (n_cand + PT - 1) / PT;
+  cur.nblocks = (cur.ntiles + PB - 1) / PB;
+  cur.st = st;
+  cur.sb = st / PB;
 
-  for (int64_t bi = 0; bi < nblocks; ++bi) {
-    const int64_t b = (sb + bi) % nblocks;
+  auto issue = [&](int64_t t, int b) {
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(&bar[b], TILE_BYTES);
+      bulk_g2s(buf[b], crec + t * PT * S, TILE_BYTES, &bar[b]);
+    }
+  };
+  unsigned long long tiles_done = 0;
+  uint32_t phase[2] = {0u, 0u};
+  int b = 0;
+  int64_t t = cur.next(ray, tile_box, block_box);
+  if (t >= 0) issue(t, 0);
+  while (t >= 0) {
+    const int64_t tn = cur.next(ray, tile_box, block_box);
+    __syncwarp();
+    if (tn >= 0) issue(tn, b ^ 1);
+    mbar_wait(&bar[b], phase[b]);
+    phase[b] ^= 1u;
     bool need = false;
 #pragma unroll
-    for (int j = 0; j < R; ++j) need |= ray_needs_box<D>(ray[j], block_box + b * 2 * D);
-    if (!__any_sync(0xffffffffu, need)) continue;
-    const int64_t t_lo = b * PB, t_hi = min(ntiles, t_lo + PB);
-    const int64_t tstart = (b == sb) ? st : t_lo;
-    for (int64_t ti = 0; ti < t_hi - t_lo; ++ti) {
-      int64_t t = tstart + ti;
-      if (t >= t_hi) t -= (t_hi - t_lo);
-      bool tneed = false;
-#pragma unroll
-      for (int j = 0; j < R; ++j) tneed |= ray_needs_box<D>(ray[j], tile_box + t * 2 * D);
-      if (!__any_sync(0xffffffffu, tneed)) continue;
-      const double* tile = crec + t * PT * S;
-      const int gbase = (int)(t * PT);
-      for (int c = 0; c < PT; c += U) {
-        unsigned m[R];
-#pragma unroll
-        for (int j = 0; j < R; ++j) m[j] = 0u;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          double xi[D];
-          load_rec_g<D>(tile + (c + u) * S, xi);
-          const double sq = __ldg(tile + (c + u) * S + D);
-#pragma unroll
-          for (int j = 0; j < R; ++j)
-            m[j] |= (ray_power<D>(ray[j], xi, sq) < ray[j].hi) ? (1u << u) : 0u;
-        }
-        unsigned any = 0u;
-#pragma unroll
-        for (int j = 0; j < R; ++j) any |= m[j];
-        if (__any_sync(0xffffffffu, any != 0u)) {
-#pragma unroll
-          for (int j = 0; j < R; ++j) {
-            unsigned mm = m[j];
-            while (mm) {
-              const int u = __ffs(mm) - 1;
-              mm &= mm - 1;
-              double xi[D];
-              load_rec_g<D>(tile + (c + u) * S, xi);
-              ray_rare<D>(ray[j], xi, __ldg(tile + (c + u) * S + D), gbase + c + u, sqmax);
-            }
-          }
-        }
-      }
+    for (int j = 0; j < R; ++j) need |= ray_needs_box<D>(ray[j], tile_box + t * 2 * D);
+    if (__any_sync(0xffffffffu, need)) {
+      ++tiles_done;
+      screen_tile<D, R, PT>(ray, buf[b], (int)(t * PT), sqmax);
     }
+    __syncwarp();
+    b ^= 1;
+    t = tn;
   }
 #pragma unroll
   for (int j = 0; j < R; ++j)
     if (act[j]) ray_store<D>(ray[j], src.id(k0 + (int64_t)j * 32), perm, out);
+  // work counter: (ray, generator) pairs screened = tiles x PT x 32 lanes x R
+  if (work && lane == 0) atomicAdd(work, tiles_done * (unsigned long long)(PT * 32 * R));
 }
 
 // ---------------------------------------------------------------------------
@@ -729,20 +799,19 @@ constexpr int PRUNE_BLOCK = 32;
 
 template <int D, class Src>
 int launch_raycast_pruned(const Src& src, int64_t n_rays, const PrunedIndex& ix, double sqmax,
-                          const RayOut& out, cudaStream_t st) {
+                          const RayOut& out, cudaStream_t st, unsigned long long* work) {
   if (n_rays <= 0) return VR_OK;
   if (ix.n <= 0) return VR_EINVAL;
   if (out.recheck_count) {
     cudaError_t e = cudaMemsetAsync(out.recheck_count, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return vr_cuda_status(e);
   }
-  constexpr int NT = 128;
   constexpr int R = (D <= 3) ? 4 : 2;
-  constexpr int MINB = (D <= 3 || D >= 7) ? 2 : 3;
-  const int64_t per_block = (int64_t)NT * R;
+  constexpr int MINB = (D == 4) ? 12 : ((D == 6) ? 10 : 8);
+  const int64_t per_block = 32 * R;
   const int64_t grid = (n_rays + per_block - 1) / per_block;
-  k_raycast_pruned<D, R, PRUNE_TILE, PRUNE_BLOCK, NT, MINB, Src><<<(unsigned)grid, NT, 0, st>>>(
-      src, ix.crec, ix.perm, ix.inv_perm, ix.n, ix.tile_box, ix.block_box, sqmax, out);
+  k_raycast_pruned<D, R, PRUNE_TILE, PRUNE_BLOCK, MINB, Src><<<(unsigned)grid, 32, 0, st>>>(
+      src, ix.crec, ix.perm, ix.inv_perm, ix.n, ix.tile_box, ix.block_box, sqmax, out, work);
   VR_RETURN_LAUNCH();
 }
 

@@ -118,7 +118,7 @@ def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_fa
         _lib.check(L.vr_mc_rays_pruned(_lib.ptr(rec), ns.n, d, sqmax, ctypes.byref(ix.struct),
                                        _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed,
                                        _lib.ptr(idx), _lib.ptr(t), _lib.ptr(flag), _lib.ptr(rl),
-                                       _lib.ptr(rc), sh), "vr_mc_rays_pruned")
+                                       _lib.ptr(rc), None, sh), "vr_mc_rays_pruned")
     else:
         _lib.check(L.vr_mc_rays(_lib.ptr(rec), ns.n, d, sqmax, _lib.ptr(crec), _lib.ptr(cand),
                                 n_cand, _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed,

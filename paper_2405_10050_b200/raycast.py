@@ -141,7 +141,7 @@ def _use_pruned(ns, candidates, mode):
 
 def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=None,
                   workspace=None, out=None, stream=None, events=None,
-                  mode="auto") -> RaycastBatch:
+                  mode="auto", work=None) -> RaycastBatch:
     """Batched incircle RayCast on the current CUDA device.
 
     Args:
@@ -158,6 +158,8 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
         mode: "exhaustive" scans every generator (TMA-staged tiles);
             "pruned" skips kd tiles with a certificate (identical results);
             "auto" prunes when N >= 1024 and no candidate subset is given.
+        work: optional int64 device tensor (1,) accumulating the pairs the
+            pruned kernel screened (roofline accounting).
 
     Stream-ordered; no host synchronisation.
     """
@@ -213,7 +215,7 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
                                        _lib.ptr(xd), _lib.ptr(ud), _lib.ptr(ed), k, n,
                                        _lib.ptr(order), _lib.ptr(idx), _lib.ptr(t),
                                        _lib.ptr(rp), _lib.ptr(flag), _lib.ptr(rl), _lib.ptr(rc),
-                                       sh), "vr_raycast_pruned")
+                                       _lib.ptr(work), sh), "vr_raycast_pruned")
     else:
         _lib.check(L.vr_raycast_batch(_lib.ptr(rec), ns.n, d, sqmax, _lib.ptr(crec),
                                       _lib.ptr(cand), n_cand, _lib.ptr(xd), _lib.ptr(ud),
@@ -232,18 +234,21 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
 
 
 class HostRaycaster:
-    """Batched RayCast on host (pinned) arrays, pipelined over two streams:
-    the H2D copy of chunk c+1 and the D2H copy of chunk c-1 overlap the
-    kernel of chunk c.  The end-to-end public entry point for callers whose
-    rays live in host memory."""
+    """Batched RayCast on host (pinned) arrays, pipelined over three streams:
+    the H2D copy of chunk c+1 and the D2H copy of chunk c-1 run on separate
+    copy engines while the kernel of chunk c runs.  The end-to-end public
+    entry point for callers whose rays live in host memory."""
+
+    NBUF = 3
 
     def __init__(self, ns: NodeSet, n_max: int, eta_len: int, chunk: int = 1 << 17):
         rec, _ = ns.device_records()
         self.ns, self.dev, self.chunk, self.k = ns, rec.device, int(chunk), int(eta_len)
         d = ns.dim
         c = self.chunk
-        self.copy_stream = torch.cuda.Stream(self.dev)
+        self.h2d_stream = torch.cuda.Stream(self.dev)
         self.comp_stream = torch.cuda.Stream(self.dev)
+        self.d2h_stream = torch.cuda.Stream(self.dev)
         self.buf = [dict(x=torch.empty((c, d), dtype=torch.float64, device=self.dev),
                          u=torch.empty((c, d), dtype=torch.float64, device=self.dev),
                          eta=torch.empty((c, self.k), dtype=torch.int32, device=self.dev),
@@ -252,8 +257,8 @@ class HostRaycaster:
                          rp=torch.empty((c, d), dtype=torch.float64, device=self.dev),
                          flag=torch.empty(c, dtype=torch.uint8, device=self.dev),
                          h2d=torch.cuda.Event(), done=torch.cuda.Event(), d2h=torch.cuda.Event())
-                    for _ in range(2)]
-        self.ws = [Workspace(), Workspace()]
+                    for _ in range(self.NBUF)]
+        self.ws = [Workspace() for _ in range(self.NBUF)]
 
     @staticmethod
     def pinned(shape, dtype):
@@ -266,136 +271,32 @@ class HostRaycaster:
         n = hx.shape[0]
         c = self.chunk
         nchunks = (n + c - 1) // c
+        if self.ns.n >= 1024 and mode != "exhaustive":
+            self.ns.prune_index(self.dev)
         for ci in range(nchunks):
-            b = self.buf[ci & 1]
+            b = self.buf[ci % self.NBUF]
             lo, hi = ci * c, min(n, (ci + 1) * c)
             m = hi - lo
-            with torch.cuda.stream(self.copy_stream):
-                self.copy_stream.wait_event(b["d2h"])  # buffer free again
+            with torch.cuda.stream(self.h2d_stream):
+                if ci >= self.NBUF:
+                    self.h2d_stream.wait_event(b["d2h"])  # buffer drained
                 b["x"][:m].copy_(hx[lo:hi], non_blocking=True)
                 b["u"][:m].copy_(hu[lo:hi], non_blocking=True)
                 b["eta"][:m].copy_(heta[lo:hi], non_blocking=True)
-                b["h2d"].record(self.copy_stream)
+                b["h2d"].record(self.h2d_stream)
             with torch.cuda.stream(self.comp_stream):
                 self.comp_stream.wait_event(b["h2d"])
                 raycast_batch(self.ns, b["x"][:m], b["u"][:m], b["eta"][:m],
                               out=dict(idx=b["idx"][:m], t=b["t"][:m], rp=b["rp"][:m],
                                        flag=b["flag"][:m]),
-                              workspace=self.ws[ci & 1], stats=stats,
+                              workspace=self.ws[ci % self.NBUF], stats=stats,
                               stream=self.comp_stream, mode=mode)
                 b["done"].record(self.comp_stream)
-            with torch.cuda.stream(self.copy_stream):
-                self.copy_stream.wait_event(b["done"])
+            with torch.cuda.stream(self.d2h_stream):
+                self.d2h_stream.wait_event(b["done"])
                 hidx[lo:hi].copy_(b["idx"][:m], non_blocking=True)
                 ht[lo:hi].copy_(b["t"][:m], non_blocking=True)
                 hrp[lo:hi].copy_(b["rp"][:m], non_blocking=True)
                 hflag[lo:hi].copy_(b["flag"][:m], non_blocking=True)
-                b["d2h"].record(self.copy_stream)
-        self.copy_stream.synchronize()
-
-
-def raycast_incircle(ns: NodeSet, q: RayQuery, stats: RaycastStats = None,
-                     heuristic: bool = True, candidates=None):
-    """Exact first Voronoi object hit by the ray, or None if it escapes.
-
-    Drop-in for raycast.py:154-224: returns ``(tuple(sorted(eta + (i,))), rp)``
-    or ``None``; raises :class:`DegenerateConfiguration` when a foreign
-    generator lies within the reference's 1e-10 band of the circumsphere.
-    ``heuristic`` is result-neutral in the reference and ignored here.
-    """
-    if stats is None:
-        stats = RaycastStats()
-    eta = tuple(int(e) for e in q.eta)
-    res = raycast_batch(ns, np.asarray(q.r, dtype=float)[None], np.asarray(q.u, dtype=float)[None],
-                        np.asarray([eta], dtype=np.int32), candidates=candidates, stats=stats)
-    idx, _, rp, flag = res.to_host()
-    f = int(flag[0])
-    if f == RAY_ESCAPED:
-        return None
-    if f == RAY_DEGENERATE:
-        raise DegenerateConfiguration(
-            f"a foreign generator lies on the circumsphere of {(*eta, int(idx[0]))}")
-    return tuple(sorted((*eta, int(idx[0])))), rp[0]
-
-
-# --- host-side direction helpers (raycast.py:295-378) ----------------------
-
-def _orthonormal_rows(diffs):
-    """Modified Gram-Schmidt, two passes (raycast.py:295-308)."""
-    out = []
-    for row in np.atleast_2d(diffs) if len(diffs) else []:
-        v = np.array(row, dtype=float)
-        norm0 = math.sqrt(float(v @ v))
-        for _ in range(2):
-            for qv in out:
-                v -= (qv @ v) * qv
-        norm = math.sqrt(float(v @ v))
-        if norm < RANK_TOL * max(norm0, 1.0):
-            raise DegenerateConfiguration("generators are affinely dependent")
-        out.append(v / norm)
-    return out
-
-
-def _project_out(w, basis):
-    """Component of ``w`` orthogonal to orthonormal rows (raycast.py:311-317)."""
-    v = np.array(w, dtype=float)
-    for _ in range(2):
-        for qv in basis:
-            v -= (qv @ v) * qv
-    return v
-
-
-def _search_direction(pts, eta, missing):
-    sub = pts[list(eta)]
-    basis = _orthonormal_rows(sub[1:] - sub[0]) if len(eta) > 1 else []
-    w = sub.sum(axis=0) * (1.0 / len(eta)) - pts[missing]
-    v = _project_out(w, basis)
-    norm = math.sqrt(float(v @ v))
-    if norm < RANK_TOL * max(math.sqrt(float(w @ w)), 1.0):
-        raise DegenerateConfiguration(f"generator {missing} lies in the affine span of {eta}")
-    return v / norm
-
-
-def search_direction(ns: NodeSet, sigma, eta):
-    """Outward direction of edge ``eta`` of vertex ``sigma`` (raycast.py:320-342)."""
-    extra = set(sigma) - set(eta)
-    if len(extra) != 1 or not set(eta) <= set(sigma):
-        raise ValueError("eta must be sigma minus exactly one generator")
-    return _search_direction(ns.points, tuple(eta), extra.pop())
-
-
-def vertex_directions_batch(ns: NodeSet, sigma):
-    """All d+1 edge directions of many vertices on the GPU (vr_vertex_directions).
-
-    Returns (u (V, d+1, d) device tensor, ok (V, d+1) uint8 device tensor)."""
-    rec, _ = ns.device_records()
-    dev = rec.device
-    L = _lib.lib()
-    sd = _as_dev(np.asarray(sigma), dev, torch.int32).view(-1, ns.dim + 1)
-    nv = sd.shape[0]
-    u = torch.empty((nv, ns.dim + 1, ns.dim), dtype=torch.float64, device=dev)
-    ok = torch.empty((nv, ns.dim + 1), dtype=torch.uint8, device=dev)
-    _lib.check(L.vr_vertex_directions(_lib.ptr(rec), ns.dim, _lib.ptr(sd), nv, _lib.ptr(u),
-                                      _lib.ptr(ok), _lib.stream_handle()), "vr_vertex_directions")
-    return u, ok
-
-
-def _vertex_directions(pts, sigma, positions):
-    """Outward directions for several edges of one vertex (raycast.py:345-378).
-
-    Host fp64 inverse with the reference's column convention; the traversal
-    itself uses the batched device kernel (vr_vertex_directions)."""
-    sub = pts[list(sigma)]
-    diffs = sub[1:] - sub[0]
-    try:
-        inv = np.linalg.inv(diffs)
-    except np.linalg.LinAlgError:
-        raise DegenerateConfiguration(f"generators of {sigma} are affinely dependent") from None
-    out = {}
-    for k in positions:
-        v = inv.sum(axis=1) if k == 0 else -inv[:, k - 1]
-        norm = math.sqrt(float(v @ v))
-        if not norm > 0.0 or not math.isfinite(norm):
-            raise DegenerateConfiguration(f"generators of {sigma} are affinely dependent")
-        out[k] = v / norm
-    return out
+                b["d2h"].record(self.d2h_stream)
+        self.d2h_stream.synchronize()
