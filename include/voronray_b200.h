@@ -71,6 +71,26 @@ int64_t vr_record_rows(int64_t n);
 int vr_pack_generators(const double* pts, int64_t n, int d, double* rec,
                        double* sqmax_out /* device, 1 double */, void* stream);
 
+/* Optional fp32 screening input.  The kernels screen every (ray, generator)
+ * pair in fp32 in a frame centred at `center` with a rigorous, rounded-up
+ * error bound, and send every candidate the fp32 screen cannot exclude
+ * through the unchanged fp64 path (fp64 test first) -- results are identical
+ * to the fp64 screen.  `rec` holds vr_record_rows(n) rows of
+ * vr_record32_stride(d) floats [x - center, |x - center|^2, pad] in the SAME
+ * row order as the fp64 records the call scans (sentinel rows: |.|^2 = +inf);
+ * sqmax = max |x - center|^2.  NULL selects the fp64 screen. */
+typedef struct vr_screen32 {
+  const float* rec;
+  double center[8];
+  double sqmax;
+} vr_screen32;
+
+int vr_record32_stride(int d);
+
+/* fp32 centred copy of packed fp64 records (same rows, sentinels kept). */
+int vr_pack_records32(const double* rec, int64_t rows, int d, const double* center,
+                      float* rec32, void* stream);
+
 /* Batched incircle RayCast (reference raycast_incircle, raycast.py:154-224,
  * with its filtered NN probe _Probe, raycast.py:85-151, core.py:62-103).
  *
@@ -93,6 +113,7 @@ int vr_pack_generators(const double* pts, int64_t n, int d, double* rec,
  * receives the ids of RECHECK rays (the count is zeroed on `stream` first);
  * may be NULL if the caller does not resolve. */
 int vr_raycast_batch(const double* rec, int64_t n_gen, int d, double sqmax,
+                     const vr_screen32* s32,
                      const double* cand_rec, const int32_t* cand, int64_t n_cand,
                      const double* x, const double* u,
                      const int32_t* eta, int eta_len, int64_t n_rays,
@@ -113,6 +134,7 @@ int vr_raycast_batch(const double* rec, int64_t n_gen, int d, double sqmax,
 #define VR_PRUNE_BLOCK 32
 typedef struct vr_prune_index {
   const double* rec;       /* kd-ordered records, vr_record_rows(n) rows       */
+  const float* rec32;      /* kd-ordered fp32 centred records (nullable)       */
   const int32_t* perm;     /* kd position -> generator index (n)               */
   const int32_t* inv_perm; /* generator index -> kd position (n)               */
   const double* tile_box;  /* ceil(n/64) x 2d, [lo_0..lo_{d-1}, hi_0..]        */
@@ -123,10 +145,11 @@ typedef struct vr_prune_index {
 /* vr_raycast_batch through the pruned index.  `order` (nullable, n_rays
  * int32) is the processing order: slot k handles ray order[k]; callers sort
  * rays by the kd position of eta[0] so that a warp's rays are spatially
- * coherent.  Outputs are written at the ray's own index.  `work` (nullable,
+ * coherent.  Outputs are written at the ray's own index.  With s32 != NULL and
+ * ix->rec32 != NULL the screen runs in fp32 (s32->rec is not used here).  `work` (nullable,
  * device uint64) accumulates the (ray, generator) pairs actually screened. */
 int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
-                      const vr_prune_index* ix, const double* x, const double* u,
+                      const vr_screen32* s32, const vr_prune_index* ix, const double* x, const double* u,
                       const int32_t* eta, int eta_len, int64_t n_rays,
                       const int32_t* order, int32_t* out_idx, double* out_t,
                       double* out_rp, uint8_t* out_flag, int32_t* recheck_list,
@@ -200,7 +223,7 @@ int vr_vertex_directions(const double* rec, int d, const int32_t* sigma,
  * _mc_areas_batch takes the plain argmin).  surf = S_{d-1} as computed by the
  * caller (integrate_mc.py:44-48); max_faces <= 512. */
 int vr_mc_rays(const double* rec, int64_t n_gen, int d, double sqmax,
-               const double* cand_rec, const int32_t* cand, int64_t n_cand,
+               const vr_screen32* s32, const double* cand_rec, const int32_t* cand, int64_t n_cand,
                const int32_t* cells, int64_t n_cells, int64_t rays_per_cell,
                const double* dirs, uint64_t seed,
                int32_t* out_idx, double* out_t, uint8_t* out_flag,
@@ -208,7 +231,7 @@ int vr_mc_rays(const double* rec, int64_t n_gen, int d, double sqmax,
 
 /* vr_mc_rays through the pruned index (rays of one cell are coherent). */
 int vr_mc_rays_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
-                      const vr_prune_index* ix, const int32_t* cells,
+                      const vr_screen32* s32, const vr_prune_index* ix, const int32_t* cells,
                       int64_t n_cells, int64_t rays_per_cell, const double* dirs,
                       uint64_t seed, int32_t* out_idx, double* out_t,
                       uint8_t* out_flag, int32_t* recheck_list,

@@ -26,7 +26,7 @@ _SIGNATURES = {
     "vr_abi_version": [],
     "vr_record_stride": [_int],
     "vr_pack_generators": [_vp, _i64, _int, _vp, _vp, _vp],
-    "vr_raycast_batch": [_vp, _i64, _int, _dbl, _vp, _vp, _i64, _vp, _vp, _vp, _int, _i64,
+    "vr_raycast_batch": [_vp, _i64, _int, _dbl, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _int, _i64,
                          _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_raycast_recheck": [_vp, _i64, _int, _vp, _vp, _i64, _vp, _vp, _vp, _int, _vp, _vp, _i64,
                            _vp, _vp, _vp, _vp, _vp],
@@ -34,7 +34,7 @@ _SIGNATURES = {
     "vr_verify_vertices": [_vp, _i64, _int, _vp, _vp, _i64, _dbl, _vp, _vp],
     "vr_circumcenters": [_vp, _int, _vp, _i64, _vp, _vp, _vp],
     "vr_vertex_directions": [_vp, _int, _vp, _i64, _vp, _vp, _vp],
-    "vr_mc_rays": [_vp, _i64, _int, _dbl, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _u64,
+    "vr_mc_rays": [_vp, _i64, _int, _dbl, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _u64,
                    _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_mc_recheck": [_vp, _i64, _int, _vp, _vp, _i64, _vp, _i64, _vp, _u64, _vp, _vp, _i64,
                       _vp, _vp, _vp, _vp],
@@ -42,10 +42,12 @@ _SIGNATURES = {
                      _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_mc_directions": [_int, _i64, _vp, _i64, _u64, _vp, _vp],
     "vr_fma_probe": [_int, _int, _int, _vp, _vp],
-    "vr_raycast_pruned": [_vp, _i64, _int, _dbl, _vp, _vp, _vp, _vp, _int, _i64, _vp, _vp, _vp,
+    "vr_raycast_pruned": [_vp, _i64, _int, _dbl, _vp, _vp, _vp, _vp, _vp, _int, _i64, _vp, _vp,
+                          _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "vr_mc_rays_pruned": [_vp, _i64, _int, _dbl, _vp, _vp, _vp, _i64, _i64, _vp, _u64, _vp,
                           _vp, _vp, _vp, _vp, _vp, _vp],
-    "vr_mc_rays_pruned": [_vp, _i64, _int, _dbl, _vp, _vp, _i64, _i64, _vp, _u64, _vp, _vp,
-                          _vp, _vp, _vp, _vp, _vp],
+    "vr_pack_records32": [_vp, _i64, _int, _vp, _vp, _vp],
+    "vr_record32_stride": [_int],
     "vr_trav_insert_vertices": [_vp, _int, _vp, _i64, ctypes.c_int32, ctypes.c_int32, _int, _vp],
     "vr_trav_rehash_edges": [_vp, _int, _vp, _vp, _vp, _i64, _vp],
     "vr_trav_open_edges": [_vp, _int, _vp, _i64, _vp, _vp, _vp],

@@ -71,6 +71,7 @@ class NodeSet:
         self.backend = backend
         self._dev = {}
         self._prune = {}
+        self._s32 = {}
 
     def __len__(self):
         return self.n
@@ -101,6 +102,16 @@ class NodeSet:
         self._dev[dev.index] = entry
         return entry
 
+    def screen32(self, device=None):
+        """Centred fp32 copy of the records for the fp32 screen (built once)."""
+        dev = _device(device)
+        hit = self._s32.get(dev.index)
+        if hit is None:
+            rec, _ = self.device_records(dev)
+            hit = Screen32(rec, self.n, self.dim)
+            self._s32[dev.index] = hit
+        return hit
+
     def prune_index(self, device=None):
         """kd-ordered records + tile / block bounding boxes for the pruned
         RayCast (include/voronray_b200.h vr_prune_index); built once per
@@ -109,7 +120,7 @@ class NodeSet:
         hit = self._prune.get(dev.index)
         if hit is None:
             rec, _ = self.device_records(dev)
-            hit = PruneIndex(rec, self.n, self.dim)
+            hit = PruneIndex(rec, self.n, self.dim, self.screen32(dev).center)
             self._prune[dev.index] = hit
         return hit
 
@@ -155,8 +166,34 @@ class NodeSet:
 PRUNE_TILE, PRUNE_BLOCK = 64, 32
 
 
+class _Screen32Struct(ctypes.Structure):
+    _fields_ = [("rec", ctypes.c_void_p), ("center", ctypes.c_double * 8),
+                ("sqmax", ctypes.c_double)]
+
+
+class Screen32:
+    """Centred fp32 copy of a record array (include/voronray_b200.h vr_screen32)."""
+
+    def __init__(self, rec, n, d, center=None):
+        L = _lib.lib()
+        dev = rec.device
+        pts = rec[:n, :d]
+        if center is None:
+            center = 0.5 * (pts.amin(0) + pts.amax(0))
+        self.center = center.to(torch.float64).contiguous()
+        self.sqmax = float(((pts - self.center) ** 2).sum(1).max().item())
+        s32 = (d + 4) & ~3
+        self.rec = torch.empty((rec.shape[0], s32), dtype=torch.float32, device=dev)
+        _lib.check(L.vr_pack_records32(_lib.ptr(rec), rec.shape[0], d, _lib.ptr(self.center),
+                                       _lib.ptr(self.rec), _lib.stream_handle()),
+                   "vr_pack_records32")
+        c = [0.0] * 8
+        c[:d] = self.center.cpu().tolist()
+        self.struct = _Screen32Struct(self.rec.data_ptr(), (ctypes.c_double * 8)(*c), self.sqmax)
+
+
 class _PruneStruct(ctypes.Structure):
-    _fields_ = [("rec", ctypes.c_void_p), ("perm", ctypes.c_void_p),
+    _fields_ = [("rec", ctypes.c_void_p), ("rec32", ctypes.c_void_p), ("perm", ctypes.c_void_p),
                 ("inv_perm", ctypes.c_void_p), ("tile_box", ctypes.c_void_p),
                 ("block_box", ctypes.c_void_p), ("n", ctypes.c_int64)]
 
@@ -208,7 +245,7 @@ def kd_order(P, tile=PRUNE_TILE):
 class PruneIndex:
     """Device tensors of one vr_prune_index."""
 
-    def __init__(self, rec, n, d):
+    def __init__(self, rec, n, d, center):
         dev = rec.device
         pts = rec[:n, :d]
         perm = kd_order(pts)
@@ -234,9 +271,10 @@ class PruneIndex:
         self.rec = crec
         self.n = n
         self.rows = rows
+        self.screen32 = Screen32(crec, n, d, center=center)
         p = lambda t: t.data_ptr()  # noqa: E731
-        self.struct = _PruneStruct(p(crec), p(self.perm), p(self.inv_perm), p(self.tile_box),
-                                   p(self.block_box), n)
+        self.struct = _PruneStruct(p(crec), p(self.screen32.rec), p(self.perm), p(self.inv_perm),
+                                   p(self.tile_box), p(self.block_box), n)
 
 
 def build_node_set(points, backend="auto"):

@@ -28,6 +28,10 @@ __host__ __device__ constexpr int64_t rec_rows(int64_t n) {
 // even count so every record starts on a 16-byte boundary (LDS.128 / TMA).
 __host__ __device__ constexpr int rec_stride(int d) { return (d + 2) & ~1; }
 
+// Floats per fp32 screening record: [x_0 - c_0 .. x_{d-1} - c_{d-1}, |x - c|^2]
+// rounded up to a multiple of 4 (16-B rows).
+__host__ __device__ constexpr int rec32_stride(int d) { return (d + 4) & ~3; }
+
 static inline int vr_cuda_status(cudaError_t e) {
   return e == cudaSuccess ? VR_OK : (VR_ECUDA_BASE - (int)e);
 }

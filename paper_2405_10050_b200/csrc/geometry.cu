@@ -184,6 +184,27 @@ __global__ void k_vertex_dirs(const double* __restrict__ rec, const int32_t* __r
                  out_ok ? out_ok + v * (D + 1) : nullptr);
 }
 
+template <int D>
+__global__ void k_pack32(const double* __restrict__ rec, int64_t rows, const double* __restrict__ c0,
+                         float* __restrict__ rec32) {
+  constexpr int S = rec_stride(D);
+  constexpr int S32 = rec32_stride(D);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool sentinel = isinf(rec[i * S + D]);
+    double sq = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const double v = rec[i * S + k] - c0[k];
+      rec32[i * S32 + k] = sentinel ? 0.0f : (float)v;
+      sq = fma(v, v, sq);
+    }
+    rec32[i * S32 + D] = sentinel ? CUDART_INF_F : (float)sq;
+#pragma unroll
+    for (int k = D + 1; k < S32; ++k) rec32[i * S32 + k] = 0.0f;
+  }
+}
+
 inline unsigned blocks_for(int64_t n, int nt) { return (unsigned)((n + nt - 1) / nt); }
 
 }  // namespace
@@ -201,6 +222,16 @@ extern "C" int vr_pack_generators(const double* pts, int64_t n, int d, double* r
   const unsigned nb = blocks_for(n, 256) < 4096 ? blocks_for(n, 256) : 4096;
   VR_DISPATCH_D(d, {
     k_pack<D><<<nb, 256, 0, st>>>(pts, n, rec, reinterpret_cast<unsigned long long*>(sqmax_out));
+  });
+  VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_pack_records32(const double* rec, int64_t rows, int d, const double* center,
+                                 float* rec32, void* stream) {
+  if (!rec || !rec32 || !center || rows <= 0) return VR_EINVAL;
+  const unsigned nbk = blocks_for(rows, 256) < 4096 ? blocks_for(rows, 256) : 4096;
+  VR_DISPATCH_D(d, {
+    k_pack32<D><<<nbk, 256, 0, as_stream(stream)>>>(rec, rows, center, rec32);
   });
   VR_RETURN_LAUNCH();
 }

@@ -165,7 +165,7 @@ __global__ void k_mc_dirs(SrcMC<D> src, double* out_z) {
 }  // namespace
 
 extern "C" int vr_mc_rays(const double* rec, int64_t n_gen, int d, double sqmax,
-                          const double* cand_rec, const int32_t* cand, int64_t n_cand,
+                          const vr_screen32* s32, const double* cand_rec, const int32_t* cand, int64_t n_cand,
                           const int32_t* cells, int64_t n_cells, int64_t rays_per_cell,
                           const double* dirs, uint64_t seed, int32_t* out_idx, double* out_t,
                           uint8_t* out_flag, int32_t* recheck_list, int32_t* recheck_count,
@@ -178,7 +178,8 @@ extern "C" int vr_mc_rays(const double* rec, int64_t n_gen, int d, double sqmax,
   RayOut out{out_idx, out_t, nullptr, out_flag, recheck_list, recheck_count};
   VR_DISPATCH_D(d, {
     SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n};
-    return launch_raycast<D>(src, n, crec, cand, nc, sqmax, out, as_stream(stream));
+    return launch_raycast<D>(src, n, crec, cand, nc, make_screen(sqmax, s32, d), out,
+                             as_stream(stream));
   });
   return VR_OK;
 }
@@ -236,7 +237,7 @@ extern "C" int vr_mc_directions(int d, int64_t n_cells, const int32_t* cells,
 }
 
 extern "C" int vr_mc_rays_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
-                                 const vr_prune_index* ix, const int32_t* cells, int64_t n_cells,
+                                 const vr_screen32* s32, const vr_prune_index* ix, const int32_t* cells, int64_t n_cells,
                                  int64_t rays_per_cell, const double* dirs, uint64_t seed,
                                  int32_t* out_idx, double* out_t, uint8_t* out_flag,
                                  int32_t* recheck_list, int32_t* recheck_count, uint64_t* work,
@@ -246,10 +247,12 @@ extern "C" int vr_mc_rays_pruned(const double* rec, int64_t n_gen, int d, double
     return VR_EINVAL;
   const int64_t n = n_cells * rays_per_cell;
   RayOut out{out_idx, out_t, nullptr, out_flag, recheck_list, recheck_count};
-  PrunedIndex pi{ix->rec, ix->perm, ix->inv_perm, ix->tile_box, ix->block_box, ix->n};
+  PrunedIndex pi{ix->rec, s32 ? ix->rec32 : nullptr, ix->perm, ix->inv_perm, ix->tile_box,
+                 ix->block_box, ix->n};
+  const Screen sc = make_screen(sqmax, s32, d);
   VR_DISPATCH_D(d, {
     SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n};
-    return launch_raycast_pruned<D>(src, n, pi, sqmax, out, as_stream(stream),
+    return launch_raycast_pruned<D>(src, n, pi, sc.fr, out, as_stream(stream),
                                     reinterpret_cast<unsigned long long*>(work));
   });
   return VR_OK;

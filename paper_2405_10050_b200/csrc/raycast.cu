@@ -27,13 +27,29 @@ extern "C" const char* vr_status_string(int status) {
   return "unknown status";
 }
 
+Screen vr::make_screen(double sqmax, const vr_screen32* s32, int d) {
+  Screen sc{};
+  sc.fr.sqmax = sqmax;
+  if (s32) {
+    sc.rec32 = s32->rec;
+    for (int k = 0; k < VR_MAX_D; ++k) sc.fr.c0[k] = k < d ? s32->center[k] : 0.0;
+    sc.fr.sqmax32 = s32->sqmax;
+  }
+  return sc;
+}
+
+extern "C" int vr_record32_stride(int d) {
+  if (d < VR_MIN_D || d > VR_MAX_D) return VR_EDIM;
+  return rec32_stride(d);
+}
+
 extern "C" int vr_record_stride(int d) {
   if (d < VR_MIN_D || d > VR_MAX_D) return VR_EDIM;
   return rec_stride(d);
 }
 
 extern "C" int vr_raycast_batch(const double* rec, int64_t n_gen, int d, double sqmax,
-                                const double* cand_rec, const int32_t* cand, int64_t n_cand,
+                                const vr_screen32* s32, const double* cand_rec, const int32_t* cand, int64_t n_cand,
                                 const double* x, const double* u, const int32_t* eta, int eta_len,
                                 int64_t n_rays, int32_t* out_idx, double* out_t, double* out_rp,
                                 uint8_t* out_flag, int32_t* recheck_list, int32_t* recheck_count,
@@ -47,7 +63,8 @@ extern "C" int vr_raycast_batch(const double* rec, int64_t n_gen, int d, double 
   RayOut out{out_idx, out_t, out_rp, out_flag, recheck_list, recheck_count};
   VR_DISPATCH_D(d, {
     SrcExplicit<D> src{x, u, eta, eta_len, rec, n_rays};
-    return launch_raycast<D>(src, n_rays, crec, cand, nc, sqmax, out, as_stream(stream));
+    return launch_raycast<D>(src, n_rays, crec, cand, nc, make_screen(sqmax, s32, d), out,
+                             as_stream(stream));
   });
   return VR_OK;
 }
@@ -71,7 +88,7 @@ extern "C" int vr_raycast_recheck(const double* rec, int64_t n_gen, int d, const
 }
 
 extern "C" int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
-                                 const vr_prune_index* ix, const double* x, const double* u,
+                                 const vr_screen32* s32, const vr_prune_index* ix, const double* x, const double* u,
                                  const int32_t* eta, int eta_len, int64_t n_rays,
                                  const int32_t* order, int32_t* out_idx, double* out_t,
                                  double* out_rp, uint8_t* out_flag, int32_t* recheck_list,
@@ -82,10 +99,12 @@ extern "C" int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double
   if (eta_len < 1 || eta_len > d || ix->n != n_gen) return VR_EINVAL;
   if ((recheck_list == nullptr) != (recheck_count == nullptr)) return VR_EINVAL;
   RayOut out{out_idx, out_t, out_rp, out_flag, recheck_list, recheck_count};
-  PrunedIndex pi{ix->rec, ix->perm, ix->inv_perm, ix->tile_box, ix->block_box, ix->n};
+  PrunedIndex pi{ix->rec, s32 ? ix->rec32 : nullptr, ix->perm, ix->inv_perm, ix->tile_box,
+                 ix->block_box, ix->n};
+  const Screen sc = make_screen(sqmax, s32, d);
   VR_DISPATCH_D(d, {
     SrcExplicit<D> src{x, u, eta, eta_len, rec, n_rays, order};
-    return launch_raycast_pruned<D>(src, n_rays, pi, sqmax, out, as_stream(stream),
+    return launch_raycast_pruned<D>(src, n_rays, pi, sc.fr, out, as_stream(stream),
                                     reinterpret_cast<unsigned long long*>(work));
   });
   return VR_OK;

@@ -27,6 +27,14 @@
 
 namespace vr {
 
+// Screening frame: fp64 max |x|^2 for the fp64 rounding bound, and the
+// centred fp32 copy's centre / max |x - c|^2 for the fp32 screen's bound.
+struct Frame {
+  double sqmax;
+  double c0[VR_MAX_D];
+  double sqmax32;
+};
+
 // Candidate records as seen by the kernel: `rec` packed [x, |x|^2, pad].
 template <int D>
 struct RayState {
@@ -42,6 +50,8 @@ struct RayState {
   double tb;    // current best t
   double denb;  // u.(x_best - x_g) of the current best
   double rho2;  // radius^2 of the current sphere (+inf before the first hit)
+  float z32[D]; // -2 (z - c0) in fp32 (fp32 screen, centred frame)
+  float hi32;   // fp32 screening bound, rounded up, incl. the fp32 error bound
   int ib;       // current best (local candidate index), -1 = none
   int near;     // 1 -> needs exact re-check
 };
@@ -78,6 +88,9 @@ __device__ __forceinline__ void ray_setup(RayState<D>& r, const double* __restri
 #pragma unroll
   for (int k = 0; k < D; ++k) r.z[k] = -2.0 * r.x[k];
   r.hi = CUDART_INF;
+  r.hi32 = CUDART_INF_F;
+#pragma unroll
+  for (int k = 0; k < D; ++k) r.z32[k] = 0.0f;
   r.lim = CUDART_INF;
   r.dlt = 0.0;
   r.tb = CUDART_INF;
@@ -90,7 +103,8 @@ __device__ __forceinline__ void ray_setup(RayState<D>& r, const double* __restri
 // Move the screening sphere to the new best crossing t.
 template <int D>
 __device__ __forceinline__ void ray_set_best(RayState<D>& r, double t, double den, int i,
-                                             double sqmax) {
+                                             const Frame& fr) {
+  const double sqmax = fr.sqmax;
   double zz = 0.0, xx = 0.0;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -114,6 +128,18 @@ __device__ __forceinline__ void ray_set_best(RayState<D>& r, double t, double de
   r.denb = den;
   r.rho2 = rho2;
   r.ib = i;
+  // fp32 screen in the centred frame: |x~|^2 - 2 z~.x~ < rho^2 - |z~|^2 + dlt
+  // (+ a bound on the fp32 evaluation error, rounded up), z~ = z - c0.
+  double zt2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const double zt = -0.5 * r.z[k] - fr.c0[k];
+    r.z32[k] = (float)(-2.0 * zt);
+    zt2 = fma(zt, zt, zt2);
+  }
+  const double e32 = 2.0 * (D + 4) * 5.960464477539063e-08 *
+                     (fr.sqmax32 + 2.0 * sqrt(zt2 * fr.sqmax32) + 1e-30);
+  r.hi32 = __double2float_ru(rho2 - zt2 + dlt + e32);
 }
 
 // Rare path: candidate i passed the (possibly stale) screening bound.  The
@@ -121,7 +147,7 @@ __device__ __forceinline__ void ray_set_best(RayState<D>& r, double t, double de
 // candidate of the same unrolled step may have moved the sphere.
 template <int D>
 __device__ __forceinline__ void ray_rare(RayState<D>& r, const double (&xi)[D], double sq, int i,
-                                         double sqmax) {
+                                         const Frame& fr) {
   double fp = sq, q = 0.0;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -143,7 +169,7 @@ __device__ __forceinline__ void ray_rare(RayState<D>& r, const double (&xi)[D], 
   const double den = q - r.s;
   const double t = (aa - r.base) / (2.0 * den);
   const double told = r.tb, denold = r.denb;
-  ray_set_best<D>(r, t, den, i, sqmax);
+  ray_set_best<D>(r, t, den, i, fr);
   // power of the previous best w.r.t. the new sphere
   if (have && 2.0 * denold * (told - t) < r.dlt) r.near = 1;
 }
@@ -158,6 +184,27 @@ __device__ __forceinline__ void load_rec(const double* p, double (&xi)[D]) {
     xi[2 * k + 1] = v.y;
   }
   if (D & 1) xi[D - 1] = p[D - 1];
+}
+
+template <int D>
+__device__ __forceinline__ float ray_power32(const RayState<D>& r, const float (&xi)[D], float sq) {
+  float fp = sq;
+#pragma unroll
+  for (int k = 0; k < D; ++k) fp = fmaf(r.z32[k], xi[k], fp);
+  return fp;
+}
+
+template <int D>
+__device__ __forceinline__ void load_rec32(const float* p, float (&xi)[D]) {
+  const float4* p4 = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int k = 0; k < (D + 3) / 4; ++k) {
+    const float4 v = p4[k];
+    if (4 * k + 0 < D) xi[4 * k + 0] = v.x;
+    if (4 * k + 1 < D) xi[4 * k + 1] = v.y;
+    if (4 * k + 2 < D) xi[4 * k + 2] = v.z;
+    if (4 * k + 3 < D) xi[4 * k + 3] = v.w;
+  }
 }
 
 template <int D>
@@ -338,31 +385,103 @@ __device__ __forceinline__ void ray_store(const RayState<D>& r, int64_t k,
 }
 
 // ---------------------------------------------------------------------------
-// Main kernel: NT threads x R rays, generator tiles of TILE records through a
-// STAGES-deep TMA ring.
+// Screening of one tile (PT records) for the R rays of every lane: blocks of
+// U=8 candidates x R rays of independent dot products (fp32 in the centred
+// frame when F32, else fp64), per-ray bitmasks, one warp vote per block,
+// then the in-order fp64 rare path.  The screen is conservative (stale-safe:
+// a candidate outside an older sphere is outside every later one; the fp32
+// bound covers the fp32 evaluation error), and the fp64 rare path re-applies
+// the exact fp64 test first, so the result is independent of F32.
 // ---------------------------------------------------------------------------
-template <int D, int R, int NT, int TILE, int STAGES, int MINB, class Src>
-__global__ void __launch_bounds__(NT, MINB)
-    k_raycast(Src src, const double* __restrict__ crec, const int32_t* __restrict__ cand,
-              int64_t n_cand, double sqmax, RayOut out) {
+template <int D, int R, int PT, bool F32>
+__device__ __forceinline__ void screen_tile(RayState<D> (&ray)[R], const double* tile,
+                                            const float* tile32, int gbase, const Frame& fr) {
   constexpr int S = rec_stride(D);
-  constexpr int U = 8;  // candidates per screening block (one warp vote each)
+  constexpr int S32 = rec32_stride(D);
+  constexpr int U = 8;
+  for (int c = 0; c < PT; c += U) {
+    unsigned m[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) m[j] = 0u;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if constexpr (F32) {
+        float xi[D];
+        load_rec32<D>(tile32 + (c + u) * S32, xi);
+        const float sq = tile32[(c + u) * S32 + D];
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          m[j] |= (ray_power32<D>(ray[j], xi, sq) < ray[j].hi32) ? (1u << u) : 0u;
+      } else {
+        double xi[D];
+        load_rec<D>(tile + (c + u) * S, xi);
+        const double sq = tile[(c + u) * S + D];
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          m[j] |= (ray_power<D>(ray[j], xi, sq) < ray[j].hi) ? (1u << u) : 0u;
+      }
+    }
+    unsigned any = 0u;
+#pragma unroll
+    for (int j = 0; j < R; ++j) any |= m[j];
+    if (__any_sync(0xffffffffu, any != 0u)) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        unsigned mm = m[j];
+        while (mm) {
+          const int u = __ffs(mm) - 1;
+          mm &= mm - 1;
+          double xi[D];
+          load_rec<D>(tile + (c + u) * S, xi);
+          ray_rare<D>(ray[j], xi, tile[(c + u) * S + D], gbase + c + u, fr);
+        }
+      }
+    }
+  }
+}
+
+template <int D, int R>
+__device__ __forceinline__ void init_padding_lane(RayState<D>& r) {
+  r.hi = -CUDART_INF;
+  r.hi32 = -CUDART_INF_F;
+  r.thr = CUDART_INF;  // never needs a box
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    r.z[k] = 0.0;
+    r.z32[k] = 0.0f;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exhaustive kernel: NT threads x R rays; every generator tile goes through a
+// STAGES-deep shared-memory ring filled by TMA bulk copies (fp64 records, plus
+// the centred fp32 copy when F32); the last warp to release a stage issues
+// its refill.
+// ---------------------------------------------------------------------------
+template <int D, int R, int NT, int TILE, int STAGES, int MINB, bool F32, class Src>
+__global__ void __launch_bounds__(NT, MINB)
+    k_raycast(Src src, const double* __restrict__ crec, const float* __restrict__ crec32,
+              const int32_t* __restrict__ cand, int64_t n_cand, Frame fr, RayOut out) {
+  constexpr int S = rec_stride(D);
+  constexpr int S32 = rec32_stride(D);
   constexpr int NW = NT / 32;
-  static_assert(TILE % U == 0 && VR_REC_PAD % TILE == 0, "tile must divide the record padding");
+  static_assert(TILE % 8 == 0 && VR_REC_PAD % TILE == 0, "tile must divide the record padding");
+  constexpr uint32_t BYTES64 = (uint32_t)(TILE * S * sizeof(double));
+  constexpr uint32_t BYTES32 = F32 ? (uint32_t)(TILE * S32 * sizeof(float)) : 0u;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* tiles = reinterpret_cast<double*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)STAGES * TILE * S * sizeof(double));
+  float* tiles32 = reinterpret_cast<float*>(smem_raw + (size_t)STAGES * BYTES64);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)STAGES * (BYTES64 + BYTES32));
   int* released = reinterpret_cast<int*>(full + STAGES);
 
   const int tid = threadIdx.x, lane = tid & 31;
-  // the record array is padded to a multiple of VR_REC_PAD with sentinel
-  // rows [0.., +inf] that can never pass the screen: every tile is full
   const int64_t ntiles = (n_cand + TILE - 1) / TILE;
-  constexpr uint32_t TILE_BYTES = (uint32_t)(TILE * S * sizeof(double));
   auto issue = [&](int64_t t) {
     const int st = (int)(t % STAGES);
-    mbar_arrive_expect_tx(&full[st], TILE_BYTES);
-    bulk_g2s(tiles + (size_t)st * TILE * S, crec + t * TILE * S, TILE_BYTES, &full[st]);
+    mbar_arrive_expect_tx(&full[st], BYTES64 + BYTES32);
+    bulk_g2s(tiles + (size_t)st * TILE * S, crec + t * TILE * S, BYTES64, &full[st]);
+    if constexpr (F32)
+      bulk_g2s(tiles32 + (size_t)st * TILE * S32, crec32 + t * TILE * S32, BYTES32, &full[st]);
   };
   if (tid == 0) {
 #pragma unroll
@@ -383,51 +502,14 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     act[j] = src.load(k0 + (int64_t)j * NT, ray[j]);
-    if (!act[j]) {  // padding lane: never passes the screen
-      ray[j].hi = -CUDART_INF;
-#pragma unroll
-      for (int k = 0; k < D; ++k) ray[j].z[k] = 0.0;
-    }
+    if (!act[j]) init_padding_lane<D, R>(ray[j]);
   }
 
   for (int64_t t = 0; t < ntiles; ++t) {
     const int st = (int)(t % STAGES);
     mbar_wait(&full[st], (uint32_t)((t / STAGES) & 1));
-    const double* tile = tiles + (size_t)st * TILE * S;
-    const int gbase = (int)(t * TILE);
-    for (int c = 0; c < TILE; c += U) {
-      // Screening block: U candidates x R rays of independent dot products,
-      // stale-safe (a candidate outside an older sphere is outside every
-      // later one), then a single warp vote guards the in-order rare path.
-      unsigned m[R];
-#pragma unroll
-      for (int j = 0; j < R; ++j) m[j] = 0u;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        double xi[D];
-        load_rec<D>(tile + (c + u) * S, xi);
-        const double sq = tile[(c + u) * S + D];
-#pragma unroll
-        for (int j = 0; j < R; ++j)
-          m[j] |= (ray_power<D>(ray[j], xi, sq) < ray[j].hi) ? (1u << u) : 0u;
-      }
-      unsigned any = 0u;
-#pragma unroll
-      for (int j = 0; j < R; ++j) any |= m[j];
-      if (__any_sync(0xffffffffu, any != 0u)) {
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-          unsigned mm = m[j];
-          while (mm) {
-            const int u = __ffs(mm) - 1;
-            mm &= mm - 1;
-            double xi[D];
-            load_rec<D>(tile + (c + u) * S, xi);
-            ray_rare<D>(ray[j], xi, tile[(c + u) * S + D], gbase + c + u, sqmax);
-          }
-        }
-      }
-    }
+    screen_tile<D, R, TILE, F32>(ray, tiles + (size_t)st * TILE * S,
+                                 tiles32 + (size_t)st * TILE * S32, (int)(t * TILE), fr);
     // release the stage; the last warp to release it issues the refill
     __syncwarp();
     if (lane == 0) {
@@ -481,8 +563,8 @@ __device__ __forceinline__ bool ray_needs_box(const RayState<D>& r, const double
 template <int D, int R, int PT, int PB>
 struct TileCursor {
   int64_t ntiles, nblocks, st, sb;
-  int64_t bi = 0;      // blocks visited so far
-  int64_t ti = 0;      // tiles visited inside the current block
+  int64_t bi = 0;  // blocks visited so far
+  int64_t ti = 0;  // tiles visited inside the current block
   bool in_block = false;
   __device__ __forceinline__ int64_t next(const RayState<D> (&ray)[R],
                                           const double* __restrict__ tile_box,
@@ -515,57 +597,24 @@ struct TileCursor {
   }
 };
 
-template <int D, int R, int PT>
-__device__ __forceinline__ void screen_tile(RayState<D> (&ray)[R], const double* tile, int gbase,
-                                            double sqmax) {
-  constexpr int S = rec_stride(D);
-  constexpr int U = 8;
-  for (int c = 0; c < PT; c += U) {
-    unsigned m[R];
-#pragma unroll
-    for (int j = 0; j < R; ++j) m[j] = 0u;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      double xi[D];
-      load_rec<D>(tile + (c + u) * S, xi);
-      const double sq = tile[(c + u) * S + D];
-#pragma unroll
-      for (int j = 0; j < R; ++j)
-        m[j] |= (ray_power<D>(ray[j], xi, sq) < ray[j].hi) ? (1u << u) : 0u;
-    }
-    unsigned any = 0u;
-#pragma unroll
-    for (int j = 0; j < R; ++j) any |= m[j];
-    if (__any_sync(0xffffffffu, any != 0u)) {
-#pragma unroll
-      for (int j = 0; j < R; ++j) {
-        unsigned mm = m[j];
-        while (mm) {
-          const int u = __ffs(mm) - 1;
-          mm &= mm - 1;
-          double xi[D];
-          load_rec<D>(tile + (c + u) * S, xi);
-          ray_rare<D>(ray[j], xi, tile[(c + u) * S + D], gbase + c + u, sqmax);
-        }
-      }
-    }
-  }
-}
-
 // One warp per CTA (warps finish at very different times; a freed slot is
 // refilled immediately).  The warp's next needed tile is fetched by TMA into
 // the other half of a two-tile shared-memory buffer while the current tile
 // is screened; the need test is re-applied before screening (spheres shrink).
-template <int D, int R, int PT, int PB, int MINB, class Src>
+template <int D, int R, int PT, int PB, int MINB, bool F32, class Src>
 __global__ void __launch_bounds__(32, MINB)
-    k_raycast_pruned(Src src, const double* __restrict__ crec, const int32_t* __restrict__ perm,
-                     const int32_t* __restrict__ inv_perm, int64_t n_cand,
-                     const double* __restrict__ tile_box, const double* __restrict__ block_box,
-                     double sqmax, RayOut out, unsigned long long* __restrict__ work) {
+    k_raycast_pruned(Src src, const double* __restrict__ crec, const float* __restrict__ crec32,
+                     const int32_t* __restrict__ perm, const int32_t* __restrict__ inv_perm,
+                     int64_t n_cand, const double* __restrict__ tile_box,
+                     const double* __restrict__ block_box, Frame fr, RayOut out,
+                     unsigned long long* __restrict__ work) {
   constexpr int S = rec_stride(D);
-  constexpr uint32_t TILE_BYTES = (uint32_t)(PT * S * sizeof(double));
+  constexpr int S32 = rec32_stride(D);
+  constexpr uint32_t BYTES64 = (uint32_t)(PT * S * sizeof(double));
+  constexpr uint32_t BYTES32 = F32 ? (uint32_t)(PT * S32 * sizeof(float)) : 0u;
   static_assert(PT % 8 == 0 && VR_REC_PAD % PT == 0, "tile must divide the record padding");
   __shared__ __align__(128) double buf[2][PT * S];
+  __shared__ __align__(128) float buf32[2][F32 ? PT * S32 : 4];
   __shared__ uint64_t bar[2];
   const int lane = threadIdx.x;
   const int64_t k0 = (int64_t)blockIdx.x * 32 * R + lane;
@@ -575,12 +624,7 @@ __global__ void __launch_bounds__(32, MINB)
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     act[j] = src.load(k0 + (int64_t)j * 32, ray[j]);
-    if (!act[j]) {
-      ray[j].hi = -CUDART_INF;
-      ray[j].thr = CUDART_INF;  // never needs a box
-#pragma unroll
-      for (int k = 0; k < D; ++k) ray[j].z[k] = 0.0;
-    }
+    if (!act[j]) init_padding_lane<D, R>(ray[j]);
   }
   if (lane == 0) {
     mbar_init(&bar[0], 1);
@@ -600,8 +644,9 @@ __global__ void __launch_bounds__(32, MINB)
   auto issue = [&](int64_t t, int b) {
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect_tx(&bar[b], TILE_BYTES);
-      bulk_g2s(buf[b], crec + t * PT * S, TILE_BYTES, &bar[b]);
+      mbar_arrive_expect_tx(&bar[b], BYTES64 + BYTES32);
+      bulk_g2s(buf[b], crec + t * PT * S, BYTES64, &bar[b]);
+      if constexpr (F32) bulk_g2s(buf32[b], crec32 + t * PT * S32, BYTES32, &bar[b]);
     }
   };
   unsigned long long tiles_done = 0;
@@ -620,7 +665,7 @@ __global__ void __launch_bounds__(32, MINB)
     for (int j = 0; j < R; ++j) need |= ray_needs_box<D>(ray[j], tile_box + t * 2 * D);
     if (__any_sync(0xffffffffu, need)) {
       ++tiles_done;
-      screen_tile<D, R, PT>(ray, buf[b], (int)(t * PT), sqmax);
+      screen_tile<D, R, PT, F32>(ray, buf[b], buf32[b], (int)(t * PT), fr);
     }
     __syncwarp();
     b ^= 1;
@@ -740,8 +785,9 @@ struct RaycastCfgT {
   static constexpr int MINB = MINB_;
   static constexpr int TILE = 256;
   static constexpr int STAGES = 4;
-  static size_t smem() {
-    return (size_t)STAGES * TILE * rec_stride(D) * sizeof(double) +
+  static size_t smem(bool f32) {
+    return (size_t)STAGES * TILE *
+               (rec_stride(D) * sizeof(double) + (f32 ? rec32_stride(D) * sizeof(float) : 0)) +
            STAGES * (sizeof(uint64_t) + sizeof(int));
   }
 };
@@ -749,17 +795,26 @@ struct RaycastCfgT {
 template <int D>
 using RaycastCfg = RaycastCfgT<D, (D <= 3) ? 4 : 2, (D <= 3 || D >= 7) ? 2 : 3>;
 
-template <class C, int D, class Src>
+// Screening inputs shared by both kernels: fp32 centred records (nullable ->
+// fp64 screen) and the frame constants.
+struct Screen {
+  const float* rec32;  // records matching `crec` (same row order), or nullptr
+  Frame fr;
+};
+
+template <class C, int D, bool F32, class Src>
 int launch_raycast_cfg(const Src& src, int64_t n_rays, const double* crec, const int32_t* cand,
-                       int64_t n_cand, double sqmax, const RayOut& out, cudaStream_t st) {
-  auto kern = k_raycast<D, C::R, C::NT, C::TILE, C::STAGES, C::MINB, Src>;
-  const size_t sm = C::smem();
+                       int64_t n_cand, const Screen& sc, const RayOut& out, cudaStream_t st) {
+  auto kern = k_raycast<D, C::R, C::NT, C::TILE, C::STAGES, C::MINB, F32, Src>;
+  const size_t sm = C::smem(F32);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int64_t per_block = (int64_t)C::NT * C::R;
   const int64_t grid = (n_rays + per_block - 1) / per_block;
-  kern<<<(unsigned)grid, C::NT, sm, st>>>(src, crec, cand, n_cand, sqmax, out);
+  kern<<<(unsigned)grid, C::NT, sm, st>>>(src, crec, sc.rec32, cand, n_cand, sc.fr, out);
   VR_RETURN_LAUNCH();
 }
+
+Screen make_screen(double sqmax, const vr_screen32* s32, int d);
 
 // Tuning hook: VR_RAYCAST_VARIANT selects alternative register blockings
 // for d = 6 (the config-2 shape); 0 = default.
@@ -767,26 +822,21 @@ int raycast_variant();
 
 template <int D, class Src>
 int launch_raycast(const Src& src, int64_t n_rays, const double* crec, const int32_t* cand,
-                   int64_t n_cand, double sqmax, const RayOut& out, cudaStream_t st) {
+                   int64_t n_cand, const Screen& sc, const RayOut& out, cudaStream_t st) {
   if (n_rays <= 0) return VR_OK;
   if (n_cand <= 0) return VR_EINVAL;
   if (out.recheck_count) {  // the re-check list is rebuilt by every launch
     cudaError_t e = cudaMemsetAsync(out.recheck_count, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return vr_cuda_status(e);
   }
-  if constexpr (D == 6) {
-    switch (raycast_variant()) {
-      case 1: return launch_raycast_cfg<RaycastCfgT<D, 2, 1>, D>(src, n_rays, crec, cand, n_cand, sqmax, out, st);
-      case 2: return launch_raycast_cfg<RaycastCfgT<D, 3, 1>, D>(src, n_rays, crec, cand, n_cand, sqmax, out, st);
-      case 3: return launch_raycast_cfg<RaycastCfgT<D, 1, 4>, D>(src, n_rays, crec, cand, n_cand, sqmax, out, st);
-      default: break;
-    }
-  }
-  return launch_raycast_cfg<RaycastCfg<D>, D>(src, n_rays, crec, cand, n_cand, sqmax, out, st);
+  if (sc.rec32)
+    return launch_raycast_cfg<RaycastCfg<D>, D, true>(src, n_rays, crec, cand, n_cand, sc, out, st);
+  return launch_raycast_cfg<RaycastCfg<D>, D, false>(src, n_rays, crec, cand, n_cand, sc, out, st);
 }
 
 struct PrunedIndex {
   const double* crec;      // records in kd-order (padded)
+  const float* crec32;     // fp32 centred records in kd-order (nullable)
   const int32_t* perm;     // kd position -> generator index
   const int32_t* inv_perm; // generator index -> kd position
   const double* tile_box;  // ntiles x 2D
@@ -797,8 +847,21 @@ struct PrunedIndex {
 constexpr int PRUNE_TILE = 64;
 constexpr int PRUNE_BLOCK = 32;
 
+template <int D, bool F32, class Src>
+int launch_pruned_f(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
+                    const RayOut& out, cudaStream_t st, unsigned long long* work) {
+  constexpr int R = (D <= 3) ? 4 : 2;
+  constexpr int MINB = (D == 4) ? 12 : ((D == 6) ? 10 : 8);
+  const int64_t per_block = 32 * R;
+  const int64_t grid = (n_rays + per_block - 1) / per_block;
+  k_raycast_pruned<D, R, PRUNE_TILE, PRUNE_BLOCK, MINB, F32, Src><<<(unsigned)grid, 32, 0, st>>>(
+      src, ix.crec, ix.crec32, ix.perm, ix.inv_perm, ix.n, ix.tile_box, ix.block_box, fr, out,
+      work);
+  VR_RETURN_LAUNCH();
+}
+
 template <int D, class Src>
-int launch_raycast_pruned(const Src& src, int64_t n_rays, const PrunedIndex& ix, double sqmax,
+int launch_raycast_pruned(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
                           const RayOut& out, cudaStream_t st, unsigned long long* work) {
   if (n_rays <= 0) return VR_OK;
   if (ix.n <= 0) return VR_EINVAL;
@@ -806,13 +869,8 @@ int launch_raycast_pruned(const Src& src, int64_t n_rays, const PrunedIndex& ix,
     cudaError_t e = cudaMemsetAsync(out.recheck_count, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return vr_cuda_status(e);
   }
-  constexpr int R = (D <= 3) ? 4 : 2;
-  constexpr int MINB = (D == 4) ? 12 : ((D == 6) ? 10 : 8);
-  const int64_t per_block = 32 * R;
-  const int64_t grid = (n_rays + per_block - 1) / per_block;
-  k_raycast_pruned<D, R, PRUNE_TILE, PRUNE_BLOCK, MINB, Src><<<(unsigned)grid, 32, 0, st>>>(
-      src, ix.crec, ix.perm, ix.inv_perm, ix.n, ix.tile_box, ix.block_box, sqmax, out, work);
-  VR_RETURN_LAUNCH();
+  if (ix.crec32) return launch_pruned_f<D, true>(src, n_rays, ix, fr, out, st, work);
+  return launch_pruned_f<D, false>(src, n_rays, ix, fr, out, st, work);
 }
 
 template <int D, class Src>

@@ -29,7 +29,7 @@ import torch
 from . import _lib
 from .core import NodeSet
 from .errors import DegenerateConfiguration, UnboundedRay
-from .raycast import RaycastStats, Workspace, _use_pruned, candidate_records
+from .raycast import RaycastStats, Workspace, _screen, _use_pruned, candidate_records
 
 Integrand = Callable[[np.ndarray], float]
 
@@ -85,7 +85,7 @@ class MCResult:
 
 def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_faces=256,
                degenerate_is_error=True, want_samples=False, workspace=None, stats=None,
-               mode="auto"):
+               mode="auto", screen="fp32"):
     """Run rays + recheck + reduce for len(cells) cells x n rays; device tensors out."""
     rec, sqmax = ns.device_records()
     dev = rec.device
@@ -103,9 +103,11 @@ def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_fa
         dd = dd.to(device=dev, dtype=torch.float64).contiguous().view(total, d)
     cand = crec = None
     n_cand = 0
+    s32 = _screen(ns, dev, screen)
     if candidates is not None:
-        cand, crec = candidate_records(ns, candidates, dev)
+        cand, crec, s32 = candidate_records(ns, candidates, dev, screen)
         n_cand = cand.shape[0]
+    s32p = ctypes.byref(s32.struct) if s32 is not None else None
     idx = ws.get("mc_idx", (total,), torch.int32, dev)
     t = ws.get("mc_t", (total,), torch.float64, dev)
     flag = ws.get("mc_flag", (total,), torch.uint8, dev)
@@ -115,12 +117,12 @@ def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_fa
     seed = int(seed) & 0xFFFFFFFFFFFFFFFF
     if _use_pruned(ns, candidates, mode):
         ix = ns.prune_index(dev)
-        _lib.check(L.vr_mc_rays_pruned(_lib.ptr(rec), ns.n, d, sqmax, ctypes.byref(ix.struct),
+        _lib.check(L.vr_mc_rays_pruned(_lib.ptr(rec), ns.n, d, sqmax, s32p, ctypes.byref(ix.struct),
                                        _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed,
                                        _lib.ptr(idx), _lib.ptr(t), _lib.ptr(flag), _lib.ptr(rl),
                                        _lib.ptr(rc), None, sh), "vr_mc_rays_pruned")
     else:
-        _lib.check(L.vr_mc_rays(_lib.ptr(rec), ns.n, d, sqmax, _lib.ptr(crec), _lib.ptr(cand),
+        _lib.check(L.vr_mc_rays(_lib.ptr(rec), ns.n, d, sqmax, s32p, _lib.ptr(crec), _lib.ptr(cand),
                                 n_cand, _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed,
                                 _lib.ptr(idx), _lib.ptr(t), _lib.ptr(flag), _lib.ptr(rl),
                                 _lib.ptr(rc), sh), "vr_mc_rays")
@@ -162,7 +164,7 @@ def _collect(cells, out, want_samples):
 
 def mc_cells(ns: NodeSet, cells, n: int, seed: int = 0, max_faces: int = 256,
              want_samples=False, stats: RaycastStats = None, chunk_rays: int = 1 << 26,
-             mode="auto"):
+             mode="auto", screen="fp32"):
     """Batched device MC (Philox directions) over many cells.
 
     Returns an :class:`MCResult`; cells whose status is not CELL_OK are the
@@ -180,7 +182,7 @@ def mc_cells(ns: NodeSet, cells, n: int, seed: int = 0, max_faces: int = 256,
     for lo in range(0, len(cells), per_chunk):
         sub = cells[lo:lo + per_chunk]
         out = _mc_device(ns, sub, n, seed=seed, max_faces=max_faces, want_samples=want_samples,
-                         workspace=ws, stats=stats, mode=mode)
+                         workspace=ws, stats=stats, mode=mode, screen=screen)
         parts.append(_collect(sub, out, want_samples))
     if len(parts) == 1:
         return parts[0]

@@ -117,15 +117,26 @@ class Workspace:
         return t[:n].view(shape)
 
 
-def candidate_records(ns: NodeSet, candidates, dev):
-    """Packed records of a candidate subset (raycast.py:100-102)."""
+def candidate_records(ns: NodeSet, candidates, dev, screen="fp64"):
+    """Packed records of a candidate subset (raycast.py:100-102); with
+    screen="fp32" also the matching centred fp32 rows (vr_screen32 struct)."""
     rec, _ = ns.device_records(dev)
     cand = _as_dev(np.asarray(candidates, dtype=np.int64).ravel(), dev, torch.int64)
     m = cand.shape[0]
     crec = torch.zeros((_lib.record_rows(m), rec.shape[1]), dtype=rec.dtype, device=dev)
     crec[:, ns.dim] = float("inf")  # sentinel rows (include/voronray_b200.h)
     crec[:m] = rec.index_select(0, cand)
-    return cand.to(torch.int32).contiguous(), crec
+    s32 = None
+    if screen == "fp32":
+        from .core import Screen32
+        s32 = Screen32(crec, m, ns.dim, center=ns.screen32(dev).center)
+    return cand.to(torch.int32).contiguous(), crec, s32
+
+
+def _screen(ns, dev, screen):
+    if screen not in ("fp32", "fp64"):
+        raise ValueError(f"unknown screen {screen!r}")
+    return ns.screen32(dev) if screen == "fp32" else None
 
 
 PRUNE_MIN_GENERATORS = 1024
@@ -141,7 +152,7 @@ def _use_pruned(ns, candidates, mode):
 
 def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=None,
                   workspace=None, out=None, stream=None, events=None,
-                  mode="auto", work=None) -> RaycastBatch:
+                  mode="auto", work=None, screen="fp32") -> RaycastBatch:
     """Batched incircle RayCast on the current CUDA device.
 
     Args:
@@ -160,6 +171,9 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
             "auto" prunes when N >= 1024 and no candidate subset is given.
         work: optional int64 device tensor (1,) accumulating the pairs the
             pruned kernel screened (roofline accounting).
+        screen: "fp32" screens pairs in fp32 (centred frame, rigorous bound)
+            and re-checks survivors in fp64; "fp64" screens in fp64.  The
+            results are identical (tests/test_raycast_gpu.py).
 
     Stream-ordered; no host synchronisation.
     """
@@ -193,11 +207,13 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
         return RaycastBatch(idx, t, rp, flag)
     cand = crec = None
     n_cand = 0
+    s32 = _screen(ns, dev, screen)
     if candidates is not None:
-        cand, crec = candidate_records(ns, candidates, dev)
+        cand, crec, s32 = candidate_records(ns, candidates, dev, screen)
         n_cand = cand.shape[0]
         if n_cand == 0:
             raise ValueError("empty candidate set")
+    s32p = ctypes.byref(s32.struct) if s32 is not None else None
     rl = ws.get("recheck_list", (n,), torch.int32, dev)
     rc = ws.get("recheck_count", (1,), torch.int32, dev)
     sh = _lib.stream_handle(stream)
@@ -211,13 +227,13 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
             # warp-coherent processing order: rays sorted by the kd position of eta[0]
             key = ix.inv_perm.index_select(0, ed[:, 0].to(torch.int64))
             order = torch.sort(key, stable=True).indices.to(torch.int32)
-        _lib.check(L.vr_raycast_pruned(_lib.ptr(rec), ns.n, d, sqmax, ctypes.byref(ix.struct),
+        _lib.check(L.vr_raycast_pruned(_lib.ptr(rec), ns.n, d, sqmax, s32p, ctypes.byref(ix.struct),
                                        _lib.ptr(xd), _lib.ptr(ud), _lib.ptr(ed), k, n,
                                        _lib.ptr(order), _lib.ptr(idx), _lib.ptr(t),
                                        _lib.ptr(rp), _lib.ptr(flag), _lib.ptr(rl), _lib.ptr(rc),
                                        _lib.ptr(work), sh), "vr_raycast_pruned")
     else:
-        _lib.check(L.vr_raycast_batch(_lib.ptr(rec), ns.n, d, sqmax, _lib.ptr(crec),
+        _lib.check(L.vr_raycast_batch(_lib.ptr(rec), ns.n, d, sqmax, s32p, _lib.ptr(crec),
                                       _lib.ptr(cand), n_cand, _lib.ptr(xd), _lib.ptr(ud),
                                       _lib.ptr(ed), k, n, _lib.ptr(idx), _lib.ptr(t),
                                       _lib.ptr(rp), _lib.ptr(flag), _lib.ptr(rl), _lib.ptr(rc),
@@ -231,6 +247,113 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
     if events is not None:
         events[2].record(stream)
     return RaycastBatch(idx, t, rp, flag)
+
+
+def raycast_incircle(ns: NodeSet, q: RayQuery, stats: RaycastStats = None,
+                     heuristic: bool = True, candidates=None):
+    """Exact first Voronoi object hit by the ray, or None if it escapes.
+
+    Drop-in for raycast.py:154-224: returns ``(tuple(sorted(eta + (i,))), rp)``
+    or ``None``; raises :class:`DegenerateConfiguration` when a foreign
+    generator lies within the reference's 1e-10 band of the circumsphere.
+    ``heuristic`` is result-neutral in the reference and ignored here.
+    """
+    if stats is None:
+        stats = RaycastStats()
+    eta = tuple(int(e) for e in q.eta)
+    res = raycast_batch(ns, np.asarray(q.r, dtype=float)[None], np.asarray(q.u, dtype=float)[None],
+                        np.asarray([eta], dtype=np.int32), candidates=candidates, stats=stats)
+    idx, _, rp, flag = res.to_host()
+    f = int(flag[0])
+    if f == RAY_ESCAPED:
+        return None
+    if f == RAY_DEGENERATE:
+        raise DegenerateConfiguration(
+            f"a foreign generator lies on the circumsphere of {(*eta, int(idx[0]))}")
+    return tuple(sorted((*eta, int(idx[0])))), rp[0]
+
+
+# --- host-side direction helpers (raycast.py:295-378) ----------------------
+
+def _orthonormal_rows(diffs):
+    """Modified Gram-Schmidt, two passes (raycast.py:295-308)."""
+    out = []
+    for row in np.atleast_2d(diffs) if len(diffs) else []:
+        v = np.array(row, dtype=float)
+        norm0 = math.sqrt(float(v @ v))
+        for _ in range(2):
+            for qv in out:
+                v -= (qv @ v) * qv
+        norm = math.sqrt(float(v @ v))
+        if norm < RANK_TOL * max(norm0, 1.0):
+            raise DegenerateConfiguration("generators are affinely dependent")
+        out.append(v / norm)
+    return out
+
+
+def _project_out(w, basis):
+    """Component of ``w`` orthogonal to orthonormal rows (raycast.py:311-317)."""
+    v = np.array(w, dtype=float)
+    for _ in range(2):
+        for qv in basis:
+            v -= (qv @ v) * qv
+    return v
+
+
+def _search_direction(pts, eta, missing):
+    sub = pts[list(eta)]
+    basis = _orthonormal_rows(sub[1:] - sub[0]) if len(eta) > 1 else []
+    w = sub.sum(axis=0) * (1.0 / len(eta)) - pts[missing]
+    v = _project_out(w, basis)
+    norm = math.sqrt(float(v @ v))
+    if norm < RANK_TOL * max(math.sqrt(float(w @ w)), 1.0):
+        raise DegenerateConfiguration(f"generator {missing} lies in the affine span of {eta}")
+    return v / norm
+
+
+def search_direction(ns: NodeSet, sigma, eta):
+    """Outward direction of edge ``eta`` of vertex ``sigma`` (raycast.py:320-342)."""
+    extra = set(sigma) - set(eta)
+    if len(extra) != 1 or not set(eta) <= set(sigma):
+        raise ValueError("eta must be sigma minus exactly one generator")
+    return _search_direction(ns.points, tuple(eta), extra.pop())
+
+
+def vertex_directions_batch(ns: NodeSet, sigma):
+    """All d+1 edge directions of many vertices on the GPU (vr_vertex_directions).
+
+    Returns (u (V, d+1, d) device tensor, ok (V, d+1) uint8 device tensor)."""
+    rec, _ = ns.device_records()
+    dev = rec.device
+    L = _lib.lib()
+    sd = _as_dev(np.asarray(sigma), dev, torch.int32).view(-1, ns.dim + 1)
+    nv = sd.shape[0]
+    u = torch.empty((nv, ns.dim + 1, ns.dim), dtype=torch.float64, device=dev)
+    ok = torch.empty((nv, ns.dim + 1), dtype=torch.uint8, device=dev)
+    _lib.check(L.vr_vertex_directions(_lib.ptr(rec), ns.dim, _lib.ptr(sd), nv, _lib.ptr(u),
+                                      _lib.ptr(ok), _lib.stream_handle()), "vr_vertex_directions")
+    return u, ok
+
+
+def _vertex_directions(pts, sigma, positions):
+    """Outward directions for several edges of one vertex (raycast.py:345-378).
+
+    Host fp64 inverse with the reference's column convention; the traversal
+    itself uses the batched device kernel (vr_vertex_directions)."""
+    sub = pts[list(sigma)]
+    diffs = sub[1:] - sub[0]
+    try:
+        inv = np.linalg.inv(diffs)
+    except np.linalg.LinAlgError:
+        raise DegenerateConfiguration(f"generators of {sigma} are affinely dependent") from None
+    out = {}
+    for k in positions:
+        v = inv.sum(axis=1) if k == 0 else -inv[:, k - 1]
+        norm = math.sqrt(float(v @ v))
+        if not norm > 0.0 or not math.isfinite(norm):
+            raise DegenerateConfiguration(f"generators of {sigma} are affinely dependent")
+        out[k] = v / norm
+    return out
 
 
 class HostRaycaster:

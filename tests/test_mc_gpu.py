@@ -135,10 +135,13 @@ def test_mc_pruned_equals_exhaustive():
     pts = np.random.default_rng(0).random((100000, 4))
     ns = vb.NodeSet(pts)
     cells = np.random.default_rng(9).choice(100000, 300, replace=False)
-    a = vb.mc_cells(ns, cells, 500, seed=3, mode="exhaustive", want_samples=True)
-    b = vb.mc_cells(ns, cells, 500, seed=3, mode="pruned", want_samples=True)
-    for f in ("volume", "face_offsets", "face_j", "face_area", "status", "first_bad", "samples"):
-        assert np.array_equal(getattr(a, f), getattr(b, f), equal_nan=True), f
+    a = vb.mc_cells(ns, cells, 500, seed=3, mode="exhaustive", want_samples=True, screen="fp64")
+    for mode in ("exhaustive", "pruned"):
+        for screen in ("fp64", "fp32"):
+            b = vb.mc_cells(ns, cells, 500, seed=3, mode=mode, want_samples=True, screen=screen)
+            for f in ("volume", "face_offsets", "face_j", "face_area", "status", "first_bad",
+                      "samples"):
+                assert np.array_equal(getattr(a, f), getattr(b, f), equal_nan=True), (f, mode)
 
 
 def test_config4_subset_vs_exact_volumes():

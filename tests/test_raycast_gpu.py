@@ -211,17 +211,21 @@ def test_pruned_equals_exhaustive(d):
     g = rng.integers(0, n, m)
     u = rng.standard_normal((m, d))
     u /= np.linalg.norm(u, axis=1, keepdims=True)
-    a = vb.raycast_batch(ns, pts[g], u, g[:, None], mode="exhaustive").to_host()
-    b = vb.raycast_batch(ns, pts[g], u, g[:, None], mode="pruned").to_host()
-    for x, y in zip(a, b):
-        assert np.array_equal(x, y, equal_nan=True)
+    a = vb.raycast_batch(ns, pts[g], u, g[:, None], mode="exhaustive", screen="fp64").to_host()
+    for mode in ("exhaustive", "pruned"):
+        for screen in ("fp64", "fp32"):
+            b = vb.raycast_batch(ns, pts[g], u, g[:, None], mode=mode, screen=screen).to_host()
+            for x, y in zip(a, b):
+                assert np.array_equal(x, y, equal_nan=True), (mode, screen)
     # edge rays with |eta| = d from descent vertices
     sig, r = vb.descent_batch(ns, rng.choice(n, 200, replace=False), seed=1)
     uu, ok = vb.vertex_directions_batch(ns, sig)
     uu = uu.cpu().numpy().reshape(-1, d)
     xs = np.repeat(r, d + 1, axis=0)
     eta = np.array([[s[j] for j in range(d + 1) if j != k] for s in sig for k in range(d + 1)])
-    a = vb.raycast_batch(ns, xs, uu, eta, mode="exhaustive").to_host()
-    b = vb.raycast_batch(ns, xs, uu, eta, mode="pruned").to_host()
-    for x, y in zip(a, b):
-        assert np.array_equal(x, y, equal_nan=True)
+    a = vb.raycast_batch(ns, xs, uu, eta, mode="exhaustive", screen="fp64").to_host()
+    for mode in ("exhaustive", "pruned"):
+        for screen in ("fp64", "fp32"):
+            b = vb.raycast_batch(ns, xs, uu, eta, mode=mode, screen=screen).to_host()
+            for x, y in zip(a, b):
+                assert np.array_equal(x, y, equal_nan=True), (mode, screen)
