@@ -83,6 +83,7 @@ typedef struct vr_screen32 {
   const float* rec;
   double center[8];
   double sqmax;
+  double bound;   /* max_k |x_k - center_k| over the generators */
 } vr_screen32;
 
 int vr_record32_stride(int d);
@@ -139,6 +140,9 @@ typedef struct vr_prune_index {
   const int32_t* inv_perm; /* generator index -> kd position (n)               */
   const double* tile_box;  /* ceil(n/64) x 2d, [lo_0..lo_{d-1}, hi_0..]        */
   const double* block_box; /* ceil(ceil(n/64)/32) x 2d                         */
+  const float* tile_box32; /* same boxes, centred at vr_screen32.center, fp32
+                              rounded outward (lo down, hi up); nullable     */
+  const float* block_box32;
   int64_t n;
 } vr_prune_index;
 

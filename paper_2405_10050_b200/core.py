@@ -168,7 +168,7 @@ PRUNE_TILE, PRUNE_BLOCK = 64, 32
 
 class _Screen32Struct(ctypes.Structure):
     _fields_ = [("rec", ctypes.c_void_p), ("center", ctypes.c_double * 8),
-                ("sqmax", ctypes.c_double)]
+                ("sqmax", ctypes.c_double), ("bound", ctypes.c_double)]
 
 
 class Screen32:
@@ -182,6 +182,7 @@ class Screen32:
             center = 0.5 * (pts.amin(0) + pts.amax(0))
         self.center = center.to(torch.float64).contiguous()
         self.sqmax = float(((pts - self.center) ** 2).sum(1).max().item())
+        self.bound = float((pts - self.center).abs().max().item())
         s32 = (d + 4) & ~3
         self.rec = torch.empty((rec.shape[0], s32), dtype=torch.float32, device=dev)
         _lib.check(L.vr_pack_records32(_lib.ptr(rec), rec.shape[0], d, _lib.ptr(self.center),
@@ -189,13 +190,15 @@ class Screen32:
                    "vr_pack_records32")
         c = [0.0] * 8
         c[:d] = self.center.cpu().tolist()
-        self.struct = _Screen32Struct(self.rec.data_ptr(), (ctypes.c_double * 8)(*c), self.sqmax)
+        self.struct = _Screen32Struct(self.rec.data_ptr(), (ctypes.c_double * 8)(*c), self.sqmax,
+                                      self.bound)
 
 
 class _PruneStruct(ctypes.Structure):
     _fields_ = [("rec", ctypes.c_void_p), ("rec32", ctypes.c_void_p), ("perm", ctypes.c_void_p),
                 ("inv_perm", ctypes.c_void_p), ("tile_box", ctypes.c_void_p),
-                ("block_box", ctypes.c_void_p), ("n", ctypes.c_int64)]
+                ("block_box", ctypes.c_void_p), ("tile_box32", ctypes.c_void_p),
+                ("block_box32", ctypes.c_void_p), ("n", ctypes.c_int64)]
 
 
 def kd_order(P, tile=PRUNE_TILE):
@@ -242,6 +245,18 @@ def kd_order(P, tile=PRUNE_TILE):
     return order
 
 
+def _outward32(lo, hi, center):
+    """fp32 copy of fp64 boxes in the centred frame, rounded outward so the
+    fp32 box contains the fp64 one (lo rounded down, hi rounded up)."""
+    lo_c, hi_c = lo - center, hi - center
+    lo32, hi32 = lo_c.to(torch.float32), hi_c.to(torch.float32)
+    ninf = torch.full_like(lo32, float("-inf"))
+    pinf = torch.full_like(hi32, float("inf"))
+    lo32 = torch.where(lo32.to(torch.float64) > lo_c, torch.nextafter(lo32, ninf), lo32)
+    hi32 = torch.where(hi32.to(torch.float64) < hi_c, torch.nextafter(hi32, pinf), hi32)
+    return torch.cat([lo32, hi32], 1).contiguous()
+
+
 class PruneIndex:
     """Device tensors of one vr_prune_index."""
 
@@ -272,9 +287,12 @@ class PruneIndex:
         self.n = n
         self.rows = rows
         self.screen32 = Screen32(crec, n, d, center=center)
+        self.tile_box32 = _outward32(lo, hi, self.screen32.center)
+        self.block_box32 = _outward32(blo, bhi, self.screen32.center)
         p = lambda t: t.data_ptr()  # noqa: E731
         self.struct = _PruneStruct(p(crec), p(self.screen32.rec), p(self.perm), p(self.inv_perm),
-                                   p(self.tile_box), p(self.block_box), n)
+                                   p(self.tile_box), p(self.block_box), p(self.tile_box32),
+                                   p(self.block_box32), n)
 
 
 def build_node_set(points, backend="auto"):

@@ -34,6 +34,7 @@ Screen vr::make_screen(double sqmax, const vr_screen32* s32, int d) {
     sc.rec32 = s32->rec;
     for (int k = 0; k < VR_MAX_D; ++k) sc.fr.c0[k] = k < d ? s32->center[k] : 0.0;
     sc.fr.sqmax32 = s32->sqmax;
+    sc.fr.bnd32 = s32->bound;
   }
   return sc;
 }
@@ -100,7 +101,7 @@ extern "C" int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double
   if ((recheck_list == nullptr) != (recheck_count == nullptr)) return VR_EINVAL;
   RayOut out{out_idx, out_t, out_rp, out_flag, recheck_list, recheck_count};
   PrunedIndex pi{ix->rec, s32 ? ix->rec32 : nullptr, ix->perm, ix->inv_perm, ix->tile_box,
-                 ix->block_box, ix->n};
+                 ix->block_box, ix->tile_box32, ix->block_box32, ix->n};
   const Screen sc = make_screen(sqmax, s32, d);
   VR_DISPATCH_D(d, {
     SrcExplicit<D> src{x, u, eta, eta_len, rec, n_rays, order};

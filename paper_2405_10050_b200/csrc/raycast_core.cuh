@@ -33,6 +33,7 @@ struct Frame {
   double sqmax;
   double c0[VR_MAX_D];
   double sqmax32;
+  double bnd32;  // max |x_k - c0_k| over generators (fp32 box-test slack)
 };
 
 // Candidate records as seen by the kernel: `rec` packed [x, |x|^2, pad].
@@ -52,8 +53,14 @@ struct RayState {
   double rho2;  // radius^2 of the current sphere (+inf before the first hit)
   float z32[D]; // -2 (z - c0) in fp32 (fp32 screen, centred frame)
   float hi32;   // fp32 screening bound, rounded up, incl. the fp32 error bound
+  float u32[D]; // fp32 direction (fp32 box tests)
+  float thr32;  // centred halfspace threshold thr - u.c0, rounded down
+  float bsl32;  // slack of the fp32 halfspace bound
+  float del32;  // slack of the fp32 box distance (centre rounding)
+  float rb32;   // (rho^2 + dlt) rounded up with the fp32 sum slack (+inf: none)
   int ib;       // current best (local candidate index), -1 = none
   int near;     // 1 -> needs exact re-check
+  int nupd;     // sphere updates (work accounting)
 };
 
 // Fill the per-ray constants from origin x, direction u and the eta
@@ -61,7 +68,7 @@ struct RayState {
 // and raycast_incircle's loop constants (raycast.py:178,186-189).
 template <int D>
 __device__ __forceinline__ void ray_setup(RayState<D>& r, const double* __restrict__ grec,
-                                          const int32_t* eta, int eta_len) {
+                                          const int32_t* eta, int eta_len, const Frame& fr) {
   constexpr int S = rec_stride(D);
   const double* xg = grec + (int64_t)eta[0] * S;
   double thr = 0.0;
@@ -98,20 +105,37 @@ __device__ __forceinline__ void ray_setup(RayState<D>& r, const double* __restri
   r.rho2 = CUDART_INF;
   r.ib = -1;
   r.near = 0;
+  r.nupd = 0;
+  // fp32 box-test constants (centred frame)
+  double uc = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    r.u32[k] = (float)r.u[k];
+    uc = fma(r.u[k], fr.c0[k], uc);
+  }
+  const double thr_c = r.thr - uc;
+  r.thr32 = __double2float_rd(thr_c - 1e-12 * (fabs(thr_c) + fabs(uc) + 1.0));
+  r.bsl32 = __double2float_ru((D + 4) * 2.384185791015625e-07 * sqrt((double)D) * fr.bnd32 + 1e-30);
+  r.del32 = 0.0f;
+  r.rb32 = CUDART_INF_F;
 }
 
 // Move the screening sphere to the new best crossing t.
-template <int D>
+template <int D, bool F32>
 __device__ __forceinline__ void ray_set_best(RayState<D>& r, double t, double den, int i,
                                              const Frame& fr) {
   const double sqmax = fr.sqmax;
-  double zz = 0.0, xx = 0.0;
+  double zz = 0.0, xx = 0.0, zt2 = 0.0, ztmax = 0.0;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    const double zk = fma(t, r.u[k], r.x[k]);
-    r.z[k] = -2.0 * zk;
+    const double zk = fma(t, r.u[k], r.x[k]);  // recomputed bitwise-identically in ray_rare
+    if constexpr (!F32) r.z[k] = -2.0 * zk;
     zz = fma(zk, zk, zz);
     xx = fma(r.x[k], r.x[k], xx);
+    const double zt = zk - fr.c0[k];
+    r.z32[k] = (float)(-2.0 * zt);
+    zt2 = fma(zt, zt, zt2);
+    ztmax = fmax(ztmax, fabs(zt));
   }
   // Every term of `scale` (and the band) is non-increasing as t decreases
   // (|z(t)|^2 and rho^2(t) are convex in t), so a verdict taken against an
@@ -128,33 +152,34 @@ __device__ __forceinline__ void ray_set_best(RayState<D>& r, double t, double de
   r.denb = den;
   r.rho2 = rho2;
   r.ib = i;
+  ++r.nupd;
   // fp32 screen in the centred frame: |x~|^2 - 2 z~.x~ < rho^2 - |z~|^2 + dlt
   // (+ a bound on the fp32 evaluation error, rounded up), z~ = z - c0.
-  double zt2 = 0.0;
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    const double zt = -0.5 * r.z[k] - fr.c0[k];
-    r.z32[k] = (float)(-2.0 * zt);
-    zt2 = fma(zt, zt, zt2);
-  }
   const double e32 = 2.0 * (D + 4) * 5.960464477539063e-08 *
                      (fr.sqmax32 + 2.0 * sqrt(zt2 * fr.sqmax32) + 1e-30);
   r.hi32 = __double2float_ru(rho2 - zt2 + dlt + e32);
+  // fp32 box test: |e32_k - e_k| <= 2^-22 (|z~|_inf + B); sum slack relative
+  r.del32 = __double2float_ru(2.384185791015625e-07 * (ztmax + fr.bnd32));
+  r.rb32 = __double2float_ru((rho2 + dlt) * (1.0 + (D + 4) * 1.1920928955078125e-07));
 }
 
 // Rare path: candidate i passed the (possibly stale) screening bound.  The
 // power w.r.t. the CURRENT sphere is recomputed first, because an earlier
 // candidate of the same unrolled step may have moved the sphere.
-template <int D>
+template <int D, bool F32>
 __device__ __forceinline__ void ray_rare(RayState<D>& r, const double (&xi)[D], double sq, int i,
                                          const Frame& fr) {
   double fp = sq, q = 0.0;
+  const bool have0 = r.ib >= 0;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    fp = fma(r.z[k], xi[k], fp);
+    // fp32-screen kernels keep no fp64 z: rebuild it exactly as set_best did
+    const double zk2 = F32 ? (have0 ? -2.0 * fma(r.tb, r.u[k], r.x[k]) : 0.0) : r.z[k];
+    fp = fma(zk2, xi[k], fp);
     q = fma(r.u[k], xi[k], q);
   }
-  if (!(fp < r.hi)) return;  // outside the current sphere's band
+  if (have0 && !(fp < r.hi)) return;  // outside the current sphere's band
+  if (i == r.ib) return;     // the current best itself (re-screened after a seed)
   if (!(q > r.thr)) return;  // outside the forward halfspace (raycast.py:110-117)
   const bool have = r.ib >= 0;
   if (have && fp >= r.lim - r.dlt) r.near = 1;
@@ -169,7 +194,7 @@ __device__ __forceinline__ void ray_rare(RayState<D>& r, const double (&xi)[D], 
   const double den = q - r.s;
   const double t = (aa - r.base) / (2.0 * den);
   const double told = r.tb, denold = r.denb;
-  ray_set_best<D>(r, t, den, i, fr);
+  ray_set_best<D, F32>(r, t, den, i, fr);
   // power of the previous best w.r.t. the new sphere
   if (have && 2.0 * denold * (told - t) < r.dlt) r.near = 1;
 }
@@ -245,7 +270,7 @@ struct SrcExplicit {
   const int32_t* order = nullptr;  // optional processing order (slot -> ray id)
   __device__ __forceinline__ int64_t id(int64_t k) const { return order ? order[k] : k; }
   __device__ __forceinline__ int32_t gen(int64_t k) const { return eta[id(k) * eta_len]; }
-  __device__ __forceinline__ bool load(int64_t k, RayState<D>& r) const {
+  __device__ __forceinline__ bool load(int64_t k, RayState<D>& r, const Frame& fr) const {
     if (k >= n) return false;
     k = id(k);
 #pragma unroll
@@ -253,7 +278,7 @@ struct SrcExplicit {
       r.x[j] = x[k * D + j];
       r.u[j] = u[k * D + j];
     }
-    ray_setup<D>(r, grec, eta + k * eta_len, eta_len);
+    ray_setup<D>(r, grec, eta + k * eta_len, eta_len, fr);
     return true;
   }
 };
@@ -330,14 +355,14 @@ struct SrcMC {
   }
   __device__ __forceinline__ int64_t id(int64_t k) const { return k; }
   __device__ __forceinline__ int32_t gen(int64_t k) const { return cells[k / per]; }
-  __device__ __forceinline__ bool load(int64_t k, RayState<D>& r) const {
+  __device__ __forceinline__ bool load(int64_t k, RayState<D>& r, const Frame& fr) const {
     if (k >= n) return false;
     const int32_t cell = cells[k / per];
     const double* xc = grec + (int64_t)cell * rec_stride(D);
 #pragma unroll
     for (int j = 0; j < D; ++j) r.x[j] = xc[j];
     direction(k, r.u);
-    ray_setup<D>(r, grec, &cell, 1);
+    ray_setup<D>(r, grec, &cell, 1, fr);
     return true;
   }
 };
@@ -393,9 +418,14 @@ __device__ __forceinline__ void ray_store(const RayState<D>& r, int64_t k,
 // bound covers the fp32 evaluation error), and the fp64 rare path re-applies
 // the exact fp64 test first, so the result is independent of F32.
 // ---------------------------------------------------------------------------
+struct WarpCounters {
+  unsigned long long rare_blocks = 0, rare_iters = 0, entries = 0;
+};
+
 template <int D, int R, int PT, bool F32>
 __device__ __forceinline__ void screen_tile(RayState<D> (&ray)[R], const double* tile,
-                                            const float* tile32, int gbase, const Frame& fr) {
+                                            const float* tile32, int gbase, const Frame& fr,
+                                            WarpCounters* wc = nullptr) {
   constexpr int S = rec_stride(D);
   constexpr int S32 = rec32_stride(D);
   constexpr int U = 8;
@@ -425,6 +455,14 @@ __device__ __forceinline__ void screen_tile(RayState<D> (&ray)[R], const double*
 #pragma unroll
     for (int j = 0; j < R; ++j) any |= m[j];
     if (__any_sync(0xffffffffu, any != 0u)) {
+      if (wc) {
+        ++wc->rare_blocks;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          wc->entries += __popc(m[j]);
+          wc->rare_iters += __reduce_max_sync(0xffffffffu, (unsigned)__popc(m[j]));
+        }
+      }
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         unsigned mm = m[j];
@@ -433,7 +471,7 @@ __device__ __forceinline__ void screen_tile(RayState<D> (&ray)[R], const double*
           mm &= mm - 1;
           double xi[D];
           load_rec<D>(tile + (c + u) * S, xi);
-          ray_rare<D>(ray[j], xi, tile[(c + u) * S + D], gbase + c + u, fr);
+          ray_rare<D, F32>(ray[j], xi, tile[(c + u) * S + D], gbase + c + u, fr);
         }
       }
     }
@@ -445,6 +483,10 @@ __device__ __forceinline__ void init_padding_lane(RayState<D>& r) {
   r.hi = -CUDART_INF;
   r.hi32 = -CUDART_INF_F;
   r.thr = CUDART_INF;  // never needs a box
+  r.thr32 = CUDART_INF_F;
+  r.bsl32 = 0.0f;
+#pragma unroll
+  for (int k = 0; k < D; ++k) r.u32[k] = 0.0f;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     r.z[k] = 0.0;
@@ -501,7 +543,7 @@ __global__ void __launch_bounds__(NT, MINB)
   const int64_t k0 = (int64_t)blockIdx.x * NT * R + tid;
 #pragma unroll
   for (int j = 0; j < R; ++j) {
-    act[j] = src.load(k0 + (int64_t)j * NT, ray[j]);
+    act[j] = src.load(k0 + (int64_t)j * NT, ray[j], fr);
     if (!act[j]) init_padding_lane<D, R>(ray[j]);
   }
 
@@ -557,10 +599,87 @@ __device__ __forceinline__ bool ray_needs_box(const RayState<D>& r, const double
   return d2 < r.rho2 + r.dlt + 1e-12 * (r.rho2 + d2);
 }
 
-// Cursor over the kd tiles in visiting order (cyclic from the warp's start
+// fp32 box test in the centred frame (boxes rounded outward on the host):
+// skip only if the fp32 bounds certify "behind the halfspace" or "outside the
+// sphere + band" for the exact box.  box32 = [lo_0..lo_{D-1}, hi_0..hi_{D-1}].
+template <int D>
+__device__ __forceinline__ bool ray_needs_box32(const RayState<D>& r,
+                                                const float* __restrict__ box) {
+  float lo[D], hi[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    lo[k] = __ldg(box + k);
+    hi[k] = __ldg(box + D + k);
+  }
+  float umax = 0.0f, d2 = 0.0f;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    umax = fmaf(r.u32[k], r.u32[k] > 0.0f ? hi[k] : lo[k], umax);
+    const float zc = -0.5f * r.z32[k];
+    const float e = fmaxf(fmaxf(lo[k] - zc, zc - hi[k]) - r.del32, 0.0f);
+    d2 = fmaf(e, e, d2);
+  }
+  if (umax + r.bsl32 <= r.thr32) return false;  // behind the forward halfspace
+  return !(d2 >= r.rb32);                        // inside sphere + band (or no sphere)
+}
+
+template <int D, bool F32>
+__device__ __forceinline__ bool ray_needs(const RayState<D>& r, const double* __restrict__ box64,
+                                          const float* __restrict__ box32, int64_t b) {
+  if constexpr (F32) return ray_needs_box32<D>(r, box32 + b * 2 * D);
+  else return ray_needs_box<D>(r, box64 + b * 2 * D);
+}
+
+// Seed pass: the valid candidate with the smallest t in one tile, found
+// without divergence (division-free comparison num_i den_b < num_b den_i,
+// den > 0), then one sphere update.  Purely an accelerator: the main scan
+// screens the seed tile again, so near-ties / rounding in the seed choice are
+// caught by the regular rare path (update or RECHECK flag).
+template <int D, int R, int PT, bool F32>
+__device__ __forceinline__ void seed_tile(RayState<D> (&ray)[R], const double* __restrict__ tile,
+                                          int gbase, const Frame& fr) {
+  constexpr int S = rec_stride(D);
+  double nb[R], db[R];
+  int ib[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    nb[j] = 1.0;
+    db[j] = 0.0;  // "t = +inf"
+    ib[j] = -1;
+  }
+#pragma unroll 2
+  for (int c = 0; c < PT; ++c) {
+    double xi[D];
+    load_rec_g<D>(tile + c * S, xi);
+    const bool real = !isinf(__ldg(tile + c * S + D));
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      double q = 0.0, aa = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        q = fma(ray[j].u[k], xi[k], q);
+        const double a = ray[j].x[k] - xi[k];
+        aa = fma(a, a, aa);
+      }
+      const double num = aa - ray[j].base, den = q - ray[j].s;
+      const bool better = real && q > ray[j].thr && num * db[j] < nb[j] * den;
+      nb[j] = better ? num : nb[j];
+      db[j] = better ? den : db[j];
+      ib[j] = better ? gbase + c : ib[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (ib[j] < 0) continue;
+    const double t = nb[j] / (2.0 * db[j]);
+    if (ray[j].ib < 0 || t < ray[j].tb) ray_set_best<D, F32>(ray[j], t, db[j], ib[j], fr);
+  }
+}
+
+// Cursor over the kd tiles in visiting order// Cursor over the kd tiles in visiting order (cyclic from the warp's start
 // tile), yielding only tiles whose block and tile boxes pass the warp-wide
 // need test against the rays' CURRENT spheres.
-template <int D, int R, int PT, int PB>
+template <int D, int R, int PT, int PB, bool F32>
 struct TileCursor {
   int64_t ntiles, nblocks, st, sb;
   int64_t bi = 0;  // blocks visited so far
@@ -568,14 +687,16 @@ struct TileCursor {
   bool in_block = false;
   __device__ __forceinline__ int64_t next(const RayState<D> (&ray)[R],
                                           const double* __restrict__ tile_box,
-                                          const double* __restrict__ block_box) {
+                                          const double* __restrict__ block_box,
+                                          const float* __restrict__ tile_box32,
+                                          const float* __restrict__ block_box32) {
     while (bi < nblocks) {
       const int64_t b = (sb + bi) % nblocks;
       const int64_t t_lo = b * PB, t_hi = min(ntiles, t_lo + PB);
       if (!in_block) {
         bool need = false;
 #pragma unroll
-        for (int j = 0; j < R; ++j) need |= ray_needs_box<D>(ray[j], block_box + b * 2 * D);
+        for (int j = 0; j < R; ++j) need |= ray_needs<D, F32>(ray[j], block_box, block_box32, b);
         if (!__any_sync(0xffffffffu, need)) { ++bi; continue; }
         in_block = true;
         ti = 0;
@@ -587,7 +708,7 @@ struct TileCursor {
         ++ti;
         bool need = false;
 #pragma unroll
-        for (int j = 0; j < R; ++j) need |= ray_needs_box<D>(ray[j], tile_box + t * 2 * D);
+        for (int j = 0; j < R; ++j) need |= ray_needs<D, F32>(ray[j], tile_box, tile_box32, t);
         if (__any_sync(0xffffffffu, need)) return t;
       }
       in_block = false;
@@ -606,7 +727,8 @@ __global__ void __launch_bounds__(32, MINB)
     k_raycast_pruned(Src src, const double* __restrict__ crec, const float* __restrict__ crec32,
                      const int32_t* __restrict__ perm, const int32_t* __restrict__ inv_perm,
                      int64_t n_cand, const double* __restrict__ tile_box,
-                     const double* __restrict__ block_box, Frame fr, RayOut out,
+                     const double* __restrict__ block_box, const float* __restrict__ tile_box32,
+                     const float* __restrict__ block_box32, Frame fr, RayOut out,
                      unsigned long long* __restrict__ work) {
   constexpr int S = rec_stride(D);
   constexpr int S32 = rec32_stride(D);
@@ -623,7 +745,7 @@ __global__ void __launch_bounds__(32, MINB)
   bool act[R];
 #pragma unroll
   for (int j = 0; j < R; ++j) {
-    act[j] = src.load(k0 + (int64_t)j * 32, ray[j]);
+    act[j] = src.load(k0 + (int64_t)j * 32, ray[j], fr);
     if (!act[j]) init_padding_lane<D, R>(ray[j]);
   }
   if (lane == 0) {
@@ -635,7 +757,8 @@ __global__ void __launch_bounds__(32, MINB)
   int64_t st = 0;
   if (lane == 0) st = inv_perm[src.gen(k0)] / PT;
   st = __shfl_sync(0xffffffffu, st, 0);
-  TileCursor<D, R, PT, PB> cur;
+  seed_tile<D, R, PT, F32>(ray, crec + st * PT * S, (int)(st * PT), fr);
+  TileCursor<D, R, PT, PB, F32> cur;
   cur.ntiles = (n_cand + PT - 1) / PT;
   cur.nblocks = (cur.ntiles + PB - 1) / PB;
   cur.st = st;
@@ -650,22 +773,23 @@ __global__ void __launch_bounds__(32, MINB)
     }
   };
   unsigned long long tiles_done = 0;
+  WarpCounters wc;
   uint32_t phase[2] = {0u, 0u};
   int b = 0;
-  int64_t t = cur.next(ray, tile_box, block_box);
+  int64_t t = cur.next(ray, tile_box, block_box, tile_box32, block_box32);
   if (t >= 0) issue(t, 0);
   while (t >= 0) {
-    const int64_t tn = cur.next(ray, tile_box, block_box);
+    const int64_t tn = cur.next(ray, tile_box, block_box, tile_box32, block_box32);
     __syncwarp();
     if (tn >= 0) issue(tn, b ^ 1);
     mbar_wait(&bar[b], phase[b]);
     phase[b] ^= 1u;
     bool need = false;
 #pragma unroll
-    for (int j = 0; j < R; ++j) need |= ray_needs_box<D>(ray[j], tile_box + t * 2 * D);
+    for (int j = 0; j < R; ++j) need |= ray_needs<D, F32>(ray[j], tile_box, tile_box32, t);
     if (__any_sync(0xffffffffu, need)) {
       ++tiles_done;
-      screen_tile<D, R, PT, F32>(ray, buf[b], buf32[b], (int)(t * PT), fr);
+      screen_tile<D, R, PT, F32>(ray, buf[b], buf32[b], (int)(t * PT), fr, work ? &wc : nullptr);
     }
     __syncwarp();
     b ^= 1;
@@ -674,8 +798,24 @@ __global__ void __launch_bounds__(32, MINB)
 #pragma unroll
   for (int j = 0; j < R; ++j)
     if (act[j]) ray_store<D>(ray[j], src.id(k0 + (int64_t)j * 32), perm, out);
-  // work counter: (ray, generator) pairs screened = tiles x PT x 32 lanes x R
-  if (work && lane == 0) atomicAdd(work, tiles_done * (unsigned long long)(PT * 32 * R));
+  // work counters: [0] (ray, generator) pairs screened = tiles x PT x 32 x R,
+  // [1] blocks with rare work, [2] warp-level rare iterations, [3] entries,
+  // [4] ray updates (sum over lanes of sphere moves)
+  if (work) {
+    unsigned long long e = wc.entries;
+    for (int off = 16; off > 0; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
+    unsigned long long up = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) up += act[j] ? ray[j].nupd : 0;
+    for (int off = 16; off > 0; off >>= 1) up += __shfl_xor_sync(0xffffffffu, up, off);
+    if (lane == 0) {
+      atomicAdd(work, tiles_done * (unsigned long long)(PT * 32 * R));
+      atomicAdd(work + 1, wc.rare_blocks);
+      atomicAdd(work + 2, wc.rare_iters);
+      atomicAdd(work + 3, e);
+      atomicAdd(work + 4, up);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -719,7 +859,7 @@ __global__ void __launch_bounds__(NT)
   for (int li = blockIdx.x; li < cntl; li += gridDim.x) {
     const int64_t k = list[li];
     RayState<D> r;
-    src.load(k, r);
+    src.load(k, r, Frame{});
     double best = CUDART_INF;
     int bi = -1;
     for (int64_t c = threadIdx.x; c < n_cand; c += NT) {
@@ -841,23 +981,43 @@ struct PrunedIndex {
   const int32_t* inv_perm; // generator index -> kd position
   const double* tile_box;  // ntiles x 2D
   const double* block_box; // nblocks x 2D
+  const float* tile_box32; // ntiles x 2D, centred, rounded outward
+  const float* block_box32;
   int64_t n;
 };
 
 constexpr int PRUNE_TILE = 64;
 constexpr int PRUNE_BLOCK = 32;
 
-template <int D, bool F32, class Src>
-int launch_pruned_f(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
-                    const RayOut& out, cudaStream_t st, unsigned long long* work) {
-  constexpr int R = (D <= 3) ? 4 : 2;
-  constexpr int MINB = (D == 4) ? 12 : ((D == 6) ? 10 : 8);
+template <int D, int R, int MINB, bool F32, class Src>
+int launch_pruned_rm(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
+                     const RayOut& out, cudaStream_t st, unsigned long long* work) {
   const int64_t per_block = 32 * R;
   const int64_t grid = (n_rays + per_block - 1) / per_block;
   k_raycast_pruned<D, R, PRUNE_TILE, PRUNE_BLOCK, MINB, F32, Src><<<(unsigned)grid, 32, 0, st>>>(
-      src, ix.crec, ix.crec32, ix.perm, ix.inv_perm, ix.n, ix.tile_box, ix.block_box, fr, out,
-      work);
+      src, ix.crec, ix.crec32, ix.perm, ix.inv_perm, ix.n, ix.tile_box, ix.block_box,
+      ix.tile_box32, ix.block_box32, fr, out, work);
   VR_RETURN_LAUNCH();
+}
+
+int raycast_variant();
+
+template <int D, bool F32, class Src>
+int launch_pruned_f(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
+                    const RayOut& out, cudaStream_t st, unsigned long long* work) {
+  if constexpr (D == 6 && F32) {
+    switch (raycast_variant()) {
+      case 1: return launch_pruned_rm<D, 2, 10, F32>(src, n_rays, ix, fr, out, st, work);
+      case 2: return launch_pruned_rm<D, 2, 8, F32>(src, n_rays, ix, fr, out, st, work);
+      case 3: return launch_pruned_rm<D, 1, 20, F32>(src, n_rays, ix, fr, out, st, work);
+      case 4: return launch_pruned_rm<D, 1, 12, F32>(src, n_rays, ix, fr, out, st, work);
+      default: break;
+    }
+  }
+  // one ray per lane: the warp's 32 rays are spatially tighter (fewer tiles
+  // pass the union test) and the lighter register file fits 12-24 warps/SM
+  constexpr int MINB = (D <= 3) ? 24 : (D <= 4 ? 20 : (D <= 6 ? 16 : 12));
+  return launch_pruned_rm<D, 1, MINB, F32>(src, n_rays, ix, fr, out, st, work);
 }
 
 template <int D, class Src>
@@ -869,7 +1029,8 @@ int launch_raycast_pruned(const Src& src, int64_t n_rays, const PrunedIndex& ix,
     cudaError_t e = cudaMemsetAsync(out.recheck_count, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return vr_cuda_status(e);
   }
-  if (ix.crec32) return launch_pruned_f<D, true>(src, n_rays, ix, fr, out, st, work);
+  if (ix.crec32 && ix.tile_box32 && ix.block_box32)
+    return launch_pruned_f<D, true>(src, n_rays, ix, fr, out, st, work);
   return launch_pruned_f<D, false>(src, n_rays, ix, fr, out, st, work);
 }
 

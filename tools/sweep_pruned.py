@@ -16,20 +16,28 @@ def run(name, ns, x, u, eta, modes=("exhaustive", "pruned")):
     n = xd.shape[0]
     ns.prune_index()
     for mode in modes:
-        work = torch.zeros(1, dtype=torch.int64, device=dev)
+        work = torch.zeros(8, dtype=torch.int64, device=dev)
         vb.raycast_batch(ns, xd, ud, ed, mode=mode)  # warm
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         torch.cuda.synchronize()
         vb.raycast_batch(ns, xd, ud, ed, mode=mode, events=e, work=work)
         torch.cuda.synchronize()
         k = e[0].elapsed_time(e[1])
-        pairs = int(work.item()) if mode == "pruned" else n * ns.n
+        w = work.cpu().numpy()
+        pairs = int(w[0]) if mode == "pruned" else n * ns.n
+        if mode == "pruned":
+            nw = (n + 63) // 64
+            print(f"   per warp: rare blocks {w[1] / nw:.1f}, rare iterations {w[2] / nw:.1f}; "
+                  f"per ray: entries {w[3] / n:.2f}, sphere updates {w[4] / n:.2f}; "
+                  f"tiles/warp {w[0] / 4096 / nw:.1f}")
         print(f"{name:28s} {mode:10s} rays={n:8d} kernel={k:8.3f} ms  rays/s={n / k * 1e3:9.3e}"
               f"  pairs/ray={pairs / n:9.1f}  Gpairs/s={pairs / k / 1e6:8.1f}", flush=True)
 
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["c2gen", "c2vert", "c5gen", "c4mc"]
+    if os.environ.get("MODES"):
+        run.__defaults__ = (tuple(os.environ["MODES"].split(",")),)
     if "c2gen" in which or "c2vert" in which:
         pts = np.random.default_rng(0).random((20000, 6))
         ns = vb.NodeSet(pts)
