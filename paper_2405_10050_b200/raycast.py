@@ -357,20 +357,22 @@ def _vertex_directions(pts, sigma, positions):
 
 
 class HostRaycaster:
-    """Batched RayCast on host (pinned) arrays, pipelined over three streams:
-    the H2D copy of chunk c+1 and the D2H copy of chunk c-1 run on separate
-    copy engines while the kernel of chunk c runs.  The end-to-end public
-    entry point for callers whose rays live in host memory."""
+    """Batched RayCast on host (pinned) arrays.  Chunks cycle through NBUF
+    device buffers; H2D copies, D2H copies and kernels run on separate
+    streams (two compute streams, so one chunk's kernel tail overlaps the
+    next chunk's kernel) -- the copy engines and the SMs work concurrently.
+    The end-to-end public entry point for callers whose rays live in host
+    memory."""
 
-    NBUF = 3
+    NBUF = 4
 
-    def __init__(self, ns: NodeSet, n_max: int, eta_len: int, chunk: int = 1 << 17):
+    def __init__(self, ns: NodeSet, n_max: int, eta_len: int, chunk: int = 1 << 18):
         rec, _ = ns.device_records()
         self.ns, self.dev, self.chunk, self.k = ns, rec.device, int(chunk), int(eta_len)
         d = ns.dim
         c = self.chunk
         self.h2d_stream = torch.cuda.Stream(self.dev)
-        self.comp_stream = torch.cuda.Stream(self.dev)
+        self.comp_streams = [torch.cuda.Stream(self.dev), torch.cuda.Stream(self.dev)]
         self.d2h_stream = torch.cuda.Stream(self.dev)
         self.buf = [dict(x=torch.empty((c, d), dtype=torch.float64, device=self.dev),
                          u=torch.empty((c, d), dtype=torch.float64, device=self.dev),
@@ -387,7 +389,7 @@ class HostRaycaster:
     def pinned(shape, dtype):
         return torch.empty(shape, dtype=dtype, pin_memory=True)
 
-    def run(self, hx, hu, heta, hidx, ht, hrp, hflag, stats=None, mode="auto"):
+    def run(self, hx, hu, heta, hidx, ht, hrp, hflag, stats=None, mode="auto", screen="fp32"):
         """hx, hu (n, d) f64, heta (n, k) i32 pinned inputs; outputs pinned
         hidx (n,) i32, ht (n,) f64, hrp (n, d) f64, hflag (n,) u8.  Returns
         after the last D2H copy has completed."""
@@ -396,8 +398,11 @@ class HostRaycaster:
         nchunks = (n + c - 1) // c
         if self.ns.n >= 1024 and mode != "exhaustive":
             self.ns.prune_index(self.dev)
+        if screen == "fp32":
+            self.ns.screen32(self.dev)
         for ci in range(nchunks):
             b = self.buf[ci % self.NBUF]
+            cs = self.comp_streams[ci & 1]
             lo, hi = ci * c, min(n, (ci + 1) * c)
             m = hi - lo
             with torch.cuda.stream(self.h2d_stream):
@@ -407,14 +412,14 @@ class HostRaycaster:
                 b["u"][:m].copy_(hu[lo:hi], non_blocking=True)
                 b["eta"][:m].copy_(heta[lo:hi], non_blocking=True)
                 b["h2d"].record(self.h2d_stream)
-            with torch.cuda.stream(self.comp_stream):
-                self.comp_stream.wait_event(b["h2d"])
+            with torch.cuda.stream(cs):
+                cs.wait_event(b["h2d"])
                 raycast_batch(self.ns, b["x"][:m], b["u"][:m], b["eta"][:m],
                               out=dict(idx=b["idx"][:m], t=b["t"][:m], rp=b["rp"][:m],
                                        flag=b["flag"][:m]),
-                              workspace=self.ws[ci % self.NBUF], stats=stats,
-                              stream=self.comp_stream, mode=mode)
-                b["done"].record(self.comp_stream)
+                              workspace=self.ws[ci % self.NBUF], stats=stats, stream=cs,
+                              mode=mode, screen=screen)
+                b["done"].record(cs)
             with torch.cuda.stream(self.d2h_stream):
                 self.d2h_stream.wait_event(b["done"])
                 hidx[lo:hi].copy_(b["idx"][:m], non_blocking=True)

@@ -1,0 +1,46 @@
+"""Where does the end-to-end (host arrays) time go?  H2D / D2H bandwidth and
+HostRaycaster chunk sizes on config-2-shaped rays."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2405_10050_b200 as vb  # noqa: E402
+from paper_2405_10050_b200.raycast import HostRaycaster  # noqa: E402
+
+n, d = 1_000_000, 6
+pts = np.random.default_rng(0).random((20000, d))
+ns = vb.NodeSet(pts)
+rng = np.random.default_rng(3)
+g = rng.integers(0, 20000, n).astype(np.int32)
+u = rng.standard_normal((n, d))
+u /= np.linalg.norm(u, axis=1, keepdims=True)
+P = HostRaycaster.pinned
+hx, hu, hg = P((n, d), torch.float64), P((n, d), torch.float64), P((n, 1), torch.int32)
+hx.copy_(torch.from_numpy(pts[g]))
+hu.copy_(torch.from_numpy(u))
+hg.copy_(torch.from_numpy(g[:, None].copy()))
+dx = torch.empty((n, d), dtype=torch.float64, device="cuda")
+for name, src, dst in (("H2D 48MB", hx, dx), ("D2H 48MB", dx, hx)):
+    dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / 5
+    print(f"{name}: {dt * 1e3:.2f} ms = {48e6 / dt / 1e9:.1f} GB/s")
+hidx, ht = P((n,), torch.int32), P((n,), torch.float64)
+hrp, hfl = P((n, d), torch.float64), P((n,), torch.uint8)
+for chunk in (1 << 16, 1 << 17, 1 << 18, 1 << 19):
+    hr = HostRaycaster(ns, n, 1, chunk=chunk)
+    hr.run(hx, hu, hg, hidx, ht, hrp, hfl)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        hr.run(hx, hu, hg, hidx, ht, hrp, hfl)
+    dt = (time.perf_counter() - t0) / 3
+    print(f"chunk {chunk}: {dt * 1e3:.2f} ms  {n / dt:.3e} rays/s")
