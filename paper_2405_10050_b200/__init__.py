@@ -14,7 +14,7 @@ from .core import (TOL_VERTEX, TOL_DEGENERATE, HALFSPACE_SLACK, BoundaryRay, Mes
 from .raycast import (RayQuery, RaycastBatch, RaycastStats, initial_heuristic, project_t,
                       raycast_batch, raycast_incircle, search_direction, vertex_directions_batch)
 from .graph import (DESCENT_RETRIES, VerifyReport, brute_force_vertices, circumcenters, descent,
-                    descent_batch, edge_set, verify_mesh, voronoi_graph)
+                    descent_batch, edge_set, verify_mesh, voronoi_graph, voronoi_local)
 from .integrate_mc import (CellIntegrals, Integrand, MCResult, mc_areas_only, mc_cells,
                            mc_directions, sample_unit_sphere, sphere_surface_area)
 
@@ -25,7 +25,8 @@ __all__ = [
     "verify_vertex", "verify_vertices", "TOL_VERTEX", "TOL_DEGENERATE", "HALFSPACE_SLACK",
     "edge_keys", "RayQuery", "RaycastStats", "RaycastBatch", "project_t", "initial_heuristic",
     "raycast_incircle", "raycast_batch", "search_direction", "vertex_directions_batch",
-    "edge_set", "descent", "descent_batch", "voronoi_graph", "verify_mesh", "VerifyReport",
+    "edge_set", "descent", "descent_batch", "voronoi_graph", "voronoi_local", "verify_mesh",
+    "VerifyReport",
     "brute_force_vertices", "circumcenters", "DESCENT_RETRIES", "CellIntegrals", "Integrand",
     "MCResult", "sample_unit_sphere", "sphere_surface_area", "mc_areas_only", "mc_cells",
     "mc_directions", "errors", "rng",

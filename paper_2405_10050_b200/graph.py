@@ -353,19 +353,27 @@ class DeviceTraversal:
 
     def seed_vertex(self, sigma):
         """Insert the descent vertex (level 0) with its fp64 circumcentre."""
-        self.ensure_vertices(1)
-        self.ensure_edges(self.d + 1)
-        s = torch.as_tensor(np.asarray(sigma, dtype=np.int32)[None], device=self.dev)
-        self.vsig[0:1] = s
-        ok = torch.empty(1, dtype=torch.uint8, device=self.dev)
-        _lib.check(self.L.vr_circumcenters(_lib.ptr(self.rec), self.d, _lib.ptr(s), 1,
+        self.seed_vertices(np.asarray(sigma, dtype=np.int32)[None])
+
+    def seed_vertices(self, sigmas):
+        """Insert distinct seed vertices (sorted sigma rows) at level 0."""
+        sig = np.ascontiguousarray(sigmas, dtype=np.int32).reshape(-1, self.d + 1)
+        m = sig.shape[0]
+        self.ensure_vertices(m)
+        self.ensure_edges((self.d + 1) * m)
+        s = torch.as_tensor(sig, device=self.dev)
+        self.vsig[0:m] = s
+        ok = torch.empty(m, dtype=torch.uint8, device=self.dev)
+        _lib.check(self.L.vr_circumcenters(_lib.ptr(self.rec), self.d, _lib.ptr(s), m,
                                            _lib.ptr(self.vr), _lib.ptr(ok), self._sh()),
                    "vr_circumcenters")
+        if not bool(ok.all()):
+            raise DegenerateConfiguration("a seed vertex has an affinely dependent sigma")
         T = self.tables()
-        _lib.check(self.L.vr_trav_insert_vertices(ctypes.byref(T), self.d, _lib.ptr(s), 1, 0, 0,
-                                                  1, self._sh()), "insert seed")
-        self.nv = 1
-        self.e_ub = self.d + 1
+        _lib.check(self.L.vr_trav_insert_vertices(ctypes.byref(T), self.d, _lib.ptr(s), m, 0, 0,
+                                                  1, self._sh()), "insert seeds")
+        self.nv = m
+        self.e_ub = (self.d + 1) * m
 
     def level(self, f0, f1, lvl, stats=None, ws=None):
         """Expand frontier vertices [f0, f1); returns the number of new vertices."""
@@ -480,4 +488,44 @@ def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heurist
                             tr.bu[:tr.nb].cpu().numpy())
     if return_info:
         return mesh, {"levels": levels, "vertices": tr.nv, "boundary": tr.nb}
+    return mesh
+
+
+def voronoi_local(ns: NodeSet, starts, hops: int, seed: int = 0, stats: RaycastStats = None,
+                  return_levels: bool = False):
+    """All Voronoi vertices within `hops` edge hops of the descent vertices of
+    `starts` (SURVEY.md §8(d) config 5 "local traversal").
+
+    The seed vertices come from the reference descent with the streams
+    ``stream(seed, "descent", s)`` (graph.py:46-85); the level-synchronous
+    traversal then runs `hops` levels.  BFS level = hop distance, so the
+    result is the union of the L-hop balls, independent of visiting order.
+    Returns a Mesh (and, with return_levels, the hop level of every vertex).
+    """
+    if stats is None:
+        stats = RaycastStats()
+    sig, _ = descent_batch(ns, starts, seed=seed, stats=stats)
+    _, first = np.unique(sig, axis=0, return_index=True)
+    sig = sig[np.sort(first)]
+    tr = DeviceTraversal(ns, vcap_hint=max(4 * ns.n, 64 * len(sig) * 4 ** min(hops, 6)))
+    tr.seed_vertices(sig)
+    from .raycast import Workspace
+    ws = Workspace()
+    f0, f1 = 0, tr.nv
+    bounds = [(0, f1)]
+    for lvl in range(1, hops + 1):
+        if f1 == f0:
+            break
+        n_new = tr.level(f0, f1, lvl, stats=stats, ws=ws)
+        f0, f1 = f1, f1 + n_new
+        bounds.append((f0, f1))
+    ek, ec = tr.edges()
+    mesh = Mesh.from_arrays(ns, tr.vsig[:tr.nv].cpu().numpy(), tr.vr[:tr.nv].cpu().numpy(),
+                            ek.cpu().numpy(), ec.cpu().numpy(), tr.bsig[:tr.nb].cpu().numpy(),
+                            tr.bu[:tr.nb].cpu().numpy())
+    if return_levels:
+        lv = np.zeros(tr.nv, dtype=np.int8)
+        for h, (a, b) in enumerate(bounds):
+            lv[a:b] = h
+        return mesh, lv
     return mesh

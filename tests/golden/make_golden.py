@@ -249,6 +249,44 @@ def mc_golden():
     np.savez_compressed(os.path.join(HERE, "mc_golden.npz"), **out)
 
 
+def config5_balls(n_seeds=5, hops=4):
+    """Reference-computed L-hop vertex balls around descent vertices at
+    N=1e6, d=8 (fp32-upcast uniform): BFS over the vertex-edge graph, every
+    edge raycast with the unmodified reference raycast_incircle."""
+    pts = np.random.default_rng(0).random((10 ** 6, 8)).astype(np.float32).astype(np.float64)
+    ns = vr.build_node_set(pts)
+    seeds = np.random.default_rng(1).choice(10 ** 6, 10000, replace=False)[:n_seeds]
+    out = {}
+    t0 = time.time()
+    for m, sd in enumerate(seeds):
+        v = vr.descent(ns, int(sd), vrng.stream(0, "descent", int(sd)))
+        dist = {v.sigma: 0}
+        coords = {v.sigma: v.r}
+        frontier = [v.sigma]
+        for h in range(1, hops + 1):
+            nxt = []
+            for sig in frontier:
+                dirs = _vertex_directions(ns.points, sig, range(9))
+                for k in range(9):
+                    eta = sig[:k] + sig[k + 1:]
+                    res = vr.raycast_incircle(ns, vr.RayQuery(eta, coords[sig], dirs[k]),
+                                              heuristic=False)
+                    if res is None:
+                        continue
+                    s2, r2 = res
+                    if s2 not in dist:
+                        dist[s2] = h
+                        coords[s2] = r2
+                        nxt.append(s2)
+            frontier = nxt
+        keys = sorted(dist)
+        out[f"seed{m}"] = np.array([int(sd)])
+        out[f"ball{m}_sigma"] = np.array(keys, dtype=np.int32)
+        out[f"ball{m}_hops"] = np.array([dist[k] for k in keys], dtype=np.int8)
+        print("config5 ball", m, len(keys), "vertices", f"{time.time() - t0:.1f}s", flush=True)
+    np.savez_compressed(os.path.join(HERE, "config5_balls.npz"), **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["mesh_config1", "meshes_small", "config2_sample", "mc_golden",
                              "config5_sample"]

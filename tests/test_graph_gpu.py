@@ -188,3 +188,27 @@ def test_mesh_helpers_match_reference_semantics():
     for s in mesh.vertices:
         for e in vb.edge_set(s):
             assert e in mesh.edge_counts
+
+
+def test_config5_local_balls_match_reference():
+    """N=1e6, d=8: L-hop balls around descent vertices equal the reference
+    BFS balls (tests/golden/config5_balls.npz, L=4) as sigma sets, and the
+    multi-seed traversal is their union."""
+    gz = golden("config5_balls.npz")
+    pts = np.random.default_rng(0).random((10 ** 6, 8)).astype(np.float32).astype(np.float64)
+    ns = vb.NodeSet(pts)
+    seeds = [int(gz[f"seed{m}"][0]) for m in range(5)]
+    union = set()
+    for m, sd in enumerate(seeds[:2]):
+        mesh, lv = vb.voronoi_local(ns, [sd], hops=4, return_levels=True)
+        a = mesh.arrays()
+        order = np.lexsort(a["sigma"].T[::-1])
+        assert np.array_equal(a["sigma"][order], gz[f"ball{m}_sigma"])
+        assert np.array_equal(lv[order], gz[f"ball{m}_hops"])
+    for m in range(5):
+        union |= {tuple(r) for r in gz[f"ball{m}_sigma"].tolist()}
+    mesh = vb.voronoi_local(ns, seeds, hops=4)
+    got = {tuple(r) for r in mesh.arrays()["sigma"].tolist()}
+    assert got == union
+    ok = vb.verify_vertices(ns, mesh.arrays()["sigma"][::13], mesh.arrays()["r"][::13])
+    assert ok.all()
