@@ -91,7 +91,7 @@ class NodeSet:
             return hit
         L = _lib.lib()
         with torch.cuda.device(dev):
-            pts = torch.from_numpy(self.points).to(dev)
+            pts = torch.from_numpy(np.array(self.points)).to(dev)
             rec = torch.empty((_lib.record_rows(self.n), self.stride), dtype=torch.float64,
                               device=dev)
             sqmax = torch.zeros(1, dtype=torch.float64, device=dev)

@@ -375,8 +375,16 @@ class DeviceTraversal:
         self.nv = m
         self.e_ub = (self.d + 1) * m
 
-    def level(self, f0, f1, lvl, stats=None, ws=None):
-        """Expand frontier vertices [f0, f1); returns the number of new vertices."""
+    def _raycast(self, rx, ru, reta, stats, ws):
+        res = raycast_batch(self.ns, rx, ru, reta, want_rp=False, stats=stats, workspace=ws)
+        return res.idx, res.flag
+
+    def level(self, f0, f1, lvl, stats=None, ws=None, raycast_fn=None):
+        """Expand frontier vertices [f0, f1); returns the number of new vertices.
+
+        raycast_fn(x, u, eta) -> (idx int32, flag uint8) replaces the local
+        fused RayCast (parallel.ShardedRaycast splits the level's rays across
+        ranks and all-gathers the hits)."""
         d, L, dev, sh = self.d, self.L, self.dev, self._sh()
         F = f1 - f0
         fs = self.vsig[f0:f1]
@@ -399,19 +407,22 @@ class DeviceTraversal:
                                        _lib.ptr(open_mask), _lib.ptr(off), _lib.ptr(rx),
                                        _lib.ptr(ru), _lib.ptr(reta), _lib.ptr(rpar),
                                        _lib.ptr(bad), sh), "emit_rays")
-        res = raycast_batch(self.ns, rx, ru, reta, want_rp=False, stats=stats, workspace=ws)
+        if raycast_fn is None:
+            hit_idx, hit_flag = self._raycast(rx, ru, reta, stats, ws)
+        else:
+            hit_idx, hit_flag = raycast_fn(rx, ru, reta)
         self.ensure_vertices(R)
         T = self.tables()
         rsig = torch.empty((R, d + 1), dtype=torch.int32, device=dev)
         slot = torch.empty(R, dtype=torch.int64, device=dev)
         newf = torch.empty(R, dtype=torch.int32, device=dev)
         escf = torch.empty(R, dtype=torch.int32, device=dev)
-        _lib.check(L.vr_trav_claim(ctypes.byref(T), d, _lib.ptr(reta), _lib.ptr(res.idx),
-                                   _lib.ptr(res.flag), R, lvl, _lib.ptr(rsig), _lib.ptr(slot),
+        _lib.check(L.vr_trav_claim(ctypes.byref(T), d, _lib.ptr(reta), _lib.ptr(hit_idx),
+                                   _lib.ptr(hit_flag), R, lvl, _lib.ptr(rsig), _lib.ptr(slot),
                                    _lib.ptr(newf), _lib.ptr(escf), sh), "claim")
         noff, ninc = _excl_cumsum(newf)
         eoff, einc = _excl_cumsum(escf)
-        ndeg = (res.flag == 3).sum()
+        ndeg = (hit_flag == 3).sum()
         summary = torch.stack([ninc[-1], einc[-1], ndeg.to(torch.int64), bad[0].to(torch.int64),
                                self.overflow[0].to(torch.int64)]).cpu().numpy()
         n_new, n_esc, n_deg, n_bad, ovf = (int(v) for v in summary)
@@ -459,8 +470,24 @@ class DeviceTraversal:
         return keys[order], cnt[order]
 
 
+def _level_raycaster(ns, stats, group):
+    """None (local fused RayCast) or a ShardedRaycast over the ranks of the
+    default / given process group."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return None
+    from .parallel import ShardedRaycast
+
+    def fn(x, u, eta):
+        r = raycast_batch(ns, x, u, eta, want_rp=False, stats=stats)
+        return r.idx, r.flag
+
+    return ShardedRaycast(fn, group)
+
+
 def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heuristic",
-                  eps: float = None, stats: RaycastStats = None, return_info: bool = False):
+                  eps: float = None, stats: RaycastStats = None, return_info: bool = False,
+                  group=None):
     """Full Voronoi mesh by exhaustive edge-tracked traversal (graph.py:88-146).
 
     Level-synchronous on the device: every level raycasts all open edges of
@@ -478,8 +505,9 @@ def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heurist
     ws = Workspace()
     f0, f1, lvl = 0, 1, 1
     levels = []
+    rfn = _level_raycaster(ns, stats, group)
     while f1 > f0:
-        n_new = tr.level(f0, f1, lvl, stats=stats, ws=ws)
+        n_new = tr.level(f0, f1, lvl, stats=stats, ws=ws, raycast_fn=rfn)
         levels.append((f1 - f0, n_new))
         f0, f1, lvl = f1, f1 + n_new, lvl + 1
     ek, ec = tr.edges()
@@ -492,7 +520,7 @@ def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heurist
 
 
 def voronoi_local(ns: NodeSet, starts, hops: int, seed: int = 0, stats: RaycastStats = None,
-                  return_levels: bool = False):
+                  return_levels: bool = False, group=None):
     """All Voronoi vertices within `hops` edge hops of the descent vertices of
     `starts` (SURVEY.md §8(d) config 5 "local traversal").
 
@@ -507,16 +535,17 @@ def voronoi_local(ns: NodeSet, starts, hops: int, seed: int = 0, stats: RaycastS
     sig, _ = descent_batch(ns, starts, seed=seed, stats=stats)
     _, first = np.unique(sig, axis=0, return_index=True)
     sig = sig[np.sort(first)]
-    tr = DeviceTraversal(ns, vcap_hint=max(4 * ns.n, 64 * len(sig) * 4 ** min(hops, 6)))
+    tr = DeviceTraversal(ns, vcap_hint=max(4 * ns.n, 6 * len(sig) * 4 ** min(hops, 8)))
     tr.seed_vertices(sig)
     from .raycast import Workspace
     ws = Workspace()
     f0, f1 = 0, tr.nv
     bounds = [(0, f1)]
+    rfn = _level_raycaster(ns, stats, group)
     for lvl in range(1, hops + 1):
         if f1 == f0:
             break
-        n_new = tr.level(f0, f1, lvl, stats=stats, ws=ws)
+        n_new = tr.level(f0, f1, lvl, stats=stats, ws=ws, raycast_fn=rfn)
         f0, f1 = f1, f1 + n_new
         bounds.append((f0, f1))
     ek, ec = tr.edges()
