@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rays-per-core", type=int, default=3000)
     ap.add_argument("--mode", choices=["pruned", "exhaustive"], default="pruned")
+    ap.add_argument("--no-extra", action="store_true", help="skip configs 1, 3, 4, 5")
     return ap.parse_args()
 
 
@@ -198,6 +199,74 @@ def fp64_peak(torch, L, _lib):
     return best
 
 
+def extra_configs(vb, torch, world, rank):
+    """The other SURVEY §8(d) configs, measured in the same run (one pass each,
+    device-synchronised wall time; the traversal phases are sequences of
+    launches with host syncs between levels).  Multi-rank: the traversal
+    levels are ray-sharded (parallel.ShardedRaycast), MC cells are sharded."""
+    from paper_2405_10050_b200 import parallel
+    out = {}
+    pts1 = np.random.default_rng(0).random((1000, 3))
+    ns1 = vb.build_node_set(pts1)
+    vb.voronoi_graph(ns1, seed=0)  # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    m1, info1 = vb.voronoi_graph(ns1, seed=0, return_info=True)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    out["config1_full_diagram"] = {"vertices": info1["vertices"], "seconds": dt,
+                                   "vertices_per_s": info1["vertices"] / dt,
+                                   "levels": len(info1["levels"]),
+                                   "reference_cpu_s_1core_build_container": 0.61}
+    pts3 = np.random.default_rng(0).standard_normal((10000, 5))
+    ns3 = vb.build_node_set(pts3)
+    ns3.prune_index()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    m3, info3 = vb.voronoi_graph(ns3, seed=0, return_info=True)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    import hashlib
+    sig = m3.arrays()["sigma"]
+    dig = hashlib.sha256(np.ascontiguousarray(sig[np.lexsort(sig.T[::-1])], dtype="<i4")
+                         .tobytes()).hexdigest()
+    out["config3_full_diagram"] = {
+        "vertices": info3["vertices"], "seconds": dt, "vertices_per_s": info3["vertices"] / dt,
+        "sigma_digest_matches_reference": dig == "f8093583cb129297758ebea66c8fcbbf3938086d"
+                                                "9f8b8ee1b0f79096a9351173",
+        "reference_cpu_s_1core_build_container": 667.0}
+    pts4 = np.random.default_rng(0).random((100000, 4))
+    ns4 = vb.NodeSet(pts4)
+    ns4.prune_index()
+    cells = np.arange(100000)
+    parallel.mc_cells_sharded(ns4, cells[:2000], 1000, seed=0)  # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res4 = parallel.mc_cells_sharded(ns4, cells, 1000, seed=0)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    out["config4_mc"] = {"cells": 100000, "rays_per_cell": 1000, "seconds": dt,
+                         "rays_per_s": 1e8 / dt, "bounded_cells": int((res4.status == 0).sum()),
+                         "reference_cpu_rays_per_s_per_core_build_container": 4180}
+    pts5 = np.random.default_rng(0).random((10 ** 6, 8)).astype(np.float32).astype(np.float64)
+    ns5 = vb.NodeSet(pts5)
+    ns5.prune_index()
+    ns5.screen32()
+    seeds = np.random.default_rng(1).choice(10 ** 6, 10000, replace=False)
+    st = vb.RaycastStats()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    m5, lv = vb.voronoi_local(ns5, seeds, hops=5, stats=st, return_levels=True)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    out["config5_local_traversal"] = {
+        "seeds": 10000, "hops": 5, "vertices": int(len(lv)), "seconds_incl_descent": dt,
+        "vertices_per_s": len(lv) / dt, "edge_raycasts_this_rank": st.raycasts,
+        "per_level": np.bincount(lv).tolist(),
+        "reference_cpu_rays_per_s_per_core_build_container": 1000}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -309,6 +378,10 @@ def run_ours(args):
     h2d = x.nbytes + u.nbytes + g.nbytes
     d2h = n * (4 + 8 + 8 * DIM + 1)
 
+    extra = None
+    if not args.no_extra:
+        extra = extra_configs(vb, torch, world, rank)
+
     result = None
     if rank == 0:
         peak = fp64_peak(torch, L, _lib)
@@ -345,6 +418,8 @@ def run_ours(args):
             "clocks": clk.summary(),
             "checks": {"escaped": n_esc, "degenerate": n_deg, "pool_build_s": t_pool},
         }
+        if extra is not None:
+            result["extra_configs"] = extra
         if world == 1 and not args.no_cpu_baseline:
             cores = host_cores()
             m = min(n, args.cpu_rays_per_core * cores)

@@ -124,25 +124,26 @@ int vr_raycast_batch(const double* rec, int64_t n_gen, int d, double sqmax,
 
 /* ---- Exact candidate pruning ---------------------
  * Generators reordered by a balanced kd partition into tiles of
- * VR_PRUNE_TILE records (padded with sentinels), each tile with an
- * axis-aligned bounding box, tiles grouped in blocks of VR_PRUNE_BLOCK tiles
- * with their own boxes.  A warp of spatially coherent rays skips a block /
- * tile only when, for every one of its rays, the box lies behind the ray's
- * forward halfspace or outside its current candidate sphere plus the
- * degeneracy/rounding band -- a certificate that no skipped generator could
- * change the result, so the output equals vr_raycast_batch's. */
+ * VR_PRUNE_TILE records (padded with sentinels).  The kd tree over tiles is
+ * stored in heap layout (node i -> children 2i+1, 2i+2; a node covering n > 1
+ * tiles [lo, hi) splits at lo + n/2), each node with an axis-aligned box.  A
+ * warp of spatially coherent rays descends a node only if some ray needs it:
+ * a subtree is skipped when, for every ray of the warp, its box lies behind
+ * the ray's forward halfspace or outside its current candidate sphere plus
+ * the degeneracy/rounding band -- a certificate that no skipped generator
+ * could change the result, so the output equals vr_raycast_batch's. */
 #define VR_PRUNE_TILE 64
-#define VR_PRUNE_BLOCK 32
 typedef struct vr_prune_index {
   const double* rec;       /* kd-ordered records, vr_record_rows(n) rows       */
   const float* rec32;      /* kd-ordered fp32 centred records (nullable)       */
   const int32_t* perm;     /* kd position -> generator index (n)               */
   const int32_t* inv_perm; /* generator index -> kd position (n)               */
   const double* tile_box;  /* ceil(n/64) x 2d, [lo_0..lo_{d-1}, hi_0..]        */
-  const double* block_box; /* ceil(ceil(n/64)/32) x 2d                         */
   const float* tile_box32; /* same boxes, centred at vr_screen32.center, fp32
                               rounded outward (lo down, hi up); nullable     */
-  const float* block_box32;
+  const double* node_box;  /* kd-tree node boxes, heap layout, x 2d            */
+  const float* node_box32; /* centred fp32 outward copies; nullable            */
+  const int32_t* node_range; /* 2 per node: first tile, last tile + 1        */
   int64_t n;
 } vr_prune_index;
 

@@ -163,7 +163,7 @@ class NodeSet:
         return (int(idx[0]), float(d1[0])), float(d2[0])
 
 
-PRUNE_TILE, PRUNE_BLOCK = 64, 32
+PRUNE_TILE = 64
 
 
 class _Screen32Struct(ctypes.Structure):
@@ -197,8 +197,9 @@ class Screen32:
 class _PruneStruct(ctypes.Structure):
     _fields_ = [("rec", ctypes.c_void_p), ("rec32", ctypes.c_void_p), ("perm", ctypes.c_void_p),
                 ("inv_perm", ctypes.c_void_p), ("tile_box", ctypes.c_void_p),
-                ("block_box", ctypes.c_void_p), ("tile_box32", ctypes.c_void_p),
-                ("block_box32", ctypes.c_void_p), ("n", ctypes.c_int64)]
+                ("tile_box32", ctypes.c_void_p), ("node_box", ctypes.c_void_p),
+                ("node_box32", ctypes.c_void_p), ("node_range", ctypes.c_void_p),
+                ("n", ctypes.c_int64)]
 
 
 def kd_order(P, tile=PRUNE_TILE):
@@ -257,6 +258,60 @@ def _outward32(lo, hi, center):
     return torch.cat([lo32, hi32], 1).contiguous()
 
 
+def kd_tree_layout(nt):
+    """Heap layout of the kd tree over nt tiles (node i -> 2i+1, 2i+2; a node
+    of n > 1 tiles [lo, hi) splits at lo + n // 2, as kd_order does).
+    Returns (ranges int32 (nodes, 2), leaf node index per tile); unused heap
+    slots have range (-1, -1)."""
+    size = 1
+    while size < nt:
+        size *= 2
+    nodes = 2 * size
+    rng = np.full((nodes, 2), -1, dtype=np.int64)
+    cur = np.array([0]), np.array([0]), np.array([nt])
+    leaf_of = np.zeros(nt, dtype=np.int64)
+    while cur[0].size:
+        idx, lo, hi = cur
+        rng[idx, 0], rng[idx, 1] = lo, hi
+        n = hi - lo
+        leaf = n == 1
+        leaf_of[lo[leaf]] = idx[leaf]
+        inner = ~leaf
+        idx, lo, hi, n = idx[inner], lo[inner], hi[inner], n[inner]
+        mid = lo + n // 2
+        cur = (np.concatenate([2 * idx + 1, 2 * idx + 2]), np.concatenate([lo, mid]),
+               np.concatenate([mid, hi]))
+    used = rng[:, 0] >= 0
+    last = int(np.nonzero(used)[0].max()) + 1
+    return rng[:last].astype(np.int32), leaf_of
+
+
+def _node_boxes(lo, hi, ranges, leaf_of):
+    """Bottom-up unions of the tile boxes over the heap-layout kd tree."""
+    dev = lo.device
+    nn = ranges.shape[0]
+    d = lo.shape[1]
+    nlo = torch.full((nn, d), float("inf"), dtype=lo.dtype, device=dev)
+    nhi = torch.full((nn, d), float("-inf"), dtype=hi.dtype, device=dev)
+    leaf = torch.as_tensor(leaf_of, device=dev)
+    nlo[leaf], nhi[leaf] = lo, hi
+    depth = int(np.floor(np.log2(max(nn, 1)))) + 1
+    for lev in range(depth - 1, -1, -1):
+        a, b = (1 << lev) - 1, min(nn, (1 << (lev + 1)) - 1)
+        if a >= nn:
+            continue
+        idx = torch.arange(a, b, device=dev)
+        l, r = 2 * idx + 1, 2 * idx + 2
+        inner = torch.as_tensor(ranges[a:b, 1] - ranges[a:b, 0] > 1, device=dev)
+        li = idx[inner]
+        if li.numel():
+            ll, rr = 2 * li + 1, 2 * li + 2
+            nlo[li] = torch.minimum(nlo[ll], nlo[rr])
+            nhi[li] = torch.maximum(nhi[ll], nhi[rr])
+    # unused heap slots keep an empty box that no ray ever needs
+    return nlo, nhi
+
+
 class PruneIndex:
     """Device tensors of one vr_prune_index."""
 
@@ -278,21 +333,23 @@ class PruneIndex:
         lo = torch.where(valid, X, torch.full_like(X, float("inf"))).amin(1)
         hi = torch.where(valid, X, torch.full_like(X, float("-inf"))).amax(1)
         self.tile_box = torch.cat([lo, hi], 1).contiguous()
-        nb = (nt + PRUNE_BLOCK - 1) // PRUNE_BLOCK
-        pad = nb * PRUNE_BLOCK - nt
-        blo = torch.cat([lo, lo[-1:].expand(pad, d)]).view(nb, PRUNE_BLOCK, d).amin(1)
-        bhi = torch.cat([hi, hi[-1:].expand(pad, d)]).view(nb, PRUNE_BLOCK, d).amax(1)
-        self.block_box = torch.cat([blo, bhi], 1).contiguous()
+        ranges, leaf_of = kd_tree_layout(nt)
+        self.node_range = torch.as_tensor(ranges, device=dev).contiguous()
+        nlo, nhi = _node_boxes(lo, hi, ranges, leaf_of)
+        used = torch.as_tensor(ranges[:, 0] >= 0, device=dev)[:, None]
+        nlo = torch.where(used, nlo, torch.zeros_like(nlo))   # unused: finite, never visited
+        nhi = torch.where(used, nhi, torch.zeros_like(nhi))
+        self.node_box = torch.cat([nlo, nhi], 1).contiguous()
         self.rec = crec
         self.n = n
         self.rows = rows
         self.screen32 = Screen32(crec, n, d, center=center)
         self.tile_box32 = _outward32(lo, hi, self.screen32.center)
-        self.block_box32 = _outward32(blo, bhi, self.screen32.center)
+        self.node_box32 = _outward32(nlo, nhi, self.screen32.center)
         p = lambda t: t.data_ptr()  # noqa: E731
         self.struct = _PruneStruct(p(crec), p(self.screen32.rec), p(self.perm), p(self.inv_perm),
-                                   p(self.tile_box), p(self.block_box), p(self.tile_box32),
-                                   p(self.block_box32), n)
+                                   p(self.tile_box), p(self.tile_box32), p(self.node_box),
+                                   p(self.node_box32), p(self.node_range), n)
 
 
 def build_node_set(points, backend="auto"):

@@ -94,14 +94,16 @@ extern "C" int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double
                                  const int32_t* order, int32_t* out_idx, double* out_t,
                                  double* out_rp, uint8_t* out_flag, int32_t* recheck_list,
                                  int32_t* recheck_count, uint64_t* work, void* stream) {
-  if (!rec || !ix || !ix->rec || !ix->perm || !ix->inv_perm || !ix->tile_box || !ix->block_box ||
+  if (!rec || !ix || !ix->rec || !ix->perm || !ix->inv_perm || !ix->tile_box || !ix->node_box ||
+      !ix->node_range ||
       !x || !u || !eta || !out_idx || !out_t || !out_flag)
     return VR_EINVAL;
   if (eta_len < 1 || eta_len > d || ix->n != n_gen) return VR_EINVAL;
   if ((recheck_list == nullptr) != (recheck_count == nullptr)) return VR_EINVAL;
   RayOut out{out_idx, out_t, out_rp, out_flag, recheck_list, recheck_count};
   PrunedIndex pi{ix->rec, s32 ? ix->rec32 : nullptr, ix->perm, ix->inv_perm, ix->tile_box,
-                 ix->block_box, ix->tile_box32, ix->block_box32, ix->n};
+                 ix->tile_box32, ix->node_box, ix->node_box32,
+                 reinterpret_cast<const int2*>(ix->node_range), ix->n};
   const Screen sc = make_screen(sqmax, s32, d);
   VR_DISPATCH_D(d, {
     SrcExplicit<D> src{x, u, eta, eta_len, rec, n_rays, order};

@@ -676,43 +676,49 @@ __device__ __forceinline__ void seed_tile(RayState<D> (&ray)[R], const double* _
   }
 }
 
-// Cursor over the kd tiles in visiting order// Cursor over the kd tiles in visiting order (cyclic from the warp's start
-// tile), yielding only tiles whose block and tile boxes pass the warp-wide
-// need test against the rays' CURRENT spheres.
-template <int D, int R, int PT, int PB, bool F32>
-struct TileCursor {
-  int64_t ntiles, nblocks, st, sb;
-  int64_t bi = 0;  // blocks visited so far
-  int64_t ti = 0;  // tiles visited inside the current block
-  bool in_block = false;
+// Warp-coherent traversal of the kd tree over tiles (heap layout: node i has
+// children 2i+1, 2i+2; node_range[i] = [first tile, last tile + 1); a leaf is
+// one tile).  A node is descended only if some ray of the warp needs its box
+// (halfspace + current sphere + band); children are pushed so that the one
+// holding the warp's start tile is visited first.
+template <int D, int R, bool F32>
+struct TreeCursor {
+  static constexpr int MAXS = 48;
+  int stack[MAXS];
+  int sp = 0;
+  int64_t st = 0;
+  unsigned long long tests = 0;
+  __device__ __forceinline__ void init(int64_t start_tile) {
+    st = start_tile;
+    sp = 0;
+    stack[sp++] = 0;
+  }
   __device__ __forceinline__ int64_t next(const RayState<D> (&ray)[R],
-                                          const double* __restrict__ tile_box,
-                                          const double* __restrict__ block_box,
-                                          const float* __restrict__ tile_box32,
-                                          const float* __restrict__ block_box32) {
-    while (bi < nblocks) {
-      const int64_t b = (sb + bi) % nblocks;
-      const int64_t t_lo = b * PB, t_hi = min(ntiles, t_lo + PB);
-      if (!in_block) {
-        bool need = false;
+                                          const double* __restrict__ node_box,
+                                          const float* __restrict__ node_box32,
+                                          const int2* __restrict__ node_range) {
+    while (sp > 0) {
+      const int node = stack[--sp];
+      const int2 rg = __ldg(node_range + node);
+      bool need = false;
 #pragma unroll
-        for (int j = 0; j < R; ++j) need |= ray_needs<D, F32>(ray[j], block_box, block_box32, b);
-        if (!__any_sync(0xffffffffu, need)) { ++bi; continue; }
-        in_block = true;
-        ti = 0;
+      for (int j = 0; j < R; ++j) need |= ray_needs<D, F32>(ray[j], node_box, node_box32, node);
+      if (!__any_sync(0xffffffffu, need)) continue;
+      ++tests;
+      if (rg.y - rg.x == 1) return rg.x;
+      const int l = 2 * node + 1, r = 2 * node + 2;
+      if (sp + 2 > MAXS) __trap();  // depth > 46: impossible for < 2^46 tiles
+      // the child holding the warp's start tile first (kd index order is
+      // spatial order, so this visits the rays' neighbourhood early)
+      const int mid = rg.x + (rg.y - rg.x) / 2;
+      const float dl = st < mid ? 0.0f : 1.0f, dr = 1.0f - dl;
+      if (dl <= dr) {
+        stack[sp++] = r;
+        stack[sp++] = l;
+      } else {
+        stack[sp++] = l;
+        stack[sp++] = r;
       }
-      const int64_t tstart = (b == sb) ? st : t_lo;
-      while (ti < t_hi - t_lo) {
-        int64_t t = tstart + ti;
-        if (t >= t_hi) t -= (t_hi - t_lo);
-        ++ti;
-        bool need = false;
-#pragma unroll
-        for (int j = 0; j < R; ++j) need |= ray_needs<D, F32>(ray[j], tile_box, tile_box32, t);
-        if (__any_sync(0xffffffffu, need)) return t;
-      }
-      in_block = false;
-      ++bi;
     }
     return -1;
   }
@@ -727,9 +733,9 @@ __global__ void __launch_bounds__(32, MINB)
     k_raycast_pruned(Src src, const double* __restrict__ crec, const float* __restrict__ crec32,
                      const int32_t* __restrict__ perm, const int32_t* __restrict__ inv_perm,
                      int64_t n_cand, const double* __restrict__ tile_box,
-                     const double* __restrict__ block_box, const float* __restrict__ tile_box32,
-                     const float* __restrict__ block_box32, Frame fr, RayOut out,
-                     unsigned long long* __restrict__ work) {
+                     const float* __restrict__ tile_box32, const double* __restrict__ node_box,
+                     const float* __restrict__ node_box32, const int2* __restrict__ node_range,
+                     Frame fr, RayOut out, unsigned long long* __restrict__ work) {
   constexpr int S = rec_stride(D);
   constexpr int S32 = rec32_stride(D);
   constexpr uint32_t BYTES64 = (uint32_t)(PT * S * sizeof(double));
@@ -758,11 +764,8 @@ __global__ void __launch_bounds__(32, MINB)
   if (lane == 0) st = inv_perm[src.gen(k0)] / PT;
   st = __shfl_sync(0xffffffffu, st, 0);
   seed_tile<D, R, PT, F32>(ray, crec + st * PT * S, (int)(st * PT), fr);
-  TileCursor<D, R, PT, PB, F32> cur;
-  cur.ntiles = (n_cand + PT - 1) / PT;
-  cur.nblocks = (cur.ntiles + PB - 1) / PB;
-  cur.st = st;
-  cur.sb = st / PB;
+  TreeCursor<D, R, F32> cur;
+  cur.init(st);
 
   auto issue = [&](int64_t t, int b) {
     if (lane == 0) {
@@ -776,10 +779,10 @@ __global__ void __launch_bounds__(32, MINB)
   WarpCounters wc;
   uint32_t phase[2] = {0u, 0u};
   int b = 0;
-  int64_t t = cur.next(ray, tile_box, block_box, tile_box32, block_box32);
+  int64_t t = cur.next(ray, node_box, node_box32, node_range);
   if (t >= 0) issue(t, 0);
   while (t >= 0) {
-    const int64_t tn = cur.next(ray, tile_box, block_box, tile_box32, block_box32);
+    const int64_t tn = cur.next(ray, node_box, node_box32, node_range);
     __syncwarp();
     if (tn >= 0) issue(tn, b ^ 1);
     mbar_wait(&bar[b], phase[b]);
@@ -814,6 +817,7 @@ __global__ void __launch_bounds__(32, MINB)
       atomicAdd(work + 2, wc.rare_iters);
       atomicAdd(work + 3, e);
       atomicAdd(work + 4, up);
+      atomicAdd(work + 5, cur.tests);
     }
   }
 }
@@ -980,9 +984,10 @@ struct PrunedIndex {
   const int32_t* perm;     // kd position -> generator index
   const int32_t* inv_perm; // generator index -> kd position
   const double* tile_box;  // ntiles x 2D
-  const double* block_box; // nblocks x 2D
   const float* tile_box32; // ntiles x 2D, centred, rounded outward
-  const float* block_box32;
+  const double* node_box;  // kd-tree nodes (heap layout) x 2D
+  const float* node_box32;
+  const int2* node_range;  // [first tile, last tile + 1) per node
   int64_t n;
 };
 
@@ -995,8 +1000,8 @@ int launch_pruned_rm(const Src& src, int64_t n_rays, const PrunedIndex& ix, cons
   const int64_t per_block = 32 * R;
   const int64_t grid = (n_rays + per_block - 1) / per_block;
   k_raycast_pruned<D, R, PRUNE_TILE, PRUNE_BLOCK, MINB, F32, Src><<<(unsigned)grid, 32, 0, st>>>(
-      src, ix.crec, ix.crec32, ix.perm, ix.inv_perm, ix.n, ix.tile_box, ix.block_box,
-      ix.tile_box32, ix.block_box32, fr, out, work);
+      src, ix.crec, ix.crec32, ix.perm, ix.inv_perm, ix.n, ix.tile_box, ix.tile_box32,
+      ix.node_box, ix.node_box32, ix.node_range, fr, out, work);
   VR_RETURN_LAUNCH();
 }
 
@@ -1029,7 +1034,7 @@ int launch_raycast_pruned(const Src& src, int64_t n_rays, const PrunedIndex& ix,
     cudaError_t e = cudaMemsetAsync(out.recheck_count, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return vr_cuda_status(e);
   }
-  if (ix.crec32 && ix.tile_box32 && ix.block_box32)
+  if (ix.crec32 && ix.tile_box32 && ix.node_box32)
     return launch_pruned_f<D, true>(src, n_rays, ix, fr, out, st, work);
   return launch_pruned_f<D, false>(src, n_rays, ix, fr, out, st, work);
 }

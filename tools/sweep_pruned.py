@@ -26,10 +26,10 @@ def run(name, ns, x, u, eta, modes=("exhaustive", "pruned")):
         w = work.cpu().numpy()
         pairs = int(w[0]) if mode == "pruned" else n * ns.n
         if mode == "pruned":
-            nw = (n + 63) // 64
+            nw = (n + 31) // 32
             print(f"   per warp: rare blocks {w[1] / nw:.1f}, rare iterations {w[2] / nw:.1f}; "
                   f"per ray: entries {w[3] / n:.2f}, sphere updates {w[4] / n:.2f}; "
-                  f"tiles/warp {w[0] / 4096 / nw:.1f}")
+                  f"tiles/warp {w[0] / 2048 / nw:.1f}, node tests passed/warp {w[5] / nw:.1f}")
         print(f"{name:28s} {mode:10s} rays={n:8d} kernel={k:8.3f} ms  rays/s={n / k * 1e3:9.3e}"
               f"  pairs/ray={pairs / n:9.1f}  Gpairs/s={pairs / k / 1e6:8.1f}", flush=True)
 
