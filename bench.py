@@ -37,7 +37,7 @@ sys.path.insert(0, ROOT)
 
 N_GEN, DIM, N_POOL, RAYS_PER_GPU = 20000, 6, 10000, 1_000_000
 METRIC = "RayCast rays/sec (config 2: d=6, N=20000)"
-FLOP_PER_PAIR = 2 * DIM + 2  # incircle-sphere test: one d-dot + one FMA per (ray, generator)
+FLOP_PER_PAIR = 2 * DIM  # incircle-sphere screen: d FMAs per (ray, generator)
 
 
 def parse():
@@ -182,8 +182,9 @@ class Clocks:
 
 
 # --------------------------------------------------------------------------
-def fp64_peak(torch, L, _lib):
-    """DFMA pipe peak measured live (MEASURED_PEAKS.json has no FP64 figure)."""
+def fma_peak(torch, L, _lib, dtype=0):
+    """DFMA (dtype 0) / FFMA (dtype 1) pipe peak measured live
+    (MEASURED_PEAKS.json has no FP64 / FP32 figure)."""
     scratch = torch.empty(16, dtype=torch.float64, device="cuda")
     sm = torch.cuda.get_device_properties(0).multi_processor_count
     blocks, iters = sm * 8, 4096
@@ -192,7 +193,7 @@ def fp64_peak(torch, L, _lib):
     for _ in range(6):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        _lib.check(L.vr_fma_probe(0, blocks, iters, _lib.ptr(scratch), sh))
+        _lib.check(L.vr_fma_probe(dtype, blocks, iters, _lib.ptr(scratch), sh))
         e1.record()
         e1.synchronize()
         best = max(best, 4096.0 * iters * blocks / (e0.elapsed_time(e1) * 1e-3) / 1e12)
@@ -267,6 +268,23 @@ def extra_configs(vb, torch, world, rank):
     return out
 
 
+def profiled_traffic():
+    """dram read + write bytes per launch of the dominant kernel, from the
+    committed ncu --set full capture (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "r1_k_raycast_pruned_ncu_full.txt")
+    if not os.path.exists(path):
+        return None
+    tot = 0.0
+    for line in open(path):
+        for key, scale in (("dram read", 1e6), ("dram write", 1e6)):
+            if line.strip().startswith(key):
+                parts = line.split()
+                val, unit = float(parts[2]), parts[3]
+                mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+                tot += val * mult
+    return tot or None
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -330,12 +348,18 @@ def run_ours(args):
     step_ms = [ev[i][0].elapsed_time(ev[i][2]) for i in range(args.warmup, args.warmup + args.steps)]
     kern_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(args.warmup, args.warmup + args.steps)]
     screened = int(work.item()) / (args.warmup + args.steps) if args.mode == "pruned" else None
-    # the exhaustive (TMA-staged, unpruned) kernel on the same rays, for its roofline
-    ex_ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    step(0, mode="exhaustive")
-    step(1, mode="exhaustive", events=ex_ev)
-    torch.cuda.synchronize()
-    ex_ms = ex_ev[0].elapsed_time(ex_ev[1])
+    # the exhaustive (TMA-staged, unpruned) kernel on the same rays, for its
+    # roofline: fp64 screen (FP64 pipe) and fp32 screen (FP32 pipe)
+    ex_ms = {}
+    for scr in ("fp64", "fp32"):
+        ex_ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        flush.fill_(7)
+        vb.raycast_batch(ns, xd, ud, gd, out=out, workspace=ws, mode="exhaustive", screen=scr)
+        flush.fill_(8)
+        vb.raycast_batch(ns, xd, ud, gd, out=out, workspace=ws, mode="exhaustive", screen=scr,
+                         events=ex_ev)
+        torch.cuda.synchronize()
+        ex_ms[scr] = ex_ev[0].elapsed_time(ex_ev[1])
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -384,11 +408,14 @@ def run_ours(args):
 
     result = None
     if rank == 0:
-        peak = fp64_peak(torch, L, _lib)
+        peak64 = fma_peak(torch, L, _lib, 0)
+        peak32 = fma_peak(torch, L, _lib, 1)
         kms = float(np.mean(kern_ms))
         pairs = screened if screened is not None else n * N_GEN
         achieved = pairs * FLOP_PER_PAIR / (kms * 1e-3) / 1e12
-        ex_achieved = n * N_GEN * FLOP_PER_PAIR / (ex_ms * 1e-3) / 1e12
+        ex64 = n * N_GEN * FLOP_PER_PAIR / (ex_ms["fp64"] * 1e-3) / 1e12
+        ex32 = n * N_GEN * FLOP_PER_PAIR / (ex_ms["fp32"] * 1e-3) / 1e12
+        traffic = profiled_traffic()
         result = {
             "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -399,19 +426,26 @@ def run_ours(args):
                        "n_generators": N_GEN, "d": DIM, "rays_per_gpu": n,
                        "parallelism": f"ray-sharded x{world}, generators replicated",
                        "l2": "flushed between timed steps (256 MB write, untimed)"},
-            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                         "kernel": ("k_raycast_pruned<6,2,64,32,10>" if args.mode == "pruned"
-                                    else "k_raycast<6,2,128,256,4,3>"),
+            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak32,
+                         "unit": "TFLOP/s", "frac": achieved / peak32, "traffic": traffic,
+                         "kernel": ("k_raycast_pruned<6,R=1,tile=64,fp32 screen>"
+                                    if args.mode == "pruned" else "k_raycast<6,2,128,256,4,3>"),
                          "kernel_ms": kms, "flop_per_pair": FLOP_PER_PAIR,
                          "pairs_per_launch": pairs, "pairs_per_ray": pairs / n,
-                         "peak_source": "measured live: DFMA probe (vr_fma_probe), "
-                                        "MEASURED_PEAKS.json has no FP64 figure"},
-            "roofline_exhaustive": {"bound": "fp64", "kernel": "k_raycast<6,2,128,256,4,3>",
-                                    "kernel_ms": ex_ms, "achieved": ex_achieved, "peak": peak,
-                                    "unit": "TFLOP/s", "frac": ex_achieved / peak,
-                                    "pairs_per_launch": n * N_GEN,
-                                    "rays_per_s": n / (ex_ms * 1e-3)},
+                         "unit_of_work": "(ray, generator) pair screened; pruned kernel counts "
+                                         "the pairs it actually screened (work counter)",
+                         "peak_source": "measured live: FFMA probe (vr_fma_probe); "
+                                        "MEASURED_PEAKS.json has no FP32/FP64 figure",
+                         "traffic_source": "profiles/r1_k_raycast_pruned_ncu_full.txt"},
+            "roofline_exhaustive": {
+                "fp64_screen": {"bound": "fp64", "kernel_ms": ex_ms["fp64"], "achieved": ex64,
+                                "peak": peak64, "unit": "TFLOP/s", "frac": ex64 / peak64,
+                                "rays_per_s": n / (ex_ms["fp64"] * 1e-3)},
+                "fp32_screen": {"bound": "fp32", "kernel_ms": ex_ms["fp32"], "achieved": ex32,
+                                "peak": peak32, "unit": "TFLOP/s", "frac": ex32 / peak32,
+                                "rays_per_s": n / (ex_ms["fp32"] * 1e-3)},
+                "kernel": "k_raycast<6,2,128,256,4,3> (TMA ring, every pair screened)",
+                "pairs_per_launch": n * N_GEN},
             "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "HostRaycaster.run (pinned host arrays)"},
             "gpu_launches": 2 * args.steps,  # fused RayCast + exact re-check per step
