@@ -140,7 +140,8 @@ typedef struct vr_prune_index {
   const int32_t* inv_perm; /* generator index -> kd position (n)               */
   const double* tile_box;  /* ceil(n/64) x 2d, [lo_0..lo_{d-1}, hi_0..]        */
   const float* tile_box32; /* same boxes, centred at vr_screen32.center, fp32
-                              rounded outward (lo down, hi up); nullable     */
+                              rounded outward (lo down, hi up), rows padded
+                              to (2d+3)&~3 floats; nullable                  */
   const double* node_box;  /* kd-tree node boxes, heap layout, x 2d            */
   const float* node_box32; /* centred fp32 outward copies; nullable            */
   const int32_t* node_range; /* 2 per node: first tile, last tile + 1        */

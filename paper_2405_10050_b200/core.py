@@ -255,7 +255,11 @@ def _outward32(lo, hi, center):
     pinf = torch.full_like(hi32, float("inf"))
     lo32 = torch.where(lo32.to(torch.float64) > lo_c, torch.nextafter(lo32, ninf), lo32)
     hi32 = torch.where(hi32.to(torch.float64) < hi_c, torch.nextafter(hi32, pinf), hi32)
-    return torch.cat([lo32, hi32], 1).contiguous()
+    d = lo.shape[1]
+    pad = ((2 * d + 3) & ~3) - 2 * d  # 16-B rows (csrc box32_stride)
+    parts = [lo32, hi32] + ([torch.zeros((lo32.shape[0], pad), dtype=torch.float32,
+                                         device=lo32.device)] if pad else [])
+    return torch.cat(parts, 1).contiguous()
 
 
 def kd_tree_layout(nt):

@@ -244,6 +244,73 @@ __device__ __forceinline__ void load_rec_g(const double* p, double (&xi)[D]) {
   if (D & 1) xi[D - 1] = __ldg(p + D - 1);
 }
 
+// Block-batched rare path for one ray: the candidates of one 8-candidate
+// block that passed the (conservative) screen, in index order.  Equivalent to
+// processing them one by one with immediate sphere updates: the final sphere
+// is that of the improving candidate with the smallest t (division-free
+// comparison, first index on exact ties), a single update; every other
+// improving candidate is re-tested against the new sphere and flags RECHECK
+// if it lies inside the new band; the previous best is tested as before.
+template <int D, bool F32>
+__device__ __forceinline__ void ray_rare_block(RayState<D>& r, const double* tile, unsigned mm,
+                                               int gbase, const Frame& fr) {
+  constexpr int S = rec_stride(D);
+  const bool have0 = r.ib >= 0;
+  double zk2[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+    zk2[k] = F32 ? (have0 ? -2.0 * fma(r.tb, r.u[k], r.x[k]) : 0.0) : r.z[k];
+  double bn = 0.0, bd = 0.0;
+  int bu = -1;
+  unsigned imp = 0u;
+  while (mm) {
+    const int u = __ffs(mm) - 1;
+    mm &= mm - 1;
+    double xi[D];
+    load_rec<D>(tile + u * S, xi);
+    double fp = tile[u * S + D], q = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      fp = fma(zk2[k], xi[k], fp);
+      q = fma(r.u[k], xi[k], q);
+    }
+    if (have0 && !(fp < r.hi)) continue;  // outside the block-start sphere's band
+    if (gbase + u == r.ib) continue;      // the current best itself
+    if (!(q > r.thr)) continue;           // behind the halfspace (raycast.py:110-117)
+    if (have0 && fp >= r.lim - r.dlt) r.near = 1;
+    if (have0 && !(fp < r.lim)) continue;
+    double aa = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const double a = r.x[k] - xi[k];
+      aa = fma(a, a, aa);
+    }
+    const double num = aa - r.base, den = q - r.s;  // raycast.py:201-203
+    if (bu < 0 || num * bd < bn * den) { bn = num; bd = den; bu = u; }
+    imp |= 1u << u;
+  }
+  if (bu < 0) return;
+  const double t = bn / (2.0 * bd);
+  const double told = r.tb, denold = r.denb;
+  ray_set_best<D, F32>(r, t, bd, gbase + bu, fr);
+  if (have0 && 2.0 * denold * (told - t) < r.dlt) r.near = 1;
+  imp &= ~(1u << bu);
+  if (imp) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) zk2[k] = -2.0 * fma(t, r.u[k], r.x[k]);
+    while (imp) {
+      const int u = __ffs(imp) - 1;
+      imp &= imp - 1;
+      double xi[D];
+      load_rec<D>(tile + u * S, xi);
+      double fp = tile[u * S + D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) fp = fma(zk2[k], xi[k], fp);
+      if (fp < r.hi) r.near = 1;  // in the new sphere's band (it has t >= t_new)
+    }
+  }
+}
+
 // Screening value of one pair: |x_i|^2 - 2 z.x_i as one chain of d FMAs
 // (z is stored pre-scaled by -2), so a pair costs d DFMA + 1 DSETP.
 template <int D>
@@ -464,16 +531,8 @@ __device__ __forceinline__ void screen_tile(RayState<D> (&ray)[R], const double*
         }
       }
 #pragma unroll
-      for (int j = 0; j < R; ++j) {
-        unsigned mm = m[j];
-        while (mm) {
-          const int u = __ffs(mm) - 1;
-          mm &= mm - 1;
-          double xi[D];
-          load_rec<D>(tile + (c + u) * S, xi);
-          ray_rare<D, F32>(ray[j], xi, tile[(c + u) * S + D], gbase + c + u, fr);
-        }
-      }
+      for (int j = 0; j < R; ++j)
+        if (m[j]) ray_rare_block<D, F32>(ray[j], tile + c * S, m[j], gbase + c, fr);
     }
   }
 }
@@ -602,14 +661,29 @@ __device__ __forceinline__ bool ray_needs_box(const RayState<D>& r, const double
 // fp32 box test in the centred frame (boxes rounded outward on the host):
 // skip only if the fp32 bounds certify "behind the halfspace" or "outside the
 // sphere + band" for the exact box.  box32 = [lo_0..lo_{D-1}, hi_0..hi_{D-1}].
+// fp32 box records: [lo_0..lo_{D-1}, hi_0..hi_{D-1}] padded to a multiple
+// of 4 floats (16-B rows, loaded as float4).
+__host__ __device__ constexpr int box32_stride(int d) { return (2 * d + 3) & ~3; }
+
 template <int D>
 __device__ __forceinline__ bool ray_needs_box32(const RayState<D>& r,
                                                 const float* __restrict__ box) {
+  constexpr int BS = box32_stride(D);
+  float v[BS];
+  const float4* b4 = reinterpret_cast<const float4*>(box);
+#pragma unroll
+  for (int k = 0; k < BS / 4; ++k) {
+    const float4 w = __ldg(b4 + k);
+    v[4 * k] = w.x;
+    v[4 * k + 1] = w.y;
+    v[4 * k + 2] = w.z;
+    v[4 * k + 3] = w.w;
+  }
   float lo[D], hi[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    lo[k] = __ldg(box + k);
-    hi[k] = __ldg(box + D + k);
+    lo[k] = v[k];
+    hi[k] = v[D + k];
   }
   float umax = 0.0f, d2 = 0.0f;
 #pragma unroll
@@ -626,7 +700,7 @@ __device__ __forceinline__ bool ray_needs_box32(const RayState<D>& r,
 template <int D, bool F32>
 __device__ __forceinline__ bool ray_needs(const RayState<D>& r, const double* __restrict__ box64,
                                           const float* __restrict__ box32, int64_t b) {
-  if constexpr (F32) return ray_needs_box32<D>(r, box32 + b * 2 * D);
+  if constexpr (F32) return ray_needs_box32<D>(r, box32 + b * box32_stride(D));
   else return ray_needs_box<D>(r, box64 + b * 2 * D);
 }
 
@@ -683,41 +757,63 @@ __device__ __forceinline__ void seed_tile(RayState<D> (&ray)[R], const double* _
 // holding the warp's start tile is visited first.
 template <int D, int R, bool F32>
 struct TreeCursor {
-  static constexpr int MAXS = 48;
-  int stack[MAXS];
+  // Warp-distributed stack: slot i lives in lane i's registers (push = one
+  // lane writes, pop = shuffle), so the DFS touches no local memory.  The DFS
+  // holds at most depth + 1 <= 32 entries for trees of < 2^31 tiles.
+  int s_node = 0, s_lo = 0, s_hi = 0;
   int sp = 0;
   int64_t st = 0;
   unsigned long long tests = 0;
-  __device__ __forceinline__ void init(int64_t start_tile) {
+  __device__ __forceinline__ bool warp_needs(const RayState<D> (&ray)[R],
+                                             const double* __restrict__ node_box,
+                                             const float* __restrict__ node_box32, int node) {
+    bool need = false;
+#pragma unroll
+    for (int j = 0; j < R; ++j) need |= ray_needs<D, F32>(ray[j], node_box, node_box32, node);
+    ++tests;
+    return __any_sync(0xffffffffu, need);
+  }
+  __device__ __forceinline__ void push(int node, int2 rg) {
+    if (sp >= 32) __trap();
+    if ((int)(threadIdx.x & 31) == sp) {
+      s_node = node;
+      s_lo = rg.x;
+      s_hi = rg.y;
+    }
+    ++sp;
+  }
+  __device__ __forceinline__ void init(int64_t start_tile, const RayState<D> (&ray)[R],
+                                       const double* __restrict__ node_box,
+                                       const float* __restrict__ node_box32,
+                                       const int2* __restrict__ node_range) {
     st = start_tile;
     sp = 0;
-    stack[sp++] = 0;
+    if (warp_needs(ray, node_box, node_box32, 0)) push(0, __ldg(node_range));
   }
+  // Children are tested when their parent is expanded (both boxes loaded
+  // together, one dependent step per level); a popped leaf is returned.
   __device__ __forceinline__ int64_t next(const RayState<D> (&ray)[R],
                                           const double* __restrict__ node_box,
                                           const float* __restrict__ node_box32,
                                           const int2* __restrict__ node_range) {
     while (sp > 0) {
-      const int node = stack[--sp];
-      const int2 rg = __ldg(node_range + node);
-      bool need = false;
-#pragma unroll
-      for (int j = 0; j < R; ++j) need |= ray_needs<D, F32>(ray[j], node_box, node_box32, node);
-      if (!__any_sync(0xffffffffu, need)) continue;
-      ++tests;
-      if (rg.y - rg.x == 1) return rg.x;
+      --sp;
+      const int node = __shfl_sync(0xffffffffu, s_node, sp);
+      const int lo = __shfl_sync(0xffffffffu, s_lo, sp);
+      const int hi = __shfl_sync(0xffffffffu, s_hi, sp);
+      if (hi - lo == 1) return lo;
       const int l = 2 * node + 1, r = 2 * node + 2;
-      if (sp + 2 > MAXS) __trap();  // depth > 46: impossible for < 2^46 tiles
+      const int2 rl = __ldg(node_range + l), rr = __ldg(node_range + r);
+      const bool nl = warp_needs(ray, node_box, node_box32, l);
+      const bool nr = warp_needs(ray, node_box, node_box32, r);
       // the child holding the warp's start tile first (kd index order is
       // spatial order, so this visits the rays' neighbourhood early)
-      const int mid = rg.x + (rg.y - rg.x) / 2;
-      const float dl = st < mid ? 0.0f : 1.0f, dr = 1.0f - dl;
-      if (dl <= dr) {
-        stack[sp++] = r;
-        stack[sp++] = l;
+      if (st < rl.y) {
+        if (nr) push(r, rr);
+        if (nl) push(l, rl);
       } else {
-        stack[sp++] = l;
-        stack[sp++] = r;
+        if (nl) push(l, rl);
+        if (nr) push(r, rr);
       }
     }
     return -1;
@@ -738,6 +834,8 @@ __global__ void __launch_bounds__(32, MINB)
                      Frame fr, RayOut out, unsigned long long* __restrict__ work) {
   constexpr int S = rec_stride(D);
   constexpr int S32 = rec32_stride(D);
+  // both copies are staged: the fp64 rows feed the rare path, which is hit
+  // often enough (tens of entries per ray at d=8) that global loads stall
   constexpr uint32_t BYTES64 = (uint32_t)(PT * S * sizeof(double));
   constexpr uint32_t BYTES32 = F32 ? (uint32_t)(PT * S32 * sizeof(float)) : 0u;
   static_assert(PT % 8 == 0 && VR_REC_PAD % PT == 0, "tile must divide the record padding");
@@ -765,7 +863,7 @@ __global__ void __launch_bounds__(32, MINB)
   st = __shfl_sync(0xffffffffu, st, 0);
   seed_tile<D, R, PT, F32>(ray, crec + st * PT * S, (int)(st * PT), fr);
   TreeCursor<D, R, F32> cur;
-  cur.init(st);
+  cur.init(st, ray, node_box, node_box32, node_range);
 
   auto issue = [&](int64_t t, int b) {
     if (lane == 0) {
