@@ -30,8 +30,8 @@ from . import _lib
 from . import rng as _rng
 from .core import (TOL_VERTEX, Mesh, NodeSet, VertexRecord, edge_keys, verify_vertices)
 from .errors import DegenerateConfiguration, RetryExhausted
-from .raycast import (RayQuery, RaycastStats, _orthonormal_rows, _project_out, raycast_batch,
-                      raycast_incircle)
+from .raycast import (RANK_TOL, RayQuery, RaycastStats, _orthonormal_rows, _project_out,
+                      raycast_batch, raycast_incircle)
 
 DESCENT_RETRIES = 100
 
@@ -88,60 +88,105 @@ def descent(ns: NodeSet, start_index: int, rng=None, stats: RaycastStats = None,
     return VertexRecord(sigma, r)
 
 
+def _mgs_batch(rows):
+    """Two-pass modified Gram-Schmidt of each (k, d) row block of `rows`
+    (m, k, d), vectorised over m (raycast.py:295-308 per block)."""
+    m, k, d = rows.shape
+    out = np.zeros_like(rows)
+    for j in range(k):
+        v = rows[:, j, :].copy()
+        n0 = np.sqrt(np.einsum("md,md->m", v, v))
+        for _ in range(2):
+            for i in range(j):
+                qv = out[:, i, :]
+                v -= np.einsum("md,md->m", qv, v)[:, None] * qv
+        nv = np.sqrt(np.einsum("md,md->m", v, v))
+        if np.any(nv < RANK_TOL * np.maximum(n0, 1.0)):
+            raise DegenerateConfiguration("generators are affinely dependent")
+        out[:, j, :] = v / nv[:, None]
+    return out
+
+
+def _project_out_batch(w, basis):
+    """Component of each w (m, d) orthogonal to its basis rows (m, k, d)."""
+    v = w.copy()
+    for _ in range(2):
+        for i in range(basis.shape[1]):
+            qv = basis[:, i, :]
+            v -= np.einsum("md,md->m", qv, v)[:, None] * qv
+    return v
+
+
 def descent_batch(ns: NodeSet, starts, seed: int = 0, stats: RaycastStats = None,
                   rngs=None):
-    """Many descents at once; same RNG streams and results as calling
-    :func:`descent` with ``stream(seed, "descent", s)`` for every start.
+    """Many descents at once; the same RNG streams and sigma as calling
+    :func:`descent` with ``stream(seed, "descent", s)`` for every start
+    (graph.py:46-85), with the Gram-Schmidt projections vectorised over the
+    starts of a level and one GPU RayCast launch per level.
 
     Returns (sigma (S, d+1) int32, r (S, d) fp64)."""
     pts = ns.points
     d = ns.dim
-    starts = [int(s) for s in starts]
+    starts = np.asarray([int(s) for s in starts], dtype=np.int64)
     S = len(starts)
     if rngs is None:
-        rngs = [_rng.stream(seed, "descent", s) for s in starts]
-    sig = [(s,) for s in starts]
-    rr = [np.array(pts[s], dtype=float) for s in starts]
-    basis = [[] for _ in starts]
-    fails = [0] * S
-    active = list(range(S))
-    while active:
-        groups = {}
-        for a in active:
-            while True:
-                u = _project_out(rngs[a].standard_normal(d), basis[a])
-                norm = np.linalg.norm(u)
-                if norm >= 1e-9:
-                    break
-            groups.setdefault(len(sig[a]), []).append((a, u / norm))
+        rngs = [_rng.stream(seed, "descent", int(s)) for s in starts]
+    sig = np.full((S, d + 1), -1, dtype=np.int64)
+    sig[:, 0] = starts
+    k = np.ones(S, dtype=np.int64)          # |sigma|
+    rr = pts[starts].astype(np.float64).copy()
+    basis = np.zeros((S, d, d))             # orthonormal rows, first k-1 valid
+    fails = np.zeros(S, dtype=np.int64)
+    active = np.arange(S)
+    while active.size:
+        # one direction per active start, drawn from its own stream in the
+        # reference order (redraw while the projection vanishes)
+        u = np.empty((active.size, d))
+        for kk in np.unique(k[active]):
+            grp = active[k[active] == kk]
+            pos = np.searchsorted(active, grp)
+            z = np.stack([rngs[a].standard_normal(d) for a in grp])
+            v = _project_out_batch(z, basis[grp, :kk - 1])
+            nrm = np.linalg.norm(v, axis=1)
+            for m in np.nonzero(nrm < 1e-9)[0]:  # free redraws (graph.py:72-74)
+                a = grp[m]
+                while True:
+                    vv = _project_out_batch(rngs[a].standard_normal(d)[None], basis[a:a + 1, :kk - 1])[0]
+                    if np.linalg.norm(vv) >= 1e-9:
+                        v[m] = vv
+                        nrm[m] = np.linalg.norm(vv)
+                        break
+            u[pos] = v / nrm[:, None]
         still = []
-        for k, items in sorted(groups.items()):
-            ids = [a for a, _ in items]
-            x = np.stack([rr[a] for a in ids])
-            u = np.stack([v for _, v in items])
-            eta = np.array([sig[a] for a in ids], dtype=np.int32).reshape(len(ids), k)
-            res = raycast_batch(ns, x, u, eta, stats=stats)
+        for kk in np.unique(k[active]):
+            sel = k[active] == kk
+            grp = active[sel]
+            res = raycast_batch(ns, rr[grp], u[sel], sig[grp, :kk].astype(np.int32), stats=stats)
             idx, _, rp, flag = res.to_host()
-            for m, a in enumerate(ids):
-                if flag[m] == 1:
-                    fails[a] += 1
-                    if fails[a] >= DESCENT_RETRIES:
-                        raise RetryExhausted(
-                            f"descent from node {starts[a]} stuck at level {len(sig[a])}")
-                    still.append(a)
-                    continue
-                if flag[m] == 3:
-                    from .errors import DegenerateConfiguration
-                    raise DegenerateConfiguration(
-                        f"degenerate raycast during descent from node {starts[a]}")
-                sig[a] = tuple(sorted((*sig[a], int(idx[m]))))
-                rr[a] = rp[m]
-                fails[a] = 0
-                if len(sig[a]) < d + 1:
-                    basis[a] = _orthonormal_rows(pts[list(sig[a][1:])] - pts[sig[a][0]])
-                    still.append(a)
-        active = sorted(still)
-    return np.array(sig, dtype=np.int32), np.array(rr, dtype=np.float64)
+            esc = flag == 1
+            if (flag == 3).any():
+                raise DegenerateConfiguration(
+                    f"degenerate raycast during descent from node {int(starts[grp[np.argmax(flag == 3)]])}")
+            fails[grp[esc]] += 1
+            if (fails[grp[esc]] >= DESCENT_RETRIES).any():
+                a = grp[esc][np.argmax(fails[grp[esc]] >= DESCENT_RETRIES)]
+                raise RetryExhausted(f"descent from node {int(starts[a])} stuck at level {kk}")
+            still.extend(grp[esc].tolist())
+            ok = ~esc
+            g_ok = grp[ok]
+            if g_ok.size:
+                new = np.sort(np.concatenate([sig[g_ok, :kk], idx[ok, None].astype(np.int64)], 1), 1)
+                sig[g_ok, :kk + 1] = new
+                k[g_ok] = kk + 1
+                rr[g_ok] = rp[ok]
+                fails[g_ok] = 0
+                cont = g_ok if kk + 1 < d + 1 else g_ok[:0]
+                if cont.size:
+                    diffs = pts[sig[cont, 1:kk + 1]] - pts[sig[cont, 0]][:, None, :]
+                    basis[cont, :kk] = _mgs_batch(diffs)
+                    still.extend(cont.tolist())
+        active = np.array(sorted(still), dtype=np.int64)
+    return sig.astype(np.int32), rr
 
 
 # ---------------------------------------------------------------------------
