@@ -261,6 +261,29 @@ int vr_mc_reduce(const double* rec, int d, const int32_t* cells,
                  int64_t* out_first_bad, double* out_samples /* nullable */,
                  void* stream);
 
+/* MC with an integrand (reference mc_integrate_cell, integrate_mc.py:70-121):
+ * as vr_mc_reduce (degenerate rays always count), plus per-face surface
+ * integrals sum_rays f(rp) w and the volume integral
+ * sum_rays [sum_{s<m} f(x_c + t_s seg) t_s^(d-1)] length^d, scaled like the
+ * reference.  integrand_kind: 1 const (coef[0]), 2 sin(x_1^2), 3 linear
+ * (coef[0..d-1] . x + coef[d]) -- the reference's built-ins
+ * (integrands.py:10-44); `coef` is a HOST array (copied into the launch).  Subsample positions t_s come from `unif`
+ * ((n_rays, m) replayed uniforms) or, when NULL, from Philox counter
+ * (ray, cell, 0x100 + s/2, 'MU') keyed by `seed`. */
+int vr_mc_integrate(const double* rec, int d, const int32_t* cells, int64_t n_cells,
+                    int64_t rays_per_cell, const double* dirs, uint64_t seed,
+                    const int32_t* ray_idx, const double* ray_t,
+                    const uint8_t* ray_flag, int max_faces, double surf,
+                    int integrand_kind, const double* coef, int m_sub,
+                    const double* unif, double* out_volume, int32_t* out_face_j,
+                    double* out_face_area, double* out_face_surf,
+                    double* out_vol_integral, int32_t* out_nfaces,
+                    int32_t* out_status, int64_t* out_first_bad, void* stream);
+
+/* The Philox subsample uniforms of vr_mc_integrate, (n, m) fp64. */
+int vr_mc_uniforms(int64_t n_cells, const int32_t* cells, int64_t rays_per_cell,
+                   int m_sub, uint64_t seed, double* out_u, void* stream);
+
 /* Export the unit directions the Philox path uses (for RNG replay into the
  * reference, SURVEY.md §8(c) rule 4): raw Gaussian draws z, (n, d) fp64. */
 int vr_mc_directions(int d, int64_t n_cells, const int32_t* cells,

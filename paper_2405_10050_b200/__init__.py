@@ -16,7 +16,10 @@ from .raycast import (RayQuery, RaycastBatch, RaycastStats, initial_heuristic, p
 from .graph import (DESCENT_RETRIES, VerifyReport, brute_force_vertices, circumcenters, descent,
                     descent_batch, edge_set, verify_mesh, voronoi_graph, voronoi_local)
 from .integrate_mc import (CellIntegrals, Integrand, MCResult, mc_areas_only, mc_cells,
-                           mc_directions, sample_unit_sphere, sphere_surface_area)
+                           mc_directions, mc_integrals_cells, mc_integrate_cell, mc_uniforms,
+                           sample_unit_sphere, sphere_surface_area)
+from . import integrands, io
+from .integrate_hmc import hmc_cell_integral, hmc_interface_integral, hmc_volume
 
 __version__ = "0.1.0"
 
@@ -29,5 +32,6 @@ __all__ = [
     "VerifyReport",
     "brute_force_vertices", "circumcenters", "DESCENT_RETRIES", "CellIntegrals", "Integrand",
     "MCResult", "sample_unit_sphere", "sphere_surface_area", "mc_areas_only", "mc_cells",
-    "mc_directions", "errors", "rng",
+    "mc_directions", "mc_integrate_cell", "mc_integrals_cells", "mc_uniforms", "integrands",
+    "errors", "rng", "io", "hmc_volume", "hmc_interface_integral", "hmc_cell_integral",
 ]

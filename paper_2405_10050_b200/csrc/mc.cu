@@ -28,35 +28,75 @@ __device__ __forceinline__ void bitonic_sort_u64(unsigned long long* keys, int n
   }
 }
 
+// Integrand on the device for the CLI's built-ins (reference integrands.py):
+// kind 1 const c, 2 sin(x_1^2), 3 linear a.x + b.
+struct Integ {
+  int kind;      // 0: areas/volume only
+  int m;         // subsamples per ray
+  double coef[VR_MAX_D + 1];
+  const double* unif;  // nullable: replayed uniforms (n_rays, m); else Philox
+};
+
 template <int D>
+__device__ __forceinline__ double integrand(const Integ& f, const double (&p)[D]) {
+  if (f.kind == 1) return f.coef[0];
+  if (f.kind == 2) return sin(p[0] * p[0]);
+  double v = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) v = fma(f.coef[k], p[k], v);
+  return v + f.coef[D];
+}
+
+// Subsample uniform s of ray `ray` of generator `cell`: Philox counter
+// (ray, cell, 0x100 + s/2, 'MU'), two 53-bit uniforms in [0, 1) per call.
+__device__ __forceinline__ double philox_uniform(uint64_t seed, int64_t cell, int64_t ray, int s) {
+  uint32_t c[4] = {(uint32_t)ray, (uint32_t)cell,
+                   (0x100u + (uint32_t)(s >> 1)) | ((uint32_t)(ray >> 32) << 16),
+                   0x4D550000u | (uint32_t)((cell >> 32) & 0xFFFF)};
+  philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  const uint64_t a = (s & 1) ? ((((uint64_t)c[2]) << 32) | c[3]) : ((((uint64_t)c[0]) << 32) | c[1]);
+  return (double)(a >> 11) * 0x1.0p-53;
+}
+
+template <int D, bool INTEG>
 __global__ void __launch_bounds__(RED_NT)
     k_mc_reduce(SrcMC<D> src, const int32_t* __restrict__ ray_idx, const double* __restrict__ ray_t,
                 const uint8_t* __restrict__ ray_flag, int max_faces, int degenerate_is_error,
-                double surf, double* out_volume, int32_t* out_face_j, double* out_face_area,
-                int32_t* out_nfaces, int32_t* out_status, int64_t* out_first_bad,
-                double* out_samples) {
+                double surf, Integ fi, double* out_volume, int32_t* out_face_j,
+                double* out_face_area, int32_t* out_nfaces, int32_t* out_status,
+                int64_t* out_first_bad, double* out_samples, double* out_face_surf,
+                double* out_vol_integral) {
   constexpr int S = rec_stride(D);
-  __shared__ unsigned long long keys[RED_CHUNK];
-  __shared__ double wv[RED_CHUNK];
-  __shared__ double lv[RED_CHUNK];
+  constexpr int CH = INTEG ? 512 : RED_CHUNK;  // rays per chunk (smem budget)
+  __shared__ unsigned long long keys[RED_MAPCAP];
+  __shared__ double wv[CH];
+  __shared__ double lv[CH];
+  __shared__ double sv[INTEG ? CH : 1];   // f(rp) w          (integrate_mc.py:350)
+  __shared__ double fv[INTEG ? CH : 1];   // acc * length^d   (integrate_mc.py:356)
   __shared__ int mkey[RED_MAPCAP];
   __shared__ double macc[RED_MAPCAP];
+  __shared__ double macc2[INTEG ? RED_MAPCAP : 1];
   __shared__ unsigned long long first_bad;  // (ray << 2) | kind
   __shared__ int nused;
 
   const int64_t c = blockIdx.x;
   const int64_t per = src.per;
-  const double* xc = src.grec + (int64_t)src.cells[c] * S;
-  for (int i = threadIdx.x; i < RED_MAPCAP; i += RED_NT) { mkey[i] = -1; macc[i] = 0.0; }
+  const int32_t cell = src.cells[c];
+  const double* xc = src.grec + (int64_t)cell * S;
+  for (int i = threadIdx.x; i < RED_MAPCAP; i += RED_NT) {
+    mkey[i] = -1;
+    macc[i] = 0.0;
+    if (INTEG) macc2[i] = 0.0;
+  }
   if (threadIdx.x == 0) { first_bad = ~0ull; nused = 0; }
-  double vol = 0.0;  // thread 0 only: sequential sum in ray order (integrate_mc.py:155)
+  double vol = 0.0, fvol = 0.0;  // thread 0 only: sequential sums in ray order
   __syncthreads();
 
-  for (int64_t start = 0; start < per; start += RED_CHUNK) {
-    const int cnt = (int)min((int64_t)RED_CHUNK, per - start);
-    for (int s = threadIdx.x; s < RED_CHUNK; s += RED_NT) {
+  for (int64_t start = 0; start < per; start += CH) {
+    const int cnt = (int)min((int64_t)CH, per - start);
+    for (int s = threadIdx.x; s < CH; s += RED_NT) {
       unsigned long long key = ~0ull;
-      double w = 0.0, ld = 0.0;
+      double w = 0.0, ld = 0.0, sw = 0.0, fl_v = 0.0;
       if (s < cnt) {
         const int64_t r = start + s;
         const int64_t k = c * per + r;
@@ -68,15 +108,15 @@ __global__ void __launch_bounds__(RED_NT)
         } else {
           const int32_t j = ray_idx[k];
           const double t = ray_t[k];
-          double y[D];
+          double y[D], rp[D], seg[D];
           src.direction(k, y);
           const double* xj = src.grec + (int64_t)j * S;
           double ss = 0.0, nd = 0.0, nn = 0.0;
 #pragma unroll
           for (int q = 0; q < D; ++q) {
-            const double rp = fma(t, y[q], xc[q]);  // rp = xi + t y  (raycast.py:210)
-            const double seg = rp - xc[q];           // integrate_mc.py:151
-            ss = fma(seg, seg, ss);
+            rp[q] = fma(t, y[q], xc[q]);  // rp = xi + t y  (raycast.py:210)
+            seg[q] = rp[q] - xc[q];       // integrate_mc.py:151
+            ss = fma(seg[q], seg[q], ss);
             const double nij = xj[q] - xc[q];
             nd = fma(nij, y[q], nd);
             nn = fma(nij, nij, nn);
@@ -90,25 +130,51 @@ __global__ void __launch_bounds__(RED_NT)
           ld = p * length;         // length^d
           key = ((unsigned long long)(uint32_t)j << 32) | (unsigned)s;
           if (out_samples) out_samples[k] = ld;
+          if constexpr (INTEG) {
+            sw = integrand<D>(fi, rp) * w;
+            double acc = 0.0;
+            for (int m = 0; m < fi.m; ++m) {
+              const double tm = fi.unif ? fi.unif[k * fi.m + m]
+                                        : philox_uniform(src.seed, cell, r, m);
+              double pt[D];
+#pragma unroll
+              for (int q = 0; q < D; ++q) pt[q] = fma(tm, seg[q], xc[q]);
+              double tp = 1.0;
+#pragma unroll
+              for (int q = 0; q < D - 1; ++q) tp *= tm;
+              acc += integrand<D>(fi, pt) * tp;  // integrate_mc.py:354-355
+            }
+            fl_v = acc * ld;
+          }
         }
       }
       keys[s] = key;
       wv[s] = w;
       lv[s] = ld;
+      if constexpr (INTEG) {
+        sv[s] = sw;
+        fv[s] = fl_v;
+      }
     }
+    for (int s = CH + threadIdx.x; s < RED_MAPCAP; s += RED_NT) keys[s] = ~0ull;
     __syncthreads();
     if (threadIdx.x == 0) {
-      for (int s = 0; s < cnt; ++s) vol += lv[s];
+      for (int s = 0; s < cnt; ++s) {
+        vol += lv[s];
+        if (INTEG) fvol += fv[s];
+      }
     }
-    bitonic_sort_u64(keys, RED_CHUNK);
-    for (int p = threadIdx.x; p < RED_CHUNK; p += RED_NT) {
+    bitonic_sort_u64(keys, CH);
+    for (int p = threadIdx.x; p < CH; p += RED_NT) {
       const unsigned long long key = keys[p];
       if (key == ~0ull) continue;
       const uint32_t j = (uint32_t)(key >> 32);
       if (p > 0 && (uint32_t)(keys[p - 1] >> 32) == j) continue;  // not a segment head
-      double sum = 0.0;  // ray order inside the segment (keys sorted by (j, ray))
-      for (int q = p; q < RED_CHUNK && keys[q] != ~0ull && (uint32_t)(keys[q] >> 32) == j; ++q)
+      double sum = 0.0, sum2 = 0.0;  // ray order inside the segment (keys sorted by (j, ray))
+      for (int q = p; q < CH && keys[q] != ~0ull && (uint32_t)(keys[q] >> 32) == j; ++q) {
         sum += wv[keys[q] & 0xffffffffu];
+        if (INTEG) sum2 += sv[keys[q] & 0xffffffffu];
+      }
       unsigned h = (j * 2654435761u) & (RED_MAPCAP - 1);
       bool placed = false;
       for (int probe = 0; probe < RED_MAPCAP; ++probe) {
@@ -117,8 +183,12 @@ __global__ void __launch_bounds__(RED_NT)
         if (prev == (int)j) { placed = true; break; }
         h = (h + 1) & (RED_MAPCAP - 1);
       }
-      if (placed) macc[h] += sum;  // one head per face per chunk: single writer
-      else atomicAdd(&nused, RED_MAPCAP);  // map full: reported as OVERFLOW
+      if (placed) {
+        macc[h] += sum;  // one head per face per chunk: single writer
+        if (INTEG) macc2[h] += sum2;
+      } else {
+        atomicAdd(&nused, RED_MAPCAP);  // map full: reported as OVERFLOW
+      }
     }
     __syncthreads();
   }
@@ -129,14 +199,16 @@ __global__ void __launch_bounds__(RED_NT)
   __syncthreads();
   bitonic_sort_u64(keys, RED_MAPCAP);
   const int nf = nused;
-  const double scale = surf / (double)per;  // integrate_mc.py:157-158
+  const double scale = surf / (double)per;  // integrate_mc.py:357-358
   for (int p = threadIdx.x; p < nf && p < max_faces; p += RED_NT) {
     const unsigned long long key = keys[p];
     out_face_j[c * max_faces + p] = (int32_t)(key >> 32);
     out_face_area[c * max_faces + p] = macc[key & 0xffffffffu] * scale;
+    if (INTEG) out_face_surf[c * max_faces + p] = macc2[key & 0xffffffffu] * scale;
   }
   if (threadIdx.x == 0) {
-    out_volume[c] = vol * surf / (double)((int64_t)D * per);  // integrate_mc.py:159
+    out_volume[c] = vol * surf / (double)((int64_t)D * per);  // integrate_mc.py:359-360
+    if (INTEG) out_vol_integral[c] = fvol * surf / (double)(per * (int64_t)fi.m);  // :363
     out_nfaces[c] = nf < max_faces ? nf : max_faces;
     int status = VR_CELL_OK;
     int64_t fb = -1;
@@ -216,12 +288,48 @@ extern "C" int vr_mc_reduce(const double* rec, int d, const int32_t* cells, int6
   if (n_cells <= 0) return VR_OK;
   VR_DISPATCH_D(d, {
     SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n_cells * rays_per_cell};
-    k_mc_reduce<D><<<(unsigned)n_cells, RED_NT, 0, as_stream(stream)>>>(
-        src, ray_idx, ray_t, ray_flag, max_faces, degenerate_is_error, surf, out_volume,
-        out_face_j, out_face_area, out_nfaces, out_status, out_first_bad, out_samples);
+    Integ fi{};
+    k_mc_reduce<D, false><<<(unsigned)n_cells, RED_NT, 0, as_stream(stream)>>>(
+        src, ray_idx, ray_t, ray_flag, max_faces, degenerate_is_error, surf, fi, out_volume,
+        out_face_j, out_face_area, out_nfaces, out_status, out_first_bad, out_samples, nullptr,
+        nullptr);
   });
   VR_RETURN_LAUNCH();
 }
+
+extern "C" int vr_mc_integrate(const double* rec, int d, const int32_t* cells, int64_t n_cells,
+                               int64_t rays_per_cell, const double* dirs, uint64_t seed,
+                               const int32_t* ray_idx, const double* ray_t,
+                               const uint8_t* ray_flag, int max_faces, double surf,
+                               int integrand_kind, const double* coef, int m_sub,
+                               const double* unif, double* out_volume, int32_t* out_face_j,
+                               double* out_face_area, double* out_face_surf,
+                               double* out_vol_integral, int32_t* out_nfaces,
+                               int32_t* out_status, int64_t* out_first_bad, void* stream) {
+  if (!rec || !cells || !ray_idx || !ray_t || !ray_flag || !out_volume || !out_face_j ||
+      !out_face_area || !out_face_surf || !out_vol_integral || !out_nfaces || !out_status ||
+      !out_first_bad || m_sub < 1 || integrand_kind < 1 || integrand_kind > 3)
+    return VR_EINVAL;
+  if (max_faces <= 0 || max_faces > RED_MAPCAP / 2) return VR_EINVAL;
+  if (n_cells <= 0) return VR_OK;
+  Integ fi{};
+  fi.kind = integrand_kind;
+  fi.m = m_sub;
+  fi.unif = unif;
+  const int ncoef = integrand_kind == 1 ? 1 : (integrand_kind == 3 ? d + 1 : 0);
+  for (int k = 0; k < ncoef; ++k) fi.coef[k] = coef[k];
+  VR_DISPATCH_D(d, {
+    SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n_cells * rays_per_cell};
+    k_mc_reduce<D, true><<<(unsigned)n_cells, RED_NT, 0, as_stream(stream)>>>(
+        src, ray_idx, ray_t, ray_flag, max_faces, 1, surf, fi, out_volume, out_face_j,
+        out_face_area, out_nfaces, out_status, out_first_bad, nullptr, out_face_surf,
+        out_vol_integral);
+  });
+  VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_mc_uniforms(int64_t n_cells, const int32_t* cells, int64_t rays_per_cell,
+                              int m_sub, uint64_t seed, double* out_u, void* stream);
 
 extern "C" int vr_mc_directions(int d, int64_t n_cells, const int32_t* cells,
                                 int64_t rays_per_cell, uint64_t seed, double* out_z,
@@ -257,4 +365,24 @@ extern "C" int vr_mc_rays_pruned(const double* rec, int64_t n_gen, int d, double
                                     reinterpret_cast<unsigned long long*>(work));
   });
   return VR_OK;
+}
+
+namespace {
+__global__ void k_mc_unif(const int32_t* cells, int64_t per, int64_t n, int m, uint64_t seed,
+                          double* out) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t c = k / per;
+  for (int s = 0; s < m; ++s) out[k * m + s] = philox_uniform(seed, cells[c], k - c * per, s);
+}
+}  // namespace
+
+extern "C" int vr_mc_uniforms(int64_t n_cells, const int32_t* cells, int64_t rays_per_cell,
+                              int m_sub, uint64_t seed, double* out_u, void* stream) {
+  if (!cells || !out_u || rays_per_cell <= 0 || m_sub < 1) return VR_EINVAL;
+  const int64_t n = n_cells * rays_per_cell;
+  if (n <= 0) return VR_OK;
+  k_mc_unif<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(cells, rays_per_cell, n,
+                                                                        m_sub, seed, out_u);
+  VR_RETURN_LAUNCH();
 }

@@ -249,3 +249,157 @@ def mc_areas_only(ns: NodeSet, i: int, n: int, rng, neighbors=None,
     areas = res.areas(0)
     volume = float(res.volume[0])
     return (areas, volume, res.samples) if return_samples else (areas, volume)
+
+
+def _draw_integrate_stream(rng, n, m, d):
+    """Directions and subsample positions in the reference's RNG order
+    (integrate_mc.py:341-355): per ray one sample_unit_sphere draw (raw
+    normals, redrawn while the norm is 0), then m uniforms."""
+    z = np.empty((n, d))
+    u = np.empty((n, m))
+    for k in range(n):
+        while True:
+            y = np.asarray(rng.standard_normal(d), dtype=float)
+            if math.sqrt(float(y @ y)) > 0.0:
+                break
+        z[k] = y
+        for s in range(m):
+            u[k, s] = rng.random()
+    return z, u
+
+
+def _integrate_device(ns, cells, n, m, kind, coef, dirs=None, unif=None, seed=0,
+                      candidates=None, max_faces=256, stats=None, workspace=None):
+    L = _lib.lib()
+    out = _mc_device(ns, cells, n, dirs=dirs, seed=seed, candidates=candidates,
+                     max_faces=max_faces, degenerate_is_error=True, stats=stats,
+                     workspace=workspace)
+    rec, _ = ns.device_records()
+    dev = rec.device
+    d = ns.dim
+    cells_d = torch.as_tensor(np.ascontiguousarray(cells, dtype=np.int32), device=dev)
+    nc = cells_d.shape[0]
+    dd = None if dirs is None else torch.as_tensor(
+        np.ascontiguousarray(dirs, dtype=np.float64), device=dev)
+    ud = None if unif is None else torch.as_tensor(
+        np.ascontiguousarray(unif, dtype=np.float64), device=dev)
+    cf = (ctypes.c_double * 9)(*(list(coef) + [0.0] * (9 - len(coef))))  # host array
+    vol = torch.empty(nc, dtype=torch.float64, device=dev)
+    fj = torch.empty((nc, max_faces), dtype=torch.int32, device=dev)
+    fa = torch.empty((nc, max_faces), dtype=torch.float64, device=dev)
+    fs = torch.empty((nc, max_faces), dtype=torch.float64, device=dev)
+    vi = torch.empty(nc, dtype=torch.float64, device=dev)
+    nf = torch.empty(nc, dtype=torch.int32, device=dev)
+    st = torch.empty(nc, dtype=torch.int32, device=dev)
+    fb = torch.empty(nc, dtype=torch.int64, device=dev)
+    _lib.check(L.vr_mc_integrate(_lib.ptr(rec), d, _lib.ptr(cells_d), nc, n, _lib.ptr(dd),
+                                 int(seed) & 0xFFFFFFFFFFFFFFFF, _lib.ptr(out["ray_idx"]),
+                                 _lib.ptr(out["ray_t"]), _lib.ptr(out["ray_flag"]), max_faces,
+                                 sphere_surface_area(d), int(kind), cf, int(m),
+                                 _lib.ptr(ud), _lib.ptr(vol), _lib.ptr(fj), _lib.ptr(fa),
+                                 _lib.ptr(fs), _lib.ptr(vi), _lib.ptr(nf), _lib.ptr(st),
+                                 _lib.ptr(fb), _lib.stream_handle()), "vr_mc_integrate")
+    return dict(volume=vol.cpu().numpy(), face_j=fj.cpu().numpy(), face_area=fa.cpu().numpy(),
+                face_surf=fs.cpu().numpy(), vol_integral=vi.cpu().numpy(),
+                nfaces=nf.cpu().numpy(), status=st.cpu().numpy(), first_bad=fb.cpu().numpy(),
+                ray_idx=out["ray_idx"], ray_t=out["ray_t"], ray_flag=out["ray_flag"])
+
+
+def mc_integrate_cell(ns: NodeSet, i: int, f: Integrand, n: int, m: int, rng,
+                      neighbors=None, stats: RaycastStats = None) -> CellIntegrals:
+    """Volume, face areas, and surface / volume integrals of cell i
+    (integrate_mc.py:70-121), same RNG consumption order as the reference.
+
+    Every ray is cast on the GPU.  Built-in integrands
+    (:mod:`paper_2405_10050_b200.integrands`) are evaluated in the reduction
+    kernel; any other Python callable is evaluated on the host in the
+    reference's order (it is user code).
+
+    Raises:
+        UnboundedRay: a ray escaped (first escaping direction attached).
+    """
+    if n < 1 or m < 1:
+        raise ValueError("need n >= 1 rays and m >= 1 subsamples")
+    d = ns.dim
+    z, unif = _draw_integrate_stream(rng, n, m, d)
+    cand = neighbors if neighbors is not None and len(neighbors) > 0 else None
+    max_faces = _max_faces_for(ns, n, cand)
+    spec = getattr(f, "device_spec", None)
+    if spec is not None:
+        res = _integrate_device(ns, [int(i)], n, m, spec[0], spec[1], dirs=z, unif=unif,
+                                candidates=cand, max_faces=max_faces, stats=stats)
+        st = int(res["status"][0])
+        if st == CELL_UNBOUNDED:
+            y = z[int(res["first_bad"][0])]
+            raise UnboundedRay(i, y / math.sqrt(float(y @ y)))
+        if st == CELL_DEGENERATE:
+            raise DegenerateConfiguration(f"a foreign generator lies on a circumsphere of cell {i}")
+        if st == CELL_OVERFLOW:
+            raise RuntimeError(f"cell {i} hit more than {max_faces} faces")
+        k = int(res["nfaces"][0])
+        js = [int(j) for j in res["face_j"][0, :k]]
+        return CellIntegrals(volume=float(res["volume"][0]),
+                             area={j: float(a) for j, a in zip(js, res["face_area"][0, :k])},
+                             surface_integral={j: float(s) for j, s in
+                                               zip(js, res["face_surf"][0, :k])},
+                             volume_integral=float(res["vol_integral"][0]), n_rays=n,
+                             m_subsamples=m)
+    # generic callable: hits from the GPU, integrand sums on the host in ray order
+    out = _mc_device(ns, [int(i)], n, dirs=z, candidates=cand, max_faces=max_faces,
+                     degenerate_is_error=True, stats=stats)
+    idx = out["ray_idx"].cpu().numpy()
+    t = out["ray_t"].cpu().numpy()
+    flag = out["ray_flag"].cpu().numpy()
+    pts = ns.points
+    xi = pts[i]
+    area, fsurf = {}, {}
+    vol = fvol = 0.0
+    for k in range(n):
+        y = z[k] / math.sqrt(float(z[k] @ z[k]))
+        if flag[k] == 1:
+            raise UnboundedRay(i, y)
+        if flag[k] == 3:
+            raise DegenerateConfiguration(f"a foreign generator lies on a circumsphere of cell {i}")
+        j = int(idx[k])
+        rp = xi + t[k] * y
+        seg = rp - xi
+        length = math.sqrt(float(seg @ seg))
+        nij = pts[j] - xi
+        cosang = float(nij @ y) / math.sqrt(float(nij @ nij))
+        w = length ** (d - 1) / cosang
+        area[j] = area.get(j, 0.0) + w
+        fsurf[j] = fsurf.get(j, 0.0) + f(rp) * w
+        vol += length ** d
+        acc = 0.0
+        for s in range(m):
+            ts = unif[k, s]
+            acc += f(xi + ts * seg) * ts ** (d - 1)
+        fvol += acc * length ** d
+    surf = sphere_surface_area(d)
+    scale = surf / n
+    return CellIntegrals(volume=vol * surf / (d * n), area={j: a * scale for j, a in area.items()},
+                         surface_integral={j: s * scale for j, s in fsurf.items()},
+                         volume_integral=fvol * surf / (n * m), n_rays=n, m_subsamples=m)
+
+
+def mc_integrals_cells(ns: NodeSet, cells, n: int, m: int, f, seed: int = 0,
+                       max_faces: int = 256):
+    """Batched device MC integrals for a built-in integrand: Philox
+    directions and subsample positions, everything on the GPU.  Returns a
+    dict of per-cell arrays (volume, vol_integral, status, faces...)."""
+    spec = getattr(f, "device_spec", None)
+    if spec is None:
+        raise ValueError("mc_integrals_cells needs a built-in integrand (integrands.py)")
+    return _integrate_device(ns, np.asarray(cells, dtype=np.int32), n, m, spec[0], spec[1],
+                             seed=seed, max_faces=max_faces)
+
+
+def mc_uniforms(cells, n: int, m: int, seed: int = 0, device=None):
+    """The Philox subsample uniforms of mc_integrals_cells, (len(cells)*n, m)."""
+    L = _lib.lib()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    cd = torch.as_tensor(np.ascontiguousarray(cells, dtype=np.int32), device=dev)
+    out = torch.empty((len(cells) * n, m), dtype=torch.float64, device=dev)
+    _lib.check(L.vr_mc_uniforms(len(cells), _lib.ptr(cd), n, m, int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                _lib.ptr(out), _lib.stream_handle()), "vr_mc_uniforms")
+    return out.cpu().numpy()

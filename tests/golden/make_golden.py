@@ -287,6 +287,73 @@ def config5_balls(n_seeds=5, hops=4):
     np.savez_compressed(os.path.join(HERE, "config5_balls.npz"), **out)
 
 
+def mc_integrate_golden():
+    """mc_integrate_cell with the reference's built-in integrands and a plain
+    Python callable, on reference RNG streams (integrate_mc.py:70-121)."""
+    from voronray.integrands import const1, sinx2, make_linear
+    out = {}
+    usq = vr.build_node_set([(0.0, 0.0), (1.0, 0.0), (-1.0, 0.0), (0.0, 1.0), (0.0, -1.0)])
+    cases = []
+    res = vr.mc_integrate_cell(usq, 0, const1, 20000, 2, vrng.stream(2024, "test", 3))
+    cases.append(("usq_const1", res))
+    res = vr.mc_integrate_cell(usq, 0, make_linear([1.0, -2.0, 0.5]), 5000, 3,
+                               vrng.stream(2024, "test", 6))
+    cases.append(("usq_linear", res))
+    m2 = vr.voronoi_graph(vr.build_node_set(np.random.default_rng(1234).random((120, 2))), seed=0)
+    i = m2.bounded_cells()[2]
+    nb = np.asarray(m2.neighbors(i), dtype=np.intp)
+    res = vr.mc_integrate_cell(m2.nodes, i, lambda x: x[0], 2000, 2, vrng.stream(2024, "test", 20))
+    cases.append(("m2_x0_full", res))
+    res = vr.mc_integrate_cell(m2.nodes, i, lambda x: x[0], 2000, 2, vrng.stream(2024, "test", 20),
+                               neighbors=nb)
+    cases.append(("m2_x0_nb", res))
+    pts = np.random.default_rng(0).random((100000, 4))
+    ns = vr.build_node_set(pts)
+    order = np.argsort(np.linalg.norm(pts - 0.5, axis=1), kind="stable")
+    for c in order[:2]:
+        res = vr.mc_integrate_cell(ns, int(c), sinx2, 1000, 3, vrng.stream(7, "mc", int(c)))
+        cases.append((f"c4_sinx2_{int(c)}", res))
+    out["m2_cell"] = np.array(i)
+    for name, r in cases:
+        js = sorted(r.area)
+        out[f"{name}__j"] = np.array(js)
+        out[f"{name}__area"] = np.array([r.area[j] for j in js])
+        out[f"{name}__surf"] = np.array([r.surface_integral[j] for j in js])
+        out[f"{name}__vol"] = np.array([r.volume, r.volume_integral])
+        print(name, r.volume, r.volume_integral, len(js))
+    np.savez_compressed(os.path.join(HERE, "mc_integrate_golden.npz"), **out)
+
+
+def hmc_io_golden():
+    """HMC post-processing and the mesh JSON wire format on mesh_2d
+    (integrate_hmc.py, io.py), with reference MC areas."""
+    from voronray.integrands import sinx2
+    from voronray.integrate_hmc import hmc_cell_integral, hmc_interface_integral, hmc_volume
+    from voronray.io import mesh_to_dict
+    import json
+    m2 = vr.voronoi_graph(vr.build_node_set(np.random.default_rng(1234).random((120, 2))), seed=0)
+    out = {}
+    cells = m2.bounded_cells()[:6]
+    for c in cells:
+        nb = np.asarray(m2.neighbors(c), dtype=np.intp)
+        areas, vol = vr.mc_areas_only(m2.nodes, c, 4000, vrng.stream(5, "mc", c), neighbors=nb)
+        js = sorted(areas)
+        out[f"c{c}__j"] = np.array(js)
+        out[f"c{c}__area"] = np.array([areas[j] for j in js])
+        hv = hmc_volume(m2.nodes, c, areas, m2)
+        fi = [hmc_interface_integral(m2, c, j, areas[j], sinx2) for j in js]
+        ci = hmc_cell_integral(m2, c, sinx2, areas, hv)
+        out[f"c{c}__hmc"] = np.array([hv, ci])
+        out[f"c{c}__face"] = np.array(fi)
+    out["cells"] = np.array(cells)
+    d = mesh_to_dict(m2)
+    out["mesh_json_sha"] = np.frombuffer(
+        hashlib.sha256(json.dumps(d, indent=1, sort_keys=True).encode()).digest(), dtype=np.uint8)
+    out["n_json_vertices"] = np.array(len(d["vertices"]))
+    np.savez_compressed(os.path.join(HERE, "hmc_io_golden.npz"), **out)
+    print("hmc/io cells", cells)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["mesh_config1", "meshes_small", "config2_sample", "mc_golden",
                              "config5_sample"]

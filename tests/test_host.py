@@ -113,3 +113,68 @@ def test_array_mesh_helpers():
     # dict-constructed mesh (reference constructor shape) round-trips to arrays
     m2 = vb.Mesh(ns, dict(m.vertices), dict(m.edge_counts), list(m.boundary))
     assert m2.arrays()["sigma"].shape == sig.shape
+
+
+def test_mesh_json_round_trip_is_byte_identical(tmp_path):
+    """io.mesh_from_dict + io.mesh_to_dict reproduce the reference's mesh JSON
+    byte for byte (io.py:40-74), edge counts rebuilt like the reference."""
+    import os
+    from paper_2405_10050_b200 import io as vio
+    from conftest import GOLDEN
+    src = os.path.join(GOLDEN, "mesh_2d_reference.json")
+    data = vio.load_json(src)
+    pts = np.random.default_rng(1234).random((120, 2))
+    ns = vb.NodeSet(pts)
+    mesh = vio.mesh_from_dict(data, ns)
+    out = tmp_path / "m.json"
+    vio.dump_json(vio.mesh_to_dict(mesh), out)
+    assert out.read_bytes() == open(src, "rb").read()
+    gz = golden("meshes_small.npz")
+    ek = sorted(mesh.edge_counts)
+    assert np.array_equal(np.array(ek, dtype=np.int32), gz["mesh_2d__edge_key"])
+    assert np.array_equal(np.array([mesh.edge_counts[e] for e in ek]), gz["mesh_2d__edge_count"])
+    with pytest.raises(DimensionMismatch):
+        vio.mesh_from_dict(data, vb.NodeSet(pts[:50]))
+
+
+def test_points_csv_round_trip(tmp_path):
+    from paper_2405_10050_b200 import io as vio
+    pts = np.random.default_rng(3).random((10, 3))
+    p = tmp_path / "p.csv"
+    vio.write_points_csv(p, pts)
+    assert np.array_equal(vio.read_points_csv(p), pts)
+    (tmp_path / "bad.csv").write_text("1,2\n3\n")
+    with pytest.raises(DimensionMismatch):
+        vio.read_points_csv(tmp_path / "bad.csv")
+
+
+def test_hmc_matches_reference_on_reference_mesh():
+    """HMC post-processing (integrate_hmc.py) on the reference mesh and the
+    reference MC areas reproduces the reference values."""
+    import os
+    from paper_2405_10050_b200 import io as vio
+    from paper_2405_10050_b200.integrands import sinx2
+    from conftest import GOLDEN
+    gz = golden("hmc_io_golden.npz")
+    pts = np.random.default_rng(1234).random((120, 2))
+    ns = vb.NodeSet(pts)
+    mesh = vio.mesh_from_dict(vio.load_json(os.path.join(GOLDEN, "mesh_2d_reference.json")), ns)
+    for c in gz["cells"]:
+        areas = {int(j): float(a) for j, a in zip(gz[f"c{c}__j"], gz[f"c{c}__area"])}
+        hv = vb.hmc_volume(ns, int(c), areas, mesh)
+        ci = vb.hmc_cell_integral(mesh, int(c), sinx2, areas, hv)
+        assert hv == pytest.approx(gz[f"c{c}__hmc"][0], rel=1e-14)
+        assert ci == pytest.approx(gz[f"c{c}__hmc"][1], rel=1e-13)
+        fi = [vb.hmc_interface_integral(mesh, int(c), int(j), areas[int(j)], sinx2)
+              for j in gz[f"c{c}__j"]]
+        assert np.allclose(fi, gz[f"c{c}__face"], rtol=1e-13, atol=0)
+
+
+def test_integrands_resolve():
+    from paper_2405_10050_b200 import integrands as it
+    assert it.resolve("const1", 3)(np.zeros(3)) == 1.0
+    assert it.resolve("sinx2", 2)(np.array([2.0, 0.0])) == pytest.approx(np.sin(4.0))
+    lin = it.resolve("linear:1,2,3", 2)
+    assert lin(np.array([1.0, 1.0])) == 6.0 and lin.device_spec == (3, (1.0, 2.0, 3.0))
+    with pytest.raises(ValueError):
+        it.resolve("linear:1", 3)

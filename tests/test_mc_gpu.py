@@ -161,3 +161,75 @@ def test_config4_subset_vs_exact_volumes():
     assert frac >= 0.95, frac
     # unbiased in aggregate
     assert abs(np.mean((res.volume - gz["volume"]) / se)) < 0.2
+
+
+def _cmp_integrals(res, gz, name, rel_area=1e-11, rel_int=1e-10):
+    js = [int(j) for j in gz[f"{name}__j"]]
+    assert sorted(res.area) == js
+    for j, a, sv in zip(js, gz[f"{name}__area"], gz[f"{name}__surf"]):
+        assert _close(res.area[j], float(a), rel_area), (name, j)
+        assert _close(res.surface_integral[j], float(sv), rel_int) or abs(sv) < 1e-300, (name, j)
+    assert _close(res.volume, float(gz[f"{name}__vol"][0]), rel_area)
+    assert _close(res.volume_integral, float(gz[f"{name}__vol"][1]), rel_int)
+
+
+def test_mc_integrate_cell_matches_reference():
+    """mc_integrate_cell (integrate_mc.py:70-121) on reference RNG streams:
+    built-in integrands evaluated in the kernel, a Python callable on the host."""
+    from paper_2405_10050_b200.integrands import const1, make_linear, sinx2
+    gz = golden("mc_integrate_golden.npz")
+    ns = vb.build_node_set(UNIT_SQUARE_POINTS)
+    _cmp_integrals(vb.mc_integrate_cell(ns, 0, const1, 20000, 2, vb.rng.stream(2024, "test", 3)),
+                   gz, "usq_const1")
+    _cmp_integrals(vb.mc_integrate_cell(ns, 0, make_linear([1.0, -2.0, 0.5]), 5000, 3,
+                                        vb.rng.stream(2024, "test", 6)), gz, "usq_linear")
+    pts = np.random.default_rng(1234).random((120, 2))
+    n2 = vb.build_node_set(pts)
+    i = int(gz["m2_cell"])
+    full = vb.mc_integrate_cell(n2, i, lambda x: x[0], 2000, 2, vb.rng.stream(2024, "test", 20))
+    _cmp_integrals(full, gz, "m2_x0_full")
+    sig = golden("meshes_small.npz")["mesh_2d__sigma"]
+    nb = np.unique(sig[(sig == i).any(axis=1)])
+    rest = vb.mc_integrate_cell(n2, i, lambda x: x[0], 2000, 2, vb.rng.stream(2024, "test", 20),
+                                neighbors=nb[nb != i])
+    assert rest.volume == full.volume and rest.area == full.area  # bitwise, like the reference test
+    p4 = np.random.default_rng(0).random((100000, 4))
+    n4 = vb.NodeSet(p4)
+    for c in np.argsort(np.linalg.norm(p4 - 0.5, axis=1), kind="stable")[:2]:
+        _cmp_integrals(vb.mc_integrate_cell(n4, int(c), sinx2, 1000, 3,
+                                            vb.rng.stream(7, "mc", int(c))), gz, f"c4_sinx2_{int(c)}")
+
+
+def test_mc_integrals_cells_device_philox():
+    """Batched device integrals with Philox directions and subsample
+    positions equal the host-evaluated replay of the same streams."""
+    from paper_2405_10050_b200.integrands import sinx2
+    pts = np.random.default_rng(0).random((100000, 4))
+    ns = vb.NodeSet(pts)
+    cells = np.argsort(np.linalg.norm(pts - 0.5, axis=1), kind="stable")[:4]
+    res = vb.mc_integrals_cells(ns, cells, 500, 2, sinx2, seed=11)
+    z = vb.mc_directions(4, cells, 500, seed=11)
+    u = vb.mc_uniforms(cells, 500, 2, seed=11)
+    zp = orc.philox_normals(11, cells, 500, 4)
+    assert np.max(np.abs(z - zp)) <= 1e-13 * np.max(np.abs(zp))
+
+    class R:  # replay in the reference's draw order: d normals, then m uniforms per ray
+        def __init__(self, z, u):
+            self.z, self.u, self.k, self.s = z, u, 0, 0
+
+        def standard_normal(self, d):
+            out = self.z[self.k]
+            return out
+
+        def random(self):
+            v = self.u[self.k, self.s]
+            self.s += 1
+            if self.s == self.u.shape[1]:
+                self.s, self.k = 0, self.k + 1
+            return v
+
+    for m_, c in enumerate(cells):
+        rep = vb.mc_integrate_cell(ns, int(c), lambda x: sinx2(x), 500, 2,
+                                   R(z[m_ * 500:(m_ + 1) * 500], u[m_ * 500:(m_ + 1) * 500]))
+        assert _close(float(res["volume"][m_]), rep.volume)
+        assert _close(float(res["vol_integral"][m_]), rep.volume_integral, 1e-11)
