@@ -239,8 +239,8 @@ int vr_mc_rays(const double* rec, int64_t n_gen, int d, double sqmax,
 int vr_mc_rays_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
                       const vr_screen32* s32, const vr_prune_index* ix, const int32_t* cells,
                       int64_t n_cells, int64_t rays_per_cell, const double* dirs,
-                      uint64_t seed, int32_t* out_idx, double* out_t,
-                      uint8_t* out_flag, int32_t* recheck_list,
+                      uint64_t seed, const int32_t* order, int32_t* out_idx,
+                      double* out_t, uint8_t* out_flag, int32_t* recheck_list,
                       int32_t* recheck_count, uint64_t* work, void* stream);
 
 int vr_mc_recheck(const double* rec, int64_t n_gen, int d,

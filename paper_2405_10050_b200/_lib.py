@@ -45,7 +45,7 @@ _SIGNATURES = {
     "vr_raycast_pruned": [_vp, _i64, _int, _dbl, _vp, _vp, _vp, _vp, _vp, _int, _i64, _vp, _vp,
                           _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_mc_rays_pruned": [_vp, _i64, _int, _dbl, _vp, _vp, _vp, _i64, _i64, _vp, _u64, _vp,
-                          _vp, _vp, _vp, _vp, _vp, _vp],
+                          _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_pack_records32": [_vp, _i64, _int, _vp, _vp, _vp],
     "vr_mc_integrate": [_vp, _int, _vp, _i64, _i64, _vp, _u64, _vp, _vp, _vp, _int, _dbl, _int,
                         _vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

@@ -347,8 +347,9 @@ extern "C" int vr_mc_directions(int d, int64_t n_cells, const int32_t* cells,
 extern "C" int vr_mc_rays_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
                                  const vr_screen32* s32, const vr_prune_index* ix, const int32_t* cells, int64_t n_cells,
                                  int64_t rays_per_cell, const double* dirs, uint64_t seed,
-                                 int32_t* out_idx, double* out_t, uint8_t* out_flag,
-                                 int32_t* recheck_list, int32_t* recheck_count, uint64_t* work,
+                                 const int32_t* order, int32_t* out_idx, double* out_t,
+                                 uint8_t* out_flag, int32_t* recheck_list,
+                                 int32_t* recheck_count, uint64_t* work,
                                  void* stream) {
   if (!rec || !ix || !ix->rec || !cells || !out_idx || !out_t || !out_flag || rays_per_cell <= 0 ||
       ix->n != n_gen)
@@ -361,6 +362,7 @@ extern "C" int vr_mc_rays_pruned(const double* rec, int64_t n_gen, int d, double
   const Screen sc = make_screen(sqmax, s32, d);
   VR_DISPATCH_D(d, {
     SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n};
+    src.order = order;
     return launch_raycast_pruned<D>(src, n, pi, sc.fr, out, as_stream(stream),
                                     reinterpret_cast<unsigned long long*>(work));
   });

@@ -409,6 +409,7 @@ struct SrcMC {
   const double* dirs;  // nullable: raw Gaussian draws (n, D)
   uint64_t seed;
   int64_t n;      // total rays
+  const int32_t* order = nullptr;  // optional processing order (slot -> ray id)
   __device__ __forceinline__ void direction(int64_t k, double (&y)[D]) const {
     double z[D];
     if (dirs) {
@@ -420,10 +421,11 @@ struct SrcMC {
     }
     normalise<D>(z, y);
   }
-  __device__ __forceinline__ int64_t id(int64_t k) const { return k; }
-  __device__ __forceinline__ int32_t gen(int64_t k) const { return cells[k / per]; }
+  __device__ __forceinline__ int64_t id(int64_t k) const { return order ? order[k] : k; }
+  __device__ __forceinline__ int32_t gen(int64_t k) const { return cells[id(k) / per]; }
   __device__ __forceinline__ bool load(int64_t k, RayState<D>& r, const Frame& fr) const {
     if (k >= n) return false;
+    k = id(k);
     const int32_t cell = cells[k / per];
     const double* xc = grec + (int64_t)cell * rec_stride(D);
 #pragma unroll

@@ -29,7 +29,8 @@ import torch
 from . import _lib
 from .core import NodeSet
 from .errors import DegenerateConfiguration, UnboundedRay
-from .raycast import RaycastStats, Workspace, _screen, _use_pruned, candidate_records
+from .raycast import (RaycastStats, Workspace, _screen, _use_pruned, candidate_records,
+                      direction_bucket)
 
 Integrand = Callable[[np.ndarray], float]
 
@@ -83,6 +84,9 @@ class MCResult:
         return {int(j): float(a) for j, a in zip(self.face_j[lo:hi], self.face_area[lo:hi])}
 
 
+MC_ORDER_RAYS = True  # direction-sorted processing order in the pruned MC path
+
+
 def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_faces=256,
                degenerate_is_error=True, want_samples=False, workspace=None, stats=None,
                mode="auto", screen="fp32"):
@@ -117,8 +121,23 @@ def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_fa
     seed = int(seed) & 0xFFFFFFFFFFFFFFFF
     if _use_pruned(ns, candidates, mode):
         ix = ns.prune_index(dev)
+        order = None
+        if MC_ORDER_RAYS and n >= 32:
+            # Rays of one cell share their origin; sorting them by direction
+            # class makes the 32 rays of a warp coherent (smaller union of
+            # spheres, fewer tree nodes).  The Philox directions are
+            # materialised once so the order can be computed; results are
+            # independent of the order.
+            if dd is None:
+                dd = ws.get("mc_dirs", (total, d), torch.float64, dev)
+                _lib.check(L.vr_mc_directions(d, nc, _lib.ptr(cells_d), n, seed, _lib.ptr(dd), sh),
+                           "vr_mc_directions")
+            key = torch.arange(total, device=dev, dtype=torch.int64).div_(n, rounding_mode="floor")
+            key.mul_(256).add_(direction_bucket(dd.view(total, d)))
+            order = torch.sort(key, stable=True).indices.to(torch.int32)
+            del key
         _lib.check(L.vr_mc_rays_pruned(_lib.ptr(rec), ns.n, d, sqmax, s32p, ctypes.byref(ix.struct),
-                                       _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed,
+                                       _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed, _lib.ptr(order),
                                        _lib.ptr(idx), _lib.ptr(t), _lib.ptr(flag), _lib.ptr(rl),
                                        _lib.ptr(rc), None, sh), "vr_mc_rays_pruned")
     else:

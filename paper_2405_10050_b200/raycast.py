@@ -133,6 +133,29 @@ def candidate_records(ns: NodeSet, candidates, dev, screen="fp64"):
     return cand.to(torch.int32).contiguous(), crec, s32
 
 
+def direction_bucket(u):
+    """Coarse direction class of unit vectors: the signed index of the
+    largest and of the second-largest |component| (< 256 classes for d <= 8)."""
+    d = u.shape[1]
+    a = u.abs()
+    i1 = a.argmax(1)
+    s1 = (u.gather(1, i1[:, None])[:, 0] > 0).to(torch.int64)
+    a2 = a.scatter(1, i1[:, None], -1.0)
+    i2 = a2.argmax(1)
+    s2 = (u.gather(1, i2[:, None])[:, 0] > 0).to(torch.int64)
+    return (i1 * 2 + s1) * (2 * d) + (i2 * 2 + s2)
+
+
+def coherent_order(ix, g, u):
+    """Processing order for the pruned kernel: rays sorted by the kd position
+    of their reference generator, then by direction class, so that the 32
+    rays of a warp start close together and (within one generator) point
+    the same way -- the warp-wide union of their spheres stays small."""
+    pos = ix.inv_perm.index_select(0, g.to(torch.int64)).to(torch.int64)
+    key = pos * 256 + direction_bucket(u)
+    return torch.sort(key, stable=True).indices.to(torch.int32)
+
+
 def _screen(ns, dev, screen):
     if screen not in ("fp32", "fp64"):
         raise ValueError(f"unknown screen {screen!r}")
@@ -224,9 +247,7 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
         ix = ns.prune_index(dev)
         cur = torch.cuda.current_stream() if stream is None else stream
         with torch.cuda.stream(cur):
-            # warp-coherent processing order: rays sorted by the kd position of eta[0]
-            key = ix.inv_perm.index_select(0, ed[:, 0].to(torch.int64))
-            order = torch.sort(key, stable=True).indices.to(torch.int32)
+            order = coherent_order(ix, ed[:, 0], ud)
         _lib.check(L.vr_raycast_pruned(_lib.ptr(rec), ns.n, d, sqmax, s32p, ctypes.byref(ix.struct),
                                        _lib.ptr(xd), _lib.ptr(ud), _lib.ptr(ed), k, n,
                                        _lib.ptr(order), _lib.ptr(idx), _lib.ptr(t),

@@ -72,10 +72,12 @@ if __name__ == "__main__":
     if "c4mc" in which:
         pts = np.random.default_rng(0).random((100000, 4))
         ns = vb.NodeSet(pts)
-        for mode in ("pruned", "pruned"):
+        import paper_2405_10050_b200.integrate_mc as im
+        for mode, order in (("pruned", False), ("pruned", False), ("pruned", True), ("pruned", True)):
+            im.MC_ORDER_RAYS = order
             torch.cuda.synchronize()
             t0 = time.time()
             vb.mc_cells(ns, np.arange(100000), 1000, seed=0, mode=mode)
             torch.cuda.synchronize()
-            print(f"c4 MC 1e8 rays {mode}: {time.time() - t0:.3f} s "
+            print(f"c4 MC 1e8 rays {mode} order={order}: {time.time() - t0:.3f} s "
                   f"({1e8 / (time.time() - t0):.3e} rays/s)", flush=True)
