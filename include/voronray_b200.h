@@ -92,6 +92,13 @@ int vr_record32_stride(int d);
 int vr_pack_records32(const double* rec, int64_t rows, int d, const double* center,
                       float* rec32, void* stream);
 
+/* Pair-interleaved copy of vr_pack_records32's rows for the pruned kernel
+ * (vr_prune_index.rec32): rows/2 pairs of (2d+5)&~3 floats
+ * [x_0a x_0b .. x_{d-1}a x_{d-1}b |.|^2_a |.|^2_b pad]; rows must be even
+ * (vr_record_rows is a multiple of 512). */
+int vr_pack_records32_pairs(const float* rec32, int64_t rows, int d, float* out,
+                            void* stream);
+
 /* Batched incircle RayCast (reference raycast_incircle, raycast.py:154-224,
  * with its filtered NN probe _Probe, raycast.py:85-151, core.py:62-103).
  *
@@ -135,7 +142,8 @@ int vr_raycast_batch(const double* rec, int64_t n_gen, int d, double sqmax,
 #define VR_PRUNE_TILE 64
 typedef struct vr_prune_index {
   const double* rec;       /* kd-ordered records, vr_record_rows(n) rows       */
-  const float* rec32;      /* kd-ordered fp32 centred records (nullable)       */
+  const float* rec32;      /* kd-ordered fp32 centred records, pair-interleaved
+                              (vr_pack_records32_pairs); nullable             */
   const int32_t* perm;     /* kd position -> generator index (n)               */
   const int32_t* inv_perm; /* generator index -> kd position (n)               */
   const double* tile_box;  /* ceil(n/64) x 2d, [lo_0..lo_{d-1}, hi_0..]        */

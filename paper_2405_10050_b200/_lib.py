@@ -47,6 +47,7 @@ _SIGNATURES = {
     "vr_mc_rays_pruned": [_vp, _i64, _int, _dbl, _vp, _vp, _vp, _i64, _i64, _vp, _u64, _vp,
                           _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_pack_records32": [_vp, _i64, _int, _vp, _vp, _vp],
+    "vr_pack_records32_pairs": [_vp, _i64, _int, _vp, _vp],
     "vr_mc_integrate": [_vp, _int, _vp, _i64, _i64, _vp, _u64, _vp, _vp, _vp, _int, _dbl, _int,
                         _vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_mc_uniforms": [_i64, _vp, _i64, _int, _u64, _vp, _vp],

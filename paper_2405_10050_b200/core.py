@@ -348,10 +348,17 @@ class PruneIndex:
         self.n = n
         self.rows = rows
         self.screen32 = Screen32(crec, n, d, center=center)
+        # the pruned kernel reads the fp32 rows pair-interleaved (packed FFMA2)
+        p2 = (2 * d + 5) & ~3
+        self.rec32p = torch.empty((rows // 2, p2), dtype=torch.float32, device=dev)
+        L = _lib.lib()
+        _lib.check(L.vr_pack_records32_pairs(_lib.ptr(self.screen32.rec), rows, d,
+                                             _lib.ptr(self.rec32p), _lib.stream_handle()),
+                   "vr_pack_records32_pairs")
         self.tile_box32 = _outward32(lo, hi, self.screen32.center)
         self.node_box32 = _outward32(nlo, nhi, self.screen32.center)
         p = lambda t: t.data_ptr()  # noqa: E731
-        self.struct = _PruneStruct(p(crec), p(self.screen32.rec), p(self.perm), p(self.inv_perm),
+        self.struct = _PruneStruct(p(crec), p(self.rec32p), p(self.perm), p(self.inv_perm),
                                    p(self.tile_box), p(self.tile_box32), p(self.node_box),
                                    p(self.node_box32), p(self.node_range), n)
 

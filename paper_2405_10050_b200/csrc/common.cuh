@@ -32,6 +32,11 @@ __host__ __device__ constexpr int rec_stride(int d) { return (d + 2) & ~1; }
 // rounded up to a multiple of 4 (16-B rows).
 __host__ __device__ constexpr int rec32_stride(int d) { return (d + 4) & ~3; }
 
+// Floats per PAIR of candidates in the pair-interleaved fp32 layout used by
+// the pruned kernel: [x_0a x_0b x_1a x_1b .. x_{d-1}a x_{d-1}b |.|^2_a |.|^2_b]
+// rounded up to a multiple of 4, so one LDS.128 feeds two packed FFMA2.
+__host__ __device__ constexpr int rec32p_stride(int d) { return (2 * d + 5) & ~3; }
+
 static inline int vr_cuda_status(cudaError_t e) {
   return e == cudaSuccess ? VR_OK : (VR_ECUDA_BASE - (int)e);
 }

@@ -205,6 +205,26 @@ __global__ void k_pack32(const double* __restrict__ rec, int64_t rows, const dou
   }
 }
 
+// fp32 records -> pair-interleaved layout (rows is even: a multiple of 512).
+template <int D>
+__global__ void k_pairs32(const float* __restrict__ rec32, int64_t rows, float* __restrict__ out) {
+  constexpr int S32 = rec32_stride(D);
+  constexpr int P2 = rec32p_stride(D);
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < rows / 2;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const float* a = rec32 + (2 * p) * S32;
+    const float* b = a + S32;
+    float* o = out + p * P2;
+#pragma unroll
+    for (int k = 0; k <= D; ++k) {
+      o[2 * k] = a[k];
+      o[2 * k + 1] = b[k];
+    }
+#pragma unroll
+    for (int k = 2 * D + 2; k < P2; ++k) o[k] = 0.0f;
+  }
+}
+
 inline unsigned blocks_for(int64_t n, int nt) { return (unsigned)((n + nt - 1) / nt); }
 
 }  // namespace
@@ -232,6 +252,16 @@ extern "C" int vr_pack_records32(const double* rec, int64_t rows, int d, const d
   const unsigned nbk = blocks_for(rows, 256) < 4096 ? blocks_for(rows, 256) : 4096;
   VR_DISPATCH_D(d, {
     k_pack32<D><<<nbk, 256, 0, as_stream(stream)>>>(rec, rows, center, rec32);
+  });
+  VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_pack_records32_pairs(const float* rec32, int64_t rows, int d, float* out,
+                                       void* stream) {
+  if (!rec32 || !out || rows <= 0 || (rows & 1)) return VR_EINVAL;
+  const unsigned nbk = blocks_for(rows / 2, 256) < 4096 ? blocks_for(rows / 2, 256) : 4096;
+  VR_DISPATCH_D(d, {
+    k_pairs32<D><<<nbk, 256, 0, as_stream(stream)>>>(rec32, rows, out);
   });
   VR_RETURN_LAUNCH();
 }

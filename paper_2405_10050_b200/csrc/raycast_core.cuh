@@ -539,6 +539,81 @@ __device__ __forceinline__ void screen_tile(RayState<D> (&ray)[R], const double*
   }
 }
 
+// Packed fp32 pairs (sm_100 FFMA2: two IEEE fp32 FMAs per instruction; a
+// scalar multiplicand is broadcast by ptxas, so z32 needs no duplication).
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+// screen_tile over the pair-interleaved fp32 layout (rec32p_stride): the same
+// per-pair values as ray_power32 (same FMA order, IEEE fp32 per lane), two
+// candidates per FFMA2; the block vote is taken on the minimum (one FMNMX per
+// candidate), and the per-candidate mask is built only when the vote fires.
+template <int D, int R, int PT>
+__device__ __forceinline__ void screen_tile_pairs(RayState<D> (&ray)[R], const double* tile,
+                                                  const float* tilep, int gbase, const Frame& fr,
+                                                  WarpCounters* wc = nullptr) {
+  constexpr int S = rec_stride(D);
+  constexpr int P2 = rec32p_stride(D);
+  constexpr int U = 8;
+  for (int c = 0; c < PT; c += U) {
+    float f[R][U];
+#pragma unroll
+    for (int p = 0; p < U / 2; ++p) {
+      const float4* q = reinterpret_cast<const float4*>(tilep + ((c >> 1) + p) * P2);
+      float v[P2];
+#pragma unroll
+      for (int k = 0; k < P2 / 4; ++k) {
+        const float4 w = q[k];
+        v[4 * k] = w.x;
+        v[4 * k + 1] = w.y;
+        v[4 * k + 2] = w.z;
+        v[4 * k + 3] = w.w;
+      }
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        uint64_t acc = f2pack(v[2 * D], v[2 * D + 1]);
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+          acc = ffma2(f2pack(ray[j].z32[k], ray[j].z32[k]), f2pack(v[2 * k], v[2 * k + 1]), acc);
+        f2unpack(acc, f[j][2 * p], f[j][2 * p + 1]);
+      }
+    }
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      float mn = f[j][0];
+#pragma unroll
+      for (int u = 1; u < U; ++u) mn = fminf(mn, f[j][u]);
+      any |= mn < ray[j].hi32;
+    }
+    if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        unsigned m = 0u;
+#pragma unroll
+        for (int u = 0; u < U; ++u) m |= (f[j][u] < ray[j].hi32) ? (1u << u) : 0u;
+        if (wc) {
+          if (j == 0) ++wc->rare_blocks;
+          wc->entries += __popc(m);
+          wc->rare_iters += __reduce_max_sync(0xffffffffu, (unsigned)__popc(m));
+        }
+        if (m) ray_rare_block<D, true>(ray[j], tile + c * S, m, gbase + c, fr);
+      }
+    }
+  }
+}
+
 template <int D, int R>
 __device__ __forceinline__ void init_padding_lane(RayState<D>& r) {
   r.hi = -CUDART_INF;
@@ -835,14 +910,14 @@ __global__ void __launch_bounds__(32, MINB)
                      const float* __restrict__ node_box32, const int2* __restrict__ node_range,
                      Frame fr, RayOut out, unsigned long long* __restrict__ work) {
   constexpr int S = rec_stride(D);
-  constexpr int S32 = rec32_stride(D);
   // both copies are staged: the fp64 rows feed the rare path, which is hit
   // often enough (tens of entries per ray at d=8) that global loads stall
   constexpr uint32_t BYTES64 = (uint32_t)(PT * S * sizeof(double));
-  constexpr uint32_t BYTES32 = F32 ? (uint32_t)(PT * S32 * sizeof(float)) : 0u;
+  constexpr int P2 = rec32p_stride(D);
+  constexpr uint32_t BYTES32 = F32 ? (uint32_t)(PT / 2 * P2 * sizeof(float)) : 0u;
   static_assert(PT % 8 == 0 && VR_REC_PAD % PT == 0, "tile must divide the record padding");
   __shared__ __align__(128) double buf[2][PT * S];
-  __shared__ __align__(128) float buf32[2][F32 ? PT * S32 : 4];
+  __shared__ __align__(128) float buf32[2][F32 ? PT / 2 * P2 : 4];
   __shared__ uint64_t bar[2];
   const int lane = threadIdx.x;
   const int64_t k0 = (int64_t)blockIdx.x * 32 * R + lane;
@@ -872,7 +947,7 @@ __global__ void __launch_bounds__(32, MINB)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive_expect_tx(&bar[b], BYTES64 + BYTES32);
       bulk_g2s(buf[b], crec + t * PT * S, BYTES64, &bar[b]);
-      if constexpr (F32) bulk_g2s(buf32[b], crec32 + t * PT * S32, BYTES32, &bar[b]);
+      if constexpr (F32) bulk_g2s(buf32[b], crec32 + t * (PT / 2) * P2, BYTES32, &bar[b]);
     }
   };
   unsigned long long tiles_done = 0;
@@ -892,7 +967,10 @@ __global__ void __launch_bounds__(32, MINB)
     for (int j = 0; j < R; ++j) need |= ray_needs<D, F32>(ray[j], tile_box, tile_box32, t);
     if (__any_sync(0xffffffffu, need)) {
       ++tiles_done;
-      screen_tile<D, R, PT, F32>(ray, buf[b], buf32[b], (int)(t * PT), fr, work ? &wc : nullptr);
+      if constexpr (F32)
+        screen_tile_pairs<D, R, PT>(ray, buf[b], buf32[b], (int)(t * PT), fr, work ? &wc : nullptr);
+      else
+        screen_tile<D, R, PT, F32>(ray, buf[b], buf32[b], (int)(t * PT), fr, work ? &wc : nullptr);
     }
     __syncwarp();
     b ^= 1;
