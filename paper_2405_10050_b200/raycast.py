@@ -387,9 +387,12 @@ class HostRaycaster:
 
     NBUF = 4
 
-    def __init__(self, ns: NodeSet, n_max: int, eta_len: int, chunk: int = 1 << 18):
+    def __init__(self, ns: NodeSet, n_max: int, eta_len: int, chunk: int = 1 << 19,
+                 min_chunk: int = 1 << 19):
         rec, _ = ns.device_records()
-        self.ns, self.dev, self.chunk, self.k = ns, rec.device, int(chunk), int(eta_len)
+        self.ns, self.dev, self.k = ns, rec.device, int(eta_len)
+        self.chunk = max(1, min(int(chunk), int(n_max)))  # device buffers hold one chunk
+        self.min_chunk = max(1, min(int(min_chunk), self.chunk))
         d = ns.dim
         c = self.chunk
         self.h2d_stream = torch.cuda.Stream(self.dev)
@@ -406,25 +409,45 @@ class HostRaycaster:
                     for _ in range(self.NBUF)]
         self.ws = [Workspace() for _ in range(self.NBUF)]
 
+    def schedule(self, n):
+        """Chunk bounds: sizes grow geometrically from min_chunk to chunk and
+        the last chunk is small again, so the first kernel starts after a
+        short H2D copy and the final D2H copy is short (pipeline fill and
+        drain), while the middle chunks keep the SMs full."""
+        out, lo, size = [], 0, self.min_chunk
+        while lo < n:
+            rest = n - lo
+            if rest <= size + self.min_chunk:
+                # tail: split the remainder so the last piece is ~min_chunk
+                tail = self.min_chunk if rest > 2 * self.min_chunk else \
+                    (rest // 2 if rest > self.chunk else 0)
+                if tail:
+                    out.append((lo, n - tail))
+                    lo = n - tail
+                out.append((lo, n))
+                break
+            out.append((lo, lo + size))
+            lo += size
+            size = min(2 * size, self.chunk)
+        return out
+
     @staticmethod
     def pinned(shape, dtype):
         return torch.empty(shape, dtype=dtype, pin_memory=True)
 
-    def run(self, hx, hu, heta, hidx, ht, hrp, hflag, stats=None, mode="auto", screen="fp32"):
+    def run(self, hx, hu, heta, hidx, ht, hrp, hflag, stats=None, mode="auto", screen="fp32",
+            sync=True):
         """hx, hu (n, d) f64, heta (n, k) i32 pinned inputs; outputs pinned
         hidx (n,) i32, ht (n,) f64, hrp (n, d) f64, hflag (n,) u8.  Returns
         after the last D2H copy has completed."""
         n = hx.shape[0]
-        c = self.chunk
-        nchunks = (n + c - 1) // c
         if self.ns.n >= 1024 and mode != "exhaustive":
             self.ns.prune_index(self.dev)
         if screen == "fp32":
             self.ns.screen32(self.dev)
-        for ci in range(nchunks):
+        for ci, (lo, hi) in enumerate(self.schedule(n)):
             b = self.buf[ci % self.NBUF]
             cs = self.comp_streams[ci & 1]
-            lo, hi = ci * c, min(n, (ci + 1) * c)
             m = hi - lo
             with torch.cuda.stream(self.h2d_stream):
                 if ci >= self.NBUF:
@@ -448,4 +471,5 @@ class HostRaycaster:
                 hrp[lo:hi].copy_(b["rp"][:m], non_blocking=True)
                 hflag[lo:hi].copy_(b["flag"][:m], non_blocking=True)
                 b["d2h"].record(self.d2h_stream)
-        self.d2h_stream.synchronize()
+        if sync:
+            self.d2h_stream.synchronize()

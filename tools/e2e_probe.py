@@ -35,12 +35,17 @@ for name, src, dst in (("H2D 48MB", hx, dx), ("D2H 48MB", dx, hx)):
     print(f"{name}: {dt * 1e3:.2f} ms = {48e6 / dt / 1e9:.1f} GB/s")
 hidx, ht = P((n,), torch.int32), P((n,), torch.float64)
 hrp, hfl = P((n, d), torch.float64), P((n,), torch.uint8)
-for chunk in (1 << 16, 1 << 17, 1 << 18, 1 << 19):
-    hr = HostRaycaster(ns, n, 1, chunk=chunk)
+for chunk, minc in ((1 << 18, 1 << 18), (1 << 19, 1 << 19), (1 << 19, 1 << 16), (1 << 19, 1 << 17),
+                    (1 << 20, 1 << 16), (1 << 18, 1 << 16)):
+    hr = HostRaycaster(ns, n, 1, chunk=chunk, min_chunk=minc)
     hr.run(hx, hu, hg, hidx, ht, hrp, hfl)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(3):
         hr.run(hx, hu, hg, hidx, ht, hrp, hfl)
     dt = (time.perf_counter() - t0) / 3
-    print(f"chunk {chunk}: {dt * 1e3:.2f} ms  {n / dt:.3e} rays/s")
+    t0 = time.perf_counter()
+    hr.run(hx, hu, hg, hidx, ht, hrp, hfl, sync=False)
+    te = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    print(f"chunk {chunk} min {minc}: {dt * 1e3:.2f} ms  {n / dt:.3e} rays/s  (host enqueue {te * 1e3:.2f} ms)")
