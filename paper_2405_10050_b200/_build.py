@@ -47,19 +47,24 @@ def needs_build():
     return any(os.path.getmtime(p) > lib_mtime for p in deps)
 
 
-def build(force=False, verbose=False, jobs=None):
-    """Compile every csrc/*.cu to an object (in parallel) and link the .so."""
-    if not force and not needs_build():
+def build(force=False, verbose=False, jobs=None, defines=(), out=None):
+    """Compile every csrc/*.cu to an object (in parallel) and link the .so.
+
+    ``defines`` / ``out`` build a tuning variant (e.g. ``-DVR_PAIR_BLOCK=16``)
+    into another file, selected at run time with VR_LIB_PATH."""
+    lib_path = out or LIB_PATH
+    if not force and not defines and out is None and not needs_build():
         return LIB_PATH
     nvcc = _nvcc()
-    objdir = os.path.join(PKG_DIR, "build")
+    objdir = os.path.join(PKG_DIR, "build" if not defines else
+                          "build_" + "_".join(x.lstrip("-D").replace("=", "") for x in defines))
     os.makedirs(objdir, exist_ok=True)
     procs = []
     objs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
-        cmd = [nvcc, *NVCC_FLAGS, "-c", src, "-o", obj]
+        cmd = [nvcc, *NVCC_FLAGS, *defines, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE,
@@ -74,15 +79,18 @@ def build(force=False, verbose=False, jobs=None):
     if failed:
         msg = "\n".join(" ".join(c) + "\n" + o for c, o in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
-    tmp = LIB_PATH + ".tmp"
+    tmp = lib_path + ".tmp"
     link = [nvcc, "-shared", "--cudart", "static",
             "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp]
     res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("link failed:\n" + res.stdout + res.stderr)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    defs = tuple(a for a in sys.argv[1:] if a.startswith("-D"))
+    outs = [a[len("--out="):] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose=True, defines=defs,
+                out=outs[0] if outs else None))

@@ -539,6 +539,10 @@ __device__ __forceinline__ void screen_tile(RayState<D> (&ray)[R], const double*
   }
 }
 
+#ifndef VR_PAIR_BLOCK
+#define VR_PAIR_BLOCK 16
+#endif
+
 // Packed fp32 pairs (sm_100 FFMA2: two IEEE fp32 FMAs per instruction; a
 // scalar multiplicand is broadcast by ptxas, so z32 needs no duplication).
 __device__ __forceinline__ uint64_t f2pack(float a, float b) {
@@ -565,7 +569,7 @@ __device__ __forceinline__ void screen_tile_pairs(RayState<D> (&ray)[R], const d
                                                   WarpCounters* wc = nullptr) {
   constexpr int S = rec_stride(D);
   constexpr int P2 = rec32p_stride(D);
-  constexpr int U = 8;
+  constexpr int U = VR_PAIR_BLOCK;
   for (int c = 0; c < PT; c += U) {
     float f[R][U];
 #pragma unroll

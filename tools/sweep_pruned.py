@@ -18,11 +18,17 @@ def run(name, ns, x, u, eta, modes=("exhaustive", "pruned")):
     for mode in modes:
         work = torch.zeros(8, dtype=torch.int64, device=dev)
         vb.raycast_batch(ns, xd, ud, ed, mode=mode)  # warm
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        torch.cuda.synchronize()
-        vb.raycast_batch(ns, xd, ud, ed, mode=mode, events=e, work=work)
-        torch.cuda.synchronize()
-        k = e[0].elapsed_time(e[1])
+        ks = []
+        for rep in range(int(os.environ.get("REPS", "5"))):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            work.zero_()
+            torch.cuda.synchronize()
+            torch.cuda.nvtx.range_push(f"sweep_{mode}")
+            vb.raycast_batch(ns, xd, ud, ed, mode=mode, events=e, work=work)
+            torch.cuda.nvtx.range_pop()
+            torch.cuda.synchronize()
+            ks.append(e[0].elapsed_time(e[1]))
+        k = float(np.median(ks))
         w = work.cpu().numpy()
         pairs = int(w[0]) if mode == "pruned" else n * ns.n
         if mode == "pruned":
