@@ -61,6 +61,9 @@ struct RayState {
   int ib;       // current best (local candidate index), -1 = none
   int near;     // 1 -> needs exact re-check
   int nupd;     // sphere updates (work accounting)
+#ifdef VR_RARE_STATS
+  int st_out, st_self, st_behind, st_band, st_imp;  // rare-path entry outcomes
+#endif
 };
 
 // Fill the per-ray constants from origin x, direction u and the eta
@@ -106,6 +109,9 @@ __device__ __forceinline__ void ray_setup(RayState<D>& r, const double* __restri
   r.ib = -1;
   r.near = 0;
   r.nupd = 0;
+#ifdef VR_RARE_STATS
+  r.st_out = r.st_self = r.st_behind = r.st_band = r.st_imp = 0;
+#endif
   // fp32 box-test constants (centred frame)
   double uc = 0.0;
 #pragma unroll
@@ -274,11 +280,18 @@ __device__ __forceinline__ void ray_rare_block(RayState<D>& r, const double* til
       fp = fma(zk2[k], xi[k], fp);
       q = fma(r.u[k], xi[k], q);
     }
-    if (have0 && !(fp < r.hi)) continue;  // outside the block-start sphere's band
-    if (gbase + u == r.ib) continue;      // the current best itself
-    if (!(q > r.thr)) continue;           // behind the halfspace (raycast.py:110-117)
+#ifdef VR_RARE_STATS
+#define VR_ST(f) ++r.f
+#else
+#define VR_ST(f) (void)0
+#endif
+    if (have0 && !(fp < r.hi)) { VR_ST(st_out); continue; }  // outside the block-start band
+    if (gbase + u == r.ib) { VR_ST(st_self); continue; }     // the current best itself
+    if (!(q > r.thr)) { VR_ST(st_behind); continue; }        // behind the halfspace (raycast.py:110-117)
     if (have0 && fp >= r.lim - r.dlt) r.near = 1;
-    if (have0 && !(fp < r.lim)) continue;
+    if (have0 && !(fp < r.lim)) { VR_ST(st_band); continue; }
+    VR_ST(st_imp);
+#undef VR_ST
     double aa = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
@@ -607,6 +620,36 @@ __device__ __forceinline__ void screen_tile_pairs(RayState<D> (&ray)[R], const d
         unsigned m = 0u;
 #pragma unroll
         for (int u = 0; u < U; ++u) m |= (f[j][u] < ray[j].hi32) ? (1u << u) : 0u;
+        // fp32 halfspace pre-filter (conservative, the box tests' bound): most
+        // candidates inside the stale sphere lie behind the ray's halfspace
+        // and would be rejected by the fp64 rare path anyway (raycast.py:110-117).
+        if (__any_sync(0xffffffffu, m != 0u)) {
+          unsigned h = 0u;
+#pragma unroll 1
+          for (int p = 0; p < U / 2; ++p) {
+            const float4* q = reinterpret_cast<const float4*>(tilep + ((c >> 1) + p) * P2);
+            float v[P2];
+#pragma unroll
+            for (int k = 0; k < P2 / 4; ++k) {
+              const float4 w = q[k];
+              v[4 * k] = w.x;
+              v[4 * k + 1] = w.y;
+              v[4 * k + 2] = w.z;
+              v[4 * k + 3] = w.w;
+            }
+            uint64_t acc = f2pack(ray[j].bsl32, ray[j].bsl32);
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+              acc = ffma2(f2pack(ray[j].u32[k], ray[j].u32[k]), f2pack(v[2 * k], v[2 * k + 1]), acc);
+            float qa, qb;
+            f2unpack(acc, qa, qb);
+            h |= (qa > ray[j].thr32 ? 1u : 0u) << (2 * p);
+            h |= (qb > ray[j].thr32 ? 1u : 0u) << (2 * p + 1);
+          }
+          m &= h;
+          const int rel = ray[j].ib - (gbase + c);  // the current best itself
+          if ((unsigned)rel < (unsigned)U) m &= ~(1u << rel);
+        }
         if (wc) {
           if (j == 0) ++wc->rare_blocks;
           wc->entries += __popc(m);
@@ -1001,6 +1044,21 @@ __global__ void __launch_bounds__(32, MINB)
       atomicAdd(work + 4, up);
       atomicAdd(work + 5, cur.tests);
     }
+#ifdef VR_RARE_STATS
+    int st[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (act[j]) {
+        st[0] += ray[j].st_out; st[1] += ray[j].st_self; st[2] += ray[j].st_behind;
+        st[3] += ray[j].st_band; st[4] += ray[j].st_imp;
+      }
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      unsigned long long v = st[q];
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) atomicAdd(work + 6 + q, v);
+    }
+#endif
   }
 }
 

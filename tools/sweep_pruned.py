@@ -16,7 +16,7 @@ def run(name, ns, x, u, eta, modes=("exhaustive", "pruned")):
     n = xd.shape[0]
     ns.prune_index()
     for mode in modes:
-        work = torch.zeros(8, dtype=torch.int64, device=dev)
+        work = torch.zeros(16, dtype=torch.int64, device=dev)
         vb.raycast_batch(ns, xd, ud, ed, mode=mode)  # warm
         ks = []
         for rep in range(int(os.environ.get("REPS", "5"))):
@@ -35,7 +35,10 @@ def run(name, ns, x, u, eta, modes=("exhaustive", "pruned")):
             nw = (n + 31) // 32
             print(f"   per warp: rare blocks {w[1] / nw:.1f}, rare iterations {w[2] / nw:.1f}; "
                   f"per ray: entries {w[3] / n:.2f}, sphere updates {w[4] / n:.2f}; "
-                  f"tiles/warp {w[0] / 2048 / nw:.1f}, node tests passed/warp {w[5] / nw:.1f}")
+                  f"tiles/warp {w[0] / 2048 / nw:.1f}, node tests/warp {w[5] / nw:.1f}")
+            if w[6:11].sum():
+                print("   rare entries per ray: outside %.2f self %.2f behind %.2f band %.2f improving %.2f"
+                      % tuple(w[6:11] / n))
         print(f"{name:28s} {mode:10s} rays={n:8d} kernel={k:8.3f} ms  rays/s={n / k * 1e3:9.3e}"
               f"  pairs/ray={pairs / n:9.1f}  Gpairs/s={pairs / k / 1e6:8.1f}", flush=True)
 
