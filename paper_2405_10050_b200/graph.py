@@ -140,10 +140,15 @@ def descent_batch(ns: NodeSet, starts, seed: int = 0, stats: RaycastStats = None
     active = np.arange(S)
     while active.size:
         # one direction per active start, drawn from its own stream in the
-        # reference order (redraw while the projection vanishes)
+        # reference order (redraw while the projection vanishes).  The level
+        # of every active start is snapshotted: starts advanced while this
+        # round's groups are processed must not be picked up again with a
+        # direction drawn for their previous level.
+        k_act = k[active].copy()
+        levels = np.unique(k_act)
         u = np.empty((active.size, d))
-        for kk in np.unique(k[active]):
-            grp = active[k[active] == kk]
+        for kk in levels:
+            grp = active[k_act == kk]
             pos = np.searchsorted(active, grp)
             z = np.stack([rngs[a].standard_normal(d) for a in grp])
             v = _project_out_batch(z, basis[grp, :kk - 1])
@@ -158,8 +163,8 @@ def descent_batch(ns: NodeSet, starts, seed: int = 0, stats: RaycastStats = None
                         break
             u[pos] = v / nrm[:, None]
         still = []
-        for kk in np.unique(k[active]):
-            sel = k[active] == kk
+        for kk in levels:
+            sel = k_act == kk
             grp = active[sel]
             res = raycast_batch(ns, rr[grp], u[sel], sig[grp, :kk].astype(np.int32), stats=stats)
             idx, _, rp, flag = res.to_host()

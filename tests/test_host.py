@@ -178,3 +178,39 @@ def test_integrands_resolve():
     assert lin(np.array([1.0, 1.0])) == 6.0 and lin.device_spec == (3, (1.0, 2.0, 3.0))
     with pytest.raises(ValueError):
         it.resolve("linear:1", 3)
+
+
+def test_descent_batch_host_logic_with_escapes(monkeypatch):
+    """descent_batch's level bookkeeping (graph.py:46-85 vectorised): with
+    the device RayCast replaced by the oracle's closed-form argmin, every
+    start must reach the same sigma as the reference loop.  Gaussian points:
+    hull starts escape and retry, so the starts sit at different levels in
+    the same round (the case a level-tracking bug breaks)."""
+    import paper_2405_10050_b200.graph as G
+
+    pts = np.random.default_rng(5).standard_normal((120, 4))
+
+    class _Res:
+        def __init__(self, idx, t, rp, flag):
+            self.v = (idx, t, rp, flag)
+
+        def to_host(self):
+            return self.v
+
+    def fake_raycast(ns, x, u, eta, stats=None):
+        idx, t = orc.raycast_argmin(pts, x, u, eta)
+        esc = idx < 0
+        rp = x + np.where(esc, 0.0, t)[:, None] * u
+        return _Res(idx, t, rp, esc.astype(np.uint8))
+
+    class _NS:
+        points, dim, n = pts, 4, 120
+
+    monkeypatch.setattr(G, "raycast_batch", fake_raycast)
+    starts = np.arange(120)
+    sig, r = G.descent_batch(_NS(), starts, seed=0)
+    nodes = orc.Nodes(pts)
+    for s in starts:
+        v_sig, v_r = orc.descent(nodes, int(s), vb.rng.stream(0, "descent", int(s)))
+        assert tuple(sig[s]) == tuple(v_sig), s
+        assert np.allclose(r[s], v_r, rtol=0, atol=1e-9 * max(1.0, np.abs(v_r).max()))

@@ -68,6 +68,29 @@ if __name__ == "__main__":
             proj = np.einsum("kd,ksd->ks", u, pts[sg])
             g = sg[np.arange(n), np.argmax(proj, 1)].astype(np.int32)
             run("c2 vertex-start (config 2)", ns, x, u, g[:, None])
+    def edge_rays(ns, pts, seeds):
+        """All d+1 edge rays of the descent vertices of `seeds` (traversal rays,
+        |eta| = d, eta sorted so eta[0] is the smallest index)."""
+        sig, r = vb.descent_batch(ns, seeds, seed=0)
+        d = pts.shape[1]
+        u, ok = vb.vertex_directions_batch(ns, sig)
+        u = u.cpu().numpy().reshape(-1, d)
+        ok = ok.cpu().numpy().reshape(-1).astype(bool)
+        x = np.repeat(r, d + 1, axis=0)
+        eta = np.stack([np.delete(s_, k) for s_ in sig for k in range(d + 1)]).astype(np.int32)
+        eta.sort(axis=1)
+        return x[ok], u[ok], eta[ok]
+
+    if "c5edge" in which:
+        pts = np.random.default_rng(0).random((10 ** 6, 8)).astype(np.float32).astype(np.float64)
+        ns = vb.NodeSet(pts)
+        seeds = np.random.default_rng(1).choice(10 ** 6, 10000, replace=False)
+        run("c5 edge rays N=1e6 d=8", ns, *edge_rays(ns, pts, seeds))
+    if "c3edge" in which:
+        pts = np.random.default_rng(0).standard_normal((10000, 5))
+        ns = vb.NodeSet(pts)
+        seeds = np.random.default_rng(1).choice(10000, 10000, replace=False)
+        run("c3 edge rays N=1e4 d=5", ns, *edge_rays(ns, pts, seeds))
     if "c5gen" in which:
         pts = np.random.default_rng(0).random((10 ** 6, 8)).astype(np.float32).astype(np.float64)
         ns = vb.NodeSet(pts)
