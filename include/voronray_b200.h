@@ -51,7 +51,7 @@ enum vr_cell_status {
   VR_CELL_OVERFLOW = 3     /* more distinct hit faces than area slots          */
 };
 
-int vr_abi_version(void);
+int vr_abi_version(void); /* 2 */
 const char* vr_status_string(int status);
 
 /* Record stride (doubles) of one packed generator for dimension d:
@@ -154,6 +154,15 @@ typedef struct vr_prune_index {
   const float* node_box32; /* centred fp32 outward copies; nullable            */
   const int32_t* node_range; /* 2 per node: first tile, last tile + 1        */
   int64_t n;
+  /* 32-ary tree over the tiles (cooperative warp-per-ray kernel): level 0 is
+   * the tiles themselves (boxes = tile_box32 rows), node j of level l covers
+   * nodes [32j, 32j+32) of level l-1; the top level holds one node.  Rows of
+   * box32 layout, level l at rows [wide_off[l], wide_off[l] + wide_cnt[l]).
+   * wide_box32 == NULL or wide_levels < 2 disables the cooperative kernel. */
+  const float* wide_box32;
+  int32_t wide_levels;
+  int64_t wide_off[8];
+  int64_t wide_cnt[8];
 } vr_prune_index;
 
 /* vr_raycast_batch through the pruned index.  `order` (nullable, n_rays

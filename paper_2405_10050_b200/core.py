@@ -199,7 +199,31 @@ class _PruneStruct(ctypes.Structure):
                 ("inv_perm", ctypes.c_void_p), ("tile_box", ctypes.c_void_p),
                 ("tile_box32", ctypes.c_void_p), ("node_box", ctypes.c_void_p),
                 ("node_box32", ctypes.c_void_p), ("node_range", ctypes.c_void_p),
-                ("n", ctypes.c_int64)]
+                ("n", ctypes.c_int64), ("wide_box32", ctypes.c_void_p),
+                ("wide_levels", ctypes.c_int32), ("wide_off", ctypes.c_int64 * 8),
+                ("wide_cnt", ctypes.c_int64 * 8)]
+
+
+WIDE = 32
+
+
+def wide_levels(lo, hi):
+    """32-ary tree over kd-ordered tile boxes: level 0 = tiles, node j of
+    level l = union of nodes [32j, 32j+32) of level l-1, up to one root (at
+    least two levels).  Returns a list of (lo, hi) fp64 tensors per level."""
+    levels = [(lo, hi)]
+    while levels[-1][0].shape[0] > 1 or len(levels) < 2:
+        a, b = levels[-1]
+        m, d = a.shape
+        g = (m + WIDE - 1) // WIDE
+        pad = g * WIDE - m
+        if pad:
+            a = torch.cat([a, torch.full((pad, d), float("inf"), dtype=a.dtype, device=a.device)])
+            b = torch.cat([b, torch.full((pad, d), float("-inf"), dtype=b.dtype, device=b.device)])
+        levels.append((a.view(g, WIDE, d).amin(1), b.view(g, WIDE, d).amax(1)))
+    if len(levels) > 8:
+        raise ValueError("too many generators for the 32-ary tile tree")
+    return levels
 
 
 def kd_order(P, tile=PRUNE_TILE):
@@ -357,10 +381,18 @@ class PruneIndex:
                    "vr_pack_records32_pairs")
         self.tile_box32 = _outward32(lo, hi, self.screen32.center)
         self.node_box32 = _outward32(nlo, nhi, self.screen32.center)
+        lv = wide_levels(lo, hi)
+        boxes = [_outward32(a, b, self.screen32.center) for a, b in lv]
+        self.wide_cnt = [int(b.shape[0]) for b in boxes]
+        self.wide_off = np.concatenate([[0], np.cumsum(self.wide_cnt)[:-1]]).astype(np.int64).tolist()
+        self.wide_box32 = torch.cat(boxes).contiguous()
         p = lambda t: t.data_ptr()  # noqa: E731
+        pad8 = lambda v: (ctypes.c_int64 * 8)(*(list(v) + [0] * (8 - len(v))))  # noqa: E731
         self.struct = _PruneStruct(p(crec), p(self.rec32p), p(self.perm), p(self.inv_perm),
                                    p(self.tile_box), p(self.tile_box32), p(self.node_box),
-                                   p(self.node_box32), p(self.node_range), n)
+                                   p(self.node_box32), p(self.node_range), n,
+                                   p(self.wide_box32), len(boxes), pad8(self.wide_off),
+                                   pad8(self.wide_cnt))
 
 
 def build_node_set(points, backend="auto"):

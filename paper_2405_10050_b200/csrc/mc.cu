@@ -356,9 +356,7 @@ extern "C" int vr_mc_rays_pruned(const double* rec, int64_t n_gen, int d, double
     return VR_EINVAL;
   const int64_t n = n_cells * rays_per_cell;
   RayOut out{out_idx, out_t, nullptr, out_flag, recheck_list, recheck_count};
-  PrunedIndex pi{ix->rec, s32 ? ix->rec32 : nullptr, ix->perm, ix->inv_perm, ix->tile_box,
-                 ix->tile_box32, ix->node_box, ix->node_box32,
-                 reinterpret_cast<const int2*>(ix->node_range), ix->n};
+  const PrunedIndex pi = pruned_index_from(ix, s32 != nullptr);
   const Screen sc = make_screen(sqmax, s32, d);
   VR_DISPATCH_D(d, {
     SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n};

@@ -13,7 +13,17 @@ int vr::raycast_variant() {
   return v;
 }
 
-extern "C" int vr_abi_version(void) { return 1; }
+// Pruned-kernel choice: VR_COOP=1 selects the cooperative warp-per-ray
+// kernel instead of the warp-per-32-rays kernel (default).
+int vr::coop_mode() {
+  static int v = [] {
+    const char* e = std::getenv("VR_COOP");
+    return e ? std::atoi(e) : -1;
+  }();
+  return v;
+}
+
+extern "C" int vr_abi_version(void) { return 2; }
 
 extern "C" const char* vr_status_string(int status) {
   switch (status) {
@@ -101,9 +111,7 @@ extern "C" int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double
   if (eta_len < 1 || eta_len > d || ix->n != n_gen) return VR_EINVAL;
   if ((recheck_list == nullptr) != (recheck_count == nullptr)) return VR_EINVAL;
   RayOut out{out_idx, out_t, out_rp, out_flag, recheck_list, recheck_count};
-  PrunedIndex pi{ix->rec, s32 ? ix->rec32 : nullptr, ix->perm, ix->inv_perm, ix->tile_box,
-                 ix->tile_box32, ix->node_box, ix->node_box32,
-                 reinterpret_cast<const int2*>(ix->node_range), ix->n};
+  const PrunedIndex pi = pruned_index_from(ix, s32 != nullptr);
   const Screen sc = make_screen(sqmax, s32, d);
   VR_DISPATCH_D(d, {
     SrcExplicit<D> src{x, u, eta, eta_len, rec, n_rays, order};

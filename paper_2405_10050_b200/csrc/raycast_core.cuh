@@ -350,6 +350,8 @@ struct SrcExplicit {
   const int32_t* order = nullptr;  // optional processing order (slot -> ray id)
   __device__ __forceinline__ int64_t id(int64_t k) const { return order ? order[k] : k; }
   __device__ __forceinline__ int32_t gen(int64_t k) const { return eta[id(k) * eta_len]; }
+  __host__ __device__ __forceinline__ int eta_count() const { return eta_len; }
+  __device__ __forceinline__ int32_t eta_at(int64_t k, int e) const { return eta[id(k) * eta_len + e]; }
   __device__ __forceinline__ bool load(int64_t k, RayState<D>& r, const Frame& fr) const {
     if (k >= n) return false;
     k = id(k);
@@ -436,6 +438,8 @@ struct SrcMC {
   }
   __device__ __forceinline__ int64_t id(int64_t k) const { return order ? order[k] : k; }
   __device__ __forceinline__ int32_t gen(int64_t k) const { return cells[id(k) / per]; }
+  __host__ __device__ __forceinline__ int eta_count() const { return 1; }
+  __device__ __forceinline__ int32_t eta_at(int64_t k, int) const { return gen(k); }
   __device__ __forceinline__ bool load(int64_t k, RayState<D>& r, const Frame& fr) const {
     if (k >= n) return false;
     k = id(k);
@@ -1063,6 +1067,336 @@ __global__ void __launch_bounds__(32, MINB)
 }
 
 // ---------------------------------------------------------------------------
+// Cooperative pruned kernel: one WARP per ray.
+//
+// In high dimension the union of 32 rays' spheres covers many more tiles than
+// each ray needs (config-5 edge rays: ~460 tiles per warp vs ~2.4 per ray for
+// the final spheres), so here the 32 lanes work on ONE ray: a tile of 64
+// candidates is screened as one pair (two candidates, packed FFMA2) per lane,
+// and the kd tiles are grouped into a 32-ary tree whose children are tested
+// one per lane.  The block-batched rare path is applied to a whole tile: the
+// improving candidates of all lanes are reduced to the smallest t (warp
+// argmin, division-free), one sphere update, every other improving candidate
+// re-tested against the new sphere (RECHECK if inside its band).  Skipping
+// is a certificate and the screen is conservative, so results equal the
+// exhaustive kernel's.
+// ---------------------------------------------------------------------------
+#ifndef VR_COOP_MINB
+#define VR_COOP_MINB 1
+#endif
+constexpr int WIDE = 32;
+constexpr int WIDE_MAX_LEVELS = 8;
+
+struct WideTree {
+  const float* box32;             // fp32 centred outward boxes, all levels (box32_stride rows)
+  int64_t off[WIDE_MAX_LEVELS];   // first row of level l (level 0 = tiles)
+  int64_t cnt[WIDE_MAX_LEVELS];   // nodes in level l
+  int levels;                     // the top level (levels - 1) holds one node
+};
+
+// fp32 box test for one ray against a box held in registers; d2 = squared
+// distance of the sphere centre to the box (ordering key).
+template <int D>
+__device__ __forceinline__ bool coop_box_need(const RayState<D>& r, const float (&v)[box32_stride(D)],
+                                              float& d2) {
+  float umax = 0.0f;
+  d2 = 0.0f;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const float lo = v[k], hi = v[D + k];
+    umax = fmaf(r.u32[k], r.u32[k] > 0.0f ? hi : lo, umax);
+    const float zc = -0.5f * r.z32[k];
+    const float e = fmaxf(fmaxf(lo - zc, zc - hi) - r.del32, 0.0f);
+    d2 = fmaf(e, e, d2);
+  }
+  if (umax + r.bsl32 <= r.thr32) return false;
+  return !(d2 >= r.rb32);
+}
+
+template <int D>
+__device__ __forceinline__ void coop_load_box(const float* p, float (&v)[box32_stride(D)]) {
+  const float4* b4 = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int k = 0; k < box32_stride(D) / 4; ++k) {
+    const float4 w = __ldg(b4 + k);
+    v[4 * k] = w.x;
+    v[4 * k + 1] = w.y;
+    v[4 * k + 2] = w.z;
+    v[4 * k + 3] = w.w;
+  }
+}
+
+// Warp argmin of t = num / (2 den) (den > 0), smallest index on exact ties;
+// lanes without a candidate pass idx < 0.  Returns the winning lane's triple.
+__device__ __forceinline__ void coop_argmin(double& num, double& den, int& idx) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double on = __shfl_xor_sync(0xffffffffu, num, off);
+    const double od = __shfl_xor_sync(0xffffffffu, den, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, off);
+    bool take;
+    if (oi < 0) take = false;
+    else if (idx < 0) take = true;
+    else {
+      const double a = on * den, b = num * od;
+      take = a < b || (a == b && oi < idx);
+    }
+    if (take) { num = on; den = od; idx = oi; }
+  }
+  // rounded products are not a strict order in near-ties: make every lane
+  // agree on lane 0's result (the ray state must stay warp-uniform)
+  num = __shfl_sync(0xffffffffu, num, 0);
+  den = __shfl_sync(0xffffffffu, den, 0);
+  idx = __shfl_sync(0xffffffffu, idx, 0);
+}
+
+// Seed: the best valid candidate of the ray's start tile (two per lane).
+template <int D, int PT>
+__device__ __forceinline__ void coop_seed(RayState<D>& r, const double* __restrict__ crec,
+                                          int64_t tile, const Frame& fr) {
+  constexpr int S = rec_stride(D);
+  const int lane = threadIdx.x & 31;
+  double bn = 1.0, bd = 0.0;
+  int bi = -1;
+#pragma unroll
+  for (int h = 0; h < PT / 32; ++h) {
+    const int64_t i = tile * PT + h * 32 + lane;
+    double xi[D];
+    load_rec_g<D>(crec + i * S, xi);
+    const bool real = !isinf(__ldg(crec + i * S + D));
+    double q = 0.0, aa = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      q = fma(r.u[k], xi[k], q);
+      const double a = r.x[k] - xi[k];
+      aa = fma(a, a, aa);
+    }
+    const double num = aa - r.base, den = q - r.s;
+    if (real && q > r.thr && (bi < 0 || num * bd < bn * den)) { bn = num; bd = den; bi = (int)i; }
+  }
+  coop_argmin(bn, bd, bi);
+  if (bi >= 0) {
+    const double t = bn / (2.0 * bd);
+    if (r.ib < 0 || t < r.tb) ray_set_best<D, true>(r, t, bd, bi, fr);
+  }
+}
+
+// Rare path for one tile: lanes hold up to two candidates that passed the
+// fp32 screens (pa / pb; candidate indices ia, ia + 1).
+template <int D>
+__device__ __forceinline__ void coop_rare(RayState<D>& r, const double* __restrict__ crec,
+                                          int ia, bool pa, bool pb, const Frame& fr) {
+  constexpr int S = rec_stride(D);
+  const bool have0 = r.ib >= 0;
+  double zk2[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) zk2[k] = have0 ? -2.0 * fma(r.tb, r.u[k], r.x[k]) : 0.0;
+  double bn = 1.0, bd = 0.0;
+  int bi = -1;
+  int near = 0;
+  unsigned imp = 0u;
+  double xs[2][D], sqs[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const bool p = h ? pb : pa;
+    if (!p) continue;
+    const int i = ia + h;
+    load_rec_g<D>(crec + (int64_t)i * S, xs[h]);
+    sqs[h] = __ldg(crec + (int64_t)i * S + D);
+    double fp = sqs[h], q = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      fp = fma(zk2[k], xs[h][k], fp);
+      q = fma(r.u[k], xs[h][k], q);
+    }
+    if (have0 && !(fp < r.hi)) continue;
+    if (!(q > r.thr)) continue;  // raycast.py:110-117
+    if (have0 && fp >= r.lim - r.dlt) near = 1;
+    if (have0 && !(fp < r.lim)) continue;
+    double aa = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const double a = r.x[k] - xs[h][k];
+      aa = fma(a, a, aa);
+    }
+    const double num = aa - r.base, den = q - r.s;  // raycast.py:201-203
+    if (bi < 0 || num * bd < bn * den) { bn = num; bd = den; bi = i; }
+    imp |= 1u << h;
+  }
+  int wi = bi;
+  double wn = bn, wd = bd;
+  coop_argmin(wn, wd, wi);
+  if (wi >= 0) {
+    const double t = wn / (2.0 * wd);
+    const double told = r.tb, denold = r.denb;
+    ray_set_best<D, true>(r, t, wd, wi, fr);
+    if (have0 && 2.0 * denold * (told - t) < r.dlt) near = 1;
+    // every other improving candidate against the new sphere
+#pragma unroll
+    for (int k = 0; k < D; ++k) zk2[k] = -2.0 * fma(t, r.u[k], r.x[k]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!((imp >> h) & 1u) || ia + h == wi) continue;
+      double fp = sqs[h];
+#pragma unroll
+      for (int k = 0; k < D; ++k) fp = fma(zk2[k], xs[h][k], fp);
+      if (fp < r.hi) near = 1;
+    }
+  }
+  if (__any_sync(0xffffffffu, near)) r.near = 1;
+}
+
+template <int D, int PT>
+__device__ __forceinline__ void coop_screen_tile(RayState<D>& r, const double* __restrict__ crec,
+                                                 const float* __restrict__ crec32p, int64_t tile,
+                                                 const Frame& fr, WarpCounters* wc) {
+  static_assert(PT == 64, "one candidate pair per lane");
+  constexpr int P2 = rec32p_stride(D);
+  const int lane = threadIdx.x & 31;
+  const float4* q4 = reinterpret_cast<const float4*>(crec32p + (tile * (PT / 2) + lane) * P2);
+  float v[P2];
+#pragma unroll
+  for (int k = 0; k < P2 / 4; ++k) {
+    const float4 w = __ldg(q4 + k);
+    v[4 * k] = w.x;
+    v[4 * k + 1] = w.y;
+    v[4 * k + 2] = w.z;
+    v[4 * k + 3] = w.w;
+  }
+  uint64_t acc = f2pack(v[2 * D], v[2 * D + 1]);
+#pragma unroll
+  for (int k = 0; k < D; ++k) acc = ffma2(f2pack(r.z32[k], r.z32[k]), f2pack(v[2 * k], v[2 * k + 1]), acc);
+  float fa, fb;
+  f2unpack(acc, fa, fb);
+  bool pa = fa < r.hi32, pb = fb < r.hi32;
+  if (!__any_sync(0xffffffffu, pa || pb)) return;
+  // conservative fp32 halfspace pre-filter + the current best itself
+  uint64_t qa2 = f2pack(r.bsl32, r.bsl32);
+#pragma unroll
+  for (int k = 0; k < D; ++k) qa2 = ffma2(f2pack(r.u32[k], r.u32[k]), f2pack(v[2 * k], v[2 * k + 1]), qa2);
+  float qa, qb;
+  f2unpack(qa2, qa, qb);
+  const int ia = (int)(tile * PT) + 2 * lane;
+  pa = pa && qa > r.thr32 && ia != r.ib;
+  pb = pb && qb > r.thr32 && ia + 1 != r.ib;
+  const unsigned m = __ballot_sync(0xffffffffu, pa || pb);
+  if (!m) return;
+  if (wc) {
+    ++wc->rare_blocks;
+    wc->entries += (pa ? 1 : 0) + (pb ? 1 : 0);
+  }
+  coop_rare<D>(r, crec, ia, pa, pb, fr);
+}
+
+template <int D, int PT, int NW, int MINB, class Src>
+__global__ void __launch_bounds__(NW * 32, MINB)
+    k_raycast_coop(Src src, int64_t n_rays, const double* __restrict__ crec,
+                   const float* __restrict__ crec32p, const int32_t* __restrict__ perm,
+                   const int32_t* __restrict__ inv_perm, WideTree wt, Frame fr, RayOut out,
+                   unsigned long long* __restrict__ work) {
+  constexpr int BS = box32_stride(D);
+  constexpr int STK = WIDE * WIDE_MAX_LEVELS;
+  __shared__ int stk_s[NW][STK];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  int* stk = stk_s[w];
+  const int64_t k = (int64_t)blockIdx.x * NW + w;
+  if (k >= n_rays) return;
+  RayState<D> r;
+  src.load(k, r, fr);
+  coop_seed<D, PT>(r, crec, inv_perm[src.gen(k)] / PT, fr);
+  // edge rays: the tiles of the other eta generators surround the origin too
+  for (int e = 1; e < src.eta_count(); ++e) coop_seed<D, PT>(r, crec, inv_perm[src.eta_at(k, e)] / PT, fr);
+  WarpCounters wc;
+  unsigned long long tiles = 0, tests = 0;
+  const int top = wt.levels - 1;
+  int sp = 1;
+  if (lane == 0) stk[0] = top << 24;
+  __syncwarp();
+  while (sp > 0) {
+    --sp;
+    const int e = stk[sp];
+    const int lev = e >> 24;
+    const int64_t c0 = (int64_t)(e & 0xFFFFFF) * WIDE;
+    const int cl = lev - 1;
+    const int64_t child = c0 + lane;
+    float box[BS];
+    bool need = false;
+    float d2 = 0.0f;
+    if (child < wt.cnt[cl]) {
+      coop_load_box<D>(wt.box32 + (wt.off[cl] + child) * BS, box);
+      need = coop_box_need<D>(r, box, d2);
+    }
+    ++tests;
+    unsigned mask = __ballot_sync(0xffffffffu, need);
+    if (cl > 0) {
+      // push: nearest child (smallest d2) on top, the rest in lane order
+      float bd2 = need ? d2 : CUDART_INF_F;
+      int bl = need ? lane : 32;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const float o = __shfl_xor_sync(0xffffffffu, bd2, off);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, off);
+        if (o < bd2 || (o == bd2 && ol < bl)) { bd2 = o; bl = ol; }
+      }
+      bl = __shfl_sync(0xffffffffu, bl, 0);
+      if (mask) {
+        const unsigned rest = mask & ~(1u << bl);
+        if (need && lane != bl) {
+          // higher lanes deeper in the stack: lane order pops ascending
+          const int pos = sp + __popc(rest >> (lane + 1));
+          if (pos >= STK) __trap();
+          stk[pos] = (cl << 24) | (int)child;
+        }
+        sp += __popc(rest);
+        if (lane == bl) stk[sp] = (cl << 24) | (int)child;
+        ++sp;
+        if (sp > STK) __trap();
+      }
+      __syncwarp();
+    } else {
+      // children are tiles: nearest first, each re-tested against the
+      // current (shrinking) sphere before it is screened
+      unsigned todo = mask;
+      while (todo) {
+        const bool mine = (todo >> lane) & 1u;
+        bool nd = false;
+        if (mine) nd = coop_box_need<D>(r, box, d2);
+        todo = __ballot_sync(0xffffffffu, nd);
+        if (!todo) break;
+        float bd2 = nd ? d2 : CUDART_INF_F;
+        int bl = nd ? lane : 32;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const float o = __shfl_xor_sync(0xffffffffu, bd2, off);
+          const int ol = __shfl_xor_sync(0xffffffffu, bl, off);
+          if (o < bd2 || (o == bd2 && ol < bl)) { bd2 = o; bl = ol; }
+        }
+        bl = __shfl_sync(0xffffffffu, bl, 0);
+        todo &= ~(1u << bl);
+        ++tiles;
+        coop_screen_tile<D, PT>(r, crec, crec32p, c0 + bl, fr, work ? &wc : nullptr);
+      }
+    }
+  }
+  if (lane == 0) ray_store<D>(r, src.id(k), perm, out);
+  if (work && lane == 0) {
+    atomicAdd(work, tiles * (unsigned long long)PT);
+    atomicAdd(work + 5, tests);
+    atomicAdd(work + 4, (unsigned long long)r.nupd);
+  }
+  if (work) {
+    unsigned long long e = wc.entries, rb = wc.rare_blocks;
+    for (int off = 16; off > 0; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
+    if (lane == 0) {
+      atomicAdd(work + 1, rb);
+      atomicAdd(work + 2, rb);
+      atomicAdd(work + 3, e);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Exact re-check: one CTA per listed ray.  Pass 1: centred t for every valid
 // candidate, lexicographic (t, index) argmin.  Pass 2: runner-up distance at
 // the winner's vertex; DEGENERATE when second < radius (1 + 1e-10)
@@ -1229,6 +1563,7 @@ struct PrunedIndex {
   const float* node_box32;
   const int2* node_range;  // [first tile, last tile + 1) per node
   int64_t n;
+  WideTree wide;           // 32-ary tree over the tiles (cooperative kernel)
 };
 
 constexpr int PRUNE_TILE = 64;
@@ -1266,6 +1601,33 @@ int launch_pruned_f(const Src& src, int64_t n_rays, const PrunedIndex& ix, const
 }
 
 template <int D, class Src>
+int launch_coop(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
+                const RayOut& out, cudaStream_t st, unsigned long long* work) {
+  constexpr int NW = 4;
+  constexpr int MINB = VR_COOP_MINB;
+  const int64_t grid = (n_rays + NW - 1) / NW;
+  k_raycast_coop<D, PRUNE_TILE, NW, MINB, Src><<<(unsigned)grid, NW * 32, 0, st>>>(
+      src, n_rays, ix.crec, ix.crec32, ix.perm, ix.inv_perm, ix.wide, fr, out, work);
+  VR_RETURN_LAUNCH();
+}
+
+int coop_mode();
+
+// Host-side view of the C-ABI index -> kernel parameters.
+inline PrunedIndex pruned_index_from(const vr_prune_index* ix, bool f32) {
+  PrunedIndex pi{ix->rec, f32 ? ix->rec32 : nullptr, ix->perm, ix->inv_perm, ix->tile_box,
+                 ix->tile_box32, ix->node_box, ix->node_box32,
+                 reinterpret_cast<const int2*>(ix->node_range), ix->n, WideTree{}};
+  pi.wide.box32 = ix->wide_box32;
+  pi.wide.levels = ix->wide_levels;
+  for (int l = 0; l < WIDE_MAX_LEVELS; ++l) {
+    pi.wide.off[l] = l < ix->wide_levels ? ix->wide_off[l] : 0;
+    pi.wide.cnt[l] = l < ix->wide_levels ? ix->wide_cnt[l] : 0;
+  }
+  return pi;
+}
+
+template <int D, class Src>
 int launch_raycast_pruned(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
                           const RayOut& out, cudaStream_t st, unsigned long long* work) {
   if (n_rays <= 0) return VR_OK;
@@ -1274,6 +1636,13 @@ int launch_raycast_pruned(const Src& src, int64_t n_rays, const PrunedIndex& ix,
     cudaError_t e = cudaMemsetAsync(out.recheck_count, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return vr_cuda_status(e);
   }
+  // The cooperative warp-per-ray kernel wins only for sparse, incoherent
+  // high-dimensional edge rays (config-5 sample: 7.2 vs 9.5 ms) and loses on
+  // dense traversal levels (config 5 L=5: 10.3 vs 7.4 s) and everywhere at
+  // d <= 6, so it is opt-in (VR_COOP=1).
+  const bool coop = coop_mode() > 0;
+  if (ix.crec32 && ix.wide.box32 && ix.wide.levels >= 2 && coop)
+    return launch_coop<D>(src, n_rays, ix, fr, out, st, work);
   if (ix.crec32 && ix.tile_box32 && ix.node_box32)
     return launch_pruned_f<D, true>(src, n_rays, ix, fr, out, st, work);
   return launch_pruned_f<D, false>(src, n_rays, ix, fr, out, st, work);

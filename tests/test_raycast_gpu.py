@@ -229,3 +229,45 @@ def test_pruned_equals_exhaustive(d):
             b = vb.raycast_batch(ns, xs, uu, eta, mode=mode, screen=screen).to_host()
             for x, y in zip(a, b):
                 assert np.array_equal(x, y, equal_nan=True), (mode, screen)
+
+
+_COOP_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2405_10050_b200 as vb
+bad = 0
+for n, d, seed in ((6000, 8, 0), (5000, 6, 1), (3000, 4, 2)):
+    pts = np.random.default_rng(seed).random((n, d))
+    ns = vb.NodeSet(pts)
+    sig, r = vb.descent_batch(ns, np.arange(0, n, n // 40), seed=0)
+    u, ok = vb.vertex_directions_batch(ns, sig)
+    u = u.cpu().numpy().reshape(-1, d)
+    x = np.repeat(r, d + 1, axis=0)
+    eta = np.stack([np.delete(s_, k) for s_ in sig for k in range(d + 1)]).astype(np.int32)
+    eta.sort(axis=1)
+    rng = np.random.default_rng(seed + 10)
+    g = rng.integers(0, n, 2000).astype(np.int32)
+    ug = rng.standard_normal((2000, d))
+    ug /= np.linalg.norm(ug, axis=1, keepdims=True)
+    for xx, uu, ee in ((x, u, eta), (pts[g], ug, g[:, None])):
+        a = vb.raycast_batch(ns, xx, uu, ee, mode="pruned")
+        b = vb.raycast_batch(ns, xx, uu, ee, mode="exhaustive")
+        bad += int(((a.idx != b.idx) | (a.flag != b.flag)).sum().item())
+        bad += int((a.t != b.t).sum().item())
+print("BAD", bad)
+"""
+
+
+def test_coop_kernel_matches_exhaustive():
+    """The opt-in cooperative warp-per-ray pruned kernel (VR_COOP=1, read once
+    per process, hence the subprocess) is bitwise equal to the exhaustive
+    kernel on edge rays (|eta| = d) and generator-start rays."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VR_COOP="1")
+    res = subprocess.run([sys.executable, "-c", _COOP_SCRIPT, root], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    assert "BAD 0" in res.stdout, res.stdout[-2000:]

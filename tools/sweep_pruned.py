@@ -29,6 +29,11 @@ def run(name, ns, x, u, eta, modes=("exhaustive", "pruned")):
             torch.cuda.synchronize()
             ks.append(e[0].elapsed_time(e[1]))
         k = float(np.median(ks))
+        if os.environ.get("CHECK") and mode == "pruned":
+            ref = vb.raycast_batch(ns, xd, ud, ed, mode="exhaustive")
+            got = vb.raycast_batch(ns, xd, ud, ed, mode="pruned")
+            bad = ((ref.idx != got.idx) | (ref.flag != got.flag)).sum().item()
+            print(f"   CHECK vs exhaustive: {bad} mismatching rays of {n}", flush=True)
         w = work.cpu().numpy()
         pairs = int(w[0]) if mode == "pruned" else n * ns.n
         if mode == "pruned":
@@ -41,6 +46,21 @@ def run(name, ns, x, u, eta, modes=("exhaustive", "pruned")):
                       % tuple(w[6:11] / n))
         print(f"{name:28s} {mode:10s} rays={n:8d} kernel={k:8.3f} ms  rays/s={n / k * 1e3:9.3e}"
               f"  pairs/ray={pairs / n:9.1f}  Gpairs/s={pairs / k / 1e6:8.1f}", flush=True)
+
+
+def edge_rays(ns, pts, seeds):
+    """All d+1 edge rays of the descent vertices of `seeds` (traversal rays,
+    |eta| = d, eta sorted so eta[0] is the smallest index)."""
+    sig, r = vb.descent_batch(ns, seeds, seed=0)
+    d = pts.shape[1]
+    u, ok = vb.vertex_directions_batch(ns, sig)
+    u = u.cpu().numpy().reshape(-1, d)
+    ok = ok.cpu().numpy().reshape(-1).astype(bool)
+    x = np.repeat(r, d + 1, axis=0)
+    eta = np.stack([np.delete(s_, k) for s_ in sig for k in range(d + 1)]).astype(np.int32)
+    eta.sort(axis=1)
+    return x[ok], u[ok], eta[ok]
+
 
 
 if __name__ == "__main__":
@@ -68,19 +88,6 @@ if __name__ == "__main__":
             proj = np.einsum("kd,ksd->ks", u, pts[sg])
             g = sg[np.arange(n), np.argmax(proj, 1)].astype(np.int32)
             run("c2 vertex-start (config 2)", ns, x, u, g[:, None])
-    def edge_rays(ns, pts, seeds):
-        """All d+1 edge rays of the descent vertices of `seeds` (traversal rays,
-        |eta| = d, eta sorted so eta[0] is the smallest index)."""
-        sig, r = vb.descent_batch(ns, seeds, seed=0)
-        d = pts.shape[1]
-        u, ok = vb.vertex_directions_batch(ns, sig)
-        u = u.cpu().numpy().reshape(-1, d)
-        ok = ok.cpu().numpy().reshape(-1).astype(bool)
-        x = np.repeat(r, d + 1, axis=0)
-        eta = np.stack([np.delete(s_, k) for s_ in sig for k in range(d + 1)]).astype(np.int32)
-        eta.sort(axis=1)
-        return x[ok], u[ok], eta[ok]
-
     if "c5edge" in which:
         pts = np.random.default_rng(0).random((10 ** 6, 8)).astype(np.float32).astype(np.float64)
         ns = vb.NodeSet(pts)
