@@ -969,11 +969,16 @@ __global__ void __launch_bounds__(32, MINB)
   constexpr int S = rec_stride(D);
   // both copies are staged: the fp64 rows feed the rare path, which is hit
   // often enough (tens of entries per ray at d=8) that global loads stall
-  constexpr uint32_t BYTES64 = (uint32_t)(PT * S * sizeof(double));
+#ifdef VR_STAGE64
+  constexpr bool STAGE64 = true;
+#else
+  constexpr bool STAGE64 = !F32;  // fp32 screen: the rare path reads fp64 rows from L2
+#endif
+  constexpr uint32_t BYTES64 = STAGE64 ? (uint32_t)(PT * S * sizeof(double)) : 0u;
   constexpr int P2 = rec32p_stride(D);
   constexpr uint32_t BYTES32 = F32 ? (uint32_t)(PT / 2 * P2 * sizeof(float)) : 0u;
   static_assert(PT % 8 == 0 && VR_REC_PAD % PT == 0, "tile must divide the record padding");
-  __shared__ __align__(128) double buf[2][PT * S];
+  __shared__ __align__(128) double buf[2][STAGE64 ? PT * S : 2];
   __shared__ __align__(128) float buf32[2][F32 ? PT / 2 * P2 : 4];
   __shared__ uint64_t bar[2];
   const int lane = threadIdx.x;
@@ -1003,7 +1008,7 @@ __global__ void __launch_bounds__(32, MINB)
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive_expect_tx(&bar[b], BYTES64 + BYTES32);
-      bulk_g2s(buf[b], crec + t * PT * S, BYTES64, &bar[b]);
+      if constexpr (STAGE64) bulk_g2s(buf[b], crec + t * PT * S, BYTES64, &bar[b]);
       if constexpr (F32) bulk_g2s(buf32[b], crec32 + t * (PT / 2) * P2, BYTES32, &bar[b]);
     }
   };
@@ -1023,7 +1028,8 @@ __global__ void __launch_bounds__(32, MINB)
     // was expanded, and re-testing skipped < 2% of the tiles on config 2)
     ++tiles_done;
     if constexpr (F32)
-      screen_tile_pairs<D, R, PT>(ray, buf[b], buf32[b], (int)(t * PT), fr, work ? &wc : nullptr);
+      screen_tile_pairs<D, R, PT>(ray, STAGE64 ? buf[b] : crec + t * PT * S, buf32[b],
+                                  (int)(t * PT), fr, work ? &wc : nullptr);
     else
       screen_tile<D, R, PT, F32>(ray, buf[b], buf32[b], (int)(t * PT), fr, work ? &wc : nullptr);
     __syncwarp();
@@ -1599,7 +1605,11 @@ int launch_pruned_f(const Src& src, int64_t n_rays, const PrunedIndex& ix, const
   }
   // one ray per lane: the warp's 32 rays are spatially tighter (fewer tiles
   // pass the union test) and the lighter register file fits 12-24 warps/SM
+#ifdef VR_PRUNED_MINB
+  constexpr int MINB = VR_PRUNED_MINB;
+#else
   constexpr int MINB = (D <= 3) ? 24 : (D <= 4 ? 20 : (D <= 6 ? 16 : 12));
+#endif
   return launch_pruned_rm<D, 1, MINB, F32>(src, n_rays, ix, fr, out, st, work);
 }
 
