@@ -331,8 +331,10 @@ def run_ours(args):
 
     def step(i, mode=args.mode, events=None):
         flush.fill_(i & 0xFF)  # L2 flush, outside the timed events
+        torch.cuda.nvtx.range_push("bench_step")  # ncu --nvtx-include "bench_step/"
         vb.raycast_batch(ns, xd, ud, gd, out=out, workspace=ws, events=events or ev[i],
                          mode=mode, work=work if mode == "pruned" else None)
+        torch.cuda.nvtx.range_pop()
 
     for i in range(args.warmup):
         step(i)
