@@ -378,17 +378,18 @@ def _vertex_directions(pts, sigma, positions):
 
 
 class HostRaycaster:
-    """Batched RayCast on host (pinned) arrays.  Chunks cycle through NBUF
+    """Batched RayCast on host (pinned) arrays.  Chunks cycle through `nbuf`
     device buffers; H2D copies, D2H copies and kernels run on separate
-    streams (two compute streams, so one chunk's kernel tail overlaps the
+    streams (several compute streams, so one chunk's kernel tail overlaps the
     next chunk's kernel) -- the copy engines and the SMs work concurrently.
-    The end-to-end public entry point for callers whose rays live in host
-    memory."""
+    Each chunk's device work replays a captured CUDA graph.  The end-to-end
+    public entry point for callers whose rays live in host memory.  Defaults
+    (128k-ray chunks, 64k first/last, 8 buffers, 4 compute streams) were
+    picked with tools/e2e_probe.py on config-2-shaped rays."""
 
-    NBUF = 4
-
-    def __init__(self, ns: NodeSet, n_max: int, eta_len: int, chunk: int = 1 << 19,
-                 min_chunk: int = 1 << 19):
+    def __init__(self, ns: NodeSet, n_max: int, eta_len: int, chunk: int = 1 << 17,
+                 min_chunk: int = 1 << 16, graphs: bool = True, nbuf: int = 8,
+                 compute_streams: int = 4):
         rec, _ = ns.device_records()
         self.ns, self.dev, self.k = ns, rec.device, int(eta_len)
         self.chunk = max(1, min(int(chunk), int(n_max)))  # device buffers hold one chunk
@@ -396,7 +397,8 @@ class HostRaycaster:
         d = ns.dim
         c = self.chunk
         self.h2d_stream = torch.cuda.Stream(self.dev)
-        self.comp_streams = [torch.cuda.Stream(self.dev), torch.cuda.Stream(self.dev)]
+        self.NBUF = max(int(nbuf), int(compute_streams))
+        self.comp_streams = [torch.cuda.Stream(self.dev) for _ in range(int(compute_streams))]
         self.d2h_stream = torch.cuda.Stream(self.dev)
         self.buf = [dict(x=torch.empty((c, d), dtype=torch.float64, device=self.dev),
                          u=torch.empty((c, d), dtype=torch.float64, device=self.dev),
@@ -408,6 +410,35 @@ class HostRaycaster:
                          h2d=torch.cuda.Event(), done=torch.cuda.Event(), d2h=torch.cuda.Event())
                     for _ in range(self.NBUF)]
         self.ws = [Workspace() for _ in range(self.NBUF)]
+        # One CUDA graph per (buffer, chunk size, mode, screen): the per-chunk
+        # work (ray order, pruned RayCast, exact re-check) replays without the
+        # ~0.5 ms of host-side launch overhead, so small chunks (short
+        # pipeline fill and drain) become affordable.
+        self.use_graphs = bool(graphs)
+        self._graphs = {}
+
+    def _compute(self, bi, m, cs, stats, mode, screen):
+        b = self.buf[bi]
+        args = (self.ns, b["x"][:m], b["u"][:m], b["eta"][:m])
+        kw = dict(out=dict(idx=b["idx"][:m], t=b["t"][:m], rp=b["rp"][:m], flag=b["flag"][:m]),
+                  workspace=self.ws[bi], stream=cs, mode=mode, screen=screen)
+        key = (bi, m, mode, screen)
+        g = self._graphs.get(key) if self.use_graphs else None
+        if g is not None:
+            g.replay()
+            if stats is not None:
+                stats.add(m)
+            return
+        raycast_batch(*args, stats=stats, **kw)  # eager (also the capture warm-up)
+        if self.use_graphs:
+            g = torch.cuda.CUDAGraph()
+            try:
+                with torch.cuda.graph(g, stream=cs):
+                    raycast_batch(*args, **kw)
+            except RuntimeError:  # capture unsupported here: stay eager (same kernels)
+                self.use_graphs = False
+                return
+            self._graphs[key] = g
 
     def schedule(self, n):
         """Chunk bounds: sizes grow geometrically from min_chunk to chunk and
@@ -447,7 +478,7 @@ class HostRaycaster:
             self.ns.screen32(self.dev)
         for ci, (lo, hi) in enumerate(self.schedule(n)):
             b = self.buf[ci % self.NBUF]
-            cs = self.comp_streams[ci & 1]
+            cs = self.comp_streams[ci % len(self.comp_streams)]
             m = hi - lo
             with torch.cuda.stream(self.h2d_stream):
                 if ci >= self.NBUF:
@@ -458,11 +489,7 @@ class HostRaycaster:
                 b["h2d"].record(self.h2d_stream)
             with torch.cuda.stream(cs):
                 cs.wait_event(b["h2d"])
-                raycast_batch(self.ns, b["x"][:m], b["u"][:m], b["eta"][:m],
-                              out=dict(idx=b["idx"][:m], t=b["t"][:m], rp=b["rp"][:m],
-                                       flag=b["flag"][:m]),
-                              workspace=self.ws[ci % self.NBUF], stats=stats, stream=cs,
-                              mode=mode, screen=screen)
+                self._compute(ci % self.NBUF, m, cs, stats, mode, screen)
                 b["done"].record(cs)
             with torch.cuda.stream(self.d2h_stream):
                 self.d2h_stream.wait_event(b["done"])

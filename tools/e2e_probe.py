@@ -33,11 +33,15 @@ for name, src, dst in (("H2D 48MB", hx, dx), ("D2H 48MB", dx, hx)):
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / 5
     print(f"{name}: {dt * 1e3:.2f} ms = {48e6 / dt / 1e9:.1f} GB/s")
+ref_idx = vb.raycast_batch(ns, hx.cuda(), hu.cuda(), hg.cuda()).idx.cpu().numpy()
 hidx, ht = P((n,), torch.int32), P((n,), torch.float64)
 hrp, hfl = P((n, d), torch.float64), P((n,), torch.uint8)
-for chunk, minc in ((1 << 18, 1 << 18), (1 << 19, 1 << 19), (1 << 19, 1 << 16), (1 << 19, 1 << 17),
-                    (1 << 20, 1 << 16), (1 << 18, 1 << 16)):
-    hr = HostRaycaster(ns, n, 1, chunk=chunk, min_chunk=minc)
+for chunk, minc, graphs, nb, cst in ((1 << 19, 1 << 19, False, 4, 2), (1 << 18, 1 << 16, True, 4, 2),
+                                    (1 << 18, 1 << 16, True, 8, 4), (1 << 17, 1 << 15, True, 8, 4),
+                                    (1 << 17, 1 << 16, True, 8, 4), (1 << 17, 1 << 17, True, 8, 4),
+                                    (1 << 16, 1 << 16, True, 16, 8), (1 << 18, 1 << 15, True, 8, 4)):
+    hr = HostRaycaster(ns, n, 1, chunk=chunk, min_chunk=minc, graphs=graphs, nbuf=nb,
+                       compute_streams=cst)
     hr.run(hx, hu, hg, hidx, ht, hrp, hfl)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -48,4 +52,5 @@ for chunk, minc in ((1 << 18, 1 << 18), (1 << 19, 1 << 19), (1 << 19, 1 << 16), 
     hr.run(hx, hu, hg, hidx, ht, hrp, hfl, sync=False)
     te = time.perf_counter() - t0
     torch.cuda.synchronize()
-    print(f"chunk {chunk} min {minc}: {dt * 1e3:.2f} ms  {n / dt:.3e} rays/s  (host enqueue {te * 1e3:.2f} ms)")
+    ok = np.array_equal(hidx.numpy(), ref_idx)
+    print(f"graphs={graphs} bufs={nb} streams={cst} chunk {chunk} min {minc}: {dt * 1e3:.2f} ms  {n / dt:.3e} rays/s  (host enqueue {te * 1e3:.2f} ms) same={ok}")
