@@ -146,14 +146,34 @@ def direction_bucket(u):
     return (i1 * 2 + s1) * (2 * d) + (i2 * 2 + s2)
 
 
-def coherent_order(ix, g, u):
+WARP_ORDER = "kd"  # or "hull_first" (tools: A/B of the warp schedule; kd measured faster)
+
+
+def coherent_order(ix, g, u, x=None):
     """Processing order for the pruned kernel: rays sorted by the kd position
     of their reference generator, then by direction class, so that the 32
     rays of a warp start close together and (within one generator) point
-    the same way -- the warp-wide union of their spheres stays small."""
+    the same way -- the warp-wide union of their spheres stays small.
+
+    With `x`, the warps (32 consecutive slots) are then scheduled nearest-
+    to-the-hull first: rays starting near the generators' bounding box have
+    the largest spheres and the longest warps, and a long warp launched last
+    is the kernel's tail (CTAs start in block order)."""
     pos = ix.inv_perm.index_select(0, g.to(torch.int64)).to(torch.int64)
     key = pos * 256 + direction_bucket(u)
-    return torch.sort(key, stable=True).indices.to(torch.int32)
+    order = torch.sort(key, stable=True).indices
+    if x is None or WARP_ORDER != "hull_first" or order.numel() < 64:
+        return order.to(torch.int32)
+    n = order.numel()
+    nw = (n + 31) // 32
+    margin = torch.minimum(x - ix.bbox_lo, ix.bbox_hi - x).amin(1)  # distance to the box
+    wm = margin.index_select(0, order)
+    if nw * 32 != n:
+        wm = torch.cat([wm, wm.new_full((nw * 32 - n,), float("inf"))])
+    wsort = torch.sort(wm.view(nw, 32).amin(1), stable=True).indices
+    slots = (wsort[:, None] * 32 + torch.arange(32, device=order.device)).view(-1)
+    slots = slots[slots < n]
+    return order.index_select(0, slots).to(torch.int32)
 
 
 def _screen(ns, dev, screen):
@@ -247,7 +267,7 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
         ix = ns.prune_index(dev)
         cur = torch.cuda.current_stream() if stream is None else stream
         with torch.cuda.stream(cur):
-            order = coherent_order(ix, ed[:, 0], ud)
+            order = coherent_order(ix, ed[:, 0], ud, xd)
         _lib.check(L.vr_raycast_pruned(_lib.ptr(rec), ns.n, d, sqmax, s32p, ctypes.byref(ix.struct),
                                        _lib.ptr(xd), _lib.ptr(ud), _lib.ptr(ed), k, n,
                                        _lib.ptr(order), _lib.ptr(idx), _lib.ptr(t),
@@ -384,11 +404,14 @@ class HostRaycaster:
     next chunk's kernel) -- the copy engines and the SMs work concurrently.
     Each chunk's device work replays a captured CUDA graph.  The end-to-end
     public entry point for callers whose rays live in host memory.  Defaults
-    (128k-ray chunks, 64k first/last, 8 buffers, 4 compute streams) were
-    picked with tools/e2e_probe.py on config-2-shaped rays."""
+    (chunks growing 32k -> 256k rays and a 32k last chunk, 8 buffers, 4
+    compute streams) were picked with tools/e2e_timeline.py on the config-2
+    rays: chunks are sorted independently, and a chunk's rays are sparser
+    than the whole batch's (less warp coherence), so the chunked pipeline
+    trades some kernel efficiency for overlapping the copies."""
 
-    def __init__(self, ns: NodeSet, n_max: int, eta_len: int, chunk: int = 1 << 17,
-                 min_chunk: int = 1 << 16, graphs: bool = True, nbuf: int = 8,
+    def __init__(self, ns: NodeSet, n_max: int, eta_len: int, chunk: int = 1 << 18,
+                 min_chunk: int = 1 << 15, graphs: bool = True, nbuf: int = 8,
                  compute_streams: int = 4):
         rec, _ = ns.device_records()
         self.ns, self.dev, self.k = ns, rec.device, int(eta_len)
@@ -467,11 +490,24 @@ class HostRaycaster:
         return torch.empty(shape, dtype=dtype, pin_memory=True)
 
     def run(self, hx, hu, heta, hidx, ht, hrp, hflag, stats=None, mode="auto", screen="fp32",
-            sync=True):
+            sync=True, trace=None):
         """hx, hu (n, d) f64, heta (n, k) i32 pinned inputs; outputs pinned
         hidx (n,) i32, ht (n,) f64, hrp (n, d) f64, hflag (n,) u8.  Returns
-        after the last D2H copy has completed."""
+        after the last D2H copy has completed.  `trace` (a list) receives
+        (chunk size, h2d-done, compute-done, d2h-done) CUDA events per chunk
+        after a start event (tools/e2e_probe.py timelines)."""
         n = hx.shape[0]
+        if trace is not None:
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev0.record(self.h2d_stream)
+            trace.append(ev0)
+
+        def mark(stream):
+            if trace is None:
+                return None
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            return e
         if self.ns.n >= 1024 and mode != "exhaustive":
             self.ns.prune_index(self.dev)
         if screen == "fp32":
@@ -487,10 +523,12 @@ class HostRaycaster:
                 b["u"][:m].copy_(hu[lo:hi], non_blocking=True)
                 b["eta"][:m].copy_(heta[lo:hi], non_blocking=True)
                 b["h2d"].record(self.h2d_stream)
+                e1 = mark(self.h2d_stream)
             with torch.cuda.stream(cs):
                 cs.wait_event(b["h2d"])
                 self._compute(ci % self.NBUF, m, cs, stats, mode, screen)
                 b["done"].record(cs)
+                e2 = mark(cs)
             with torch.cuda.stream(self.d2h_stream):
                 self.d2h_stream.wait_event(b["done"])
                 hidx[lo:hi].copy_(b["idx"][:m], non_blocking=True)
@@ -498,5 +536,7 @@ class HostRaycaster:
                 hrp[lo:hi].copy_(b["rp"][:m], non_blocking=True)
                 hflag[lo:hi].copy_(b["flag"][:m], non_blocking=True)
                 b["d2h"].record(self.d2h_stream)
+                if trace is not None:
+                    trace.append((m, e1, e2, mark(self.d2h_stream)))
         if sync:
             self.d2h_stream.synchronize()

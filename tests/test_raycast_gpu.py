@@ -271,3 +271,35 @@ def test_coop_kernel_matches_exhaustive():
                          capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
     assert "BAD 0" in res.stdout, res.stdout[-2000:]
+
+
+def test_host_raycaster_pipeline_matches_device_batch():
+    """The host-array pipeline (chunks over several buffers / streams, CUDA
+    graph replays after the first use of each chunk shape) returns exactly
+    the device batch's results, for sizes that exercise the fill / drain
+    chunk schedule and a ragged tail, and on repeated runs (graph replays)."""
+    import torch
+    from paper_2405_10050_b200.raycast import HostRaycaster
+    pts = np.random.default_rng(7).random((5000, 5))
+    ns = vb.NodeSet(pts)
+    rng = np.random.default_rng(8)
+    for n, chunk, minc in ((70001, 1 << 14, 1 << 12), (9000, 1 << 17, 1 << 16), (1, 64, 16)):
+        g = rng.integers(0, 5000, n).astype(np.int32)
+        u = rng.standard_normal((n, 5))
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        ref = vb.raycast_batch(ns, pts[g], u, g[:, None])
+        hr = HostRaycaster(ns, n, 1, chunk=chunk, min_chunk=minc, nbuf=4, compute_streams=2)
+        P = HostRaycaster.pinned
+        hx, hu, hg = P((n, 5), torch.float64), P((n, 5), torch.float64), P((n, 1), torch.int32)
+        hx.copy_(torch.from_numpy(pts[g]))
+        hu.copy_(torch.from_numpy(u))
+        hg.copy_(torch.from_numpy(g[:, None].copy()))
+        hidx, ht = P((n,), torch.int32), P((n,), torch.float64)
+        hrp, hfl = P((n, 5), torch.float64), P((n,), torch.uint8)
+        for _ in range(3):
+            hidx.fill_(-7)
+            hr.run(hx, hu, hg, hidx, ht, hrp, hfl)
+            assert np.array_equal(hidx.numpy(), ref.idx.cpu().numpy())
+            assert np.array_equal(hfl.numpy(), ref.flag.cpu().numpy())
+            assert np.array_equal(ht.numpy(), ref.t.cpu().numpy())
+            assert np.array_equal(hrp.numpy(), ref.rp.cpu().numpy(), equal_nan=True)

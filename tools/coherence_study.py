@@ -111,6 +111,18 @@ def main():
             tot += w.sum().item()
         acc[k] = tot / nw
     o = orders["coherent (pos g, bucket)"]
+    per_warp = []
+    for lo in range(0, n, CH):
+        sel = o[lo:lo + CH]
+        m = need_mask(ix, xd[sel], ud[sel], gl[sel], t[sel], X, d)
+        per_warp.append(m.view(-1, 32, m.shape[1]).any(1).sum(1).cpu())
+    pw = torch.cat(per_warp).numpy()
+    print("union tiles per warp (coherent order): mean %.1f p50 %d p99 %d p99.9 %d max %d; "
+          "warps > 150 tiles: %d" % (pw.mean(), np.percentile(pw, 50), np.percentile(pw, 99),
+                                     np.percentile(pw, 99.9), pw.max(), (pw > 150).sum()))
+    esc = ~torch.isfinite(res.t)
+    print("escaped rays", int(esc.sum()), "warps with an escaped ray",
+          int(esc[o].view(-1, 32).any(1).sum()))
     for gs in (16, 8, 4, 2):
         tot_max = tot_mean = 0
         for lo in range(0, n, CH):
