@@ -15,6 +15,7 @@ coordinate / edge / boundary arrays and the reference's dict views
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 from itertools import combinations
 
@@ -163,7 +164,7 @@ class NodeSet:
         return (int(idx[0]), float(d1[0])), float(d2[0])
 
 
-PRUNE_TILE = 64
+PRUNE_TILE = int(os.environ.get("VR_PRUNE_TILE", "64"))  # must match the library (64)
 
 
 class _Screen32Struct(ctypes.Structure):

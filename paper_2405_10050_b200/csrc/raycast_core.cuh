@@ -1014,7 +1014,7 @@ __global__ void __launch_bounds__(32, MINB)
   };
   unsigned long long tiles_done = 0;
   WarpCounters wc;
-  uint32_t phase[2] = {0u, 0u};
+  uint32_t phases = 0u;  // mbarrier parity of buffer b = bit b (a register, not a local array)
   int b = 0;
   int64_t t = cur.next(ray, node_box, node_box32, node_range);
   if (t >= 0) issue(t, 0);
@@ -1022,8 +1022,8 @@ __global__ void __launch_bounds__(32, MINB)
     const int64_t tn = cur.next(ray, node_box, node_box32, node_range);
     __syncwarp();
     if (tn >= 0) issue(tn, b ^ 1);
-    mbar_wait(&bar[b], phase[b]);
-    phase[b] ^= 1u;
+    mbar_wait(&bar[b], (phases >> b) & 1u);
+    phases ^= 1u << b;
     // (no re-test of the tile box here: the leaf was tested when its parent
     // was expanded, and re-testing skipped < 2% of the tiles on config 2)
     ++tiles_done;
@@ -1575,7 +1575,11 @@ struct PrunedIndex {
   WideTree wide;           // 32-ary tree over the tiles (cooperative kernel)
 };
 
+#ifdef VR_PRUNE_TILE_OVERRIDE  // tuning builds only (the Python index must match: VR_PRUNE_TILE)
+constexpr int PRUNE_TILE = VR_PRUNE_TILE_OVERRIDE;
+#else
 constexpr int PRUNE_TILE = 64;
+#endif
 constexpr int PRUNE_BLOCK = 32;
 
 template <int D, int R, int MINB, bool F32, class Src>
@@ -1619,9 +1623,12 @@ int launch_coop(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Fra
   constexpr int NW = 4;
   constexpr int MINB = VR_COOP_MINB;
   const int64_t grid = (n_rays + NW - 1) / NW;
-  k_raycast_coop<D, PRUNE_TILE, NW, MINB, Src><<<(unsigned)grid, NW * 32, 0, st>>>(
-      src, n_rays, ix.crec, ix.crec32, ix.perm, ix.inv_perm, ix.wide, fr, out, work);
-  VR_RETURN_LAUNCH();
+  if constexpr (PRUNE_TILE == 64) {
+    k_raycast_coop<D, PRUNE_TILE, NW, MINB, Src><<<(unsigned)grid, NW * 32, 0, st>>>(
+        src, n_rays, ix.crec, ix.crec32, ix.perm, ix.inv_perm, ix.wide, fr, out, work);
+    VR_RETURN_LAUNCH();
+  }
+  return VR_EINVAL;
 }
 
 int coop_mode();

@@ -120,6 +120,17 @@ def main():
     print("union tiles per warp (coherent order): mean %.1f p50 %d p99 %d p99.9 %d max %d; "
           "warps > 150 tiles: %d" % (pw.mean(), np.percentile(pw, 50), np.percentile(pw, 99),
                                      np.percentile(pw, 99.9), pw.max(), (pw > 150).sum()))
+    # outliers: union without the k rays of largest individual need
+    for kx in (1, 2, 4, 8):
+        tot_u = 0
+        for lo in range(0, n, CH):
+            sel = o[lo:lo + CH]
+            m = need_mask(ix, xd[sel], ud[sel], gl[sel], t[sel], X, d).view(-1, 32, ix.tile_box.shape[0])
+            need = m.sum(2)                                   # (warps, 32)
+            drop = need.topk(kx, dim=1).indices               # (warps, kx)
+            keep = torch.ones_like(need, dtype=torch.bool).scatter_(1, drop, False)
+            tot_u += (m & keep[:, :, None]).any(1).sum().item()
+        print(f"  union without the {kx} largest rays per warp: {tot_u / nw:.1f} tiles")
     esc = ~torch.isfinite(res.t)
     print("escaped rays", int(esc.sum()), "warps with an escaped ray",
           int(esc[o].view(-1, 32).any(1).sum()))
