@@ -893,26 +893,31 @@ template <int D, int R, bool F32>
 struct TreeCursor {
   // Warp-distributed stack: slot i lives in lane i's registers (push = one
   // lane writes, pop = shuffle), so the DFS touches no local memory.  The DFS
-  // holds at most depth + 1 <= 32 entries for trees of < 2^31 tiles.
+  // holds at most depth + 1 <= 32 entries for trees of < 2^31 tiles.  Each
+  // entry keeps the lanes whose rays needed the node when it was pushed
+  // (spheres only shrink, so the mask stays a superset of the later need).
   int s_node = 0, s_lo = 0, s_hi = 0;
+  unsigned s_mask = 0u;
   int sp = 0;
   int64_t st = 0;
   unsigned long long tests = 0;
-  __device__ __forceinline__ bool warp_needs(const RayState<D> (&ray)[R],
-                                             const double* __restrict__ node_box,
-                                             const float* __restrict__ node_box32, int node) {
+  unsigned leaf_mask = 0u;  // lanes needing the leaf returned by next()
+  __device__ __forceinline__ unsigned warp_needs(const RayState<D> (&ray)[R],
+                                                 const double* __restrict__ node_box,
+                                                 const float* __restrict__ node_box32, int node) {
     bool need = false;
 #pragma unroll
     for (int j = 0; j < R; ++j) need |= ray_needs<D, F32>(ray[j], node_box, node_box32, node);
     ++tests;
-    return __any_sync(0xffffffffu, need);
+    return __ballot_sync(0xffffffffu, need);
   }
-  __device__ __forceinline__ void push(int node, int2 rg) {
+  __device__ __forceinline__ void push(int node, int2 rg, unsigned m) {
     if (sp >= 32) __trap();
     if ((int)(threadIdx.x & 31) == sp) {
       s_node = node;
       s_lo = rg.x;
       s_hi = rg.y;
+      s_mask = m;
     }
     ++sp;
   }
@@ -922,7 +927,8 @@ struct TreeCursor {
                                        const int2* __restrict__ node_range) {
     st = start_tile;
     sp = 0;
-    if (warp_needs(ray, node_box, node_box32, 0)) push(0, __ldg(node_range));
+    const unsigned m = warp_needs(ray, node_box, node_box32, 0);
+    if (m) push(0, __ldg(node_range), m);
   }
   // Children are tested when their parent is expanded (both boxes loaded
   // together, one dependent step per level); a popped leaf is returned.
@@ -935,24 +941,118 @@ struct TreeCursor {
       const int node = __shfl_sync(0xffffffffu, s_node, sp);
       const int lo = __shfl_sync(0xffffffffu, s_lo, sp);
       const int hi = __shfl_sync(0xffffffffu, s_hi, sp);
-      if (hi - lo == 1) return lo;
+      if (hi - lo == 1) {
+        leaf_mask = __shfl_sync(0xffffffffu, s_mask, sp);
+        return lo;
+      }
       const int l = 2 * node + 1, r = 2 * node + 2;
       const int2 rl = __ldg(node_range + l), rr = __ldg(node_range + r);
-      const bool nl = warp_needs(ray, node_box, node_box32, l);
-      const bool nr = warp_needs(ray, node_box, node_box32, r);
+      const unsigned nl = warp_needs(ray, node_box, node_box32, l);
+      const unsigned nr = warp_needs(ray, node_box, node_box32, r);
       // the child holding the warp's start tile first (kd index order is
       // spatial order, so this visits the rays' neighbourhood early)
       if (st < rl.y) {
-        if (nr) push(r, rr);
-        if (nl) push(l, rl);
+        if (nr) push(r, rr, nr);
+        if (nl) push(l, rl, nl);
       } else {
-        if (nl) push(l, rl);
-        if (nr) push(r, rr);
+        if (nl) push(l, rl, nl);
+        if (nr) push(r, rr, nr);
       }
     }
     return -1;
   }
 };
+
+// Remapped screening (below) pays off where warp unions are large relative
+// to each ray's need: d >= 7 (config-5 rays: 15.4 -> 10.8 ms per 200k).  At
+// d <= 6 its extra registers cost more than it saves (config 2: 3.58 -> 3.71
+// ms), so it is compiled out there.
+template <int D>
+__host__ __device__ constexpr int remap_max() {
+#ifdef VR_REMAP_MAX
+  return VR_REMAP_MAX;
+#else
+  return D >= 7 ? 16 : 0;
+#endif
+}
+
+// Screening of one tile when only the rays of `mask` (c lanes) need it:
+// G = 32 / 2^ceil(log2 c) lanes share each such ray (its screening state is
+// shuffled in), each lane screens PT / G candidates, the hits are OR-reduced
+// inside the group and handed to the owner lane, which runs the fp64 rare
+// path on them (two 32-candidate blocks, in order).  Same verdicts as
+// screen_tile_pairs for the needing rays; rays not in `mask` do not need any
+// candidate of the tile (the tile box certifies it), so skipping them is exact.
+template <int D, int PT>
+__device__ __forceinline__ void screen_tile_remap(RayState<D>& r, const double* tile64,
+                                                  const float* tilep, int gbase, unsigned mask,
+                                                  const Frame& fr, WarpCounters* wc) {
+  static_assert(PT == 64, "64-bit hit masks");
+  constexpr int P2 = rec32p_stride(D);
+  const int lane = threadIdx.x & 31;
+  const int c = __popc(mask);
+  const int G = c <= 1 ? 32 : c <= 2 ? 16 : c <= 4 ? 8 : c <= 8 ? 4 : 2;
+  const int slot = lane / G, sub = lane % G;
+  const bool valid = slot < c;
+  const int owner = valid ? (int)__fns(mask, 0, slot + 1) : lane;
+  // the owner's screening state
+  float z[D], u[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    z[k] = __shfl_sync(0xffffffffu, r.z32[k], owner);
+    u[k] = __shfl_sync(0xffffffffu, r.u32[k], owner);
+  }
+  const float hi32 = __shfl_sync(0xffffffffu, r.hi32, owner);
+  const float thr32 = __shfl_sync(0xffffffffu, r.thr32, owner);
+  const float bsl32 = __shfl_sync(0xffffffffu, r.bsl32, owner);
+  const int ib = __shfl_sync(0xffffffffu, r.ib, owner);
+  const int npairs = (PT / 2) / G;  // pairs per lane
+  unsigned long long hits = 0ull;
+  if (valid) {
+    for (int p = 0; p < npairs; ++p) {
+      const int pp = sub * npairs + p;  // pair index inside the tile
+      const float4* q = reinterpret_cast<const float4*>(tilep + pp * P2);
+      float v[P2];
+#pragma unroll
+      for (int k = 0; k < P2 / 4; ++k) {
+        const float4 w = q[k];
+        v[4 * k] = w.x;
+        v[4 * k + 1] = w.y;
+        v[4 * k + 2] = w.z;
+        v[4 * k + 3] = w.w;
+      }
+      uint64_t acc = f2pack(v[2 * D], v[2 * D + 1]);
+#pragma unroll
+      for (int k = 0; k < D; ++k) acc = ffma2(f2pack(z[k], z[k]), f2pack(v[2 * k], v[2 * k + 1]), acc);
+      float fa, fb;
+      f2unpack(acc, fa, fb);
+      if (fa < hi32 || fb < hi32) {  // rare: conservative fp32 halfspace pre-filter
+        uint64_t qa2 = f2pack(bsl32, bsl32);
+#pragma unroll
+        for (int k = 0; k < D; ++k) qa2 = ffma2(f2pack(u[k], u[k]), f2pack(v[2 * k], v[2 * k + 1]), qa2);
+        float qa, qb;
+        f2unpack(qa2, qa, qb);
+        const int ia = 2 * pp;
+        if (fa < hi32 && qa > thr32 && gbase + ia != ib) hits |= 1ull << ia;
+        if (fb < hi32 && qb > thr32 && gbase + ia + 1 != ib) hits |= 1ull << (ia + 1);
+      }
+    }
+  }
+  if (!__any_sync(0xffffffffu, hits != 0ull)) return;
+  // OR inside each group of G lanes (aligned, contiguous), then to the owner
+  for (int off = 1; off < G; off <<= 1) hits |= __shfl_xor_sync(0xffffffffu, hits, off);
+  const bool mine = (mask >> lane) & 1u;
+  const int my_slot = __popc(mask & ((1u << lane) - 1u));
+  const unsigned long long h = __shfl_sync(0xffffffffu, hits, (mine ? my_slot : 0) * G);
+  if (!mine || !h) return;
+  if (wc) {
+    ++wc->rare_blocks;
+    wc->entries += __popcll(h);
+  }
+  const unsigned lo = (unsigned)h, hi = (unsigned)(h >> 32);
+  if (lo) ray_rare_block<D, true>(r, tile64, lo, gbase, fr);
+  if (hi) ray_rare_block<D, true>(r, tile64 + 32 * rec_stride(D), hi, gbase + 32, fr);
+}
 
 // One warp per CTA (warps finish at very different times; a freed slot is
 // refilled immediately).  The warp's next needed tile is fetched by TMA into
@@ -1017,9 +1117,11 @@ __global__ void __launch_bounds__(32, MINB)
   uint32_t phases = 0u;  // mbarrier parity of buffer b = bit b (a register, not a local array)
   int b = 0;
   int64_t t = cur.next(ray, node_box, node_box32, node_range);
+  unsigned tmask = cur.leaf_mask;
   if (t >= 0) issue(t, 0);
   while (t >= 0) {
     const int64_t tn = cur.next(ray, node_box, node_box32, node_range);
+    const unsigned tn_mask = cur.leaf_mask;
     __syncwarp();
     if (tn >= 0) issue(tn, b ^ 1);
     mbar_wait(&bar[b], (phases >> b) & 1u);
@@ -1027,7 +1129,14 @@ __global__ void __launch_bounds__(32, MINB)
     // (no re-test of the tile box here: the leaf was tested when its parent
     // was expanded, and re-testing skipped < 2% of the tiles on config 2)
     ++tiles_done;
-    if constexpr (F32)
+    if constexpr (F32 && R == 1 && PT == 64 && remap_max<D>() > 0) {
+      if (__popc(tmask) <= remap_max<D>())
+        screen_tile_remap<D, PT>(ray[0], STAGE64 ? buf[b] : crec + t * PT * S, buf32[b],
+                                 (int)(t * PT), tmask, fr, work ? &wc : nullptr);
+      else
+        screen_tile_pairs<D, R, PT>(ray, STAGE64 ? buf[b] : crec + t * PT * S, buf32[b],
+                                    (int)(t * PT), fr, work ? &wc : nullptr);
+    } else if constexpr (F32)
       screen_tile_pairs<D, R, PT>(ray, STAGE64 ? buf[b] : crec + t * PT * S, buf32[b],
                                   (int)(t * PT), fr, work ? &wc : nullptr);
     else
@@ -1035,6 +1144,7 @@ __global__ void __launch_bounds__(32, MINB)
     __syncwarp();
     b ^= 1;
     t = tn;
+    tmask = tn_mask;
   }
 #pragma unroll
   for (int j = 0; j < R; ++j)
