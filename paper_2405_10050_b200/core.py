@@ -465,6 +465,7 @@ class Mesh:
         self._edge_counts = edge_counts
         self._boundary = boundary
         self._arr = None
+        self._dev = None
         self._cell_csr = None
         self._neighbors = {}
         self._unbounded = None
@@ -482,9 +483,50 @@ class Mesh:
                       boundary_u=np.ascontiguousarray(boundary_u, dtype=np.float64))
         return m
 
+    @classmethod
+    def from_device(cls, nodes, sigma, r, edge_key, edge_count, boundary_sigma, boundary_u):
+        """Mesh over device tensors (traversal output), kept resident in HBM:
+        the host arrays (and the lexicographic edge order) are produced on
+        first access, so a traversal whose result is consumed on the device
+        (or only counted) never pays for the device -> host copy."""
+        m = cls(nodes)
+        m._dev = dict(sigma=sigma, r=r, edge_key=edge_key, edge_count=edge_count,
+                      boundary_sigma=boundary_sigma, boundary_u=boundary_u)
+        return m
+
+    def device_arrays(self):
+        """The device tensors of a traversal mesh (edges in hash order), or None."""
+        return self._dev
+
+    def _materialize(self):
+        import torch
+        dv = self._dev
+        ek, ec = dv["edge_key"], dv["edge_count"]
+        if ek.shape[0]:
+            order = torch.arange(ek.shape[0], device=ek.device)
+            for c in range(ek.shape[1] - 1, -1, -1):  # stable LSD lexicographic sort
+                _, o = torch.sort(ek[:, c].index_select(0, order), stable=True)
+                order = order.index_select(0, o)
+            ek, ec = ek.index_select(0, order), ec.index_select(0, order)
+
+        def host(t, dtype):
+            t = t.contiguous()
+            if t.is_cuda and t.numel():
+                buf = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                buf.copy_(t)
+                t = buf
+            return np.ascontiguousarray(t.cpu().numpy(), dtype=dtype)
+
+        self._arr = dict(sigma=host(dv["sigma"], np.int32), r=host(dv["r"], np.float64),
+                         edge_key=host(ek, np.int32), edge_count=host(ec, np.int32),
+                         boundary_sigma=host(dv["boundary_sigma"], np.int32),
+                         boundary_u=host(dv["boundary_u"], np.float64))
+
     def arrays(self):
         """sigma (V, d+1) int32, r (V, d), edge_key (E, d), edge_count (E,),
         boundary_sigma (B, d+1), boundary_u (B, d)."""
+        if self._arr is None and self._dev is not None:
+            self._materialize()
         if self._arr is None:
             d = self.nodes.dim
             verts = list(self._vertices.values()) if self._vertices else []
@@ -503,6 +545,8 @@ class Mesh:
 
     @property
     def n_vertices(self):
+        if self._arr is None and self._dev is not None:
+            return int(self._dev["sigma"].shape[0])
         return self.arrays()["sigma"].shape[0]
 
     @property
@@ -517,6 +561,7 @@ class Mesh:
     def vertices(self, value):
         self._vertices = value
         self._arr = None
+        self._dev = None
 
     @property
     def edge_counts(self):

@@ -501,7 +501,7 @@ class DeviceTraversal:
         return n_new
 
     def edges(self):
-        """Published edge keys (sorted lexicographically) and counts."""
+        """Published edge keys and counts (device tensors, hash-table order)."""
         flag = torch.empty(self.ecap, dtype=torch.int32, device=self.dev)
         _lib.check(self.L.vr_trav_published(_lib.ptr(self.estate), self.ecap, _lib.ptr(flag),
                                             self._sh()), "published")
@@ -513,11 +513,7 @@ class DeviceTraversal:
         _lib.check(self.L.vr_trav_edge_compact(ctypes.byref(T), self.d, _lib.ptr(off),
                                                _lib.ptr(keys), _lib.ptr(cnt), self._sh()),
                    "edge_compact")
-        order = torch.arange(ne, device=self.dev)
-        for c in range(self.d - 1, -1, -1):  # stable LSD lexicographic sort
-            _, o = torch.sort(keys[order, c], stable=True)
-            order = order[o]
-        return keys[order], cnt[order]
+        return keys, cnt  # hash order; Mesh sorts lexicographically on materialisation
 
 
 def _level_raycaster(ns, stats, group):
@@ -561,9 +557,8 @@ def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heurist
         levels.append((f1 - f0, n_new))
         f0, f1, lvl = f1, f1 + n_new, lvl + 1
     ek, ec = tr.edges()
-    mesh = Mesh.from_arrays(ns, tr.vsig[:tr.nv].cpu().numpy(), tr.vr[:tr.nv].cpu().numpy(),
-                            ek.cpu().numpy(), ec.cpu().numpy(), tr.bsig[:tr.nb].cpu().numpy(),
-                            tr.bu[:tr.nb].cpu().numpy())
+    mesh = Mesh.from_device(ns, tr.vsig[:tr.nv], tr.vr[:tr.nv], ek, ec, tr.bsig[:tr.nb],
+                            tr.bu[:tr.nb])
     if return_info:
         return mesh, {"levels": levels, "vertices": tr.nv, "boundary": tr.nb}
     return mesh
@@ -599,9 +594,8 @@ def voronoi_local(ns: NodeSet, starts, hops: int, seed: int = 0, stats: RaycastS
         f0, f1 = f1, f1 + n_new
         bounds.append((f0, f1))
     ek, ec = tr.edges()
-    mesh = Mesh.from_arrays(ns, tr.vsig[:tr.nv].cpu().numpy(), tr.vr[:tr.nv].cpu().numpy(),
-                            ek.cpu().numpy(), ec.cpu().numpy(), tr.bsig[:tr.nb].cpu().numpy(),
-                            tr.bu[:tr.nb].cpu().numpy())
+    mesh = Mesh.from_device(ns, tr.vsig[:tr.nv], tr.vr[:tr.nv], ek, ec, tr.bsig[:tr.nb],
+                            tr.bu[:tr.nb])
     if return_levels:
         lv = np.zeros(tr.nv, dtype=np.int8)
         for h, (a, b) in enumerate(bounds):
