@@ -178,6 +178,15 @@ int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
                       double* out_rp, uint8_t* out_flag, int32_t* recheck_list,
                       int32_t* recheck_count, uint64_t* work, void* stream);
 
+/* Processing-order keys for the pruned kernels: keys[k] = base * 256 + the
+ * direction class of u[k] (signed index of the largest and second-largest
+ * |u_j|), base = inv_perm[eta[k * eta_len]] (kd position of the reference
+ * generator) or, with eta == NULL, k / rays_per_cell (MC).  Sorting the keys
+ * (stable) gives the `order` argument of vr_raycast_pruned / vr_mc_rays_pruned. */
+int vr_ray_keys(const int32_t* inv_perm, const int32_t* eta, int eta_len,
+                int64_t rays_per_cell, const double* u, int64_t n, int d, int64_t* keys,
+                void* stream);
+
 /* Exact re-evaluation of the rays listed in recheck_list[0 .. *count)
  * (count read on device): centred t for every candidate, argmin with the
  * smallest-index tie-break, then the reference's runner-up degeneracy band

@@ -48,6 +48,7 @@ _SIGNATURES = {
                           _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_pack_records32": [_vp, _i64, _int, _vp, _vp, _vp],
     "vr_pack_records32_pairs": [_vp, _i64, _int, _vp, _vp],
+    "vr_ray_keys": [_vp, _vp, _int, _i64, _vp, _i64, _int, _vp, _vp],
     "vr_mc_integrate": [_vp, _int, _vp, _i64, _i64, _vp, _u64, _vp, _vp, _vp, _int, _dbl, _int,
                         _vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_mc_uniforms": [_i64, _vp, _i64, _int, _u64, _vp, _vp],

@@ -372,8 +372,6 @@ class PruneIndex:
         self.rec = crec
         self.n = n
         self.rows = rows
-        self.bbox_lo = pts.amin(0).contiguous()  # generator bounding box (ray scheduling)
-        self.bbox_hi = pts.amax(0).contiguous()
         self.screen32 = Screen32(crec, n, d, center=center)
         # the pruned kernel reads the fp32 rows pair-interleaved (packed FFMA2)
         p2 = (2 * d + 5) & ~3

@@ -30,7 +30,7 @@ from . import _lib
 from .core import NodeSet
 from .errors import DegenerateConfiguration, UnboundedRay
 from .raycast import (RaycastStats, Workspace, _screen, _use_pruned, candidate_records,
-                      direction_bucket)
+                      ray_keys)
 
 Integrand = Callable[[np.ndarray], float]
 
@@ -132,8 +132,7 @@ def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_fa
                 dd = ws.get("mc_dirs", (total, d), torch.float64, dev)
                 _lib.check(L.vr_mc_directions(d, nc, _lib.ptr(cells_d), n, seed, _lib.ptr(dd), sh),
                            "vr_mc_directions")
-            key = torch.arange(total, device=dev, dtype=torch.int64).div_(n, rounding_mode="floor")
-            key.mul_(256).add_(direction_bucket(dd.view(total, d)))
+            key = ray_keys(dd.view(total, d), rays_per_cell=n)
             order = torch.sort(key, stable=True).indices.to(torch.int32)
             del key
         _lib.check(L.vr_mc_rays_pruned(_lib.ptr(rec), ns.n, d, sqmax, s32p, ctypes.byref(ix.struct),

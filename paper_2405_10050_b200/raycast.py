@@ -146,34 +146,34 @@ def direction_bucket(u):
     return (i1 * 2 + s1) * (2 * d) + (i2 * 2 + s2)
 
 
-WARP_ORDER = "kd"  # or "hull_first" (tools: A/B of the warp schedule; kd measured faster)
+def ray_keys(u, eta=None, inv_perm=None, rays_per_cell=1):
+    """Processing-order keys on the device (vr_ray_keys): base * 256 +
+    direction_bucket(u), base = inv_perm[eta[:, 0]] or, without eta,
+    k // rays_per_cell."""
+    n, d = u.shape
+    keys = torch.empty(n, dtype=torch.int64, device=u.device)
+    L = _lib.lib()
+    if eta is not None:
+        eta = eta.view(n, -1)
+        _lib.check(L.vr_ray_keys(_lib.ptr(inv_perm), _lib.ptr(eta), eta.shape[1], 1,
+                                 _lib.ptr(u), n, d, _lib.ptr(keys), _lib.stream_handle()),
+                   "vr_ray_keys")
+    else:
+        _lib.check(L.vr_ray_keys(None, None, 0, int(rays_per_cell), _lib.ptr(u), n, d,
+                                 _lib.ptr(keys), _lib.stream_handle()), "vr_ray_keys")
+    return keys
 
 
-def coherent_order(ix, g, u, x=None):
+def coherent_order(ix, eta, u):
     """Processing order for the pruned kernel: rays sorted by the kd position
-    of their reference generator, then by direction class, so that the 32
-    rays of a warp start close together and (within one generator) point
-    the same way -- the warp-wide union of their spheres stays small.
-
-    With `x`, the warps (32 consecutive slots) are then scheduled nearest-
-    to-the-hull first: rays starting near the generators' bounding box have
-    the largest spheres and the longest warps, and a long warp launched last
-    is the kernel's tail (CTAs start in block order)."""
-    pos = ix.inv_perm.index_select(0, g.to(torch.int64)).to(torch.int64)
-    key = pos * 256 + direction_bucket(u)
-    order = torch.sort(key, stable=True).indices
-    if x is None or WARP_ORDER != "hull_first" or order.numel() < 64:
-        return order.to(torch.int32)
-    n = order.numel()
-    nw = (n + 31) // 32
-    margin = torch.minimum(x - ix.bbox_lo, ix.bbox_hi - x).amin(1)  # distance to the box
-    wm = margin.index_select(0, order)
-    if nw * 32 != n:
-        wm = torch.cat([wm, wm.new_full((nw * 32 - n,), float("inf"))])
-    wsort = torch.sort(wm.view(nw, 32).amin(1), stable=True).indices
-    slots = (wsort[:, None] * 32 + torch.arange(32, device=order.device)).view(-1)
-    slots = slots[slots < n]
-    return order.index_select(0, slots).to(torch.int32)
+    of their reference generator (eta[:, 0]), then by direction class, so
+    that the 32 rays of a warp start close together and (within one
+    generator) point the same way -- the warp-wide union of their spheres
+    stays small.  (Scheduling the longest, near-hull warps first was
+    measured slower: it breaks the locality of consecutive warps.)"""
+    eta = eta.to(torch.int32).contiguous()
+    keys = ray_keys(u.contiguous(), eta, ix.inv_perm)
+    return torch.sort(keys, stable=True).indices.to(torch.int32)
 
 
 def _screen(ns, dev, screen):
@@ -267,7 +267,7 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
         ix = ns.prune_index(dev)
         cur = torch.cuda.current_stream() if stream is None else stream
         with torch.cuda.stream(cur):
-            order = coherent_order(ix, ed[:, 0], ud, xd)
+            order = coherent_order(ix, ed, ud)
         _lib.check(L.vr_raycast_pruned(_lib.ptr(rec), ns.n, d, sqmax, s32p, ctypes.byref(ix.struct),
                                        _lib.ptr(xd), _lib.ptr(ud), _lib.ptr(ed), k, n,
                                        _lib.ptr(order), _lib.ptr(idx), _lib.ptr(t),

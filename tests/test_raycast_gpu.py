@@ -303,3 +303,22 @@ def test_host_raycaster_pipeline_matches_device_batch():
             assert np.array_equal(hfl.numpy(), ref.flag.cpu().numpy())
             assert np.array_equal(ht.numpy(), ref.t.cpu().numpy())
             assert np.array_equal(hrp.numpy(), ref.rp.cpu().numpy(), equal_nan=True)
+
+
+def test_ray_keys_match_torch_restatement():
+    """vr_ray_keys (processing-order keys) equals the torch formula
+    inv_perm[eta0] * 256 + direction_bucket(u), and the MC form k // per."""
+    import torch
+    from paper_2405_10050_b200.raycast import direction_bucket, ray_keys
+    pts = np.random.default_rng(11).random((3000, 7))
+    ns = vb.NodeSet(pts)
+    ix = ns.prune_index()
+    rng = np.random.default_rng(12)
+    u = torch.from_numpy(rng.standard_normal((5000, 7))).cuda()
+    u[:10, 3] = 0.0  # ties in |u| handled like argmax (first index)
+    u[10:20] = 1.0
+    eta = torch.from_numpy(rng.integers(0, 3000, (5000, 3)).astype(np.int32)).cuda()
+    want = ix.inv_perm.index_select(0, eta[:, 0].long()).long() * 256 + direction_bucket(u)
+    assert torch.equal(ray_keys(u, eta, ix.inv_perm), want)
+    want_mc = torch.arange(5000, device="cuda") // 7 * 256 + direction_bucket(u)
+    assert torch.equal(ray_keys(u, rays_per_cell=7), want_mc)

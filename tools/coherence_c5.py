@@ -26,7 +26,7 @@ def main():
     ix = ns.prune_index()
     X = torch.from_numpy(pts).to(dev)
     g = ed[:, 0].to(torch.int64)
-    o = coherent_order(ix, ed[:, 0], ud).to(torch.int64)
+    o = coherent_order(ix, ed, ud).to(torch.int64)
     n = (xd.shape[0] // 32) * 32
     CH = 1024
     tot = {gs: 0.0 for gs in (32, 16, 8, 4, 1)}

@@ -80,7 +80,7 @@ def main():
 
     orders = {
         "input order": torch.arange(n, device=dev),
-        "coherent (pos g, bucket)": coherent_order(ix, gd, ud).to(torch.int64),
+        "coherent (pos g, bucket)": coherent_order(ix, gd[:, None], ud).to(torch.int64),
         "pos g only": torch.sort(pos[gl], stable=True).indices,
         "vertex id (p), bucket": torch.sort(torch.from_numpy(p).to(dev) * 256 + bucket, stable=True).indices,
         "pos seed hit": torch.sort(pos[sb] * 1_000_000 + pos[gl], stable=True).indices,

@@ -65,9 +65,6 @@ def edge_rays(ns, pts, seeds):
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["c2gen", "c2vert", "c5gen", "c4mc"]
-    if os.environ.get("WARP_ORDER"):
-        import paper_2405_10050_b200.raycast as _rc
-        _rc.WARP_ORDER = os.environ["WARP_ORDER"]
     if os.environ.get("MODES"):
         run.__defaults__ = (tuple(os.environ["MODES"].split(",")),)
     if "c2gen" in which or "c2vert" in which:
