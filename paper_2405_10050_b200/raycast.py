@@ -173,6 +173,8 @@ def coherent_order(ix, eta, u):
     measured slower: it breaks the locality of consecutive warps.)"""
     eta = eta.to(torch.int32).contiguous()
     keys = ray_keys(u.contiguous(), eta, ix.inv_perm)
+    if ix.n < (1 << 23):  # keys < 2^31: a 32-bit radix sort (half the passes)
+        keys = keys.to(torch.int32)
     return torch.sort(keys, stable=True).indices.to(torch.int32)
 
 
