@@ -1065,7 +1065,8 @@ __global__ void __launch_bounds__(32, MINB)
                      int64_t n_cand, const double* __restrict__ tile_box,
                      const float* __restrict__ tile_box32, const double* __restrict__ node_box,
                      const float* __restrict__ node_box32, const int2* __restrict__ node_range,
-                     Frame fr, RayOut out, unsigned long long* __restrict__ work) {
+                     Frame fr, RayOut out, unsigned long long* __restrict__ work,
+                     unsigned long long* __restrict__ next_item) {
   constexpr int S = rec_stride(D);
   // both copies are staged: the fp64 rows feed the rare path, which is hit
   // often enough (tens of entries per ray at d=8) that global loads stall
@@ -1082,7 +1083,21 @@ __global__ void __launch_bounds__(32, MINB)
   __shared__ __align__(128) float buf32[2][F32 ? PT / 2 * P2 : 4];
   __shared__ uint64_t bar[2];
   const int lane = threadIdx.x;
-  const int64_t k0 = (int64_t)blockIdx.x * 32 * R + lane;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  uint32_t phases = 0u;  // mbarrier parity of buffer b = bit b (a register, not a local array)
+  // Work items = groups of 32 R consecutive slots of the processing order.
+  // Without a counter one item per CTA; with one (persistent launch: about
+  // one CTA per resident warp slot) items are handed out in order by an
+  // atomic counter, so no SM idles between CTAs and the tail balances.
+  const int64_t n_items = (src.n + 32 * R - 1) / (32 * R);
+  int64_t item = blockIdx.x;
+  while (item < n_items) {
+  const int64_t k0 = item * 32 * R + lane;
 
   RayState<D> ray[R];
   bool act[R];
@@ -1091,12 +1106,6 @@ __global__ void __launch_bounds__(32, MINB)
     act[j] = src.load(k0 + (int64_t)j * 32, ray[j], fr);
     if (!act[j]) init_padding_lane<D, R>(ray[j]);
   }
-  if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
   int64_t st = 0;
   if (lane == 0) st = inv_perm[src.gen(k0)] / PT;
   st = __shfl_sync(0xffffffffu, st, 0);
@@ -1114,7 +1123,6 @@ __global__ void __launch_bounds__(32, MINB)
   };
   unsigned long long tiles_done = 0;
   WarpCounters wc;
-  uint32_t phases = 0u;  // mbarrier parity of buffer b = bit b (a register, not a local array)
   int b = 0;
   int64_t t = cur.next(ray, node_box, node_box32, node_range);
   unsigned tmask = cur.leaf_mask;
@@ -1182,6 +1190,12 @@ __global__ void __launch_bounds__(32, MINB)
       if (lane == 0) atomicAdd(work + 6 + q, v);
     }
 #endif
+  }
+  if (!next_item) break;
+  __syncwarp();  // every lane is done with the shared buffers of this item
+  unsigned long long nx = 0;
+  if (lane == 0) nx = atomicAdd(next_item, 1ull);
+  item = (int64_t)gridDim.x + (int64_t)__shfl_sync(0xffffffffu, nx, 0);
   }
 }
 
@@ -1696,11 +1710,32 @@ template <int D, int R, int MINB, bool F32, class Src>
 int launch_pruned_rm(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
                      const RayOut& out, cudaStream_t st, unsigned long long* work) {
   const int64_t per_block = 32 * R;
-  const int64_t grid = (n_rays + per_block - 1) / per_block;
-  k_raycast_pruned<D, R, PRUNE_TILE, PRUNE_BLOCK, MINB, F32, Src><<<(unsigned)grid, 32, 0, st>>>(
-      src, ix.crec, ix.crec32, ix.perm, ix.inv_perm, ix.n, ix.tile_box, ix.tile_box32,
-      ix.node_box, ix.node_box32, ix.node_range, fr, out, work);
-  VR_RETURN_LAUNCH();
+  const int64_t items = (n_rays + per_block - 1) / per_block;
+  auto kern = k_raycast_pruned<D, R, PRUNE_TILE, PRUNE_BLOCK, MINB, F32, Src>;
+  unsigned long long* next_item = nullptr;
+  int64_t grid = items;
+#ifdef VR_PERSISTENT
+  static int slots = 0;  // resident CTAs on the whole GPU (one warp each)
+  if (!slots) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, 0);
+    slots = sms * per_sm;
+  }
+  if (items > slots) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&next_item), sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(next_item, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return vr_cuda_status(e);
+    grid = slots;
+  }
+#endif
+  kern<<<(unsigned)grid, 32, 0, st>>>(src, ix.crec, ix.crec32, ix.perm, ix.inv_perm, ix.n,
+                                      ix.tile_box, ix.tile_box32, ix.node_box, ix.node_box32,
+                                      ix.node_range, fr, out, work, next_item);
+  cudaError_t le = cudaGetLastError();
+  if (next_item) cudaFreeAsync(next_item, st);
+  return vr_cuda_status(le);
 }
 
 int raycast_variant();
