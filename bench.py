@@ -222,6 +222,7 @@ def extra_configs(vb, torch, world, rank):
     pts3 = np.random.default_rng(0).standard_normal((10000, 5))
     ns3 = vb.build_node_set(pts3)
     ns3.prune_index()
+    vb.voronoi_graph(ns3, seed=0)  # warm (table allocation, lazy module loading)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     m3, info3 = vb.voronoi_graph(ns3, seed=0, return_info=True)
