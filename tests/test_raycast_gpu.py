@@ -322,3 +322,47 @@ def test_ray_keys_match_torch_restatement():
     assert torch.equal(ray_keys(u, eta, ix.inv_perm), want)
     want_mc = torch.arange(5000, device="cuda") // 7 * 256 + direction_bucket(u)
     assert torch.equal(ray_keys(u, rays_per_cell=7), want_mc)
+
+
+def test_config2_full_size_properties():
+    """BASELINE config 2 at full size (1e6 rays, N=20,000, d=6), through
+    size-independent properties: (1) the pruned and exhaustive kernels agree
+    bitwise on every ray (index, t, flag); (2) every hit point rp lies on the
+    boundary between g and the hit generator with no generator strictly
+    closer (nearest distance == |rp - x_g| == |rp - x_i| within the 1e-9
+    coordinate tolerance -- the incircle property, checked against all N);
+    (3) escaped rays have no generator in their forward halfspace."""
+    import torch
+    import bench
+    pts = bench.generators()
+    ns = vb.NodeSet(pts)
+    s, p, u = bench.ray_recipe(10 ** 6)
+    need = np.unique(p)
+    sig_n, r_n = vb.descent_batch(ns, s[need], seed=0)
+    pool_sig = np.zeros((bench.N_POOL, bench.DIM + 1), dtype=np.int32)
+    pool_r = np.zeros((bench.N_POOL, bench.DIM))
+    pool_sig[need], pool_r[need] = sig_n, r_n
+    x, u, g = bench.assemble(pts, pool_sig, pool_r, p, u)
+    xd, ud, gd = (torch.from_numpy(a).cuda() for a in (x, u, g))
+    a = vb.raycast_batch(ns, xd, ud, gd, mode="pruned")
+    b = vb.raycast_batch(ns, xd, ud, gd, mode="exhaustive")
+    assert torch.equal(a.idx, b.idx) and torch.equal(a.flag, b.flag) and torch.equal(a.t, b.t)
+    flag = a.flag.cpu().numpy()
+    assert not (flag == 3).any() and not (flag == 2).any()
+    ok = np.nonzero(flag == 0)[0]
+    X = torch.from_numpy(pts).cuda()
+    rp = a.rp[ok]
+    rho = torch.linalg.norm(rp - X[gd[ok, 0].long()], dim=1)
+    rho_i = torch.linalg.norm(rp - X[a.idx[ok].long()], dim=1)
+    tol = 1e-9 * torch.clamp(rho, min=1.0)
+    assert bool(((rho_i - rho).abs() <= tol).all())
+    sample = ok[np.random.default_rng(0).choice(len(ok), 50000, replace=False)]
+    _, d1, _ = ns._nearest_dev(a.rp[sample].cpu().numpy(), None)
+    rs = torch.linalg.norm(a.rp[sample] - X[gd[sample, 0].long()], dim=1).cpu().numpy()
+    assert np.all(np.abs(d1 - rs) <= 1e-9 * np.maximum(1.0, rs))
+    esc = np.nonzero(flag == 1)[0]
+    assert 0 < len(esc) < 2000
+    ue = ud[esc]
+    thr = (ue * X[gd[esc, 0].long()]).sum(1)
+    thr = thr + 1e-12 * torch.clamp(thr.abs(), min=1.0)
+    assert bool(((X @ ue.T).max(0).values <= thr).all())
