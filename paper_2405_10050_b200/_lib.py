@@ -124,3 +124,16 @@ def ptr(t):
 def stream_handle(stream=None):
     s = torch.cuda.current_stream() if stream is None else stream
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def to_host(t):
+    """Device tensor -> numpy through a pinned staging buffer (pageable
+    .cpu() copies of large arrays run several times slower)."""
+    import torch
+    t = t.contiguous()
+    if t.is_cuda and t.numel() > (1 << 16):
+        buf = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        buf.copy_(t)
+        return buf.numpy()
+    return t.cpu().numpy()
+

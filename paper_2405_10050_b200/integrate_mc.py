@@ -167,17 +167,18 @@ def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_fa
 
 
 def _collect(cells, out, want_samples):
-    vol = out["volume"].cpu().numpy()
-    nf = out["nfaces"].cpu().numpy()
-    fj = out["face_j"].cpu().numpy()
-    fa = out["face_area"].cpu().numpy()
+    """Compact the per-cell face tables on the device (cells x max_faces ->
+    the faces actually hit, CSR order) before the host copy."""
+    nf_d = out["nfaces"]
+    fj_d, fa_d = out["face_j"], out["face_area"]
+    mask = torch.arange(fj_d.shape[1], device=fj_d.device)[None, :] < nf_d[:, None]
+    nf = _lib.to_host(nf_d)
     off = np.zeros(len(nf) + 1, dtype=np.int64)
     np.cumsum(nf, out=off[1:])
-    mask = np.arange(fj.shape[1])[None, :] < nf[:, None]
-    return MCResult(cells=np.asarray(cells), volume=vol, face_offsets=off, face_j=fj[mask],
-                    face_area=fa[mask], status=out["status"].cpu().numpy(),
-                    first_bad=out["first_bad"].cpu().numpy(),
-                    samples=out["samples"].cpu().numpy() if want_samples else None)
+    return MCResult(cells=np.asarray(cells), volume=_lib.to_host(out["volume"]), face_offsets=off,
+                    face_j=_lib.to_host(fj_d[mask]), face_area=_lib.to_host(fa_d[mask]),
+                    status=_lib.to_host(out["status"]), first_bad=_lib.to_host(out["first_bad"]),
+                    samples=_lib.to_host(out["samples"]) if want_samples else None)
 
 
 def mc_cells(ns: NodeSet, cells, n: int, seed: int = 0, max_faces: int = 256,
