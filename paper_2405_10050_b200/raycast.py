@@ -98,8 +98,8 @@ class RaycastBatch:
         self.idx, self.t, self.rp, self.flag = idx, t, rp, flag
 
     def to_host(self):
-        return (self.idx.cpu().numpy(), self.t.cpu().numpy(),
-                None if self.rp is None else self.rp.cpu().numpy(), self.flag.cpu().numpy())
+        h = _lib.to_host
+        return (h(self.idx), h(self.t), None if self.rp is None else h(self.rp), h(self.flag))
 
 
 class Workspace:
