@@ -8,6 +8,10 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2405_10050_b200 as vb  # noqa: E402
+import paper_2405_10050_b200.raycast as _rc  # noqa: E402
+
+if os.environ.get("PRUNE_MIN"):
+    _rc.PRUNE_MIN_GENERATORS = int(os.environ["PRUNE_MIN"])
 
 for name, pts in (("config1", np.random.default_rng(0).random((1000, 3))),
                   ("config3", np.random.default_rng(0).standard_normal((10000, 5)))):
