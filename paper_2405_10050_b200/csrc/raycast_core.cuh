@@ -541,6 +541,25 @@ __device__ __forceinline__ void screen_tile(RayState<D> (&ray)[R], const double*
 #pragma unroll
     for (int j = 0; j < R; ++j) any |= m[j];
     if (__any_sync(0xffffffffu, any != 0u)) {
+      if constexpr (F32) {
+        // conservative fp32 halfspace pre-filter + the current best itself
+        // (most screen hits of a stale sphere lie behind the ray)
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          unsigned mm = m[j], h = 0u;
+          while (mm) {
+            const int u = __ffs(mm) - 1;
+            mm &= mm - 1;
+            float xi[D];
+            load_rec32<D>(tile32 + (c + u) * S32, xi);
+            float q = ray[j].bsl32;
+#pragma unroll
+            for (int k = 0; k < D; ++k) q = fmaf(ray[j].u32[k], xi[k], q);
+            if (q > ray[j].thr32 && gbase + c + u != ray[j].ib) h |= 1u << u;
+          }
+          m[j] = h;
+        }
+      }
       if (wc) {
         ++wc->rare_blocks;
 #pragma unroll
