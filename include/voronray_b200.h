@@ -51,7 +51,7 @@ enum vr_cell_status {
   VR_CELL_OVERFLOW = 3     /* more distinct hit faces than area slots          */
 };
 
-int vr_abi_version(void); /* 2 */
+int vr_abi_version(void); /* 3 */
 const char* vr_status_string(int status);
 
 /* Record stride (doubles) of one packed generator for dimension d:
@@ -84,6 +84,9 @@ typedef struct vr_screen32 {
   double center[8];
   double sqmax;
   double bound;   /* max_k |x_k - center_k| over the generators */
+  const float* rec_pairs; /* optional: the same rows pair-interleaved
+                             (vr_pack_records32_pairs); enables the packed
+                             FFMA2 screen of vr_raycast_batch / vr_mc_rays */
 } vr_screen32;
 
 int vr_record32_stride(int d);

@@ -169,7 +169,8 @@ PRUNE_TILE = int(os.environ.get("VR_PRUNE_TILE", "64"))  # must match the librar
 
 class _Screen32Struct(ctypes.Structure):
     _fields_ = [("rec", ctypes.c_void_p), ("center", ctypes.c_double * 8),
-                ("sqmax", ctypes.c_double), ("bound", ctypes.c_double)]
+                ("sqmax", ctypes.c_double), ("bound", ctypes.c_double),
+                ("rec_pairs", ctypes.c_void_p)]
 
 
 class Screen32:
@@ -189,10 +190,14 @@ class Screen32:
         _lib.check(L.vr_pack_records32(_lib.ptr(rec), rec.shape[0], d, _lib.ptr(self.center),
                                        _lib.ptr(self.rec), _lib.stream_handle()),
                    "vr_pack_records32")
+        rows = rec.shape[0]
+        self.rec_pairs = torch.empty((rows // 2, (2 * d + 5) & ~3), dtype=torch.float32, device=dev)
+        _lib.check(L.vr_pack_records32_pairs(_lib.ptr(self.rec), rows, d, _lib.ptr(self.rec_pairs),
+                                             _lib.stream_handle()), "vr_pack_records32_pairs")
         c = [0.0] * 8
         c[:d] = self.center.cpu().tolist()
         self.struct = _Screen32Struct(self.rec.data_ptr(), (ctypes.c_double * 8)(*c), self.sqmax,
-                                      self.bound)
+                                      self.bound, self.rec_pairs.data_ptr())
 
 
 class _PruneStruct(ctypes.Structure):
@@ -374,12 +379,7 @@ class PruneIndex:
         self.rows = rows
         self.screen32 = Screen32(crec, n, d, center=center)
         # the pruned kernel reads the fp32 rows pair-interleaved (packed FFMA2)
-        p2 = (2 * d + 5) & ~3
-        self.rec32p = torch.empty((rows // 2, p2), dtype=torch.float32, device=dev)
-        L = _lib.lib()
-        _lib.check(L.vr_pack_records32_pairs(_lib.ptr(self.screen32.rec), rows, d,
-                                             _lib.ptr(self.rec32p), _lib.stream_handle()),
-                   "vr_pack_records32_pairs")
+        self.rec32p = self.screen32.rec_pairs
         self.tile_box32 = _outward32(lo, hi, self.screen32.center)
         self.node_box32 = _outward32(nlo, nhi, self.screen32.center)
         lv = wide_levels(lo, hi)

@@ -23,7 +23,7 @@ int vr::coop_mode() {
   return v;
 }
 
-extern "C" int vr_abi_version(void) { return 2; }
+extern "C" int vr_abi_version(void) { return 3; }
 
 extern "C" const char* vr_status_string(int status) {
   switch (status) {
@@ -42,6 +42,7 @@ Screen vr::make_screen(double sqmax, const vr_screen32* s32, int d) {
   sc.fr.sqmax = sqmax;
   if (s32) {
     sc.rec32 = s32->rec;
+    sc.rec32p = s32->rec_pairs;
     for (int k = 0; k < VR_MAX_D; ++k) sc.fr.c0[k] = k < d ? s32->center[k] : 0.0;
     sc.fr.sqmax32 = s32->sqmax;
     sc.fr.bnd32 = s32->bound;

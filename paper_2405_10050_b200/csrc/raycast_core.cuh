@@ -712,16 +712,21 @@ __device__ __forceinline__ void init_padding_lane(RayState<D>& r) {
 // the centred fp32 copy when F32); the last warp to release a stage issues
 // its refill.
 // ---------------------------------------------------------------------------
-template <int D, int R, int NT, int TILE, int STAGES, int MINB, bool F32, class Src>
+template <int D, int R, int NT, int TILE, int STAGES, int MINB, bool F32, class Src,
+          bool PAIRS = false>
 __global__ void __launch_bounds__(NT, MINB)
     k_raycast(Src src, const double* __restrict__ crec, const float* __restrict__ crec32,
               const int32_t* __restrict__ cand, int64_t n_cand, Frame fr, RayOut out) {
   constexpr int S = rec_stride(D);
-  constexpr int S32 = rec32_stride(D);
+  // fp32 rows: row layout (S32 floats per record) or pair-interleaved (P2
+  // floats per two records, packed FFMA2 screen)
+  constexpr int S32 = PAIRS ? rec32p_stride(D) : rec32_stride(D);
+  constexpr int F32_PER_TILE = PAIRS ? TILE / 2 * S32 : TILE * S32;
   constexpr int NW = NT / 32;
-  static_assert(TILE % 8 == 0 && VR_REC_PAD % TILE == 0, "tile must divide the record padding");
+  static_assert(TILE % 16 == 0 && VR_REC_PAD % TILE == 0, "tile must divide the record padding");
+  static_assert(!PAIRS || F32, "pairs are an fp32 layout");
   constexpr uint32_t BYTES64 = (uint32_t)(TILE * S * sizeof(double));
-  constexpr uint32_t BYTES32 = F32 ? (uint32_t)(TILE * S32 * sizeof(float)) : 0u;
+  constexpr uint32_t BYTES32 = F32 ? (uint32_t)(F32_PER_TILE * sizeof(float)) : 0u;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* tiles = reinterpret_cast<double*>(smem_raw);
   float* tiles32 = reinterpret_cast<float*>(smem_raw + (size_t)STAGES * BYTES64);
@@ -735,7 +740,7 @@ __global__ void __launch_bounds__(NT, MINB)
     mbar_arrive_expect_tx(&full[st], BYTES64 + BYTES32);
     bulk_g2s(tiles + (size_t)st * TILE * S, crec + t * TILE * S, BYTES64, &full[st]);
     if constexpr (F32)
-      bulk_g2s(tiles32 + (size_t)st * TILE * S32, crec32 + t * TILE * S32, BYTES32, &full[st]);
+      bulk_g2s(tiles32 + (size_t)st * F32_PER_TILE, crec32 + t * F32_PER_TILE, BYTES32, &full[st]);
   };
   if (tid == 0) {
 #pragma unroll
@@ -762,8 +767,12 @@ __global__ void __launch_bounds__(NT, MINB)
   for (int64_t t = 0; t < ntiles; ++t) {
     const int st = (int)(t % STAGES);
     mbar_wait(&full[st], (uint32_t)((t / STAGES) & 1));
-    screen_tile<D, R, TILE, F32>(ray, tiles + (size_t)st * TILE * S,
-                                 tiles32 + (size_t)st * TILE * S32, (int)(t * TILE), fr);
+    if constexpr (PAIRS)
+      screen_tile_pairs<D, R, TILE>(ray, tiles + (size_t)st * TILE * S,
+                                    tiles32 + (size_t)st * F32_PER_TILE, (int)(t * TILE), fr);
+    else
+      screen_tile<D, R, TILE, F32>(ray, tiles + (size_t)st * TILE * S,
+                                   tiles32 + (size_t)st * F32_PER_TILE, (int)(t * TILE), fr);
     // release the stage; the last warp to release it issues the refill
     __syncwarp();
     if (lane == 0) {
@@ -1665,22 +1674,35 @@ struct RaycastCfgT {
 template <int D>
 using RaycastCfg = RaycastCfgT<D, (D <= 3) ? 4 : 2, (D <= 3 || D >= 7) ? 2 : 3>;
 
+// packed-pair fp32 screen (screen_tile_pairs): R rays per thread share each
+// loaded candidate pair
+#ifndef VR_EX_R
+#define VR_EX_R 2
+#endif
+#ifndef VR_EX_MINB
+#define VR_EX_MINB 2
+#endif
+template <int D>
+using RaycastPairsCfg = RaycastCfgT<D, VR_EX_R, VR_EX_MINB>;
+
 // Screening inputs shared by both kernels: fp32 centred records (nullable ->
 // fp64 screen) and the frame constants.
 struct Screen {
-  const float* rec32;  // records matching `crec` (same row order), or nullptr
+  const float* rec32;   // records matching `crec` (same row order), or nullptr
+  const float* rec32p;  // the same rows pair-interleaved (nullable: row layout)
   Frame fr;
 };
 
-template <class C, int D, bool F32, class Src>
+template <class C, int D, bool F32, class Src, bool PAIRS = false>
 int launch_raycast_cfg(const Src& src, int64_t n_rays, const double* crec, const int32_t* cand,
                        int64_t n_cand, const Screen& sc, const RayOut& out, cudaStream_t st) {
-  auto kern = k_raycast<D, C::R, C::NT, C::TILE, C::STAGES, C::MINB, F32, Src>;
+  auto kern = k_raycast<D, C::R, C::NT, C::TILE, C::STAGES, C::MINB, F32, Src, PAIRS>;
   const size_t sm = C::smem(F32);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int64_t per_block = (int64_t)C::NT * C::R;
   const int64_t grid = (n_rays + per_block - 1) / per_block;
-  kern<<<(unsigned)grid, C::NT, sm, st>>>(src, crec, sc.rec32, cand, n_cand, sc.fr, out);
+  kern<<<(unsigned)grid, C::NT, sm, st>>>(src, crec, PAIRS ? sc.rec32p : sc.rec32, cand, n_cand,
+                                          sc.fr, out);
   VR_RETURN_LAUNCH();
 }
 
@@ -1699,6 +1721,11 @@ int launch_raycast(const Src& src, int64_t n_rays, const double* crec, const int
     cudaError_t e = cudaMemsetAsync(out.recheck_count, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return vr_cuda_status(e);
   }
+#ifndef VR_NO_EXHAUSTIVE_PAIRS
+  if (sc.rec32p)
+    return launch_raycast_cfg<RaycastPairsCfg<D>, D, true, Src, true>(src, n_rays, crec, cand,
+                                                                      n_cand, sc, out, st);
+#endif
   if (sc.rec32)
     return launch_raycast_cfg<RaycastCfg<D>, D, true>(src, n_rays, crec, cand, n_cand, sc, out, st);
   return launch_raycast_cfg<RaycastCfg<D>, D, false>(src, n_rays, crec, cand, n_cand, sc, out, st);
