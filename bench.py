@@ -429,11 +429,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded config-2 recipe, SURVEY.md §8(d))",
-            "config": {"workload": "config2: batched RayCast N=20000 d=6, 1e6 rays/GPU from "
-                                   "descent vertices, eta=(g,)",
-                       "n_generators": N_GEN, "d": DIM, "rays_per_gpu": n,
-                       "parallelism": f"ray-sharded x{world}, generators replicated",
-                       "l2": "flushed between timed steps (256 MB write, untimed)"},
+            "config": arm_config(world, n),
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak32,
                          "unit": "TFLOP/s", "frac": achieved / peak32, "traffic": traffic,
                          "kernel": ("k_raycast_pruned<6,R=1,tile=64,fp32 screen>"
@@ -481,6 +477,15 @@ def run_ours(args):
     return result
 
 
+def arm_config(world, n):
+    """The `config` object of both arms (same workload, same keys)."""
+    return {"workload": "config2: batched RayCast N=20000 d=6, 1e6 rays/GPU from "
+                        "descent vertices, eta=(g,)",
+            "n_generators": N_GEN, "d": DIM, "rays_per_gpu": n,
+            "parallelism": f"ray-sharded x{world}, generators replicated",
+            "l2": "flushed between timed steps (256 MB write, untimed)"}
+
+
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -513,12 +518,12 @@ def run_reference(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded config-2 recipe)",
-            "config": {"workload": "config2: batched RayCast N=20000 d=6", "n_generators": N_GEN,
-                       "d": DIM, "rays_per_step": m},
+            "data": "synthetic (seeded config-2 recipe, SURVEY.md §8(d))",
+            "config": arm_config(world, args.rays),
             "cpu_baseline": {"value": value, "unit": "rays/s", "cores": cores, "kind": "port",
-                             "sample": f"{m} config-2 rays per step, oracle restatement of "
-                                       "raycast_incircle (kd-tree probe loop, scipy cKDTree)"},
+                             "sample": f"{m} config-2 rays per step (the first rays of the same "
+                                       "recipe), oracle restatement of raycast_incircle "
+                                       "(kd-tree probe loop, scipy cKDTree)"},
             "e2e": {"value": value, "unit": "rays/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
