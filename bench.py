@@ -452,7 +452,7 @@ def run_ours(args):
                 "pairs_per_launch": n * N_GEN},
             "e2e": {"value": e2e_value, "unit": "rays/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "HostRaycaster.run (pinned host arrays)"},
-            "gpu_launches": 3 * args.steps,  # ray keys + fused RayCast + exact re-check per step
+            "gpu_launches": (3 if args.mode == "pruned" else 2) * args.steps,  # [ray keys +] RayCast + re-check
             "clocks": clk.summary(),
             "checks": {"escaped": n_esc, "degenerate": n_deg, "pool_build_s": t_pool},
         }
