@@ -169,42 +169,6 @@ __device__ __forceinline__ void ray_set_best(RayState<D>& r, double t, double de
   r.rb32 = __double2float_ru((rho2 + dlt) * (1.0 + (D + 4) * 1.1920928955078125e-07));
 }
 
-// Rare path: candidate i passed the (possibly stale) screening bound.  The
-// power w.r.t. the CURRENT sphere is recomputed first, because an earlier
-// candidate of the same unrolled step may have moved the sphere.
-template <int D, bool F32>
-__device__ __forceinline__ void ray_rare(RayState<D>& r, const double (&xi)[D], double sq, int i,
-                                         const Frame& fr) {
-  double fp = sq, q = 0.0;
-  const bool have0 = r.ib >= 0;
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    // fp32-screen kernels keep no fp64 z: rebuild it exactly as set_best did
-    const double zk2 = F32 ? (have0 ? -2.0 * fma(r.tb, r.u[k], r.x[k]) : 0.0) : r.z[k];
-    fp = fma(zk2, xi[k], fp);
-    q = fma(r.u[k], xi[k], q);
-  }
-  if (have0 && !(fp < r.hi)) return;  // outside the current sphere's band
-  if (i == r.ib) return;     // the current best itself (re-screened after a seed)
-  if (!(q > r.thr)) return;  // outside the forward halfspace (raycast.py:110-117)
-  const bool have = r.ib >= 0;
-  if (have && fp >= r.lim - r.dlt) r.near = 1;
-  if (have && !(fp < r.lim)) return;
-  // reference centred crossing (raycast.py:201-203)
-  double aa = 0.0;
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    double a = r.x[k] - xi[k];
-    aa = fma(a, a, aa);
-  }
-  const double den = q - r.s;
-  const double t = (aa - r.base) / (2.0 * den);
-  const double told = r.tb, denold = r.denb;
-  ray_set_best<D, F32>(r, t, den, i, fr);
-  // power of the previous best w.r.t. the new sphere
-  if (have && 2.0 * denold * (told - t) < r.dlt) r.near = 1;
-}
-
 template <int D>
 __device__ __forceinline__ void load_rec(const double* p, double (&xi)[D]) {
   const double2* p2 = reinterpret_cast<const double2*>(p);
