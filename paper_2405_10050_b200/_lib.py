@@ -15,6 +15,8 @@ import torch
 from ._build import LIB_PATH
 from .errors import DeviceUnavailable
 
+ABI_VERSION = 3  # vr_abi_version() of the library this package expects
+
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
 _int = ctypes.c_int
