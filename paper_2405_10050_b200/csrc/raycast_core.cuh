@@ -979,11 +979,12 @@ template <int D, int PT>
 __device__ __forceinline__ void screen_tile_remap(RayState<D>& r, const double* tile64,
                                                   const float* tilep, int gbase, unsigned mask,
                                                   const Frame& fr, WarpCounters* wc) {
-  static_assert(PT == 64, "64-bit hit masks");
+  static_assert(PT == 32 || PT == 64, "hits fit a 64-bit mask");
   constexpr int P2 = rec32p_stride(D);
   const int lane = threadIdx.x & 31;
   const int c = __popc(mask);
-  const int G = c <= 1 ? 32 : c <= 2 ? 16 : c <= 4 ? 8 : c <= 8 ? 4 : 2;
+  const int G0 = c <= 1 ? 32 : c <= 2 ? 16 : c <= 4 ? 8 : c <= 8 ? 4 : 2;
+  const int G = G0 < PT / 2 ? G0 : PT / 2;  // at least one candidate pair per lane
   const int slot = lane / G, sub = lane % G;
   const bool valid = slot < c;
   const int owner = valid ? (int)__fns(mask, 0, slot + 1) : lane;
@@ -1129,7 +1130,7 @@ __global__ void __launch_bounds__(32, MINB)
     // (no re-test of the tile box here: the leaf was tested when its parent
     // was expanded, and re-testing skipped < 2% of the tiles on config 2)
     ++tiles_done;
-    if constexpr (F32 && R == 1 && PT == 64 && remap_max<D>() > 0) {
+    if constexpr (F32 && R == 1 && (PT == 32 || PT == 64) && remap_max<D>() > 0) {
       if (__popc(tmask) <= remap_max<D>())
         screen_tile_remap<D, PT>(ray[0], STAGE64 ? buf[b] : crec + t * PT * S, buf32[b],
                                  (int)(t * PT), tmask, fr, work ? &wc : nullptr);
