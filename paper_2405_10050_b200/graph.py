@@ -117,6 +117,36 @@ def _project_out_batch(w, basis):
     return v
 
 
+class _Draws:
+    """Standard-normal d-vectors per start, in each start's stream order.
+
+    With the package's own streams (rngs=None) each start's Generator draws
+    a block of K vectors at once -- one (K, d) draw equals K sequential (d,)
+    draws bitwise -- so the per-level Python loop
+    touches no Generator; caller-supplied rngs are drawn from one vector at
+    a time so that their state advances exactly as in the reference."""
+
+    def __init__(self, rngs, seed, starts, d, block=None):
+        self.d = d
+        self.own = rngs is None
+        self.rngs = [_rng.stream(seed, "descent", int(s)) for s in starts] if self.own else rngs
+        if self.own:
+            self.K = block or (d + 3)
+            self.buf = np.stack([g.standard_normal((self.K, d)) for g in self.rngs])
+            self.ptr = np.zeros(len(starts), dtype=np.int64)
+
+    def take(self, grp):
+        if not self.own:
+            return np.stack([self.rngs[a].standard_normal(self.d) for a in grp])
+        empty = grp[self.ptr[grp] >= self.K]
+        for a in empty:  # refill (many escapes / redraws): the next block of the stream
+            self.buf[a] = self.rngs[a].standard_normal((self.K, self.d))
+            self.ptr[a] = 0
+        z = self.buf[grp, self.ptr[grp]]
+        self.ptr[grp] += 1
+        return z
+
+
 def descent_batch(ns: NodeSet, starts, seed: int = 0, stats: RaycastStats = None,
                   rngs=None):
     """Many descents at once; the same RNG streams and sigma as calling
@@ -129,8 +159,7 @@ def descent_batch(ns: NodeSet, starts, seed: int = 0, stats: RaycastStats = None
     d = ns.dim
     starts = np.asarray([int(s) for s in starts], dtype=np.int64)
     S = len(starts)
-    if rngs is None:
-        rngs = [_rng.stream(seed, "descent", int(s)) for s in starts]
+    draws = _Draws(rngs, seed, starts, d)
     sig = np.full((S, d + 1), -1, dtype=np.int64)
     sig[:, 0] = starts
     k = np.ones(S, dtype=np.int64)          # |sigma|
@@ -150,13 +179,13 @@ def descent_batch(ns: NodeSet, starts, seed: int = 0, stats: RaycastStats = None
         for kk in levels:
             grp = active[k_act == kk]
             pos = np.searchsorted(active, grp)
-            z = np.stack([rngs[a].standard_normal(d) for a in grp])
+            z = draws.take(grp)
             v = _project_out_batch(z, basis[grp, :kk - 1])
             nrm = np.linalg.norm(v, axis=1)
             for m in np.nonzero(nrm < 1e-9)[0]:  # free redraws (graph.py:72-74)
                 a = grp[m]
                 while True:
-                    vv = _project_out_batch(rngs[a].standard_normal(d)[None], basis[a:a + 1, :kk - 1])[0]
+                    vv = _project_out_batch(draws.take(np.array([a])), basis[a:a + 1, :kk - 1])[0]
                     if np.linalg.norm(vv) >= 1e-9:
                         v[m] = vv
                         nrm[m] = np.linalg.norm(vv)

@@ -214,3 +214,21 @@ def test_descent_batch_host_logic_with_escapes(monkeypatch):
         v_sig, v_r = orc.descent(nodes, int(s), vb.rng.stream(0, "descent", int(s)))
         assert tuple(sig[s]) == tuple(v_sig), s
         assert np.allclose(r[s], v_r, rtol=0, atol=1e-9 * max(1.0, np.abs(v_r).max()))
+
+
+def test_descent_draw_blocks_are_the_reference_stream():
+    """descent_batch draws its directions in (K, d) blocks per start; the
+    vectors must be the start's stream(seed, "descent", s) in order, across
+    block refills and uneven consumption."""
+    from paper_2405_10050_b200.graph import _Draws
+    starts = np.array([5, 17, 99, 4000])
+    dr = _Draws(None, 3, starts, 4, block=3)
+    seq = {a: [] for a in range(len(starts))}
+    for it in range(11):
+        grp = np.array([0, 2]) if it % 2 else np.arange(len(starts))
+        for a, row in zip(grp, dr.take(grp)):
+            seq[a].append(row)
+    for a, s in enumerate(starts):
+        g = vb.rng.stream(3, "descent", int(s))
+        for row in seq[a]:
+            assert np.array_equal(row, g.standard_normal(4))
