@@ -223,9 +223,10 @@ def extra_configs(vb, torch, world, rank):
     ns3 = vb.build_node_set(pts3)
     ns3.prune_index()
     vb.voronoi_graph(ns3, seed=0)  # warm (table allocation, lazy module loading)
+    w3 = torch.zeros(16, dtype=torch.int64, device="cuda")
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    m3, info3 = vb.voronoi_graph(ns3, seed=0, return_info=True)
+    m3, info3 = vb.voronoi_graph(ns3, seed=0, return_info=True, work=w3)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     import hashlib
@@ -240,19 +241,22 @@ def extra_configs(vb, torch, world, rank):
         "host_materialise_s": dt_host,
         "sigma_digest_matches_reference": dig == "f8093583cb129297758ebea66c8fcbbf3938086d"
                                                 "9f8b8ee1b0f79096a9351173",
+        "pairs_screened": int(w3[0].item()), "d": 5,
         "reference_cpu_s_1core_build_container": 667.0}
     pts4 = np.random.default_rng(0).random((100000, 4))
     ns4 = vb.NodeSet(pts4)
     ns4.prune_index()
     cells = np.arange(100000)
     parallel.mc_cells_sharded(ns4, cells[:2000], 1000, seed=0)  # warm
+    w4 = torch.zeros(16, dtype=torch.int64, device="cuda")
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    res4 = parallel.mc_cells_sharded(ns4, cells, 1000, seed=0)
+    res4 = parallel.mc_cells_sharded(ns4, cells, 1000, seed=0, work=w4)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     out["config4_mc"] = {"cells": 100000, "rays_per_cell": 1000, "seconds": dt,
                          "rays_per_s": 1e8 / dt, "bounded_cells": int((res4.status == 0).sum()),
+                         "pairs_screened": int(w4[0].item()), "d": 4,
                          "reference_cpu_rays_per_s_per_core_build_container": 4180}
     pts5 = np.random.default_rng(0).random((10 ** 6, 8)).astype(np.float32).astype(np.float64)
     ns5 = vb.NodeSet(pts5)
@@ -262,12 +266,14 @@ def extra_configs(vb, torch, world, rank):
     st = vb.RaycastStats()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    m5, lv = vb.voronoi_local(ns5, seeds, hops=5, stats=st, return_levels=True)
+    w5 = torch.zeros(16, dtype=torch.int64, device="cuda")
+    m5, lv = vb.voronoi_local(ns5, seeds, hops=5, stats=st, return_levels=True, work=w5)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     out["config5_local_traversal"] = {
         "seeds": 10000, "hops": 5, "vertices": int(len(lv)), "seconds_incl_descent": dt,
         "mesh": "device-resident (HBM), not copied to the host",
+        "pairs_screened": int(w5[0].item()), "d": 8,
         "vertices_per_s": len(lv) / dt, "edge_raycasts_this_rank": st.raycasts,
         "per_level": np.bincount(lv).tolist(),
         "reference_cpu_rays_per_s_per_core_build_container": 1000}
@@ -332,7 +338,7 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)]
           for _ in range(args.warmup + args.steps)]
-    work = torch.zeros(1, dtype=torch.int64, device=dev)
+    work = torch.zeros(16, dtype=torch.int64, device=dev)  # VR_WORK_COUNTERS
     ns.prune_index()  # kd index built once per NodeSet, outside the timing
 
     def step(i, mode=args.mode, events=None):
@@ -355,7 +361,7 @@ def run_ours(args):
         dist.barrier()
     step_ms = [ev[i][0].elapsed_time(ev[i][2]) for i in range(args.warmup, args.warmup + args.steps)]
     kern_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(args.warmup, args.warmup + args.steps)]
-    screened = int(work.item()) / (args.warmup + args.steps) if args.mode == "pruned" else None
+    screened = int(work[0].item()) / (args.warmup + args.steps) if args.mode == "pruned" else None
     # the exhaustive (TMA-staged, unpruned) kernel on the same rays, for its
     # roofline: fp64 screen (FP64 pipe) and fp32 screen (FP32 pipe)
     ex_ms = {}
@@ -457,6 +463,16 @@ def run_ours(args):
             "checks": {"escaped": n_esc, "degenerate": n_deg, "pool_build_s": t_pool},
         }
         if extra is not None:
+            for key, ent in extra.items():
+                if "pairs_screened" in ent:
+                    secs = ent.get("seconds", ent.get("seconds_incl_descent"))
+                    fl = 2 * ent["d"]
+                    ach = ent["pairs_screened"] * fl / secs / 1e12
+                    ent["roofline"] = {
+                        "bound": "fp32", "flop_per_pair": fl, "achieved": ach, "peak": peak32,
+                        "unit": "TFLOP/s", "frac": ach / peak32,
+                        "time_basis": "whole-config wall time (all phases), so a lower "
+                                      "bound on the pruned kernel's own rate"}
             result["extra_configs"] = extra
         if world == 1 and not args.no_cpu_baseline:
             cores = host_cores()

@@ -172,8 +172,13 @@ typedef struct vr_prune_index {
  * int32) is the processing order: slot k handles ray order[k]; callers sort
  * rays by the kd position of eta[0] so that a warp's rays are spatially
  * coherent.  Outputs are written at the ray's own index.  With s32 != NULL and
- * ix->rec32 != NULL the screen runs in fp32 (s32->rec is not used here).  `work` (nullable,
- * device uint64) accumulates the (ray, generator) pairs actually screened. */
+ * ix->rec32 != NULL the screen runs in fp32 (s32->rec is not used here).  `work`
+ * (nullable, >= VR_WORK_COUNTERS device uint64, zeroed by the caller)
+ * accumulates work counters: [0] (ray, generator) pairs screened (32 lanes x
+ * 64 per tile), [1] screening blocks with rare work, [2] warp-level rare
+ * iterations, [3] rare entries, [4] sphere updates, [5] tree-node tests;
+ * builds with VR_RARE_STATS also use [6..10]. */
+#define VR_WORK_COUNTERS 16
 int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
                       const vr_screen32* s32, const vr_prune_index* ix, const double* x, const double* u,
                       const int32_t* eta, int eta_len, int64_t n_rays,

@@ -367,6 +367,7 @@ class DeviceTraversal:
         self.nv = 0
         self.nb = 0
         self.e_ub = 0
+        self.work = None  # optional VR_WORK_COUNTERS tensor (pruned-kernel accounting)
 
     def _alloc_vtable(self, cap):
         d = self.d
@@ -455,7 +456,8 @@ class DeviceTraversal:
         self.e_ub = (self.d + 1) * m
 
     def _raycast(self, rx, ru, reta, stats, ws):
-        res = raycast_batch(self.ns, rx, ru, reta, want_rp=False, stats=stats, workspace=ws)
+        res = raycast_batch(self.ns, rx, ru, reta, want_rp=False, stats=stats, workspace=ws,
+                            work=self.work)
         return res.idx, res.flag
 
     def level(self, f0, f1, lvl, stats=None, ws=None, raycast_fn=None):
@@ -562,7 +564,7 @@ def _level_raycaster(ns, stats, group):
 
 def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heuristic",
                   eps: float = None, stats: RaycastStats = None, return_info: bool = False,
-                  group=None):
+                  group=None, work=None):
     """Full Voronoi mesh by exhaustive edge-tracked traversal (graph.py:88-146).
 
     Level-synchronous on the device: every level raycasts all open edges of
@@ -575,6 +577,7 @@ def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heurist
         stats = RaycastStats()
     first = descent(ns, 0, _rng.stream(seed, "descent", 0), stats)
     tr = DeviceTraversal(ns)
+    tr.work = work
     tr.seed_vertex(first.sigma)
     from .raycast import Workspace
     ws = Workspace()
@@ -594,7 +597,7 @@ def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heurist
 
 
 def voronoi_local(ns: NodeSet, starts, hops: int, seed: int = 0, stats: RaycastStats = None,
-                  return_levels: bool = False, group=None):
+                  return_levels: bool = False, group=None, work=None):
     """All Voronoi vertices within `hops` edge hops of the descent vertices of
     `starts` (SURVEY.md §8(d) config 5 "local traversal").
 
@@ -610,6 +613,7 @@ def voronoi_local(ns: NodeSet, starts, hops: int, seed: int = 0, stats: RaycastS
     _, first = np.unique(sig, axis=0, return_index=True)
     sig = sig[np.sort(first)]
     tr = DeviceTraversal(ns, vcap_hint=max(4 * ns.n, 6 * len(sig) * 4 ** min(hops, 8)))
+    tr.work = work
     tr.seed_vertices(sig)
     from .raycast import Workspace
     ws = Workspace()

@@ -89,7 +89,7 @@ MC_ORDER_RAYS = True  # direction-sorted processing order in the pruned MC path
 
 def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_faces=256,
                degenerate_is_error=True, want_samples=False, workspace=None, stats=None,
-               mode="auto", screen="fp32"):
+               mode="auto", screen="fp32", work=None):
     """Run rays + recheck + reduce for len(cells) cells x n rays; device tensors out."""
     rec, sqmax = ns.device_records()
     dev = rec.device
@@ -138,7 +138,7 @@ def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_fa
         _lib.check(L.vr_mc_rays_pruned(_lib.ptr(rec), ns.n, d, sqmax, s32p, ctypes.byref(ix.struct),
                                        _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed, _lib.ptr(order),
                                        _lib.ptr(idx), _lib.ptr(t), _lib.ptr(flag), _lib.ptr(rl),
-                                       _lib.ptr(rc), None, sh), "vr_mc_rays_pruned")
+                                       _lib.ptr(rc), _lib.ptr(work), sh), "vr_mc_rays_pruned")
     else:
         _lib.check(L.vr_mc_rays(_lib.ptr(rec), ns.n, d, sqmax, s32p, _lib.ptr(crec), _lib.ptr(cand),
                                 n_cand, _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed,
@@ -183,7 +183,7 @@ def _collect(cells, out, want_samples):
 
 def mc_cells(ns: NodeSet, cells, n: int, seed: int = 0, max_faces: int = 256,
              want_samples=False, stats: RaycastStats = None, chunk_rays: int = 1 << 26,
-             mode="auto", screen="fp32"):
+             mode="auto", screen="fp32", work=None):
     """Batched device MC (Philox directions) over many cells.
 
     Returns an :class:`MCResult`; cells whose status is not CELL_OK are the
@@ -201,7 +201,7 @@ def mc_cells(ns: NodeSet, cells, n: int, seed: int = 0, max_faces: int = 256,
     for lo in range(0, len(cells), per_chunk):
         sub = cells[lo:lo + per_chunk]
         out = _mc_device(ns, sub, n, seed=seed, max_faces=max_faces, want_samples=want_samples,
-                         workspace=ws, stats=stats, mode=mode, screen=screen)
+                         workspace=ws, stats=stats, mode=mode, screen=screen, work=work)
         parts.append(_collect(sub, out, want_samples))
     if len(parts) == 1:
         return parts[0]

@@ -214,7 +214,8 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
         mode: "exhaustive" scans every generator (TMA-staged tiles);
             "pruned" skips kd tiles with a certificate (identical results);
             "auto" prunes when N >= PRUNE_MIN_GENERATORS and no candidate subset is given.
-        work: optional int64 device tensor (1,) accumulating the pairs the
+        work: optional zeroed int64 device tensor of >= 16 entries (see
+            VR_WORK_COUNTERS in the header); [0] accumulates the pairs the
             pruned kernel screened (roofline accounting).
         screen: "fp32" screens pairs in fp32 (centred frame, rigorous bound)
             and re-checks survivors in fp64; "fp64" screens in fp64.  The
@@ -263,6 +264,8 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
     rc = ws.get("recheck_count", (1,), torch.int32, dev)
     sh = _lib.stream_handle(stream)
     pruned = _use_pruned(ns, candidates, mode)
+    if work is not None and work.numel() < 16:
+        raise ValueError("work must hold at least 16 counters (VR_WORK_COUNTERS)")
     if events is not None:
         events[0].record(stream)
     if pruned:
