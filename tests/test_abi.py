@@ -65,3 +65,28 @@ def test_no_cpu_fallback(built_library):
         vb.raycast_batch(ns, np.zeros((1, 2)), np.array([[0.0, 1.0]]), np.zeros((1, 1), int))
     with pytest.raises(DeviceUnavailable):
         vb.mc_areas_only(ns, 0, 10, np.random.default_rng(0))
+
+
+@pytest.mark.gpu
+def test_integration_md_binding_runs():
+    """The ctypes binding printed in INTEGRATION.md (what a reference
+    maintainer would paste) runs as written and matches raycast_batch."""
+    import numpy as np
+    import paper_2405_10050_b200 as vb
+    from paper_2405_10050_b200._build import LIB_PATH
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    code = re.search(r"```python\n(# pkg/src/voronray/_b200.py.*?)```", text, re.S).group(1)
+    code = code.replace("/path/to/paper_2405_10050_b200/_voronray_b200.so", LIB_PATH)
+    env = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), env)
+    pts = np.random.default_rng(4).random((700, 4))
+    ns = vb.NodeSet(pts)
+    dn = env["DeviceNodes"](ns)
+    rng = np.random.default_rng(5)
+    g = rng.integers(0, 700, 300).astype(np.int32)
+    u = rng.standard_normal((300, 4))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    idx, t, rp, fl = env["raycast_many"](dn, pts[g], u, g[:, None])
+    ref = vb.raycast_batch(ns, pts[g], u, g[:, None])
+    assert np.array_equal(idx, ref.idx.cpu().numpy())
+    assert np.array_equal(fl, ref.flag.cpu().numpy())
