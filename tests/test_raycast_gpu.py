@@ -366,3 +366,33 @@ def test_config2_full_size_properties():
     thr = (ue * X[gd[esc, 0].long()]).sum(1)
     thr = thr + 1e-12 * torch.clamp(thr.abs(), min=1.0)
     assert bool(((X @ ue.T).max(0).values <= thr).all())
+
+
+@pytest.mark.parametrize("case", ["offset", "anisotropic", "clustered"])
+def test_fp32_screen_robust_to_scale(case):
+    """The fp32 screen's rigorous bound must hold for badly scaled inputs:
+    a large common offset (1e3 + 1e-3 * U), wildly different axis scales,
+    and tight clusters.  Pruned fp32 == exhaustive fp64 bitwise."""
+    rng = np.random.default_rng(77)
+    n, d = 6000, 4
+    if case == "offset":
+        pts = 1e3 + 1e-3 * rng.random((n, d))
+    elif case == "anisotropic":
+        pts = rng.random((n, d)) * np.array([1e4, 1.0, 1e-4, 3e2])
+    else:
+        centers = rng.random((20, d)) * 100
+        pts = centers[rng.integers(0, 20, n)] + 1e-3 * rng.standard_normal((n, d))
+    ns = vb.build_node_set(pts)
+    m = 5000
+    g = rng.integers(0, n, m)
+    u = rng.standard_normal((m, d))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    a = vb.raycast_batch(ns, pts[g], u, g[:, None], mode="exhaustive", screen="fp64").to_host()
+    for mode in ("pruned", "exhaustive"):
+        b = vb.raycast_batch(ns, pts[g], u, g[:, None], mode=mode, screen="fp32").to_host()
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y, equal_nan=True), mode
+    want, _ = orc.raycast_argmin(pts, pts[g[:300]], u[:300], g[:300, None])
+    got = a[0][:300]
+    ok = a[3][:300] != 3
+    assert np.array_equal(got[ok], want[ok])
