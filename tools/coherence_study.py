@@ -120,6 +120,16 @@ def main():
     print("union tiles per warp (coherent order): mean %.1f p50 %d p99 %d p99.9 %d max %d; "
           "warps > 150 tiles: %d" % (pw.mean(), np.percentile(pw, 50), np.percentile(pw, 99),
                                      np.percentile(pw, 99.9), pw.max(), (pw > 150).sum()))
+    # union with the SEED spheres (best candidate of the start tile), i.e. a
+    # tile list fixed before any screening
+    ts = torch.where(torch.isfinite(tseed), tseed, torch.full_like(tseed, 1e3))
+    tot_s = per_s = 0
+    for lo in range(0, n, CH):
+        sel = o[lo:lo + CH]
+        m = need_mask(ix, xd[sel], ud[sel], gl[sel], ts[sel], X, d)
+        per_s += m.sum().item()
+        tot_s += m.view(-1, 32, m.shape[1]).any(1).sum().item()
+    print(f"  seed spheres: per-ray need {per_s / n:.1f} tiles, warp union {tot_s / nw:.1f} tiles")
     # outliers: union without the k rays of largest individual need
     for kx in (1, 2, 4, 8):
         tot_u = 0
