@@ -1,11 +1,9 @@
 """Multi-rank host logic on CPU (gloo, world_size 2): sharding, variable-
 length all-gather, the per-level sharded RayCast exchange of the traversal
 (driven here by the CPU oracle as the per-rank raycaster), MC gathers."""
-import os
 import socket
 
 import numpy as np
-import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as tmp

@@ -4,7 +4,7 @@ escape status; coordinates within 1e-9 * max(1, |r'|)."""
 import numpy as np
 import pytest
 
-from conftest import config2_rays, golden
+from conftest import golden
 
 pytestmark = pytest.mark.gpu
 
