@@ -362,6 +362,13 @@ def run_ours(args):
     step_ms = [ev[i][0].elapsed_time(ev[i][2]) for i in range(args.warmup, args.warmup + args.steps)]
     kern_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(args.warmup, args.warmup + args.steps)]
     screened = int(work[0].item()) / (args.warmup + args.steps) if args.mode == "pruned" else None
+    wk = (work.double().cpu() / (args.warmup + args.steps)).tolist()
+    n_warps = (n + 31) // 32
+    counters = {"tiles_per_warp": wk[0] / (64 * 32) / n_warps,
+                "tree_node_tests_per_warp": wk[5] / n_warps,
+                "rare_blocks_per_warp": wk[1] / n_warps,
+                "rare_iters_per_warp": wk[2] / n_warps,
+                "rare_entries_per_ray": wk[3] / n, "sphere_updates_per_ray": wk[4] / n}
     # the exhaustive (TMA-staged, unpruned) kernel on the same rays, for its
     # roofline: fp64 screen (FP64 pipe) and fp32 screen (FP32 pipe)
     ex_ms = {}
@@ -442,6 +449,10 @@ def run_ours(args):
                                     if args.mode == "pruned" else "k_raycast<6,2,128,256,4,3>"),
                          "kernel_ms": kms, "flop_per_pair": FLOP_PER_PAIR,
                          "pairs_per_launch": pairs, "pairs_per_ray": pairs / n,
+                         "work_counters": counters if args.mode == "pruned" else None,
+                         "screen": ("tensor-core (mma.sync tf32) + fp32 pre-filter + fp64 rare path"
+                                    if os.environ.get("VR_MMA", "1") != "0"
+                                    else "packed FFMA2 fp32 + fp64 rare path"),
                          "unit_of_work": "(ray, generator) pair screened; pruned kernel counts "
                                          "the pairs it actually screened (work counter)",
                          "peak_source": "measured live: FFMA probe (vr_fma_probe); "

@@ -15,7 +15,7 @@ import torch
 from ._build import LIB_PATH
 from .errors import DeviceUnavailable
 
-ABI_VERSION = 3  # vr_abi_version() of the library this package expects
+ABI_VERSION = 4  # vr_abi_version() of the library this package expects
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -50,6 +50,7 @@ _SIGNATURES = {
                           _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_pack_records32": [_vp, _i64, _int, _vp, _vp, _vp],
     "vr_pack_records32_pairs": [_vp, _i64, _int, _vp, _vp],
+    "vr_pack_records_mma": [_vp, _i64, _int, _vp, _vp],
     "vr_ray_keys": [_vp, _vp, _int, _i64, _vp, _i64, _int, _vp, _vp],
     "vr_mc_integrate": [_vp, _int, _vp, _i64, _i64, _vp, _u64, _vp, _vp, _vp, _int, _dbl, _int,
                         _vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

@@ -207,7 +207,7 @@ class _PruneStruct(ctypes.Structure):
                 ("node_box32", ctypes.c_void_p), ("node_range", ctypes.c_void_p),
                 ("n", ctypes.c_int64), ("wide_box32", ctypes.c_void_p),
                 ("wide_levels", ctypes.c_int32), ("wide_off", ctypes.c_int64 * 8),
-                ("wide_cnt", ctypes.c_int64 * 8)]
+                ("wide_cnt", ctypes.c_int64 * 8), ("recB", ctypes.c_void_p)]
 
 
 WIDE = 32
@@ -387,13 +387,22 @@ class PruneIndex:
         self.wide_cnt = [int(b.shape[0]) for b in boxes]
         self.wide_off = np.concatenate([[0], np.cumsum(self.wide_cnt)[:-1]]).astype(np.int64).tolist()
         self.wide_box32 = torch.cat(boxes).contiguous()
+        # tensor-core screen operand (d <= 6): rec32 rows in mma B-fragment order
+        self.recB = None
+        if d <= 6 and PRUNE_TILE == 64 and os.environ.get("VR_MMA", "1") != "0":
+            self.recB = torch.empty((rows, 8), dtype=torch.float32, device=dev)
+            L = _lib.lib()
+            _lib.check(L.vr_pack_records_mma(_lib.ptr(self.screen32.rec), rows, d,
+                                             _lib.ptr(self.recB), _lib.stream_handle()),
+                       "vr_pack_records_mma")
         p = lambda t: t.data_ptr()  # noqa: E731
         pad8 = lambda v: (ctypes.c_int64 * 8)(*(list(v) + [0] * (8 - len(v))))  # noqa: E731
         self.struct = _PruneStruct(p(crec), p(self.rec32p), p(self.perm), p(self.inv_perm),
                                    p(self.tile_box), p(self.tile_box32), p(self.node_box),
                                    p(self.node_box32), p(self.node_range), n,
                                    p(self.wide_box32), len(boxes), pad8(self.wide_off),
-                                   pad8(self.wide_cnt))
+                                   pad8(self.wide_cnt),
+                                   p(self.recB) if self.recB is not None else None)
 
 
 def build_node_set(points, backend="auto"):

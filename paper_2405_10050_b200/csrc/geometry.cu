@@ -225,6 +225,31 @@ __global__ void k_pairs32(const float* __restrict__ rec32, int64_t rows, float* 
   }
 }
 
+// fp32 records -> mma.sync m16n8k8 B fragments (tf32, round to nearest):
+// thread (tile, block, lane) writes the two values lane l of block j needs.
+template <int D>
+__global__ void k_pack_mma(const float* __restrict__ rec32, int64_t rows, float* __restrict__ out) {
+  static_assert(D + 2 <= 8, "one k8 step holds [x, |x|^2, 1]");
+  constexpr int S32 = rec32_stride(D);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < rows * 4;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(q & 31);
+    const int64_t row = (q >> 5) * 8 + (lane >> 2);  // (tile * 8 + block) * 8 + group
+    const float* a = rec32 + row * S32;
+    float v[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = (lane & 3) + 4 * h;
+      float f = k < D ? a[k] : (k == D ? a[D] : (k == D + 1 ? 1.0f : 0.0f));
+      if (k == D && isinf(f)) f = 1e30f;  // sentinel: never passes (finite, no inf - inf)
+      uint32_t t;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(f));
+      v[h] = __uint_as_float(t);
+    }
+    reinterpret_cast<float2*>(out)[q] = make_float2(v[0], v[1]);
+  }
+}
+
 inline unsigned blocks_for(int64_t n, int nt) { return (unsigned)((n + nt - 1) / nt); }
 
 }  // namespace
@@ -263,6 +288,22 @@ extern "C" int vr_pack_records32_pairs(const float* rec32, int64_t rows, int d, 
   VR_DISPATCH_D(d, {
     k_pairs32<D><<<nbk, 256, 0, as_stream(stream)>>>(rec32, rows, out);
   });
+  VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_pack_records_mma(const float* rec32, int64_t rows, int d, float* out,
+                                   void* stream) {
+  if (!rec32 || !out || rows <= 0 || (rows & 63)) return VR_EINVAL;
+  if (d > 6) return VR_EDIM;
+  const unsigned nbk = blocks_for(rows * 4, 256) < 4096 ? blocks_for(rows * 4, 256) : 4096;
+  switch (d) {
+    case 2: k_pack_mma<2><<<nbk, 256, 0, as_stream(stream)>>>(rec32, rows, out); break;
+    case 3: k_pack_mma<3><<<nbk, 256, 0, as_stream(stream)>>>(rec32, rows, out); break;
+    case 4: k_pack_mma<4><<<nbk, 256, 0, as_stream(stream)>>>(rec32, rows, out); break;
+    case 5: k_pack_mma<5><<<nbk, 256, 0, as_stream(stream)>>>(rec32, rows, out); break;
+    case 6: k_pack_mma<6><<<nbk, 256, 0, as_stream(stream)>>>(rec32, rows, out); break;
+    default: return VR_EDIM;
+  }
   VR_RETURN_LAUNCH();
 }
 

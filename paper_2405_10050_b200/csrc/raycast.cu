@@ -13,6 +13,16 @@ int vr::raycast_variant() {
   return v;
 }
 
+// Tensor-core screen of the pruned kernel (d <= 6, index built with recB):
+// on unless VR_MMA=0.
+int vr::mma_mode() {
+  static int v = [] {
+    const char* e = std::getenv("VR_MMA");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 // Pruned-kernel choice: VR_COOP=1 selects the cooperative warp-per-ray
 // kernel instead of the warp-per-32-rays kernel (default).
 int vr::coop_mode() {
@@ -23,7 +33,7 @@ int vr::coop_mode() {
   return v;
 }
 
-extern "C" int vr_abi_version(void) { return 3; }
+extern "C" int vr_abi_version(void) { return 4; }
 
 extern "C" const char* vr_status_string(int status) {
   switch (status) {

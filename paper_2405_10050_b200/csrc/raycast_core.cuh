@@ -58,6 +58,7 @@ struct RayState {
   float bsl32;  // slack of the fp32 halfspace bound
   float del32;  // slack of the fp32 box distance (centre rounding)
   float rb32;   // (rho^2 + dlt) rounded up with the fp32 sum slack (+inf: none)
+  float ctc;    // tensor-core screen constant: -(hi32 + tf32 error bound), tf32, rounded down
   int ib;       // current best (local candidate index), -1 = none
   int near;     // 1 -> needs exact re-check
   int nupd;     // sphere updates (work accounting)
@@ -65,6 +66,19 @@ struct RayState {
   int st_out, st_self, st_behind, st_band, st_imp;  // rare-path entry outcomes
 #endif
 };
+
+// tf32 helpers of the tensor-core screen.  tf32_down: the largest tf32 value
+// <= v (clears the 13 low mantissa bits toward -inf).
+__device__ __forceinline__ float tf32_down(float v) {
+  uint32_t b = __float_as_uint(v);
+  if (b & 0x1fffu) b = v < 0.0f ? (b & ~0x1fffu) + 0x2000u : (b & ~0x1fffu);
+  return __uint_as_float(b);
+}
+__device__ __forceinline__ uint32_t tf32_rn(float v) {
+  uint32_t t;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(v));
+  return t;
+}
 
 // Fill the per-ray constants from origin x, direction u and the eta
 // generators (global records).  Mirrors _Probe.__init__ (raycast.py:93-96)
@@ -124,6 +138,7 @@ __device__ __forceinline__ void ray_setup(RayState<D>& r, const double* __restri
   r.bsl32 = __double2float_ru((D + 4) * 2.384185791015625e-07 * sqrt((double)D) * fr.bnd32 + 1e-30);
   r.del32 = 0.0f;
   r.rb32 = CUDART_INF_F;
+  r.ctc = -1e20f;  // no sphere yet: every real candidate passes the tensor-core screen
 }
 
 // Move the screening sphere to the new best crossing t.
@@ -167,6 +182,16 @@ __device__ __forceinline__ void ray_set_best(RayState<D>& r, double t, double de
   // fp32 box test: |e32_k - e_k| <= 2^-22 (|z~|_inf + B); sum slack relative
   r.del32 = __double2float_ru(2.384185791015625e-07 * (ztmax + fr.bnd32));
   r.rb32 = __double2float_ru((rho2 + dlt) * (1.0 + (D + 4) * 1.1920928955078125e-07));
+  // Tensor-core screen (screen_tile_mma): the same fp32 inputs rounded to
+  // tf32 (relative error 2^-11 each, products exact in fp32) and summed by
+  // the MMA: |f_tc - f_32| <= 2^-10 sum|z_k x_k| + 2^-11 |x|^2 + accumulation
+  // (bounded here by 2^-16 of every term's magnitude), with
+  // sum|z_k x_k| <= |z32| |x~|max, |z32|^2 = 4 |z~|^2.  Safety factor 1.25.
+  const double sx = sqrt(4.0 * zt2 * fr.sqmax32);
+  const double h32 = (double)r.hi32;
+  const double etc = 1.25 * (9.765625e-04 * sx + 4.8828125e-04 * fr.sqmax32 +
+                             1.52587890625e-05 * (sx + fr.sqmax32 + fabs(h32)));
+  r.ctc = tf32_down(__double2float_rd(-(h32 + etc)));
 }
 
 template <int D>
@@ -661,6 +686,7 @@ __device__ __forceinline__ void init_padding_lane(RayState<D>& r) {
   r.thr = CUDART_INF;  // never needs a box
   r.thr32 = CUDART_INF_F;
   r.bsl32 = 0.0f;
+  r.ctc = 1e30f;  // never passes the tensor-core screen
 #pragma unroll
   for (int k = 0; k < D; ++k) r.u32[k] = 0.0f;
 #pragma unroll
@@ -1047,13 +1073,167 @@ __device__ __forceinline__ void screen_tile_remap(RayState<D>& r, const double* 
   if (hi) ray_rare_block<D, true>(r, tile64 + 32 * rec_stride(D), hi, gbase + 32, fr);
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core screen (d <= 6, one ray per lane): the incircle powers of the
+// warp's 32 rays against a 64-candidate tile are one 32 x 64 x 8 product
+//     f~ = [z32, 1, ctc] . [x~, |x~|^2, 1]  =  |x~|^2 - 2 z~.x~ - (hi32 + e_tc)
+// on the legacy warp tensor path (mma.sync m16n8k8 tf32: 2 ray blocks x 8
+// candidate blocks = 16 HMMA per tile, B fragments staged by TMA in fragment
+// order, 8 LDS.64).  A pair passes iff f~ < 0 (sign bit, incl. -0): ctc folds
+// the fp32 bound hi32 and the tf32 error bound into the product, so the
+// screen stays conservative (ray_set_best derives the bound).  The A
+// fragments are rebuilt through shared memory after sphere updates; a stale
+// sphere only screens more pairs (the band only shrinks), never fewer.
+// Passing pairs go through the same fp32 halfspace pre-filter and fp64 rare
+// path as screen_tile_pairs, so the verdicts are unchanged.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], float2 b) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%10,%10,%10,%10};"
+      : "=f"(c[0]), "=f"(c[1]), "=f"(c[2]), "=f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(__float_as_uint(b.x)),
+        "r"(__float_as_uint(b.y)), "f"(0.0f));
+}
+
+constexpr int MMA_AROW = 9;  // shared A-row stride in floats (odd: conflict-free column reads)
+
+// The A operand lives in shared memory (row r = ray of lane r:
+// [tf32(z32_r), 1, ctc_r, 0 ..]), rewritten after sphere updates; the
+// fragments are re-read per tile (8 LDS) instead of holding 8 registers.
+template <int D>
+__device__ __forceinline__ void mma_store_a(const RayState<D>& r, float* sA) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float v = k < D ? __uint_as_float(tf32_rn(r.z32[k])) : k == D ? 1.0f
+                  : k == D + 1 ? r.ctc : 0.0f;
+    sA[lane * MMA_AROW + k] = v;
+  }
+  __syncwarp();
+}
+
+// Halfspace operand (constant per ray): row r = [tf32(u32_r), 0, c2_r, 0 ..]
+// with h~ = u~.x~ + c2 > 0 whenever the fp32 pre-filter of screen_tile_pairs
+// (bsl32 + u32.x~ > thr32) could keep the candidate: c2 = bsl32 - thr32 + e_u
+// rounded up in tf32, e_u >= |u~.x~ (tf32 MMA) - u32.x~| (2^-10 |u||x~|max +
+// 2^-16 of the magnitudes, x 1.25).
+__device__ __forceinline__ float tf32_up(float v) { return -tf32_down(-v); }
+
+template <int D>
+__device__ __forceinline__ void mma_store_u(const RayState<D>& r, const Frame& fr, float* sU) {
+  const int lane = threadIdx.x & 31;
+  const double xm = sqrt(fr.sqmax32);
+  const double eu = 1.25 * (9.775161743164062e-04 * xm +
+                            1.52587890625e-05 * (xm + fabs((double)r.thr32) + 1.0));
+  double c2 = (double)r.bsl32 - (double)r.thr32 + eu;
+  c2 = fmin(fmax(c2, -1e30), 1e30);  // padding lanes (thr32 = +inf): finite
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float v = k < D ? __uint_as_float(tf32_rn(r.u32[k])) : k == D + 1
+                  ? tf32_up(__double2float_ru(c2)) : 0.0f;
+    sU[lane * MMA_AROW + k] = v;
+  }
+  __syncwarp();
+}
+
+// Fragments of rays 0-15 (a[0]) and 16-31 (a[1]): lane l holds
+// A[16m + g][t], A[16m + g + 8][t], A[16m + g][t + 4], A[16m + g + 8][t + 4],
+// g = l >> 2, t = l & 3.
+__device__ __forceinline__ void mma_load_a(const float* sA, uint32_t (&a)[2][4]) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    a[m][0] = __float_as_uint(sA[(16 * m + g) * MMA_AROW + t]);
+    a[m][1] = __float_as_uint(sA[(16 * m + g + 8) * MMA_AROW + t]);
+    a[m][2] = __float_as_uint(sA[(16 * m + g) * MMA_AROW + t + 4]);
+    a[m][3] = __float_as_uint(sA[(16 * m + g + 8) * MMA_AROW + t + 4]);
+  }
+}
+
+// Spread the 4 low bits of x to the even bit positions 0, 2, 4, 6.
+__device__ __forceinline__ uint32_t spread4(uint32_t x) {
+  x = (x | (x << 2)) & 0x33u;
+  return (x | (x << 1)) & 0x55u;
+}
+
+template <int D>
+__device__ __forceinline__ void screen_tile_mma(RayState<D>& r, const double* tile64,
+                                                const float* tileB, const float* tilep, int gbase,
+                                                const Frame& fr, WarpCounters* wc, float* sA,
+                                                const float* sU) {
+  constexpr int S = rec_stride(D);
+  constexpr int P2 = rec32p_stride(D);
+  const int lane = threadIdx.x & 31;
+  const float2* B = reinterpret_cast<const float2*>(tileB);
+  uint32_t a[2][4];
+  mma_load_a(sA, a);
+  uint32_t acc = 0u;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 b = B[j * 32 + lane];
+    float c0[4], c1[4];
+    mma_tf32(c0, a[0], b);
+    mma_tf32(c1, a[1], b);
+    acc |= __float_as_uint(c0[0]) | __float_as_uint(c0[1]) | __float_as_uint(c0[2]) |
+           __float_as_uint(c0[3]) | __float_as_uint(c1[0]) | __float_as_uint(c1[1]) |
+           __float_as_uint(c1[2]) | __float_as_uint(c1[3]);
+  }
+  if (!__any_sync(0xffffffffu, (int)acc < 0)) return;
+  // Some pair passed: recompute, add the halfspace product (the conservative
+  // pre-filter: most pairs inside a stale sphere lie behind the ray), and
+  // route each ray's 64 verdicts to its lane with ballots.  C element (m, e)
+  // of lane (g, t) is ray 16m + 8(e >> 1) + g, column 8j + 2t + (e & 1); ray
+  // r = lane reads bits 4g .. 4g+3 of the ballots of elements
+  // (r >> 4, 2((r >> 3) & 1) + {0, 1}).
+  uint32_t au[2][4];
+  mma_load_a(sU, au);
+  const int rm = lane >> 4, rh = (lane >> 3) & 1, sh = 4 * (lane & 7);
+  unsigned long long m = 0ull;
+#pragma unroll 1
+  for (int j = 0; j < 8; ++j) {
+    const float2 b = B[j * 32 + lane];
+    float c0[4], c1[4], h0[4], h1[4];
+    mma_tf32(c0, a[0], b);
+    mma_tf32(c1, a[1], b);
+    mma_tf32(h0, au[0], b);
+    mma_tf32(h1, au[1], b);
+    uint32_t v[2][4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[0][e] = __ballot_sync(0xffffffffu, (int)(__float_as_uint(c0[e]) & ~__float_as_uint(h0[e])) < 0);
+      v[1][e] = __ballot_sync(0xffffffffu, (int)(__float_as_uint(c1[e]) & ~__float_as_uint(h1[e])) < 0);
+    }
+    const uint32_t ev = rm ? (rh ? v[1][2] : v[1][0]) : (rh ? v[0][2] : v[0][0]);
+    const uint32_t od = rm ? (rh ? v[1][3] : v[1][1]) : (rh ? v[0][3] : v[0][1]);
+    const uint32_t byte = spread4((ev >> sh) & 0xfu) | (spread4((od >> sh) & 0xfu) << 1);
+    m |= (unsigned long long)byte << (8 * j);
+  }
+  const int rel = r.ib - gbase;  // the current best itself
+  if ((unsigned)rel < 64u) m &= ~(1ull << rel);
+  const unsigned long long keep = m;
+  if (wc) {
+    ++wc->rare_blocks;
+    wc->entries += __popcll(keep);
+    wc->rare_iters += __reduce_max_sync(0xffffffffu, (unsigned)__popcll(keep));
+  }
+  const int nupd0 = r.nupd;
+  const unsigned lo = (unsigned)keep, hi = (unsigned)(keep >> 32);
+  if (lo) ray_rare_block<D, true>(r, tile64, lo, gbase, fr);
+  if (hi) ray_rare_block<D, true>(r, tile64 + 32 * S, hi, gbase + 32, fr);
+  if (__any_sync(0xffffffffu, r.nupd != nupd0)) mma_store_a<D>(r, sA);
+}
+
 // One warp per CTA (warps finish at very different times; a freed slot is
 // refilled immediately).  The warp's next needed tile is fetched by TMA into
 // the other half of a two-tile shared-memory buffer while the current tile
 // is screened; the need test is re-applied before screening (spheres shrink).
-template <int D, int R, int PT, int PB, int MINB, bool F32, class Src>
+template <int D, int R, int PT, int PB, int MINB, bool F32, class Src, bool MMA = false>
 __global__ void __launch_bounds__(32, MINB)
     k_raycast_pruned(Src src, const double* __restrict__ crec, const float* __restrict__ crec32,
+                     const float* __restrict__ crecB,
                      const int32_t* __restrict__ perm, const int32_t* __restrict__ inv_perm,
                      int64_t n_cand, const double* __restrict__ tile_box,
                      const float* __restrict__ tile_box32, const double* __restrict__ node_box,
@@ -1074,6 +1254,11 @@ __global__ void __launch_bounds__(32, MINB)
   static_assert(PT % 8 == 0 && VR_REC_PAD % PT == 0, "tile must divide the record padding");
   __shared__ __align__(128) double buf[2][STAGE64 ? PT * S : 2];
   __shared__ __align__(128) float buf32[2][F32 ? PT / 2 * P2 : 4];
+  static_assert(!MMA || (F32 && R == 1 && PT == 64 && D <= 6), "tensor-core screen shape");
+  constexpr uint32_t BYTESB = MMA ? (uint32_t)(PT * 8 * sizeof(float)) : 0u;
+  __shared__ __align__(128) float bufB[2][MMA ? PT * 8 : 4];
+  __shared__ float sA[MMA ? 32 * MMA_AROW : 1];
+  __shared__ float sU[MMA ? 32 * MMA_AROW : 1];
   __shared__ uint64_t bar[2];
   const int lane = threadIdx.x;
   if (lane == 0) {
@@ -1105,13 +1290,18 @@ __global__ void __launch_bounds__(32, MINB)
   seed_tile<D, R, PT, F32>(ray, crec + st * PT * S, (int)(st * PT), fr);
   TreeCursor<D, R, F32> cur;
   cur.init(st, ray, node_box, node_box32, node_range);
+  if constexpr (MMA) {
+    mma_store_a<D>(ray[0], sA);
+    mma_store_u<D>(ray[0], fr, sU);
+  }
 
   auto issue = [&](int64_t t, int b) {
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect_tx(&bar[b], BYTES64 + BYTES32);
+      mbar_arrive_expect_tx(&bar[b], BYTES64 + BYTES32 + BYTESB);
       if constexpr (STAGE64) bulk_g2s(buf[b], crec + t * PT * S, BYTES64, &bar[b]);
       if constexpr (F32) bulk_g2s(buf32[b], crec32 + t * (PT / 2) * P2, BYTES32, &bar[b]);
+      if constexpr (MMA) bulk_g2s(bufB[b], crecB + t * PT * 8, BYTESB, &bar[b]);
     }
   };
   unsigned long long tiles_done = 0;
@@ -1130,7 +1320,10 @@ __global__ void __launch_bounds__(32, MINB)
     // (no re-test of the tile box here: the leaf was tested when its parent
     // was expanded, and re-testing skipped < 2% of the tiles on config 2)
     ++tiles_done;
-    if constexpr (F32 && R == 1 && (PT == 32 || PT == 64) && remap_max<D>() > 0) {
+    if constexpr (MMA) {
+      screen_tile_mma<D>(ray[0], crec + t * PT * S, bufB[b], buf32[b], (int)(t * PT), fr,
+                         work ? &wc : nullptr, sA, sU);
+    } else if constexpr (F32 && R == 1 && (PT == 32 || PT == 64) && remap_max<D>() > 0) {
       if (__popc(tmask) <= remap_max<D>())
         screen_tile_remap<D, PT>(ray[0], STAGE64 ? buf[b] : crec + t * PT * S, buf32[b],
                                  (int)(t * PT), tmask, fr, work ? &wc : nullptr);
@@ -1708,6 +1901,7 @@ struct PrunedIndex {
   const int2* node_range;  // [first tile, last tile + 1) per node
   int64_t n;
   WideTree wide;           // 32-ary tree over the tiles (cooperative kernel)
+  const float* crecB;      // tensor-core screen operand (nullable, d <= 6)
 };
 
 #ifdef VR_PRUNE_TILE_OVERRIDE  // tuning builds only (the Python index must match: VR_PRUNE_TILE)
@@ -1717,12 +1911,12 @@ constexpr int PRUNE_TILE = 64;
 #endif
 constexpr int PRUNE_BLOCK = 32;
 
-template <int D, int R, int MINB, bool F32, class Src>
+template <int D, int R, int MINB, bool F32, class Src, bool MMA = false>
 int launch_pruned_rm(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
                      const RayOut& out, cudaStream_t st, unsigned long long* work) {
   const int64_t per_block = 32 * R;
   const int64_t items = (n_rays + per_block - 1) / per_block;
-  auto kern = k_raycast_pruned<D, R, PRUNE_TILE, PRUNE_BLOCK, MINB, F32, Src>;
+  auto kern = k_raycast_pruned<D, R, PRUNE_TILE, PRUNE_BLOCK, MINB, F32, Src, MMA>;
   unsigned long long* next_item = nullptr;
   int64_t grid = items;
 #ifdef VR_PERSISTENT
@@ -1741,7 +1935,7 @@ int launch_pruned_rm(const Src& src, int64_t n_rays, const PrunedIndex& ix, cons
     grid = slots;
   }
 #endif
-  kern<<<(unsigned)grid, 32, 0, st>>>(src, ix.crec, ix.crec32, ix.perm, ix.inv_perm, ix.n,
+  kern<<<(unsigned)grid, 32, 0, st>>>(src, ix.crec, ix.crec32, ix.crecB, ix.perm, ix.inv_perm, ix.n,
                                       ix.tile_box, ix.tile_box32, ix.node_box, ix.node_box32,
                                       ix.node_range, fr, out, work, next_item);
   cudaError_t le = cudaGetLastError();
@@ -1750,6 +1944,7 @@ int launch_pruned_rm(const Src& src, int64_t n_rays, const PrunedIndex& ix, cons
 }
 
 int raycast_variant();
+int mma_mode();  // VR_MMA=0 disables the tensor-core screen (A/B runs)
 
 template <int D, bool F32, class Src>
 int launch_pruned_f(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
@@ -1770,6 +1965,15 @@ int launch_pruned_f(const Src& src, int64_t n_rays, const PrunedIndex& ix, const
 #else
   constexpr int MINB = (D <= 3) ? 24 : (D <= 4 ? 20 : (D <= 6 ? 16 : 12));
 #endif
+#ifdef VR_MMA_MINB
+  constexpr int MMA_MINB = VR_MMA_MINB;
+#else
+  constexpr int MMA_MINB = MINB;
+#endif
+  if constexpr (F32 && D <= 6 && PRUNE_TILE == 64) {
+    if (ix.crecB && mma_mode() != 0)
+      return launch_pruned_rm<D, 1, MMA_MINB, F32, Src, true>(src, n_rays, ix, fr, out, st, work);
+  }
   return launch_pruned_rm<D, 1, MINB, F32>(src, n_rays, ix, fr, out, st, work);
 }
 
@@ -1794,6 +1998,7 @@ inline PrunedIndex pruned_index_from(const vr_prune_index* ix, bool f32) {
   PrunedIndex pi{ix->rec, f32 ? ix->rec32 : nullptr, ix->perm, ix->inv_perm, ix->tile_box,
                  ix->tile_box32, ix->node_box, ix->node_box32,
                  reinterpret_cast<const int2*>(ix->node_range), ix->n, WideTree{}};
+  pi.crecB = f32 ? ix->recB : nullptr;
   pi.wide.box32 = ix->wide_box32;
   pi.wide.levels = ix->wide_levels;
   for (int l = 0; l < WIDE_MAX_LEVELS; ++l) {
