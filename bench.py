@@ -369,6 +369,9 @@ def run_ours(args):
                 "rare_blocks_per_warp": wk[1] / n_warps,
                 "rare_iters_per_warp": wk[2] / n_warps,
                 "rare_entries_per_ray": wk[3] / n, "sphere_updates_per_ray": wk[4] / n}
+    if any(wk[6:11]):  # VR_RARE_STATS builds: rare-path entry outcomes per ray
+        counters["rare_outcomes_per_ray"] = dict(zip(
+            ("outside", "self", "behind", "band", "improves"), [v / n for v in wk[6:11]]))
     # the exhaustive (TMA-staged, unpruned) kernel on the same rays, for its
     # roofline: fp64 screen (FP64 pipe) and fp32 screen (FP32 pipe)
     ex_ms = {}
@@ -450,7 +453,7 @@ def run_ours(args):
                          "kernel_ms": kms, "flop_per_pair": FLOP_PER_PAIR,
                          "pairs_per_launch": pairs, "pairs_per_ray": pairs / n,
                          "work_counters": counters if args.mode == "pruned" else None,
-                         "screen": ("tensor-core (mma.sync tf32) + fp32 pre-filter + fp64 rare path"
+                         "screen": ("tensor-core (mma.sync tf32: sphere + halfspace products) + fp64 rare path"
                                     if os.environ.get("VR_MMA", "1") != "0"
                                     else "packed FFMA2 fp32 + fp64 rare path"),
                          "unit_of_work": "(ray, generator) pair screened; pruned kernel counts "

@@ -60,6 +60,7 @@ struct RayState {
   float rb32;   // (rho^2 + dlt) rounded up with the fp32 sum slack (+inf: none)
   float ctc;    // tensor-core screen constant: -(hi32 + tf32 error bound), tf32, rounded down
   int ib;       // current best (local candidate index), -1 = none
+  int gk;       // local index of the reference generator g (never valid: u.x_g <= thr), -1 = unknown
   int near;     // 1 -> needs exact re-check
   int nupd;     // sphere updates (work accounting)
 #ifdef VR_RARE_STATS
@@ -139,6 +140,7 @@ __device__ __forceinline__ void ray_setup(RayState<D>& r, const double* __restri
   r.del32 = 0.0f;
   r.rb32 = CUDART_INF_F;
   r.ctc = -1e20f;  // no sphere yet: every real candidate passes the tensor-core screen
+  r.gk = -1;
 }
 
 // Move the screening sphere to the new best crossing t.
@@ -687,6 +689,8 @@ __device__ __forceinline__ void init_padding_lane(RayState<D>& r) {
   r.thr32 = CUDART_INF_F;
   r.bsl32 = 0.0f;
   r.ctc = 1e30f;  // never passes the tensor-core screen
+  r.ib = -1;
+  r.gk = -1;
 #pragma unroll
   for (int k = 0; k < D; ++k) r.u32[k] = 0.0f;
 #pragma unroll
@@ -1161,11 +1165,10 @@ __device__ __forceinline__ uint32_t spread4(uint32_t x) {
 
 template <int D>
 __device__ __forceinline__ void screen_tile_mma(RayState<D>& r, const double* tile64,
-                                                const float* tileB, const float* tilep, int gbase,
+                                                const float* tileB, int gbase,
                                                 const Frame& fr, WarpCounters* wc, float* sA,
                                                 const float* sU) {
   constexpr int S = rec_stride(D);
-  constexpr int P2 = rec32p_stride(D);
   const int lane = threadIdx.x & 31;
   const float2* B = reinterpret_cast<const float2*>(tileB);
   uint32_t a[2][4];
@@ -1213,6 +1216,11 @@ __device__ __forceinline__ void screen_tile_mma(RayState<D>& r, const double* ti
   }
   const int rel = r.ib - gbase;  // the current best itself
   if ((unsigned)rel < 64u) m &= ~(1ull << rel);
+  // g lies on every sphere of the ray (power 0) and on the halfspace boundary
+  // (u.x_g = s < thr), so both products always pass it; it is never valid
+  // (raycast.py:110-117), so dropping it is exact.
+  const int relg = r.gk - gbase;
+  if ((unsigned)relg < 64u) m &= ~(1ull << relg);
   const unsigned long long keep = m;
   if (wc) {
     ++wc->rare_blocks;
@@ -1250,10 +1258,12 @@ __global__ void __launch_bounds__(32, MINB)
 #endif
   constexpr uint32_t BYTES64 = STAGE64 ? (uint32_t)(PT * S * sizeof(double)) : 0u;
   constexpr int P2 = rec32p_stride(D);
-  constexpr uint32_t BYTES32 = F32 ? (uint32_t)(PT / 2 * P2 * sizeof(float)) : 0u;
+  // the tensor-core screen needs neither the fp32 pair rows nor the fp64 rows
+  // in shared memory (its halfspace product replaces the pair pre-filter)
+  constexpr uint32_t BYTES32 = F32 && !MMA ? (uint32_t)(PT / 2 * P2 * sizeof(float)) : 0u;
   static_assert(PT % 8 == 0 && VR_REC_PAD % PT == 0, "tile must divide the record padding");
   __shared__ __align__(128) double buf[2][STAGE64 ? PT * S : 2];
-  __shared__ __align__(128) float buf32[2][F32 ? PT / 2 * P2 : 4];
+  __shared__ __align__(128) float buf32[2][F32 && !MMA ? PT / 2 * P2 : 4];
   static_assert(!MMA || (F32 && R == 1 && PT == 64 && D <= 6), "tensor-core screen shape");
   constexpr uint32_t BYTESB = MMA ? (uint32_t)(PT * 8 * sizeof(float)) : 0u;
   __shared__ __align__(128) float bufB[2][MMA ? PT * 8 : 4];
@@ -1284,6 +1294,11 @@ __global__ void __launch_bounds__(32, MINB)
     act[j] = src.load(k0 + (int64_t)j * 32, ray[j], fr);
     if (!act[j]) init_padding_lane<D, R>(ray[j]);
   }
+  if constexpr (MMA) {
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (act[j]) ray[j].gk = inv_perm[src.gen(k0 + (int64_t)j * 32)];
+  }
   int64_t st = 0;
   if (lane == 0) st = inv_perm[src.gen(k0)] / PT;
   st = __shfl_sync(0xffffffffu, st, 0);
@@ -1300,7 +1315,7 @@ __global__ void __launch_bounds__(32, MINB)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive_expect_tx(&bar[b], BYTES64 + BYTES32 + BYTESB);
       if constexpr (STAGE64) bulk_g2s(buf[b], crec + t * PT * S, BYTES64, &bar[b]);
-      if constexpr (F32) bulk_g2s(buf32[b], crec32 + t * (PT / 2) * P2, BYTES32, &bar[b]);
+      if constexpr (F32 && !MMA) bulk_g2s(buf32[b], crec32 + t * (PT / 2) * P2, BYTES32, &bar[b]);
       if constexpr (MMA) bulk_g2s(bufB[b], crecB + t * PT * 8, BYTESB, &bar[b]);
     }
   };
@@ -1321,7 +1336,7 @@ __global__ void __launch_bounds__(32, MINB)
     // was expanded, and re-testing skipped < 2% of the tiles on config 2)
     ++tiles_done;
     if constexpr (MMA) {
-      screen_tile_mma<D>(ray[0], crec + t * PT * S, bufB[b], buf32[b], (int)(t * PT), fr,
+      screen_tile_mma<D>(ray[0], crec + t * PT * S, bufB[b], (int)(t * PT), fr,
                          work ? &wc : nullptr, sA, sU);
     } else if constexpr (F32 && R == 1 && (PT == 32 || PT == 64) && remap_max<D>() > 0) {
       if (__popc(tmask) <= remap_max<D>())
