@@ -247,7 +247,7 @@ def extra_configs(vb, torch, world, rank):
     ns4 = vb.NodeSet(pts4)
     ns4.prune_index()
     cells = np.arange(100000)
-    parallel.mc_cells_sharded(ns4, cells[:2000], 1000, seed=0)  # warm
+    parallel.mc_cells_sharded(ns4, cells, 1000, seed=0)  # warm (allocator growth at full size)
     w4 = torch.zeros(16, dtype=torch.int64, device="cuda")
     torch.cuda.synchronize()
     t0 = time.perf_counter()

@@ -103,11 +103,12 @@ int vr_pack_records32_pairs(const float* rec32, int64_t rows, int d, float* out,
                             void* stream);
 
 /* fp32 centred records (vr_pack_records32 layout) -> the tensor-core screen
- * operand of the pruned kernel (vr_prune_index.recB), d <= 6: per tile of 64
- * rows, 8 column blocks of 8 candidates, each 32 lanes x 2 tf32 values, lane l
- * holding features (l & 3) and (l & 3) + 4 of candidate 8 * block + (l >> 2),
- * features [x_0 .. x_{d-1}, |x|^2, 1, 0 ..] (sentinel |x|^2 -> 1e30).  `out`
- * holds rows * 8 floats; rows must be a multiple of 64. */
+ * operand of the pruned kernel (vr_prune_index.recB): features
+ * [x_0 .. x_{d-1}, |x|^2, 1, 0 ..] (sentinel |x|^2 -> 1e30) in KS = ceil((d+2)/8)
+ * k-steps of 8; per tile of 64 rows, 8 blocks of 8 candidates, per block KS
+ * steps of 32 lanes x 2 tf32 values, lane l holding features 8s + (l & 3) and
+ * 8s + (l & 3) + 4 of candidate 8 * block + (l >> 2).  `out` holds
+ * rows * 8 * KS floats; rows must be a multiple of 64. */
 int vr_pack_records_mma(const float* rec32, int64_t rows, int d, float* out, void* stream);
 
 /* Batched incircle RayCast (reference raycast_incircle, raycast.py:154-224,
@@ -174,7 +175,7 @@ typedef struct vr_prune_index {
   int32_t wide_levels;
   int64_t wide_off[8];
   int64_t wide_cnt[8];
-  /* Tensor-core screen operand (vr_pack_records_mma, d <= 6): the rec32 rows
+  /* Tensor-core screen operand (vr_pack_records_mma): the rec32 rows
    * in mma.sync m16n8k8 B-fragment order, tf32-rounded.  Nullable: without it
    * the pruned kernel screens with packed FFMA2 on rec32. */
   const float* recB;

@@ -387,10 +387,11 @@ class PruneIndex:
         self.wide_cnt = [int(b.shape[0]) for b in boxes]
         self.wide_off = np.concatenate([[0], np.cumsum(self.wide_cnt)[:-1]]).astype(np.int64).tolist()
         self.wide_box32 = torch.cat(boxes).contiguous()
-        # tensor-core screen operand (d <= 6): rec32 rows in mma B-fragment order
+        # tensor-core screen operand (used from d = 5): rec32 rows in mma B-fragment order
         self.recB = None
-        if d <= 6 and PRUNE_TILE == 64 and os.environ.get("VR_MMA", "1") != "0":
-            self.recB = torch.empty((rows, 8), dtype=torch.float32, device=dev)
+        if PRUNE_TILE == 64 and d >= 5 and os.environ.get("VR_MMA", "1") != "0":
+            ks = (d + 2 + 7) // 8
+            self.recB = torch.empty((rows, 8 * ks), dtype=torch.float32, device=dev)
             L = _lib.lib()
             _lib.check(L.vr_pack_records_mma(_lib.ptr(self.screen32.rec), rows, d,
                                              _lib.ptr(self.recB), _lib.stream_handle()),

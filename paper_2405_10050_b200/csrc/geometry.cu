@@ -226,20 +226,23 @@ __global__ void k_pairs32(const float* __restrict__ rec32, int64_t rows, float* 
 }
 
 // fp32 records -> mma.sync m16n8k8 B fragments (tf32, round to nearest):
-// thread (tile, block, lane) writes the two values lane l of block j needs.
+// thread (tile, block, k-step, lane) writes the two values lane l of that
+// block and k-step needs; KS = ceil((D + 2) / 8) k8 steps.
 template <int D>
 __global__ void k_pack_mma(const float* __restrict__ rec32, int64_t rows, float* __restrict__ out) {
-  static_assert(D + 2 <= 8, "one k8 step holds [x, |x|^2, 1]");
+  constexpr int KS = (D + 2 + 7) / 8;
   constexpr int S32 = rec32_stride(D);
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < rows * 4;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < rows * 4 * KS;
        q += (int64_t)gridDim.x * blockDim.x) {
     const int lane = (int)(q & 31);
-    const int64_t row = (q >> 5) * 8 + (lane >> 2);  // (tile * 8 + block) * 8 + group
+    const int step = (int)((q >> 5) % KS);
+    const int64_t blk = (q >> 5) / KS;                 // tile * 8 + block
+    const int64_t row = blk * 8 + (lane >> 2);
     const float* a = rec32 + row * S32;
     float v[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int k = (lane & 3) + 4 * h;
+      const int k = 8 * step + (lane & 3) + 4 * h;
       float f = k < D ? a[k] : (k == D ? a[D] : (k == D + 1 ? 1.0f : 0.0f));
       if (k == D && isinf(f)) f = 1e30f;  // sentinel: never passes (finite, no inf - inf)
       uint32_t t;
@@ -294,16 +297,11 @@ extern "C" int vr_pack_records32_pairs(const float* rec32, int64_t rows, int d, 
 extern "C" int vr_pack_records_mma(const float* rec32, int64_t rows, int d, float* out,
                                    void* stream) {
   if (!rec32 || !out || rows <= 0 || (rows & 63)) return VR_EINVAL;
-  if (d > 6) return VR_EDIM;
-  const unsigned nbk = blocks_for(rows * 4, 256) < 4096 ? blocks_for(rows * 4, 256) : 4096;
-  switch (d) {
-    case 2: k_pack_mma<2><<<nbk, 256, 0, as_stream(stream)>>>(rec32, rows, out); break;
-    case 3: k_pack_mma<3><<<nbk, 256, 0, as_stream(stream)>>>(rec32, rows, out); break;
-    case 4: k_pack_mma<4><<<nbk, 256, 0, as_stream(stream)>>>(rec32, rows, out); break;
-    case 5: k_pack_mma<5><<<nbk, 256, 0, as_stream(stream)>>>(rec32, rows, out); break;
-    case 6: k_pack_mma<6><<<nbk, 256, 0, as_stream(stream)>>>(rec32, rows, out); break;
-    default: return VR_EDIM;
-  }
+  const int64_t n2 = rows * 4 * ((d + 2 + 7) / 8);
+  const unsigned nbk = blocks_for(n2, 256) < 4096 ? blocks_for(n2, 256) : 4096;
+  VR_DISPATCH_D(d, {
+    k_pack_mma<D><<<nbk, 256, 0, as_stream(stream)>>>(rec32, rows, out);
+  });
   VR_RETURN_LAUNCH();
 }
 

@@ -1078,8 +1078,8 @@ __device__ __forceinline__ void screen_tile_remap(RayState<D>& r, const double* 
 }
 
 // ---------------------------------------------------------------------------
-// Tensor-core screen (d <= 6, one ray per lane): the incircle powers of the
-// warp's 32 rays against a 64-candidate tile are one 32 x 64 x 8 product
+// Tensor-core screen (one ray per lane): the incircle powers of the
+// warp's 32 rays against a 64-candidate tile are one 32 x 64 x 8KS product
 //     f~ = [z32, 1, ctc] . [x~, |x~|^2, 1]  =  |x~|^2 - 2 z~.x~ - (hi32 + e_tc)
 // on the legacy warp tensor path (mma.sync m16n8k8 tf32: 2 ray blocks x 8
 // candidate blocks = 16 HMMA per tile, B fragments staged by TMA in fragment
@@ -1099,20 +1099,32 @@ __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], 
         "r"(__float_as_uint(b.y)), "f"(0.0f));
 }
 
-constexpr int MMA_AROW = 9;  // shared A-row stride in floats (odd: conflict-free column reads)
+__device__ __forceinline__ void mma_tf32_acc(float (&c)[4], const uint32_t (&a)[4], float2 b) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(__float_as_uint(b.x)),
+        "r"(__float_as_uint(b.y)));
+}
+
+// k8 steps of the screen product: features [x (D), |x|^2, 1] padded to 8 KS.
+__host__ __device__ constexpr int mma_ksteps(int d) { return (d + 2 + 7) / 8; }
+// shared A-row stride in floats (odd: conflict-free column reads)
+__host__ __device__ constexpr int mma_arow(int d) { return 8 * mma_ksteps(d) + 1; }
 
 // The A operand lives in shared memory (row r = ray of lane r:
 // [tf32(z32_r), 1, ctc_r, 0 ..]), rewritten after sphere updates; the
-// fragments are re-read per tile (8 LDS) instead of holding 8 registers.
+// fragments are re-read per tile (8 KS LDS) instead of holding registers.
 template <int D>
 __device__ __forceinline__ void mma_store_a(const RayState<D>& r, float* sA) {
+  constexpr int KW = 8 * mma_ksteps(D), AR = mma_arow(D);
   const int lane = threadIdx.x & 31;
   __syncwarp();
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < KW; ++k) {
     const float v = k < D ? __uint_as_float(tf32_rn(r.z32[k])) : k == D ? 1.0f
                   : k == D + 1 ? r.ctc : 0.0f;
-    sA[lane * MMA_AROW + k] = v;
+    sA[lane * AR + k] = v;
   }
   __syncwarp();
 }
@@ -1126,6 +1138,7 @@ __device__ __forceinline__ float tf32_up(float v) { return -tf32_down(-v); }
 
 template <int D>
 __device__ __forceinline__ void mma_store_u(const RayState<D>& r, const Frame& fr, float* sU) {
+  constexpr int KW = 8 * mma_ksteps(D), AR = mma_arow(D);
   const int lane = threadIdx.x & 31;
   const double xm = sqrt(fr.sqmax32);
   const double eu = 1.25 * (9.775161743164062e-04 * xm +
@@ -1134,27 +1147,41 @@ __device__ __forceinline__ void mma_store_u(const RayState<D>& r, const Frame& f
   c2 = fmin(fmax(c2, -1e30), 1e30);  // padding lanes (thr32 = +inf): finite
   __syncwarp();
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < KW; ++k) {
     const float v = k < D ? __uint_as_float(tf32_rn(r.u32[k])) : k == D + 1
                   ? tf32_up(__double2float_ru(c2)) : 0.0f;
-    sU[lane * MMA_AROW + k] = v;
+    sU[lane * AR + k] = v;
   }
   __syncwarp();
 }
 
-// Fragments of rays 0-15 (a[0]) and 16-31 (a[1]): lane l holds
-// A[16m + g][t], A[16m + g + 8][t], A[16m + g][t + 4], A[16m + g + 8][t + 4],
-// g = l >> 2, t = l & 3.
-__device__ __forceinline__ void mma_load_a(const float* sA, uint32_t (&a)[2][4]) {
+// Fragments of rays 0-15 (a[s][0]) and 16-31 (a[s][1]) for k-step s: lane l
+// holds A[16m + g][8s + t], A[16m + g + 8][8s + t], A[16m + g][8s + t + 4],
+// A[16m + g + 8][8s + t + 4], g = l >> 2, t = l & 3.
+template <int D>
+__device__ __forceinline__ void mma_load_a(const float* sA, uint32_t (&a)[mma_ksteps(D)][2][4]) {
+  constexpr int AR = mma_arow(D);
   const int lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-  for (int m = 0; m < 2; ++m) {
-    a[m][0] = __float_as_uint(sA[(16 * m + g) * MMA_AROW + t]);
-    a[m][1] = __float_as_uint(sA[(16 * m + g + 8) * MMA_AROW + t]);
-    a[m][2] = __float_as_uint(sA[(16 * m + g) * MMA_AROW + t + 4]);
-    a[m][3] = __float_as_uint(sA[(16 * m + g + 8) * MMA_AROW + t + 4]);
-  }
+  for (int q = 0; q < mma_ksteps(D); ++q)
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      a[q][m][0] = __float_as_uint(sA[(16 * m + g) * AR + 8 * q + t]);
+      a[q][m][1] = __float_as_uint(sA[(16 * m + g + 8) * AR + 8 * q + t]);
+      a[q][m][2] = __float_as_uint(sA[(16 * m + g) * AR + 8 * q + t + 4]);
+      a[q][m][3] = __float_as_uint(sA[(16 * m + g + 8) * AR + 8 * q + t + 4]);
+    }
+}
+
+// C (rays 16m .. 16m+15, candidates 8j .. 8j+7) of the screen product.
+template <int KS>
+__device__ __forceinline__ void mma_block(float (&c)[4], const uint32_t (&a)[KS][2][4], int m,
+                                          const float2* Bj) {
+  const int lane = threadIdx.x & 31;
+  mma_tf32(c, a[0][m], Bj[lane]);
+#pragma unroll
+  for (int q = 1; q < KS; ++q) mma_tf32_acc(c, a[q][m], Bj[q * 32 + lane]);
 }
 
 // Spread the 4 low bits of x to the even bit positions 0, 2, 4, 6.
@@ -1169,17 +1196,17 @@ __device__ __forceinline__ void screen_tile_mma(RayState<D>& r, const double* ti
                                                 const Frame& fr, WarpCounters* wc, float* sA,
                                                 const float* sU) {
   constexpr int S = rec_stride(D);
+  constexpr int KS = mma_ksteps(D);
   const int lane = threadIdx.x & 31;
-  const float2* B = reinterpret_cast<const float2*>(tileB);
-  uint32_t a[2][4];
-  mma_load_a(sA, a);
+  const float2* B = reinterpret_cast<const float2*>(tileB);  // [8 blocks][KS][32 lanes]
+  uint32_t a[KS][2][4];
+  mma_load_a<D>(sA, a);
   uint32_t acc = 0u;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const float2 b = B[j * 32 + lane];
     float c0[4], c1[4];
-    mma_tf32(c0, a[0], b);
-    mma_tf32(c1, a[1], b);
+    mma_block<KS>(c0, a, 0, B + j * KS * 32);
+    mma_block<KS>(c1, a, 1, B + j * KS * 32);
     acc |= __float_as_uint(c0[0]) | __float_as_uint(c0[1]) | __float_as_uint(c0[2]) |
            __float_as_uint(c0[3]) | __float_as_uint(c1[0]) | __float_as_uint(c1[1]) |
            __float_as_uint(c1[2]) | __float_as_uint(c1[3]);
@@ -1191,18 +1218,17 @@ __device__ __forceinline__ void screen_tile_mma(RayState<D>& r, const double* ti
   // of lane (g, t) is ray 16m + 8(e >> 1) + g, column 8j + 2t + (e & 1); ray
   // r = lane reads bits 4g .. 4g+3 of the ballots of elements
   // (r >> 4, 2((r >> 3) & 1) + {0, 1}).
-  uint32_t au[2][4];
-  mma_load_a(sU, au);
+  uint32_t au[KS][2][4];
+  mma_load_a<D>(sU, au);
   const int rm = lane >> 4, rh = (lane >> 3) & 1, sh = 4 * (lane & 7);
   unsigned long long m = 0ull;
 #pragma unroll 1
   for (int j = 0; j < 8; ++j) {
-    const float2 b = B[j * 32 + lane];
     float c0[4], c1[4], h0[4], h1[4];
-    mma_tf32(c0, a[0], b);
-    mma_tf32(c1, a[1], b);
-    mma_tf32(h0, au[0], b);
-    mma_tf32(h1, au[1], b);
+    mma_block<KS>(c0, a, 0, B + j * KS * 32);
+    mma_block<KS>(c1, a, 1, B + j * KS * 32);
+    mma_block<KS>(h0, au, 0, B + j * KS * 32);
+    mma_block<KS>(h1, au, 1, B + j * KS * 32);
     uint32_t v[2][4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -1260,15 +1286,18 @@ __global__ void __launch_bounds__(32, MINB)
   constexpr int P2 = rec32p_stride(D);
   // the tensor-core screen needs neither the fp32 pair rows nor the fp64 rows
   // in shared memory (its halfspace product replaces the pair pre-filter)
+  // (for d >= 7 it also replaces the remapped screen of sparse tiles: a
+  // remap/tensor-core hybrid measured slower on config 5, 1.60 vs 1.32 s)
   constexpr uint32_t BYTES32 = F32 && !MMA ? (uint32_t)(PT / 2 * P2 * sizeof(float)) : 0u;
   static_assert(PT % 8 == 0 && VR_REC_PAD % PT == 0, "tile must divide the record padding");
   __shared__ __align__(128) double buf[2][STAGE64 ? PT * S : 2];
   __shared__ __align__(128) float buf32[2][F32 && !MMA ? PT / 2 * P2 : 4];
-  static_assert(!MMA || (F32 && R == 1 && PT == 64 && D <= 6), "tensor-core screen shape");
-  constexpr uint32_t BYTESB = MMA ? (uint32_t)(PT * 8 * sizeof(float)) : 0u;
-  __shared__ __align__(128) float bufB[2][MMA ? PT * 8 : 4];
-  __shared__ float sA[MMA ? 32 * MMA_AROW : 1];
-  __shared__ float sU[MMA ? 32 * MMA_AROW : 1];
+  static_assert(!MMA || (F32 && R == 1 && PT == 64), "tensor-core screen shape");
+  constexpr int KW = 8 * mma_ksteps(D);
+  constexpr uint32_t BYTESB = MMA ? (uint32_t)(PT * KW * sizeof(float)) : 0u;
+  __shared__ __align__(128) float bufB[2][MMA ? PT * KW : 4];
+  __shared__ float sA[MMA ? 32 * mma_arow(D) : 1];
+  __shared__ float sU[MMA ? 32 * mma_arow(D) : 1];
   __shared__ uint64_t bar[2];
   const int lane = threadIdx.x;
   if (lane == 0) {
@@ -1316,7 +1345,7 @@ __global__ void __launch_bounds__(32, MINB)
       mbar_arrive_expect_tx(&bar[b], BYTES64 + BYTES32 + BYTESB);
       if constexpr (STAGE64) bulk_g2s(buf[b], crec + t * PT * S, BYTES64, &bar[b]);
       if constexpr (F32 && !MMA) bulk_g2s(buf32[b], crec32 + t * (PT / 2) * P2, BYTES32, &bar[b]);
-      if constexpr (MMA) bulk_g2s(bufB[b], crecB + t * PT * 8, BYTESB, &bar[b]);
+      if constexpr (MMA) bulk_g2s(bufB[b], crecB + t * PT * KW, BYTESB, &bar[b]);
     }
   };
   unsigned long long tiles_done = 0;
@@ -1985,7 +2014,9 @@ int launch_pruned_f(const Src& src, int64_t n_rays, const PrunedIndex& ix, const
 #else
   constexpr int MMA_MINB = MINB;
 #endif
-  if constexpr (F32 && D <= 6 && PRUNE_TILE == 64) {
+  // tensor-core screen from d = 5 (config 4, d = 4: 0.126 vs 0.118 s with
+  // the packed-FFMA2 screen, whose cost scales with d)
+  if constexpr (F32 && PRUNE_TILE == 64 && D >= 5) {
     if (ix.crecB && mma_mode() != 0)
       return launch_pruned_rm<D, 1, MMA_MINB, F32, Src, true>(src, n_rays, ix, fr, out, st, work);
   }

@@ -396,3 +396,78 @@ def test_fp32_screen_robust_to_scale(case):
     got = a[0][:300]
     ok = a[3][:300] != 3
     assert np.array_equal(got[ok], want[ok])
+
+
+def _tf32_rna(a):
+    """cvt.rna.tf32.f32 restated in numpy: keep 10 explicit mantissa bits,
+    round to nearest, ties away from zero."""
+    b = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = ((b + 0x1000) & ~np.uint64(0x1FFF)).astype(np.uint32)
+    return r.view(np.float32)
+
+
+@pytest.mark.parametrize("d", [5, 6, 8])
+def test_pack_records_mma_layout(d):
+    """vr_pack_records_mma writes the rec32 features [x~, |x~|^2, 1, 0..]
+    (sentinel |x~|^2 -> 1e30), tf32-rounded, in mma.sync m16n8k8 B-fragment
+    order: [tile][block of 8][k-step][lane][2], lane l holding features
+    8s + (l & 3) and 8s + (l & 3) + 4 of candidate 8 * block + (l >> 2)."""
+    pts = np.random.default_rng(40 + d).standard_normal((1000, d))
+    ns = vb.NodeSet(pts)
+    ix = ns.prune_index()
+    rec32 = ix.screen32.rec.cpu().numpy()
+    rows = rec32.shape[0]
+    ks = (d + 2 + 7) // 8
+    feat = np.zeros((rows, 8 * ks), dtype=np.float32)
+    feat[:, :d] = rec32[:, :d]
+    sq = rec32[:, d].copy()
+    sq[np.isinf(sq)] = 1e30
+    feat[:, d] = sq
+    feat[:, d + 1] = 1.0
+    feat = _tf32_rna(feat)
+    lane = np.arange(32)
+    want = np.empty((rows // 64, 8, ks, 32, 2), dtype=np.float32)
+    for s in range(ks):
+        for blk in range(8):
+            cand = np.arange(rows // 64)[:, None] * 64 + 8 * blk + (lane >> 2)[None, :]
+            want[:, blk, s, :, 0] = feat[cand, 8 * s + (lane & 3)]
+            want[:, blk, s, :, 1] = feat[cand, 8 * s + (lane & 3) + 4]
+    got = ix.recB.cpu().numpy().reshape(want.shape)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+_MMA_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2405_10050_b200 as vb
+out = []
+for n, d, seed in ((20000, 6, 0), (30000, 8, 1), (8000, 5, 2)):
+    pts = np.random.default_rng(seed).random((n, d))
+    ns = vb.NodeSet(pts)
+    rng = np.random.default_rng(seed + 10)
+    g = rng.integers(0, n, 20000).astype(np.int32)
+    u = rng.standard_normal((20000, d))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    out += list(vb.raycast_batch(ns, pts[g], u, g[:, None], mode="pruned").to_host())
+np.savez(sys.argv[2], *out)
+"""
+
+
+def test_tensor_core_screen_matches_ffma2_screen(tmp_path):
+    """The tensor-core screen (default from d = 5) and the packed-FFMA2 fp32
+    screen (VR_MMA=0, read once per process, hence subprocesses) return
+    bitwise-identical results on generator-start rays, d = 5, 6, 8."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("1", "0"):
+        path = str(tmp_path / f"mma{mode}.npz")
+        env = dict(os.environ, VR_MMA=mode)
+        p = subprocess.run([sys.executable, "-c", _MMA_SCRIPT, root, path], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[mode] = np.load(path)
+    for k in res["1"].files:
+        assert np.array_equal(res["1"][k], res["0"][k], equal_nan=True), k
