@@ -179,6 +179,9 @@ typedef struct vr_prune_index {
    * in mma.sync m16n8k8 B-fragment order, tf32-rounded.  Nullable: without it
    * the pruned kernel screens with packed FFMA2 on rec32. */
   const float* recB;
+  /* The kd-ordered fp32 centred rows in vr_pack_records32 layout (the
+   * tensor-core kernel's seed pass); required with recB. */
+  const float* rec32rows;
 } vr_prune_index;
 
 /* vr_raycast_batch through the pruned index.  `order` (nullable, n_rays

@@ -207,7 +207,8 @@ class _PruneStruct(ctypes.Structure):
                 ("node_box32", ctypes.c_void_p), ("node_range", ctypes.c_void_p),
                 ("n", ctypes.c_int64), ("wide_box32", ctypes.c_void_p),
                 ("wide_levels", ctypes.c_int32), ("wide_off", ctypes.c_int64 * 8),
-                ("wide_cnt", ctypes.c_int64 * 8), ("recB", ctypes.c_void_p)]
+                ("wide_cnt", ctypes.c_int64 * 8), ("recB", ctypes.c_void_p),
+                ("rec32rows", ctypes.c_void_p)]
 
 
 WIDE = 32
@@ -403,7 +404,8 @@ class PruneIndex:
                                    p(self.node_box32), p(self.node_range), n,
                                    p(self.wide_box32), len(boxes), pad8(self.wide_off),
                                    pad8(self.wide_cnt),
-                                   p(self.recB) if self.recB is not None else None)
+                                   p(self.recB) if self.recB is not None else None,
+                                   p(self.screen32.rec))
 
 
 def build_node_set(points, backend="auto"):

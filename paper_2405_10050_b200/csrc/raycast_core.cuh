@@ -906,6 +906,71 @@ __device__ __forceinline__ void seed_tile(RayState<D> (&ray)[R], const double* _
   }
 }
 
+// fp32 seed pass (tensor-core kernel): the same division-free argmin over
+// the start tile, evaluated on the centred fp32 rows (broadcast loads, 4
+// candidates in flight) with the conservative fp32 halfspace test; only the
+// winner is re-evaluated in fp64 (reference formula, raycast.py:201-203) and
+// must pass the exact halfspace test before it seeds the sphere.  Like the
+// fp64 seed it is purely an accelerator: the main scan screens the seed tile
+// again, so a suboptimal (or skipped) seed never changes a result.
+template <int D>
+__device__ __forceinline__ void seed_tile32(RayState<D>& r, const float* __restrict__ tile32,
+                                            const double* __restrict__ tile64, int gbase,
+                                            const Frame& fr) {
+  constexpr int S = rec_stride(D);
+  constexpr int S32 = rec32_stride(D);
+  float xo[D];
+  double uc = 0.0, xx = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    xo[k] = (float)(r.x[k] - fr.c0[k]);
+    uc = fma(r.u[k], fr.c0[k], uc);
+    xx = fma((double)xo[k], (double)xo[k], xx);
+  }
+  const float base = (float)r.base, sc = (float)(r.s - uc);
+  // The eta generators (equidistant to x: num ~ 0) pass the conservative
+  // fp32 halfspace test and would win with t ~ 0; real candidates have
+  // num > 0 by the empty sphere of the origin vertex.  Skip num below a bound
+  // on the fp32 error of |x~ - x~_i|^2 - base (seed quality only).
+  const float nmin = (float)(16.0 * D * 5.960464477539063e-08 * (2.0 * fr.sqmax32 + 2.0 * xx + r.base));
+  const int gl = r.gk - gbase;
+  float nb = 1.0f, db = 0.0f;  // "t = +inf"
+  int ib = -1;
+#pragma unroll 4
+  for (int c = 0; c < 64; ++c) {
+    float xi[D];
+    load_rec32<D>(tile32 + c * S32, xi);
+    const float sq = __ldg(tile32 + c * S32 + D);
+    float q = r.bsl32, aa = 0.0f;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      q = fmaf(r.u32[k], xi[k], q);
+      const float a = xo[k] - xi[k];
+      aa = fmaf(a, a, aa);
+    }
+    const float num = aa - base, den = q - r.bsl32 - sc;
+    const bool better = !isinf(sq) && c != gl && q > r.thr32 && den > 0.0f && num > nmin &&
+                        num * db < nb * den;
+    nb = better ? num : nb;
+    db = better ? den : db;
+    ib = better ? c : ib;
+  }
+  if (ib < 0) return;
+  double xi[D];
+  load_rec_g<D>(tile64 + ib * S, xi);
+  double q = 0.0, aa = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    q = fma(r.u[k], xi[k], q);
+    const double a = r.x[k] - xi[k];
+    aa = fma(a, a, aa);
+  }
+  if (!(q > r.thr)) return;  // the fp32 choice was not valid
+  const double num = aa - r.base, den = q - r.s;
+  const double t = num / (2.0 * den);
+  if (r.ib < 0 || t < r.tb) ray_set_best<D, true>(r, t, den, gbase + ib, fr);
+}
+
 // Warp-coherent traversal of the kd tree over tiles (heap layout: node i has
 // children 2i+1, 2i+2; node_range[i] = [first tile, last tile + 1); a leaf is
 // one tile).  A node is descended only if some ray of the warp needs its box
@@ -1267,7 +1332,7 @@ __device__ __forceinline__ void screen_tile_mma(RayState<D>& r, const double* ti
 template <int D, int R, int PT, int PB, int MINB, bool F32, class Src, bool MMA = false>
 __global__ void __launch_bounds__(32, MINB)
     k_raycast_pruned(Src src, const double* __restrict__ crec, const float* __restrict__ crec32,
-                     const float* __restrict__ crecB,
+                     const float* __restrict__ crecB, const float* __restrict__ crec32s,
                      const int32_t* __restrict__ perm, const int32_t* __restrict__ inv_perm,
                      int64_t n_cand, const double* __restrict__ tile_box,
                      const float* __restrict__ tile_box32, const double* __restrict__ node_box,
@@ -1331,7 +1396,10 @@ __global__ void __launch_bounds__(32, MINB)
   int64_t st = 0;
   if (lane == 0) st = inv_perm[src.gen(k0)] / PT;
   st = __shfl_sync(0xffffffffu, st, 0);
-  seed_tile<D, R, PT, F32>(ray, crec + st * PT * S, (int)(st * PT), fr);
+  if constexpr (MMA)
+    seed_tile32<D>(ray[0], crec32s + st * PT * rec32_stride(D), crec + st * PT * S, (int)(st * PT), fr);
+  else
+    seed_tile<D, R, PT, F32>(ray, crec + st * PT * S, (int)(st * PT), fr);
   TreeCursor<D, R, F32> cur;
   cur.init(st, ray, node_box, node_box32, node_range);
   if constexpr (MMA) {
@@ -1945,7 +2013,8 @@ struct PrunedIndex {
   const int2* node_range;  // [first tile, last tile + 1) per node
   int64_t n;
   WideTree wide;           // 32-ary tree over the tiles (cooperative kernel)
-  const float* crecB;      // tensor-core screen operand (nullable, d <= 6)
+  const float* crecB;      // tensor-core screen operand (nullable)
+  const float* crec32s;    // kd-ordered fp32 centred rows, vr_pack_records32 layout (with crecB)
 };
 
 #ifdef VR_PRUNE_TILE_OVERRIDE  // tuning builds only (the Python index must match: VR_PRUNE_TILE)
@@ -1979,7 +2048,7 @@ int launch_pruned_rm(const Src& src, int64_t n_rays, const PrunedIndex& ix, cons
     grid = slots;
   }
 #endif
-  kern<<<(unsigned)grid, 32, 0, st>>>(src, ix.crec, ix.crec32, ix.crecB, ix.perm, ix.inv_perm, ix.n,
+  kern<<<(unsigned)grid, 32, 0, st>>>(src, ix.crec, ix.crec32, ix.crecB, ix.crec32s, ix.perm, ix.inv_perm, ix.n,
                                       ix.tile_box, ix.tile_box32, ix.node_box, ix.node_box32,
                                       ix.node_range, fr, out, work, next_item);
   cudaError_t le = cudaGetLastError();
@@ -2017,7 +2086,7 @@ int launch_pruned_f(const Src& src, int64_t n_rays, const PrunedIndex& ix, const
   // tensor-core screen from d = 5 (config 4, d = 4: 0.126 vs 0.118 s with
   // the packed-FFMA2 screen, whose cost scales with d)
   if constexpr (F32 && PRUNE_TILE == 64 && D >= 5) {
-    if (ix.crecB && mma_mode() != 0)
+    if (ix.crecB && ix.crec32s && mma_mode() != 0)
       return launch_pruned_rm<D, 1, MMA_MINB, F32, Src, true>(src, n_rays, ix, fr, out, st, work);
   }
   return launch_pruned_rm<D, 1, MINB, F32>(src, n_rays, ix, fr, out, st, work);
@@ -2045,6 +2114,7 @@ inline PrunedIndex pruned_index_from(const vr_prune_index* ix, bool f32) {
                  ix->tile_box32, ix->node_box, ix->node_box32,
                  reinterpret_cast<const int2*>(ix->node_range), ix->n, WideTree{}};
   pi.crecB = f32 ? ix->recB : nullptr;
+  pi.crec32s = f32 ? ix->rec32rows : nullptr;
   pi.wide.box32 = ix->wide_box32;
   pi.wide.levels = ix->wide_levels;
   for (int l = 0; l < WIDE_MAX_LEVELS; ++l) {
