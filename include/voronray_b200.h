@@ -417,9 +417,11 @@ int vr_trav_edge_compact(const vr_traverse_tables* tab, int d,
                          int32_t* out_count, void* stream);
 
 /* Roofline probe: `blocks` x 256 threads x iters x 8 independent FMA chains
- * (dtype 0 = fp64 DFMA, 1 = fp32 FFMA); flops = 4096 * iters * blocks.  Used
- * by bench.py to measure the FP64/FP32 pipe peaks live (MEASURED_PEAKS.json
- * has only HBM and bf16). */
+ * (dtype 0 = fp64 DFMA, 1 = fp32 FFMA; flops = 4096 * iters * blocks) or
+ * 8 independent tf32 mma.sync m16n8k8 per warp (dtype 2, the legacy warp
+ * tensor path of the pruned kernel's screen; flops = 131072 * iters * blocks).
+ * Used by bench.py to measure the FP64 / FP32 / warp-MMA peaks live
+ * (MEASURED_PEAKS.json has only HBM and bf16). */
 int vr_fma_probe(int dtype, int blocks, int iters, void* scratch, void* stream);
 
 #ifdef __cplusplus
