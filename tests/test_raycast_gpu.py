@@ -368,17 +368,20 @@ def test_config2_full_size_properties():
     assert bool(((X @ ue.T).max(0).values <= thr).all())
 
 
+@pytest.mark.parametrize("d", [4, 6, 8])
 @pytest.mark.parametrize("case", ["offset", "anisotropic", "clustered"])
-def test_fp32_screen_robust_to_scale(case):
-    """The fp32 screen's rigorous bound must hold for badly scaled inputs:
-    a large common offset (1e3 + 1e-3 * U), wildly different axis scales,
-    and tight clusters.  Pruned fp32 == exhaustive fp64 bitwise."""
-    rng = np.random.default_rng(77)
-    n, d = 6000, 4
+def test_fp32_screen_robust_to_scale(case, d):
+    """The fp32 screen's and the tensor-core (tf32) screen's rigorous bounds
+    must hold for badly scaled inputs: a large common offset
+    (1e3 + 1e-3 * U), wildly different axis scales, and tight clusters.
+    Pruned fp32 (FFMA2 at d = 4, tensor core at d = 6, 8) == exhaustive fp64
+    bitwise."""
+    rng = np.random.default_rng(77 + d)
+    n = 6000
     if case == "offset":
         pts = 1e3 + 1e-3 * rng.random((n, d))
     elif case == "anisotropic":
-        pts = rng.random((n, d)) * np.array([1e4, 1.0, 1e-4, 3e2])
+        pts = rng.random((n, d)) * np.array([1e4, 1.0, 1e-4, 3e2, 10.0, 1e-2, 5.0, 0.1])[:d]
     else:
         centers = rng.random((20, d)) * 100
         pts = centers[rng.integers(0, 20, n)] + 1e-3 * rng.standard_normal((n, d))

@@ -39,7 +39,9 @@ hrp, hfl = P((n, d), torch.float64), P((n,), torch.uint8)
 for chunk, minc, graphs, nb, cst in ((1 << 19, 1 << 19, False, 4, 2), (1 << 18, 1 << 16, True, 4, 2),
                                     (1 << 18, 1 << 16, True, 8, 4), (1 << 17, 1 << 15, True, 8, 4),
                                     (1 << 17, 1 << 16, True, 8, 4), (1 << 17, 1 << 17, True, 8, 4),
-                                    (1 << 16, 1 << 16, True, 16, 8), (1 << 18, 1 << 15, True, 8, 4)):
+                                    (1 << 16, 1 << 16, True, 16, 8), (1 << 18, 1 << 15, True, 8, 4),
+                                    (1 << 19, 1 << 15, True, 8, 4), (1 << 19, 1 << 16, True, 4, 4),
+                                    (1 << 18, 1 << 14, True, 8, 4), (1 << 18, 1 << 15, True, 8, 8)):
     hr = HostRaycaster(ns, n, 1, chunk=chunk, min_chunk=minc, graphs=graphs, nbuf=nb,
                        compute_streams=cst)
     hr.run(hx, hu, hg, hidx, ht, hrp, hfl)
