@@ -136,9 +136,17 @@ __device__ bool lu_factor(double (&A)[D][D], int (&piv)[D]) {
     }
     piv[c] = p;
     if (!(best > 0.0) || !isfinite(best)) return false;
-    if (p != c) {
+    // row swap with static indices only (a runtime row index would put A in
+    // local memory): exact, so the factors are unchanged
 #pragma unroll
-      for (int k = 0; k < D; ++k) { double t = A[c][k]; A[c][k] = A[p][k]; A[p][k] = t; }
+    for (int r = c + 1; r < D; ++r) {
+      const bool sw = r == p;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const double a = A[c][k], b = A[r][k];
+        A[c][k] = sw ? b : a;
+        A[r][k] = sw ? a : b;
+      }
     }
     double inv = 1.0 / A[c][c];
 #pragma unroll
@@ -158,8 +166,14 @@ __device__ void lu_solve(const double (&A)[D][D], const int (&piv)[D], double (&
   // P b first (full-row swaps in lu_factor give P A = L U), then L y = P b.
 #pragma unroll
   for (int c = 0; c < D; ++c) {
-    int p = piv[c];
-    if (p != c) { double t = b[c]; b[c] = b[p]; b[p] = t; }
+    const int p = piv[c];
+#pragma unroll
+    for (int r = c + 1; r < D; ++r) {
+      const bool sw = r == p;
+      const double x = b[c], y = b[r];
+      b[c] = sw ? y : x;
+      b[r] = sw ? x : y;
+    }
   }
 #pragma unroll
   for (int c = 0; c < D; ++c) {

@@ -314,6 +314,20 @@ __global__ void k_finalize(Tables t, const double* __restrict__ rec,
 #pragma unroll
   for (int j = 0; j < D; ++j) vr[id * D + j] = x0[j] + b[j];
   t.vval[slot[k]] = (int32_t)id;
+}
+
+// The d+1 edge-count bumps of every new vertex (graph.py:115-120), split from
+// k_finalize: the hash probes are latency-bound and want full occupancy,
+// while the fp64 circumcentre solve holds ~200 registers (10 warps/SM; config
+// 5: the fused kernel took 116 ms of the traversal's GPU time).
+template <int D>
+__global__ void k_bump_new(Tables t, const int32_t* __restrict__ ray_sigma,
+                           const int32_t* __restrict__ new_flag, int64_t n) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n || !new_flag[k]) return;
+  int32_t s[D + 1];
+#pragma unroll
+  for (int a = 0; a <= D; ++a) s[a] = ray_sigma[k * (D + 1) + a];
   bump_edges<D>(t, s);
 }
 
@@ -443,6 +457,7 @@ extern "C" int vr_trav_finalize(const vr_traverse_tables* tab, const double* rec
   VR_DISPATCH_D(d, {
     k_finalize<D><<<nb(n_rays, 128), 128, 0, as_stream(stream)>>>(
         t, rec, ray_sigma, slot, new_flag, new_off, n_rays, base_id, vsig, vr, bad);
+    k_bump_new<D><<<nb(n_rays), 256, 0, as_stream(stream)>>>(t, ray_sigma, new_flag, n_rays);
   });
   VR_RETURN_LAUNCH();
 }

@@ -414,7 +414,10 @@ class DeviceTraversal:
     def ensure_edges(self, extra):
         if 2 * (self.e_ub + extra) > self.ecap:
             ok, os_, oc, ocap = self.ekeys, self.estate, self.ecount, self.ecap
-            self._alloc_etable(_pow2(4 * (self.e_ub + extra)))
+            # e_ub counts every (vertex, edge) incidence, about twice the
+            # distinct edges, so 2x keeps the real load near 0.25 (4x made
+            # config 5's table 2^31 slots, 86 GB)
+            self._alloc_etable(_pow2(2 * (self.e_ub + extra)))
             T = self.tables()
             _lib.check(self.L.vr_trav_rehash_edges(ctypes.byref(T), self.d, _lib.ptr(ok),
                                                    _lib.ptr(os_), _lib.ptr(oc), ocap,
