@@ -416,6 +416,20 @@ int vr_trav_edge_compact(const vr_traverse_tables* tab, int d,
                          const int64_t* off, int32_t* out_keys,
                          int32_t* out_count, void* stream);
 
+/* ---- Host descent streams (host code; no GPU needed) ----------------------
+ * stream(seed, tag, index) of the reference (pkg/src/voronray/rng.py:18-28):
+ * numpy Generator(PCG64(SeedSequence(entropy=seed, spawn_key=(tag, index)))),
+ * restated over arrays of streams.  vr_host_streams writes 4 uint64 per
+ * stream (PCG64 state high, low, increment high, low); vr_host_normals draws
+ * `count` standard normals per listed stream (rows[i], or i when rows is
+ * NULL) into out[i * count ..] with NumPy's ziggurat (libnpyrandom, linked
+ * in) and advances the states: bit-identical to
+ * Generator.standard_normal(count) (descent, graph.py:46-85). */
+int vr_host_streams(uint64_t seed, uint64_t tag, const int64_t* index, int64_t n,
+                    uint64_t* state);
+int vr_host_normals(uint64_t* state, const int64_t* rows, int64_t n, int64_t count,
+                    double* out);
+
 /* Roofline probe: `blocks` x 256 threads x iters x 8 independent FMA chains
  * (dtype 0 = fp64 DFMA, 1 = fp32 FFMA; flops = 4096 * iters * blocks) or
  * 8 independent tf32 mma.sync m16n8k8 per warp (dtype 2, the legacy warp

@@ -34,6 +34,17 @@ def _nvcc():
     raise RuntimeError("nvcc not found; the B200 library cannot be built")
 
 
+def _npyrandom():
+    """NumPy's static distribution library (random_standard_normal): the
+    host descent streams (csrc/host_rng.cu) draw with NumPy's own ziggurat so
+    that they are bit-identical to numpy.random.Generator."""
+    import numpy
+    lib = os.path.join(os.path.dirname(numpy.__file__), "random", "lib", "libnpyrandom.a")
+    if not os.path.exists(lib):
+        raise RuntimeError(f"{lib} not found (needed by csrc/host_rng.cu)")
+    return [lib, "-lm"]
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -81,7 +92,7 @@ def build(force=False, verbose=False, jobs=None, defines=(), out=None):
         raise RuntimeError(f"nvcc failed:\n{msg}")
     tmp = lib_path + ".tmp"
     link = [nvcc, "-shared", "--cudart", "static",
-            "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp]
+            "-gencode", "arch=compute_100a,code=sm_100a", *objs, *_npyrandom(), "-o", tmp]
     res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("link failed:\n" + res.stdout + res.stderr)

@@ -51,6 +51,8 @@ _SIGNATURES = {
     "vr_pack_records32": [_vp, _i64, _int, _vp, _vp, _vp],
     "vr_pack_records32_pairs": [_vp, _i64, _int, _vp, _vp],
     "vr_pack_records_mma": [_vp, _i64, _int, _vp, _vp],
+    "vr_host_streams": [ctypes.c_uint64, ctypes.c_uint64, _vp, _i64, _vp],
+    "vr_host_normals": [_vp, _vp, _i64, _i64, _vp],
     "vr_ray_keys": [_vp, _vp, _int, _i64, _vp, _i64, _int, _vp, _vp],
     "vr_mc_integrate": [_vp, _int, _vp, _i64, _i64, _vp, _u64, _vp, _vp, _vp, _int, _dbl, _int,
                         _vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

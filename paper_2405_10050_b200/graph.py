@@ -129,19 +129,48 @@ class _Draws:
     def __init__(self, rngs, seed, starts, d, block=None):
         self.d = d
         self.own = rngs is None
-        self.rngs = [_rng.stream(seed, "descent", int(s)) for s in starts] if self.own else rngs
+        self.rngs = rngs
         if self.own:
             self.K = block or (d + 3)
-            self.buf = np.stack([g.standard_normal((self.K, d)) for g in self.rngs])
-            self.ptr = np.zeros(len(starts), dtype=np.int64)
+            S = len(starts)
+            self.ptr = np.zeros(S, dtype=np.int64)
+            if 0 <= int(seed) < 1 << 64:
+                # the package's streams restated over all starts at once in
+                # the host library (csrc/host_rng.cu: SeedSequence + PCG64 +
+                # NumPy's ziggurat, bit-identical to _rng.stream; ~2 us per
+                # start instead of ~20 us for a Generator object)
+                self.L = _lib.load_library()
+                idx = np.ascontiguousarray(starts, dtype=np.int64)
+                self.state = np.zeros((S, 4), dtype=np.uint64)
+                _lib.check(self.L.vr_host_streams(int(seed), _rng.PURPOSES["descent"],
+                                                  idx.ctypes.data, S, self.state.ctypes.data),
+                           "vr_host_streams")
+                self.buf = np.empty((S, self.K, d))
+                self._draw(None, S, self.buf)
+            else:
+                self.state = None
+                self.rngs = [_rng.stream(seed, "descent", int(s)) for s in starts]
+                self.buf = np.stack([g.standard_normal((self.K, d)) for g in self.rngs])
+
+    def _draw(self, rows, n, out):
+        _lib.check(self.L.vr_host_normals(self.state.ctypes.data,
+                                          None if rows is None else rows.ctypes.data, n,
+                                          self.K * self.d, out.ctypes.data), "vr_host_normals")
 
     def take(self, grp):
         if not self.own:
             return np.stack([self.rngs[a].standard_normal(self.d) for a in grp])
         empty = grp[self.ptr[grp] >= self.K]
-        for a in empty:  # refill (many escapes / redraws): the next block of the stream
-            self.buf[a] = self.rngs[a].standard_normal((self.K, self.d))
-            self.ptr[a] = 0
+        if empty.size:  # refill (many escapes / redraws): the next block of each stream
+            if self.state is not None:
+                rows = np.ascontiguousarray(empty, dtype=np.int64)
+                blk = np.empty((rows.size, self.K, self.d))
+                self._draw(rows, rows.size, blk)
+                self.buf[rows] = blk
+            else:
+                for a in empty:
+                    self.buf[a] = self.rngs[a].standard_normal((self.K, self.d))
+            self.ptr[empty] = 0
         z = self.buf[grp, self.ptr[grp]]
         self.ptr[grp] += 1
         return z
@@ -192,11 +221,19 @@ def descent_batch(ns: NodeSet, starts, seed: int = 0, stats: RaycastStats = None
                         break
             u[pos] = v / nrm[:, None]
         still = []
+        # one RayCast for the whole round: eta is padded with copies of its
+        # first entry g (thr is a max over eta and g = eta[0], so the padded
+        # query is the same query), instead of one launch + sync per level
+        kmax = int(k_act.max())
+        eta = np.repeat(sig[active, :1], kmax, axis=1)
+        for kk in levels:
+            eta[k_act == kk, :kk] = sig[active[k_act == kk], :kk]
+        res = raycast_batch(ns, rr[active], u, eta.astype(np.int32), stats=stats)
+        idx_all, _, rp_all, flag_all = res.to_host()
         for kk in levels:
             sel = k_act == kk
             grp = active[sel]
-            res = raycast_batch(ns, rr[grp], u[sel], sig[grp, :kk].astype(np.int32), stats=stats)
-            idx, _, rp, flag = res.to_host()
+            idx, rp, flag = idx_all[sel], rp_all[sel], flag_all[sel]
             esc = flag == 1
             if (flag == 3).any():
                 raise DegenerateConfiguration(
@@ -405,7 +442,7 @@ class DeviceTraversal:
                                  torch.empty((cap - self.nv, self.d), dtype=torch.float64,
                                              device=self.dev)])
         if 2 * need > self.vcap:
-            self._alloc_vtable(_pow2(4 * need))
+            self._alloc_vtable(_pow2(2 * need))  # load <= 0.5
             T = self.tables()
             _lib.check(self.L.vr_trav_insert_vertices(ctypes.byref(T), self.d,
                                                       _lib.ptr(self.vsig), self.nv, 0, -1, 0,

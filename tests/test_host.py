@@ -232,3 +232,37 @@ def test_descent_draw_blocks_are_the_reference_stream():
         g = vb.rng.stream(3, "descent", int(s))
         for row in seq[a]:
             assert np.array_equal(row, g.standard_normal(4))
+
+
+def test_host_streams_are_numpy_generators():
+    """vr_host_streams / vr_host_normals (csrc/host_rng.cu: SeedSequence +
+    PCG64 restated over arrays, NumPy's ziggurat linked in) reproduce
+    numpy.random.Generator(PCG64(SeedSequence(entropy=seed,
+    spawn_key=(tag, index)))) bitwise: PCG state, normals, and the state
+    advance across repeated draws, for several seeds, tags and indices
+    (including multi-word ones)."""
+    from paper_2405_10050_b200 import _lib
+    L = _lib.load_library()
+    idx = np.array([0, 1, 7, 65535, 2 ** 32 - 1, 2 ** 32, 2 ** 40 + 3], dtype=np.int64)
+    for seed, tag in ((0, 0), (1, 0), (12345, 1), (2 ** 33 + 1, 3)):
+        st = np.zeros((idx.size, 4), dtype=np.uint64)
+        assert L.vr_host_streams(seed, tag, idx.ctypes.data, idx.size, st.ctypes.data) == 0
+        gens = [np.random.Generator(np.random.PCG64(
+            np.random.SeedSequence(entropy=seed, spawn_key=(tag, int(i))))) for i in idx]
+        for g, row in zip(gens, st):
+            s = g.bit_generator.state["state"]
+            assert s["state"] == (int(row[0]) << 64) | int(row[1])
+            assert s["inc"] == (int(row[2]) << 64) | int(row[3])
+        for count in (1, 37, 300):
+            rows = np.array([2, 0, 5], dtype=np.int64)
+            out = np.zeros((rows.size, count))
+            assert L.vr_host_normals(st.ctypes.data, rows.ctypes.data, rows.size, count,
+                                     out.ctypes.data) == 0
+            for k, r in enumerate(rows):
+                assert np.array_equal(out[k], gens[r].standard_normal(count))
+    # seeds outside uint64 keep the numpy Generators (same streams)
+    from paper_2405_10050_b200.graph import _Draws
+    dr = _Draws(None, 2 ** 70, np.array([3, 4]), 3, block=2)
+    assert dr.state is None
+    assert np.array_equal(dr.take(np.array([1]))[0],
+                          vb.rng.stream(2 ** 70, "descent", 4).standard_normal(3))
