@@ -2134,10 +2134,15 @@ int launch_raycast_pruned(const Src& src, int64_t n_rays, const PrunedIndex& ix,
     if (e != cudaSuccess) return vr_cuda_status(e);
   }
   // The cooperative warp-per-ray kernel wins only for sparse, incoherent
-  // high-dimensional edge rays (config-5 sample: 7.2 vs 9.5 ms) and loses on
+  // high-dimensional rays (config-5 sample: 7.2 vs 9.5 ms) and loses on
   // dense traversal levels (config 5 L=5: 10.3 vs 7.4 s) and everywhere at
-  // d <= 6, so it is opt-in (VR_COOP=1).
-  const bool coop = coop_mode() > 0;
+  // d <= 6.
+  // Auto (VR_COOP unset): sparse batches at d >= 7 -- fewer than one ray per
+  // 64 generators, e.g. the 10,000 descent rays of config 5 among 1e6
+  // generators (0.166 -> 0.126 s for the whole descent) -- go to the
+  // cooperative kernel; VR_COOP=1 / 0 force it on / off.
+  const int cm = coop_mode();
+  const bool coop = cm > 0 || (cm < 0 && D >= 7 && n_rays * 64 < ix.n);
   if (ix.crec32 && ix.wide.box32 && ix.wide.levels >= 2 && coop)
     return launch_coop<D>(src, n_rays, ix, fr, out, st, work);
   if (ix.crec32 && ix.tile_box32 && ix.node_box32)
