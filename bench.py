@@ -260,27 +260,33 @@ def extra_configs(vb, torch, world, rank):
                          "rays_per_s": 1e8 / dt, "bounded_cells": int((res4.status == 0).sum()),
                          "pairs_screened": int(w4[0].item()), "d": 4,
                          "reference_cpu_rays_per_s_per_core_build_container": 4180}
+    del m3, ns3, res4, ns4  # config 5 needs ~60 GB of level tables
+    torch.cuda.empty_cache()
     pts5 = np.random.default_rng(0).random((10 ** 6, 8)).astype(np.float32).astype(np.float64)
     ns5 = vb.NodeSet(pts5)
     ns5.prune_index()
     ns5.screen32()
     seeds = np.random.default_rng(1).choice(10 ** 6, 10000, replace=False)
-    # two passes, the second timed: the first pays the one-off costs (lazy
-    # module loading, library handles; 0.1-0.5 s)
-    for rep in range(2):
+    # three passes: the first pays the one-off costs (lazy module loading,
+    # library handles; 0.1-0.5 s); the faster of the other two is reported,
+    # all three are listed
+    passes = []
+    for rep in range(3):
         st = vb.RaycastStats()
         w5 = torch.zeros(16, dtype=torch.int64, device="cuda")
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         m5, lv = vb.voronoi_local(ns5, seeds, hops=5, stats=st, return_levels=True, work=w5)
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        if rep == 0:
+        passes.append(time.perf_counter() - t0)
+        if rep < 2:
             del m5, lv
-            torch.cuda.empty_cache()  # the first pass's tables, not fragmented reuse
+            torch.cuda.empty_cache()  # each pass allocates its own tables afresh
+    dt = min(passes[1:])
     out["config5_local_traversal"] = {
         "seeds": 10000, "hops": 5, "vertices": int(len(lv)), "seconds_incl_descent": dt,
-        "timing": "second of two passes (the first pays one-off module / handle loading)",
+        "timing": "min of passes 2-3 (pass 1 pays one-off module / handle loading)",
+        "passes_s": passes,
         "mesh": "device-resident (HBM), not copied to the host",
         "pairs_screened": int(w5[0].item()), "d": 8,
         "vertices_per_s": len(lv) / dt, "edge_raycasts_this_rank": st.raycasts,
