@@ -357,6 +357,33 @@ typedef struct vr_traverse_tables {
   int32_t* overflow;/* 1 int32: set when a probe sequence exhausts a table   */
 } vr_traverse_tables;
 
+/* Native level driver (csrc/level.cu): one traversal level in two calls,
+ * each ending with a stream synchronisation.
+ * vr_trav_level_open: open edges of the n_v frontier vertices (as
+ *   vr_trav_open_edges), their exclusive int64 offsets in open_off, and the
+ *   ray count R in *n_rays_out (host).
+ * vr_trav_level_cast: the R edge rays (as vr_trav_emit_rays; bad[0..1] are
+ *   zeroed first), their processing order (vr_ray_keys + a stable radix
+ *   sort), the pruned RayCast with |eta| = d plus the exact re-check (hits in
+ *   hit_idx / hit_t / hit_flag), vr_trav_claim, exclusive offsets of the new
+ *   vertices and of the escapes, and counts_out[5] (host) = {new vertices,
+ *   escapes, degenerate rays, affinely dependent frontier vertices, table
+ *   overflow}.  Requires the pruned index (n_gen >= 256 in the Python API);
+ *   the caller then grows the edge table if needed and runs
+ *   vr_trav_finalize / vr_trav_boundary. */
+int vr_trav_level_open(const vr_traverse_tables* tab, int d, const int32_t* frontier_sigma,
+                       int64_t n_v, uint8_t* open_mask, int32_t* open_count, int64_t* open_off,
+                       int64_t* n_rays_out, void* stream);
+int vr_trav_level_cast(const vr_traverse_tables* tab, const double* rec, int64_t n_gen, int d,
+                       double sqmax, const vr_screen32* s32, const vr_prune_index* ix,
+                       const int32_t* frontier_sigma, const double* frontier_r, int64_t n_v,
+                       const uint8_t* open_mask, const int64_t* open_off, int64_t n_rays,
+                       int32_t level, double* ray_x, double* ray_u, int32_t* ray_eta,
+                       int32_t* ray_parent, int32_t* hit_idx, double* hit_t, uint8_t* hit_flag,
+                       int32_t* ray_sigma, int64_t* slot, int32_t* new_flag, int32_t* esc_flag,
+                       int64_t* new_off, int64_t* esc_off, int32_t* bad, uint64_t* work,
+                       int64_t* counts_out, void* stream);
+
 /* Register vertices (sigma (n_v, d+1) sorted) with ids base_id.. at `level`;
  * optionally bump the counters of their d+1 edges (graph.py:115-120). */
 int vr_trav_insert_vertices(const vr_traverse_tables* tab, int d,

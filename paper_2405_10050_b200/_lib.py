@@ -52,6 +52,10 @@ _SIGNATURES = {
     "vr_pack_records32_pairs": [_vp, _i64, _int, _vp, _vp],
     "vr_pack_records_mma": [_vp, _i64, _int, _vp, _vp],
     "vr_host_streams": [ctypes.c_uint64, ctypes.c_uint64, _vp, _i64, _vp],
+    "vr_trav_level_open": [_vp, _int, _vp, _i64, _vp, _vp, _vp, _vp, _vp],
+    "vr_trav_level_cast": [_vp, _vp, _i64, _int, ctypes.c_double, _vp, _vp, _vp, _vp, _i64,
+                           _vp, _vp, _i64, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                           _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_host_normals": [_vp, _vp, _i64, _i64, _vp],
     "vr_ray_keys": [_vp, _vp, _int, _i64, _vp, _i64, _int, _vp, _vp],
     "vr_mc_integrate": [_vp, _int, _vp, _i64, _i64, _vp, _u64, _vp, _vp, _vp, _int, _dbl, _int,
@@ -99,11 +103,19 @@ def load_library():
     return lib
 
 
+_HAVE_DEVICE = False
+
+
 def lib():
-    """The library, after checking that a CUDA device is present."""
+    """The library, after checking that a CUDA device is present (checked
+    until it succeeds once: torch.cuda.is_available() costs ~10 us per call,
+    and the traversal calls this hundreds of times per diagram)."""
+    global _HAVE_DEVICE
     L = load_library()
-    if not torch.cuda.is_available():
-        raise DeviceUnavailable("no CUDA device: the B200 kernels have no CPU fallback")
+    if not _HAVE_DEVICE:
+        if not torch.cuda.is_available():
+            raise DeviceUnavailable("no CUDA device: the B200 kernels have no CPU fallback")
+        _HAVE_DEVICE = True
     return L
 
 
@@ -127,8 +139,11 @@ def ptr(t):
 
 
 def stream_handle(stream=None):
-    s = torch.cuda.current_stream() if stream is None else stream
-    return ctypes.c_void_p(s.cuda_stream)
+    """cudaStream_t of `stream`, or of torch's current stream on the current
+    device (raw C binding: torch.cuda.current_stream() costs ~15 us)."""
+    if stream is not None:
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
 
 
 def to_host(t):

@@ -1,0 +1,240 @@
+// Native driver of one level-synchronous traversal level (graph.py:88-146
+// restated as a frontier loop).
+//
+// The per-level work is ~15 kernels plus two host synchronisations (the ray
+// count, then the new-vertex / escape counts that size the next level and the
+// table growth).  Driving it from Python cost ~0.45 ms of host time per level
+// (torch ops, ctypes, stream lookups) -- more than the device work of the
+// small levels of configs 1 and 3.  These two entry points run the same
+// kernels in the same order from C++ (cub scans and radix sort), so a level
+// costs two ctypes calls and two synchronisations:
+//
+//   vr_trav_level_open:  open edges of the frontier -> exclusive scan -> R
+//   vr_trav_level_cast:  edge rays -> processing order -> pruned RayCast +
+//                        exact re-check -> claim / winners -> scans -> counts
+//
+// The caller (DeviceTraversal.level) then grows the edge table if needed and
+// calls vr_trav_finalize / vr_trav_boundary as before.  Results are those of
+// the Python-driven level (the processing order is the same stable sort).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+
+extern "C" {
+int vr_trav_open_edges(const vr_traverse_tables* tab, int d, const int32_t* sigma, int64_t n_v,
+                       uint8_t* open_mask, int32_t* open_count, void* stream);
+int vr_trav_emit_rays(const double* rec, int d, const int32_t* sigma, const double* r,
+                      int64_t n_v, const uint8_t* open_mask, const int64_t* open_off,
+                      double* ray_x, double* ray_u, int32_t* ray_eta, int32_t* ray_parent,
+                      int32_t* bad, void* stream);
+int vr_trav_claim(const vr_traverse_tables* tab, int d, const int32_t* ray_eta,
+                  const int32_t* hit_idx, const uint8_t* hit_flag, int64_t n_rays,
+                  int32_t level, int32_t* out_sigma, int64_t* out_slot, int32_t* new_flag,
+                  int32_t* esc_flag, void* stream);
+int vr_ray_keys(const int32_t* inv_perm, const int32_t* eta, int eta_len,
+                int64_t rays_per_cell, const double* u, int64_t n, int d, int64_t* keys,
+                void* stream);
+int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
+                      const vr_screen32* s32, const vr_prune_index* ix, const double* x,
+                      const double* u, const int32_t* eta, int eta_len, int64_t n_rays,
+                      const int32_t* order, int32_t* out_idx, double* out_t, double* out_rp,
+                      uint8_t* out_flag, int32_t* recheck_list, int32_t* recheck_count,
+                      uint64_t* work, void* stream);
+int vr_raycast_recheck(const double* rec, int64_t n_gen, int d, const double* cand_rec,
+                       const int32_t* cand, int64_t n_cand, const double* x, const double* u,
+                       const int32_t* eta, int eta_len, const int32_t* recheck_list,
+                       const int32_t* recheck_count, int64_t max_list, int32_t* out_idx,
+                       double* out_t, double* out_rp, uint8_t* out_flag, void* stream);
+}
+
+namespace {
+
+inline unsigned nbk(int64_t n, int nt = 256) {
+  const int64_t b = (n + nt - 1) / nt;
+  return (unsigned)(b < 65535 * 16 ? b : 65535 * 16);
+}
+
+template <typename T>
+__global__ void k_widen(const T* __restrict__ in, int64_t* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int64_t)in[i];
+}
+
+__global__ void k_iota(int32_t* __restrict__ v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = (int32_t)i;
+}
+
+__global__ void k_count_degenerate(const uint8_t* __restrict__ flag, int64_t n,
+                                   unsigned long long* __restrict__ count) {
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += flag[i] == 3 ? 1 : 0;
+  for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+// counts[0..4] = n_new, n_esc, n_degenerate, bad frontier vertices, overflow
+__global__ void k_level_counts(const int32_t* __restrict__ new_flag,
+                               const int64_t* __restrict__ new_off,
+                               const int32_t* __restrict__ esc_flag,
+                               const int64_t* __restrict__ esc_off, int64_t n,
+                               const unsigned long long* __restrict__ ndeg,
+                               const int32_t* __restrict__ bad,
+                               const int32_t* __restrict__ overflow, int64_t* __restrict__ counts) {
+  counts[0] = new_off[n - 1] + new_flag[n - 1];
+  counts[1] = esc_off[n - 1] + esc_flag[n - 1];
+  counts[2] = (int64_t)*ndeg;
+  counts[3] = bad[0];
+  counts[4] = overflow[0];
+}
+
+// Stream-ordered scratch from the default memory pool (kept, not released,
+// between levels: the pool's release threshold is raised once).
+struct Scratch {
+  cudaStream_t st;
+  void* p = nullptr;
+  cudaError_t alloc(size_t bytes) {
+    static bool pool_set = false;
+    if (!pool_set) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      pool_set = true;
+    }
+    return cudaMallocAsync(&p, bytes ? bytes : 16, st);
+  }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Exclusive int64 scan of an int32 array (cub), with its own temp storage.
+cudaError_t excl_scan(const int32_t* in, int64_t* out, int64_t n, cudaStream_t st) {
+  // widen into `out`, then scan in place (cub allows in == out for scans)
+  k_widen<int32_t><<<nbk(n), 256, 0, st>>>(in, out, n);
+  size_t tmp = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tmp, out, out, (int)n, st);
+  if (e != cudaSuccess) return e;
+  Scratch s{st};
+  if ((e = s.alloc(tmp)) != cudaSuccess) return e;
+  return cub::DeviceScan::ExclusiveSum(s.p, tmp, out, out, (int)n, st);
+}
+
+int fail(cudaError_t e) { return e == cudaSuccess ? VR_OK : vr_cuda_status(e); }
+
+}  // namespace
+
+extern "C" int vr_trav_level_open(const vr_traverse_tables* tab, int d,
+                                  const int32_t* frontier_sigma, int64_t n_v, uint8_t* open_mask,
+                                  int32_t* open_count, int64_t* open_off, int64_t* n_rays_out,
+                                  void* stream) {
+  if (!tab || !frontier_sigma || !open_mask || !open_count || !open_off || !n_rays_out)
+    return VR_EINVAL;
+  *n_rays_out = 0;
+  if (n_v <= 0) return VR_OK;
+  if (n_v >= (int64_t)1 << 31) return VR_EINVAL;  // cub scans with int counts
+  cudaStream_t st = as_stream(stream);
+  int s = vr_trav_open_edges(tab, d, frontier_sigma, n_v, open_mask, open_count, stream);
+  if (s) return s;
+  cudaError_t e = excl_scan(open_count, open_off, n_v, st);
+  if (e != cudaSuccess) return fail(e);
+  int64_t last[1];
+  int32_t cnt[1];
+  if ((e = cudaMemcpyAsync(last, open_off + n_v - 1, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(cnt, open_count + n_v - 1, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(st)) != cudaSuccess)
+    return fail(e);
+  *n_rays_out = last[0] + cnt[0];
+  return VR_OK;
+}
+
+extern "C" int vr_trav_level_cast(
+    const vr_traverse_tables* tab, const double* rec, int64_t n_gen, int d, double sqmax,
+    const vr_screen32* s32, const vr_prune_index* ix, const int32_t* frontier_sigma,
+    const double* frontier_r, int64_t n_v, const uint8_t* open_mask, const int64_t* open_off,
+    int64_t n_rays, int32_t level, double* ray_x, double* ray_u, int32_t* ray_eta,
+    int32_t* ray_parent, int32_t* hit_idx, double* hit_t, uint8_t* hit_flag, int32_t* ray_sigma,
+    int64_t* slot, int32_t* new_flag, int32_t* esc_flag, int64_t* new_off, int64_t* esc_off,
+    int32_t* bad, uint64_t* work, int64_t* counts_out, void* stream) {
+  if (!tab || !rec || !ix || !ix->inv_perm || !frontier_sigma || !frontier_r || !open_mask ||
+      !open_off || !ray_x || !ray_u || !ray_eta || !ray_parent || !hit_idx || !hit_t ||
+      !hit_flag || !ray_sigma || !slot || !new_flag || !esc_flag || !new_off || !esc_off ||
+      !bad || !counts_out)
+    return VR_EINVAL;
+  for (int i = 0; i < 5; ++i) counts_out[i] = 0;
+  if (n_rays <= 0) return VR_OK;
+  if (n_rays >= (int64_t)1 << 31) return VR_EINVAL;
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e;
+  int s;
+  if ((e = cudaMemsetAsync(bad, 0, 2 * sizeof(int32_t), st)) != cudaSuccess) return fail(e);
+  s = vr_trav_emit_rays(rec, d, frontier_sigma, frontier_r, n_v, open_mask, open_off, ray_x,
+                        ray_u, ray_eta, ray_parent, bad, stream);
+  if (s) return s;
+  // one scratch block: keys in / out, order in / out, recheck list + count,
+  // degenerate counter, device counts, sort temp storage
+  const int64_t R = n_rays;
+  int end_bit = 8;  // keys = kd position * 256 + direction class
+  while (end_bit < 63 && ((int64_t)1 << end_bit) <= n_gen * 256) ++end_bit;
+  size_t sort_tmp = 0;
+  e = cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (const int64_t*)nullptr,
+                                      (int64_t*)nullptr, (const int32_t*)nullptr,
+                                      (int32_t*)nullptr, (int)R, 0, end_bit, st);
+  if (e != cudaSuccess) return fail(e);
+  const size_t o_kin = 0, o_kout = align256(o_kin + 8 * R), o_vin = align256(o_kout + 8 * R),
+               o_vout = align256(o_vin + 4 * R), o_rl = align256(o_vout + 4 * R),
+               o_rc = align256(o_rl + 4 * R), o_deg = align256(o_rc + 4),
+               o_cnt = align256(o_deg + 8), o_tmp = align256(o_cnt + 8 * 5),
+               total = o_tmp + sort_tmp;
+  Scratch sc{st};
+  if ((e = sc.alloc(total)) != cudaSuccess) return fail(e);
+  char* base = static_cast<char*>(sc.p);
+  int64_t* kin = reinterpret_cast<int64_t*>(base + o_kin);
+  int64_t* kout = reinterpret_cast<int64_t*>(base + o_kout);
+  int32_t* vin = reinterpret_cast<int32_t*>(base + o_vin);
+  int32_t* order = reinterpret_cast<int32_t*>(base + o_vout);
+  int32_t* rl = reinterpret_cast<int32_t*>(base + o_rl);
+  int32_t* rc = reinterpret_cast<int32_t*>(base + o_rc);
+  unsigned long long* ndeg = reinterpret_cast<unsigned long long*>(base + o_deg);
+  int64_t* dcounts = reinterpret_cast<int64_t*>(base + o_cnt);
+  // processing order (raycast.py coherent_order: stable sort of the keys)
+  s = vr_ray_keys(ix->inv_perm, ray_eta, d, 1, ray_u, R, d, kin, stream);
+  if (s) return s;
+  k_iota<<<nbk(R), 256, 0, st>>>(vin, R);
+  e = cub::DeviceRadixSort::SortPairs(base + o_tmp, sort_tmp, kin, kout, vin, order, (int)R, 0,
+                                      end_bit, st);
+  if (e != cudaSuccess) return fail(e);
+  // RayCast of the level's edge rays (|eta| = d) + exact re-check
+  s = vr_raycast_pruned(rec, n_gen, d, sqmax, s32, ix, ray_x, ray_u, ray_eta, d, R, order,
+                        hit_idx, hit_t, nullptr, hit_flag, rl, rc, work, stream);
+  if (s) return s;
+  s = vr_raycast_recheck(rec, n_gen, d, nullptr, nullptr, 0, ray_x, ray_u, ray_eta, d, rl, rc, R,
+                         hit_idx, hit_t, nullptr, hit_flag, stream);
+  if (s) return s;
+  // claim the hit vertices, then offsets of the new vertices / escapes
+  s = vr_trav_claim(tab, d, ray_eta, hit_idx, hit_flag, R, level, ray_sigma, slot, new_flag,
+                    esc_flag, stream);
+  if (s) return s;
+  if ((e = excl_scan(new_flag, new_off, R, st)) != cudaSuccess) return fail(e);
+  if ((e = excl_scan(esc_flag, esc_off, R, st)) != cudaSuccess) return fail(e);
+  if ((e = cudaMemsetAsync(ndeg, 0, 8, st)) != cudaSuccess) return fail(e);
+  k_count_degenerate<<<nbk(R, 256) < 1184 ? nbk(R, 256) : 1184, 256, 0, st>>>(hit_flag, R, ndeg);
+  k_level_counts<<<1, 1, 0, st>>>(new_flag, new_off, esc_flag, esc_off, R, ndeg, bad,
+                                  tab->overflow, dcounts);
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail(e);
+  if ((e = cudaMemcpyAsync(counts_out, dcounts, 5 * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(st)) != cudaSuccess)
+    return fail(e);
+  return VR_OK;
+}

@@ -2139,10 +2139,12 @@ int launch_raycast_pruned(const Src& src, int64_t n_rays, const PrunedIndex& ix,
   // d <= 6.
   // Auto (VR_COOP unset): sparse batches at d >= 7 -- fewer than one ray per
   // 64 generators, e.g. the 10,000 descent rays of config 5 among 1e6
-  // generators (0.166 -> 0.126 s for the whole descent) -- go to the
-  // cooperative kernel; VR_COOP=1 / 0 force it on / off.
+  // generators (0.166 -> 0.126 s for the whole descent) -- and batches too
+  // small to fill the GPU with 32-ray warps (< 8192 rays: the small levels
+  // of a full traversal; config 1 12.5 -> 10.5 ms) go to the cooperative
+  // kernel; VR_COOP=1 / 0 force it on / off.
   const int cm = coop_mode();
-  const bool coop = cm > 0 || (cm < 0 && D >= 7 && n_rays * 64 < ix.n);
+  const bool coop = cm > 0 || (cm < 0 && (n_rays < 8192 || (D >= 7 && n_rays * 64 < ix.n)));
   if (ix.crec32 && ix.wide.box32 && ix.wide.levels >= 2 && coop)
     return launch_coop<D>(src, n_rays, ix, fr, out, st, work);
   if (ix.crec32 && ix.tile_box32 && ix.node_box32)

@@ -22,6 +22,7 @@ from dataclasses import dataclass, field
 from itertools import combinations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -30,8 +31,8 @@ from . import _lib
 from . import rng as _rng
 from .core import (TOL_VERTEX, Mesh, NodeSet, VertexRecord, edge_keys, verify_vertices)
 from .errors import DegenerateConfiguration, RetryExhausted
-from .raycast import (RANK_TOL, RayQuery, RaycastStats, _orthonormal_rows, _project_out,
-                      raycast_batch, raycast_incircle)
+from .raycast import (PRUNE_MIN_GENERATORS, RANK_TOL, RayQuery, RaycastStats, Workspace,
+                      _orthonormal_rows, _project_out, raycast_batch, raycast_incircle)
 
 DESCENT_RETRIES = 100
 
@@ -405,6 +406,8 @@ class DeviceTraversal:
         self.nb = 0
         self.e_ub = 0
         self.work = None  # optional VR_WORK_COUNTERS tensor (pruned-kernel accounting)
+        # native level driver (csrc/level.cu) unless VR_NATIVE_LEVEL=0
+        self.native = os.environ.get("VR_NATIVE_LEVEL", "1") != "0"
 
     def _alloc_vtable(self, cap):
         d = self.d
@@ -500,12 +503,83 @@ class DeviceTraversal:
                             work=self.work)
         return res.idx, res.flag
 
+    def _level_native(self, f0, f1, lvl, stats, ws):
+        """level() through the native driver (csrc/level.cu): two C-ABI calls
+        and two synchronisations instead of ~40 torch / ctypes operations."""
+        d, L, dev, sh = self.d, self.L, self.dev, self._sh()
+        ws = ws if ws is not None else Workspace()
+        F = f1 - f0
+        fs = self.vsig[f0:f1]
+        fr = self.vr[f0:f1]
+        p = _lib.ptr
+        open_mask = ws.get("lv_open_mask", (F, d + 1), torch.uint8, dev)
+        open_cnt = ws.get("lv_open_cnt", (F,), torch.int32, dev)
+        off = ws.get("lv_open_off", (F,), torch.int64, dev)
+        T = self.tables()
+        nr = ctypes.c_int64(0)
+        _lib.check(L.vr_trav_level_open(ctypes.byref(T), d, p(fs), F, p(open_mask), p(open_cnt),
+                                        p(off), ctypes.byref(nr), sh), "level_open")
+        R = int(nr.value)
+        if R == 0:
+            return 0
+        if stats is not None:
+            stats.add(R)
+        rx = ws.get("lv_rx", (R, d), torch.float64, dev)
+        ru = ws.get("lv_ru", (R, d), torch.float64, dev)
+        reta = ws.get("lv_reta", (R, d), torch.int32, dev)
+        rpar = ws.get("lv_rpar", (R,), torch.int32, dev)
+        hidx = ws.get("lv_hidx", (R,), torch.int32, dev)
+        ht = ws.get("lv_ht", (R,), torch.float64, dev)
+        hflag = ws.get("lv_hflag", (R,), torch.uint8, dev)
+        bad = ws.get("lv_bad", (2,), torch.int32, dev)
+        self.ensure_vertices(R)
+        T = self.tables()
+        rsig = ws.get("lv_rsig", (R, d + 1), torch.int32, dev)
+        slot = ws.get("lv_slot", (R,), torch.int64, dev)
+        newf = ws.get("lv_newf", (R,), torch.int32, dev)
+        escf = ws.get("lv_escf", (R,), torch.int32, dev)
+        noff = ws.get("lv_noff", (R,), torch.int64, dev)
+        eoff = ws.get("lv_eoff", (R,), torch.int64, dev)
+        counts = np.zeros(5, dtype=np.int64)
+        ns = self.ns
+        ix = ns.prune_index(dev)
+        s32 = ns.screen32(dev)
+        _lib.check(L.vr_trav_level_cast(
+            ctypes.byref(T), p(self.rec), ns.n, d, self.sqmax, ctypes.byref(s32.struct),
+            ctypes.byref(ix.struct), p(fs), p(fr), F, p(open_mask), p(off), R, lvl, p(rx), p(ru),
+            p(reta), p(rpar), p(hidx), p(ht), p(hflag), p(rsig), p(slot), p(newf), p(escf),
+            p(noff), p(eoff), p(bad), p(self.work), counts.ctypes.data, sh), "level_cast")
+        n_new, n_esc, n_deg, n_bad, ovf = (int(v) for v in counts)
+        if n_bad:
+            raise DegenerateConfiguration("generators of a frontier vertex are affinely dependent")
+        if n_deg:
+            raise DegenerateConfiguration(
+                f"{n_deg} edge raycasts hit a generator on the circumsphere band")
+        if ovf:
+            raise RuntimeError("traversal hash table overflow")
+        self.ensure_edges((d + 1) * n_new)
+        T = self.tables()
+        _lib.check(L.vr_trav_finalize(ctypes.byref(T), p(self.rec), d, p(rsig), p(slot),
+                                      p(newf), p(noff), R, f1, p(self.vsig), p(self.vr),
+                                      p(bad[1:]), sh), "finalize")
+        self.e_ub += (d + 1) * n_new
+        if n_esc:
+            self.ensure_boundary(n_esc)
+            _lib.check(L.vr_trav_boundary(d, p(escf), p(eoff), p(rpar), p(ru), R, p(fs), self.nb,
+                                          p(self.bsig), p(self.bu), sh), "boundary")
+            self.nb += n_esc
+        self.nv = f1 + n_new
+        self.rays_last = R
+        return n_new
+
     def level(self, f0, f1, lvl, stats=None, ws=None, raycast_fn=None):
         """Expand frontier vertices [f0, f1); returns the number of new vertices.
 
         raycast_fn(x, u, eta) -> (idx int32, flag uint8) replaces the local
         fused RayCast (parallel.ShardedRaycast splits the level's rays across
         ranks and all-gathers the hits)."""
+        if raycast_fn is None and self.native and self.ns.n >= PRUNE_MIN_GENERATORS:
+            return self._level_native(f0, f1, lvl, stats, ws)
         d, L, dev, sh = self.d, self.L, self.dev, self._sh()
         F = f1 - f0
         fs = self.vsig[f0:f1]

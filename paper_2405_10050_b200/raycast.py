@@ -110,7 +110,9 @@ class Workspace:
 
     def get(self, name, shape, dtype, dev):
         t = self._bufs.get(name)
-        n = int(np.prod(shape))
+        n = 1
+        for s in shape:  # (np.prod costs ~5 us; the traversal calls this ~15x per level)
+            n *= int(s)
         if t is None or t.numel() < n or t.dtype != dtype or t.device != dev:
             t = torch.empty(max(n, 1), dtype=dtype, device=dev)
             self._bufs[name] = t
@@ -270,9 +272,11 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
         events[0].record(stream)
     if pruned:
         ix = ns.prune_index(dev)
-        cur = torch.cuda.current_stream() if stream is None else stream
-        with torch.cuda.stream(cur):
+        if stream is None:
             order = coherent_order(ix, ed, ud)
+        else:
+            with torch.cuda.stream(stream):
+                order = coherent_order(ix, ed, ud)
         _lib.check(L.vr_raycast_pruned(_lib.ptr(rec), ns.n, d, sqmax, s32p, ctypes.byref(ix.struct),
                                        _lib.ptr(xd), _lib.ptr(ud), _lib.ptr(ed), k, n,
                                        _lib.ptr(order), _lib.ptr(idx), _lib.ptr(t),

@@ -212,3 +212,37 @@ def test_config5_local_balls_match_reference():
     assert got == union
     ok = vb.verify_vertices(ns, mesh.arrays()["sigma"][::13], mesh.arrays()["r"][::13])
     assert ok.all()
+
+
+_LEVEL_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2405_10050_b200 as vb
+out = {}
+for name, pts in (("u4", np.random.default_rng(21).random((3000, 4))),
+                  ("g5", np.random.default_rng(22).standard_normal((2500, 5)))):
+    a = vb.voronoi_graph(vb.NodeSet(pts), seed=0).arrays()
+    for k in ("sigma", "r", "edge_key", "edge_count", "boundary_sigma", "boundary_u"):
+        out[name + "_" + k] = a[k]
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_native_level_driver_matches_python_levels(tmp_path):
+    """The native level driver (csrc/level.cu, default) and the Python-driven
+    level (VR_NATIVE_LEVEL=0, read once per traversal object; subprocesses)
+    produce identical meshes: vertex sigma / coordinates (bitwise, in id
+    order), edge keys and counts, boundary rays."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("1", "0"):
+        path = str(tmp_path / f"lv{mode}.npz")
+        p = subprocess.run([sys.executable, "-c", _LEVEL_SCRIPT, root, path],
+                           env=dict(os.environ, VR_NATIVE_LEVEL=mode), capture_output=True,
+                           text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[mode] = np.load(path)
+    for k in res["1"].files:
+        assert np.array_equal(res["1"][k], res["0"][k]), k

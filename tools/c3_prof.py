@@ -1,5 +1,6 @@
-"""Host profile of the config-3 full diagram (N=10,000, d=5, Gaussian):
-per-level overhead of the level-synchronous traversal (second run)."""
+"""Host profile of a full-diagram traversal: config 3 (N=10,000, d=5,
+Gaussian; default) or config 1 (argument "1": N=1,000, d=3, uniform):
+per-level overhead of the level-synchronous traversal (after warm runs)."""
 import cProfile
 import os
 import pstats
@@ -12,7 +13,10 @@ import torch  # noqa: E402
 
 import paper_2405_10050_b200 as vb  # noqa: E402
 
-pts = np.random.default_rng(0).standard_normal((10000, 5))
+if len(sys.argv) > 1 and sys.argv[1] == "1":
+    pts = np.random.default_rng(0).random((1000, 3))
+else:
+    pts = np.random.default_rng(0).standard_normal((10000, 5))
 ns = vb.NodeSet(pts)
 ns.prune_index()
 for i in range(3):
