@@ -457,39 +457,44 @@ def run_ours(args):
         ex64 = n * N_GEN * FLOP_PER_PAIR / (ex_ms["fp64"] * 1e-3) / 1e12
         ex32 = n * N_GEN * FLOP_PER_PAIR / (ex_ms["fp32"] * 1e-3) / 1e12
         traffic = profiled_traffic()
+        tc_on = mma_on and args.mode == "pruned"
+        # FFMA-equivalent view: the screen's d-dot (2d flop per screened
+        # pair) against the live FFMA peak (the packed-FFMA2 build's pipe)
+        cuda_core = {"bound": "fp32", "achieved": achieved, "peak": peak32, "unit": "TFLOP/s",
+                     "frac": achieved / peak32, "flop_per_pair": FLOP_PER_PAIR,
+                     "peak_source": "measured live: FFMA probe (vr_fma_probe dtype 1)"}
+        common = {"traffic": traffic,
+                  "kernel": ("k_raycast_pruned<6,R=1,tile=64,tensor-core screen>" if tc_on else
+                             "k_raycast_pruned<6,R=1,tile=64,fp32 screen>"
+                             if args.mode == "pruned" else "k_raycast<6,2,128,256,4,3>"),
+                  "kernel_ms": kms, "pairs_per_launch": pairs, "pairs_per_ray": pairs / n,
+                  "work_counters": counters if args.mode == "pruned" else None,
+                  "screen": ("tensor-core (mma.sync tf32: sphere + halfspace products) + fp64 rare path"
+                             if tc_on else "packed FFMA2 fp32 + fp64 rare path"),
+                  "unit_of_work": "(ray, generator) pair screened; the pruned kernel counts "
+                                  "the pairs it actually screened (work counter)",
+                  "traffic_source": "profiles/r1_k_raycast_pruned_ncu_full.txt",
+                  "note": "latency-bound (tree walk, fp64 rare path): neither pipe saturates; "
+                          "see DESIGN.md section 2"}
+        if tc_on:
+            # the screen runs on the warp tensor path: its tf32 product
+            # [z, 1, c] . [x, |x|^2, 1] is 2 (d + 2) flop per screened pair
+            tc_ach = pairs * 2 * (DIM + 2) / (kms * 1e-3) / 1e12
+            roofline = {"bound": "tensor", "achieved": tc_ach, "peak": peak_tc, "unit": "TFLOP/s",
+                        "frac": tc_ach / peak_tc, "flop_per_pair": 2 * (DIM + 2),
+                        "peak_source": "measured live: tf32 mma.sync m16n8k8 probe (vr_fma_probe "
+                                       "dtype 2), the instruction the screen issues",
+                        "frac_of_tcgen05_tf32_nominal": tc_ach / 1100.0,
+                        "cuda_core_equivalent": cuda_core, **common}
+        else:
+            roofline = {**cuda_core, **common}
         result = {
             "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded config-2 recipe, SURVEY.md §8(d))",
             "config": arm_config(world, n),
-            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak32,
-                         "unit": "TFLOP/s", "frac": achieved / peak32, "traffic": traffic,
-                         "kernel": ("k_raycast_pruned<6,R=1,tile=64,fp32 screen>"
-                                    if args.mode == "pruned" else "k_raycast<6,2,128,256,4,3>"),
-                         "kernel_ms": kms, "flop_per_pair": FLOP_PER_PAIR,
-                         "pairs_per_launch": pairs, "pairs_per_ray": pairs / n,
-                         "work_counters": counters if args.mode == "pruned" else None,
-                         "screen": ("tensor-core (mma.sync tf32: sphere + halfspace products) + fp64 rare path"
-                                    if os.environ.get("VR_MMA", "1") != "0"
-                                    else "packed FFMA2 fp32 + fp64 rare path"),
-                         "unit_of_work": "(ray, generator) pair screened; pruned kernel counts "
-                                         "the pairs it actually screened (work counter)",
-                         "peak_source": "measured live: FFMA probe (vr_fma_probe); "
-                                        "MEASURED_PEAKS.json has no FP32/FP64 figure",
-                         "traffic_source": "profiles/r1_k_raycast_pruned_ncu_full.txt",
-                         # the screen itself runs on the warp tensor path: its
-                         # tf32 product is 2 (d + 2) flop per screened pair
-                         # (features [x, |x|^2, 1]), against the live mma.sync peak
-                         "tensor_pipe": ({
-                             "bound": "tensor", "unit": "TFLOP/s",
-                             "flop_per_pair": 2 * (DIM + 2),
-                             "achieved": pairs * 2 * (DIM + 2) / (kms * 1e-3) / 1e12,
-                             "peak": peak_tc,
-                             "frac": pairs * 2 * (DIM + 2) / (kms * 1e-3) / 1e12 / peak_tc,
-                             "peak_source": "measured live: tf32 mma.sync m16n8k8 probe "
-                                            "(vr_fma_probe dtype 2)"}
-                             if mma_on and args.mode == "pruned" else None)},
+            "roofline": roofline,
             "roofline_exhaustive": {
                 "fp64_screen": {"bound": "fp64", "kernel_ms": ex_ms["fp64"], "achieved": ex64,
                                 "peak": peak64, "unit": "TFLOP/s", "frac": ex64 / peak64,
