@@ -14,15 +14,28 @@ from paper_2405_10050_b200.raycast import HostRaycaster  # noqa: E402
 n, d = 1_000_000, 6
 pts = np.random.default_rng(0).random((20000, d))
 ns = vb.NodeSet(pts)
-rng = np.random.default_rng(3)
-g = rng.integers(0, 20000, n).astype(np.int32)
-u = rng.standard_normal((n, d))
-u /= np.linalg.norm(u, axis=1, keepdims=True)
+if len(sys.argv) > 1 and sys.argv[1] == "config2":
+    # the bench's config-2 rays (descent-vertex origins)
+    import bench
+    s, p_all, u_all = bench.ray_recipe(n)
+    need = np.unique(p_all)
+    sig_n, r_n = vb.descent_batch(ns, s[need], seed=0)
+    pool_sig = np.zeros((bench.N_POOL, d + 1), dtype=np.int32)
+    pool_r = np.zeros((bench.N_POOL, d))
+    pool_sig[need], pool_r[need] = sig_n, r_n
+    xv, u, g1 = bench.assemble(pts, pool_sig, pool_r, p_all, u_all)
+    g = g1[:, 0]
+else:
+    rng = np.random.default_rng(3)
+    g = rng.integers(0, 20000, n).astype(np.int32)
+    u = rng.standard_normal((n, d))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    xv = pts[g]
 P = HostRaycaster.pinned
 hx, hu, hg = P((n, d), torch.float64), P((n, d), torch.float64), P((n, 1), torch.int32)
-hx.copy_(torch.from_numpy(pts[g]))
+hx.copy_(torch.from_numpy(np.ascontiguousarray(xv)))
 hu.copy_(torch.from_numpy(u))
-hg.copy_(torch.from_numpy(g[:, None].copy()))
+hg.copy_(torch.from_numpy(np.ascontiguousarray(g[:, None], dtype=np.int32)))
 dx = torch.empty((n, d), dtype=torch.float64, device="cuda")
 for name, src, dst in (("H2D 48MB", hx, dx), ("D2H 48MB", dx, hx)):
     dst.copy_(src, non_blocking=True)
