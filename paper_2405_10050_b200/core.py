@@ -390,7 +390,8 @@ class PruneIndex:
         self.wide_box32 = torch.cat(boxes).contiguous()
         # tensor-core screen operand (used from d = 5): rec32 rows in mma B-fragment order
         self.recB = None
-        if PRUNE_TILE == 64 and d >= 5 and os.environ.get("VR_MMA", "1") != "0":
+        if PRUNE_TILE == 64 and d >= int(os.environ.get("VR_MMA_MIN_D", "5")) and \
+                os.environ.get("VR_MMA", "1") != "0":
             ks = (d + 2 + 7) // 8
             self.recB = torch.empty((rows, 8 * ks), dtype=torch.float32, device=dev)
             L = _lib.lib()

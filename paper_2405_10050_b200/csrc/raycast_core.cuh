@@ -2085,7 +2085,10 @@ int launch_pruned_f(const Src& src, int64_t n_rays, const PrunedIndex& ix, const
 #endif
   // tensor-core screen from d = 5 (config 4, d = 4: 0.126 vs 0.118 s with
   // the packed-FFMA2 screen, whose cost scales with d)
-  if constexpr (F32 && PRUNE_TILE == 64 && D >= 5) {
+#ifndef VR_MMA_MIN_D
+#define VR_MMA_MIN_D 5
+#endif
+  if constexpr (F32 && PRUNE_TILE == 64 && D >= VR_MMA_MIN_D) {
     if (ix.crecB && ix.crec32s && mma_mode() != 0)
       return launch_pruned_rm<D, 1, MMA_MINB, F32, Src, true>(src, n_rays, ix, fr, out, st, work);
   }
