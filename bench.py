@@ -323,9 +323,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # VR_DIST_BACKEND=gloo is a functional check of the multi-rank path on a
+    # box with fewer GPUs than ranks (ranks share a GPU; no kernel waits on
+    # another rank, the collectives run on the host) -- its numbers mean nothing
+    backend = os.environ.get("VR_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     L = _lib.lib()
 
     pts = generators()

@@ -661,16 +661,16 @@ class DeviceTraversal:
         return keys, cnt  # hash order; Mesh sorts lexicographically on materialisation
 
 
-def _level_raycaster(ns, stats, group):
+def _level_raycaster(ns, stats, group, work=None):
     """None (local fused RayCast) or a ShardedRaycast over the ranks of the
-    default / given process group."""
+    default / given process group (`work`: this rank's kernel work counters)."""
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
         return None
     from .parallel import ShardedRaycast
 
     def fn(x, u, eta):
-        r = raycast_batch(ns, x, u, eta, want_rp=False, stats=stats)
+        r = raycast_batch(ns, x, u, eta, want_rp=False, stats=stats, work=work)
         return r.idx, r.flag
 
     return ShardedRaycast(fn, group)
@@ -697,7 +697,7 @@ def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heurist
     ws = Workspace()
     f0, f1, lvl = 0, 1, 1
     levels = []
-    rfn = _level_raycaster(ns, stats, group)
+    rfn = _level_raycaster(ns, stats, group, tr.work)
     while f1 > f0:
         n_new = tr.level(f0, f1, lvl, stats=stats, ws=ws, raycast_fn=rfn)
         levels.append((f1 - f0, n_new))
@@ -733,7 +733,7 @@ def voronoi_local(ns: NodeSet, starts, hops: int, seed: int = 0, stats: RaycastS
     ws = Workspace()
     f0, f1 = 0, tr.nv
     bounds = [(0, f1)]
-    rfn = _level_raycaster(ns, stats, group)
+    rfn = _level_raycaster(ns, stats, group, work)
     for lvl in range(1, hops + 1):
         if f1 == f0:
             break
