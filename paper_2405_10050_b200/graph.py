@@ -723,7 +723,21 @@ def voronoi_local(ns: NodeSet, starts, hops: int, seed: int = 0, stats: RaycastS
     """
     if stats is None:
         stats = RaycastStats()
-    sig, _ = descent_batch(ns, starts, seed=seed, stats=stats)
+    import torch.distributed as dist
+    size = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    if size > 1:
+        # each rank descends its contiguous share of the starts (every start
+        # has its own stream, so the result does not depend on the sharding);
+        # one all-gather of the sigmas
+        from .parallel import allgather_rows, shard_bounds
+        starts = np.asarray([int(s) for s in starts], dtype=np.int64)
+        lo, hi = shard_bounds(len(starts), size, dist.get_rank(group))
+        part, _ = descent_batch(ns, starts[lo:hi], seed=seed, stats=stats)
+        dev = ns.device_records()[0].device
+        sig = allgather_rows(torch.as_tensor(part.reshape(-1, ns.dim + 1), device=dev),
+                             group).cpu().numpy()
+    else:
+        sig, _ = descent_batch(ns, starts, seed=seed, stats=stats)
     _, first = np.unique(sig, axis=0, return_index=True)
     sig = sig[np.sort(first)]
     tr = DeviceTraversal(ns, vcap_hint=max(4 * ns.n, 6 * len(sig) * 4 ** min(hops, 8)))

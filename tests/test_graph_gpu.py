@@ -246,3 +246,49 @@ def test_native_level_driver_matches_python_levels(tmp_path):
         res[mode] = np.load(path)
     for k in res["1"].files:
         assert np.array_equal(res["1"][k], res["0"][k]), k
+
+
+_SHARDED_SCRIPT = r"""
+import os, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, sys.argv[1])
+import paper_2405_10050_b200 as vb
+torch.cuda.set_device(0)          # both ranks on one GPU: host (gloo) collectives only
+dist.init_process_group("gloo")
+pts = np.random.default_rng(31).random((20000, 5))
+ns = vb.NodeSet(pts)
+seeds = np.random.default_rng(32).choice(20000, 150, replace=False)
+m, lv = vb.voronoi_local(ns, seeds, hops=3, return_levels=True)
+a = m.arrays()
+if dist.get_rank() == 0:
+    sig = a["sigma"]
+    order = np.lexsort(sig.T[::-1])
+    np.savez(sys.argv[2], sigma=sig[order], level=lv[order])
+dist.destroy_process_group()
+"""
+
+
+def test_sharded_local_traversal_matches_single_rank(tmp_path):
+    """voronoi_local over two ranks (gloo; descents and level raycasts
+    sharded, hits all-gathered) returns the single-rank vertex set with the
+    same hop levels.  Both ranks share the one GPU: the collectives run on
+    the host, no kernel waits on another rank."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "sharded.py"
+    script.write_text(_SHARDED_SCRIPT)
+    out = str(tmp_path / "sharded.npz")
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", "29533", str(script), root, out],
+                       capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    got = np.load(out)
+    pts = np.random.default_rng(31).random((20000, 5))
+    ns = vb.NodeSet(pts)
+    seeds = np.random.default_rng(32).choice(20000, 150, replace=False)
+    m, lv = vb.voronoi_local(ns, seeds, hops=3, return_levels=True)
+    sig = m.arrays()["sigma"]
+    order = np.lexsort(sig.T[::-1])
+    assert np.array_equal(sig[order], got["sigma"])
+    assert np.array_equal(lv[order], got["level"])
