@@ -154,6 +154,14 @@ def main():
             tot_mean += w.float().mean(1).sum().item()
         print(f"  groups of {gs:2d} rays: union tiles/group {tot_mean / nw:7.2f}, "
               f"max over the warp's groups {tot_max / nw:7.2f}")
+    for gsz in (64, 128):  # larger groups (2 / 4 rays per lane, or CTA-wide)
+        tot_g = 0
+        for lo in range(0, n, CH):
+            sel = o[lo:lo + CH]
+            m = need_mask(ix, xd[sel], ud[sel], gl[sel], t[sel], X, d)
+            tot_g += m.view(-1, gsz, m.shape[1]).any(1).sum().item()
+        print(f"  groups of {gsz:3d} rays: union tiles/group {tot_g / (n // gsz):7.2f} "
+              f"({tot_g / (n // gsz) / gsz:.3f} per ray)")
     print(f"tiles total {ix.tile_box.shape[0]}; per-ray need (final sphere) {per_ray / n:.2f}")
     for k in orders:
         print(f"  {k:32s} union tiles/warp {acc[k]:7.2f}")
