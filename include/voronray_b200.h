@@ -250,6 +250,16 @@ int vr_verify_vertices(const double* rec, int64_t n_gen, int d,
 int vr_circumcenters(const double* rec, int d, const int32_t* sigma,
                      int64_t n_v, double* out_r, uint8_t* out_ok, void* stream);
 
+/* Descent directions (graph.py:46-85): for each of n starts with sigma
+ * (n, d+1) holding k[i] valid entries, the two-pass modified Gram-Schmidt
+ * basis of x_sigma[j] - x_sigma[0] (j = 1 .. k-1; raycast.py:295-308) and
+ * the component out_v of the drawn normal z (n, d) orthogonal to it (two
+ * passes, raycast.py:311-317), its norm out_nrm, and out_bad = 1 where the
+ * rows are affinely dependent (|v| < tol * max(|v0|, 1)). */
+int vr_descent_directions(const double* rec, int d, const int32_t* sigma, const int32_t* k,
+                          const double* z, int64_t n, double tol, double* out_v,
+                          double* out_nrm, uint8_t* out_bad, void* stream);
+
 /* Outward edge directions of vertices (reference _vertex_directions,
  * raycast.py:345-378): column k-1 of -D^{-1} (k>0) or the row sums of D^{-1}
  * (k=0), D rows x_s - x_s0, normalised.  out_u is (n_v, d+1, d);

@@ -253,6 +253,71 @@ __global__ void k_pack_mma(const float* __restrict__ rec32, int64_t rows, float*
   }
 }
 
+// Descent directions (graph.py:46-85, raycast.py:295-317): per start, the
+// two-pass modified Gram-Schmidt basis of the rows x_sigma[i] - x_sigma[0]
+// (i = 1 .. k-1, the reference's _orthonormal_rows) and the component of the
+// drawn normal z orthogonal to it (two passes, _project_out), one thread per
+// start.  bad = the rows are affinely dependent (|v| < tol max(|v0|, 1)).
+template <int D>
+__global__ void k_descent_dirs(const double* __restrict__ rec, const int32_t* __restrict__ sigma,
+                               const int32_t* __restrict__ kcount, const double* __restrict__ z,
+                               int64_t n, double tol, double* __restrict__ out_v,
+                               double* __restrict__ out_nrm, uint8_t* __restrict__ out_bad) {
+  constexpr int S = rec_stride(D);
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int k = kcount[s];
+  const int32_t* sg = sigma + s * (D + 1);
+  const double* x0 = rec + (int64_t)sg[0] * S;
+  double q[D][D];  // orthonormal rows 0 .. k-2
+  bool bad = false;
+  for (int j = 0; j + 1 < k; ++j) {
+    const double* xa = rec + (int64_t)sg[j + 1] * S;
+    double v[D];
+    double n0 = 0.0;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      v[c] = xa[c] - x0[c];
+      n0 += v[c] * v[c];
+    }
+    n0 = sqrt(n0);
+    for (int pass = 0; pass < 2; ++pass)
+      for (int i = 0; i < j; ++i) {
+        double dot = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) dot += q[i][c] * v[c];
+#pragma unroll
+        for (int c = 0; c < D; ++c) v[c] -= dot * q[i][c];
+      }
+    double nv = 0.0;
+#pragma unroll
+    for (int c = 0; c < D; ++c) nv += v[c] * v[c];
+    nv = sqrt(nv);
+    if (nv < tol * fmax(n0, 1.0)) bad = true;
+#pragma unroll
+    for (int c = 0; c < D; ++c) q[j][c] = v[c] / nv;
+  }
+  double w[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) w[c] = z[s * D + c];
+  for (int pass = 0; pass < 2; ++pass)
+    for (int i = 0; i + 1 < k; ++i) {
+      double dot = 0.0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) dot += q[i][c] * w[c];
+#pragma unroll
+      for (int c = 0; c < D; ++c) w[c] -= dot * q[i][c];
+    }
+  double nw = 0.0;
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    nw += w[c] * w[c];
+    out_v[s * D + c] = w[c];
+  }
+  out_nrm[s] = sqrt(nw);
+  out_bad[s] = bad ? 1 : 0;
+}
+
 inline unsigned blocks_for(int64_t n, int nt) { return (unsigned)((n + nt - 1) / nt); }
 
 }  // namespace
@@ -336,6 +401,19 @@ extern "C" int vr_circumcenters(const double* rec, int d, const int32_t* sigma, 
   VR_DISPATCH_D(d, {
     k_circumcenters<D><<<blocks_for(n_v, 128), 128, 0, as_stream(stream)>>>(rec, sigma, n_v,
                                                                               out_r, out_ok);
+  });
+  VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_descent_directions(const double* rec, int d, const int32_t* sigma,
+                                     const int32_t* k, const double* z, int64_t n, double tol,
+                                     double* out_v, double* out_nrm, uint8_t* out_bad,
+                                     void* stream) {
+  if (!rec || !sigma || !k || !z || !out_v || !out_nrm || !out_bad) return VR_EINVAL;
+  if (n <= 0) return VR_OK;
+  VR_DISPATCH_D(d, {
+    k_descent_dirs<D><<<blocks_for(n, 128), 128, 0, as_stream(stream)>>>(
+        rec, sigma, k, z, n, tol, out_v, out_nrm, out_bad);
   });
   VR_RETURN_LAUNCH();
 }

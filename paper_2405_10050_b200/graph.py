@@ -108,6 +108,25 @@ def _mgs_batch(rows):
     return out
 
 
+def _descent_directions(ns, sigma, kcount, z):
+    """(v, |v|, bad) for each start: the draw z projected out of the
+    Gram-Schmidt basis of its sigma rows (vr_descent_directions)."""
+    rec, _ = ns.device_records()
+    dev = rec.device
+    L = _lib.lib()
+    n, d = z.shape
+    sd = torch.as_tensor(np.ascontiguousarray(sigma, dtype=np.int32), device=dev)
+    kd = torch.as_tensor(np.ascontiguousarray(kcount, dtype=np.int32), device=dev)
+    zd = torch.as_tensor(np.ascontiguousarray(z, dtype=np.float64), device=dev)
+    v = torch.empty((n, d), dtype=torch.float64, device=dev)
+    nrm = torch.empty(n, dtype=torch.float64, device=dev)
+    bad = torch.empty(n, dtype=torch.uint8, device=dev)
+    _lib.check(L.vr_descent_directions(_lib.ptr(rec), d, _lib.ptr(sd), _lib.ptr(kd), _lib.ptr(zd),
+                                       n, RANK_TOL, _lib.ptr(v), _lib.ptr(nrm), _lib.ptr(bad),
+                                       _lib.stream_handle()), "vr_descent_directions")
+    return v.cpu().numpy(), nrm.cpu().numpy(), bad.cpu().numpy().astype(bool)
+
+
 def _project_out_batch(w, basis):
     """Component of each w (m, d) orthogonal to its basis rows (m, k, d)."""
     v = w.copy()
@@ -194,7 +213,6 @@ def descent_batch(ns: NodeSet, starts, seed: int = 0, stats: RaycastStats = None
     sig[:, 0] = starts
     k = np.ones(S, dtype=np.int64)          # |sigma|
     rr = pts[starts].astype(np.float64).copy()
-    basis = np.zeros((S, d, d))             # orthonormal rows, first k-1 valid
     fails = np.zeros(S, dtype=np.int64)
     active = np.arange(S)
     while active.size:
@@ -205,22 +223,32 @@ def descent_batch(ns: NodeSet, starts, seed: int = 0, stats: RaycastStats = None
         # direction drawn for their previous level.
         k_act = k[active].copy()
         levels = np.unique(k_act)
-        u = np.empty((active.size, d))
+        # one draw per active start from its own stream (stream order is per
+        # start, so drawing level group by level group is the same draw)
+        z = np.empty((active.size, d))
         for kk in levels:
             grp = active[k_act == kk]
-            pos = np.searchsorted(active, grp)
-            z = draws.take(grp)
-            v = _project_out_batch(z, basis[grp, :kk - 1])
-            nrm = np.linalg.norm(v, axis=1)
-            for m in np.nonzero(nrm < 1e-9)[0]:  # free redraws (graph.py:72-74)
-                a = grp[m]
-                while True:
-                    vv = _project_out_batch(draws.take(np.array([a])), basis[a:a + 1, :kk - 1])[0]
-                    if np.linalg.norm(vv) >= 1e-9:
-                        v[m] = vv
-                        nrm[m] = np.linalg.norm(vv)
-                        break
-            u[pos] = v / nrm[:, None]
+            z[np.searchsorted(active, grp)] = draws.take(grp)
+        # Gram-Schmidt basis of each start's sigma rows and the projection of
+        # its draw, one GPU thread per start (vr_descent_directions; the
+        # numpy restatement _mgs_batch / _project_out_batch below serves the
+        # rare redraws)
+        v, nrm, bad = _descent_directions(ns, sig[active], k_act, z)
+        if bad.any():
+            a = active[np.argmax(bad)]
+            raise DegenerateConfiguration(
+                f"generators are affinely dependent (descent from node {int(starts[a])})")
+        for m in np.nonzero(nrm < 1e-9)[0]:  # free redraws (graph.py:72-74)
+            a, kk = active[m], int(k_act[m])
+            diffs = pts[sig[a, 1:kk]] - pts[sig[a, 0]]
+            bas = _mgs_batch(diffs[None]) if kk > 1 else np.zeros((1, 0, d))
+            while True:
+                vv = _project_out_batch(draws.take(np.array([a])), bas)[0]
+                if np.linalg.norm(vv) >= 1e-9:
+                    v[m] = vv
+                    nrm[m] = np.linalg.norm(vv)
+                    break
+        u = v / nrm[:, None]
         still = []
         # one RayCast for the whole round: eta is padded with copies of its
         # first entry g (thr is a max over eta and g = eta[0], so the padded
@@ -254,8 +282,6 @@ def descent_batch(ns: NodeSet, starts, seed: int = 0, stats: RaycastStats = None
                 fails[g_ok] = 0
                 cont = g_ok if kk + 1 < d + 1 else g_ok[:0]
                 if cont.size:
-                    diffs = pts[sig[cont, 1:kk + 1]] - pts[sig[cont, 0]][:, None, :]
-                    basis[cont, :kk] = _mgs_batch(diffs)
                     still.extend(cont.tolist())
         active = np.array(sorted(still), dtype=np.int64)
     return sig.astype(np.int32), rr

@@ -206,7 +206,18 @@ def test_descent_batch_host_logic_with_escapes(monkeypatch):
     class _NS:
         points, dim, n = pts, 4, 120
 
+    def numpy_directions(ns, sigma, kcount, z):
+        # host restatement of vr_descent_directions (the device kernel)
+        v = np.empty_like(z)
+        bad = np.zeros(len(z), dtype=bool)
+        for i, (sg, kk) in enumerate(zip(sigma, kcount)):
+            diffs = pts[sg[1:kk]] - pts[sg[0]]
+            bas = G._mgs_batch(diffs[None]) if kk > 1 else np.zeros((1, 0, 4))
+            v[i] = G._project_out_batch(z[i:i + 1], bas)[0]
+        return v, np.linalg.norm(v, axis=1), bad
+
     monkeypatch.setattr(G, "raycast_batch", fake_raycast)
+    monkeypatch.setattr(G, "_descent_directions", numpy_directions)
     starts = np.arange(120)
     sig, r = G.descent_batch(_NS(), starts, seed=0)
     nodes = orc.Nodes(pts)
