@@ -219,7 +219,9 @@ import sys, numpy as np
 sys.path.insert(0, sys.argv[1])
 import paper_2405_10050_b200 as vb
 out = {}
-for name, pts in (("u4", np.random.default_rng(21).random((3000, 4))),
+for name, pts in (("u2", np.random.default_rng(23).random((5000, 2))),
+                  ("g3", np.random.default_rng(24).standard_normal((4000, 3))),
+                  ("u4", np.random.default_rng(21).random((3000, 4))),
                   ("g5", np.random.default_rng(22).standard_normal((2500, 5)))):
     a = vb.voronoi_graph(vb.NodeSet(pts), seed=0).arrays()
     for k in ("sigma", "r", "edge_key", "edge_count", "boundary_sigma", "boundary_u"):
