@@ -11,23 +11,6 @@ constexpr int RED_NT = 256;
 constexpr int RED_CHUNK = 1024;   // rays per reduction chunk (4 per thread)
 constexpr int RED_MAPCAP = 1024;  // smem face map capacity (max_faces <= 512)
 
-__device__ __forceinline__ void bitonic_sort_u64(unsigned long long* keys, int n) {
-  // n is a power of two; ascending.
-  for (int k = 2; k <= n; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int l = i ^ j;
-        if (l > i) {
-          const unsigned long long a = keys[i], b = keys[l];
-          const bool up = (i & k) == 0;
-          if ((a > b) == up) { keys[i] = b; keys[l] = a; }
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
 // Integrand on the device for the CLI's built-ins (reference integrands.py):
 // kind 1 const c, 2 sin(x_1^2), 3 linear a.x + b.
 struct Integ {
@@ -68,7 +51,7 @@ __global__ void __launch_bounds__(RED_NT)
                 double* out_vol_integral) {
   constexpr int S = rec_stride(D);
   constexpr int CH = INTEG ? 512 : RED_CHUNK;  // rays per chunk (smem budget)
-  __shared__ unsigned long long keys[RED_MAPCAP];
+  __shared__ unsigned long long keys[CH];  // (face << 32 | ray) per ray of the chunk, ~0 if none
   __shared__ double wv[CH];
   __shared__ double lv[CH];
   __shared__ double sv[INTEG ? CH : 1];   // f(rp) w          (integrate_mc.py:350)
@@ -76,8 +59,11 @@ __global__ void __launch_bounds__(RED_NT)
   __shared__ int mkey[RED_MAPCAP];
   __shared__ double macc[RED_MAPCAP];
   __shared__ double macc2[INTEG ? RED_MAPCAP : 1];
+  __shared__ int rslot[CH];          // face-map slot of each ray of the chunk (-1: none)
+  __shared__ int flist[RED_MAPCAP];  // slots in use, in insertion order
   __shared__ unsigned long long first_bad;  // (ray << 2) | kind
-  __shared__ int nused;
+  __shared__ int nused;  // faces (+ RED_MAPCAP per face that found no slot: OVERFLOW)
+  __shared__ int nface;  // entries of flist
 
   const int64_t c = blockIdx.x;
   const int64_t per = src.per;
@@ -88,8 +74,8 @@ __global__ void __launch_bounds__(RED_NT)
     macc[i] = 0.0;
     if (INTEG) macc2[i] = 0.0;
   }
-  if (threadIdx.x == 0) { first_bad = ~0ull; nused = 0; }
-  double vol = 0.0, fvol = 0.0;  // thread 0 only: sequential sums in ray order
+  if (threadIdx.x == 0) { first_bad = ~0ull; nused = 0; nface = 0; }
+  double vol = 0.0, fvol = 0.0;  // lane 0 of the last warp: sequential sums in ray order
   __syncthreads();
 
   for (int64_t start = 0; start < per; start += CH) {
@@ -156,57 +142,86 @@ __global__ void __launch_bounds__(RED_NT)
         fv[s] = fl_v;
       }
     }
-    for (int s = CH + threadIdx.x; s < RED_MAPCAP; s += RED_NT) keys[s] = ~0ull;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int s = 0; s < cnt; ++s) {
+    // Each ray's face slot (insert-or-find in the face map; a new face is
+    // appended to flist).
+    for (int s = threadIdx.x; s < cnt; s += RED_NT) {
+      const unsigned long long key = keys[s];
+      int slot = -1;
+      if (key != ~0ull) {
+        const uint32_t j = (uint32_t)(key >> 32);
+        unsigned h = (j * 2654435761u) & (RED_MAPCAP - 1);
+        for (int probe = 0; probe < RED_MAPCAP; ++probe) {
+          const int prev = atomicCAS(&mkey[h], -1, (int)j);
+          if (prev == -1) {
+            atomicAdd(&nused, 1);
+            flist[atomicAdd(&nface, 1)] = (int)h;
+            slot = (int)h;
+            break;
+          }
+          if (prev == (int)j) { slot = (int)h; break; }
+          h = (h + 1) & (RED_MAPCAP - 1);
+        }
+        if (slot < 0) atomicAdd(&nused, RED_MAPCAP);  // map full: reported as OVERFLOW
+      }
+      rslot[s] = slot;
+    }
+    __syncthreads();
+    constexpr int NWR = RED_NT / 32;
+    if (threadIdx.x == RED_NT - 32) {  // volume: sequential sum in ray order (integrate_mc.py:156),
+      for (int s = 0; s < cnt; ++s) {  // on the last warp, which takes no faces
         vol += lv[s];
         if (INTEG) fvol += fv[s];
       }
     }
-    bitonic_sort_u64(keys, CH);
-    for (int p = threadIdx.x; p < CH; p += RED_NT) {
-      const unsigned long long key = keys[p];
-      if (key == ~0ull) continue;
-      const uint32_t j = (uint32_t)(key >> 32);
-      if (p > 0 && (uint32_t)(keys[p - 1] >> 32) == j) continue;  // not a segment head
-      double sum = 0.0, sum2 = 0.0;  // ray order inside the segment (keys sorted by (j, ray))
-      for (int q = p; q < CH && keys[q] != ~0ull && (uint32_t)(keys[q] >> 32) == j; ++q) {
-        sum += wv[keys[q] & 0xffffffffu];
-        if (INTEG) sum2 += sv[keys[q] & 0xffffffffu];
-      }
-      unsigned h = (j * 2654435761u) & (RED_MAPCAP - 1);
-      bool placed = false;
-      for (int probe = 0; probe < RED_MAPCAP; ++probe) {
-        const int prev = atomicCAS(&mkey[h], -1, (int)j);
-        if (prev == -1) { atomicAdd(&nused, 1); placed = true; break; }
-        if (prev == (int)j) { placed = true; break; }
-        h = (h + 1) & (RED_MAPCAP - 1);
-      }
-      if (placed) {
-        macc[h] += sum;  // one head per face per chunk: single writer
-        if (INTEG) macc2[h] += sum2;
-      } else {
-        atomicAdd(&nused, RED_MAPCAP);  // map full: reported as OVERFLOW
+    // Per face, the weights of its rays summed in ray order (the reference's
+    // accumulation order): one warp per face finds the face's rays 32 at a
+    // time with a ballot, lane 0 adds them in order.  (Replaces a bitonic
+    // sort of the (face, ray) keys: 55 block-wide stages per chunk.)
+    {
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      const int nf_now = nface;
+      for (int f = warp; warp < NWR - 1 && f < nf_now; f += NWR - 1) {
+        const int slot = flist[f];
+        double sum = 0.0, sum2 = 0.0;
+        for (int base = 0; base < cnt; base += 32) {
+          const int s = base + lane;
+          unsigned m = __ballot_sync(0xffffffffu, s < cnt && rslot[s] == slot);
+          if (lane == 0) {
+            while (m) {
+              const int q = base + __ffs(m) - 1;
+              m &= m - 1;
+              sum += wv[q];
+              if (INTEG) sum2 += sv[q];
+            }
+          }
+        }
+        if (lane == 0) {
+          macc[slot] += sum;  // one writer per face per chunk
+          if (INTEG) macc2[slot] += sum2;
+        }
       }
     }
     __syncthreads();
   }
 
-  // Emit faces sorted by neighbour index.
-  for (int i = threadIdx.x; i < RED_MAPCAP; i += RED_NT)
-    keys[i] = mkey[i] < 0 ? ~0ull : (((unsigned long long)(uint32_t)mkey[i] << 32) | (unsigned)i);
-  __syncthreads();
-  bitonic_sort_u64(keys, RED_MAPCAP);
+  // Emit faces sorted by neighbour index: a face's position is the number of
+  // faces with a smaller index (distinct indices).
   const int nf = nused;
+  const int nl = nface;
   const double scale = surf / (double)per;  // integrate_mc.py:357-358
-  for (int p = threadIdx.x; p < nf && p < max_faces; p += RED_NT) {
-    const unsigned long long key = keys[p];
-    out_face_j[c * max_faces + p] = (int32_t)(key >> 32);
-    out_face_area[c * max_faces + p] = macc[key & 0xffffffffu] * scale;
-    if (INTEG) out_face_surf[c * max_faces + p] = macc2[key & 0xffffffffu] * scale;
+  for (int f = threadIdx.x; f < nl; f += RED_NT) {
+    const int slot = flist[f];
+    const int j = mkey[slot];
+    int p = 0;
+    for (int g = 0; g < nl; ++g) p += mkey[flist[g]] < j ? 1 : 0;
+    if (p < max_faces) {
+      out_face_j[c * max_faces + p] = j;
+      out_face_area[c * max_faces + p] = macc[slot] * scale;
+      if (INTEG) out_face_surf[c * max_faces + p] = macc2[slot] * scale;
+    }
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == RED_NT - 32) {
     out_volume[c] = vol * surf / (double)((int64_t)D * per);  // integrate_mc.py:359-360
     if (INTEG) out_vol_integral[c] = fvol * surf / (double)(per * (int64_t)fi.m);  // :363
     out_nfaces[c] = nf < max_faces ? nf : max_faces;
