@@ -414,7 +414,7 @@ class DeviceTraversal:
     """Device state of one traversal: vertex / edge hash tables, vertex,
     boundary arrays.  Capacities grow geometrically between levels."""
 
-    def __init__(self, ns: NodeSet, vcap_hint=None):
+    def __init__(self, ns: NodeSet, vcap_hint=None, ecap_hint=None):
         rec, sqmax = ns.device_records()
         self.ns, self.rec, self.sqmax, self.dev = ns, rec, sqmax, rec.device
         self.d = ns.dim
@@ -423,7 +423,7 @@ class DeviceTraversal:
         vcap = _pow2(vcap_hint or 4 * max(1024, ns.n))
         self.overflow = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self._alloc_vtable(vcap)
-        self._alloc_etable(_pow2(2 * vcap))
+        self._alloc_etable(_pow2(ecap_hint or 2 * vcap))
         self.vsig = torch.empty((vcap // 2, d + 1), dtype=torch.int32, device=self.dev)
         self.vr = torch.empty((vcap // 2, d), dtype=torch.float64, device=self.dev)
         self.bsig = torch.empty((1024, d + 1), dtype=torch.int32, device=self.dev)
@@ -716,7 +716,13 @@ def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heurist
     if stats is None:
         stats = RaycastStats()
     first = descent(ns, 0, _rng.stream(seed, "descent", 0), stats)
-    tr = DeviceTraversal(ns)
+    # size the tables for the expected diagram (mean Voronoi vertices per
+    # generator of a Poisson diagram in d dimensions) so that they rarely
+    # grow: config 3 rehashed its edge table 8 times from the default size
+    vpg = {2: 2, 3: 7, 4: 32, 5: 190, 6: 1300, 7: 9000, 8: 66000}.get(ns.dim, 4)
+    v_est = min(ns.n * vpg, 1 << 26)
+    tr = DeviceTraversal(ns, vcap_hint=max(4 * ns.n, 2 * v_est),
+                         ecap_hint=2 * (ns.dim + 1) * v_est)
     tr.work = work
     tr.seed_vertex(first.sigma)
     from .raycast import Workspace
