@@ -182,6 +182,10 @@ typedef struct vr_prune_index {
   /* The kd-ordered fp32 centred rows in vr_pack_records32 layout (the
    * tensor-core kernel's seed pass); required with recB. */
   const float* rec32rows;
+  /* The node boxes of node_box32 as centre / half-extent rows [c, h] (same
+   * stride; [c - h, c + h] contains the exact box), read by the tensor-core
+   * kernel's tree walk; required with recB. */
+  const float* node_cb32;
 } vr_prune_index;
 
 /* vr_raycast_batch through the pruned index.  `order` (nullable, n_rays

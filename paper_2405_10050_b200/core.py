@@ -208,7 +208,7 @@ class _PruneStruct(ctypes.Structure):
                 ("n", ctypes.c_int64), ("wide_box32", ctypes.c_void_p),
                 ("wide_levels", ctypes.c_int32), ("wide_off", ctypes.c_int64 * 8),
                 ("wide_cnt", ctypes.c_int64 * 8), ("recB", ctypes.c_void_p),
-                ("rec32rows", ctypes.c_void_p)]
+                ("rec32rows", ctypes.c_void_p), ("node_cb32", ctypes.c_void_p)]
 
 
 WIDE = 32
@@ -275,6 +275,22 @@ def kd_order(P, tile=PRUNE_TILE):
         lens = torch.stack([left, seg_len - left], 1).reshape(-1)
         seg_start, seg_len = starts[exists], lens[exists]
     return order
+
+
+def _centre_half32(lo, hi, center):
+    """fp32 centre / half-extent rows [c, h] of fp64 boxes in the centred
+    frame with [c - h, c + h] containing the box exactly (h rounded up)."""
+    lo_c, hi_c = lo - center, hi - center
+    c32 = (0.5 * (lo_c + hi_c)).to(torch.float32)
+    c64 = c32.to(torch.float64)
+    h = torch.maximum(hi_c - c64, c64 - lo_c)
+    h32 = h.to(torch.float32)
+    h32 = torch.where(h32.to(torch.float64) < h, torch.nextafter(h32, torch.full_like(h32, float("inf"))), h32)
+    d = lo.shape[1]
+    pad = ((2 * d + 3) & ~3) - 2 * d  # 16-B rows (csrc box32_stride)
+    parts = [c32, h32] + ([torch.zeros((c32.shape[0], pad), dtype=torch.float32,
+                                       device=c32.device)] if pad else [])
+    return torch.cat(parts, 1).contiguous()
 
 
 def _outward32(lo, hi, center):
@@ -383,6 +399,7 @@ class PruneIndex:
         self.rec32p = self.screen32.rec_pairs
         self.tile_box32 = _outward32(lo, hi, self.screen32.center)
         self.node_box32 = _outward32(nlo, nhi, self.screen32.center)
+        self.node_cb32 = _centre_half32(nlo, nhi, self.screen32.center)
         lv = wide_levels(lo, hi)
         boxes = [_outward32(a, b, self.screen32.center) for a, b in lv]
         self.wide_cnt = [int(b.shape[0]) for b in boxes]
@@ -406,7 +423,7 @@ class PruneIndex:
                                    p(self.wide_box32), len(boxes), pad8(self.wide_off),
                                    pad8(self.wide_cnt),
                                    p(self.recB) if self.recB is not None else None,
-                                   p(self.screen32.rec))
+                                   p(self.screen32.rec), p(self.node_cb32))
 
 
 def build_node_set(points, backend="auto"):
