@@ -51,7 +51,7 @@ enum vr_cell_status {
   VR_CELL_OVERFLOW = 3     /* more distinct hit faces than area slots          */
 };
 
-int vr_abi_version(void); /* 4 */
+int vr_abi_version(void); /* 5 */
 const char* vr_status_string(int status);
 
 /* Record stride (doubles) of one packed generator for dimension d:
@@ -215,6 +215,51 @@ int vr_ray_keys(const int32_t* inv_perm, const int32_t* eta, int eta_len,
                 int64_t rays_per_cell, const double* u, int64_t n, int d, int64_t* keys,
                 void* stream);
 
+/* The processing order itself: the keys of vr_ray_keys (32-bit when
+ * n_base * 256 < 2^32; n_base = the range of base, i.e. n_gen or the cell
+ * count) sorted by a stable LSD radix sort, order[k] = ray id of slot k.
+ * Call with workspace == NULL to receive the workspace size in
+ * *workspace_bytes; otherwise *workspace_bytes is the size passed. */
+int vr_ray_order(const int32_t* inv_perm, const int32_t* eta, int eta_len,
+                 int64_t rays_per_cell, const double* u, int64_t n, int d, int64_t n_base,
+                 int32_t* order, void* workspace, int64_t* workspace_bytes, void* stream);
+
+/* ---- Native build of the pruned index ------------------------------------
+ * Replaces the spatial index the reference builds inside NodeSet.__init__
+ * (core.py:52-57: scipy cKDTree, used by the kd-tree NN probe core.py:92-103).
+ *
+ * vr_screen32_stats: the fp32 screening frame of n packed records (the
+ *   vr_screen32 fields): stats[0..7] = centre (the bounding-box midpoint, or
+ *   `center` (device, d doubles) when given), stats[8] = max |x - c|^2,
+ *   stats[9] = max_k |x_k - c_k|.  `stats` is 32 device doubles (16..31 are
+ *   scratch).  Read it back once to fill a vr_screen32.
+ * vr_prune_index_layout: device bytes of the index arena and of the build
+ *   workspace for n generators (flags: VR_PRUNE_MMA also packs recB, the
+ *   tensor-core screen operand used from d = 5), tile / node / 32-ary level
+ *   counts.
+ * vr_build_prune_index: balanced kd partition (per depth: node bounding
+ *   boxes, widest axis, stable radix sort of the coordinate + a stable sort
+ *   by segment; a node of > 1 tiles splits after floor(tiles / 2) whole
+ *   tiles), the kd-ordered records with sentinel rows, perm / inv_perm, tile
+ *   / node / 32-ary boxes (fp64 + outward fp32 rows in the frame centred at
+ *   `center`, device d doubles: vr_screen32_stats of the generators) and the
+ *   fp32 / pair / tensor-core screening copies, all inside `arena`; fills
+ *   *out (host struct) with pointers into it.  Stream-ordered, no sync. */
+typedef struct vr_prune_layout {
+  int64_t arena_bytes;
+  int64_t workspace_bytes;
+  int64_t n_tiles;
+  int64_t n_nodes;
+  int32_t wide_levels;
+} vr_prune_layout;
+#define VR_PRUNE_MMA 1
+int vr_screen32_stats(const double* rec, int64_t n, int d, const double* center, double* stats,
+                      void* stream);
+int vr_prune_index_layout(int64_t n, int d, int flags, vr_prune_layout* out);
+int vr_build_prune_index(const double* rec, int64_t n, int d, const double* center, int flags,
+                         void* arena, int64_t arena_bytes, void* workspace,
+                         int64_t workspace_bytes, vr_prune_index* out, void* stream);
+
 /* Exact re-evaluation of the rays listed in recheck_list[0 .. *count)
  * (count read on device): centred t for every candidate, argmin with the
  * smallest-index tie-break, then the reference's runner-up degeneracy band
@@ -291,7 +336,14 @@ int vr_vertex_directions(const double* rec, int d, const int32_t* sigma,
  * or degenerate ray of the cell in ray order; degenerate rays count only when
  * degenerate_is_error (the per-ray path raises, the neighbour-batch path
  * _mc_areas_batch takes the plain argmin).  surf = S_{d-1} as computed by the
- * caller (integrate_mc.py:44-48); max_faces <= 512. */
+ * caller (integrate_mc.py:44-48).  Face counts are unbounded like the
+ * reference's dict (integrate_mc.py:147-160): the per-cell face map holds
+ * 2 max_faces slots (at least 1024) in shared memory, or, past 160 KB, in
+ * `map_ws` (device, vr_mc_map_bytes bytes; NULL otherwise); a cell with more
+ * than max_faces faces reports VR_CELL_OVERFLOW and is re-reduced by the
+ * caller with a larger max_faces (faces <= rays and <= n_gen - 1).
+ * cell_sel (nullable, n_sel int32 row indices): reduce only those cell rows,
+ * block b writing output row b (the overflow re-run). */
 int vr_mc_rays(const double* rec, int64_t n_gen, int d, double sqmax,
                const vr_screen32* s32, const double* cand_rec, const int32_t* cand, int64_t n_cand,
                const int32_t* cells, int64_t n_cells, int64_t rays_per_cell,
@@ -315,11 +367,13 @@ int vr_mc_recheck(const double* rec, int64_t n_gen, int d,
                   int64_t max_list, int32_t* out_idx, double* out_t,
                   uint8_t* out_flag, void* stream);
 
+int64_t vr_mc_map_bytes(int64_t n_blocks, int max_faces, int integrate);
 int vr_mc_reduce(const double* rec, int d, const int32_t* cells,
                  int64_t n_cells, int64_t rays_per_cell, const double* dirs,
                  uint64_t seed, const int32_t* ray_idx, const double* ray_t,
                  const uint8_t* ray_flag, int max_faces,
                  int degenerate_is_error, double surf,
+                 const int32_t* cell_sel, int64_t n_sel, void* map_ws, int64_t map_ws_bytes,
                  double* out_volume, int32_t* out_face_j, double* out_face_area,
                  int32_t* out_nfaces, int32_t* out_status,
                  int64_t* out_first_bad, double* out_samples /* nullable */,
@@ -339,7 +393,8 @@ int vr_mc_integrate(const double* rec, int d, const int32_t* cells, int64_t n_ce
                     const int32_t* ray_idx, const double* ray_t,
                     const uint8_t* ray_flag, int max_faces, double surf,
                     int integrand_kind, const double* coef, int m_sub,
-                    const double* unif, double* out_volume, int32_t* out_face_j,
+                    const double* unif, const int32_t* cell_sel, int64_t n_sel,
+                    void* map_ws, int64_t map_ws_bytes, double* out_volume, int32_t* out_face_j,
                     double* out_face_area, double* out_face_surf,
                     double* out_vol_integral, int32_t* out_nfaces,
                     int32_t* out_status, int64_t* out_first_bad, void* stream);
@@ -377,8 +432,7 @@ typedef struct vr_traverse_tables {
  *   vr_trav_open_edges), their exclusive int64 offsets in open_off, and the
  *   ray count R in *n_rays_out (host).
  * vr_trav_level_cast: the R edge rays (as vr_trav_emit_rays; bad[0..1] are
- *   zeroed first), their processing order (vr_ray_keys + a stable radix
- *   sort), the pruned RayCast with |eta| = d plus the exact re-check (hits in
+ *   zeroed first), their processing order (vr_ray_order), the pruned RayCast with |eta| = d plus the exact re-check (hits in
  *   hit_idx / hit_t / hit_flag), vr_trav_claim, exclusive offsets of the new
  *   vertices and of the escapes, and counts_out[5] (host) = {new vertices,
  *   escapes, degenerate rays, affinely dependent frontier vertices, table
@@ -387,7 +441,8 @@ typedef struct vr_traverse_tables {
  *   vr_trav_finalize / vr_trav_boundary. */
 int vr_trav_level_open(const vr_traverse_tables* tab, int d, const int32_t* frontier_sigma,
                        int64_t n_v, uint8_t* open_mask, int32_t* open_count, int64_t* open_off,
-                       int64_t* n_rays_out, void* stream);
+                       int64_t* n_rays_out, void* workspace, int64_t workspace_bytes,
+                       void* stream);
 int vr_trav_level_cast(const vr_traverse_tables* tab, const double* rec, int64_t n_gen, int d,
                        double sqmax, const vr_screen32* s32, const vr_prune_index* ix,
                        const int32_t* frontier_sigma, const double* frontier_r, int64_t n_v,
@@ -396,7 +451,12 @@ int vr_trav_level_cast(const vr_traverse_tables* tab, const double* rec, int64_t
                        int32_t* ray_parent, int32_t* hit_idx, double* hit_t, uint8_t* hit_flag,
                        int32_t* ray_sigma, int64_t* slot, int32_t* new_flag, int32_t* esc_flag,
                        int64_t* new_off, int64_t* esc_off, int32_t* bad, uint64_t* work,
-                       int64_t* counts_out, void* stream);
+                       int64_t* counts_out, void* workspace, int64_t workspace_bytes,
+                       void* stream);
+/* Device scratch (bytes) both calls need for n_v frontier vertices and
+ * n_rays edge rays (n_rays = 0: vr_trav_level_open only); a smaller
+ * workspace returns VR_ECAPACITY. */
+int vr_trav_level_workspace(int64_t n_v, int64_t n_rays, int64_t n_gen, int d, int64_t* bytes);
 
 /* Register vertices (sigma (n_v, d+1) sorted) with ids base_id.. at `level`;
  * optionally bump the counters of their d+1 edges (graph.py:115-120). */

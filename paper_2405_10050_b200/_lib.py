@@ -15,7 +15,7 @@ import torch
 from ._build import LIB_PATH
 from .errors import DeviceUnavailable
 
-ABI_VERSION = 4  # vr_abi_version() of the library this package expects
+ABI_VERSION = 5  # vr_abi_version() of the library this package expects
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -41,7 +41,7 @@ _SIGNATURES = {
     "vr_mc_recheck": [_vp, _i64, _int, _vp, _vp, _i64, _vp, _i64, _vp, _u64, _vp, _vp, _i64,
                       _vp, _vp, _vp, _vp],
     "vr_mc_reduce": [_vp, _int, _vp, _i64, _i64, _vp, _u64, _vp, _vp, _vp, _int, _int, _dbl,
-                     _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+                     _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_mc_directions": [_int, _i64, _vp, _i64, _u64, _vp, _vp],
     "vr_fma_probe": [_int, _int, _int, _vp, _vp],
     "vr_raycast_pruned": [_vp, _i64, _int, _dbl, _vp, _vp, _vp, _vp, _vp, _int, _i64, _vp, _vp,
@@ -54,14 +54,20 @@ _SIGNATURES = {
     "vr_host_streams": [ctypes.c_uint64, ctypes.c_uint64, _vp, _i64, _vp],
     "vr_descent_directions": [_vp, _int, _vp, _vp, _vp, _i64, ctypes.c_double, _vp, _vp, _vp,
                               _vp],
-    "vr_trav_level_open": [_vp, _int, _vp, _i64, _vp, _vp, _vp, _vp, _vp],
+    "vr_trav_level_open": [_vp, _int, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
     "vr_trav_level_cast": [_vp, _vp, _i64, _int, ctypes.c_double, _vp, _vp, _vp, _vp, _i64,
                            _vp, _vp, _i64, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                           _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+                           _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
     "vr_host_normals": [_vp, _vp, _i64, _i64, _vp],
     "vr_ray_keys": [_vp, _vp, _int, _i64, _vp, _i64, _int, _vp, _vp],
+    "vr_ray_order": [_vp, _vp, _int, _i64, _vp, _i64, _int, _i64, _vp, _vp, _vp, _vp],
+    "vr_screen32_stats": [_vp, _i64, _int, _vp, _vp, _vp],
+    "vr_prune_index_layout": [_i64, _int, _int, _vp],
+    "vr_build_prune_index": [_vp, _i64, _int, _vp, _int, _vp, _i64, _vp, _i64, _vp, _vp],
+    "vr_trav_level_workspace": [_i64, _i64, _i64, _int, _vp],
     "vr_mc_integrate": [_vp, _int, _vp, _i64, _i64, _vp, _u64, _vp, _vp, _vp, _int, _dbl, _int,
-                        _vp, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+                        _vp, _int, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                        _vp, _vp],
     "vr_mc_uniforms": [_i64, _vp, _i64, _int, _u64, _vp, _vp],
     "vr_record32_stride": [_int],
     "vr_trav_insert_vertices": [_vp, _int, _vp, _i64, ctypes.c_int32, ctypes.c_int32, _int, _vp],
@@ -77,7 +83,7 @@ _SIGNATURES = {
 }
 
 # Symbols declared in include/voronray_b200.h that the .so must export.
-EXPORTED = tuple(_SIGNATURES) + ("vr_status_string", "vr_record_rows")
+EXPORTED = tuple(_SIGNATURES) + ("vr_status_string", "vr_record_rows", "vr_mc_map_bytes")
 
 _LIB = None
 
@@ -97,6 +103,8 @@ def load_library():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
         fn.restype = ctypes.c_int
+    lib.vr_mc_map_bytes.argtypes = [_i64, _int, _int]
+    lib.vr_mc_map_bytes.restype = ctypes.c_int64
     lib.vr_record_rows.argtypes = [_i64]
     lib.vr_record_rows.restype = ctypes.c_int64
     lib.vr_status_string.argtypes = [_int]

@@ -164,7 +164,7 @@ class NodeSet:
         return (int(idx[0]), float(d1[0])), float(d2[0])
 
 
-PRUNE_TILE = int(os.environ.get("VR_PRUNE_TILE", "64"))  # must match the library (64)
+PRUNE_TILE = 64  # VR_PRUNE_TILE of the library
 
 
 class _Screen32Struct(ctypes.Structure):
@@ -173,18 +173,25 @@ class _Screen32Struct(ctypes.Structure):
                 ("rec_pairs", ctypes.c_void_p)]
 
 
+def screen_stats(rec, n, d, center=None):
+    """(centre (d,) device fp64, sqmax, bound) of the fp32 screening frame of
+    n packed records (vr_screen32_stats): the bounding-box midpoint unless
+    `center` (device tensor) is given; one host read-back."""
+    L = _lib.lib()
+    stats = torch.empty(32, dtype=torch.float64, device=rec.device)
+    _lib.check(L.vr_screen32_stats(_lib.ptr(rec), int(n), d, _lib.ptr(center), _lib.ptr(stats),
+                                   _lib.stream_handle()), "vr_screen32_stats")
+    host = stats[:10].cpu().numpy()
+    return stats[:d].clone(), float(host[8]), float(host[9]), host[:d].tolist()
+
+
 class Screen32:
     """Centred fp32 copy of a record array (include/voronray_b200.h vr_screen32)."""
 
     def __init__(self, rec, n, d, center=None):
         L = _lib.lib()
         dev = rec.device
-        pts = rec[:n, :d]
-        if center is None:
-            center = 0.5 * (pts.amin(0) + pts.amax(0))
-        self.center = center.to(torch.float64).contiguous()
-        self.sqmax = float(((pts - self.center) ** 2).sum(1).max().item())
-        self.bound = float((pts - self.center).abs().max().item())
+        self.center, self.sqmax, self.bound, c_host = screen_stats(rec, n, d, center)
         s32 = (d + 4) & ~3
         self.rec = torch.empty((rec.shape[0], s32), dtype=torch.float32, device=dev)
         _lib.check(L.vr_pack_records32(_lib.ptr(rec), rec.shape[0], d, _lib.ptr(self.center),
@@ -195,7 +202,7 @@ class Screen32:
         _lib.check(L.vr_pack_records32_pairs(_lib.ptr(self.rec), rows, d, _lib.ptr(self.rec_pairs),
                                              _lib.stream_handle()), "vr_pack_records32_pairs")
         c = [0.0] * 8
-        c[:d] = self.center.cpu().tolist()
+        c[:d] = c_host
         self.struct = _Screen32Struct(self.rec.data_ptr(), (ctypes.c_double * 8)(*c), self.sqmax,
                                       self.bound, self.rec_pairs.data_ptr())
 
@@ -211,219 +218,73 @@ class _PruneStruct(ctypes.Structure):
                 ("rec32rows", ctypes.c_void_p), ("node_cb32", ctypes.c_void_p)]
 
 
-WIDE = 32
+class _PruneLayout(ctypes.Structure):
+    _fields_ = [("arena_bytes", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
+                ("n_tiles", ctypes.c_int64), ("n_nodes", ctypes.c_int64),
+                ("wide_levels", ctypes.c_int32)]
 
 
-def wide_levels(lo, hi):
-    """32-ary tree over kd-ordered tile boxes: level 0 = tiles, node j of
-    level l = union of nodes [32j, 32j+32) of level l-1, up to one root (at
-    least two levels).  Returns a list of (lo, hi) fp64 tensors per level."""
-    levels = [(lo, hi)]
-    while levels[-1][0].shape[0] > 1 or len(levels) < 2:
-        a, b = levels[-1]
-        m, d = a.shape
-        g = (m + WIDE - 1) // WIDE
-        pad = g * WIDE - m
-        if pad:
-            a = torch.cat([a, torch.full((pad, d), float("inf"), dtype=a.dtype, device=a.device)])
-            b = torch.cat([b, torch.full((pad, d), float("-inf"), dtype=b.dtype, device=b.device)])
-        levels.append((a.view(g, WIDE, d).amin(1), b.view(g, WIDE, d).amax(1)))
-    if len(levels) > 8:
-        raise ValueError("too many generators for the 32-ary tile tree")
-    return levels
-
-
-def kd_order(P, tile=PRUNE_TILE):
-    """Balanced kd partition on the device: returns the permutation (int64)
-    placing generators so that every leaf occupies whole tiles of `tile`
-    rows (only the last tile is partial).  Each split sorts a segment along
-    its widest extent and cuts after floor(tiles/2) full tiles."""
-    n, d = P.shape
-    dev = P.device
-    order = torch.arange(n, device=dev)
-    seg_start = torch.zeros(1, dtype=torch.int64, device=dev)
-    seg_len = torch.full((1,), n, dtype=torch.int64, device=dev)
-    seg_of = torch.zeros(n, dtype=torch.int64, device=dev)
-    pos = torch.arange(n, device=dev)
-    inf = float("inf")
-    while True:
-        split = seg_len > tile
-        if not bool(split.any()):
-            break
-        X = P[order]
-        nseg = seg_start.numel()
-        idx = seg_of[:, None].expand(n, d)
-        mn = torch.full((nseg, d), inf, dtype=P.dtype, device=dev).scatter_reduce(
-            0, idx, X, "amin", include_self=True)
-        mx = torch.full((nseg, d), -inf, dtype=P.dtype, device=dev).scatter_reduce(
-            0, idx, X, "amax", include_self=True)
-        dim = (mx - mn).argmax(1)
-        key = X.gather(1, dim[seg_of][:, None]).squeeze(1)
-        key = torch.where(split[seg_of], key, torch.zeros_like(key))
-        o1 = torch.sort(key, stable=True).indices
-        o2 = torch.sort(seg_of[o1], stable=True).indices
-        order = order[o1[o2]]
-        nt = (seg_len + tile - 1) // tile
-        left = torch.where(split, (nt // 2) * tile, seg_len)
-        rel = pos - seg_start[seg_of]
-        is_right = split[seg_of] & (rel >= left[seg_of])
-        # children ids: left = 2s, right = 2s+1, compacted to existing ones
-        exists = torch.stack([torch.ones_like(split), split], 1).reshape(-1)
-        new_id = torch.cumsum(exists.to(torch.int64), 0) - 1
-        seg_of = new_id[2 * seg_of + is_right.to(torch.int64)]
-        starts = torch.stack([seg_start, seg_start + left], 1).reshape(-1)
-        lens = torch.stack([left, seg_len - left], 1).reshape(-1)
-        seg_start, seg_len = starts[exists], lens[exists]
-    return order
-
-
-def _centre_half32(lo, hi, center):
-    """fp32 centre / half-extent rows [c, h] of fp64 boxes in the centred
-    frame with [c - h, c + h] containing the box exactly (h rounded up)."""
-    lo_c, hi_c = lo - center, hi - center
-    c32 = (0.5 * (lo_c + hi_c)).to(torch.float32)
-    c64 = c32.to(torch.float64)
-    h = torch.maximum(hi_c - c64, c64 - lo_c)
-    h32 = h.to(torch.float32)
-    h32 = torch.where(h32.to(torch.float64) < h, torch.nextafter(h32, torch.full_like(h32, float("inf"))), h32)
-    d = lo.shape[1]
-    pad = ((2 * d + 3) & ~3) - 2 * d  # 16-B rows (csrc box32_stride)
-    parts = [c32, h32] + ([torch.zeros((c32.shape[0], pad), dtype=torch.float32,
-                                       device=c32.device)] if pad else [])
-    return torch.cat(parts, 1).contiguous()
-
-
-def _outward32(lo, hi, center):
-    """fp32 copy of fp64 boxes in the centred frame, rounded outward so the
-    fp32 box contains the fp64 one (lo rounded down, hi rounded up)."""
-    lo_c, hi_c = lo - center, hi - center
-    lo32, hi32 = lo_c.to(torch.float32), hi_c.to(torch.float32)
-    ninf = torch.full_like(lo32, float("-inf"))
-    pinf = torch.full_like(hi32, float("inf"))
-    lo32 = torch.where(lo32.to(torch.float64) > lo_c, torch.nextafter(lo32, ninf), lo32)
-    hi32 = torch.where(hi32.to(torch.float64) < hi_c, torch.nextafter(hi32, pinf), hi32)
-    d = lo.shape[1]
-    pad = ((2 * d + 3) & ~3) - 2 * d  # 16-B rows (csrc box32_stride)
-    parts = [lo32, hi32] + ([torch.zeros((lo32.shape[0], pad), dtype=torch.float32,
-                                         device=lo32.device)] if pad else [])
-    return torch.cat(parts, 1).contiguous()
-
-
-def kd_tree_layout(nt):
-    """Heap layout of the kd tree over nt tiles (node i -> 2i+1, 2i+2; a node
-    of n > 1 tiles [lo, hi) splits at lo + n // 2, as kd_order does).
-    Returns (ranges int32 (nodes, 2), leaf node index per tile); unused heap
-    slots have range (-1, -1)."""
-    size = 1
-    while size < nt:
-        size *= 2
-    nodes = 2 * size
-    rng = np.full((nodes, 2), -1, dtype=np.int64)
-    cur = np.array([0]), np.array([0]), np.array([nt])
-    leaf_of = np.zeros(nt, dtype=np.int64)
-    while cur[0].size:
-        idx, lo, hi = cur
-        rng[idx, 0], rng[idx, 1] = lo, hi
-        n = hi - lo
-        leaf = n == 1
-        leaf_of[lo[leaf]] = idx[leaf]
-        inner = ~leaf
-        idx, lo, hi, n = idx[inner], lo[inner], hi[inner], n[inner]
-        mid = lo + n // 2
-        cur = (np.concatenate([2 * idx + 1, 2 * idx + 2]), np.concatenate([lo, mid]),
-               np.concatenate([mid, hi]))
-    used = rng[:, 0] >= 0
-    last = int(np.nonzero(used)[0].max()) + 1
-    return rng[:last].astype(np.int32), leaf_of
-
-
-def _node_boxes(lo, hi, ranges, leaf_of):
-    """Bottom-up unions of the tile boxes over the heap-layout kd tree."""
-    dev = lo.device
-    nn = ranges.shape[0]
-    d = lo.shape[1]
-    nlo = torch.full((nn, d), float("inf"), dtype=lo.dtype, device=dev)
-    nhi = torch.full((nn, d), float("-inf"), dtype=hi.dtype, device=dev)
-    leaf = torch.as_tensor(leaf_of, device=dev)
-    nlo[leaf], nhi[leaf] = lo, hi
-    depth = int(np.floor(np.log2(max(nn, 1)))) + 1
-    for lev in range(depth - 1, -1, -1):
-        a, b = (1 << lev) - 1, min(nn, (1 << (lev + 1)) - 1)
-        if a >= nn:
-            continue
-        idx = torch.arange(a, b, device=dev)
-        l, r = 2 * idx + 1, 2 * idx + 2
-        inner = torch.as_tensor(ranges[a:b, 1] - ranges[a:b, 0] > 1, device=dev)
-        li = idx[inner]
-        if li.numel():
-            ll, rr = 2 * li + 1, 2 * li + 2
-            nlo[li] = torch.minimum(nlo[ll], nlo[rr])
-            nhi[li] = torch.maximum(nhi[ll], nhi[rr])
-    # unused heap slots keep an empty box that no ray ever needs
-    return nlo, nhi
+VR_PRUNE_MMA = 1
+MMA_MIN_D = int(os.environ.get("VR_MMA_MIN_D", "5"))  # tensor-core screen from this d
 
 
 class PruneIndex:
-    """Device tensors of one vr_prune_index."""
+    """One vr_prune_index, built natively (vr_build_prune_index) into a single
+    device arena: kd-ordered records, perm / inv_perm, tile / node / 32-ary
+    boxes and the fp32 / tensor-core screening copies.  The spatial index the
+    reference builds in NodeSet.__init__ (core.py:52-57).  Tensor views of the
+    arena are exposed for tests and tools."""
 
-    def __init__(self, rec, n, d, center):
+    def __init__(self, rec, n, d, center, workspace=None):
+        L = _lib.lib()
         dev = rec.device
-        pts = rec[:n, :d]
-        perm = kd_order(pts)
-        rows = rec.shape[0]
-        crec = torch.zeros_like(rec)
-        crec[:, d] = float("inf")
-        crec[:n] = rec[perm]
-        self.perm = perm.to(torch.int32).contiguous()
-        inv = torch.empty(n, dtype=torch.int64, device=dev)
-        inv[perm] = torch.arange(n, device=dev)
-        self.inv_perm = inv.to(torch.int32).contiguous()
-        nt = (n + PRUNE_TILE - 1) // PRUNE_TILE
-        X = crec[:nt * PRUNE_TILE, :d].view(nt, PRUNE_TILE, d)
-        valid = (torch.arange(nt * PRUNE_TILE, device=dev) < n).view(nt, PRUNE_TILE, 1)
-        lo = torch.where(valid, X, torch.full_like(X, float("inf"))).amin(1)
-        hi = torch.where(valid, X, torch.full_like(X, float("-inf"))).amax(1)
-        self.tile_box = torch.cat([lo, hi], 1).contiguous()
-        ranges, leaf_of = kd_tree_layout(nt)
-        self.node_range = torch.as_tensor(ranges, device=dev).contiguous()
-        nlo, nhi = _node_boxes(lo, hi, ranges, leaf_of)
-        used = torch.as_tensor(ranges[:, 0] >= 0, device=dev)[:, None]
-        nlo = torch.where(used, nlo, torch.zeros_like(nlo))   # unused: finite, never visited
-        nhi = torch.where(used, nhi, torch.zeros_like(nhi))
-        self.node_box = torch.cat([nlo, nhi], 1).contiguous()
-        self.rec = crec
-        self.n = n
-        self.rows = rows
-        self.screen32 = Screen32(crec, n, d, center=center)
-        # the pruned kernel reads the fp32 rows pair-interleaved (packed FFMA2)
-        self.rec32p = self.screen32.rec_pairs
-        self.tile_box32 = _outward32(lo, hi, self.screen32.center)
-        self.node_box32 = _outward32(nlo, nhi, self.screen32.center)
-        self.node_cb32 = _centre_half32(nlo, nhi, self.screen32.center)
-        lv = wide_levels(lo, hi)
-        boxes = [_outward32(a, b, self.screen32.center) for a, b in lv]
-        self.wide_cnt = [int(b.shape[0]) for b in boxes]
-        self.wide_off = np.concatenate([[0], np.cumsum(self.wide_cnt)[:-1]]).astype(np.int64).tolist()
-        self.wide_box32 = torch.cat(boxes).contiguous()
-        # tensor-core screen operand (used from d = 5): rec32 rows in mma B-fragment order
-        self.recB = None
-        if PRUNE_TILE == 64 and d >= int(os.environ.get("VR_MMA_MIN_D", "5")) and \
-                os.environ.get("VR_MMA", "1") != "0":
-            ks = (d + 2 + 7) // 8
-            self.recB = torch.empty((rows, 8 * ks), dtype=torch.float32, device=dev)
-            L = _lib.lib()
-            _lib.check(L.vr_pack_records_mma(_lib.ptr(self.screen32.rec), rows, d,
-                                             _lib.ptr(self.recB), _lib.stream_handle()),
-                       "vr_pack_records_mma")
-        p = lambda t: t.data_ptr()  # noqa: E731
-        pad8 = lambda v: (ctypes.c_int64 * 8)(*(list(v) + [0] * (8 - len(v))))  # noqa: E731
-        self.struct = _PruneStruct(p(crec), p(self.rec32p), p(self.perm), p(self.inv_perm),
-                                   p(self.tile_box), p(self.tile_box32), p(self.node_box),
-                                   p(self.node_box32), p(self.node_range), n,
-                                   p(self.wide_box32), len(boxes), pad8(self.wide_off),
-                                   pad8(self.wide_cnt),
-                                   p(self.recB) if self.recB is not None else None,
-                                   p(self.screen32.rec), p(self.node_cb32))
+        flags = VR_PRUNE_MMA if (d >= MMA_MIN_D and os.environ.get("VR_MMA", "1") != "0") else 0
+        lay = _PruneLayout()
+        _lib.check(L.vr_prune_index_layout(int(n), d, flags, ctypes.byref(lay)),
+                   "vr_prune_index_layout")
+        self.arena = torch.empty(int(lay.arena_bytes), dtype=torch.uint8, device=dev)
+        if workspace is not None:
+            ws = workspace.get("prune_build", (int(lay.workspace_bytes),), torch.uint8, dev)
+        else:
+            ws = torch.empty(int(lay.workspace_bytes), dtype=torch.uint8, device=dev)
+        self.struct = _PruneStruct()
+        _lib.check(L.vr_build_prune_index(_lib.ptr(rec), int(n), d, _lib.ptr(center), flags,
+                                          _lib.ptr(self.arena), int(lay.arena_bytes), _lib.ptr(ws),
+                                          int(lay.workspace_bytes), ctypes.byref(self.struct),
+                                          _lib.stream_handle()), "vr_build_prune_index")
+        del ws  # stream-ordered: the caching allocator reuses it after the build
+        self.n, self.d, self.rows = int(n), d, _lib.record_rows(n)
+        self.n_tiles, self.n_nodes = int(lay.n_tiles), int(lay.n_nodes)
+        base = self.arena.data_ptr()
+        st = self.struct
+
+        def view(ptr, shape, dtype):
+            if not ptr:
+                return None
+            esz = torch.empty(0, dtype=dtype).element_size()
+            cnt = 1
+            for x in shape:
+                cnt *= int(x)
+            off = int(ptr) - base
+            return self.arena[off:off + cnt * esz].view(dtype).view(*shape)
+
+        b32 = (2 * d + 3) & ~3
+        ks = (d + 2 + 7) // 8
+        self.rec = view(st.rec, (self.rows, (d + 2) & ~1), torch.float64)
+        self.rec32rows = view(st.rec32rows, (self.rows, (d + 4) & ~3), torch.float32)
+        self.rec32p = view(st.rec32, (self.rows // 2, (2 * d + 5) & ~3), torch.float32)
+        self.perm = view(st.perm, (self.n,), torch.int32)
+        self.inv_perm = view(st.inv_perm, (self.n,), torch.int32)
+        self.tile_box = view(st.tile_box, (self.n_tiles, 2 * d), torch.float64)
+        self.tile_box32 = view(st.tile_box32, (self.n_tiles, b32), torch.float32)
+        self.node_box = view(st.node_box, (self.n_nodes, 2 * d), torch.float64)
+        self.node_box32 = view(st.node_box32, (self.n_nodes, b32), torch.float32)
+        self.node_cb32 = view(st.node_cb32, (self.n_nodes, b32), torch.float32)
+        self.node_range = view(st.node_range, (self.n_nodes, 2), torch.int32)
+        self.wide_cnt = [int(st.wide_cnt[i]) for i in range(st.wide_levels)]
+        self.wide_off = [int(st.wide_off[i]) for i in range(st.wide_levels)]
+        self.wide_box32 = view(st.wide_box32, (sum(self.wide_cnt), b32), torch.float32)
+        self.recB = view(st.recB, (self.rows, 8 * ks), torch.float32)
 
 
 def build_node_set(points, backend="auto"):
@@ -607,6 +468,36 @@ class Mesh:
                               for s, u in zip(a["boundary_sigma"], a["boundary_u"])]
         return self._boundary
 
+    def contains(self, sigma):
+        """Membership of sorted sigma rows in the vertex set (the reference's
+        ``sigma in mesh.vertices``, core.py:205-221), vectorised: bool array.
+        A device-resident traversal mesh is searched on the device (64-bit
+        row hashes, sorted once, exact row comparison of the hash matches),
+        so nothing is copied to the host."""
+        d1 = self.nodes.dim + 1
+        q = np.ascontiguousarray(sigma, dtype=np.int32).reshape(-1, d1)
+        if self._dev is not None and self._arr is None:
+            S = self._dev["sigma"]
+            if S.shape[0] == 0 or q.shape[0] == 0:
+                return np.zeros(q.shape[0], dtype=bool)
+            if getattr(self, "_hash_index", None) is None:
+                h = _row_hash(S)
+                hs, order = torch.sort(h)
+                self._hash_index = (hs, order)
+            hs, order = self._hash_index
+            qd = torch.from_numpy(q).to(S.device)
+            qh = _row_hash(qd)
+            pos = torch.searchsorted(hs, qh)
+            found = torch.zeros(q.shape[0], dtype=torch.bool, device=S.device)
+            last = S.shape[0] - 1
+            for k in range(4):  # equal hashes are adjacent; 4 covers any real collision
+                pk = (pos + k).clamp(max=last)
+                found |= (hs[pk] == qh) & (S[order[pk]] == qd).all(1)
+            return found.cpu().numpy()
+        a = self.arrays()["sigma"]
+        have = {tuple(r) for r in a.tolist()}
+        return np.array([tuple(r) in have for r in q.tolist()], dtype=bool)
+
     # -- cell maps (core.py:223-276) ---------------------------------------
     def _csr(self):
         if self._cell_csr is None:
@@ -677,6 +568,15 @@ class Mesh:
             self._unbounded_faces = frozenset(pairs)
         key = (i, j) if i < j else (j, i)
         return key in self._unbounded_faces
+
+
+def _row_hash(rows):
+    """64-bit polynomial hash of int32 rows (device tensor), wrapping."""
+    h = torch.zeros(rows.shape[0], dtype=torch.int64, device=rows.device)
+    for k in range(rows.shape[1]):
+        h = h * 1000003 + rows[:, k].to(torch.int64)
+        h = h ^ (h >> 29)
+    return h
 
 
 def verify_vertices(ns: NodeSet, sigma, r, tol: float = TOL_VERTEX):

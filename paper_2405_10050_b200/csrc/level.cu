@@ -16,7 +16,6 @@
 // The caller (DeviceTraversal.level) then grows the edge table if needed and
 // calls vr_trav_finalize / vr_trav_boundary as before.  Results are those of
 // the Python-driven level (the processing order is the same stable sort).
-#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
@@ -32,9 +31,9 @@ int vr_trav_claim(const vr_traverse_tables* tab, int d, const int32_t* ray_eta,
                   const int32_t* hit_idx, const uint8_t* hit_flag, int64_t n_rays,
                   int32_t level, int32_t* out_sigma, int64_t* out_slot, int32_t* new_flag,
                   int32_t* esc_flag, void* stream);
-int vr_ray_keys(const int32_t* inv_perm, const int32_t* eta, int eta_len,
-                int64_t rays_per_cell, const double* u, int64_t n, int d, int64_t* keys,
-                void* stream);
+int vr_ray_order(const int32_t* inv_perm, const int32_t* eta, int eta_len,
+                 int64_t rays_per_cell, const double* u, int64_t n, int d, int64_t n_base,
+                 int32_t* order, void* workspace, int64_t* workspace_bytes, void* stream);
 int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double sqmax,
                       const vr_screen32* s32, const vr_prune_index* ix, const double* x,
                       const double* u, const int32_t* eta, int eta_len, int64_t n_rays,
@@ -62,12 +61,6 @@ __global__ void k_widen(const T* __restrict__ in, int64_t* __restrict__ out, int
     out[i] = (int64_t)in[i];
 }
 
-__global__ void k_iota(int32_t* __restrict__ v, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    v[i] = (int32_t)i;
-}
-
 __global__ void k_count_degenerate(const uint8_t* __restrict__ flag, int64_t n,
                                    unsigned long long* __restrict__ count) {
   unsigned long long c = 0;
@@ -93,61 +86,80 @@ __global__ void k_level_counts(const int32_t* __restrict__ new_flag,
   counts[4] = overflow[0];
 }
 
-// Stream-ordered scratch from the default memory pool (kept, not released,
-// between levels: the pool's release threshold is raised once).
-struct Scratch {
-  cudaStream_t st;
-  void* p = nullptr;
-  cudaError_t alloc(size_t bytes) {
-    static bool pool_set = false;
-    if (!pool_set) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      }
-      pool_set = true;
-    }
-    return cudaMallocAsync(&p, bytes ? bytes : 16, st);
-  }
-  ~Scratch() {
-    if (p) cudaFreeAsync(p, st);
-  }
-};
-
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-// Exclusive int64 scan of an int32 array (cub), with its own temp storage.
-cudaError_t excl_scan(const int32_t* in, int64_t* out, int64_t n, cudaStream_t st) {
+size_t scan_tmp_bytes(int64_t n) {
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, (const int64_t*)nullptr, (int64_t*)nullptr,
+                                (int)(n > 0 ? n : 1));
+  return tmp;
+}
+
+// Exclusive int64 scan of an int32 array (cub) with caller scratch.
+cudaError_t excl_scan(const int32_t* in, int64_t* out, int64_t n, void* tmp, size_t tmp_bytes,
+                      cudaStream_t st) {
   // widen into `out`, then scan in place (cub allows in == out for scans)
   k_widen<int32_t><<<nbk(n), 256, 0, st>>>(in, out, n);
-  size_t tmp = 0;
-  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tmp, out, out, (int)n, st);
-  if (e != cudaSuccess) return e;
-  Scratch s{st};
-  if ((e = s.alloc(tmp)) != cudaSuccess) return e;
-  return cub::DeviceScan::ExclusiveSum(s.p, tmp, out, out, (int)n, st);
+  return cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, out, out, (int)n, st);
+}
+
+// Scratch layout of vr_trav_level_cast (R rays): order, recheck list / count,
+// degenerate counter, device counts, then scratch shared by the ray-order
+// sort and the scans.
+struct CastPlan {
+  size_t o_order, o_rl, o_rc, o_deg, o_cnt, o_tmp, tmp, total;
+};
+
+int cast_plan(int64_t R, int64_t n_gen, int d, CastPlan& p) {
+  int64_t order_ws = 0;
+  int s = vr_ray_order(nullptr, nullptr, d, 1, nullptr, R, d, n_gen, nullptr, nullptr, &order_ws,
+                       nullptr);
+  if (s) return s;
+  const size_t scan = scan_tmp_bytes(R);
+  p.tmp = (size_t)order_ws > scan ? (size_t)order_ws : scan;
+  p.o_order = 0;
+  p.o_rl = align256(p.o_order + 4 * R);
+  p.o_rc = align256(p.o_rl + 4 * R);
+  p.o_deg = align256(p.o_rc + 4);
+  p.o_cnt = align256(p.o_deg + 8);
+  p.o_tmp = align256(p.o_cnt + 8 * 5);
+  p.total = p.o_tmp + p.tmp;
+  return VR_OK;
 }
 
 int fail(cudaError_t e) { return e == cudaSuccess ? VR_OK : vr_cuda_status(e); }
 
 }  // namespace
 
+extern "C" int vr_trav_level_workspace(int64_t n_v, int64_t n_rays, int64_t n_gen, int d,
+                                       int64_t* bytes) {
+  if (!bytes || n_v < 0 || n_rays < 0) return VR_EINVAL;
+  size_t need = align256(scan_tmp_bytes(n_v));
+  if (n_rays > 0) {
+    CastPlan p;
+    int s = cast_plan(n_rays, n_gen, d, p);
+    if (s) return s;
+    if (p.total > need) need = p.total;
+  }
+  *bytes = (int64_t)need;
+  return VR_OK;
+}
+
 extern "C" int vr_trav_level_open(const vr_traverse_tables* tab, int d,
                                   const int32_t* frontier_sigma, int64_t n_v, uint8_t* open_mask,
                                   int32_t* open_count, int64_t* open_off, int64_t* n_rays_out,
-                                  void* stream) {
+                                  void* workspace, int64_t workspace_bytes, void* stream) {
   if (!tab || !frontier_sigma || !open_mask || !open_count || !open_off || !n_rays_out)
     return VR_EINVAL;
   *n_rays_out = 0;
   if (n_v <= 0) return VR_OK;
   if (n_v >= (int64_t)1 << 31) return VR_EINVAL;  // cub scans with int counts
+  const size_t tmp = scan_tmp_bytes(n_v);
+  if (!workspace || workspace_bytes < (int64_t)tmp) return VR_ECAPACITY;
   cudaStream_t st = as_stream(stream);
   int s = vr_trav_open_edges(tab, d, frontier_sigma, n_v, open_mask, open_count, stream);
   if (s) return s;
-  cudaError_t e = excl_scan(open_count, open_off, n_v, st);
+  cudaError_t e = excl_scan(open_count, open_off, n_v, workspace, tmp, st);
   if (e != cudaSuccess) return fail(e);
   int64_t last[1];
   int32_t cnt[1];
@@ -166,7 +178,8 @@ extern "C" int vr_trav_level_cast(
     int64_t n_rays, int32_t level, double* ray_x, double* ray_u, int32_t* ray_eta,
     int32_t* ray_parent, int32_t* hit_idx, double* hit_t, uint8_t* hit_flag, int32_t* ray_sigma,
     int64_t* slot, int32_t* new_flag, int32_t* esc_flag, int64_t* new_off, int64_t* esc_off,
-    int32_t* bad, uint64_t* work, int64_t* counts_out, void* stream) {
+    int32_t* bad, uint64_t* work, int64_t* counts_out, void* workspace, int64_t workspace_bytes,
+    void* stream) {
   if (!tab || !rec || !ix || !ix->inv_perm || !frontier_sigma || !frontier_r || !open_mask ||
       !open_off || !ray_x || !ray_u || !ray_eta || !ray_parent || !hit_idx || !hit_t ||
       !hit_flag || !ray_sigma || !slot || !new_flag || !esc_flag || !new_off || !esc_off ||
@@ -175,46 +188,28 @@ extern "C" int vr_trav_level_cast(
   for (int i = 0; i < 5; ++i) counts_out[i] = 0;
   if (n_rays <= 0) return VR_OK;
   if (n_rays >= (int64_t)1 << 31) return VR_EINVAL;
+  const int64_t R = n_rays;
+  CastPlan P;
+  int s = cast_plan(R, n_gen, d, P);
+  if (s) return s;
+  if (!workspace || workspace_bytes < (int64_t)P.total) return VR_ECAPACITY;
   cudaStream_t st = as_stream(stream);
   cudaError_t e;
-  int s;
   if ((e = cudaMemsetAsync(bad, 0, 2 * sizeof(int32_t), st)) != cudaSuccess) return fail(e);
   s = vr_trav_emit_rays(rec, d, frontier_sigma, frontier_r, n_v, open_mask, open_off, ray_x,
                         ray_u, ray_eta, ray_parent, bad, stream);
   if (s) return s;
-  // one scratch block: keys in / out, order in / out, recheck list + count,
-  // degenerate counter, device counts, sort temp storage
-  const int64_t R = n_rays;
-  int end_bit = 8;  // keys = kd position * 256 + direction class
-  while (end_bit < 63 && ((int64_t)1 << end_bit) <= n_gen * 256) ++end_bit;
-  size_t sort_tmp = 0;
-  e = cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (const int64_t*)nullptr,
-                                      (int64_t*)nullptr, (const int32_t*)nullptr,
-                                      (int32_t*)nullptr, (int)R, 0, end_bit, st);
-  if (e != cudaSuccess) return fail(e);
-  const size_t o_kin = 0, o_kout = align256(o_kin + 8 * R), o_vin = align256(o_kout + 8 * R),
-               o_vout = align256(o_vin + 4 * R), o_rl = align256(o_vout + 4 * R),
-               o_rc = align256(o_rl + 4 * R), o_deg = align256(o_rc + 4),
-               o_cnt = align256(o_deg + 8), o_tmp = align256(o_cnt + 8 * 5),
-               total = o_tmp + sort_tmp;
-  Scratch sc{st};
-  if ((e = sc.alloc(total)) != cudaSuccess) return fail(e);
-  char* base = static_cast<char*>(sc.p);
-  int64_t* kin = reinterpret_cast<int64_t*>(base + o_kin);
-  int64_t* kout = reinterpret_cast<int64_t*>(base + o_kout);
-  int32_t* vin = reinterpret_cast<int32_t*>(base + o_vin);
-  int32_t* order = reinterpret_cast<int32_t*>(base + o_vout);
-  int32_t* rl = reinterpret_cast<int32_t*>(base + o_rl);
-  int32_t* rc = reinterpret_cast<int32_t*>(base + o_rc);
-  unsigned long long* ndeg = reinterpret_cast<unsigned long long*>(base + o_deg);
-  int64_t* dcounts = reinterpret_cast<int64_t*>(base + o_cnt);
+  char* base = static_cast<char*>(workspace);
+  int32_t* order = reinterpret_cast<int32_t*>(base + P.o_order);
+  int32_t* rl = reinterpret_cast<int32_t*>(base + P.o_rl);
+  int32_t* rc = reinterpret_cast<int32_t*>(base + P.o_rc);
+  unsigned long long* ndeg = reinterpret_cast<unsigned long long*>(base + P.o_deg);
+  int64_t* dcounts = reinterpret_cast<int64_t*>(base + P.o_cnt);
+  void* tmp = base + P.o_tmp;
   // processing order (raycast.py coherent_order: stable sort of the keys)
-  s = vr_ray_keys(ix->inv_perm, ray_eta, d, 1, ray_u, R, d, kin, stream);
+  int64_t tb = (int64_t)P.tmp;
+  s = vr_ray_order(ix->inv_perm, ray_eta, d, 1, ray_u, R, d, n_gen, order, tmp, &tb, stream);
   if (s) return s;
-  k_iota<<<nbk(R), 256, 0, st>>>(vin, R);
-  e = cub::DeviceRadixSort::SortPairs(base + o_tmp, sort_tmp, kin, kout, vin, order, (int)R, 0,
-                                      end_bit, st);
-  if (e != cudaSuccess) return fail(e);
   // RayCast of the level's edge rays (|eta| = d) + exact re-check
   s = vr_raycast_pruned(rec, n_gen, d, sqmax, s32, ix, ray_x, ray_u, ray_eta, d, R, order,
                         hit_idx, hit_t, nullptr, hit_flag, rl, rc, work, stream);
@@ -226,8 +221,8 @@ extern "C" int vr_trav_level_cast(
   s = vr_trav_claim(tab, d, ray_eta, hit_idx, hit_flag, R, level, ray_sigma, slot, new_flag,
                     esc_flag, stream);
   if (s) return s;
-  if ((e = excl_scan(new_flag, new_off, R, st)) != cudaSuccess) return fail(e);
-  if ((e = excl_scan(esc_flag, esc_off, R, st)) != cudaSuccess) return fail(e);
+  if ((e = excl_scan(new_flag, new_off, R, tmp, P.tmp, st)) != cudaSuccess) return fail(e);
+  if ((e = excl_scan(esc_flag, esc_off, R, tmp, P.tmp, st)) != cudaSuccess) return fail(e);
   if ((e = cudaMemsetAsync(ndeg, 0, 8, st)) != cudaSuccess) return fail(e);
   k_count_degenerate<<<nbk(R, 256) < 1184 ? nbk(R, 256) : 1184, 256, 0, st>>>(hit_flag, R, ndeg);
   k_level_counts<<<1, 1, 0, st>>>(new_flag, new_off, esc_flag, esc_off, R, ndeg, bad,

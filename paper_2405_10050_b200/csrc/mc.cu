@@ -9,7 +9,18 @@ namespace {
 
 constexpr int RED_NT = 256;
 constexpr int RED_CHUNK = 1024;   // rays per reduction chunk (4 per thread)
-constexpr int RED_MAPCAP = 1024;  // smem face map capacity (max_faces <= 512)
+constexpr int RED_MAPCAP = 1024;  // minimum face map capacity (max_faces <= 512)
+// Face maps larger than this many bytes live in a caller workspace in global
+// memory instead of dynamic shared memory (unbounded face counts).
+constexpr int RED_SMEM_MAP_MAX = 160 * 1024;
+
+__host__ __device__ constexpr int map_entry_bytes(bool integ) { return integ ? 24 : 16; }
+
+inline int map_capacity(int max_faces) {
+  int cap = RED_MAPCAP;
+  while (cap < 2 * max_faces) cap *= 2;
+  return cap;
+}
 
 // Integrand on the device for the CLI's built-ins (reference integrands.py):
 // kind 1 const c, 2 sin(x_1^2), 3 linear a.x + b.
@@ -48,7 +59,8 @@ __global__ void __launch_bounds__(RED_NT)
                 double surf, Integ fi, double* out_volume, int32_t* out_face_j,
                 double* out_face_area, int32_t* out_nfaces, int32_t* out_status,
                 int64_t* out_first_bad, double* out_samples, double* out_face_surf,
-                double* out_vol_integral) {
+                double* out_vol_integral, const int32_t* __restrict__ cell_sel, int mapcap,
+                unsigned char* __restrict__ gmap) {
   constexpr int S = rec_stride(D);
   constexpr int CH = INTEG ? 512 : RED_CHUNK;  // rays per chunk (smem budget)
   __shared__ unsigned long long keys[CH];  // (face << 32 | ray) per ray of the chunk, ~0 if none
@@ -56,20 +68,29 @@ __global__ void __launch_bounds__(RED_NT)
   __shared__ double lv[CH];
   __shared__ double sv[INTEG ? CH : 1];   // f(rp) w          (integrate_mc.py:350)
   __shared__ double fv[INTEG ? CH : 1];   // acc * length^d   (integrate_mc.py:356)
-  __shared__ int mkey[RED_MAPCAP];
-  __shared__ double macc[RED_MAPCAP];
-  __shared__ double macc2[INTEG ? RED_MAPCAP : 1];
   __shared__ int rslot[CH];          // face-map slot of each ray of the chunk (-1: none)
-  __shared__ int flist[RED_MAPCAP];  // slots in use, in insertion order
   __shared__ unsigned long long first_bad;  // (ray << 2) | kind
-  __shared__ int nused;  // faces (+ RED_MAPCAP per face that found no slot: OVERFLOW)
+  __shared__ int nused;  // faces (+ mapcap per face that found no slot: OVERFLOW)
   __shared__ int nface;  // entries of flist
+  // face map (mapcap entries): accumulators, keys (neighbour index, -1 free)
+  // and the slots in insertion order -- in dynamic shared memory, or in the
+  // caller's global workspace for very large face counts
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  unsigned char* mbase =
+      gmap ? gmap + (size_t)blockIdx.x * mapcap * map_entry_bytes(INTEG) : dyn_smem;
+  double* macc = reinterpret_cast<double*>(mbase);
+  double* macc2 = macc + mapcap;  // INTEG only
+  int* mkey = reinterpret_cast<int*>(macc + (INTEG ? 2 : 1) * (size_t)mapcap);
+  int* flist = mkey + mapcap;
 
-  const int64_t c = blockIdx.x;
+  // block b reduces cell row cell_sel[b] (all rows without a selection);
+  // its outputs go to row b
+  const int64_t o = blockIdx.x;
+  const int64_t c = cell_sel ? (int64_t)cell_sel[o] : o;
   const int64_t per = src.per;
   const int32_t cell = src.cells[c];
   const double* xc = src.grec + (int64_t)cell * S;
-  for (int i = threadIdx.x; i < RED_MAPCAP; i += RED_NT) {
+  for (int i = threadIdx.x; i < mapcap; i += RED_NT) {
     mkey[i] = -1;
     macc[i] = 0.0;
     if (INTEG) macc2[i] = 0.0;
@@ -150,8 +171,8 @@ __global__ void __launch_bounds__(RED_NT)
       int slot = -1;
       if (key != ~0ull) {
         const uint32_t j = (uint32_t)(key >> 32);
-        unsigned h = (j * 2654435761u) & (RED_MAPCAP - 1);
-        for (int probe = 0; probe < RED_MAPCAP; ++probe) {
+        unsigned h = (j * 2654435761u) & (mapcap - 1);
+        for (int probe = 0; probe < mapcap; ++probe) {
           const int prev = atomicCAS(&mkey[h], -1, (int)j);
           if (prev == -1) {
             atomicAdd(&nused, 1);
@@ -160,9 +181,9 @@ __global__ void __launch_bounds__(RED_NT)
             break;
           }
           if (prev == (int)j) { slot = (int)h; break; }
-          h = (h + 1) & (RED_MAPCAP - 1);
+          h = (h + 1) & (mapcap - 1);
         }
-        if (slot < 0) atomicAdd(&nused, RED_MAPCAP);  // map full: reported as OVERFLOW
+        if (slot < 0) atomicAdd(&nused, mapcap);  // map full: reported as OVERFLOW
       }
       rslot[s] = slot;
     }
@@ -183,7 +204,9 @@ __global__ void __launch_bounds__(RED_NT)
       const int nf_now = nface;
       for (int f = warp; warp < NWR - 1 && f < nf_now; f += NWR - 1) {
         const int slot = flist[f];
-        double sum = 0.0, sum2 = 0.0;
+        // continue the face's running sums: one sequential sum in ray order
+        // across chunks (integrate_mc.py:154-155)
+        double sum = macc[slot], sum2 = INTEG ? macc2[slot] : 0.0;
         for (int base = 0; base < cnt; base += 32) {
           const int s = base + lane;
           unsigned m = __ballot_sync(0xffffffffu, s < cnt && rslot[s] == slot);
@@ -197,8 +220,8 @@ __global__ void __launch_bounds__(RED_NT)
           }
         }
         if (lane == 0) {
-          macc[slot] += sum;  // one writer per face per chunk
-          if (INTEG) macc2[slot] += sum2;
+          macc[slot] = sum;  // one writer per face per chunk
+          if (INTEG) macc2[slot] = sum2;
         }
       }
     }
@@ -216,15 +239,15 @@ __global__ void __launch_bounds__(RED_NT)
     int p = 0;
     for (int g = 0; g < nl; ++g) p += mkey[flist[g]] < j ? 1 : 0;
     if (p < max_faces) {
-      out_face_j[c * max_faces + p] = j;
-      out_face_area[c * max_faces + p] = macc[slot] * scale;
-      if (INTEG) out_face_surf[c * max_faces + p] = macc2[slot] * scale;
+      out_face_j[o * max_faces + p] = j;
+      out_face_area[o * max_faces + p] = macc[slot] * scale;
+      if (INTEG) out_face_surf[o * max_faces + p] = macc2[slot] * scale;
     }
   }
   if (threadIdx.x == RED_NT - 32) {
-    out_volume[c] = vol * surf / (double)((int64_t)D * per);  // integrate_mc.py:359-360
-    if (INTEG) out_vol_integral[c] = fvol * surf / (double)(per * (int64_t)fi.m);  // :363
-    out_nfaces[c] = nf < max_faces ? nf : max_faces;
+    out_volume[o] = vol * surf / (double)((int64_t)D * per);  // integrate_mc.py:359-360
+    if (INTEG) out_vol_integral[o] = fvol * surf / (double)(per * (int64_t)fi.m);  // :363
+    out_nfaces[o] = nf < max_faces ? nf : max_faces;
     int status = VR_CELL_OK;
     int64_t fb = -1;
     if (first_bad != ~0ull) {
@@ -233,8 +256,8 @@ __global__ void __launch_bounds__(RED_NT)
     } else if (nf > max_faces) {
       status = VR_CELL_OVERFLOW;
     }
-    out_status[c] = status;
-    out_first_bad[c] = fb;
+    out_status[o] = status;
+    out_first_bad[o] = fb;
   }
 }
 
@@ -289,27 +312,76 @@ extern "C" int vr_mc_recheck(const double* rec, int64_t n_gen, int d, const doub
   return VR_OK;
 }
 
+namespace {
+
+// Launch k_mc_reduce over n_blocks cell rows (cell_sel: row per block, or
+// all rows) with a face map of map_capacity(max_faces) entries, in dynamic
+// shared memory up to RED_SMEM_MAP_MAX bytes, else in map_ws.
+template <int D, bool INTEG>
+int launch_reduce(const SrcMC<D>& src, int64_t n_blocks, const int32_t* ray_idx,
+                  const double* ray_t, const uint8_t* ray_flag, int max_faces,
+                  int degenerate_is_error, double surf, const Integ& fi, double* out_volume,
+                  int32_t* out_face_j, double* out_face_area, int32_t* out_nfaces,
+                  int32_t* out_status, int64_t* out_first_bad, double* out_samples,
+                  double* out_face_surf, double* out_vol_integral, const int32_t* cell_sel,
+                  void* map_ws, int64_t map_ws_bytes, cudaStream_t st) {
+  const int cap = map_capacity(max_faces);
+  const int64_t map_bytes = (int64_t)cap * map_entry_bytes(INTEG);
+  unsigned char* gmap = nullptr;
+  int smem = 0;
+  if (map_bytes > RED_SMEM_MAP_MAX) {
+    if (!map_ws || map_ws_bytes < map_bytes * n_blocks) return VR_ECAPACITY;
+    gmap = static_cast<unsigned char*>(map_ws);
+  } else {
+    smem = (int)map_bytes;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(k_mc_reduce<D, INTEG>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           RED_SMEM_MAP_MAX);
+      if (e != cudaSuccess) return vr_cuda_status(e);
+      attr_set = true;
+    }
+  }
+  k_mc_reduce<D, INTEG><<<(unsigned)n_blocks, RED_NT, smem, st>>>(
+      src, ray_idx, ray_t, ray_flag, max_faces, degenerate_is_error, surf, fi, out_volume,
+      out_face_j, out_face_area, out_nfaces, out_status, out_first_bad, out_samples,
+      out_face_surf, out_vol_integral, cell_sel, cap, gmap);
+  VR_RETURN_LAUNCH();
+}
+
+}  // namespace
+
+extern "C" int64_t vr_mc_map_bytes(int64_t n_blocks, int max_faces, int integrate) {
+  if (n_blocks <= 0 || max_faces <= 0) return 0;
+  const int64_t map_bytes = (int64_t)map_capacity(max_faces) * map_entry_bytes(integrate != 0);
+  return map_bytes > RED_SMEM_MAP_MAX ? map_bytes * n_blocks : 0;
+}
+
 extern "C" int vr_mc_reduce(const double* rec, int d, const int32_t* cells, int64_t n_cells,
                             int64_t rays_per_cell, const double* dirs, uint64_t seed,
                             const int32_t* ray_idx, const double* ray_t, const uint8_t* ray_flag,
                             int max_faces, int degenerate_is_error, double surf,
-                            double* out_volume, int32_t* out_face_j, double* out_face_area,
-                            int32_t* out_nfaces, int32_t* out_status, int64_t* out_first_bad,
-                            double* out_samples, void* stream) {
+                            const int32_t* cell_sel, int64_t n_sel, void* map_ws,
+                            int64_t map_ws_bytes, double* out_volume, int32_t* out_face_j,
+                            double* out_face_area, int32_t* out_nfaces, int32_t* out_status,
+                            int64_t* out_first_bad, double* out_samples, void* stream) {
   if (!rec || !cells || !ray_idx || !ray_t || !ray_flag || !out_volume || !out_face_j ||
       !out_face_area || !out_nfaces || !out_status || !out_first_bad)
     return VR_EINVAL;
-  if (max_faces <= 0 || max_faces > RED_MAPCAP / 2) return VR_EINVAL;
-  if (n_cells <= 0) return VR_OK;
+  if (max_faces <= 0 || max_faces > (1 << 28)) return VR_EINVAL;
+  const int64_t nb = cell_sel ? n_sel : n_cells;
+  if (nb <= 0) return VR_OK;
   VR_DISPATCH_D(d, {
     SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n_cells * rays_per_cell};
     Integ fi{};
-    k_mc_reduce<D, false><<<(unsigned)n_cells, RED_NT, 0, as_stream(stream)>>>(
-        src, ray_idx, ray_t, ray_flag, max_faces, degenerate_is_error, surf, fi, out_volume,
-        out_face_j, out_face_area, out_nfaces, out_status, out_first_bad, out_samples, nullptr,
-        nullptr);
+    return launch_reduce<D, false>(src, nb, ray_idx, ray_t, ray_flag, max_faces,
+                                   degenerate_is_error, surf, fi, out_volume, out_face_j,
+                                   out_face_area, out_nfaces, out_status, out_first_bad,
+                                   out_samples, nullptr, nullptr, cell_sel, map_ws, map_ws_bytes,
+                                   as_stream(stream));
   });
-  VR_RETURN_LAUNCH();
+  return VR_OK;
 }
 
 extern "C" int vr_mc_integrate(const double* rec, int d, const int32_t* cells, int64_t n_cells,
@@ -317,16 +389,18 @@ extern "C" int vr_mc_integrate(const double* rec, int d, const int32_t* cells, i
                                const int32_t* ray_idx, const double* ray_t,
                                const uint8_t* ray_flag, int max_faces, double surf,
                                int integrand_kind, const double* coef, int m_sub,
-                               const double* unif, double* out_volume, int32_t* out_face_j,
-                               double* out_face_area, double* out_face_surf,
+                               const double* unif, const int32_t* cell_sel, int64_t n_sel,
+                               void* map_ws, int64_t map_ws_bytes, double* out_volume,
+                               int32_t* out_face_j, double* out_face_area, double* out_face_surf,
                                double* out_vol_integral, int32_t* out_nfaces,
                                int32_t* out_status, int64_t* out_first_bad, void* stream) {
   if (!rec || !cells || !ray_idx || !ray_t || !ray_flag || !out_volume || !out_face_j ||
       !out_face_area || !out_face_surf || !out_vol_integral || !out_nfaces || !out_status ||
       !out_first_bad || m_sub < 1 || integrand_kind < 1 || integrand_kind > 3)
     return VR_EINVAL;
-  if (max_faces <= 0 || max_faces > RED_MAPCAP / 2) return VR_EINVAL;
-  if (n_cells <= 0) return VR_OK;
+  if (max_faces <= 0 || max_faces > (1 << 28)) return VR_EINVAL;
+  const int64_t nb = cell_sel ? n_sel : n_cells;
+  if (nb <= 0) return VR_OK;
   Integ fi{};
   fi.kind = integrand_kind;
   fi.m = m_sub;
@@ -335,12 +409,12 @@ extern "C" int vr_mc_integrate(const double* rec, int d, const int32_t* cells, i
   for (int k = 0; k < ncoef; ++k) fi.coef[k] = coef[k];
   VR_DISPATCH_D(d, {
     SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n_cells * rays_per_cell};
-    k_mc_reduce<D, true><<<(unsigned)n_cells, RED_NT, 0, as_stream(stream)>>>(
-        src, ray_idx, ray_t, ray_flag, max_faces, 1, surf, fi, out_volume, out_face_j,
-        out_face_area, out_nfaces, out_status, out_first_bad, nullptr, out_face_surf,
-        out_vol_integral);
+    return launch_reduce<D, true>(src, nb, ray_idx, ray_t, ray_flag, max_faces, 1, surf, fi,
+                                  out_volume, out_face_j, out_face_area, out_nfaces, out_status,
+                                  out_first_bad, nullptr, out_face_surf, out_vol_integral,
+                                  cell_sel, map_ws, map_ws_bytes, as_stream(stream));
   });
-  VR_RETURN_LAUNCH();
+  return VR_OK;
 }
 
 extern "C" int vr_mc_uniforms(int64_t n_cells, const int32_t* cells, int64_t rays_per_cell,

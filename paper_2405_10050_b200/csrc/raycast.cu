@@ -33,7 +33,7 @@ int vr::coop_mode() {
   return v;
 }
 
-extern "C" int vr_abi_version(void) { return 4; }
+extern "C" int vr_abi_version(void) { return 5; }
 
 extern "C" const char* vr_status_string(int status) {
   switch (status) {
@@ -132,52 +132,5 @@ extern "C" int vr_raycast_pruned(const double* rec, int64_t n_gen, int d, double
   return VR_OK;
 }
 
-// ---------------------------------------------------------------------------
-// Processing-order keys for the pruned kernels (one pass; sorted by the
-// caller): key = base * 256 + direction class, where base is the kd position
-// of the ray's reference generator (inv_perm[eta[k * eta_len]]) or, with
-// eta == NULL, k / per (MC: rays of one cell), and the direction class is the
-// signed index of the largest and second-largest |u_j| (< 256 for d <= 8).
-// ---------------------------------------------------------------------------
-namespace {
-template <int D>
-__global__ void k_ray_keys(const int32_t* __restrict__ inv_perm, const int32_t* __restrict__ eta,
-                           int eta_len, int64_t per, const double* __restrict__ u, int64_t n,
-                           int64_t* __restrict__ keys) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    double a1 = -1.0, a2 = -1.0;
-    int i1 = 0, i2 = 0;
-    bool s1 = false, s2 = false;
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      const double v = u[k * D + j], a = fabs(v);
-      if (a > a1) {  // first index on ties (torch.argmax semantics)
-        a2 = a1; i2 = i1; s2 = s1;
-        a1 = a; i1 = j; s1 = v > 0.0;
-      } else if (a > a2) {
-        a2 = a; i2 = j; s2 = v > 0.0;
-      }
-    }
-    const int64_t bucket = (int64_t)(i1 * 2 + (s1 ? 1 : 0)) * (2 * D) + (i2 * 2 + (s2 ? 1 : 0));
-    const int64_t base = eta ? (int64_t)inv_perm[eta[k * eta_len]] : k / per;
-    keys[k] = base * 256 + bucket;
-  }
-}
-}  // namespace
-
-extern "C" int vr_ray_keys(const int32_t* inv_perm, const int32_t* eta, int eta_len,
-                           int64_t rays_per_cell, const double* u, int64_t n, int d,
-                           int64_t* keys, void* stream) {
-  if (n <= 0) return VR_OK;
-  if (!u || !keys || (eta && (!inv_perm || eta_len < 1)) || (!eta && rays_per_cell < 1))
-    return VR_EINVAL;
-  const int64_t nb64 = (n + 255) / 256;
-  const unsigned nb = (unsigned)(nb64 < 8192 ? nb64 : 8192);
-  VR_DISPATCH_D(d, {
-    k_ray_keys<D><<<nb, 256, 0, as_stream(stream)>>>(inv_perm, eta, eta_len, rays_per_cell, u, n,
-                                                      keys);
-  });
-  VR_RETURN_LAUNCH();
-}
-
+// Processing-order keys / order of a ray batch: csrc/index.cu (vr_ray_keys,
+// vr_ray_order).

@@ -543,8 +543,13 @@ class DeviceTraversal:
         off = ws.get("lv_open_off", (F,), torch.int64, dev)
         T = self.tables()
         nr = ctypes.c_int64(0)
+        wsb = ctypes.c_int64(0)
+        _lib.check(L.vr_trav_level_workspace(F, 0, self.ns.n, d, ctypes.byref(wsb)),
+                   "level_workspace")
+        scratch = ws.get("lv_scratch", (wsb.value,), torch.uint8, dev)
         _lib.check(L.vr_trav_level_open(ctypes.byref(T), d, p(fs), F, p(open_mask), p(open_cnt),
-                                        p(off), ctypes.byref(nr), sh), "level_open")
+                                        p(off), ctypes.byref(nr), p(scratch), scratch.numel(), sh),
+                   "level_open")
         R = int(nr.value)
         if R == 0:
             return 0
@@ -570,11 +575,14 @@ class DeviceTraversal:
         ns = self.ns
         ix = ns.prune_index(dev)
         s32 = ns.screen32(dev)
+        _lib.check(L.vr_trav_level_workspace(F, R, ns.n, d, ctypes.byref(wsb)), "level_workspace")
+        scratch = ws.get("lv_scratch", (wsb.value,), torch.uint8, dev)
         _lib.check(L.vr_trav_level_cast(
             ctypes.byref(T), p(self.rec), ns.n, d, self.sqmax, ctypes.byref(s32.struct),
             ctypes.byref(ix.struct), p(fs), p(fr), F, p(open_mask), p(off), R, lvl, p(rx), p(ru),
             p(reta), p(rpar), p(hidx), p(ht), p(hflag), p(rsig), p(slot), p(newf), p(escf),
-            p(noff), p(eoff), p(bad), p(self.work), counts.ctypes.data, sh), "level_cast")
+            p(noff), p(eoff), p(bad), p(self.work), counts.ctypes.data, p(scratch),
+            scratch.numel(), sh), "level_cast")
         n_new, n_esc, n_deg, n_bad, ovf = (int(v) for v in counts)
         if n_bad:
             raise DegenerateConfiguration("generators of a frontier vertex are affinely dependent")
@@ -702,6 +710,24 @@ def _level_raycaster(ns, stats, group, work=None):
     return ShardedRaycast(fn, group)
 
 
+def _table_estimate(ns, v_guess):
+    """Vertex count the traversal tables are pre-sized for: the Poisson
+    estimate, capped by C(N, d+1) and by a quarter of the free device memory
+    (~(d+1)(4d + 28) + 8d bytes per vertex of tables and arrays); the tables
+    still grow geometrically past it, so the cap only bounds the up-front
+    allocation of small high-d inputs."""
+    from math import comb
+    d = ns.dim
+    v = min(int(v_guess), comb(ns.n, d + 1), 1 << 26)
+    try:
+        free, _ = torch.cuda.mem_get_info(ns.device_records()[0].device)
+        per_vertex = (d + 1) * (4 * d + 28) + 8 * d + 16 * (d + 1)
+        v = min(v, max(1 << 12, free // 4 // per_vertex))
+    except RuntimeError:
+        pass
+    return max(int(v), 1)
+
+
 def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heuristic",
                   eps: float = None, stats: RaycastStats = None, return_info: bool = False,
                   group=None, work=None):
@@ -720,7 +746,7 @@ def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heurist
     # generator of a Poisson diagram in d dimensions) so that they rarely
     # grow: config 3 rehashed its edge table 8 times from the default size
     vpg = {2: 2, 3: 7, 4: 32, 5: 190, 6: 1300, 7: 9000, 8: 66000}.get(ns.dim, 4)
-    v_est = min(ns.n * vpg, 1 << 26)
+    v_est = _table_estimate(ns, ns.n * vpg)
     tr = DeviceTraversal(ns, vcap_hint=max(4 * ns.n, 2 * v_est),
                          ecap_hint=2 * (ns.dim + 1) * v_est)
     tr.work = work

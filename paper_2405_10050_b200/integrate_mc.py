@@ -30,12 +30,11 @@ from . import _lib
 from .core import NodeSet
 from .errors import DegenerateConfiguration, UnboundedRay
 from .raycast import (RaycastStats, Workspace, _screen, _use_pruned, candidate_records,
-                      ray_keys)
+                      ray_order)
 
 Integrand = Callable[[np.ndarray], float]
 
 CELL_OK, CELL_UNBOUNDED, CELL_DEGENERATE, CELL_OVERFLOW = 0, 1, 2, 3
-MAX_FACES_LIMIT = 512
 
 
 @dataclass
@@ -132,9 +131,7 @@ def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_fa
                 dd = ws.get("mc_dirs", (total, d), torch.float64, dev)
                 _lib.check(L.vr_mc_directions(d, nc, _lib.ptr(cells_d), n, seed, _lib.ptr(dd), sh),
                            "vr_mc_directions")
-            key = ray_keys(dd.view(total, d), rays_per_cell=n)
-            order = torch.sort(key, stable=True).indices.to(torch.int32)
-            del key
+            order = ray_order(dd.view(total, d), rays_per_cell=n, n_base=nc, workspace=ws)
         _lib.check(L.vr_mc_rays_pruned(_lib.ptr(rec), ns.n, d, sqmax, s32p, ctypes.byref(ix.struct),
                                        _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed, _lib.ptr(order),
                                        _lib.ptr(idx), _lib.ptr(t), _lib.ptr(flag), _lib.ptr(rl),
@@ -155,29 +152,89 @@ def _mc_device(ns: NodeSet, cells, n, dirs=None, seed=0, candidates=None, max_fa
     st = torch.empty(nc, dtype=torch.int32, device=dev)
     fb = torch.empty(nc, dtype=torch.int64, device=dev)
     smp = torch.empty(total, dtype=torch.float64, device=dev) if want_samples else None
+    mb = int(L.vr_mc_map_bytes(nc, max_faces, 0))  # > 0 only past the shared-memory face map
+    mws = ws.get("mc_map", (mb,), torch.uint8, dev) if mb else None
     _lib.check(L.vr_mc_reduce(_lib.ptr(rec), d, _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed,
                               _lib.ptr(idx), _lib.ptr(t), _lib.ptr(flag), max_faces,
                               1 if degenerate_is_error else 0, sphere_surface_area(d),
+                              None, 0, _lib.ptr(mws), mb,
                               _lib.ptr(vol), _lib.ptr(fj), _lib.ptr(fa), _lib.ptr(nf),
                               _lib.ptr(st), _lib.ptr(fb), _lib.ptr(smp), sh), "vr_mc_reduce")
     if stats is not None:
         stats.add(total)
+    # faces of a cell are bounded by its rays and by its possible neighbours
+    bound = max(1, min(n, n_cand if candidates is not None else ns.n - 1))
+
+    def rereduce(rows):
+        """Reduce the cell rows `rows` again with a face table large enough
+        for any cell (the reference's face dict is unbounded,
+        integrate_mc.py:147-160); the ray results are reused."""
+        m = len(rows)
+        sel = torch.as_tensor(np.ascontiguousarray(rows, dtype=np.int32), device=dev)
+        mb = int(L.vr_mc_map_bytes(m, bound, 0))
+        mws = torch.empty(mb, dtype=torch.uint8, device=dev) if mb else None
+        o = dict(volume=torch.empty(m, dtype=torch.float64, device=dev),
+                 face_j=torch.empty((m, bound), dtype=torch.int32, device=dev),
+                 face_area=torch.empty((m, bound), dtype=torch.float64, device=dev),
+                 nfaces=torch.empty(m, dtype=torch.int32, device=dev),
+                 status=torch.empty(m, dtype=torch.int32, device=dev),
+                 first_bad=torch.empty(m, dtype=torch.int64, device=dev))
+        _lib.check(L.vr_mc_reduce(_lib.ptr(rec), d, _lib.ptr(cells_d), nc, n, _lib.ptr(dd), seed,
+                                  _lib.ptr(idx), _lib.ptr(t), _lib.ptr(flag), bound,
+                                  1 if degenerate_is_error else 0, sphere_surface_area(d),
+                                  _lib.ptr(sel), m, _lib.ptr(mws), mb,
+                                  _lib.ptr(o["volume"]), _lib.ptr(o["face_j"]),
+                                  _lib.ptr(o["face_area"]), _lib.ptr(o["nfaces"]),
+                                  _lib.ptr(o["status"]), _lib.ptr(o["first_bad"]), None,
+                                  _lib.stream_handle()), "vr_mc_reduce (large faces)")
+        return o
+
     return dict(volume=vol, face_j=fj, face_area=fa, nfaces=nf, status=st, first_bad=fb,
-                samples=smp, ray_idx=idx, ray_t=t, ray_flag=flag)
+                samples=smp, ray_idx=idx, ray_t=t, ray_flag=flag, rereduce=rereduce,
+                max_faces=max_faces, face_bound=bound)
 
 
 def _collect(cells, out, want_samples):
     """Compact the per-cell face tables on the device (cells x max_faces ->
-    the faces actually hit, CSR order) before the host copy."""
+    the faces actually hit, CSR order) before the host copy.  Cells whose
+    faces overflowed the table are reduced again with a table large enough
+    for any cell (out["rereduce"]) and spliced in, so no cell is lost."""
     nf_d = out["nfaces"]
     fj_d, fa_d = out["face_j"], out["face_area"]
+    status = _lib.to_host(out["status"]).copy()
+    ovf = np.nonzero(status == CELL_OVERFLOW)[0]
+    if ovf.size and out.get("rereduce") is not None and out["face_bound"] > out["max_faces"]:
+        nf_d = nf_d.clone()
+        nf_d[torch.as_tensor(ovf, device=nf_d.device)] = 0
     mask = torch.arange(fj_d.shape[1], device=fj_d.device)[None, :] < nf_d[:, None]
-    nf = _lib.to_host(nf_d)
+    nf = _lib.to_host(nf_d).astype(np.int64)
+    face_j = _lib.to_host(fj_d[mask])
+    face_area = _lib.to_host(fa_d[mask])
+    volume = _lib.to_host(out["volume"]).copy()
+    first_bad = _lib.to_host(out["first_bad"]).copy()
+    if ovf.size and out.get("rereduce") is not None and out["face_bound"] > out["max_faces"]:
+        r = out["rereduce"](ovf)
+        rn = _lib.to_host(r["nfaces"]).astype(np.int64)
+        rmask = torch.arange(r["face_j"].shape[1], device=fj_d.device)[None, :] < r["nfaces"][:, None]
+        rj, ra = _lib.to_host(r["face_j"][rmask]), _lib.to_host(r["face_area"][rmask])
+        nf[ovf] = rn
+        status[ovf] = _lib.to_host(r["status"])
+        first_bad[ovf] = _lib.to_host(r["first_bad"])
+        volume[ovf] = _lib.to_host(r["volume"])
+        owner = np.repeat(np.arange(len(nf)), nf)
+        big = np.zeros(len(nf), dtype=bool)
+        big[ovf] = True
+        sel = big[owner]
+        fj_all = np.empty(owner.size, dtype=np.int32)
+        fa_all = np.empty(owner.size, dtype=np.float64)
+        fj_all[~sel], fa_all[~sel] = face_j, face_area
+        fj_all[sel], fa_all[sel] = rj, ra
+        face_j, face_area = fj_all, fa_all
     off = np.zeros(len(nf) + 1, dtype=np.int64)
     np.cumsum(nf, out=off[1:])
-    return MCResult(cells=np.asarray(cells), volume=_lib.to_host(out["volume"]), face_offsets=off,
-                    face_j=_lib.to_host(fj_d[mask]), face_area=_lib.to_host(fa_d[mask]),
-                    status=_lib.to_host(out["status"]), first_bad=_lib.to_host(out["first_bad"]),
+    return MCResult(cells=np.asarray(cells), volume=volume, face_offsets=off,
+                    face_j=face_j, face_area=face_area, status=status.astype(np.int32),
+                    first_bad=first_bad,
                     samples=_lib.to_host(out["samples"]) if want_samples else None)
 
 
@@ -192,8 +249,8 @@ def mc_cells(ns: NodeSet, cells, n: int, seed: int = 0, max_faces: int = 256,
     """
     if n < 1:
         raise ValueError("need n >= 1 rays")
-    if not 1 <= max_faces <= MAX_FACES_LIMIT:
-        raise ValueError(f"max_faces must be in [1, {MAX_FACES_LIMIT}]")
+    if max_faces < 1:
+        raise ValueError("max_faces must be positive")
     cells = np.ascontiguousarray(cells, dtype=np.int32)
     per_chunk = max(1, chunk_rays // n)
     parts = []
@@ -233,9 +290,11 @@ def mc_directions(ns_dim: int, cells, n: int, seed: int = 0, device=None):
 
 
 def _max_faces_for(ns, n, neighbors):
+    """Face-table width that no cell can overflow: distinct faces are
+    bounded by the rays and by the possible neighbours."""
     if neighbors is not None:
-        return max(1, min(MAX_FACES_LIMIT, len(neighbors), n))
-    return max(1, min(MAX_FACES_LIMIT, n, ns.n - 1))
+        return max(1, min(len(neighbors), n))
+    return max(1, min(n, ns.n - 1))
 
 
 def mc_areas_only(ns: NodeSet, i: int, n: int, rng, neighbors=None,
@@ -250,6 +309,10 @@ def mc_areas_only(ns: NodeSet, i: int, n: int, rng, neighbors=None,
     if n < 1:
         raise ValueError("need n >= 1 rays")
     d = ns.dim
+    if neighbors is not None and len(neighbors) == 0:
+        # reference: an empty candidate list makes every probe all-invalid, so
+        # the first ray escapes (integrate_mc.py:143-146 -> _cast, raycast.py:100-117)
+        raise UnboundedRay(i, sample_unit_sphere(d, rng))
     z = np.asarray(rng.standard_normal((n, d)), dtype=np.float64).reshape(n, d)
     use_nb = neighbors is not None and len(neighbors) > 0
     max_faces = _max_faces_for(ns, n, neighbors if use_nb else None)
@@ -263,8 +326,6 @@ def mc_areas_only(ns: NodeSet, i: int, n: int, rng, neighbors=None,
         raise UnboundedRay(i, y / math.sqrt(float(y @ y)))
     if st == CELL_DEGENERATE:
         raise DegenerateConfiguration(f"a foreign generator lies on a circumsphere of cell {i}")
-    if st == CELL_OVERFLOW:
-        raise RuntimeError(f"cell {i} hit more than {max_faces} faces")
     areas = res.areas(0)
     volume = float(res.volume[0])
     return (areas, volume, res.samples) if return_samples else (areas, volume)
@@ -311,13 +372,22 @@ def _integrate_device(ns, cells, n, m, kind, coef, dirs=None, unif=None, seed=0,
     nf = torch.empty(nc, dtype=torch.int32, device=dev)
     st = torch.empty(nc, dtype=torch.int32, device=dev)
     fb = torch.empty(nc, dtype=torch.int64, device=dev)
+    mb = int(L.vr_mc_map_bytes(nc, max_faces, 1))
+    mws = torch.empty(mb, dtype=torch.uint8, device=dev) if mb else None
     _lib.check(L.vr_mc_integrate(_lib.ptr(rec), d, _lib.ptr(cells_d), nc, n, _lib.ptr(dd),
                                  int(seed) & 0xFFFFFFFFFFFFFFFF, _lib.ptr(out["ray_idx"]),
                                  _lib.ptr(out["ray_t"]), _lib.ptr(out["ray_flag"]), max_faces,
                                  sphere_surface_area(d), int(kind), cf, int(m),
-                                 _lib.ptr(ud), _lib.ptr(vol), _lib.ptr(fj), _lib.ptr(fa),
+                                 _lib.ptr(ud), None, 0, _lib.ptr(mws), mb,
+                                 _lib.ptr(vol), _lib.ptr(fj), _lib.ptr(fa),
                                  _lib.ptr(fs), _lib.ptr(vi), _lib.ptr(nf), _lib.ptr(st),
                                  _lib.ptr(fb), _lib.stream_handle()), "vr_mc_integrate")
+    if max_faces < out["face_bound"] and bool((st == CELL_OVERFLOW).any()):
+        # a cell hit more faces than the table holds: redo the reduction with
+        # a table no cell can overflow (the reference's face dict is unbounded)
+        return _integrate_device(ns, cells, n, m, kind, coef, dirs=dirs, unif=unif, seed=seed,
+                                 candidates=candidates, max_faces=out["face_bound"],
+                                 stats=None, workspace=workspace)
     return dict(volume=vol.cpu().numpy(), face_j=fj.cpu().numpy(), face_area=fa.cpu().numpy(),
                 face_surf=fs.cpu().numpy(), vol_integral=vi.cpu().numpy(),
                 nfaces=nf.cpu().numpy(), status=st.cpu().numpy(), first_bad=fb.cpu().numpy(),
@@ -340,6 +410,8 @@ def mc_integrate_cell(ns: NodeSet, i: int, f: Integrand, n: int, m: int, rng,
     if n < 1 or m < 1:
         raise ValueError("need n >= 1 rays and m >= 1 subsamples")
     d = ns.dim
+    if neighbors is not None and len(neighbors) == 0:
+        raise UnboundedRay(i, sample_unit_sphere(d, rng))  # as mc_areas_only
     z, unif = _draw_integrate_stream(rng, n, m, d)
     cand = neighbors if neighbors is not None and len(neighbors) > 0 else None
     max_faces = _max_faces_for(ns, n, cand)
@@ -353,8 +425,6 @@ def mc_integrate_cell(ns: NodeSet, i: int, f: Integrand, n: int, m: int, rng,
             raise UnboundedRay(i, y / math.sqrt(float(y @ y)))
         if st == CELL_DEGENERATE:
             raise DegenerateConfiguration(f"a foreign generator lies on a circumsphere of cell {i}")
-        if st == CELL_OVERFLOW:
-            raise RuntimeError(f"cell {i} hit more than {max_faces} faces")
         k = int(res["nfaces"][0])
         js = [int(j) for j in res["face_j"][0, :k]]
         return CellIntegrals(volume=float(res["volume"][0]),

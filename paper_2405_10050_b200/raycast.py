@@ -166,18 +166,48 @@ def ray_keys(u, eta=None, inv_perm=None, rays_per_cell=1):
     return keys
 
 
-def coherent_order(ix, eta, u):
+def ray_order(u, eta=None, inv_perm=None, rays_per_cell=1, n_base=None, workspace=None,
+              stream=None):
+    """Processing order of a ray batch for the pruned kernels (vr_ray_order:
+    the vr_ray_keys keys, 32-bit when they fit, sorted by the library's own
+    stable radix sort): int32 device tensor, slot -> ray id.  `n_base` is
+    the range of the key base (the generator count, or the cell count when
+    eta is None); buffers come from `workspace` when given."""
+    n, d = u.shape
+    dev = u.device
+    L = _lib.lib()
+    nbytes = ctypes.c_int64(0)
+    _lib.check(L.vr_ray_order(None, None, d, 1, None, n, d, int(n_base), None, None,
+                              ctypes.byref(nbytes), None), "vr_ray_order (size)")
+    if workspace is not None:
+        tmp = workspace.get("order_tmp", (max(1, nbytes.value),), torch.uint8, dev)
+        order = workspace.get("order", (n,), torch.int32, dev)
+    else:
+        tmp = torch.empty(max(1, nbytes.value), dtype=torch.uint8, device=dev)
+        order = torch.empty(n, dtype=torch.int32, device=dev)
+    if eta is not None:
+        eta = eta.view(n, -1)
+        _lib.check(L.vr_ray_order(_lib.ptr(inv_perm), _lib.ptr(eta), eta.shape[1], 1, _lib.ptr(u),
+                                  n, d, int(n_base), _lib.ptr(order), _lib.ptr(tmp),
+                                  ctypes.byref(nbytes), _lib.stream_handle(stream)),
+                   "vr_ray_order")
+    else:
+        _lib.check(L.vr_ray_order(None, None, 0, int(rays_per_cell), _lib.ptr(u), n, d,
+                                  int(n_base), _lib.ptr(order), _lib.ptr(tmp),
+                                  ctypes.byref(nbytes), _lib.stream_handle(stream)),
+                   "vr_ray_order")
+    return order
+
+
+def coherent_order(ix, eta, u, workspace=None, stream=None):
     """Processing order for the pruned kernel: rays sorted by the kd position
     of their reference generator (eta[:, 0]), then by direction class, so
     that the 32 rays of a warp start close together and (within one
     generator) point the same way -- the warp-wide union of their spheres
     stays small.  (Scheduling the longest, near-hull warps first was
     measured slower: it breaks the locality of consecutive warps.)"""
-    eta = eta.to(torch.int32).contiguous()
-    keys = ray_keys(u.contiguous(), eta, ix.inv_perm)
-    if ix.n < (1 << 23):  # keys < 2^31: a 32-bit radix sort (half the passes)
-        keys = keys.to(torch.int32)
-    return torch.sort(keys, stable=True).indices.to(torch.int32)
+    return ray_order(u.contiguous(), eta.to(torch.int32).contiguous(), ix.inv_perm,
+                     n_base=ix.n, workspace=workspace, stream=stream)
 
 
 def _screen(ns, dev, screen):
@@ -257,10 +287,17 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
     n_cand = 0
     s32 = _screen(ns, dev, screen)
     if candidates is not None:
+        if len(np.asarray(candidates).ravel()) == 0:
+            # reference _Probe with an empty candidate array: every probe is
+            # all-invalid, so the ray escapes (raycast.py:100-102, 188-191)
+            idx.fill_(-1)
+            t.fill_(float("nan"))
+            flag.fill_(RAY_ESCAPED)
+            if rp is not None:
+                rp.fill_(float("nan"))
+            return RaycastBatch(idx, t, rp, flag)
         cand, crec, s32 = candidate_records(ns, candidates, dev, screen)
         n_cand = cand.shape[0]
-        if n_cand == 0:
-            raise ValueError("empty candidate set")
     s32p = ctypes.byref(s32.struct) if s32 is not None else None
     rl = ws.get("recheck_list", (n,), torch.int32, dev)
     rc = ws.get("recheck_count", (1,), torch.int32, dev)
@@ -272,11 +309,7 @@ def raycast_batch(ns: NodeSet, x, u, eta, candidates=None, want_rp=True, stats=N
         events[0].record(stream)
     if pruned:
         ix = ns.prune_index(dev)
-        if stream is None:
-            order = coherent_order(ix, ed, ud)
-        else:
-            with torch.cuda.stream(stream):
-                order = coherent_order(ix, ed, ud)
+        order = coherent_order(ix, ed, ud, workspace=ws, stream=stream)
         _lib.check(L.vr_raycast_pruned(_lib.ptr(rec), ns.n, d, sqmax, s32p, ctypes.byref(ix.struct),
                                        _lib.ptr(xd), _lib.ptr(ud), _lib.ptr(ed), k, n,
                                        _lib.ptr(order), _lib.ptr(idx), _lib.ptr(t),
@@ -441,7 +474,19 @@ class HostRaycaster:
                          flag=torch.empty(c, dtype=torch.uint8, device=self.dev),
                          h2d=torch.cuda.Event(), done=torch.cuda.Event(), d2h=torch.cuda.Event())
                     for _ in range(self.NBUF)]
+        # Each buffer's workspace is sized for a full chunk here, so a later
+        # (larger) chunk never reallocates a buffer an earlier captured graph
+        # still points at.
         self.ws = [Workspace() for _ in range(self.NBUF)]
+        nbytes = ctypes.c_int64(0)
+        L = _lib.lib()
+        _lib.check(L.vr_ray_order(None, None, d, 1, None, c, d, ns.n, None, None,
+                                  ctypes.byref(nbytes), None), "vr_ray_order (size)")
+        for w in self.ws:
+            w.get("recheck_list", (c,), torch.int32, self.dev)
+            w.get("recheck_count", (1,), torch.int32, self.dev)
+            w.get("order", (c,), torch.int32, self.dev)
+            w.get("order_tmp", (max(1, nbytes.value),), torch.uint8, self.dev)
         # One CUDA graph per (buffer, chunk size, mode, screen): the per-chunk
         # work (ray order, pruned RayCast, exact re-check) replays without the
         # ~0.5 ms of host-side launch overhead, so small chunks (short

@@ -287,6 +287,65 @@ def config5_balls(n_seeds=5, hops=4):
     np.savez_compressed(os.path.join(HERE, "config5_balls.npz"), **out)
 
 
+_C5_NS = None
+
+
+def _c5_ball(args):
+    """One seed's L-hop ball (BFS, every edge raycast by the reference)."""
+    m, sd, hops = args
+    ns = _C5_NS
+    t0 = time.time()
+    v = vr.descent(ns, int(sd), vrng.stream(0, "descent", int(sd)))
+    dist = {v.sigma: 0}
+    coords = {v.sigma: v.r}
+    frontier = [v.sigma]
+    for h in range(1, hops + 1):
+        nxt = []
+        for sig in frontier:
+            dirs = _vertex_directions(ns.points, sig, range(9))
+            for k in range(9):
+                eta = sig[:k] + sig[k + 1:]
+                res = vr.raycast_incircle(ns, vr.RayQuery(eta, coords[sig], dirs[k]),
+                                          heuristic=False)
+                if res is None:
+                    continue
+                s2, r2 = res
+                if s2 not in dist:
+                    dist[s2] = h
+                    coords[s2] = r2
+                    nxt.append(s2)
+        frontier = nxt
+    keys = sorted(dist)
+    print("config5 L5 ball", m, len(keys), "vertices", f"{time.time() - t0:.1f}s", flush=True)
+    return (m, int(sd), np.array(keys, dtype=np.int32),
+            np.array([dist[k] for k in keys], dtype=np.int8),
+            np.array([coords[k] for k in keys]))
+
+
+def config5_balls_l5(n_seeds=20, hops=5, procs=8):
+    """SURVEY.md §8(d) config-5 pin at bench scale: the L=5 balls of the
+    first 20 canonical seeds (reference descent + raycast_incircle BFS, as
+    config5_balls above), one process per seed with the NodeSet fork-shared.
+    The GPU test asserts every ball is contained in the 10,000-seed L=5
+    vertex set (and equals the GPU's own ball of that seed)."""
+    import multiprocessing as mp
+    global _C5_NS
+    pts = np.random.default_rng(0).random((10 ** 6, 8)).astype(np.float32).astype(np.float64)
+    _C5_NS = vr.build_node_set(pts)
+    seeds = np.random.default_rng(1).choice(10 ** 6, 10000, replace=False)[:n_seeds]
+    t0 = time.time()
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_c5_ball, [(m, int(sd), hops) for m, sd in enumerate(seeds)], chunksize=1)
+    out = {"hops": np.array([hops]), "seeds": seeds.astype(np.int64)}
+    for m, sd, sig, hp, r in res:
+        out[f"ball{m}_sigma"] = sig
+        out[f"ball{m}_hops"] = hp
+        out[f"ball{m}_r"] = r
+    out["reference_wall_s"] = np.array([time.time() - t0])
+    out["procs"] = np.array([procs])
+    np.savez_compressed(os.path.join(HERE, "config5_balls_l5.npz"), **out)
+
+
 def mc_integrate_golden():
     """mc_integrate_cell with the reference's built-in integrands and a plain
     Python callable, on reference RNG streams (integrate_mc.py:70-121)."""

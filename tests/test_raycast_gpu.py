@@ -418,7 +418,7 @@ def test_pack_records_mma_layout(d):
     pts = np.random.default_rng(40 + d).standard_normal((1000, d))
     ns = vb.NodeSet(pts)
     ix = ns.prune_index()
-    rec32 = ix.screen32.rec.cpu().numpy()
+    rec32 = ix.rec32rows.cpu().numpy()
     rows = rec32.shape[0]
     ks = (d + 2 + 7) // 8
     feat = np.zeros((rows, 8 * ks), dtype=np.float32)
