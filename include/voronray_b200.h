@@ -539,6 +539,51 @@ int vr_host_normals(uint64_t* state, const int64_t* rows, int64_t n, int64_t cou
  * (MEASURED_PEAKS.json has only HBM and bf16). */
 int vr_fma_probe(int dtype, int blocks, int iters, void* scratch, void* stream);
 
+/* ---- HMC post-processing --------------------------
+ * Replaces integrate_hmc.py:21-91 (hmc_volume, hmc_interface_integral,
+ * hmc_cell_integral) with segmented reductions over the sigma-keyed vertex
+ * set.
+ *
+ * vr_hmc_face_index: the interface index of a mesh (sigma (n_v, d+1) sorted
+ *   rows, edges (n_e, d) with counts): keys / vid (n_v d(d+1)/2 each) = the
+ *   (generator pair, vertex id) incidences radix-sorted by pair (stable, so
+ *   an interface's vertices stay in vertex order: Mesh.face_vertices,
+ *   core.py:223-246); ukeys (<= n_e d(d-1)/2) = sorted generator pairs of the
+ *   boundary edges (count 1: Mesh.face_is_unbounded, core.py:262-276),
+ *   *n_ukeys_out (host; the call synchronises); cell_unbounded (n_gen uint8:
+ *   Mesh.unbounded_cells); nb_count (n_gen int32: |Mesh.neighbors(i)|).
+ *   workspace == NULL: *workspace_bytes receives the scratch size.
+ * vr_hmc_faces: per queried interface (face_i, face_j, area): the vertex run
+ *   [out_first, + out_count) in `vid`, status (0 ok, 1 unbounded interface,
+ *   2 fewer than d vertices -- the reference raises UnboundedFace for both --
+ *   3 not an interface of the mesh), the vertex mean of f (compensated sum;
+ *   the reference uses math.fsum), the vertex centroid and
+ *   F = (d mean + f(centroid)) A / (d + 1) (integrate_hmc.py:42-64).
+ *   integrand_kind 0 skips f (centroid / counts only), else 1 const, 2
+ *   sin(x_1^2), 3 linear (integrands.py:10-44); coef is a HOST array.
+ * vr_hmc_cells: per cell c with faces [face_off[c], face_off[c+1]):
+ *   volume = (1/d) sum_j |x_i - x_j|/2 A_ij (integrate_hmc.py:21-39) and,
+ *   with an integrand, (d sum_j h_j F_ij / d + f(x_i) V) / (d + 1)
+ *   (integrate_hmc.py:67-91; V = volume_in[c] when given, else the pyramid
+ *   volume); out_status bit 0 unbounded cell (UnboundedCell), bit 1 a mesh
+ *   neighbour without an area (MissingNeighbor), bit 2 a failed interface. */
+int vr_hmc_face_index(const int32_t* sigma, int64_t n_v, int d, int64_t n_gen,
+                      const int32_t* edge_key, const int32_t* edge_count, int64_t n_e,
+                      uint64_t* keys, int32_t* vid, uint64_t* ukeys, int64_t* n_ukeys_out,
+                      uint8_t* cell_unbounded, int32_t* nb_count, void* workspace,
+                      int64_t* workspace_bytes, void* stream);
+int vr_hmc_faces(const uint64_t* keys, const int32_t* vid, int64_t n_keys, const uint64_t* ukeys,
+                 int64_t n_ukeys, const double* r, int d, const int32_t* face_i,
+                 const int32_t* face_j, const double* area, int64_t n_f, int integrand_kind,
+                 const double* coef, double* out_F, int32_t* out_status, int32_t* out_first,
+                 int32_t* out_count, double* out_mean, double* out_centroid, void* stream);
+int vr_hmc_cells(const double* rec, int d, const int32_t* cells, int64_t n_c,
+                 const int64_t* face_off, const int32_t* face_j, const double* area,
+                 const double* F, const int32_t* face_status, const uint8_t* cell_unbounded,
+                 const int32_t* nb_count, int integrand_kind, const double* coef,
+                 const double* volume_in, double* out_volume, double* out_integral,
+                 int32_t* out_status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -409,7 +409,8 @@ def vertex_directions_batch(ns: NodeSet, sigma):
     rec, _ = ns.device_records()
     dev = rec.device
     L = _lib.lib()
-    sd = _as_dev(np.asarray(sigma), dev, torch.int32).view(-1, ns.dim + 1)
+    sd = _as_dev(sigma if isinstance(sigma, torch.Tensor) else np.asarray(sigma), dev,
+                 torch.int32).view(-1, ns.dim + 1)
     nv = sd.shape[0]
     u = torch.empty((nv, ns.dim + 1, ns.dim), dtype=torch.float64, device=dev)
     ok = torch.empty((nv, ns.dim + 1), dtype=torch.uint8, device=dev)
