@@ -584,6 +584,25 @@ int vr_hmc_cells(const double* rec, int d, const int32_t* cells, int64_t n_c,
                  const double* volume_in, double* out_volume, double* out_integral,
                  int32_t* out_status, void* stream);
 
+/* ---- Mesh arrays (csrc/mesh.cu) ------------------------------------------
+ * vr_lex_order: stable lexicographic order of n rows of k int32 (k LSD
+ *   radix passes), order[i] = row id -- the order of `sorted()` over sigma /
+ *   eta tuples (the reference's dict views, core.py:205-221).
+ * vr_edge_incidence: the d-subsets of the n_v sigma rows (every vertex is
+ *   incident to its d+1 edges, graph.py:115-120) as distinct lexicographically
+ *   sorted keys (out_keys, <= n_v (d+1) rows of d) with their incidence
+ *   counts; *n_unique_out (host; the call synchronises).
+ * vr_edge_check: incident[e] = incidence count of recorded edge e (0 if no
+ *   vertex has it) -- verify_mesh's edge-consistency pass (graph.py:214-229).
+ * Workspace convention as vr_ray_order (NULL: size query). */
+int vr_lex_order(const int32_t* rows, int64_t n, int k, int32_t* order, void* workspace,
+                 int64_t* workspace_bytes, void* stream);
+int vr_edge_incidence(const int32_t* sigma, int64_t n_v, int d, int32_t* out_keys,
+                      int32_t* out_counts, int64_t* n_unique_out, void* workspace,
+                      int64_t* workspace_bytes, void* stream);
+int vr_edge_check(const int32_t* inc_keys, const int32_t* inc_counts, int64_t n_inc,
+                  const int32_t* edge_keys, int64_t n_e, int d, int32_t* incident, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

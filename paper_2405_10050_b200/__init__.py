@@ -19,7 +19,8 @@ from .integrate_mc import (CellIntegrals, Integrand, MCResult, mc_areas_only, mc
                            mc_directions, mc_integrals_cells, mc_integrate_cell, mc_uniforms,
                            sample_unit_sphere, sphere_surface_area)
 from . import integrands, io
-from .integrate_hmc import hmc_cell_integral, hmc_interface_integral, hmc_volume
+from .integrate_hmc import (HMCResult, face_index, hmc_cell_integral, hmc_cells,
+                            hmc_interface_integral, hmc_volume)
 
 __version__ = "0.1.0"
 
@@ -34,4 +35,5 @@ __all__ = [
     "MCResult", "sample_unit_sphere", "sphere_surface_area", "mc_areas_only", "mc_cells",
     "mc_directions", "mc_integrate_cell", "mc_integrals_cells", "mc_uniforms", "integrands",
     "errors", "rng", "io", "hmc_volume", "hmc_interface_integral", "hmc_cell_integral",
+    "hmc_cells", "HMCResult", "face_index",
 ]

@@ -65,6 +65,9 @@ _SIGNATURES = {
     "vr_prune_index_layout": [_i64, _int, _int, _vp],
     "vr_build_prune_index": [_vp, _i64, _int, _vp, _int, _vp, _i64, _vp, _i64, _vp, _vp],
     "vr_trav_level_workspace": [_i64, _i64, _i64, _int, _vp],
+    "vr_lex_order": [_vp, _i64, _int, _vp, _vp, _vp, _vp],
+    "vr_edge_incidence": [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp],
+    "vr_edge_check": [_vp, _vp, _i64, _vp, _i64, _int, _vp, _vp],
     "vr_hmc_face_index": [_vp, _i64, _int, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
                           _vp, _vp, _vp],
     "vr_hmc_faces": [_vp, _vp, _i64, _vp, _i64, _vp, _int, _vp, _vp, _vp, _i64, _int, _vp, _vp,

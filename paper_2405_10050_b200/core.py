@@ -391,11 +391,8 @@ class Mesh:
         import torch
         dv = self._dev
         ek, ec = dv["edge_key"], dv["edge_count"]
-        if ek.shape[0]:
-            order = torch.arange(ek.shape[0], device=ek.device)
-            for c in range(ek.shape[1] - 1, -1, -1):  # stable LSD lexicographic sort
-                _, o = torch.sort(ek[:, c].index_select(0, order), stable=True)
-                order = order.index_select(0, o)
+        if ek.shape[0]:  # the reference's sorted(edge_counts) order (vr_lex_order)
+            order = lex_order(ek)
             ek, ec = ek.index_select(0, order), ec.index_select(0, order)
 
         def host(t, dtype):
@@ -570,6 +567,44 @@ class Mesh:
         return key in self._unbounded_faces
 
 
+def lex_order(rows):
+    """Stable lexicographic row order of an int32 device tensor (vr_lex_order)."""
+    rows = rows.to(torch.int32).contiguous()
+    n, k = rows.shape
+    L = _lib.lib()
+    nb = ctypes.c_int64(0)
+    _lib.check(L.vr_lex_order(None, n, k, None, None, ctypes.byref(nb), None), "vr_lex_order")
+    ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=rows.device)
+    order = torch.empty(n, dtype=torch.int32, device=rows.device)
+    _lib.check(L.vr_lex_order(_lib.ptr(rows), n, k, _lib.ptr(order), _lib.ptr(ws),
+                              ctypes.byref(nb), _lib.stream_handle()), "vr_lex_order")
+    return order.long()
+
+
+def edge_incidence(ns, sigma):
+    """(distinct edge keys (E, d) lexicographic, incidence counts (E,)) of the
+    sigma rows, on the device (vr_edge_incidence)."""
+    rec, _ = ns.device_records()
+    dev = rec.device
+    d = ns.dim
+    sig = (sigma if isinstance(sigma, torch.Tensor) else torch.as_tensor(
+        np.ascontiguousarray(sigma, dtype=np.int32))).to(device=dev, dtype=torch.int32)
+    sig = sig.reshape(-1, d + 1).contiguous()
+    nv = sig.shape[0]
+    L = _lib.lib()
+    nb = ctypes.c_int64(0)
+    nu = ctypes.c_int64(0)
+    _lib.check(L.vr_edge_incidence(None, nv, d, None, None, None, None, ctypes.byref(nb), None),
+               "vr_edge_incidence (size)")
+    ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=dev)
+    keys = torch.empty((max(nv * (d + 1), 1), d), dtype=torch.int32, device=dev)
+    cnt = torch.empty(max(nv * (d + 1), 1), dtype=torch.int32, device=dev)
+    _lib.check(L.vr_edge_incidence(_lib.ptr(sig), nv, d, _lib.ptr(keys), _lib.ptr(cnt),
+                                   ctypes.byref(nu), _lib.ptr(ws), ctypes.byref(nb),
+                                   _lib.stream_handle()), "vr_edge_incidence")
+    return keys[:nu.value], cnt[:nu.value]
+
+
 def _row_hash(rows):
     """64-bit polynomial hash of int32 rows (device tensor), wrapping."""
     h = torch.zeros(rows.shape[0], dtype=torch.int64, device=rows.device)
@@ -579,22 +614,31 @@ def _row_hash(rows):
     return h
 
 
+def verify_vertices_device(ns: NodeSet, sigma, r, tol: float = TOL_VERTEX):
+    """verify_vertex (core.py:279-296) for device tensors sigma (V, d+1) /
+    r (V, d): equidistance and the incircle scan against all N generators
+    (vr_verify_vertices); a device bool tensor."""
+    rec, _ = ns.device_records()
+    dev = rec.device
+    sd = sigma.to(device=dev, dtype=torch.int32).reshape(-1, ns.dim + 1).contiguous()
+    rd = r.to(device=dev, dtype=torch.float64).reshape(-1, ns.dim).contiguous()
+    ok = torch.empty(sd.shape[0], dtype=torch.uint8, device=dev)
+    if sd.shape[0]:
+        _lib.check(_lib.lib().vr_verify_vertices(_lib.ptr(rec), ns.n, ns.dim, _lib.ptr(sd),
+                                                 _lib.ptr(rd), sd.shape[0], float(tol),
+                                                 _lib.ptr(ok), _lib.stream_handle()),
+                   "vr_verify_vertices")
+    return ok.bool()
+
+
 def verify_vertices(ns: NodeSet, sigma, r, tol: float = TOL_VERTEX):
     """Batched verify_vertex on the GPU: bool array, one per vertex."""
     sigma = np.ascontiguousarray(sigma, dtype=np.int32).reshape(-1, ns.dim + 1)
     r = np.ascontiguousarray(r, dtype=np.float64).reshape(-1, ns.dim)
     if sigma.shape[0] == 0:
         return np.zeros(0, dtype=bool)
-    rec, _ = ns.device_records()
-    dev = rec.device
-    L = _lib.lib()
-    sd = torch.from_numpy(sigma).to(dev)
-    rd = torch.from_numpy(r).to(dev)
-    ok = torch.empty(sigma.shape[0], dtype=torch.uint8, device=dev)
-    _lib.check(L.vr_verify_vertices(_lib.ptr(rec), ns.n, ns.dim, _lib.ptr(sd), _lib.ptr(rd),
-                                    sigma.shape[0], float(tol), _lib.ptr(ok),
-                                    _lib.stream_handle()), "vr_verify_vertices")
-    return ok.cpu().numpy().astype(bool)
+    ok = verify_vertices_device(ns, torch.from_numpy(sigma), torch.from_numpy(r), tol)
+    return ok.cpu().numpy()
 
 
 def verify_vertex(mesh: Mesh, v: VertexRecord, tol: float = TOL_VERTEX) -> bool:

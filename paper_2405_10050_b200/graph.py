@@ -29,7 +29,8 @@ import torch
 
 from . import _lib
 from . import rng as _rng
-from .core import (TOL_VERTEX, Mesh, NodeSet, VertexRecord, edge_keys, verify_vertices)
+from .core import (TOL_VERTEX, Mesh, NodeSet, VertexRecord, edge_incidence, edge_keys,
+                   verify_vertices, verify_vertices_device)
 from .errors import DegenerateConfiguration, RetryExhausted
 from .raycast import (PRUNE_MIN_GENERATORS, RANK_TOL, RayQuery, RaycastStats, Workspace,
                       _orthonormal_rows, _project_out, raycast_batch, raycast_incircle)
@@ -347,38 +348,56 @@ class VerifyReport:
 
 
 def verify_mesh(mesh: Mesh, oracle: bool = None, coord_tol: float = 1e-8) -> VerifyReport:
-    """Vertex, edge-consistency and (small instances) oracle checks (graph.py:202-245)."""
+    """Vertex, edge-consistency and (small instances) oracle checks
+    (graph.py:202-245), on the device: verify_vertices over every vertex,
+    then the incidence count of every recorded edge (vr_edge_incidence /
+    vr_edge_check) against its recorded count -- an interior edge (count 2)
+    must have exactly two incident vertices, whose sigmas then intersect in
+    eta; a boundary edge (count 1) exactly one.  Only failures are brought
+    to the host."""
     ns = mesh.nodes
-    verts = mesh.vertices
-    report = VerifyReport(vertices_total=len(verts))
-    keys = list(verts.keys())
-    if keys:
-        sig = np.array(keys, dtype=np.int32)
-        r = np.array([verts[k].r for k in keys], dtype=np.float64)
-        ok = verify_vertices(ns, sig, r)
-        report.vertex_failures = [keys[i] for i in np.nonzero(~ok)[0]]
-    by_edge = {}
-    for s in verts:
-        for e in edge_keys(s):
-            by_edge.setdefault(e, []).append(s)
-    for eta, count in mesh.edge_counts.items():
-        incident = by_edge.get(eta, [])
-        if count == 2:
-            if len(incident) != 2:
-                report.edge_failures.append((eta, f"count 2 but {len(incident)} vertices"))
-                continue
-            if set(incident[0]) & set(incident[1]) != set(eta):
-                report.edge_failures.append((eta, "incident sigmas do not intersect in eta"))
-        elif count == 1:
-            if len(incident) != 1:
-                report.edge_failures.append((eta, f"count 1 but {len(incident)} vertices"))
-        else:
-            report.edge_failures.append((eta, f"invalid count {count}"))
+    dv = mesh.device_arrays()
+    a = None if dv is not None else mesh.arrays()
+    dev = ns.device_records()[0].device
+    if dv is not None:
+        sig_d, r_d, ek_d, ec_d = dv["sigma"], dv["r"], dv["edge_key"], dv["edge_count"]
+    else:
+        sig_d = torch.as_tensor(a["sigma"], device=dev)
+        r_d = torch.as_tensor(a["r"], device=dev)
+        ek_d = torch.as_tensor(a["edge_key"], device=dev)
+        ec_d = torch.as_tensor(a["edge_count"], device=dev)
+    nv = int(sig_d.shape[0])
+    report = VerifyReport(vertices_total=nv)
+    if nv:
+        ok = verify_vertices_device(ns, sig_d, r_d)
+        bad = torch.nonzero(~ok).flatten().cpu().numpy()
+        sig_bad = sig_d[torch.as_tensor(bad, device=dev)].cpu().numpy() if bad.size else []
+        report.vertex_failures = [tuple(int(x) for x in s) for s in sig_bad]
+    if ek_d.shape[0]:
+        ikeys, icnt = edge_incidence(ns, sig_d)
+        inc = torch.empty(ek_d.shape[0], dtype=torch.int32, device=dev)
+        ek32 = ek_d.to(torch.int32).contiguous()
+        _lib.check(_lib.lib().vr_edge_check(_lib.ptr(ikeys), _lib.ptr(icnt), ikeys.shape[0],
+                                            _lib.ptr(ek32), ek32.shape[0], ns.dim, _lib.ptr(inc),
+                                            _lib.stream_handle()), "vr_edge_check")
+        ec = ec_d.to(torch.int32)
+        fail = ((ec != 1) & (ec != 2)) | (inc != ec)
+        idx = torch.nonzero(fail).flatten()
+        if idx.numel():
+            keys = ek32[idx].cpu().numpy()
+            cs, ks = ec[idx].cpu().numpy(), inc[idx].cpu().numpy()
+            for key, c, k in zip(keys, cs, ks):
+                eta = tuple(int(x) for x in key)
+                if c in (1, 2):
+                    report.edge_failures.append((eta, f"count {int(c)} but {int(k)} vertices"))
+                else:
+                    report.edge_failures.append((eta, f"invalid count {int(c)}"))
     if oracle is None:
         oracle = ns.dim <= 3 and ns.n <= 200
     if oracle:
         report.oracle_checked = True
         truth = brute_force_vertices(ns)
+        verts = mesh.vertices
         ours = {s: v.r for s, v in verts.items()}
         report.oracle_missing = sorted(set(truth) - set(ours))
         report.oracle_extra = sorted(set(ours) - set(truth))

@@ -150,6 +150,10 @@ def test_config3_full_diagram():
     assert int((a["edge_count"] == 2).sum()) == ref["n_interior_edges"]
     ok = vb.verify_vertices(mesh.nodes, a["sigma"][::97], a["r"][::97])
     assert ok.all()
+    # verify_mesh at full size on the device: every vertex against all
+    # generators, every recorded edge's incidence count
+    rep = vb.verify_mesh(mesh, oracle=False)
+    assert rep.passed and rep.vertices_total == ref["n_vertices"]
 
 
 def test_verify_mesh_and_perturbation():
@@ -162,6 +166,24 @@ def test_verify_mesh_and_perturbation():
     mesh.vertices[sig] = VertexRecord(sig, good.r + np.array([1e-3, 0.0]))
     bad = vb.verify_mesh(mesh, oracle=False)
     assert not bad.passed and sig in bad.vertex_failures
+    # edge-consistency failures (graph.py:214-229): a wrong count, a
+    # recorded edge no vertex has, an invalid count
+    a = vb.voronoi_graph(vb.build_node_set(pts), seed=0).arrays()
+    ek, ec = a["edge_key"].copy(), a["edge_count"].copy()
+    i2 = int(np.nonzero(ec == 2)[0][0])
+    i1 = int(np.nonzero(ec == 1)[0][0])
+    ec[i2], ec[i1] = 1, 3
+    ek = np.vstack([ek, [[118, 119]]])
+    ec = np.append(ec, 2)
+    m2 = vb.Mesh.from_arrays(mesh.nodes, a["sigma"], a["r"], ek, ec, a["boundary_sigma"],
+                             a["boundary_u"])
+    rep = vb.verify_mesh(m2, oracle=False)
+    got = dict(rep.edge_failures)
+    assert got[tuple(a["edge_key"][i2])] == "count 1 but 2 vertices"
+    assert got[tuple(a["edge_key"][i1])] == "invalid count 3"
+    if (118, 119) not in {tuple(k) for k in a["edge_key"]}:
+        assert got[(118, 119)] == "count 2 but 0 vertices"
+    assert not rep.vertex_failures
 
 
 def test_determinism_and_seed_independence():

@@ -137,6 +137,25 @@ def test_mesh_json_round_trip_is_byte_identical(tmp_path):
         vio.mesh_from_dict(data, vb.NodeSet(pts[:50]))
 
 
+def test_streamed_mesh_json_equals_dict_dump(tmp_path):
+    """io.write_mesh_json streams the bytes of dump_json(mesh_to_dict(m))
+    without building per-vertex dicts; the reference file reproduces."""
+    import os
+    from paper_2405_10050_b200 import io as vio
+    from conftest import GOLDEN
+    src = os.path.join(GOLDEN, "mesh_2d_reference.json")
+    mesh = vio.mesh_from_dict(vio.load_json(src), vb.NodeSet(np.random.default_rng(1234).random((120, 2))))
+    vio.write_mesh_json(mesh, tmp_path / "s.json")
+    assert (tmp_path / "s.json").read_bytes() == open(src, "rb").read()
+    # empty boundary / a single vertex
+    ns = vb.NodeSet([(0.0, 0.0), (1.0, 0.0), (0.0, 1.0)])
+    m = vb.Mesh.from_arrays(ns, np.array([[0, 1, 2]]), np.array([[0.5, 0.5]]),
+                            np.zeros((0, 2)), np.zeros(0), np.zeros((0, 3)), np.zeros((0, 2)))
+    vio.write_mesh_json(m, tmp_path / "t.json")
+    vio.dump_json(vio.mesh_to_dict(m), tmp_path / "u.json")
+    assert (tmp_path / "t.json").read_bytes() == (tmp_path / "u.json").read_bytes()
+
+
 def test_points_csv_round_trip(tmp_path):
     from paper_2405_10050_b200 import io as vio
     pts = np.random.default_rng(3).random((10, 3))
@@ -146,28 +165,6 @@ def test_points_csv_round_trip(tmp_path):
     (tmp_path / "bad.csv").write_text("1,2\n3\n")
     with pytest.raises(DimensionMismatch):
         vio.read_points_csv(tmp_path / "bad.csv")
-
-
-def test_hmc_matches_reference_on_reference_mesh():
-    """HMC post-processing (integrate_hmc.py) on the reference mesh and the
-    reference MC areas reproduces the reference values."""
-    import os
-    from paper_2405_10050_b200 import io as vio
-    from paper_2405_10050_b200.integrands import sinx2
-    from conftest import GOLDEN
-    gz = golden("hmc_io_golden.npz")
-    pts = np.random.default_rng(1234).random((120, 2))
-    ns = vb.NodeSet(pts)
-    mesh = vio.mesh_from_dict(vio.load_json(os.path.join(GOLDEN, "mesh_2d_reference.json")), ns)
-    for c in gz["cells"]:
-        areas = {int(j): float(a) for j, a in zip(gz[f"c{c}__j"], gz[f"c{c}__area"])}
-        hv = vb.hmc_volume(ns, int(c), areas, mesh)
-        ci = vb.hmc_cell_integral(mesh, int(c), sinx2, areas, hv)
-        assert hv == pytest.approx(gz[f"c{c}__hmc"][0], rel=1e-14)
-        assert ci == pytest.approx(gz[f"c{c}__hmc"][1], rel=1e-13)
-        fi = [vb.hmc_interface_integral(mesh, int(c), int(j), areas[int(j)], sinx2)
-              for j in gz[f"c{c}__j"]]
-        assert np.allclose(fi, gz[f"c{c}__face"], rtol=1e-13, atol=0)
 
 
 def test_integrands_resolve():
