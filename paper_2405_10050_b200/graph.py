@@ -356,9 +356,10 @@ def verify_mesh(mesh: Mesh, oracle: bool = None, coord_tol: float = 1e-8) -> Ver
     eta; a boundary edge (count 1) exactly one.  Only failures are brought
     to the host."""
     ns = mesh.nodes
+    dev = ns.device_records()[0].device
+    d = ns.dim
     dv = mesh.device_arrays()
     a = None if dv is not None else mesh.arrays()
-    dev = ns.device_records()[0].device
     if dv is not None:
         sig_d, r_d, ek_d, ec_d = dv["sigma"], dv["r"], dv["edge_key"], dv["edge_count"]
     else:
@@ -366,6 +367,18 @@ def verify_mesh(mesh: Mesh, oracle: bool = None, coord_tol: float = 1e-8) -> Ver
         r_d = torch.as_tensor(a["r"], device=dev)
         ek_d = torch.as_tensor(a["edge_key"], device=dev)
         ec_d = torch.as_tensor(a["edge_count"], device=dev)
+    # the reference-style dict views, once materialised, are what a caller
+    # edits (mesh.vertices[sigma] = ...): verify what they hold
+    if mesh._vertices is not None:
+        keys = list(mesh._vertices)
+        sig_d = torch.as_tensor(np.array(keys, dtype=np.int32).reshape(-1, d + 1), device=dev)
+        r_d = torch.as_tensor(np.array([mesh._vertices[k].r for k in keys],
+                                       dtype=np.float64).reshape(-1, d), device=dev)
+    if mesh._edge_counts is not None:
+        ek_d = torch.as_tensor(np.array(list(mesh._edge_counts), dtype=np.int32).reshape(-1, d),
+                               device=dev)
+        ec_d = torch.as_tensor(np.array(list(mesh._edge_counts.values()), dtype=np.int32),
+                               device=dev)
     nv = int(sig_d.shape[0])
     report = VerifyReport(vertices_total=nv)
     if nv:
