@@ -494,12 +494,62 @@ int vr_trav_claim(const vr_traverse_tables* tab, int d, const int32_t* ray_eta,
                   void* stream);
 
 /* New vertex base_id + new_off[k]: store sigma', its fp64 circumcentre
- * (no chained drift, SURVEY.md §8(c) rule 3) and bump its edge counters. */
+ * (no chained drift, SURVEY.md §8(c) rule 3) and, with bump != 0, bump its
+ * edge counters (graph.py:115-120; the owner-sharded traversal bumps at
+ * the edge owners instead, vr_trav_bump_keys). */
 int vr_trav_finalize(const vr_traverse_tables* tab, const double* rec, int d,
                      const int32_t* ray_sigma, const int64_t* slot,
                      const int32_t* new_flag, const int64_t* new_off,
                      int64_t n_rays, int32_t base_id, int32_t* vsig, double* vr,
-                     int32_t* bad, void* stream);
+                     int32_t* bad, int bump, void* stream);
+
+/* ---- Owner-sharded traversal (csrc/shard.cu) -------------
+ * Vertex sigma lives on rank owner(sigma), edge eta on owner(eta) (a hash of
+ * the sorted tuple, high bits, mod n_parts).  Per level each rank raycasts
+ * the open edges of its own frontier (vr_shard_open: open iff the edge's
+ * count, returned by its owner at the previous level, is < 2 --
+ * graph.py:127-128; vr_trav_level_rays: rays + order + pruned RayCast +
+ * exact re-check), sends the hit sigma' to their owners (vr_shard_bucket +
+ * an all-to-all), which dedupe them (vr_trav_claim_sigma: insert-or-find,
+ * smallest received row wins) and store the new vertices
+ * (vr_trav_finalize, bump = 0); the new vertices' edges (vr_vertex_edges)
+ * go to the edge owners, which bump them and answer with the counts
+ * (vr_trav_bump_keys) -- the next level's open test.  Results are those of
+ * the single-GPU level-synchronous traversal for any rank count.
+ *
+ * vr_shard_bucket: owner of each of n rows of k int32, a stable send order
+ *   perm (grouped by owner) and per-owner counts (device int64[n_parts]).
+ * vr_shard_gather_rows: out[i] = rows[perm[i]]; vr_shard_scatter_rows:
+ *   out[perm[i]] = rows[i] (k int32 per row).
+ * vr_shard_open: open mask / counts / exclusive offsets from per-vertex edge
+ *   counts (n_v, d+1), the ray count in *n_rays_out (host, synchronises). */
+int vr_shard_bucket(const int32_t* rows, int64_t n, int k, int n_parts, int32_t* perm,
+                    int64_t* counts, void* workspace, int64_t* workspace_bytes, void* stream);
+int vr_shard_gather_rows(const int32_t* rows, int k, const int32_t* perm, int64_t n,
+                         int32_t* out, void* stream);
+int vr_shard_scatter_rows(const int32_t* rows, int k, const int32_t* perm, int64_t n,
+                          int32_t* out, void* stream);
+int vr_shard_open(const int32_t* edge_counts, int64_t n_v, int d, uint8_t* open_mask,
+                  int32_t* open_count, int64_t* open_off, int64_t* n_rays_out, void* workspace,
+                  int64_t* workspace_bytes, void* stream);
+int vr_trav_claim_sigma(const vr_traverse_tables* tab, int d, const int32_t* rows, int64_t n,
+                        int32_t level, int64_t* out_slot, int32_t* new_flag, void* stream);
+int vr_trav_bump_keys(const vr_traverse_tables* tab, int d, const int32_t* keys, int64_t n,
+                      int32_t* counts_out, void* stream);
+/* The d+1 edges (d-subsets, sigma[k] omitted, k = 0..d) of n_v sigma rows. */
+int vr_vertex_edges(const int32_t* sigma, int64_t n_v, int d, int32_t* out, void* stream);
+/* vr_trav_level_cast without the local claim: the R edge rays of the
+ * frontier (emit), their order, the pruned RayCast + re-check; counts_out[3]
+ * (host) = {escapes, degenerate rays, affinely dependent frontier vertices}.
+ * Workspace: vr_trav_level_workspace(n_v, n_rays, ...). */
+int vr_trav_level_rays(const double* rec, int64_t n_gen, int d, double sqmax,
+                       const vr_screen32* s32, const vr_prune_index* ix,
+                       const int32_t* frontier_sigma, const double* frontier_r, int64_t n_v,
+                       const uint8_t* open_mask, const int64_t* open_off, int64_t n_rays,
+                       double* ray_x, double* ray_u, int32_t* ray_eta, int32_t* ray_parent,
+                       int32_t* hit_idx, double* hit_t, uint8_t* hit_flag, int32_t* bad,
+                       uint64_t* work, int64_t* counts_out, void* workspace,
+                       int64_t workspace_bytes, void* stream);
 
 /* Escaped rays -> BoundaryRay(sigma_parent, u) at base_b + esc_off[k]
  * (graph.py:138-139). */

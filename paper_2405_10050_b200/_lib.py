@@ -65,6 +65,15 @@ _SIGNATURES = {
     "vr_prune_index_layout": [_i64, _int, _int, _vp],
     "vr_build_prune_index": [_vp, _i64, _int, _vp, _int, _vp, _i64, _vp, _i64, _vp, _vp],
     "vr_trav_level_workspace": [_i64, _i64, _i64, _int, _vp],
+    "vr_shard_bucket": [_vp, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp],
+    "vr_shard_gather_rows": [_vp, _int, _vp, _i64, _vp, _vp],
+    "vr_shard_scatter_rows": [_vp, _int, _vp, _i64, _vp, _vp],
+    "vr_shard_open": [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "vr_trav_claim_sigma": [_vp, _int, _vp, _i64, ctypes.c_int32, _vp, _vp, _vp],
+    "vr_trav_bump_keys": [_vp, _int, _vp, _i64, _vp, _vp],
+    "vr_vertex_edges": [_vp, _i64, _int, _vp, _vp],
+    "vr_trav_level_rays": [_vp, _i64, _int, _dbl, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _vp,
+                           _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
     "vr_lex_order": [_vp, _i64, _int, _vp, _vp, _vp, _vp],
     "vr_edge_incidence": [_vp, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_edge_check": [_vp, _vp, _i64, _vp, _i64, _int, _vp, _vp],
@@ -85,7 +94,7 @@ _SIGNATURES = {
     "vr_trav_emit_rays": [_vp, _int, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_trav_claim": [_vp, _int, _vp, _vp, _vp, _i64, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp],
     "vr_trav_finalize": [_vp, _vp, _int, _vp, _vp, _vp, _vp, _i64, ctypes.c_int32, _vp, _vp,
-                         _vp, _vp],
+                         _vp, _int, _vp],
     "vr_trav_boundary": [_int, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp],
     "vr_trav_published": [_vp, _i64, _vp, _vp],
     "vr_trav_edge_compact": [_vp, _int, _vp, _vp, _vp, _vp],

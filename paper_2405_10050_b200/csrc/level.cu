@@ -71,6 +71,32 @@ __global__ void k_count_degenerate(const uint8_t* __restrict__ flag, int64_t n,
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
 }
 
+// cnt[0] += escaped rays, cnt[1] += degenerate rays
+__global__ void k_count_flags(const uint8_t* __restrict__ flag, int64_t n,
+                              unsigned long long* __restrict__ cnt) {
+  unsigned long long esc = 0, deg = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    esc += flag[i] == 1 ? 1 : 0;
+    deg += flag[i] == 3 ? 1 : 0;
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    esc += __shfl_xor_sync(0xffffffffu, esc, off);
+    deg += __shfl_xor_sync(0xffffffffu, deg, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (esc) atomicAdd(cnt, esc);
+    if (deg) atomicAdd(cnt + 1, deg);
+  }
+}
+
+__global__ void k_rays_counts(const unsigned long long* __restrict__ cnt,
+                              const int32_t* __restrict__ bad, int64_t* __restrict__ counts) {
+  counts[0] = (int64_t)cnt[0];
+  counts[1] = (int64_t)cnt[1];
+  counts[2] = bad[0];
+}
+
 // counts[0..4] = n_new, n_esc, n_degenerate, bad frontier vertices, overflow
 __global__ void k_level_counts(const int32_t* __restrict__ new_flag,
                                const int64_t* __restrict__ new_off,
@@ -121,7 +147,7 @@ int cast_plan(int64_t R, int64_t n_gen, int d, CastPlan& p) {
   p.o_rl = align256(p.o_order + 4 * R);
   p.o_rc = align256(p.o_rl + 4 * R);
   p.o_deg = align256(p.o_rc + 4);
-  p.o_cnt = align256(p.o_deg + 8);
+  p.o_cnt = align256(p.o_deg + 16);
   p.o_tmp = align256(p.o_cnt + 8 * 5);
   p.total = p.o_tmp + p.tmp;
   return VR_OK;
@@ -229,6 +255,63 @@ extern "C" int vr_trav_level_cast(
                                   tab->overflow, dcounts);
   if ((e = cudaGetLastError()) != cudaSuccess) return fail(e);
   if ((e = cudaMemcpyAsync(counts_out, dcounts, 5 * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(st)) != cudaSuccess)
+    return fail(e);
+  return VR_OK;
+}
+
+// The rays of one level without the local claim (owner-sharded traversal:
+// the hits go to their owners).  counts_out[3] = {escapes, degenerate rays,
+// affinely dependent frontier vertices}.
+extern "C" int vr_trav_level_rays(const double* rec, int64_t n_gen, int d, double sqmax,
+                                  const vr_screen32* s32, const vr_prune_index* ix,
+                                  const int32_t* frontier_sigma, const double* frontier_r,
+                                  int64_t n_v, const uint8_t* open_mask, const int64_t* open_off,
+                                  int64_t n_rays, double* ray_x, double* ray_u, int32_t* ray_eta,
+                                  int32_t* ray_parent, int32_t* hit_idx, double* hit_t,
+                                  uint8_t* hit_flag, int32_t* bad, uint64_t* work,
+                                  int64_t* counts_out, void* workspace, int64_t workspace_bytes,
+                                  void* stream) {
+  if (!rec || !ix || !ix->inv_perm || !frontier_sigma || !frontier_r || !open_mask ||
+      !open_off || !ray_x || !ray_u || !ray_eta || !ray_parent || !hit_idx || !hit_t ||
+      !hit_flag || !bad || !counts_out)
+    return VR_EINVAL;
+  for (int i = 0; i < 3; ++i) counts_out[i] = 0;
+  if (n_rays <= 0) return VR_OK;
+  if (n_rays >= (int64_t)1 << 31) return VR_EINVAL;
+  const int64_t R = n_rays;
+  CastPlan P;
+  int s = cast_plan(R, n_gen, d, P);
+  if (s) return s;
+  if (!workspace || workspace_bytes < (int64_t)P.total) return VR_ECAPACITY;
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(bad, 0, 2 * sizeof(int32_t), st)) != cudaSuccess) return fail(e);
+  s = vr_trav_emit_rays(rec, d, frontier_sigma, frontier_r, n_v, open_mask, open_off, ray_x,
+                        ray_u, ray_eta, ray_parent, bad, stream);
+  if (s) return s;
+  char* base = static_cast<char*>(workspace);
+  int32_t* order = reinterpret_cast<int32_t*>(base + P.o_order);
+  int32_t* rl = reinterpret_cast<int32_t*>(base + P.o_rl);
+  int32_t* rc = reinterpret_cast<int32_t*>(base + P.o_rc);
+  unsigned long long* ndeg = reinterpret_cast<unsigned long long*>(base + P.o_deg);
+  int64_t* dcounts = reinterpret_cast<int64_t*>(base + P.o_cnt);
+  void* tmp = base + P.o_tmp;
+  int64_t tb = (int64_t)P.tmp;
+  s = vr_ray_order(ix->inv_perm, ray_eta, d, 1, ray_u, R, d, n_gen, order, tmp, &tb, stream);
+  if (s) return s;
+  s = vr_raycast_pruned(rec, n_gen, d, sqmax, s32, ix, ray_x, ray_u, ray_eta, d, R, order,
+                        hit_idx, hit_t, nullptr, hit_flag, rl, rc, work, stream);
+  if (s) return s;
+  s = vr_raycast_recheck(rec, n_gen, d, nullptr, nullptr, 0, ray_x, ray_u, ray_eta, d, rl, rc, R,
+                         hit_idx, hit_t, nullptr, hit_flag, stream);
+  if (s) return s;
+  if ((e = cudaMemsetAsync(ndeg, 0, 16, st)) != cudaSuccess) return fail(e);
+  const unsigned g = nbk(R, 256) < 1184 ? nbk(R, 256) : 1184;
+  k_count_flags<<<g, 256, 0, st>>>(hit_flag, R, ndeg);
+  k_rays_counts<<<1, 1, 0, st>>>(ndeg, bad, dcounts);
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail(e);
+  if ((e = cudaMemcpyAsync(counts_out, dcounts, 3 * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
       (e = cudaStreamSynchronize(st)) != cudaSuccess)
     return fail(e);
   return VR_OK;

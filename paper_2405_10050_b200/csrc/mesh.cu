@@ -239,3 +239,13 @@ extern "C" int vr_edge_check(const int32_t* inc_keys, const int32_t* inc_counts,
   });
   VR_RETURN_LAUNCH();
 }
+
+extern "C" int vr_vertex_edges(const int32_t* sigma, int64_t n_v, int d, int32_t* out,
+                               void* stream) {
+  if (n_v <= 0) return VR_OK;
+  if (!sigma || !out) return VR_EINVAL;
+  VR_DISPATCH_D(d, {
+    k_incidences<D><<<grid_for(n_v), 256, 0, as_stream(stream)>>>(sigma, n_v, out);
+  });
+  VR_RETURN_LAUNCH();
+}

@@ -264,6 +264,61 @@ __global__ void k_claim(Tables t, const int32_t* __restrict__ ray_eta,
   out_slot[k] = h;
 }
 
+// Claim received sigma rows (owner-sharded traversal): as k_claim with the
+// candidate already formed; row k claims with id k (smallest row wins).
+template <int D>
+__global__ void k_claim_sigma(Tables t, const int32_t* __restrict__ rows, int64_t n,
+                              int32_t level, int64_t* __restrict__ out_slot) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int32_t s[D + 1];
+#pragma unroll
+  for (int a = 0; a <= D; ++a) s[a] = rows[k * (D + 1) + a];
+  bool ins;
+  const int64_t h = table_insert<D + 1>(t.vkeys, t.vstate, t.vcap, s, ins, t.overflow,
+                                        [&](int64_t hh) {
+                                          t.vval[hh] = (int32_t)k;
+                                          t.vlevel[hh] = level;
+                                        });
+  if (h >= 0 && !ins && __ldcg(t.vlevel + h) == level) atomicMin(&t.vval[h], (int32_t)k);
+  out_slot[k] = h;
+}
+
+__global__ void k_winners_sigma(Tables t, const int64_t* __restrict__ slot, int64_t n,
+                                int32_t level, int32_t* __restrict__ new_flag) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t h = slot[k];
+  new_flag[k] = (h >= 0 && t.vlevel[h] == level && t.vval[h] == (int32_t)k) ? 1 : 0;
+}
+
+// Edge-owner side of the sharded bump: +1 per received key (insert-or-find),
+// then, after every bump of the level, the count of each key.
+template <int D>
+__global__ void k_bump_keys(Tables t, const int32_t* __restrict__ keys, int64_t n) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int32_t e[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) e[a] = keys[k * D + a];
+  bool ins;
+  const int64_t h = table_insert<D>(t.ekeys, t.estate, t.ecap, e, ins, t.overflow,
+                                    [&](int64_t) {});
+  if (h >= 0) atomicAdd(&t.ecount[h], 1);
+}
+
+template <int D>
+__global__ void k_edge_counts(Tables t, const int32_t* __restrict__ keys, int64_t n,
+                              int32_t* __restrict__ out) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int32_t e[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) e[a] = keys[k * D + a];
+  const int64_t h = table_find<D>(t.ekeys, t.estate, t.ecap, e);
+  out[k] = h >= 0 ? __ldcg(t.ecount + h) : 0;
+}
+
 template <int D>
 __global__ void k_winners(Tables t, const int64_t* __restrict__ slot,
                           const uint8_t* __restrict__ hit_flag, int64_t n, int32_t level,
@@ -449,7 +504,7 @@ extern "C" int vr_trav_finalize(const vr_traverse_tables* tab, const double* rec
                                 const int32_t* ray_sigma, const int64_t* slot,
                                 const int32_t* new_flag, const int64_t* new_off, int64_t n_rays,
                                 int32_t base_id, int32_t* vsig, double* vr, int32_t* bad,
-                                void* stream) {
+                                int bump, void* stream) {
   if (!tab || !rec || !ray_sigma || !slot || !new_flag || !new_off || !vsig || !vr || !bad)
     return VR_EINVAL;
   if (n_rays <= 0) return VR_OK;
@@ -457,7 +512,8 @@ extern "C" int vr_trav_finalize(const vr_traverse_tables* tab, const double* rec
   VR_DISPATCH_D(d, {
     k_finalize<D><<<nb(n_rays, 128), 128, 0, as_stream(stream)>>>(
         t, rec, ray_sigma, slot, new_flag, new_off, n_rays, base_id, vsig, vr, bad);
-    k_bump_new<D><<<nb(n_rays), 256, 0, as_stream(stream)>>>(t, ray_sigma, new_flag, n_rays);
+    if (bump)
+      k_bump_new<D><<<nb(n_rays), 256, 0, as_stream(stream)>>>(t, ray_sigma, new_flag, n_rays);
   });
   VR_RETURN_LAUNCH();
 }
@@ -490,6 +546,32 @@ extern "C" int vr_trav_edge_compact(const vr_traverse_tables* tab, int d, const 
   const Tables t = from(tab);
   VR_DISPATCH_D(d, {
     k_edge_compact<D><<<nb(t.ecap), 256, 0, as_stream(stream)>>>(t, off, out_keys, out_count);
+  });
+  VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_trav_claim_sigma(const vr_traverse_tables* tab, int d, const int32_t* rows,
+                                   int64_t n, int32_t level, int64_t* out_slot,
+                                   int32_t* new_flag, void* stream) {
+  if (!tab || !rows || !out_slot || !new_flag) return VR_EINVAL;
+  if (n <= 0) return VR_OK;
+  const Tables t = from(tab);
+  VR_DISPATCH_D(d, {
+    k_claim_sigma<D><<<nb(n), 256, 0, as_stream(stream)>>>(t, rows, n, level, out_slot);
+  });
+  k_winners_sigma<<<nb(n), 256, 0, as_stream(stream)>>>(t, out_slot, n, level, new_flag);
+  VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_trav_bump_keys(const vr_traverse_tables* tab, int d, const int32_t* keys,
+                                 int64_t n, int32_t* counts_out, void* stream) {
+  if (!tab || !keys) return VR_EINVAL;
+  if (n <= 0) return VR_OK;
+  const Tables t = from(tab);
+  VR_DISPATCH_D(d, {
+    k_bump_keys<D><<<nb(n), 256, 0, as_stream(stream)>>>(t, keys, n);
+    if (counts_out)
+      k_edge_counts<D><<<nb(n), 256, 0, as_stream(stream)>>>(t, keys, n, counts_out);
   });
   VR_RETURN_LAUNCH();
 }

@@ -627,7 +627,7 @@ class DeviceTraversal:
         T = self.tables()
         _lib.check(L.vr_trav_finalize(ctypes.byref(T), p(self.rec), d, p(rsig), p(slot),
                                       p(newf), p(noff), R, f1, p(self.vsig), p(self.vr),
-                                      p(bad[1:]), sh), "finalize")
+                                      p(bad[1:]), 1, sh), "finalize")
         self.e_ub += (d + 1) * n_new
         if n_esc:
             self.ensure_boundary(n_esc)
@@ -699,7 +699,7 @@ class DeviceTraversal:
         _lib.check(L.vr_trav_finalize(ctypes.byref(T), _lib.ptr(self.rec), d, _lib.ptr(rsig),
                                       _lib.ptr(slot), _lib.ptr(newf), _lib.ptr(noff), R, f1,
                                       _lib.ptr(self.vsig), _lib.ptr(self.vr), _lib.ptr(bad[1:]),
-                                      sh), "finalize")
+                                      1, sh), "finalize")
         self.e_ub += (d + 1) * n_new
         if n_esc:
             self.ensure_boundary(n_esc)
@@ -760,6 +760,21 @@ def _table_estimate(ns, v_guess):
     return max(int(v), 1)
 
 
+def _group_size(group):
+    import torch.distributed as dist
+    return dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+
+
+def _sharding():
+    """Multi-rank traversal scheme: "owner" (default; parallel.ShardedTraversal,
+    owner-sharded tables, per-level all-to-all) or "replicated" (replicated
+    tables, ray-sharded levels, one all-gather of the hits per level)."""
+    mode = os.environ.get("VR_SHARDING", "owner")
+    if mode not in ("owner", "replicated"):
+        raise ValueError(f"VR_SHARDING must be owner or replicated, got {mode!r}")
+    return mode
+
+
 def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heuristic",
                   eps: float = None, stats: RaycastStats = None, return_info: bool = False,
                   group=None, work=None):
@@ -779,6 +794,27 @@ def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heurist
     # grow: config 3 rehashed its edge table 8 times from the default size
     vpg = {2: 2, 3: 7, 4: 32, 5: 190, 6: 1300, 7: 9000, 8: 66000}.get(ns.dim, 4)
     v_est = _table_estimate(ns, ns.n * vpg)
+    size = _group_size(group)
+    if size > 1 and _sharding() == "owner":
+        from .parallel import DeviceShardOps, ShardedTraversal
+        share = v_est // size + 1024
+        st = ShardedTraversal(ns, DeviceShardOps(ns, vcap_hint=max(4096, 2 * share),
+                                                 ecap_hint=2 * (ns.dim + 1) * share), group)
+        st.ops.work = work
+        st.seed(np.asarray([first.sigma], dtype=np.int32))
+        levels, lvl = [], 1
+        while True:
+            n_new = st.level(lvl, stats)
+            levels.append(n_new)
+            if n_new == 0:
+                break
+            lvl += 1
+        mesh = st.gather()
+        if return_info:
+            return mesh, {"levels": levels, "vertices": mesh.n_vertices,
+                          "boundary": int(mesh.device_arrays()["boundary_sigma"].shape[0]),
+                          "sharding": "owner"}
+        return mesh
     tr = DeviceTraversal(ns, vcap_hint=max(4 * ns.n, 2 * v_est),
                          ecap_hint=2 * (ns.dim + 1) * v_est)
     tr.work = work
@@ -830,6 +866,16 @@ def voronoi_local(ns: NodeSet, starts, hops: int, seed: int = 0, stats: RaycastS
         sig, _ = descent_batch(ns, starts, seed=seed, stats=stats)
     _, first = np.unique(sig, axis=0, return_index=True)
     sig = sig[np.sort(first)]
+    if size > 1 and _sharding() == "owner":
+        from .parallel import DeviceShardOps, ShardedTraversal
+        share = 6 * len(sig) * 4 ** min(hops, 8) // size + 1024
+        st = ShardedTraversal(ns, DeviceShardOps(ns, vcap_hint=max(4096, share)), group)
+        st.ops.work = work
+        st.seed(sig)
+        for lvl in range(1, hops + 1):
+            if st.level(lvl, stats) == 0:
+                break
+        return st.gather(with_levels=True) if return_levels else st.gather()
     tr = DeviceTraversal(ns, vcap_hint=max(4 * ns.n, 6 * len(sig) * 4 ** min(hops, 8)))
     tr.work = work
     tr.seed_vertices(sig)

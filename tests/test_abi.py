@@ -79,14 +79,16 @@ def test_integration_md_binding_runs():
     code = code.replace("/path/to/paper_2405_10050_b200/_voronray_b200.so", LIB_PATH)
     env = {}
     exec(compile(code, "INTEGRATION.md", "exec"), env)
-    pts = np.random.default_rng(4).random((700, 4))
-    ns = vb.NodeSet(pts)
-    dn = env["DeviceNodes"](ns)
-    rng = np.random.default_rng(5)
-    g = rng.integers(0, 700, 300).astype(np.int32)
-    u = rng.standard_normal((300, 4))
-    u /= np.linalg.norm(u, axis=1, keepdims=True)
-    idx, t, rp, fl = env["raycast_many"](dn, pts[g], u, g[:, None])
-    ref = vb.raycast_batch(ns, pts[g], u, g[:, None])
-    assert np.array_equal(idx, ref.idx.cpu().numpy())
-    assert np.array_equal(fl, ref.flag.cpu().numpy())
+    for n, d in ((700, 4), (5000, 6), (3000, 8)):
+        pts = np.random.default_rng(4 + d).random((n, d))
+        ns = vb.NodeSet(pts)
+        dn = env["DeviceNodes"](ns)
+        rng = np.random.default_rng(5 + d)
+        g = rng.integers(0, n, 3000).astype(np.int32)
+        u = rng.standard_normal((3000, d))
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        idx, t, rp, fl = env["raycast_many"](dn, pts[g], u, g[:, None])
+        ref = vb.raycast_batch(ns, pts[g], u, g[:, None], mode="exhaustive", screen="fp64")
+        assert np.array_equal(idx, ref.idx.cpu().numpy())
+        assert np.array_equal(fl, ref.flag.cpu().numpy())
+        assert np.array_equal(t, ref.t.cpu().numpy(), equal_nan=True)

@@ -353,3 +353,76 @@ def test_config5_bench_scale_balls_contained_and_verified():
     sel = torch.as_tensor(pick, device=dv["sigma"].device)
     ok = vb.verify_vertices(ns, dv["sigma"][sel].cpu().numpy(), dv["r"][sel].cpu().numpy())
     assert ok.all()
+
+
+_OWNER_SCRIPT = r"""
+import hashlib, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, sys.argv[1])
+import paper_2405_10050_b200 as vb
+torch.cuda.set_device(0)          # both ranks on one GPU: host (gloo) collectives only
+dist.init_process_group("gloo")
+out = {}
+def dig(a):
+    a = a[np.lexsort(a.T[::-1])]
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<i4").tobytes()).hexdigest()
+for name, pts in (("c1", np.random.default_rng(0).random((1000, 3))),
+                  ("c3", np.random.default_rng(0).standard_normal((10000, 5)))):
+    m, info = vb.voronoi_graph(vb.NodeSet(pts), seed=0, return_info=True)
+    a = m.arrays()
+    out[name + "_sigma"] = np.array([dig(a["sigma"])])
+    out[name + "_boundary"] = np.array([dig(a["boundary_sigma"])])
+    out[name + "_edges"] = np.array([a["edge_key"].shape[0], int((a["edge_count"] == 2).sum())])
+    out[name + "_sharding"] = np.array([info.get("sharding", "")])
+g = np.load(sys.argv[3])
+pts5 = np.random.default_rng(0).random((10 ** 6, 8)).astype(np.float32).astype(np.float64)
+ns5 = vb.NodeSet(pts5)
+m, lv = vb.voronoi_local(ns5, g["seeds"], hops=5, return_levels=True)
+a = m.arrays()
+o = np.lexsort(a["sigma"].T[::-1])
+out["c5_sigma"], out["c5_levels"] = a["sigma"][o], lv[o]
+if dist.get_rank() == 0:
+    np.savez(sys.argv[2], **out)
+dist.destroy_process_group()
+"""
+
+
+def test_owner_sharded_traversal_two_ranks_matches_reference(tmp_path):
+    """Owner-sharded traversal (parallel.ShardedTraversal + DeviceShardOps:
+    vertex / edge hash shards per rank, per-level all-to-all of hit sigmas and
+    edge keys) over two ranks sharing the one GPU (gloo: host collectives, no
+    kernel waits on another rank): configs 1 and 3 give the reference's
+    sigma / boundary digests and edge counts, and the L=5 traversal from the
+    20 golden config-5 seeds is exactly the union of the reference balls with
+    each vertex at its minimal hop level."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "owner.py"
+    script.write_text(_OWNER_SCRIPT)
+    out = str(tmp_path / "owner.npz")
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", "29547", str(script), root, out,
+                        os.path.join(GOLDEN, "config5_balls_l5.npz")],
+                       capture_output=True, text=True, timeout=1200)
+    assert p.returncode == 0, p.stderr[-3000:]
+    got = np.load(out)
+    assert got["c1_sharding"][0] == "owner"
+    assert got["c1_sigma"][0] == "b1f6f8721369b9116ff154e6673225998fb3785479bb65c18dafb6b2db2c0b1a"
+    assert got["c1_boundary"][0] == "eb6f64df1d992a4685bc309040f1aa6c09d6c7927edaa76dfa05006870927f78"
+    gz1 = golden("mesh_config1.npz")
+    assert got["c1_edges"][0] == len(gz1["edge_key"])
+    with open(os.path.join(GOLDEN, "config3_reference.json")) as fh:
+        ref3 = json.load(fh)
+    assert got["c3_sigma"][0] == ref3["sigma_digest"]
+    assert got["c3_boundary"][0] == ref3["boundary_digest"]
+    assert list(got["c3_edges"]) == [ref3["n_edges"], ref3["n_interior_edges"]]
+    gz = golden("config5_balls_l5.npz")
+    best = {}
+    for m in range(20):
+        for row, h in zip(gz[f"ball{m}_sigma"].tolist(), gz[f"ball{m}_hops"].tolist()):
+            t = tuple(row)
+            best[t] = min(h, best.get(t, 99))
+    keys = sorted(best)
+    assert np.array_equal(got["c5_sigma"], np.array(keys, dtype=np.int32))
+    assert np.array_equal(got["c5_levels"], np.array([best[k] for k in keys], dtype=np.int8))
