@@ -553,8 +553,8 @@ extern "C" int vr_trav_edge_compact(const vr_traverse_tables* tab, int d, const 
 extern "C" int vr_trav_claim_sigma(const vr_traverse_tables* tab, int d, const int32_t* rows,
                                    int64_t n, int32_t level, int64_t* out_slot,
                                    int32_t* new_flag, void* stream) {
-  if (!tab || !rows || !out_slot || !new_flag) return VR_EINVAL;
   if (n <= 0) return VR_OK;
+  if (!tab || !rows || !out_slot || !new_flag) return VR_EINVAL;
   const Tables t = from(tab);
   VR_DISPATCH_D(d, {
     k_claim_sigma<D><<<nb(n), 256, 0, as_stream(stream)>>>(t, rows, n, level, out_slot);
@@ -565,8 +565,8 @@ extern "C" int vr_trav_claim_sigma(const vr_traverse_tables* tab, int d, const i
 
 extern "C" int vr_trav_bump_keys(const vr_traverse_tables* tab, int d, const int32_t* keys,
                                  int64_t n, int32_t* counts_out, void* stream) {
-  if (!tab || !keys) return VR_EINVAL;
   if (n <= 0) return VR_OK;
+  if (!tab || !keys) return VR_EINVAL;
   const Tables t = from(tab);
   VR_DISPATCH_D(d, {
     k_bump_keys<D><<<nb(n), 256, 0, as_stream(stream)>>>(t, keys, n);
