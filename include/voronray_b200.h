@@ -111,6 +111,11 @@ int vr_pack_records32_pairs(const float* rec32, int64_t rows, int d, float* out,
  * rows * 8 * KS floats; rows must be a multiple of 64. */
 int vr_pack_records_mma(const float* rec32, int64_t rows, int d, float* out, void* stream);
 
+/* fp32 centred records -> the tcgen05 screen operand (vr_prune_index.recU):
+ * the features of vr_pack_records_mma in the canonical UMMA layout;
+ * `out` holds rows * 8 * ceil((d+2)/8) floats; rows a multiple of 64. */
+int vr_pack_records_umma(const float* rec32, int64_t rows, int d, float* out, void* stream);
+
 /* Batched incircle RayCast (reference raycast_incircle, raycast.py:154-224,
  * with its filtered NN probe _Probe, raycast.py:85-151, core.py:62-103).
  *
@@ -186,6 +191,12 @@ typedef struct vr_prune_index {
    * stride; [c - h, c + h] contains the exact box), read by the tensor-core
    * kernel's tree walk; required with recB. */
   const float* node_cb32;
+  /* tcgen05 screen operand (vr_pack_records_umma; nullable): the fp32 rows
+   * as tf32 features [x, |x|^2, 1, 0 ..] per tile of 64 in the canonical
+   * K-major no-swizzle UMMA layout -- per k-step of 8 features, 8-row x
+   * 16-byte core matrices: float index s*512 + (c >> 3)*64 + q*32 + (c & 7)*4
+   * + e for candidate c, feature 8s + 4q + e. */
+  const float* recU;
 } vr_prune_index;
 
 /* vr_raycast_batch through the pruned index.  `order` (nullable, n_rays
@@ -252,7 +263,8 @@ typedef struct vr_prune_layout {
   int64_t n_nodes;
   int32_t wide_levels;
 } vr_prune_layout;
-#define VR_PRUNE_MMA 1
+#define VR_PRUNE_MMA 1   /* also pack recB (mma.sync screen operand)  */
+#define VR_PRUNE_UMMA 2  /* also pack recU (tcgen05 screen operand)   */
 int vr_screen32_stats(const double* rec, int64_t n, int d, const double* center, double* stats,
                       void* stream);
 int vr_prune_index_layout(int64_t n, int d, int flags, vr_prune_layout* out);

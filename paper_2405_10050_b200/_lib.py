@@ -51,6 +51,7 @@ _SIGNATURES = {
     "vr_pack_records32": [_vp, _i64, _int, _vp, _vp, _vp],
     "vr_pack_records32_pairs": [_vp, _i64, _int, _vp, _vp],
     "vr_pack_records_mma": [_vp, _i64, _int, _vp, _vp],
+    "vr_pack_records_umma": [_vp, _i64, _int, _vp, _vp],
     "vr_host_streams": [ctypes.c_uint64, ctypes.c_uint64, _vp, _i64, _vp],
     "vr_descent_directions": [_vp, _int, _vp, _vp, _vp, _i64, ctypes.c_double, _vp, _vp, _vp,
                               _vp],

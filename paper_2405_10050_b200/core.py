@@ -215,7 +215,8 @@ class _PruneStruct(ctypes.Structure):
                 ("n", ctypes.c_int64), ("wide_box32", ctypes.c_void_p),
                 ("wide_levels", ctypes.c_int32), ("wide_off", ctypes.c_int64 * 8),
                 ("wide_cnt", ctypes.c_int64 * 8), ("recB", ctypes.c_void_p),
-                ("rec32rows", ctypes.c_void_p), ("node_cb32", ctypes.c_void_p)]
+                ("rec32rows", ctypes.c_void_p), ("node_cb32", ctypes.c_void_p),
+                ("recU", ctypes.c_void_p)]
 
 
 class _PruneLayout(ctypes.Structure):
@@ -225,6 +226,7 @@ class _PruneLayout(ctypes.Structure):
 
 
 VR_PRUNE_MMA = 1
+VR_PRUNE_UMMA = 2
 MMA_MIN_D = int(os.environ.get("VR_MMA_MIN_D", "5"))  # tensor-core screen from this d
 
 
@@ -238,7 +240,10 @@ class PruneIndex:
     def __init__(self, rec, n, d, center, workspace=None):
         L = _lib.lib()
         dev = rec.device
-        flags = VR_PRUNE_MMA if (d >= MMA_MIN_D and os.environ.get("VR_MMA", "1") != "0") else 0
+        # tensor-core screen operands from d = MMA_MIN_D: mma.sync fragments
+        # (recB) and the canonical tcgen05 layout (recU); VR_MMA=0 disables
+        flags = (VR_PRUNE_MMA | VR_PRUNE_UMMA) if (d >= MMA_MIN_D and
+                                                   os.environ.get("VR_MMA", "2") != "0") else 0
         lay = _PruneLayout()
         _lib.check(L.vr_prune_index_layout(int(n), d, flags, ctypes.byref(lay)),
                    "vr_prune_index_layout")
@@ -285,6 +290,7 @@ class PruneIndex:
         self.wide_off = [int(st.wide_off[i]) for i in range(st.wide_levels)]
         self.wide_box32 = view(st.wide_box32, (sum(self.wide_cnt), b32), torch.float32)
         self.recB = view(st.recB, (self.rows, 8 * ks), torch.float32)
+        self.recU = view(st.recU, (self.rows, 8 * ks), torch.float32)
 
 
 def build_node_set(points, backend="auto"):

@@ -253,6 +253,28 @@ __global__ void k_pack_mma(const float* __restrict__ rec32, int64_t rows, float*
   }
 }
 
+// fp32 records -> the tcgen05 operand: the same tf32 features as k_pack_mma,
+// candidate c of tile t, feature f = 8s + 4q + e at float
+// t * 512 KS + s * 512 + ((c & 63) >> 3) * 64 + q * 32 + (c & 7) * 4 + e.
+template <int D>
+__global__ void k_pack_umma(const float* __restrict__ rec32, int64_t rows, float* __restrict__ out) {
+  constexpr int KS = (D + 2 + 7) / 8;
+  constexpr int S32 = rec32_stride(D);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * 8 * KS;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / (8 * KS);
+    const int f = (int)(i - row * 8 * KS);
+    const float* a = rec32 + row * S32;
+    float v = f < D ? a[f] : (f == D ? a[D] : (f == D + 1 ? 1.0f : 0.0f));
+    if (f == D && isinf(v)) v = 1e30f;  // sentinel: never passes
+    uint32_t tb;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(tb) : "f"(v));
+    const int64_t t = row >> 6;
+    const int c = (int)(row & 63), s = f >> 3, q = (f >> 2) & 1, e = f & 3;
+    out[t * 512 * KS + s * 512 + (c >> 3) * 64 + q * 32 + (c & 7) * 4 + e] = __uint_as_float(tb);
+  }
+}
+
 // Descent directions (graph.py:46-85, raycast.py:295-317): per start, the
 // two-pass modified Gram-Schmidt basis of the rows x_sigma[i] - x_sigma[0]
 // (i = 1 .. k-1, the reference's _orthonormal_rows) and the component of the
@@ -425,6 +447,17 @@ extern "C" int vr_vertex_directions(const double* rec, int d, const int32_t* sig
   VR_DISPATCH_D(d, {
     k_vertex_dirs<D><<<blocks_for(n_v, 128), 128, 0, as_stream(stream)>>>(rec, sigma, n_v, out_u,
                                                                             out_ok);
+  });
+  VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_pack_records_umma(const float* rec32, int64_t rows, int d, float* out,
+                                    void* stream) {
+  if (!rec32 || !out || rows <= 0 || (rows & 63)) return VR_EINVAL;
+  const int64_t n2 = rows * 8 * ((d + 2 + 7) / 8);
+  const unsigned nbk = blocks_for(n2, 256) < 4096 ? blocks_for(n2, 256) : 4096;
+  VR_DISPATCH_D(d, {
+    k_pack_umma<D><<<nbk, 256, 0, as_stream(stream)>>>(rec32, rows, out);
   });
   VR_RETURN_LAUNCH();
 }

@@ -31,6 +31,7 @@ int vr_pack_records32(const double* rec, int64_t rows, int d, const double* cent
                       float* rec32, void* stream);
 int vr_pack_records32_pairs(const float* rec32, int64_t rows, int d, float* out, void* stream);
 int vr_pack_records_mma(const float* rec32, int64_t rows, int d, float* out, void* stream);
+int vr_pack_records_umma(const float* rec32, int64_t rows, int d, float* out, void* stream);
 }
 
 namespace {
@@ -535,7 +536,7 @@ struct IndexPlan {
   int depth_max;
   // arena offsets
   size_t a_rec, a_rec32, a_pairs, a_perm, a_inv, a_tbox, a_tbox32, a_nbox, a_nbox32, a_ncb32,
-      a_range, a_wide32, a_recB, a_stats, arena;
+      a_range, a_wide32, a_recB, a_recU, a_stats, arena;
   // workspace offsets
   size_t w_key, w_key2, w_val, w_val2, w_seg, w_seg2, w_id, w_order, w_bbox, w_wide, w_lvl,
       w_tmp, sort_tmp, workspace;
@@ -583,6 +584,8 @@ int index_plan(int64_t n, int d, int flags, IndexPlan& P) {
   P.a_wide32 = a;  a = align256(a + sizeof(float) * P.wide_total * B32);
   P.a_recB = a;
   if (flags & VR_PRUNE_MMA) a = align256(a + sizeof(float) * P.rows * 8 * KS);
+  P.a_recU = a;
+  if (flags & VR_PRUNE_UMMA) a = align256(a + sizeof(float) * P.rows * 8 * KS);
   P.a_stats = a;   a = align256(a + sizeof(double) * 32);
   P.arena = a;
   // build scratch
@@ -671,6 +674,7 @@ extern "C" int vr_build_prune_index(const double* rec, int64_t n, int d, const d
   int32_t* range = reinterpret_cast<int32_t*>(A + P.a_range);
   float* wide32 = reinterpret_cast<float*>(A + P.a_wide32);
   float* recB = (flags & VR_PRUNE_MMA) ? reinterpret_cast<float*>(A + P.a_recB) : nullptr;
+  float* recU = (flags & VR_PRUNE_UMMA) ? reinterpret_cast<float*>(A + P.a_recU) : nullptr;
   double* cdev = reinterpret_cast<double*>(A + P.a_stats);
   double* key = reinterpret_cast<double*>(W + P.w_key);
   double* key2 = reinterpret_cast<double*>(W + P.w_key2);
@@ -727,6 +731,7 @@ extern "C" int vr_build_prune_index(const double* rec, int64_t n, int d, const d
   if ((s = vr_pack_records32(crec, P.rows, d, cdev, rec32, stream))) return s;
   if ((s = vr_pack_records32_pairs(rec32, P.rows, d, pairs, stream))) return s;
   if (recB && (s = vr_pack_records_mma(rec32, P.rows, d, recB, stream))) return s;
+  if (recU && (s = vr_pack_records_umma(rec32, P.rows, d, recU, stream))) return s;
   out->rec = crec;
   out->rec32 = pairs;
   out->perm = perm;
@@ -746,6 +751,7 @@ extern "C" int vr_build_prune_index(const double* rec, int64_t n, int d, const d
   out->recB = recB;
   out->rec32rows = rec32;
   out->node_cb32 = ncb32;
+  out->recU = recU;
   return VR_OK;
 }
 

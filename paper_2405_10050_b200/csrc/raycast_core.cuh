@@ -1430,8 +1430,15 @@ __global__ void __launch_bounds__(32, MINB)
   int64_t st = 0;
   if (lane == 0) st = inv_perm[src.gen(k0)] / PT;
   st = __shfl_sync(0xffffffffu, st, 0);
-  if constexpr (MMA)
-    seed_tile32<D>(ray[0], crec32s + st * PT * rec32_stride(D), crec + st * PT * S, (int)(st * PT), fr);
+  if constexpr (MMA) {
+#ifdef VR_SEED_OWN
+    // each ray seeds on the tile of its own reference generator
+    const int64_t so = act[0] ? (int64_t)ray[0].gk / PT : st;
+#else
+    const int64_t so = st;
+#endif
+    seed_tile32<D>(ray[0], crec32s + so * PT * rec32_stride(D), crec + so * PT * S, (int)(so * PT), fr);
+  }
   else
     seed_tile<D, R, PT, F32>(ray, crec + st * PT * S, (int)(st * PT), fr);
   // (the tensor-core kernel's node_box32 argument holds centre / half-extent rows)
@@ -2051,7 +2058,12 @@ struct PrunedIndex {
   const float* crecB;      // tensor-core screen operand (nullable)
   const float* crec32s;    // kd-ordered fp32 centred rows, vr_pack_records32 layout (with crecB)
   const float* node_cb32;  // node boxes as centre / half-extent rows (with crecB)
+  const float* crecU;      // tcgen05 screen operand, canonical UMMA layout (nullable)
 };
+
+template <int D, class Src>
+int launch_pruned_tc(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
+                     const RayOut& out, cudaStream_t st, unsigned long long* work);
 
 #ifdef VR_PRUNE_TILE_OVERRIDE  // tuning builds only (the Python index must match: VR_PRUNE_TILE)
 constexpr int PRUNE_TILE = VR_PRUNE_TILE_OVERRIDE;
@@ -2126,6 +2138,9 @@ int launch_pruned_f(const Src& src, int64_t n_rays, const PrunedIndex& ix, const
 #define VR_MMA_MIN_D 5
 #endif
   if constexpr (F32 && PRUNE_TILE == 64 && D >= VR_MMA_MIN_D) {
+    // 5th-generation tensor cores (tcgen05 + TMEM, 128-ray CTAs): VR_MMA=2
+    if (ix.crecU && ix.crec32s && ix.node_cb32 && mma_mode() == 2)
+      return launch_pruned_tc<D>(src, n_rays, ix, fr, out, st, work);
     if (ix.crecB && ix.crec32s && ix.node_cb32 && mma_mode() != 0)
       return launch_pruned_rm<D, 1, MMA_MINB, F32, Src, true>(src, n_rays, ix, fr, out, st, work);
   }
@@ -2156,6 +2171,7 @@ inline PrunedIndex pruned_index_from(const vr_prune_index* ix, bool f32) {
   pi.crecB = f32 ? ix->recB : nullptr;
   pi.crec32s = f32 ? ix->rec32rows : nullptr;
   pi.node_cb32 = f32 ? ix->node_cb32 : nullptr;
+  pi.crecU = f32 ? ix->recU : nullptr;
   pi.wide.box32 = ix->wide_box32;
   pi.wide.levels = ix->wide_levels;
   for (int l = 0; l < WIDE_MAX_LEVELS; ++l) {
@@ -2205,3 +2221,5 @@ int launch_recheck(const Src& src, int64_t max_list, const double* crec, const i
 }
 
 }  // namespace vr
+
+#include "raycast_tc.cuh"
