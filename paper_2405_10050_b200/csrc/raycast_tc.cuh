@@ -237,11 +237,7 @@ __global__ void __launch_bounds__(TC_RAYS, MINB)
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
   const int64_t st = start_tile_s;
-#ifdef VR_SEED_OWN
   const int64_t so = act ? (int64_t)ray.gk / TC_TILE : st;  // the ray's own start tile
-#else
-  const int64_t so = st;
-#endif
   seed_tile32<D>(ray, crec32s + so * TC_TILE * rec32_stride(D), crec + so * TC_TILE * S,
                  (int)(so * TC_TILE), fr);
   tc_store_a<D>(ray, sA, tid);
