@@ -31,7 +31,11 @@ TOL_DEGENERATE = 1e-10
 HALFSPACE_SLACK = 1e-12
 _SCAN_MAX = 2048
 
-MIN_DIM, MAX_DIM = 2, 8
+# d = 2 .. 16: the exhaustive fp64 RayCast, MC and traversal kernels; the
+# fp32 / tensor-core screens and the kd-pruned kernels cover d <= 8 (the
+# configs' range), so larger d takes the exhaustive fp64 path automatically.
+MIN_DIM, MAX_DIM = 2, 16
+FAST_MAX_DIM = 8
 
 
 def _device(device=None):
@@ -103,8 +107,16 @@ class NodeSet:
         self._dev[dev.index] = entry
         return entry
 
+    @property
+    def fast_paths(self):
+        """The fp32 screens and the kd-pruned kernels exist for d <= 8."""
+        return self.dim <= FAST_MAX_DIM
+
     def screen32(self, device=None):
-        """Centred fp32 copy of the records for the fp32 screen (built once)."""
+        """Centred fp32 copy of the records for the fp32 screen (built once);
+        None for d > 8 (fp64 screen only)."""
+        if not self.fast_paths:
+            return None
         dev = _device(device)
         hit = self._s32.get(dev.index)
         if hit is None:
@@ -117,6 +129,9 @@ class NodeSet:
         """kd-ordered records + tile / block bounding boxes for the pruned
         RayCast (include/voronray_b200.h vr_prune_index); built once per
         device on the GPU."""
+        if not self.fast_paths:
+            raise ValueError(f"the kd-pruned kernels cover d <= {FAST_MAX_DIM}; d={self.dim} "
+                             "uses the exhaustive fp64 scan")
         dev = _device(device)
         hit = self._prune.get(dev.index)
         if hit is None:

@@ -10,7 +10,8 @@
 #include "../../include/voronray_b200.h"
 
 #define VR_MIN_D 2
-#define VR_MAX_D 8
+#define VR_MAX_D 8       // the fp32 / tensor-core / pruned fast paths
+#define VR_MAX_D_ALL 16  // exhaustive fp64 RayCast, MC, traversal, mesh ops
 
 // Reference tolerances (pkg/src/voronray/core.py:24-29).
 #define VR_TOL_VERTEX 1e-8
@@ -57,6 +58,27 @@ static inline int vr_cuda_status(cudaError_t e) {
     case 7: { constexpr int D = 7; __VA_ARGS__; } break;    \
     case 8: { constexpr int D = 8; __VA_ARGS__; } break;    \
     default: return VR_EDIM;                                \
+  }
+
+// d = 9 .. 16 (the exhaustive fp64 paths only), and d = 2 .. 16.
+#define VR_DISPATCH_D_HIGH(d, ...)                           \
+  switch (d) {                                               \
+    case 9: { constexpr int D = 9; __VA_ARGS__; } break;     \
+    case 10: { constexpr int D = 10; __VA_ARGS__; } break;   \
+    case 11: { constexpr int D = 11; __VA_ARGS__; } break;   \
+    case 12: { constexpr int D = 12; __VA_ARGS__; } break;   \
+    case 13: { constexpr int D = 13; __VA_ARGS__; } break;   \
+    case 14: { constexpr int D = 14; __VA_ARGS__; } break;   \
+    case 15: { constexpr int D = 15; __VA_ARGS__; } break;   \
+    case 16: { constexpr int D = 16; __VA_ARGS__; } break;   \
+    default: return VR_EDIM;                                 \
+  }
+
+#define VR_DISPATCH_D_ALL(d, ...)                            \
+  if ((d) > VR_MAX_D) {                                      \
+    VR_DISPATCH_D_HIGH(d, __VA_ARGS__)                       \
+  } else {                                                   \
+    VR_DISPATCH_D(d, __VA_ARGS__)                            \
   }
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }

@@ -355,7 +355,7 @@ extern "C" int vr_pack_generators(const double* pts, int64_t n, int d, double* r
     if (e != cudaSuccess) return vr_cuda_status(e);
   }
   const unsigned nb = blocks_for(n, 256) < 4096 ? blocks_for(n, 256) : 4096;
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_pack<D><<<nb, 256, 0, st>>>(pts, n, rec, reinterpret_cast<unsigned long long*>(sqmax_out));
   });
   VR_RETURN_LAUNCH();
@@ -397,7 +397,7 @@ extern "C" int vr_nearest_batch(const double* rec, int64_t n_gen, int d, const d
                                 double* out_d1, double* out_d2, void* stream) {
   if (!rec || !q || !out_idx || n_gen <= 0) return VR_EINVAL;
   if (n_q <= 0) return VR_OK;
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_nearest<D><<<blocks_for(n_q, 128), 128, 0, as_stream(stream)>>>(rec, n_gen, q, n_q, skip,
                                                                         out_idx, out_d1, out_d2);
   });
@@ -409,7 +409,7 @@ extern "C" int vr_verify_vertices(const double* rec, int64_t n_gen, int d, const
                                   void* stream) {
   if (!rec || !sigma || !r || !out_ok) return VR_EINVAL;
   if (n_v <= 0) return VR_OK;
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_verify<D><<<blocks_for(n_v, 128), 128, 0, as_stream(stream)>>>(rec, n_gen, sigma, r, n_v,
                                                                        tol, out_ok);
   });
@@ -420,7 +420,7 @@ extern "C" int vr_circumcenters(const double* rec, int d, const int32_t* sigma, 
                                 double* out_r, uint8_t* out_ok, void* stream) {
   if (!rec || !sigma || !out_r) return VR_EINVAL;
   if (n_v <= 0) return VR_OK;
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_circumcenters<D><<<blocks_for(n_v, 128), 128, 0, as_stream(stream)>>>(rec, sigma, n_v,
                                                                               out_r, out_ok);
   });
@@ -433,7 +433,7 @@ extern "C" int vr_descent_directions(const double* rec, int d, const int32_t* si
                                      void* stream) {
   if (!rec || !sigma || !k || !z || !out_v || !out_nrm || !out_bad) return VR_EINVAL;
   if (n <= 0) return VR_OK;
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_descent_dirs<D><<<blocks_for(n, 128), 128, 0, as_stream(stream)>>>(
         rec, sigma, k, z, n, tol, out_v, out_nrm, out_bad);
   });
@@ -444,7 +444,7 @@ extern "C" int vr_vertex_directions(const double* rec, int d, const int32_t* sig
                                     double* out_u, uint8_t* out_ok, void* stream) {
   if (!rec || !sigma || !out_u) return VR_EINVAL;
   if (n_v <= 0) return VR_OK;
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_vertex_dirs<D><<<blocks_for(n_v, 128), 128, 0, as_stream(stream)>>>(rec, sigma, n_v, out_u,
                                                                             out_ok);
   });

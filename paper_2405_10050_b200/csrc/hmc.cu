@@ -111,7 +111,7 @@ __device__ __forceinline__ double integrand(int kind, const double* coef, const 
 }
 
 struct Coef {
-  double c[VR_MAX_D + 1];
+  double c[VR_MAX_D_ALL + 1];
 };
 
 // Per queried interface (cell i, neighbour j, area A):
@@ -281,7 +281,7 @@ extern "C" int vr_hmc_face_index(const int32_t* sigma, int64_t n_v, int d, int64
                                  int32_t* nb_count, void* workspace, int64_t* workspace_bytes,
                                  void* stream) {
   if (!workspace_bytes || n_v < 0 || n_e < 0 || n_gen < 1) return VR_EINVAL;
-  if (d < VR_MIN_D || d > VR_MAX_D) return VR_EDIM;
+  if (d < VR_MIN_D || d > VR_MAX_D_ALL) return VR_EDIM;
   IndexPlan P;
   int s = index_plan(n_v, d, n_e, n_gen, P);
   if (s) return s;
@@ -308,7 +308,7 @@ extern "C" int vr_hmc_face_index(const int32_t* sigma, int64_t n_v, int d, int64
       (e = cudaMemsetAsync(nb_count, 0, 4 * n_gen, st)) != cudaSuccess ||
       (e = cudaMemsetAsync(cnt, 0, 8, st)) != cudaSuccess)
     return vr_cuda_status(e);
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     if (nk > 0) k_vertex_pairs<D><<<grid_for(n_v), 256, 0, st>>>(sigma, n_v, kin, vin);
     if (n_e > 0)
       k_boundary_pairs<D><<<grid_for(n_e), 256, 0, st>>>(edge_key, edge_count, n_e,
@@ -348,7 +348,7 @@ extern "C" int vr_hmc_faces(const uint64_t* keys, const int32_t* vid, int64_t n_
   Coef c{};
   const int ncoef = integrand_kind == 1 ? 1 : (integrand_kind == 3 ? d + 1 : 0);
   for (int k = 0; k < ncoef; ++k) c.c[k] = coef[k];
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_hmc_faces<D><<<grid_for(n_f, 128), 128, 0, as_stream(stream)>>>(
         keys, vid, n_keys, ukeys, n_ukeys, r, face_i, face_j, area, n_f, integrand_kind, c,
         out_F, out_status, out_first, out_count, out_mean, out_centroid);
@@ -370,7 +370,7 @@ extern "C" int vr_hmc_cells(const double* rec, int d, const int32_t* cells, int6
   Coef c{};
   const int ncoef = integrand_kind == 1 ? 1 : (integrand_kind == 3 ? d + 1 : 0);
   for (int k = 0; k < ncoef; ++k) c.c[k] = coef[k];
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_hmc_cells<D><<<grid_for(n_c, 128), 128, 0, as_stream(stream)>>>(
         rec, cells, n_c, face_off, face_j, area, F, face_status, cell_unbounded, nb_count,
         integrand_kind, c, volume_in, out_volume, out_integral, out_status);

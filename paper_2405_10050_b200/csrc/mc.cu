@@ -27,7 +27,7 @@ inline int map_capacity(int max_faces) {
 struct Integ {
   int kind;      // 0: areas/volume only
   int m;         // subsamples per ray
-  double coef[VR_MAX_D + 1];
+  double coef[VR_MAX_D_ALL + 1];
   const double* unif;  // nullable: replayed uniforms (n_rays, m); else Philox
 };
 
@@ -286,6 +286,14 @@ extern "C" int vr_mc_rays(const double* rec, int64_t n_gen, int d, double sqmax,
   if (!crec || nc <= 0) return VR_EINVAL;
   const int64_t n = n_cells * rays_per_cell;
   RayOut out{out_idx, out_t, nullptr, out_flag, recheck_list, recheck_count};
+  if (d > VR_MAX_D) {
+    if (s32) return VR_EDIM;  // fp32 screen: d <= 8
+    VR_DISPATCH_D_HIGH(d, {
+      SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n};
+      return launch_raycast_fp64<D>(src, n, crec, cand, nc, make_screen(sqmax, nullptr, d), out,
+                                    as_stream(stream));
+    });
+  }
   VR_DISPATCH_D(d, {
     SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n};
     return launch_raycast<D>(src, n, crec, cand, nc, make_screen(sqmax, s32, d), out,
@@ -304,7 +312,7 @@ extern "C" int vr_mc_recheck(const double* rec, int64_t n_gen, int d, const doub
   const double* crec = cand ? cand_rec : rec;
   const int64_t nc = cand ? n_cand : n_gen;
   RayOut out{out_idx, out_t, nullptr, out_flag, nullptr, nullptr};
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, INT64_MAX};
     return launch_recheck<D>(src, max_list, crec, cand, nc, recheck_list, recheck_count, out,
                              as_stream(stream));
@@ -372,7 +380,7 @@ extern "C" int vr_mc_reduce(const double* rec, int d, const int32_t* cells, int6
   if (max_faces <= 0 || max_faces > (1 << 28)) return VR_EINVAL;
   const int64_t nb = cell_sel ? n_sel : n_cells;
   if (nb <= 0) return VR_OK;
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n_cells * rays_per_cell};
     Integ fi{};
     return launch_reduce<D, false>(src, nb, ray_idx, ray_t, ray_flag, max_faces,
@@ -407,7 +415,7 @@ extern "C" int vr_mc_integrate(const double* rec, int d, const int32_t* cells, i
   fi.unif = unif;
   const int ncoef = integrand_kind == 1 ? 1 : (integrand_kind == 3 ? d + 1 : 0);
   for (int k = 0; k < ncoef; ++k) fi.coef[k] = coef[k];
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     SrcMC<D> src{rec, cells, rays_per_cell, dirs, seed, n_cells * rays_per_cell};
     return launch_reduce<D, true>(src, nb, ray_idx, ray_t, ray_flag, max_faces, 1, surf, fi,
                                   out_volume, out_face_j, out_face_area, out_nfaces, out_status,
@@ -426,7 +434,7 @@ extern "C" int vr_mc_directions(int d, int64_t n_cells, const int32_t* cells,
   if (!cells || !out_z || rays_per_cell <= 0) return VR_EINVAL;
   const int64_t n = n_cells * rays_per_cell;
   if (n <= 0) return VR_OK;
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     SrcMC<D> src{nullptr, cells, rays_per_cell, nullptr, seed, n};
     k_mc_dirs<D><<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(src, out_z);
   });

@@ -184,7 +184,7 @@ extern "C" int vr_edge_incidence(const int32_t* sigma, int64_t n_v, int d, int32
                                  int32_t* out_counts, int64_t* n_unique_out, void* workspace,
                                  int64_t* workspace_bytes, void* stream) {
   if (!workspace_bytes || n_v < 0) return VR_EINVAL;
-  if (d < VR_MIN_D || d > VR_MAX_D) return VR_EDIM;
+  if (d < VR_MIN_D || d > VR_MAX_D_ALL) return VR_EDIM;
   const int64_t n = n_v * (d + 1);
   if (n >= ((int64_t)1 << 31)) return VR_EINVAL;
   size_t scan_tmp = 0;
@@ -209,9 +209,9 @@ extern "C" int vr_edge_incidence(const int32_t* sigma, int64_t n_v, int d, int32
   int32_t* head = reinterpret_cast<int32_t*>(W + o_head);
   int32_t* pos = reinterpret_cast<int32_t*>(W + o_pos);
   cudaError_t e;
-  VR_DISPATCH_D(d, { k_incidences<D><<<grid_for(n_v), 256, 0, st>>>(sigma, n_v, rows); });
+  VR_DISPATCH_D_ALL(d, { k_incidences<D><<<grid_for(n_v), 256, 0, st>>>(sigma, n_v, rows); });
   if ((e = lex_sort(rows, n, d, idx, W + o_lex, st)) != cudaSuccess) return vr_cuda_status(e);
-  VR_DISPATCH_D(d, { k_heads<D><<<grid_for(n), 256, 0, st>>>(rows, idx, n, head); });
+  VR_DISPATCH_D_ALL(d, { k_heads<D><<<grid_for(n), 256, 0, st>>>(rows, idx, n, head); });
   size_t t = scan_tmp;
   if ((e = cub::DeviceScan::InclusiveSum(W + o_scan, t, head, pos, (int)n, st)) != cudaSuccess)
     return vr_cuda_status(e);
@@ -221,7 +221,7 @@ extern "C" int vr_edge_incidence(const int32_t* sigma, int64_t n_v, int d, int32
     return vr_cuda_status(e);
   if ((e = cudaMemsetAsync(out_counts, 0, 4 * (size_t)nu, st)) != cudaSuccess)
     return vr_cuda_status(e);
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_runs<D><<<grid_for(n), 256, 0, st>>>(rows, idx, head, pos, n, out_keys, out_counts);
   });
   *n_unique_out = nu;
@@ -233,7 +233,7 @@ extern "C" int vr_edge_check(const int32_t* inc_keys, const int32_t* inc_counts,
                              void* stream) {
   if (n_e <= 0) return VR_OK;
   if (!edge_keys || !incident || (n_inc > 0 && (!inc_keys || !inc_counts))) return VR_EINVAL;
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_edge_check<D><<<grid_for(n_e), 256, 0, as_stream(stream)>>>(inc_keys, inc_counts, n_inc,
                                                                     edge_keys, n_e, incident);
   });
@@ -244,7 +244,7 @@ extern "C" int vr_vertex_edges(const int32_t* sigma, int64_t n_v, int d, int32_t
                                void* stream) {
   if (n_v <= 0) return VR_OK;
   if (!sigma || !out) return VR_EINVAL;
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_incidences<D><<<grid_for(n_v), 256, 0, as_stream(stream)>>>(sigma, n_v, out);
   });
   VR_RETURN_LAUNCH();

@@ -39,7 +39,7 @@ extern "C" const char* vr_status_string(int status) {
   switch (status) {
     case VR_OK: return "ok";
     case VR_EINVAL: return "invalid argument";
-    case VR_EDIM: return "dimension outside [2, 8]";
+    case VR_EDIM: return "dimension outside the supported range ([2, 16]; fp32 / pruned paths [2, 8])";
     case VR_ECAPACITY: return "workspace or table capacity exceeded";
     default: break;
   }
@@ -53,7 +53,7 @@ Screen vr::make_screen(double sqmax, const vr_screen32* s32, int d) {
   if (s32) {
     sc.rec32 = s32->rec;
     sc.rec32p = s32->rec_pairs;
-    for (int k = 0; k < VR_MAX_D; ++k) sc.fr.c0[k] = k < d ? s32->center[k] : 0.0;
+    for (int k = 0; k < VR_MAX_D_ALL; ++k) sc.fr.c0[k] = k < d && k < 8 ? s32->center[k] : 0.0;
     sc.fr.sqmax32 = s32->sqmax;
     sc.fr.bnd32 = s32->bound;
   }
@@ -66,7 +66,7 @@ extern "C" int vr_record32_stride(int d) {
 }
 
 extern "C" int vr_record_stride(int d) {
-  if (d < VR_MIN_D || d > VR_MAX_D) return VR_EDIM;
+  if (d < VR_MIN_D || d > VR_MAX_D_ALL) return VR_EDIM;
   return rec_stride(d);
 }
 
@@ -83,6 +83,14 @@ extern "C" int vr_raycast_batch(const double* rec, int64_t n_gen, int d, double 
   const int64_t nc = cand ? n_cand : n_gen;
   if (!crec || nc <= 0) return VR_EINVAL;
   RayOut out{out_idx, out_t, out_rp, out_flag, recheck_list, recheck_count};
+  if (d > VR_MAX_D) {
+    if (s32) return VR_EDIM;  // fp32 screen: d <= 8
+    VR_DISPATCH_D_HIGH(d, {
+      SrcExplicit<D> src{x, u, eta, eta_len, rec, n_rays};
+      return launch_raycast_fp64<D>(src, n_rays, crec, cand, nc, make_screen(sqmax, nullptr, d),
+                                    out, as_stream(stream));
+    });
+  }
   VR_DISPATCH_D(d, {
     SrcExplicit<D> src{x, u, eta, eta_len, rec, n_rays};
     return launch_raycast<D>(src, n_rays, crec, cand, nc, make_screen(sqmax, s32, d), out,
@@ -101,7 +109,7 @@ extern "C" int vr_raycast_recheck(const double* rec, int64_t n_gen, int d, const
   const double* crec = cand ? cand_rec : rec;
   const int64_t nc = cand ? n_cand : n_gen;
   RayOut out{out_idx, out_t, out_rp, out_flag, nullptr, nullptr};
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     SrcExplicit<D> src{x, u, eta, eta_len, rec, INT64_MAX};
     return launch_recheck<D>(src, max_list, crec, cand, nc, recheck_list, recheck_count, out,
                              as_stream(stream));

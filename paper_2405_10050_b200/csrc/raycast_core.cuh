@@ -31,7 +31,7 @@ namespace vr {
 // centred fp32 copy's centre / max |x - c|^2 for the fp32 screen's bound.
 struct Frame {
   double sqmax;
-  double c0[VR_MAX_D];
+  double c0[VR_MAX_D_ALL];
   double sqmax32;
   double bnd32;  // max |x_k - c0_k| over generators (fp32 box-test slack)
 };
@@ -2017,6 +2017,21 @@ int launch_raycast_cfg(const Src& src, int64_t n_rays, const double* crec, const
 }
 
 Screen make_screen(double sqmax, const vr_screen32* s32, int d);
+
+// d = 9 .. 16: the exhaustive fp64 screen only (one ray per thread; the
+// fp32 / tensor-core / pruned paths are specialised for d <= 8).
+template <int D, class Src>
+int launch_raycast_fp64(const Src& src, int64_t n_rays, const double* crec, const int32_t* cand,
+                        int64_t n_cand, const Screen& sc, const RayOut& out, cudaStream_t st) {
+  if (n_rays <= 0) return VR_OK;
+  if (n_cand <= 0) return VR_EINVAL;
+  if (out.recheck_count) {
+    cudaError_t e = cudaMemsetAsync(out.recheck_count, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return vr_cuda_status(e);
+  }
+  return launch_raycast_cfg<RaycastCfgT<D, 1, 1>, D, false>(src, n_rays, crec, cand, n_cand, sc,
+                                                             out, st);
+}
 
 // Tuning hook: VR_RAYCAST_VARIANT selects alternative register blockings
 // for d = 6 (the config-2 shape); 0 = default.

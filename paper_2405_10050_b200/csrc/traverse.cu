@@ -436,7 +436,7 @@ extern "C" int vr_trav_insert_vertices(const vr_traverse_tables* tab, int d, con
   if (!tab || !sigma || !pow2(tab->vcap) || !pow2(tab->ecap)) return VR_EINVAL;
   if (n_v <= 0) return VR_OK;
   const Tables t = from(tab);
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_insert_vertices<D><<<nb(n_v), 256, 0, as_stream(stream)>>>(t, sigma, n_v, base_id, level,
                                                                   bump_edges_flag);
   });
@@ -448,7 +448,7 @@ extern "C" int vr_trav_rehash_edges(const vr_traverse_tables* tab, int d, const 
                                     void* stream) {
   if (!tab || !okeys || !ostate || !ocount || !pow2(tab->ecap)) return VR_EINVAL;
   const Tables t = from(tab);
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_rehash_edges<D><<<nb(ocap), 256, 0, as_stream(stream)>>>(t, okeys, ostate, ocount, ocap);
   });
   VR_RETURN_LAUNCH();
@@ -460,7 +460,7 @@ extern "C" int vr_trav_open_edges(const vr_traverse_tables* tab, int d, const in
   if (!tab || !sigma || !open_mask || !open_count) return VR_EINVAL;
   if (n_v <= 0) return VR_OK;
   const Tables t = from(tab);
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_open_edges<D><<<nb(n_v, 128), 128, 0, as_stream(stream)>>>(t, sigma, n_v, open_mask,
                                                                   open_count);
   });
@@ -475,7 +475,7 @@ extern "C" int vr_trav_emit_rays(const double* rec, int d, const int32_t* sigma,
       !ray_parent || !bad)
     return VR_EINVAL;
   if (n_v <= 0) return VR_OK;
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_emit_rays<D><<<nb(n_v, 128), 128, 0, as_stream(stream)>>>(
         rec, sigma, r, n_v, open_mask, open_off, ray_x, ray_u, ray_eta, ray_parent, bad);
   });
@@ -491,7 +491,7 @@ extern "C" int vr_trav_claim(const vr_traverse_tables* tab, int d, const int32_t
     return VR_EINVAL;
   if (n_rays <= 0) return VR_OK;
   const Tables t = from(tab);
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_claim<D><<<nb(n_rays), 256, 0, as_stream(stream)>>>(t, ray_eta, hit_idx, hit_flag, n_rays,
                                                           level, out_sigma, out_slot);
     k_winners<D><<<nb(n_rays), 256, 0, as_stream(stream)>>>(t, out_slot, hit_flag, n_rays, level,
@@ -509,7 +509,7 @@ extern "C" int vr_trav_finalize(const vr_traverse_tables* tab, const double* rec
     return VR_EINVAL;
   if (n_rays <= 0) return VR_OK;
   const Tables t = from(tab);
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_finalize<D><<<nb(n_rays, 128), 128, 0, as_stream(stream)>>>(
         t, rec, ray_sigma, slot, new_flag, new_off, n_rays, base_id, vsig, vr, bad);
     if (bump)
@@ -525,7 +525,7 @@ extern "C" int vr_trav_boundary(int d, const int32_t* esc_flag, const int64_t* e
   if (!esc_flag || !esc_off || !ray_parent || !ray_u || !frontier_sigma || !bsig || !bu)
     return VR_EINVAL;
   if (n_rays <= 0) return VR_OK;
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_boundary<D><<<nb(n_rays), 256, 0, as_stream(stream)>>>(esc_flag, esc_off, ray_parent, ray_u,
                                                              n_rays, frontier_sigma, base_b, bsig,
                                                              bu);
@@ -544,7 +544,7 @@ extern "C" int vr_trav_edge_compact(const vr_traverse_tables* tab, int d, const 
                                     int32_t* out_keys, int32_t* out_count, void* stream) {
   if (!tab || !off || !out_keys || !out_count) return VR_EINVAL;
   const Tables t = from(tab);
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_edge_compact<D><<<nb(t.ecap), 256, 0, as_stream(stream)>>>(t, off, out_keys, out_count);
   });
   VR_RETURN_LAUNCH();
@@ -556,7 +556,7 @@ extern "C" int vr_trav_claim_sigma(const vr_traverse_tables* tab, int d, const i
   if (n <= 0) return VR_OK;
   if (!tab || !rows || !out_slot || !new_flag) return VR_EINVAL;
   const Tables t = from(tab);
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_claim_sigma<D><<<nb(n), 256, 0, as_stream(stream)>>>(t, rows, n, level, out_slot);
   });
   k_winners_sigma<<<nb(n), 256, 0, as_stream(stream)>>>(t, out_slot, n, level, new_flag);
@@ -568,7 +568,7 @@ extern "C" int vr_trav_bump_keys(const vr_traverse_tables* tab, int d, const int
   if (n <= 0) return VR_OK;
   if (!tab || !keys) return VR_EINVAL;
   const Tables t = from(tab);
-  VR_DISPATCH_D(d, {
+  VR_DISPATCH_D_ALL(d, {
     k_bump_keys<D><<<nb(n), 256, 0, as_stream(stream)>>>(t, keys, n);
     if (counts_out)
       k_edge_counts<D><<<nb(n), 256, 0, as_stream(stream)>>>(t, keys, n, counts_out);

@@ -465,7 +465,7 @@ class DeviceTraversal:
         self.e_ub = 0
         self.work = None  # optional VR_WORK_COUNTERS tensor (pruned-kernel accounting)
         # native level driver (csrc/level.cu) unless VR_NATIVE_LEVEL=0
-        self.native = os.environ.get("VR_NATIVE_LEVEL", "1") != "0"
+        self.native = os.environ.get("VR_NATIVE_LEVEL", "1") != "0" and ns.fast_paths
 
     def _alloc_vtable(self, cap):
         d = self.d
@@ -795,7 +795,7 @@ def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heurist
     vpg = {2: 2, 3: 7, 4: 32, 5: 190, 6: 1300, 7: 9000, 8: 66000}.get(ns.dim, 4)
     v_est = _table_estimate(ns, ns.n * vpg)
     size = _group_size(group)
-    if size > 1 and _sharding() == "owner":
+    if size > 1 and _sharding() == "owner" and ns.fast_paths:
         from .parallel import DeviceShardOps, ShardedTraversal
         share = v_est // size + 1024
         st = ShardedTraversal(ns, DeviceShardOps(ns, vcap_hint=max(4096, 2 * share),
@@ -866,7 +866,7 @@ def voronoi_local(ns: NodeSet, starts, hops: int, seed: int = 0, stats: RaycastS
         sig, _ = descent_batch(ns, starts, seed=seed, stats=stats)
     _, first = np.unique(sig, axis=0, return_index=True)
     sig = sig[np.sort(first)]
-    if size > 1 and _sharding() == "owner":
+    if size > 1 and _sharding() == "owner" and ns.fast_paths:
         from .parallel import DeviceShardOps, ShardedTraversal
         share = 6 * len(sig) * 4 ** min(hops, 8) // size + 1024
         st = ShardedTraversal(ns, DeviceShardOps(ns, vcap_hint=max(4096, share)), group)

@@ -129,7 +129,7 @@ def candidate_records(ns: NodeSet, candidates, dev, screen="fp64"):
     crec[:, ns.dim] = float("inf")  # sentinel rows (include/voronray_b200.h)
     crec[:m] = rec.index_select(0, cand)
     s32 = None
-    if screen == "fp32":
+    if screen == "fp32" and ns.fast_paths:
         from .core import Screen32
         s32 = Screen32(crec, m, ns.dim, center=ns.screen32(dev).center)
     return cand.to(torch.int32).contiguous(), crec, s32
@@ -213,7 +213,7 @@ def coherent_order(ix, eta, u, workspace=None, stream=None):
 def _screen(ns, dev, screen):
     if screen not in ("fp32", "fp64"):
         raise ValueError(f"unknown screen {screen!r}")
-    return ns.screen32(dev) if screen == "fp32" else None
+    return ns.screen32(dev) if screen == "fp32" else None  # None for d > 8: fp64
 
 
 PRUNE_MIN_GENERATORS = 256  # below: one exhaustive scan is as fast (config 1 uses pruned: 19 -> 17 ms)
@@ -222,7 +222,7 @@ PRUNE_MIN_GENERATORS = 256  # below: one exhaustive scan is as fast (config 1 us
 def _use_pruned(ns, candidates, mode):
     if mode not in ("auto", "pruned", "exhaustive"):
         raise ValueError(f"unknown mode {mode!r}")
-    if candidates is not None or mode == "exhaustive":
+    if candidates is not None or mode == "exhaustive" or not ns.fast_paths:
         return False
     return mode == "pruned" or ns.n >= PRUNE_MIN_GENERATORS
 
@@ -481,8 +481,9 @@ class HostRaycaster:
         self.ws = [Workspace() for _ in range(self.NBUF)]
         nbytes = ctypes.c_int64(0)
         L = _lib.lib()
-        _lib.check(L.vr_ray_order(None, None, d, 1, None, c, d, ns.n, None, None,
-                                  ctypes.byref(nbytes), None), "vr_ray_order (size)")
+        if ns.fast_paths:
+            _lib.check(L.vr_ray_order(None, None, d, 1, None, c, d, ns.n, None, None,
+                                      ctypes.byref(nbytes), None), "vr_ray_order (size)")
         for w in self.ws:
             w.get("recheck_list", (c,), torch.int32, self.dev)
             w.get("recheck_count", (1,), torch.int32, self.dev)
@@ -563,7 +564,7 @@ class HostRaycaster:
             e = torch.cuda.Event(enable_timing=True)
             e.record(stream)
             return e
-        if self.ns.n >= PRUNE_MIN_GENERATORS and mode != "exhaustive":
+        if self.ns.n >= PRUNE_MIN_GENERATORS and mode != "exhaustive" and self.ns.fast_paths:
             self.ns.prune_index(self.dev)
         if screen == "fp32":
             self.ns.screen32(self.dev)

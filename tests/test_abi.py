@@ -46,10 +46,11 @@ def test_loads_and_reports(built_library):
     L = _lib.load_library()
     assert L.vr_abi_version() == _lib.ABI_VERSION == 5
     assert [L.vr_record_stride(d) for d in range(2, 9)] == [4, 4, 6, 6, 8, 8, 10]
-    assert L.vr_record_stride(9) < 0
+    assert L.vr_record_stride(9) == 10 and L.vr_record_stride(16) == 18
+    assert L.vr_record_stride(17) < 0
     assert L.vr_record_rows(1) == 512 and L.vr_record_rows(512) == 512
     assert L.vr_record_rows(513) == 1024
-    assert L.vr_status_string(-2) == b"dimension outside [2, 8]"
+    assert L.vr_status_string(-2).startswith(b"dimension outside the supported range")
     for name in _lib.EXPORTED:
         getattr(L, name)
     assert set(_lib.EXPORTED) <= declared_symbols()

@@ -26,7 +26,7 @@ def test_build_validation():
     with pytest.raises(DimensionMismatch):
         vb.build_node_set([(0.0,), (1.0,), (2.0,)])
     with pytest.raises(DimensionMismatch):
-        vb.build_node_set(np.random.default_rng(0).random((20, 9)))
+        vb.build_node_set(np.random.default_rng(0).random((40, 17)))  # kernels cover d <= 16
     with pytest.raises(ValueError):
         vb.NodeSet(np.random.default_rng(0).random((5, 2)), backend="octree")
     with pytest.raises(ValueError):
