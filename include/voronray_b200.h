@@ -470,6 +470,50 @@ int vr_trav_level_cast(const vr_traverse_tables* tab, const double* rec, int64_t
  * workspace returns VR_ECAPACITY. */
 int vr_trav_level_workspace(int64_t n_v, int64_t n_rays, int64_t n_gen, int d, int64_t* bytes);
 
+/* Native multi-level driver: the whole level loop in C++ (open -> capacity
+ * checks -> cast -> finalize + boundary per level, the two synchronisations
+ * of the level calls and no other host work).  Runs levels state->level ..
+ * last_level (-1: until no vertex is new) over the frontier [f0, f1) of
+ * vertex ids; level_new[l] receives the new-vertex count of level l.  It
+ * returns VR_OK with state->need = VR_RUN_DONE, or with a capacity the
+ * caller must grow (workspace bytes, vertex arrays / table, edge table,
+ * boundary arrays: need_amount) before calling again -- state->phase
+ * remembers a level whose cast is done -- or VR_RUN_ERROR with the
+ * degenerate / affinely dependent / overflow counts set.  Workspace size for
+ * F frontier vertices and R rays: vr_trav_run_workspace. */
+enum vr_run_need {
+  VR_RUN_DONE = 0,
+  VR_RUN_NEED_WORKSPACE = 1,
+  VR_RUN_NEED_VERTICES = 2,
+  VR_RUN_NEED_EDGES = 3,
+  VR_RUN_NEED_BOUNDARY = 4,
+  VR_RUN_ERROR = 5
+};
+typedef struct vr_trav_state {
+  int32_t* vsig;         /* vertex arrays: sigma (vcap_arrays, d+1), r (vcap_arrays, d) */
+  double* vr;
+  int64_t vcap_arrays;
+  int32_t* bsig;         /* boundary rays: sigma (bcap, d+1), u (bcap, d) */
+  double* bu;
+  int64_t bcap;
+  int64_t nv, nb, e_ub;  /* vertices, boundary rays, edge incidences so far */
+  int64_t f0, f1;        /* frontier: vertex ids [f0, f1) */
+  int32_t level;         /* level to run next */
+  int32_t phase;         /* 0: level not started, 1: cast done, finalize pending */
+  int64_t pending_rays;
+  int64_t n_new, n_esc, n_degenerate, n_bad, overflow;  /* last cast */
+  int64_t rays;          /* edge raycasts so far */
+  int32_t need;          /* vr_run_need */
+  int64_t need_amount;
+} vr_trav_state;
+int vr_trav_run_workspace(int64_t n_frontier, int64_t n_rays, int64_t n_gen, int d,
+                          int64_t* bytes);
+int vr_trav_run(const vr_traverse_tables* tab, vr_trav_state* state, const double* rec,
+                int64_t n_gen, int d, double sqmax, const vr_screen32* s32,
+                const vr_prune_index* ix, int32_t last_level, int64_t* level_new,
+                int64_t level_cap, uint64_t* work, void* workspace, int64_t workspace_bytes,
+                void* stream);
+
 /* Register vertices (sigma (n_v, d+1) sorted) with ids base_id.. at `level`;
  * optionally bump the counters of their d+1 edges (graph.py:115-120). */
 int vr_trav_insert_vertices(const vr_traverse_tables* tab, int d,

@@ -66,6 +66,9 @@ _SIGNATURES = {
     "vr_prune_index_layout": [_i64, _int, _int, _vp],
     "vr_build_prune_index": [_vp, _i64, _int, _vp, _int, _vp, _i64, _vp, _i64, _vp, _vp],
     "vr_trav_level_workspace": [_i64, _i64, _i64, _int, _vp],
+    "vr_trav_run_workspace": [_i64, _i64, _i64, _int, _vp],
+    "vr_trav_run": [_vp, _vp, _vp, _i64, _int, _dbl, _vp, _vp, ctypes.c_int32, _vp, _i64, _vp,
+                    _vp, _i64, _vp],
     "vr_shard_bucket": [_vp, _i64, _int, _int, _vp, _vp, _vp, _vp, _vp],
     "vr_shard_gather_rows": [_vp, _int, _vp, _i64, _vp, _vp],
     "vr_shard_scatter_rows": [_vp, _int, _vp, _i64, _vp, _vp],

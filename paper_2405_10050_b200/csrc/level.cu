@@ -316,3 +316,201 @@ extern "C" int vr_trav_level_rays(const double* rec, int64_t n_gen, int d, doubl
     return fail(e);
   return VR_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Native multi-level driver (vr_trav_run): the level loop itself in C++.
+// Each level is open -> (capacity checks) -> cast -> finalize + boundary,
+// with the two host synchronisations of the level calls and nothing else on
+// the host; it returns to the caller only when the traversal is done, the
+// level limit is reached, or a capacity (workspace, vertex arrays / table,
+// edge table, boundary arrays) must grow -- the caller grows it and calls
+// again (state->phase records whether the current level's cast is done).
+// ---------------------------------------------------------------------------
+extern "C" {
+int vr_trav_finalize(const vr_traverse_tables* tab, const double* rec, int d,
+                     const int32_t* ray_sigma, const int64_t* slot, const int32_t* new_flag,
+                     const int64_t* new_off, int64_t n_rays, int32_t base_id, int32_t* vsig,
+                     double* vr, int32_t* bad, int bump, void* stream);
+int vr_trav_boundary(int d, const int32_t* esc_flag, const int64_t* esc_off,
+                     const int32_t* ray_parent, const double* ray_u, int64_t n_rays,
+                     const int32_t* frontier_sigma, int64_t base_b, int32_t* bsig, double* bu,
+                     void* stream);
+}
+
+namespace {
+
+// Per-level buffers carved from the caller's workspace (F frontier
+// vertices, R rays), then the scratch of the two level calls.
+struct RunPlan {
+  size_t o_mask, o_cnt, o_off, o_x, o_u, o_eta, o_par, o_hidx, o_ht, o_hflag, o_rsig, o_slot,
+      o_newf, o_escf, o_noff, o_eoff, o_bad, o_scr, scratch, total;
+};
+
+int run_plan(int64_t F, int64_t R, int64_t n_gen, int d, RunPlan& p) {
+  int64_t scr = 0;
+  int s = vr_trav_level_workspace(F, R, n_gen, d, &scr);
+  if (s) return s;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align256(o + bytes);
+    return at;
+  };
+  p.o_mask = take((size_t)F * (d + 1));
+  p.o_cnt = take(4 * (size_t)F);
+  p.o_off = take(8 * (size_t)F);
+  p.o_x = take(8 * (size_t)R * d);
+  p.o_u = take(8 * (size_t)R * d);
+  p.o_eta = take(4 * (size_t)R * d);
+  p.o_par = take(4 * (size_t)R);
+  p.o_hidx = take(4 * (size_t)R);
+  p.o_ht = take(8 * (size_t)R);
+  p.o_hflag = take((size_t)R);
+  p.o_rsig = take(4 * (size_t)R * (d + 1));
+  p.o_slot = take(8 * (size_t)R);
+  p.o_newf = take(4 * (size_t)R);
+  p.o_escf = take(4 * (size_t)R);
+  p.o_noff = take(8 * (size_t)R);
+  p.o_eoff = take(8 * (size_t)R);
+  p.o_bad = take(16);
+  p.scratch = (size_t)scr;
+  p.o_scr = take(p.scratch);
+  p.total = o;
+  return VR_OK;
+}
+
+}  // namespace
+
+extern "C" int vr_trav_run_workspace(int64_t n_frontier, int64_t n_rays, int64_t n_gen, int d,
+                                     int64_t* bytes) {
+  if (!bytes) return VR_EINVAL;
+  RunPlan p;
+  const int s = run_plan(n_frontier, n_rays, n_gen, d, p);
+  if (s) return s;
+  *bytes = (int64_t)p.total;
+  return VR_OK;
+}
+
+extern "C" int vr_trav_run(const vr_traverse_tables* tab, vr_trav_state* S, const double* rec,
+                           int64_t n_gen, int d, double sqmax, const vr_screen32* s32,
+                           const vr_prune_index* ix, int32_t last_level, int64_t* level_new,
+                           int64_t level_cap, uint64_t* work, void* workspace,
+                           int64_t workspace_bytes, void* stream) {
+  if (!tab || !S || !rec || !ix || !level_new) return VR_EINVAL;
+  cudaStream_t st = as_stream(stream);
+  char* W = static_cast<char*>(workspace);
+  S->need = VR_RUN_DONE;
+  while (true) {
+    const int64_t F = S->f1 - S->f0;
+    if (F <= 0 || (last_level >= 0 && S->level > last_level)) {
+      S->need = VR_RUN_DONE;
+      return VR_OK;
+    }
+    if (S->level >= level_cap) return VR_ECAPACITY;
+    const int32_t* fs = S->vsig + S->f0 * (d + 1);
+    const double* fr = S->vr + S->f0 * d;
+    // workspace for the open step (R unknown yet: R <= (d+1) F)
+    RunPlan p0;
+    int s = run_plan(F, 0, n_gen, d, p0);
+    if (s) return s;
+    if (!workspace || workspace_bytes < (int64_t)p0.total) {
+      S->need = VR_RUN_NEED_WORKSPACE;
+      S->need_amount = (int64_t)p0.total;
+      return VR_OK;
+    }
+    uint8_t* mask = reinterpret_cast<uint8_t*>(W + p0.o_mask);
+    int32_t* ocnt = reinterpret_cast<int32_t*>(W + p0.o_cnt);
+    int64_t* ooff = reinterpret_cast<int64_t*>(W + p0.o_off);
+    int64_t R = S->pending_rays;
+    if (S->phase == 0) {
+      s = vr_trav_level_open(tab, d, fs, F, mask, ocnt, ooff, &R, W + p0.o_scr,
+                             (int64_t)p0.scratch, stream);
+      if (s) return s;
+      if (R == 0) {  // nothing open: the traversal ends here
+        level_new[S->level] = 0;
+        S->f0 = S->f1;
+        S->level += 1;
+        S->need = VR_RUN_DONE;
+        return VR_OK;
+      }
+      S->pending_rays = R;
+    }
+    RunPlan p;
+    if ((s = run_plan(F, R, n_gen, d, p))) return s;
+    if (workspace_bytes < (int64_t)p.total) {
+      S->need = VR_RUN_NEED_WORKSPACE;
+      S->need_amount = (int64_t)p.total;
+      S->phase = 0;  // the open step is redone with the grown workspace
+      return VR_OK;
+    }
+    // the open step's buffers sit at the same offsets in both plans
+    double* rx = reinterpret_cast<double*>(W + p.o_x);
+    double* ru = reinterpret_cast<double*>(W + p.o_u);
+    int32_t* reta = reinterpret_cast<int32_t*>(W + p.o_eta);
+    int32_t* rpar = reinterpret_cast<int32_t*>(W + p.o_par);
+    int32_t* hidx = reinterpret_cast<int32_t*>(W + p.o_hidx);
+    double* ht = reinterpret_cast<double*>(W + p.o_ht);
+    uint8_t* hflag = reinterpret_cast<uint8_t*>(W + p.o_hflag);
+    int32_t* rsig = reinterpret_cast<int32_t*>(W + p.o_rsig);
+    int64_t* slot = reinterpret_cast<int64_t*>(W + p.o_slot);
+    int32_t* newf = reinterpret_cast<int32_t*>(W + p.o_newf);
+    int32_t* escf = reinterpret_cast<int32_t*>(W + p.o_escf);
+    int64_t* noff = reinterpret_cast<int64_t*>(W + p.o_noff);
+    int64_t* eoff = reinterpret_cast<int64_t*>(W + p.o_eoff);
+    int32_t* bad = reinterpret_cast<int32_t*>(W + p.o_bad);
+    if (S->phase == 0) {
+      // capacity for up to R new vertices (arrays; vertex table at load <= 0.5)
+      // and their edges (edge table at load <= 0.5 of the incidence count)
+      if (S->nv + R > S->vcap_arrays || 2 * (S->nv + R) > tab->vcap) {
+        S->need = VR_RUN_NEED_VERTICES;
+        S->need_amount = S->nv + R;
+        return VR_OK;
+      }
+      if (2 * (S->e_ub + (d + 1) * R) > tab->ecap) {
+        S->need = VR_RUN_NEED_EDGES;
+        S->need_amount = S->e_ub + (d + 1) * R;
+        return VR_OK;
+      }
+      int64_t counts[5];
+      s = vr_trav_level_cast(tab, rec, n_gen, d, sqmax, s32, ix, fs, fr, F, mask, ooff, R,
+                             S->level, rx, ru, reta, rpar, hidx, ht, hflag, rsig, slot, newf,
+                             escf, noff, eoff, bad, work, counts, W + p.o_scr,
+                             (int64_t)p.scratch, stream);
+      if (s) return s;
+      S->n_new = counts[0];
+      S->n_esc = counts[1];
+      S->n_degenerate = counts[2];
+      S->n_bad = counts[3];
+      S->overflow = counts[4];
+      if (S->n_degenerate || S->n_bad || S->overflow) {
+        S->need = VR_RUN_ERROR;
+        return VR_OK;
+      }
+      S->phase = 1;
+    }
+    // phase 1: the cast is done -- store the new vertices, bump their edges,
+    // record the boundary rays
+    if (S->nb + S->n_esc > S->bcap) {
+      S->need = VR_RUN_NEED_BOUNDARY;
+      S->need_amount = S->nb + S->n_esc;
+      return VR_OK;
+    }
+    s = vr_trav_finalize(tab, rec, d, rsig, slot, newf, noff, R, (int32_t)S->f1, S->vsig, S->vr,
+                         bad + 1, 1, stream);
+    if (s) return s;
+    if (S->n_esc) {
+      s = vr_trav_boundary(d, escf, eoff, rpar, ru, R, fs, S->nb, S->bsig, S->bu, stream);
+      if (s) return s;
+    }
+    S->e_ub += (d + 1) * S->n_new;
+    S->nb += S->n_esc;
+    S->nv = S->f1 + S->n_new;
+    level_new[S->level] = S->n_new;
+    S->rays += R;
+    S->f0 = S->f1;
+    S->f1 = S->nv;
+    S->level += 1;
+    S->phase = 0;
+    S->pending_rays = 0;
+  }
+}

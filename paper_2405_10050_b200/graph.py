@@ -432,6 +432,21 @@ class _Tables(ctypes.Structure):
                 ("ecap", ctypes.c_int64), ("overflow", ctypes.c_void_p)]
 
 
+class _RunState(ctypes.Structure):  # vr_trav_state
+    _fields_ = [("vsig", ctypes.c_void_p), ("vr", ctypes.c_void_p), ("vcap_arrays", ctypes.c_int64),
+                ("bsig", ctypes.c_void_p), ("bu", ctypes.c_void_p), ("bcap", ctypes.c_int64),
+                ("nv", ctypes.c_int64), ("nb", ctypes.c_int64), ("e_ub", ctypes.c_int64),
+                ("f0", ctypes.c_int64), ("f1", ctypes.c_int64), ("level", ctypes.c_int32),
+                ("phase", ctypes.c_int32), ("pending_rays", ctypes.c_int64),
+                ("n_new", ctypes.c_int64), ("n_esc", ctypes.c_int64),
+                ("n_degenerate", ctypes.c_int64), ("n_bad", ctypes.c_int64),
+                ("overflow", ctypes.c_int64), ("rays", ctypes.c_int64), ("need", ctypes.c_int32),
+                ("need_amount", ctypes.c_int64)]
+
+
+RUN_DONE, RUN_NEED_WS, RUN_NEED_V, RUN_NEED_E, RUN_NEED_B, RUN_ERROR = range(6)
+
+
 def _pow2(n):
     return 1 << max(10, int(n - 1).bit_length())
 
@@ -638,6 +653,59 @@ class DeviceTraversal:
         self.rays_last = R
         return n_new
 
+    def run(self, f0, f1, first_level, last_level=-1, stats=None, ws=None):
+        """Levels first_level .. last_level (-1: until done) natively
+        (vr_trav_run: the level loop in C++, two synchronisations per level,
+        no per-level host work); returns the new-vertex count per level.
+        Capacities grow here when the driver asks for them."""
+        d, L, p = self.d, self.L, _lib.ptr
+        ws = ws if ws is not None else Workspace()
+        ns = self.ns
+        ix, s32 = ns.prune_index(self.dev), ns.screen32(self.dev)
+        cap = 4096
+        level_new = np.zeros(cap, dtype=np.int64)
+        S = _RunState()
+        S.nv, S.nb, S.e_ub = self.nv, self.nb, self.e_ub
+        S.f0, S.f1, S.level, S.phase = f0, f1, first_level, 0
+        wsb = 0
+        scratch = None
+        while True:
+            S.vsig, S.vr, S.vcap_arrays = p(self.vsig).value, p(self.vr).value, self.vsig.shape[0]
+            S.bsig, S.bu, S.bcap = p(self.bsig).value, p(self.bu).value, self.bsig.shape[0]
+            T = self.tables()
+            _lib.check(L.vr_trav_run(ctypes.byref(T), ctypes.byref(S), p(self.rec), ns.n, d,
+                                     self.sqmax, ctypes.byref(s32.struct), ctypes.byref(ix.struct),
+                                     int(last_level), level_new.ctypes.data, cap, p(self.work),
+                                     p(scratch), wsb, _lib.stream_handle()), "vr_trav_run")
+            need, amt = int(S.need), int(S.need_amount)
+            if need == RUN_DONE:
+                break
+            if need == RUN_NEED_WS:
+                scratch = ws.get("run_scratch", (int(1.25 * amt) + 4096,), torch.uint8, self.dev)
+                wsb = scratch.numel()
+            elif need == RUN_NEED_V:
+                self.nv = int(S.nv)
+                self.ensure_vertices(amt - self.nv)
+            elif need == RUN_NEED_E:
+                self.e_ub = int(S.e_ub)
+                self.ensure_edges(amt - self.e_ub)
+            elif need == RUN_NEED_B:
+                self.nb = int(S.nb)
+                self.ensure_boundary(amt - self.nb)
+            else:
+                if S.n_bad:
+                    raise DegenerateConfiguration(
+                        "generators of a frontier vertex are affinely dependent")
+                if S.n_degenerate:
+                    raise DegenerateConfiguration(
+                        f"{int(S.n_degenerate)} edge raycasts hit a generator on the circumsphere band")
+                raise RuntimeError("traversal hash table overflow")
+        self.nv, self.nb, self.e_ub = int(S.nv), int(S.nb), int(S.e_ub)
+        if stats is not None:
+            stats.add(int(S.rays))
+        self.rays_last = int(S.rays)
+        return [int(v) for v in level_new[first_level:int(S.level)]], int(S.f0), int(S.f1)
+
     def level(self, f0, f1, lvl, stats=None, ws=None, raycast_fn=None):
         """Expand frontier vertices [f0, f1); returns the number of new vertices.
 
@@ -824,6 +892,11 @@ def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heurist
     f0, f1, lvl = 0, 1, 1
     levels = []
     rfn = _level_raycaster(ns, stats, group, tr.work)
+    if rfn is None and tr.native and ns.n >= PRUNE_MIN_GENERATORS:
+        news, _, _ = tr.run(0, 1, 1, -1, stats=stats, ws=ws)  # the native level loop
+        sizes = [1] + news
+        levels = [(sizes[k], news[k]) for k in range(len(news))]
+        f0 = f1 = tr.nv
     while f1 > f0:
         n_new = tr.level(f0, f1, lvl, stats=stats, ws=ws, raycast_fn=rfn)
         levels.append((f1 - f0, n_new))
@@ -884,6 +957,12 @@ def voronoi_local(ns: NodeSet, starts, hops: int, seed: int = 0, stats: RaycastS
     f0, f1 = 0, tr.nv
     bounds = [(0, f1)]
     rfn = _level_raycaster(ns, stats, group, work)
+    if rfn is None and tr.native and ns.n >= PRUNE_MIN_GENERATORS and hops >= 1:
+        news, _, _ = tr.run(0, f1, 1, hops, stats=stats, ws=ws)  # the native level loop
+        for n_new in news:
+            f0, f1 = f1, f1 + n_new
+            bounds.append((f0, f1))
+        hops = 0
     for lvl in range(1, hops + 1):
         if f1 == f0:
             break
