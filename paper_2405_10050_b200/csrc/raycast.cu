@@ -33,6 +33,14 @@ int vr::coop_mode() {
   return v;
 }
 
+// Tensor-core sweep (k_raycast_sweep, d <= 6): VR_SWEEP=1 selects it (read
+// per launch, so tests can switch it); off by default -- it is bound by the
+// TMEM read rate.
+int vr::sweep_mode() {
+  const char* e = std::getenv("VR_SWEEP");
+  return e ? std::atoi(e) : 0;
+}
+
 extern "C" int vr_abi_version(void) { return 5; }
 
 extern "C" const char* vr_status_string(int status) {

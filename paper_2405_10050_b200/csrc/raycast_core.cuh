@@ -2085,6 +2085,11 @@ constexpr int PRUNE_TILE = 64;
 #endif
 constexpr int PRUNE_BLOCK = 32;
 
+template <int D, class Src>
+int launch_sweep(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
+                 const RayOut& out, cudaStream_t st, unsigned long long* work);
+int sweep_mode();  // VR_SWEEP=1 / 0 forces the tensor-core sweep on / off
+
 template <int D, int R, int MINB, bool F32, class Src, bool MMA = false>
 int launch_pruned_rm(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
                      const RayOut& out, cudaStream_t st, unsigned long long* work) {
@@ -2213,6 +2218,10 @@ int launch_raycast_pruned(const Src& src, int64_t n_rays, const PrunedIndex& ix,
   // small to fill the GPU with 32-ray warps (< 8192 rays: the small levels
   // of a full traversal; config 1 12.5 -> 10.5 ms) go to the cooperative
   // kernel; VR_COOP=1 / 0 force it on / off.
+  if constexpr (PRUNE_TILE == 64 && D <= 6) {
+    if (ix.crec32 && ix.crecU && ix.crec32s && sweep_mode() > 0)
+      return launch_sweep<D>(src, n_rays, ix, fr, out, st, work);
+  }
   const int cm = coop_mode();
   const bool coop = cm > 0 || (cm < 0 && (n_rays < 8192 || (D >= 7 && n_rays * 64 < ix.n)));
   if (ix.crec32 && ix.wide.box32 && ix.wide.levels >= 2 && coop)

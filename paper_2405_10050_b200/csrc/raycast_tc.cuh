@@ -352,4 +352,250 @@ int launch_pruned_tc(const Src& src, int64_t n_rays, const PrunedIndex& ix, cons
   VR_RETURN_LAUNCH();
 }
 
+
+// ---------------------------------------------------------------------------
+// Sweep kernel: the tensor-core screen of EVERY generator for 128 rays per
+// CTA, no kd walk (small N at d <= 6, e.g. config 2: N = 20,000).  The warp
+// kernels spend their time in the tree walk and its divergent decisions;
+// here one thread issues a single tcgen05.mma of M = 128 rays x N = NB
+// candidates (K = 8: [z32, 1, ctc] . [x~, |x~|^2, 1], the same operands and
+// conservative bound as k_raycast_tc) per step, into one of two TMEM
+// accumulators, while the four warps drain the other one: each thread
+// tcgen05.ld's its ray's NB results and ORs their sign bits (~0.5 LOP3 per
+// pair).  The rare pairs go through the unchanged fp64 rare path
+// (ray_rare_block), so results are bitwise those of every other screen.
+//
+// Pipeline (thread 0 issues TMA and MMA; all 128 threads drain):
+//   step j:  issue MMA j+1 (A[(j+1)&1], B stage (j+1)%ST) -> TMEM[(j+1)&1]
+//            wait MMA j; refill B stage j%ST with block j+ST
+//            drain TMEM[j&1]; rare path; rewrite A[j&1] rows of rays whose
+//            sphere moved in this or the previous step
+//            barrier (TMEM[j&1] drained and A[j&1] written before MMA j+2)
+// A ray's row is rewritten into both buffers over two steps after an update,
+// so an MMA reads either the current or an older (larger) sphere: stale
+// spheres screen a superset, which keeps the screen conservative.
+// Blocks of NB candidates are visited in a spiral around the CTA's home
+// block (the kd tile of its first ray's generator): the rays' spheres shrink
+// within the first few steps and the remaining blocks rarely hit.
+// ---------------------------------------------------------------------------
+constexpr int SWEEP_RAYS = 128;
+constexpr int SWEEP_STAGES = 4;
+
+__host__ __device__ constexpr uint32_t sweep_idesc(int nb) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(nb >> 3) << 17) |
+         ((uint32_t)(SWEEP_RAYS >> 4) << 24);
+}
+
+template <int NB>
+__device__ __forceinline__ void umma_tf32_n(uint32_t d_tmem, uint64_t a, uint64_t b) {
+  asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 0;" ::"r"(d_tmem), "l"(a),
+               "l"(b), "r"(sweep_idesc(NB))
+               : "memory");
+}
+
+__device__ __forceinline__ uint32_t or32(const uint32_t (&v)[32]) {
+  uint32_t a = v[0] | v[1] | v[2], b = v[3] | v[4] | v[5], c = v[6] | v[7] | v[8];
+  uint32_t e = v[9] | v[10] | v[11], f = v[12] | v[13] | v[14], g = v[15] | v[16] | v[17];
+  uint32_t h = v[18] | v[19] | v[20], i = v[21] | v[22] | v[23], j = v[24] | v[25] | v[26];
+  uint32_t k = v[27] | v[28] | v[29], l = v[30] | v[31];
+  return (a | b | c) | (e | f | g) | (h | i | j) | (k | l);
+}
+
+// The sweep screens with ONE product per ray: the sphere row [z32, 1, ctc]
+// once the ray has a best candidate, before that the negated halfspace row
+// [-u32, 0, -c2] (f~ = -(u~.x~ + c2) < 0 iff the candidate may lie in front,
+// the conservative pre-filter of tc_store_u), so a ray whose seed found
+// nothing sends only the candidates ahead of it to the rare path.
+template <int D>
+__device__ __forceinline__ void sweep_store_a(const RayState<D>& r, const Frame& fr, float* sA,
+                                              int m, bool act) {
+  if (r.ib >= 0 || !act) {
+    tc_store_a<D>(r, sA, m);
+    return;
+  }
+  const double xm = sqrt(fr.sqmax32);
+  const double eu = 1.25 * (9.775161743164062e-04 * xm +
+                            1.52587890625e-05 * (xm + fabs((double)r.thr32) + 1.0));
+  double c2 = (double)r.bsl32 - (double)r.thr32 + eu;
+  c2 = fmin(fmax(c2, -1e30), 1e30);
+  float f[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    f[k] = k < D ? -__uint_as_float(tf32_rn(r.u32[k]))
+                 : k == D + 1 ? -tf32_up(__double2float_ru(c2)) : 0.0f;
+  tc_store_row<D>(sA, m, f);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int D, int NB, int MINB, class Src>
+__global__ void __launch_bounds__(SWEEP_RAYS, MINB)
+    k_raycast_sweep(Src src, const double* __restrict__ crec, const float* __restrict__ crecU,
+                    const float* __restrict__ crec32s, const int32_t* __restrict__ perm,
+                    const int32_t* __restrict__ inv_perm, int64_t n_rows, Frame fr, RayOut out,
+                    unsigned long long* __restrict__ work) {
+  static_assert(tc_ksteps(D) == 1, "sweep kernel: one k-step (d <= 6)");
+  static_assert(NB % 64 == 0 && NB <= 256, "NB: whole 64-row tiles");
+  constexpr int S = rec_stride(D);
+  constexpr uint32_t BLK_BYTES = NB * 32;
+  __shared__ __align__(1024) float sA[2][SWEEP_RAYS * 8];
+  __shared__ __align__(1024) float sB[SWEEP_STAGES][NB * 8];
+  __shared__ __align__(8) uint64_t bar_b[SWEEP_STAGES];
+  __shared__ __align__(8) uint64_t bar_mma[2];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ int64_t home_s;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_s)),
+                 "r"((uint32_t)(2 * NB)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  const int64_t nblk = n_rows / NB;
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < SWEEP_STAGES; ++i) mbar_init(&bar_b[i], 1);
+    mbar_init(&bar_mma[0], 1);
+    mbar_init(&bar_mma[1], 1);
+    fence_mbar_init();
+    home_s = (int64_t)inv_perm[src.gen((int64_t)blockIdx.x * SWEEP_RAYS)] / NB;
+  }
+  const int64_t k = (int64_t)blockIdx.x * SWEEP_RAYS + tid;
+  RayState<D> ray;
+  const bool act = src.load(k, ray, fr);
+  if (!act) init_padding_lane<D, 1>(ray);
+  if (act) ray.gk = inv_perm[src.gen(k)];
+  if (act) {
+    const int64_t so = (int64_t)ray.gk / TC_TILE;  // the ray's own tile
+    seed_tile32<D>(ray, crec32s + so * TC_TILE * rec32_stride(D), crec + so * TC_TILE * S,
+                   (int)(so * TC_TILE), fr);
+  }
+  sweep_store_a<D>(ray, fr, sA[0], tid, act);
+  sweep_store_a<D>(ray, fr, sA[1], tid, act);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+  const int64_t home = home_s;
+  auto block_of = [&](int64_t j) -> int64_t {  // spiral: home, +1, -1, +2, -2, ...
+    const int64_t off = (j & 1) ? (j + 1) >> 1 : -(j >> 1);
+    int64_t b = (home + off) % nblk;
+    return b < 0 ? b + nblk : b;
+  };
+  auto issue_b = [&](int64_t j) {
+    const int st = (int)(j % SWEEP_STAGES);
+    mbar_arrive_expect_tx(&bar_b[st], BLK_BYTES);
+    bulk_g2s(sB[st], crecU + block_of(j) * (NB * 8), BLK_BYTES, &bar_b[st]);
+  };
+  auto issue_mma = [&](int64_t j) {
+    const int st = (int)(j % SWEEP_STAGES);
+    mbar_wait(&bar_b[st], (uint32_t)((j / SWEEP_STAGES) & 1));
+    tc_fence_after();
+    umma_tf32_n<NB>(tmem + (uint32_t)((j & 1) * NB), umma_desc(smem_u32(sA[j & 1])),
+                    umma_desc(smem_u32(sB[st])));
+    umma_commit(&bar_mma[j & 1]);
+  };
+  if (tid == 0) {
+    for (int64_t j = 0; j < SWEEP_STAGES && j < nblk; ++j) issue_b(j);
+    issue_mma(0);
+  }
+  const uint32_t row = tmem + ((uint32_t)(warp * 32) << 16);
+  unsigned long long rare_blocks = 0, entries = 0, rare_steps = 0;
+  int dirty = 0;
+  for (int64_t j = 0; j < nblk; ++j) {
+    if (tid == 0 && j + 1 < nblk) issue_mma(j + 1);
+    mbar_wait(&bar_mma[j & 1], (uint32_t)((j >> 1) & 1));
+    tc_fence_after();
+    if (tid == 0 && j + SWEEP_STAGES < nblk) issue_b(j + SWEEP_STAGES);  // stage j free
+    const uint32_t acc = row + (uint32_t)((j & 1) * NB);
+    uint32_t any = 0u;
+#pragma unroll
+    for (int q = 0; q < NB / 32; ++q) {
+      uint32_t v[32];
+      tmem_ld32(acc + 32 * q, v);
+      tmem_wait_ld();
+      any |= or32(v);
+    }
+    const int64_t b = block_of(j);
+    const int gb = (int)(b * NB);
+    if (__any_sync(0xffffffffu, (int)(any >> 31))) {
+      ++rare_steps;
+      const int nupd0 = ray.nupd;
+#pragma unroll 1
+      for (int q = 0; q < NB / 32; ++q) {
+        uint32_t v[32];
+        tmem_ld32(acc + 32 * q, v);
+        tmem_wait_ld();
+        uint32_t m = sign_mask32(v);
+        const int base = gb + 32 * q;
+        const int rel = ray.ib - base;  // the current best itself
+        if ((unsigned)rel < 32u) m &= ~(1u << rel);
+        const int relg = ray.gk - base;  // g: on every sphere, never valid
+        if ((unsigned)relg < 32u) m &= ~(1u << relg);
+        if (m) {
+          ++rare_blocks;
+          entries += __popc(m);
+          ray_rare_block<D, true>(ray, crec + (int64_t)base * S, m, base, fr);
+        }
+      }
+      if (ray.nupd != nupd0) dirty = 2;
+    }
+    if (dirty) {
+      sweep_store_a<D>(ray, fr, sA[j & 1], tid, act);
+      --dirty;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  if (act) ray_store<D>(ray, src.id(k), perm, out);
+  if (work) {
+    unsigned long long e = entries, rb = rare_blocks, up = act ? ray.nupd : 0, a = act ? 1 : 0;
+    for (int off = 16; off > 0; off >>= 1) {
+      e += __shfl_xor_sync(0xffffffffu, e, off);
+      rb += __shfl_xor_sync(0xffffffffu, rb, off);
+      up += __shfl_xor_sync(0xffffffffu, up, off);
+      a += __shfl_xor_sync(0xffffffffu, a, off);
+    }
+    if ((tid & 31) == 0) {
+      atomicAdd(work, a * (unsigned long long)n_rows);
+      atomicAdd(work + 1, rb);
+      atomicAdd(work + 2, rare_steps);  // warp steps that entered the rare path
+      atomicAdd(work + 3, e);
+      atomicAdd(work + 4, up);
+    }
+#ifdef VR_RARE_STATS
+    int stv[5] = {ray.st_out, ray.st_self, ray.st_behind, ray.st_band, ray.st_imp};
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      unsigned long long v = act ? stv[q] : 0;
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if ((tid & 31) == 0) atomicAdd(work + 6 + q, v);
+    }
+#endif
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"((uint32_t)(2 * NB)));
+  }
+}
+
+template <int D, class Src>
+int launch_sweep(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
+                 const RayOut& out, cudaStream_t st, unsigned long long* work) {
+  if constexpr (tc_ksteps(D) == 1) {
+#ifndef VR_SWEEP_NB
+#define VR_SWEEP_NB 128
+#endif
+    constexpr int NB = VR_SWEEP_NB;
+    const int64_t grid = (n_rays + SWEEP_RAYS - 1) / SWEEP_RAYS;
+    k_raycast_sweep<D, NB, (NB <= 128 ? 2 : 1), Src><<<(unsigned)grid, SWEEP_RAYS, 0, st>>>(
+        src, ix.crec, ix.crecU, ix.crec32s, ix.perm, ix.inv_perm, rec_rows(ix.n), fr, out, work);
+    VR_RETURN_LAUNCH();
+  }
+  return VR_EINVAL;
+}
+
 }  // namespace vr

@@ -63,3 +63,29 @@ for m in (1_000_000, 500_000, 250_000, 131072, 65536):
     torch.cuda.synchronize()
     ms = ev[0].elapsed_time(ev[2])
     print(f"device-resident slice {m:8d}: {ms:.3f} ms  -> {ms * 1e6 / m:.2f} ms per 1e6 rays")
+# raw copy-engine rates: 100 MB pinned H2D, 61 MB D2H, alone and concurrent
+hb = P((100_000_000,), torch.uint8)
+db = torch.empty(100_000_000, dtype=torch.uint8, device="cuda")
+hb2 = P((61_000_000,), torch.uint8)
+db2 = torch.empty(61_000_000, dtype=torch.uint8, device="cuda")
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+for rep in range(3):
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        e[0].record(s1); db.copy_(hb, non_blocking=True); e[1].record(s1)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s2):
+        e[2].record(s2); hb2.copy_(db2, non_blocking=True); e[3].record(s2)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        e[4].record(s1); db.copy_(hb, non_blocking=True)
+    with torch.cuda.stream(s2):
+        s2.wait_event(e[4]); hb2.copy_(db2, non_blocking=True)
+    s1.wait_stream(s2)
+    with torch.cuda.stream(s1):
+        e[5].record(s1)
+    torch.cuda.synchronize()
+    print(f"H2D 100 MB {e[0].elapsed_time(e[1]):.3f} ms ({100 / e[0].elapsed_time(e[1]):.1f} GB/s), "
+          f"D2H 61 MB {e[2].elapsed_time(e[3]):.3f} ms ({61 / e[2].elapsed_time(e[3]):.1f} GB/s), "
+          f"both concurrent {e[4].elapsed_time(e[5]):.3f} ms")
