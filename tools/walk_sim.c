@@ -97,8 +97,41 @@ static int need(const Tree* T, const Ray* r, int64_t node, double* lb, double* d
   return 1;
 }
 
+static int sub_rows = 0;        /* 0: off; else rows per sub-box */
+static int64_t sub_needed = 0;  /* sub-boxes needed over the batch */
+void set_sub(int v) { sub_rows = v; sub_needed = 0; }
+int64_t get_sub_needed(void) { return sub_needed; }
+
+static void count_subs(const Tree* T, const Ray* r, int64_t tile) {
+  const int d = T->d;
+  double ux = 0;
+  for (int k = 0; k < d; ++k) ux += r->u[k] * r->x[k];
+  const double rho2 = isfinite(r->tb) ? r->r02 - 2 * r->tb * (r->s - ux) + r->tb * r->tb : INFINITY;
+  for (int s0 = 0; s0 < T->pt; s0 += sub_rows) {
+    double lo[16], hi[16];
+    int any = 0;
+    for (int k = 0; k < d; ++k) { lo[k] = INFINITY; hi[k] = -INFINITY; }
+    for (int j = s0; j < s0 + sub_rows; ++j) {
+      const double* y = T->rec + (tile * T->pt + j) * T->rs;
+      if (isinf(y[d])) continue;
+      any = 1;
+      for (int k = 0; k < d; ++k) { lo[k] = fmin(lo[k], y[k]); hi[k] = fmax(hi[k], y[k]); }
+    }
+    if (!any) continue;
+    double dz = 0, um = 0;
+    for (int k = 0; k < d; ++k) {
+      double z = r->x[k] + (isfinite(r->tb) ? r->tb : 0) * r->u[k];
+      double f = fmax(fmax(lo[k] - z, z - hi[k]), 0);
+      dz += f * f;
+      um += r->u[k] * (r->u[k] > 0 ? hi[k] : lo[k]);
+    }
+    if (um > r->thr && dz < rho2) ++sub_needed;
+  }
+}
+
 static void screen_tile(const Tree* T, Ray* r, int64_t tile) {
   const int d = T->d;
+  if (sub_rows) count_subs(T, r, tile);
   for (int j = 0; j < T->pt; ++j) {
     int64_t i = tile * T->pt + j;
     const double* y = T->rec + i * T->rs;

@@ -112,8 +112,38 @@ def main(nray=int(os.environ.get("NRAY", "1500"))):
 
     names = {0: "start-tile child first", 1: "nearest (d2) first", 2: "lower bound first (DFS)",
              3: "best-first (LB heap)"}
+    W.get_sub_needed.restype = ctypes.c_int64
+    W.set_joint(0)
+
+    def kd_within_tiles(rec, levels):
+        """rows of each 64-row tile re-ordered by `levels` median splits on
+        the widest dimension (sub-boxes of 64 >> levels rows)"""
+        rows = rec.reshape(-1, PT, rec.shape[1]).copy()
+        for lv in range(levels):
+            g = 1 << lv
+            blk = rows.reshape(rows.shape[0] * g, PT // g, rows.shape[2])
+            xs_ = np.where(np.isinf(blk[:, :, d:d + 1]), np.nan, blk[:, :, :d])
+            ext = np.nanmax(xs_, 1) - np.nanmin(xs_, 1)
+            ax = np.nan_to_num(ext, nan=-1).argmax(1)
+            key = np.take_along_axis(np.nan_to_num(xs_, nan=np.inf), ax[:, None, None], 2)[:, :, 0]
+            o = np.argsort(key, 1, kind="stable")
+            blk = np.take_along_axis(blk, o[:, :, None], 1)
+            rows = blk.reshape(rows.shape)
+        return np.ascontiguousarray(rows.reshape(rec.shape))
+
+    rec_orig = rec
+    for tag, rr in (("tile row order", rec_orig), ("kd within tiles", kd_within_tiles(rec_orig, 3))):
+        rec = rr
+        for sub in (32, 16, 8):
+            W.set_sub(sub)
+            tl, ts, ag = run(0, "oracle", 1)
+            print(f"{tag}: oracle seed, {sub}-row sub-boxes: tiles/ray {tl:.2f} -> pairs/ray "
+                  f"{64 * tl:.0f}; needed sub-boxes/ray {W.get_sub_needed() / n:.2f} -> pairs/ray "
+                  f"{sub * W.get_sub_needed() / n:.0f}", flush=True)
+    rec = rec_orig
+    W.set_sub(0)
     for seedmode in ("oracle", "own"):
-      for joint in (0, 1):
+      for joint in (0,):
         W.set_joint(joint)
         print(f"joint box/halfspace/sphere test: {joint}")
         for lb in (1,):
