@@ -18,6 +18,8 @@
 // the Python-driven level (the processing order is the same stable sort).
 #include <cub/device/device_scan.cuh>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 extern "C" {
@@ -337,7 +339,21 @@ int vr_trav_boundary(int d, const int32_t* esc_flag, const int64_t* esc_off,
                      void* stream);
 }
 
+namespace vr {
+int trav_run_small(const vr_traverse_tables* tab, vr_trav_state* S, const double* rec,
+                   int64_t n_gen, int d, double sqmax, const vr_screen32* s32,
+                   const vr_prune_index* ix, int32_t last_level, int64_t* level_new,
+                   int64_t level_cap, uint64_t* work, void* workspace, int64_t workspace_bytes,
+                   cudaStream_t st, int* handled, int32_t* bail_code);
+}
+
 namespace {
+
+// VR_SMALL_LEVELS=0 disables the persistent small-level kernel (A/B runs).
+bool small_mode() {
+  const char* e = std::getenv("VR_SMALL_LEVELS");
+  return !e || std::atoi(e) != 0;
+}
 
 // Per-level buffers carved from the caller's workspace (F frontier
 // vertices, R rays), then the scratch of the two level calls.
@@ -400,6 +416,7 @@ extern "C" int vr_trav_run(const vr_traverse_tables* tab, vr_trav_state* S, cons
   cudaStream_t st = as_stream(stream);
   char* W = static_cast<char*>(workspace);
   S->need = VR_RUN_DONE;
+  int32_t host_level = -1;  // a level the persistent kernel handed back
   while (true) {
     const int64_t F = S->f1 - S->f0;
     if (F <= 0 || (last_level >= 0 && S->level > last_level)) {
@@ -407,6 +424,22 @@ extern "C" int vr_trav_run(const vr_traverse_tables* tab, vr_trav_state* S, cons
       return VR_OK;
     }
     if (S->level >= level_cap) return VR_ECAPACITY;
+    // small levels: the persistent kernel (level_small.cu) runs as many as
+    // stay small in one launch
+    if (S->phase == 0 && F <= 8192 && S->level != host_level && small_mode()) {
+      int handled = 0;
+      int32_t bail = 0;
+      const int s0 = vr::trav_run_small(tab, S, rec, n_gen, d, sqmax, s32, ix, last_level,
+                                        level_new, level_cap, work, workspace, workspace_bytes,
+                                        st, &handled, &bail);
+      if (s0) return s0;
+      if (handled) {
+        if (S->need != bail) return VR_OK;  // done, error, or a capacity to grow
+        host_level = S->level;               // this level is too large: host path
+        S->need = VR_RUN_DONE;
+        continue;
+      }
+    }
     const int32_t* fs = S->vsig + S->f0 * (d + 1);
     const double* fr = S->vr + S->f0 * d;
     // workspace for the open step (R unknown yet: R <= (d+1) F)

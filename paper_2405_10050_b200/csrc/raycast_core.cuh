@@ -1759,20 +1759,21 @@ __device__ __forceinline__ void coop_screen_tile(RayState<D>& r, const double* _
   coop_rare<D>(r, crec, ia, pa, pb, fr);
 }
 
-template <int D, int PT, int NW, int MINB, class Src>
-__global__ void __launch_bounds__(NW * 32, MINB)
-    k_raycast_coop(Src src, int64_t n_rays, const double* __restrict__ crec,
-                   const float* __restrict__ crec32p, const int32_t* __restrict__ perm,
-                   const int32_t* __restrict__ inv_perm, WideTree wt, Frame fr, RayOut out,
-                   unsigned long long* __restrict__ work) {
+constexpr int COOP_STK = WIDE * WIDE_MAX_LEVELS;  // shared ints per warp (DFS stack)
+
+// One ray (slot k of src) on the calling warp; `stk` = COOP_STK shared ints
+// of this warp.  The body of k_raycast_coop, also run by the persistent
+// small-traversal kernel (level_small.cu).
+template <int D, int PT, class Src>
+__device__ __forceinline__ void coop_ray(const Src& src, int64_t k, const double* __restrict__ crec,
+                                         const float* __restrict__ crec32p,
+                                         const int32_t* __restrict__ perm,
+                                         const int32_t* __restrict__ inv_perm, const WideTree& wt,
+                                         const Frame& fr, const RayOut& out,
+                                         unsigned long long* __restrict__ work, int* stk) {
   constexpr int BS = box32_stride(D);
-  constexpr int STK = WIDE * WIDE_MAX_LEVELS;
-  __shared__ int stk_s[NW][STK];
+  constexpr int STK = COOP_STK;
   const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  int* stk = stk_s[w];
-  const int64_t k = (int64_t)blockIdx.x * NW + w;
-  if (k >= n_rays) return;
   RayState<D> r;
   src.load(k, r, fr);
   coop_seed<D, PT>(r, crec, inv_perm[src.gen(k)] / PT, fr);
@@ -1867,6 +1868,19 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   }
 }
 
+template <int D, int PT, int NW, int MINB, class Src>
+__global__ void __launch_bounds__(NW * 32, MINB)
+    k_raycast_coop(Src src, int64_t n_rays, const double* __restrict__ crec,
+                   const float* __restrict__ crec32p, const int32_t* __restrict__ perm,
+                   const int32_t* __restrict__ inv_perm, WideTree wt, Frame fr, RayOut out,
+                   unsigned long long* __restrict__ work) {
+  __shared__ int stk_s[NW][COOP_STK];
+  const int w = threadIdx.x >> 5;
+  const int64_t k = (int64_t)blockIdx.x * NW + w;
+  if (k >= n_rays) return;
+  coop_ray<D, PT>(src, k, crec, crec32p, perm, inv_perm, wt, fr, out, work, stk_s[w]);
+}
+
 // ---------------------------------------------------------------------------
 // Exact re-check: one CTA per listed ray.  Pass 1: centred t for every valid
 // candidate, lexicographic (t, index) argmin.  Pass 2: runner-up distance at
@@ -1896,17 +1910,15 @@ __device__ __forceinline__ void block_argmin(double& t, int& i, double* sh_t, in
   i = sh_i[0];
 }
 
+// Exact re-check of ray k by the whole (NT-thread) block; sh_t / sh_i are
+// NT / 32 shared slots.  Returns with the result stored.
 template <int D, int NT, class Src>
-__global__ void __launch_bounds__(NT)
-    k_raycast_recheck(Src src, const double* __restrict__ crec, const int32_t* __restrict__ cand,
-                      int64_t n_cand, const int32_t* __restrict__ list,
-                      const int32_t* __restrict__ count, RayOut out) {
+__device__ __forceinline__ void recheck_ray(const Src& src, int64_t k,
+                                            const double* __restrict__ crec,
+                                            const int32_t* __restrict__ cand, int64_t n_cand,
+                                            const RayOut& out, double* sh_t, int* sh_i) {
   constexpr int S = rec_stride(D);
-  __shared__ double sh_t[NT / 32];
-  __shared__ int sh_i[NT / 32];
-  const int cntl = *count;
-  for (int li = blockIdx.x; li < cntl; li += gridDim.x) {
-    const int64_t k = list[li];
+  {
     RayState<D> r;
     src.load(k, r, Frame{});
     double best = CUDART_INF;
@@ -1935,7 +1947,7 @@ __global__ void __launch_bounds__(NT)
         if (out.rp)
           for (int j = 0; j < D; ++j) out.rp[k * D + j] = CUDART_NAN;
       }
-      continue;
+      return;
     }
     double rp[D];
 #pragma unroll
@@ -1964,6 +1976,18 @@ __global__ void __launch_bounds__(NT)
       out.flag[k] = (second < radius * (1.0 + VR_TOL_DEGENERATE)) ? VR_RAY_DEGENERATE : VR_RAY_OK;
     }
   }
+}
+
+template <int D, int NT, class Src>
+__global__ void __launch_bounds__(NT)
+    k_raycast_recheck(Src src, const double* __restrict__ crec, const int32_t* __restrict__ cand,
+                      int64_t n_cand, const int32_t* __restrict__ list,
+                      const int32_t* __restrict__ count, RayOut out) {
+  __shared__ double sh_t[NT / 32];
+  __shared__ int sh_i[NT / 32];
+  const int cntl = *count;
+  for (int li = blockIdx.x; li < cntl; li += gridDim.x)
+    recheck_ray<D, NT>(src, list[li], crec, cand, n_cand, out, sh_t, sh_i);
 }
 
 // Host-side launch helpers -------------------------------------------------

@@ -248,28 +248,38 @@ for name, pts in (("u2", np.random.default_rng(23).random((5000, 2))),
     a = vb.voronoi_graph(vb.NodeSet(pts), seed=0).arrays()
     for k in ("sigma", "r", "edge_key", "edge_count", "boundary_sigma", "boundary_u"):
         out[name + "_" + k] = a[k]
+pts = np.random.default_rng(25).random((30000, 7))
+m, lv = vb.voronoi_local(vb.NodeSet(pts), np.arange(0, 30000, 300), hops=3, return_levels=True)
+a = m.arrays()
+out["loc7_sigma"], out["loc7_r"], out["loc7_level"] = a["sigma"], a["r"], lv
 np.savez(sys.argv[2], **out)
 """
 
 
 def test_native_level_driver_matches_python_levels(tmp_path):
-    """The native level driver (csrc/level.cu, default) and the Python-driven
-    level (VR_NATIVE_LEVEL=0, read once per traversal object; subprocesses)
-    produce identical meshes: vertex sigma / coordinates (bitwise, in id
-    order), edge keys and counts, boundary rays."""
+    """The native level driver (csrc/level.cu, default; small levels in the
+    persistent kernel of csrc/level_small.cu), the same driver level by level
+    (VR_SMALL_LEVELS=0) and the Python-driven level (VR_NATIVE_LEVEL=0, read
+    once per traversal object; subprocesses) produce identical meshes: vertex
+    sigma / coordinates (bitwise, in id order), edge keys and counts, boundary
+    rays; full diagrams at d = 2..5 (levels crossing the small-kernel limit
+    both ways) and a d = 7 local traversal with its hop levels."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
-    for mode in ("1", "0"):
+    # native driver with the persistent small-level kernel (default), native
+    # driver level by level only, Python-driven levels
+    for mode, env in (("1", {}), ("s0", {"VR_SMALL_LEVELS": "0"}), ("0", {"VR_NATIVE_LEVEL": "0"})):
         path = str(tmp_path / f"lv{mode}.npz")
         p = subprocess.run([sys.executable, "-c", _LEVEL_SCRIPT, root, path],
-                           env=dict(os.environ, VR_NATIVE_LEVEL=mode), capture_output=True,
+                           env=dict(os.environ, **env), capture_output=True,
                            text=True, timeout=600)
         assert p.returncode == 0, p.stderr[-2000:]
         res[mode] = np.load(path)
-    for k in res["1"].files:
-        assert np.array_equal(res["1"][k], res["0"][k]), k
+    for other in ("s0", "0"):
+        for k in res["1"].files:
+            assert np.array_equal(res["1"][k], res[other][k]), (other, k)
 
 
 _SHARDED_SCRIPT = r"""
