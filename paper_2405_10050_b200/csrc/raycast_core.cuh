@@ -886,6 +886,35 @@ __device__ __forceinline__ bool ray_needs_box32_ch(const RayState<D>& r,
   return !(d2 >= r.rb32);                        // inside sphere + band (or no sphere)
 }
 
+// ray_needs_box32_ch plus the sphere-distance term d2 (child ordering).
+template <int D>
+__device__ __forceinline__ bool ray_needs_box32_ch_d2(const RayState<D>& r,
+                                                      const float* __restrict__ box, float& d2) {
+  constexpr int BS = box32_stride(D);
+  float v[BS];
+  const float4* b4 = reinterpret_cast<const float4*>(box);
+#pragma unroll
+  for (int k = 0; k < BS / 4; ++k) {
+    const float4 w = __ldg(b4 + k);
+    v[4 * k] = w.x;
+    v[4 * k + 1] = w.y;
+    v[4 * k + 2] = w.z;
+    v[4 * k + 3] = w.w;
+  }
+  float umax = 0.0f;
+  d2 = 0.0f;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    umax = fmaf(r.u32[k], v[k], umax);
+    umax = fmaf(fabsf(r.u32[k]), v[D + k], umax);
+    const float zc = -0.5f * r.z32[k];
+    const float e = fmaxf(fabsf(zc - v[k]) - v[D + k] - r.del32, 0.0f);
+    d2 = fmaf(e, e, d2);
+  }
+  if (umax + r.bsl32 <= r.thr32) return false;
+  return !(d2 >= r.rb32);
+}
+
 template <int D, bool F32, bool CH = false>
 __device__ __forceinline__ bool ray_needs(const RayState<D>& r, const double* __restrict__ box64,
                                           const float* __restrict__ box32, int64_t b) {
@@ -1068,6 +1097,31 @@ struct TreeCursor {
       }
       const int l = 2 * node + 1, r = 2 * node + 2;
       const int2 rl = __ldg(node_range + l), rr = __ldg(node_range + r);
+#ifndef VR_NEAR_ORDER_MAX_D  // tuning knob: 0 restores start-tile-first everywhere
+#define VR_NEAR_ORDER_MAX_D 6
+#endif
+      if constexpr (F32 && CH && R == 1 && D <= VR_NEAR_ORDER_MAX_D) {
+        // nearer child first, by a vote of the lanes that need both (config
+        // 2: 3,163 -> 2,971 pairs per ray, kernel 2.435 -> 2.40 ms; at d = 8
+        // the rare-path entries grow 19% for 2% fewer pairs, so it stops at
+        // d = 6)
+        float dl, dr;
+        const bool al = ray_needs_box32_ch_d2<D>(ray[0], node_box32 + (int64_t)l * box32_stride(D), dl);
+        const bool ar = ray_needs_box32_ch_d2<D>(ray[0], node_box32 + (int64_t)r * box32_stride(D), dr);
+        tests += 2;
+        const unsigned nl = __ballot_sync(0xffffffffu, al), nr = __ballot_sync(0xffffffffu, ar);
+        const unsigned both = __ballot_sync(0xffffffffu, al && ar);
+        const unsigned pl = __ballot_sync(0xffffffffu, al && ar && dl <= dr);
+        const bool left_first = both ? 2 * __popc(pl) >= __popc(both) : st < rl.y;
+        if (left_first) {
+          if (nr) push(r, rr, nr);
+          if (nl) push(l, rl, nl);
+        } else {
+          if (nl) push(l, rl, nl);
+          if (nr) push(r, rr, nr);
+        }
+        continue;
+      }
       const unsigned nl = warp_needs(ray, node_box, node_box32, l);
       const unsigned nr = warp_needs(ray, node_box, node_box32, r);
       // the child holding the warp's start tile first (kd index order is
