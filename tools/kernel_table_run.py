@@ -1,7 +1,9 @@
 """Workload for the per-kernel ncu table (tools/kernel_table.py): one pass of
 each config's device path -- config 2 (1e6 descent-vertex rays, N=20k, d=6),
-config 4 (MC, 1e5 cells x 1000 rays, d=4), config 5 (L=5 balls around 10k
-seeds, N=1e6, d=8).  Run under ncu with -k regex:^k_ (our kernels only)."""
+config 4 (MC, 1e5 cells x 1000 rays, d=4), config 1 (full diagram, N=1000,
+d=3: the persistent small-level kernel), config 3 (full diagram, N=1e4,
+d=5), config 5 (L=5 balls around 10k seeds, N=1e6, d=8).  Run under ncu
+with -k regex:^k_ (our kernels only)."""
 import os
 import sys
 
@@ -37,6 +39,24 @@ ns4.prune_index()
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_push("config4")
 res = vb.mc_cells(ns4, np.arange(100000), 1000, seed=0)
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_pop()
+
+pts1 = np.random.default_rng(0).random((1000, 3))
+ns1 = vb.build_node_set(pts1)
+vb.voronoi_graph(ns1, seed=0)
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_push("config1")
+vb.voronoi_graph(ns1, seed=0)
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_pop()
+
+pts3 = np.random.default_rng(0).standard_normal((10000, 5))
+ns3 = vb.build_node_set(pts3)
+ns3.prune_index()
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_push("config3")
+vb.voronoi_graph(ns3, seed=0)
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_pop()
 
