@@ -499,7 +499,9 @@ typedef struct vr_trav_state {
   int64_t nv, nb, e_ub;  /* vertices, boundary rays, edge incidences so far */
   int64_t f0, f1;        /* frontier: vertex ids [f0, f1) */
   int32_t level;         /* level to run next */
-  int32_t phase;         /* 0: level not started, 1: cast done, finalize pending */
+  int32_t phase;         /* 0: level not started, 2: open step done (its result is
+                            the workspace prefix: grow the workspace keeping its
+                            contents), 1: cast done, finalize pending */
   int64_t pending_rays;
   int64_t n_new, n_esc, n_degenerate, n_bad, overflow;  /* last cast */
   int64_t rays;          /* edge raycasts so far */

@@ -467,13 +467,17 @@ extern "C" int vr_trav_run(const vr_traverse_tables* tab, vr_trav_state* S, cons
         return VR_OK;
       }
       S->pending_rays = R;
+      // the open result (mask, counts, offsets: the workspace prefix) stays
+      // valid across capacity returns: growing the tables does not change an
+      // edge count, and the caller keeps the prefix when the workspace grows
+      // (re-opening the last config-5 level cost ~17 ms per return)
+      S->phase = 2;
     }
     RunPlan p;
     if ((s = run_plan(F, R, n_gen, d, p))) return s;
     if (workspace_bytes < (int64_t)p.total) {
       S->need = VR_RUN_NEED_WORKSPACE;
       S->need_amount = (int64_t)p.total;
-      S->phase = 0;  // the open step is redone with the grown workspace
       return VR_OK;
     }
     // the open step's buffers sit at the same offsets in both plans
@@ -491,7 +495,7 @@ extern "C" int vr_trav_run(const vr_traverse_tables* tab, vr_trav_state* S, cons
     int64_t* noff = reinterpret_cast<int64_t*>(W + p.o_noff);
     int64_t* eoff = reinterpret_cast<int64_t*>(W + p.o_eoff);
     int32_t* bad = reinterpret_cast<int32_t*>(W + p.o_bad);
-    if (S->phase == 0) {
+    if (S->phase == 2) {
       // capacity for up to R new vertices (arrays; vertex table at load <= 0.5)
       // and their edges (edge table at load <= 0.5 of the incidence count)
       if (S->nv + R > S->vcap_arrays || 2 * (S->nv + R) > tab->vcap) {

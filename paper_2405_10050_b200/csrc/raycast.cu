@@ -41,6 +41,12 @@ int vr::sweep_mode() {
   return e ? std::atoi(e) : 0;
 }
 
+// mma.sync sweep (k_raycast_hsweep, d <= 6): VR_HSWEEP=1 / 0 (read per launch).
+int vr::hsweep_mode() {
+  const char* e = std::getenv("VR_HSWEEP");
+  return e ? std::atoi(e) : 0;
+}
+
 extern "C" int vr_abi_version(void) { return 5; }
 
 extern "C" const char* vr_status_string(int status) {

@@ -1413,6 +1413,112 @@ __device__ __forceinline__ void screen_tile_mma(RayState<D>& r, const double* ti
   if (__any_sync(0xffffffffu, r.nupd != nupd0)) mma_store_a<D>(r, sA);
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core sweep on the warp path (k_raycast_hsweep, d <= 6): every
+// generator screened, no kd walk.  NW warps x 32 rays per CTA share a
+// STAGES-deep ring of TC-candidate B blocks (mma.sync fragment layout,
+// vr_pack_records_mma) filled by TMA bulk copies; the last warp to release
+// a stage issues its refill, so no warp waits for another.  Each 64-candidate
+// tile goes through screen_tile_mma (16 HMMA + one OR vote in the common
+// no-hit case; the ballot routing, halfspace product and fp64 rare path on a
+// hit), so results are bitwise the pruned kernel's.  Blocks are visited in a
+// spiral around the CTA's home block (kd order), so spheres shrink early.
+// ---------------------------------------------------------------------------
+template <int D, int NW, int STAGES, int TC, int MINB, class Src>
+__global__ void __launch_bounds__(NW * 32, MINB)
+    k_raycast_hsweep(Src src, int64_t n_rays, const double* __restrict__ crec,
+                     const float* __restrict__ crecB, const float* __restrict__ crec32s,
+                     const int32_t* __restrict__ perm, const int32_t* __restrict__ inv_perm,
+                     int64_t n_rows, Frame fr, RayOut out, unsigned long long* __restrict__ work) {
+  constexpr int S = rec_stride(D);
+  constexpr int KS = mma_ksteps(D);
+  constexpr int AR = mma_arow(D);
+  constexpr int BLK = TC * 8 * KS;  // floats per stage block
+  static_assert(TC % 64 == 0, "whole 64-candidate tiles per stage");
+  extern __shared__ __align__(128) float sBdyn[];  // STAGES x BLK floats (dynamic)
+  float (*sB)[BLK] = reinterpret_cast<float (*)[BLK]>(sBdyn);
+  __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ int released[STAGES];
+  __shared__ float sA[NW][32 * AR];
+  __shared__ float sU[NW][32 * AR];
+  __shared__ int64_t home_s;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t nblk = n_rows / TC;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      released[i] = 0;
+    }
+    fence_mbar_init();
+    home_s = (int64_t)inv_perm[src.gen((int64_t)blockIdx.x * NW * 32)] / TC;
+  }
+  __syncthreads();
+  const int64_t home = home_s;
+  auto block_of = [&](int64_t j) -> int64_t {  // home, +1, -1, +2, -2, ...
+    const int64_t off = (j & 1) ? (j + 1) >> 1 : -(j >> 1);
+    int64_t b = home + off;
+    if (b >= nblk) b -= nblk;
+    if (b < 0) b += nblk;
+    return b;
+  };
+  auto issue = [&](int64_t j) {
+    const int st = (int)(j % STAGES);
+    mbar_arrive_expect_tx(&full[st], BLK * 4);
+    bulk_g2s(sB[st], crecB + block_of(j) * BLK, BLK * 4, &full[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t j = 0; j < STAGES && j < nblk; ++j) issue(j);
+  const int64_t k = ((int64_t)blockIdx.x * NW + w) * 32 + lane;
+  RayState<D> ray;
+  const bool act = k < n_rays && src.load(k, ray, fr);
+  if (!act) init_padding_lane<D, 1>(ray);
+  if (act) {
+    ray.gk = inv_perm[src.gen(k)];
+    const int64_t so = (int64_t)ray.gk / 64;
+    seed_tile32<D>(ray, crec32s + so * 64 * rec32_stride(D), crec + so * 64 * S, (int)(so * 64), fr);
+  }
+  mma_store_a<D>(ray, sA[w]);
+  mma_store_u<D>(ray, fr, sU[w]);
+  WarpCounters wc;
+  for (int64_t j = 0; j < nblk; ++j) {
+    const int st = (int)(j % STAGES);
+    mbar_wait(&full[st], (uint32_t)((j / STAGES) & 1));
+    const int64_t b = block_of(j);
+#pragma unroll 1
+    for (int sub = 0; sub < TC / 64; ++sub) {
+      const int gbase = (int)(b * TC + sub * 64);
+      screen_tile_mma<D>(ray, crec + (int64_t)gbase * S, sB[st] + sub * 512 * KS, gbase, fr,
+                         work ? &wc : nullptr, sA[w], sU[w]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      // the last warp done with this stage refills it
+      if (atomicAdd(&released[st], 1) == NW - 1) {
+        released[st] = 0;
+        if (j + STAGES < nblk) issue(j + STAGES);
+      }
+    }
+  }
+  if (act) ray_store<D>(ray, src.id(k), perm, out);
+  if (work) {
+    unsigned long long up = act ? ray.nupd : 0, a = act ? 1 : 0;
+    unsigned long long e = wc.entries;
+    for (int off = 16; off > 0; off >>= 1) {
+      up += __shfl_xor_sync(0xffffffffu, up, off);
+      a += __shfl_xor_sync(0xffffffffu, a, off);
+      e += __shfl_xor_sync(0xffffffffu, e, off);
+    }
+    if (lane == 0) {
+      atomicAdd(work, a * (unsigned long long)n_rows);
+      atomicAdd(work + 1, wc.rare_blocks);
+      atomicAdd(work + 2, wc.rare_iters);
+      atomicAdd(work + 3, e);
+      atomicAdd(work + 4, up);
+    }
+  }
+}
+
 // One warp per CTA (warps finish at very different times; a freed slot is
 // refilled immediately).  The warp's next needed tile is fetched by TMA into
 // the other half of a two-tile shared-memory buffer while the current tile
@@ -2258,6 +2364,35 @@ int launch_coop(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Fra
 }
 
 int coop_mode();
+int hsweep_mode();  // VR_HSWEEP=1 / 0: the mma.sync sweep on / off (default: auto)
+
+template <int D, class Src>
+int launch_hsweep(const Src& src, int64_t n_rays, const PrunedIndex& ix, const Frame& fr,
+                  const RayOut& out, cudaStream_t st, unsigned long long* work) {
+  if constexpr (mma_ksteps(D) == 1 && PRUNE_TILE == 64) {
+// measured (config 2): 4 warps x 4 stages 3.95 ms; 4 x 6 4.48 ms; 8 x 8
+// 4.11 ms; 8 x 12 5.84 ms
+#ifndef VR_HSWEEP_NW
+#define VR_HSWEEP_NW 4
+#endif
+#ifndef VR_HSWEEP_MINB
+#define VR_HSWEEP_MINB 4
+#endif
+#ifndef VR_HSWEEP_STAGES
+#define VR_HSWEEP_STAGES 4
+#endif
+    constexpr int NW = VR_HSWEEP_NW, STAGES = VR_HSWEEP_STAGES, TC = 256;
+    const int64_t per = (int64_t)NW * 32;
+    const int64_t grid = (n_rays + per - 1) / per;
+    auto kern = k_raycast_hsweep<D, NW, STAGES, TC, VR_HSWEEP_MINB, Src>;
+    const int smem = STAGES * TC * 8 * mma_ksteps(D) * 4;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(src, n_rays, ix.crec, ix.crecB, ix.crec32s, ix.perm,
+                                                ix.inv_perm, rec_rows(ix.n), fr, out, work);
+    VR_RETURN_LAUNCH();
+  }
+  return VR_EINVAL;
+}
 
 // Host-side view of the C-ABI index -> kernel parameters.
 inline PrunedIndex pruned_index_from(const vr_prune_index* ix, bool f32) {
@@ -2299,6 +2434,10 @@ int launch_raycast_pruned(const Src& src, int64_t n_rays, const PrunedIndex& ix,
   if constexpr (PRUNE_TILE == 64 && D <= 6) {
     if (ix.crec32 && ix.crecU && ix.crec32s && sweep_mode() > 0)
       return launch_sweep<D>(src, n_rays, ix, fr, out, st, work);
+  }
+  if constexpr (mma_ksteps(D) == 1 && PRUNE_TILE == 64) {
+    if (ix.crec32 && ix.crecB && ix.crec32s && rec_rows(ix.n) % 256 == 0 && hsweep_mode() > 0)
+      return launch_hsweep<D>(src, n_rays, ix, fr, out, st, work);
   }
   const int cm = coop_mode();
   const bool coop = cm > 0 || (cm < 0 && (n_rays < 8192 || (D >= 7 && n_rays * 64 < ix.n)));

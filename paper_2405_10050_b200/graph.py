@@ -681,7 +681,11 @@ class DeviceTraversal:
             if need == RUN_DONE:
                 break
             if need == RUN_NEED_WS:
+                old = scratch
                 scratch = ws.get("run_scratch", (int(1.25 * amt) + 4096,), torch.uint8, self.dev)
+                if old is not None and int(S.phase) == 2 and scratch.data_ptr() != old.data_ptr():
+                    # the level's open step is done: its result is the prefix
+                    scratch[:old.numel()].copy_(old)
                 wsb = scratch.numel()
             elif need == RUN_NEED_V:
                 self.nv = int(S.nv)

@@ -234,10 +234,11 @@ def test_pruned_equals_exhaustive(d):
 @pytest.mark.gpu
 @pytest.mark.parametrize("d", [5, 6])
 def test_sweep_kernel_matches_exhaustive(d, monkeypatch):
-    """The opt-in tcgen05 sweep (VR_SWEEP=1: every generator screened by one
-    M=128 x N=128 tf32 MMA per step, TMEM double-buffered) is bitwise equal to
-    the exhaustive fp64 kernel on generator-start and edge rays, including
-    whatever rays start without a seed sphere (halfspace row)."""
+    """The opt-in sweeps -- tcgen05 (VR_SWEEP=1: every generator screened by
+    one M=128 x N=128 tf32 MMA per step, TMEM double-buffered) and mma.sync
+    (VR_HSWEEP=1: 128-ray CTAs over a TMA ring of 256-candidate blocks) --
+    are bitwise equal to the exhaustive fp64 kernel on generator-start and
+    edge rays, including whatever rays start without a seed sphere."""
     import torch
     rng = np.random.default_rng(900 + d)
     n = 6000
@@ -254,15 +255,18 @@ def test_sweep_kernel_matches_exhaustive(d, monkeypatch):
     eta = np.array([[s[j] for j in range(d + 1) if j != k] for s in sig for k in range(d + 1)])
     cases = ((pts[g], u, g[:, None]), (xs, uu, eta))
     refs = [vb.raycast_batch(ns, *c, mode="exhaustive", screen="fp64").to_host() for c in cases]
-    monkeypatch.setenv("VR_SWEEP", "1")
-    work = torch.zeros(16, dtype=torch.int64, device="cuda")
-    for c, a in zip(cases, refs):
-        b = vb.raycast_batch(ns, *c, mode="pruned", work=work).to_host()
-        for x, y in zip(a, b):
-            assert np.array_equal(x, y, equal_nan=True)
-    # the sweep screened every record row for every ray
     rows = vb._lib.record_rows(n)
-    assert int(work[0]) == rows * (m + len(xs))
+    # the tcgen05 sweep (VR_SWEEP) and the mma.sync sweep (VR_HSWEEP)
+    for var in ("VR_SWEEP", "VR_HSWEEP"):
+        monkeypatch.setenv(var, "1")
+        work = torch.zeros(16, dtype=torch.int64, device="cuda")
+        for c, a in zip(cases, refs):
+            b = vb.raycast_batch(ns, *c, mode="pruned", work=work).to_host()
+            for x, y in zip(a, b):
+                assert np.array_equal(x, y, equal_nan=True), var
+        # the sweep screened every record row for every ray
+        assert int(work[0]) == rows * (m + len(xs)), var
+        monkeypatch.delenv(var)
 
 
 _COOP_SCRIPT = r"""

@@ -33,7 +33,9 @@ def main(n=int(os.environ.get("NRAYS", "1000000"))):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         work = torch.zeros(16, dtype=torch.int64, device=dev)
         flush.fill_(i)
+        torch.cuda.nvtx.range_push("ab")
         res = vb.raycast_batch(ns, xd, ud, gd, workspace=ws, events=ev, mode="pruned", work=work)
+        torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
         if i >= 3:
             ts.append(ev[0].elapsed_time(ev[2]))
@@ -42,7 +44,7 @@ def main(n=int(os.environ.get("NRAYS", "1000000"))):
     ex = vb.raycast_batch(ns, xd, ud, gd, mode="exhaustive", screen="fp64")
     same = all(torch.equal(getattr(res, f), getattr(ex, f)) for f in ("idx", "flag")) and \
         torch.equal(torch.nan_to_num(res.t, posinf=1e300), torch.nan_to_num(ex.t, posinf=1e300))
-    tag = f"VR_SWEEP={os.environ.get('VR_SWEEP', '-')} VR_MMA={os.environ.get('VR_MMA', '-')}"
+    tag = f"VR_SWEEP={os.environ.get('VR_SWEEP', '-')} VR_HSWEEP={os.environ.get('VR_HSWEEP', '-')}"
     print(f"{tag}: step {np.median(ts):.3f} ms kernel {np.median(ks):.3f} ms  "
           f"pairs/ray {wk[0] / n:.0f} rare blocks/ray {wk[1] / n:.2f} entries/ray {wk[3] / n:.2f} "
           f"updates/ray {wk[4] / n:.2f} degenerate {int((res.flag == 3).sum())} "
