@@ -345,6 +345,7 @@ int trav_run_small(const vr_traverse_tables* tab, vr_trav_state* S, const double
                    const vr_prune_index* ix, int32_t last_level, int64_t* level_new,
                    int64_t level_cap, uint64_t* work, void* workspace, int64_t workspace_bytes,
                    cudaStream_t st, int* handled, int32_t* bail_code);
+int64_t small_rmax(int d);  // rays per level the persistent kernel takes
 }
 
 namespace {
@@ -426,7 +427,10 @@ extern "C" int vr_trav_run(const vr_traverse_tables* tab, vr_trav_state* S, cons
     if (S->level >= level_cap) return VR_ECAPACITY;
     // small levels: the persistent kernel (level_small.cu) runs as many as
     // stay small in one launch
-    if (S->phase == 0 && F <= 8192 && S->level != host_level && small_mode()) {
+    // (expected rays ~ F (d+1) / 2: about half the edges of a frontier
+    // vertex are open; larger levels skip the attempt)
+    if (S->phase == 0 && S->level != host_level && small_mode() &&
+        F * (d + 1) <= 2 * vr::small_rmax(d)) {
       int handled = 0;
       int32_t bail = 0;
       const int s0 = vr::trav_run_small(tab, S, rec, n_gen, d, sqmax, s32, ix, last_level,

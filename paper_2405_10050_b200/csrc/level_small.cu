@@ -266,20 +266,40 @@ SmallPlan small_plan(int64_t F, int64_t R, int d, int64_t level_cap) {
   return p;
 }
 
+// Resident CTAs of the cooperative grid (one per SM, two if registers allow).
+template <int D>
+int small_grid() {
+  static int grid = -1;
+  if (grid < 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_trav_small<D>, SM_NT, 0);
+    grid = sms * (per < 2 ? per : 2);
+  }
+  return grid;
+}
+
+int small_grid_d(int d) {
+  switch (d) {
+    case 2: return small_grid<2>();
+    case 3: return small_grid<3>();
+    case 4: return small_grid<4>();
+    case 5: return small_grid<5>();
+    case 6: return small_grid<6>();
+    case 7: return small_grid<7>();
+    case 8: return small_grid<8>();
+    default: return 0;
+  }
+}
+
 template <int D>
 int launch_small(const Tables& t, const double* rec, int64_t n_gen, const PrunedIndex& pi,
                  const Frame& fr, const SmallBufs& B, int32_t last_level, int64_t level_cap,
                  int64_t fmax, int64_t rmax, unsigned long long* work, cudaStream_t st) {
   auto kern = k_trav_small<D>;
-  static int grid = 0;
-  if (!grid) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, SM_NT, 0);
-    grid = sms * (per < 2 ? per : 2);
-    if (grid <= 0) return VR_EINVAL;
-  }
+  const int grid = small_grid<D>();
+  if (grid <= 0) return VR_EINVAL;
   Tables tt = t;
   const double* r = rec;
   int64_t ng = n_gen;
@@ -298,6 +318,8 @@ int launch_small(const Tables& t, const double* rec, int64_t n_gen, const Pruned
 
 namespace vr {
 
+int64_t small_rmax(int d) { return 2 * (int64_t)small_grid_d(d) * SM_NW; }
+
 // Levels of the traversal in the persistent kernel while they are small;
 // returns VR_OK with *handled = 1 when it ran (S updated; S->need tells the
 // caller what happened: NEED_BAIL -> run the current level on the host path).
@@ -308,8 +330,13 @@ int trav_run_small(const vr_traverse_tables* tab, vr_trav_state* S, const double
                    cudaStream_t st, int* handled, int32_t* bail_code) {
   *handled = 0;
   *bail_code = NEED_BAIL;
-  constexpr int64_t FMAX = 8192, RMAX = 8192;
   if (!s32 || !ix->wide_box32 || ix->wide_levels < 2 || d > 8) return VR_OK;
+  // The kernel's register footprint (the union of its phases) allows ~8
+  // warps per SM, so a level's rays run in ceil(R / warps) rounds of one
+  // warp per ray: levels of up to two rounds stay here (config 3's levels of
+  // 3-7 rounds ran 5 ms slower in it than on the host path).
+  const int64_t RMAX = small_rmax(d), FMAX = RMAX;
+  if (RMAX <= 0) return VR_OK;
   const SmallPlan P = small_plan(FMAX, RMAX, d, level_cap);
   if (!workspace || workspace_bytes < (int64_t)P.total) {
     S->need = VR_RUN_NEED_WORKSPACE;
