@@ -49,7 +49,7 @@ def main(frac=0.25):
     g = eta[:, 0].to(torch.int64)
     o = coherent_order(ix, eta, uu).to(torch.int64)
     CH = 1024
-    tot = {gs: 0.0 for gs in (128, 32, 1)}
+    tot = {gs: 0.0 for gs in (128, 32, 16, 8, 1)}
     starts = np.linspace(0, n - CH, 64).astype(np.int64) // 32 * 32
     for lo in starts:
         s_ = o[lo:lo + CH]
