@@ -51,7 +51,7 @@ enum vr_cell_status {
   VR_CELL_OVERFLOW = 3     /* more distinct hit faces than area slots          */
 };
 
-int vr_abi_version(void); /* 5 */
+int vr_abi_version(void); /* 6 */
 const char* vr_status_string(int status);
 
 /* Record stride (doubles) of one packed generator for dimension d:
@@ -619,6 +619,22 @@ int vr_trav_boundary(int d, const int32_t* esc_flag, const int64_t* esc_off,
 /* flag[h] = (state[h] == 2), for compaction of a table. */
 int vr_trav_published(const int32_t* state, int64_t cap, int32_t* flag,
                       void* stream);
+
+/* Edge-table compaction in two passes (slot order, the same order as
+ * vr_trav_published + prefix sum + vr_trav_edge_compact):
+ * vr_trav_edges_count: published slots per chunk of 4096, exclusive offsets
+ *   in chunk_off (ceil(ecap / 4096) + 1 int64; the last entry is the total),
+ *   *n_edges (host) = the total; ends with a stream synchronisation.  NULL
+ *   workspace: *workspace_bytes = the scan scratch needed.
+ * vr_trav_edges_compact: the slot of every published row (out_slot,
+ *   n_edges int64 scratch), then keys (n_edges, d) and counts in slot
+ *   order. */
+int vr_trav_edges_count(const vr_traverse_tables* tab, int64_t* chunk_off,
+                        int64_t* n_edges, void* workspace, int64_t* workspace_bytes,
+                        void* stream);
+int vr_trav_edges_compact(const vr_traverse_tables* tab, int d,
+                          const int64_t* chunk_off, int64_t n_edges, int64_t* out_slot,
+                          int32_t* out_keys, int32_t* out_count, void* stream);
 
 /* Compact the edge table (published slots, exclusive offsets `off`). */
 int vr_trav_edge_compact(const vr_traverse_tables* tab, int d,

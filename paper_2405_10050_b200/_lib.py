@@ -15,7 +15,7 @@ import torch
 from ._build import LIB_PATH
 from .errors import DeviceUnavailable
 
-ABI_VERSION = 5  # vr_abi_version() of the library this package expects
+ABI_VERSION = 6  # vr_abi_version() of the library this package expects
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -102,6 +102,8 @@ _SIGNATURES = {
     "vr_trav_boundary": [_int, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp],
     "vr_trav_published": [_vp, _i64, _vp, _vp],
     "vr_trav_edge_compact": [_vp, _int, _vp, _vp, _vp, _vp],
+    "vr_trav_edges_count": [_vp, _vp, _vp, _vp, _vp, _vp],
+    "vr_trav_edges_compact": [_vp, _int, _vp, _i64, _vp, _vp, _vp, _vp],
 }
 
 # Symbols declared in include/voronray_b200.h that the .so must export.

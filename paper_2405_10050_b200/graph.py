@@ -784,18 +784,26 @@ class DeviceTraversal:
         return n_new
 
     def edges(self):
-        """Published edge keys and counts (device tensors, hash-table order)."""
-        flag = torch.empty(self.ecap, dtype=torch.int32, device=self.dev)
-        _lib.check(self.L.vr_trav_published(_lib.ptr(self.estate), self.ecap, _lib.ptr(flag),
-                                            self._sh()), "published")
-        off, inc = _excl_cumsum(flag)
-        ne = int(inc[-1].item())
-        keys = torch.empty((ne, self.d), dtype=torch.int32, device=self.dev)
-        cnt = torch.empty(ne, dtype=torch.int32, device=self.dev)
+        """Published edge keys and counts (device tensors, hash-table order):
+        two native passes over the slot states (vr_trav_edges_count /
+        vr_trav_edges_compact)."""
         T = self.tables()
-        _lib.check(self.L.vr_trav_edge_compact(ctypes.byref(T), self.d, _lib.ptr(off),
-                                               _lib.ptr(keys), _lib.ptr(cnt), self._sh()),
-                   "edge_compact")
+        nbytes = ctypes.c_int64(0)
+        _lib.check(self.L.vr_trav_edges_count(ctypes.byref(T), None, None, None,
+                                              ctypes.byref(nbytes), None), "edges_count (size)")
+        nc = (self.ecap + 4095) // 4096
+        off = torch.empty(nc + 1, dtype=torch.int64, device=self.dev)
+        tmp = torch.empty(max(1, nbytes.value), dtype=torch.uint8, device=self.dev)
+        ne = ctypes.c_int64(0)
+        _lib.check(self.L.vr_trav_edges_count(ctypes.byref(T), _lib.ptr(off), ctypes.byref(ne),
+                                              _lib.ptr(tmp), ctypes.byref(nbytes), self._sh()),
+                   "edges_count")
+        keys = torch.empty((ne.value, self.d), dtype=torch.int32, device=self.dev)
+        cnt = torch.empty(ne.value, dtype=torch.int32, device=self.dev)
+        slots = torch.empty(max(1, ne.value), dtype=torch.int64, device=self.dev)
+        _lib.check(self.L.vr_trav_edges_compact(ctypes.byref(T), self.d, _lib.ptr(off), ne.value,
+                                                _lib.ptr(slots), _lib.ptr(keys), _lib.ptr(cnt),
+                                                self._sh()), "edges_compact")
         return keys, cnt  # hash order; Mesh sorts lexicographically on materialisation
 
 
