@@ -10,6 +10,8 @@
 // normals with NumPy's own ziggurat sampler (random_standard_normal from
 // NumPy's static libnpyrandom, linked in), so every value is bit-identical
 // to the Generator's (tests/test_host.py checks it against numpy).
+#include <thread>
+#include <vector>
 #include <cstdint>
 #include <cstring>
 
@@ -158,16 +160,35 @@ extern "C" int vr_host_streams(uint64_t seed, uint64_t tag, const int64_t* index
 // For each listed stream (rows[i], or i when rows == NULL), `count` standard
 // normals in Generator.standard_normal order into out[i * count ..]; the
 // stream states advance in place.
+// Streams are independent, so large batches split over host threads (config
+// 5's 10,000 descent streams x 88 normals: ~8 ms on one core).  Each stream
+// is drawn by exactly one thread, in its own order: bitwise the serial draw.
 extern "C" int vr_host_normals(uint64_t* state, const int64_t* rows, int64_t n, int64_t count,
                                double* out) {
   if (n < 0 || count < 0 || (n > 0 && (!state || !out))) return VR_EINVAL;
-  for (int64_t i = 0; i < n; ++i) {
-    uint64_t* st = state + 4 * (rows ? rows[i] : i);
-    Pcg g = unpack(st);
-    bitgen_t bg{&g, pcg_next64, pcg_next32, pcg_next_double, pcg_next64};
-    double* o = out + i * count;
-    for (int64_t k = 0; k < count; ++k) o[k] = random_standard_normal(&bg);
-    pack(g, st);
+  auto work = [=](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) {
+      uint64_t* st = state + 4 * (rows ? rows[i] : i);
+      Pcg g = unpack(st);
+      bitgen_t bg{&g, pcg_next64, pcg_next32, pcg_next_double, pcg_next64};
+      double* o = out + i * count;
+      for (int64_t k = 0; k < count; ++k) o[k] = random_standard_normal(&bg);
+      pack(g, st);
+    }
+  };
+  const int64_t total = n * count;
+  unsigned hw = std::thread::hardware_concurrency();
+  int64_t nt = total >= (1 << 16) ? (int64_t)(hw ? hw : 1) : 1;
+  if (nt > 16) nt = 16;
+  if (nt > n) nt = n;
+  if (nt <= 1) {
+    work(0, n);
+    return VR_OK;
   }
+  std::vector<std::thread> th;
+  th.reserve((size_t)nt - 1);
+  for (int64_t t = 1; t < nt; ++t) th.emplace_back(work, n * t / nt, n * (t + 1) / nt);
+  work(0, n / nt);
+  for (auto& x : th) x.join();
   return VR_OK;
 }

@@ -272,7 +272,7 @@ def descent_batch(ns: NodeSet, starts, seed: int = 0, stats: RaycastStats = None
             if (fails[grp[esc]] >= DESCENT_RETRIES).any():
                 a = grp[esc][np.argmax(fails[grp[esc]] >= DESCENT_RETRIES)]
                 raise RetryExhausted(f"descent from node {int(starts[a])} stuck at level {kk}")
-            still.extend(grp[esc].tolist())
+            still.append(grp[esc])
             ok = ~esc
             g_ok = grp[ok]
             if g_ok.size:
@@ -281,10 +281,9 @@ def descent_batch(ns: NodeSet, starts, seed: int = 0, stats: RaycastStats = None
                 k[g_ok] = kk + 1
                 rr[g_ok] = rp[ok]
                 fails[g_ok] = 0
-                cont = g_ok if kk + 1 < d + 1 else g_ok[:0]
-                if cont.size:
-                    still.extend(cont.tolist())
-        active = np.array(sorted(still), dtype=np.int64)
+                if kk + 1 < d + 1:
+                    still.append(g_ok)
+        active = np.sort(np.concatenate(still)) if still else np.zeros(0, dtype=np.int64)
     return sig.astype(np.int32), rr
 
 

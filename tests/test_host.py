@@ -268,6 +268,20 @@ def test_host_streams_are_numpy_generators():
                                      out.ctypes.data) == 0
             for k, r in enumerate(rows):
                 assert np.array_equal(out[k], gens[r].standard_normal(count))
+    # a batch large enough for the multi-threaded draw (streams split over
+    # host threads): bitwise the numpy Generators, state advanced per stream
+    big = np.arange(3000, dtype=np.int64) * 7 + 11
+    st = np.zeros((big.size, 4), dtype=np.uint64)
+    assert L.vr_host_streams(5, 0, big.ctypes.data, big.size, st.ctypes.data) == 0
+    out = np.zeros((big.size, 40))
+    assert L.vr_host_normals(st.ctypes.data, None, big.size, 40, out.ctypes.data) == 0
+    out2 = np.zeros((big.size, 3))
+    assert L.vr_host_normals(st.ctypes.data, None, big.size, 3, out2.ctypes.data) == 0
+    for k in (0, 1, 1499, 2998, 2999):
+        g = np.random.Generator(np.random.PCG64(np.random.SeedSequence(entropy=5,
+                                                                       spawn_key=(0, int(big[k])))))
+        assert np.array_equal(out[k], g.standard_normal(40))
+        assert np.array_equal(out2[k], g.standard_normal(3))
     # seeds outside uint64 keep the numpy Generators (same streams)
     from paper_2405_10050_b200.graph import _Draws
     dr = _Draws(None, 2 ** 70, np.array([3, 4]), 3, block=2)
