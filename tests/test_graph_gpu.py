@@ -282,6 +282,29 @@ def test_native_level_driver_matches_python_levels(tmp_path):
             assert np.array_equal(res["1"][k], res[other][k]), (other, k)
 
 
+@pytest.mark.parametrize("d", [2, 3, 4, 5, 6])
+def test_small_level_kernel_fuzz(d, monkeypatch):
+    """The persistent small-level kernel (default) and the host-driven level
+    loop (VR_SMALL_LEVELS=0, read per call) give bitwise-identical meshes on
+    random inputs of several sizes and distributions, including clustered
+    points (uneven levels) and sizes whose levels cross the kernel's limit."""
+    rng = np.random.default_rng(4200 + d)
+    cases = [rng.random((60, d)), rng.standard_normal((400, d)),
+             np.vstack([rng.normal(0.0, 0.05, (300, d)), rng.random((300, d))])]
+    if d <= 4:
+        cases.append(rng.random((3000, d)))
+    for pts in cases:
+        ns = vb.build_node_set(pts)
+        monkeypatch.setenv("VR_SMALL_LEVELS", "1")
+        a, ia = vb.voronoi_graph(ns, seed=3, return_info=True)
+        monkeypatch.setenv("VR_SMALL_LEVELS", "0")
+        b, ib = vb.voronoi_graph(ns, seed=3, return_info=True)
+        assert ia["levels"] == ib["levels"]
+        xa, xb = a.arrays(), b.arrays()
+        for k in ("sigma", "r", "edge_key", "edge_count", "boundary_sigma", "boundary_u"):
+            assert np.array_equal(xa[k], xb[k]), (len(pts), k)
+
+
 _SHARDED_SCRIPT = r"""
 import os, sys, numpy as np, torch, torch.distributed as dist
 sys.path.insert(0, sys.argv[1])
