@@ -344,16 +344,71 @@ def raycast_incircle(ns: NodeSet, q: RayQuery, stats: RaycastStats = None,
     if stats is None:
         stats = RaycastStats()
     eta = tuple(int(e) for e in q.eta)
-    res = raycast_batch(ns, np.asarray(q.r, dtype=float)[None], np.asarray(q.u, dtype=float)[None],
-                        np.asarray([eta], dtype=np.int32), candidates=candidates, stats=stats)
-    idx, _, rp, flag = res.to_host()
-    f = int(flag[0])
+    if candidates is None and 1 <= len(eta) <= ns.dim:
+        i, f, rp = _single_ray(ns, q.r, q.u, eta, stats)
+    else:
+        res = raycast_batch(ns, np.asarray(q.r, dtype=float)[None],
+                            np.asarray(q.u, dtype=float)[None], np.asarray([eta], dtype=np.int32),
+                            candidates=candidates, stats=stats)
+        idx, _, rpa, flag = res.to_host()
+        i, f, rp = int(idx[0]), int(flag[0]), rpa[0]
     if f == RAY_ESCAPED:
         return None
     if f == RAY_DEGENERATE:
         raise DegenerateConfiguration(
-            f"a foreign generator lies on the circumsphere of {(*eta, int(idx[0]))}")
-    return tuple(sorted((*eta, int(idx[0])))), rp[0]
+            f"a foreign generator lies on the circumsphere of {(*eta, i)}")
+    return tuple(sorted((*eta, i))), rp
+
+
+class _SingleRay:
+    """Reused buffers of the one-ray drop-in call (raycast_incircle): the
+    inputs packed in one pinned host block and copied with one H2D, the
+    outputs (rp, t, idx, flag) views of one device block read back with one
+    D2H -- a call is the RayCast launches plus two copies and one sync, with
+    no per-call allocations (the reference's loops, descent and the DFS, call
+    it once per step)."""
+
+    def __init__(self, ns, k):
+        rec, _ = ns.device_records()
+        self.dev, d = rec.device, ns.dim
+        self.k = k
+        self.nin = 16 * d + 4 * k
+        self.nout = 8 * d + 16
+        self.h_in = torch.empty(self.nin, dtype=torch.uint8, pin_memory=True)
+        self.h_out = torch.empty(self.nout, dtype=torch.uint8, pin_memory=True)
+        self.d_in = torch.empty(self.nin, dtype=torch.uint8, device=self.dev)
+        self.d_out = torch.empty(self.nout, dtype=torch.uint8, device=self.dev)
+        hi = self.h_in.numpy()
+        self.hx = hi[:8 * d].view(np.float64)
+        self.hu = hi[8 * d:16 * d].view(np.float64)
+        self.he = hi[16 * d:].view(np.int32)
+        self.x = self.d_in[:8 * d].view(torch.float64).view(1, d)
+        self.u = self.d_in[8 * d:16 * d].view(torch.float64).view(1, d)
+        self.eta = self.d_in[16 * d:].view(torch.int32).view(1, k)
+        self.out = dict(rp=self.d_out[:8 * d].view(torch.float64).view(1, d),
+                        t=self.d_out[8 * d:8 * d + 8].view(torch.float64),
+                        idx=self.d_out[8 * d + 8:8 * d + 12].view(torch.int32),
+                        flag=self.d_out[8 * d + 12:8 * d + 13])
+        ho = self.h_out.numpy()
+        self.h_rp = ho[:8 * d].view(np.float64)
+        self.h_idx = ho[8 * d + 8:8 * d + 12].view(np.int32)
+        self.h_flag = ho[8 * d + 12:8 * d + 13]
+        self.ws = Workspace()
+
+
+def _single_ray(ns, r, u, eta, stats):
+    cache = ns.__dict__.setdefault("_single_ray_bufs", {})
+    sb = cache.get(len(eta))
+    if sb is None:
+        sb = cache[len(eta)] = _SingleRay(ns, len(eta))
+    sb.hx[:] = np.asarray(r, dtype=np.float64).ravel()
+    sb.hu[:] = np.asarray(u, dtype=np.float64).ravel()
+    sb.he[:] = eta
+    sb.d_in.copy_(sb.h_in, non_blocking=True)
+    raycast_batch(ns, sb.x, sb.u, sb.eta, out=sb.out, workspace=sb.ws, stats=stats)
+    sb.h_out.copy_(sb.d_out, non_blocking=True)
+    torch.cuda.current_stream(sb.dev).synchronize()
+    return int(sb.h_idx[0]), int(sb.h_flag[0]), sb.h_rp.copy()
 
 
 # --- host-side direction helpers (raycast.py:295-378) ----------------------
