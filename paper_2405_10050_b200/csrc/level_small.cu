@@ -17,6 +17,8 @@
 // through the device copy of vr_trav_state.
 #include <cooperative_groups.h>
 
+#include <atomic>
+
 #include "raycast_core.cuh"
 #include "trav_core.cuh"
 
@@ -266,18 +268,24 @@ SmallPlan small_plan(int64_t F, int64_t R, int d, int64_t level_cap) {
   return p;
 }
 
-// Resident CTAs of the cooperative grid (one per SM, two if registers allow).
+// Resident CTAs of the cooperative grid on the current device (one per SM,
+// two if registers allow), cached per device.
 template <int D>
 int small_grid() {
-  static int grid = -1;
-  if (grid < 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_trav_small<D>, SM_NT, 0);
-    grid = sms * (per < 2 ? per : 2);
+  constexpr int MAXDEV = 64;
+  static std::atomic<int> grid[MAXDEV];  // 0: not computed yet
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return 0;
+  if (dev < MAXDEV) {
+    const int g = grid[dev].load(std::memory_order_relaxed);
+    if (g > 0) return g;
   }
-  return grid;
+  int sms = 0, per = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_trav_small<D>, SM_NT, 0);
+  const int g = sms * (per < 2 ? per : 2);
+  if (dev < MAXDEV && g > 0) grid[dev].store(g, std::memory_order_relaxed);
+  return g;
 }
 
 int small_grid_d(int d) {
