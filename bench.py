@@ -210,6 +210,9 @@ def _median_passes(fn, passes, torch, reset=None):
     for rep in range(passes + 1):
         if reset is not None and rep:
             reset()
+        out = None  # the previous pass's result is freed first: its device
+        # blocks are what this pass's allocations reuse (otherwise two passes'
+        # tables coexist and the first timed passes pay for cudaMalloc)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         out = fn()
