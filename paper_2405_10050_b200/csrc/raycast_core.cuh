@@ -1582,7 +1582,10 @@ __global__ void __launch_bounds__(32, MINB)
     act[j] = src.load(k0 + (int64_t)j * 32, ray[j], fr);
     if (!act[j]) init_padding_lane<D, R>(ray[j]);
   }
-  if constexpr (MMA) {
+  // fp32 seed (seed_tile32) wherever the kd-ordered fp32 rows are there:
+  // the tensor-core kernel and the one-ray-per-lane FFMA2 kernel
+  constexpr bool SEED32 = MMA || (F32 && R == 1);
+  if constexpr (SEED32) {
 #pragma unroll
     for (int j = 0; j < R; ++j)
       if (act[j]) ray[j].gk = inv_perm[src.gen(k0 + (int64_t)j * 32)];
@@ -1590,12 +1593,19 @@ __global__ void __launch_bounds__(32, MINB)
   int64_t st = 0;
   if (lane == 0) st = inv_perm[src.gen(k0)] / PT;
   st = __shfl_sync(0xffffffffu, st, 0);
-  if constexpr (MMA) {
+  if constexpr (SEED32) {
     // each ray seeds on the tile of its own reference generator (sparse
     // batches, where a warp spans several generators: 64k config-2 rays
-    // 9.97 -> 7.83 ms per 1e6; dense batches unchanged)
-    const int64_t so = act[0] ? (int64_t)ray[0].gk / PT : st;
-    seed_tile32<D>(ray[0], crec32s + so * PT * rec32_stride(D), crec + so * PT * S, (int)(so * PT), fr);
+    // 9.97 -> 7.83 ms per 1e6; dense batches unchanged), division-free in
+    // fp32 with one fp64 evaluation of the winner (the fp64 seed over 64
+    // candidates was 16% of config 4's kernel samples)
+    if (crec32s) {
+      const int64_t so = act[0] ? (int64_t)ray[0].gk / PT : st;
+      seed_tile32<D>(ray[0], crec32s + so * PT * rec32_stride(D), crec + so * PT * S,
+                     (int)(so * PT), fr);
+    } else {
+      seed_tile<D, R, PT, F32>(ray, crec + st * PT * S, (int)(st * PT), fr);
+    }
   }
   else
     seed_tile<D, R, PT, F32>(ray, crec + st * PT * S, (int)(st * PT), fr);
