@@ -999,7 +999,11 @@ __device__ __forceinline__ void seed_tile32(RayState<D>& r, const float* __restr
   const int gl = r.gk - gbase;
   float nb = 1.0f, db = 0.0f;  // "t = +inf"
   int ib = -1;
-#pragma unroll 4
+#ifndef VR_SEED_UNROLL
+#define VR_SEED_UNROLL 4
+#endif
+  constexpr int SEED_UNROLL = VR_SEED_UNROLL;
+#pragma unroll SEED_UNROLL
   for (int c = 0; c < 64; ++c) {
     float xi[D];
     load_rec32<D>(tile32 + c * S32, xi);
