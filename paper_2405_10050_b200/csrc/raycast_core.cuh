@@ -1056,6 +1056,7 @@ struct TreeCursor {
   int64_t st = 0;
   unsigned long long tests = 0;
   unsigned leaf_mask = 0u;  // lanes needing the leaf returned by next()
+  int pend = 0, pend_end = 0;  // rest of a popped multi-tile leaf (VR_LEAF_TILES > 1)
   __device__ __forceinline__ unsigned warp_needs(const RayState<D> (&ray)[R],
                                                  const double* __restrict__ node_box,
                                                  const float* __restrict__ node_box32, int node) {
@@ -1081,6 +1082,7 @@ struct TreeCursor {
                                        const int2* __restrict__ node_range) {
     st = start_tile;
     sp = 0;
+    pend = pend_end = 0;
     const unsigned m = warp_needs(ray, node_box, node_box32, 0);
     if (m) push(0, __ldg(node_range), m);
   }
@@ -1090,13 +1092,21 @@ struct TreeCursor {
                                           const double* __restrict__ node_box,
                                           const float* __restrict__ node_box32,
                                           const int2* __restrict__ node_range) {
+#ifndef VR_LEAF_TILES  // tuning knob: nodes of <= VR_LEAF_TILES tiles are screened whole
+#define VR_LEAF_TILES 1
+#endif
+    if (VR_LEAF_TILES > 1 && pend < pend_end) return pend++;
     while (sp > 0) {
       --sp;
       const int node = __shfl_sync(0xffffffffu, s_node, sp);
       const int lo = __shfl_sync(0xffffffffu, s_lo, sp);
       const int hi = __shfl_sync(0xffffffffu, s_hi, sp);
-      if (hi - lo == 1) {
+      if (hi - lo <= VR_LEAF_TILES) {
         leaf_mask = __shfl_sync(0xffffffffu, s_mask, sp);
+        if (VR_LEAF_TILES > 1) {
+          pend = lo + 1;
+          pend_end = hi;
+        }
         return lo;
       }
       const int l = 2 * node + 1, r = 2 * node + 2;
