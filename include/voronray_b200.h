@@ -51,7 +51,7 @@ enum vr_cell_status {
   VR_CELL_OVERFLOW = 3     /* more distinct hit faces than area slots          */
 };
 
-int vr_abi_version(void); /* 6 */
+int vr_abi_version(void); /* 7 */
 const char* vr_status_string(int status);
 
 /* Record stride (doubles) of one packed generator for dimension d:
@@ -507,9 +507,20 @@ typedef struct vr_trav_state {
   int64_t rays;          /* edge raycasts so far */
   int32_t need;          /* vr_run_need */
   int64_t need_amount;
+  int32_t sub_n, sub_j;  /* sub-rounds of the current level (set by the driver;
+                            start at 0): round sub_j of sub_n is next */
 } vr_trav_state;
 int vr_trav_run_workspace(int64_t n_frontier, int64_t n_rays, int64_t n_gen, int d,
                           int64_t* bytes);
+/* Sub-rounds of large levels in vr_trav_run: a level of F frontier vertices is
+ * cast in about F (d + 1) / 2 / rays_per_round interleaved rounds (at most
+ * max_rounds <= 64; vertex v of the frontier belongs to round v % rounds), so
+ * that vertices found by an earlier round close the edges later rounds would
+ * have cast (graph.py:115-128).  rays_per_round 0 = never split; -1 / -1 =
+ * back to the defaults (environment VR_SUB_RAYS / VR_SUB_MAX).  The vertex
+ * set, edge counts and boundary rays do not depend on the setting; vertex ids
+ * within a level do.  Process-wide. */
+int vr_trav_set_sub_rounds(int64_t rays_per_round, int max_rounds);
 int vr_trav_run(const vr_traverse_tables* tab, vr_trav_state* state, const double* rec,
                 int64_t n_gen, int d, double sqmax, const vr_screen32* s32,
                 const vr_prune_index* ix, int32_t last_level, int64_t* level_new,
@@ -526,6 +537,12 @@ int vr_trav_insert_vertices(const vr_traverse_tables* tab, int d,
 int vr_trav_rehash_edges(const vr_traverse_tables* tab, int d,
                          const int32_t* okeys, const int32_t* ostate,
                          const int32_t* ocount, int64_t ocap, void* stream);
+
+/* vr_trav_open_edges restricted to the frontier vertices with
+ * v % sub_n == sub_j (sub-rounds of a level; the others report no open edge). */
+int vr_trav_open_edges_sub(const vr_traverse_tables* tab, int d,
+                           const int32_t* sigma, int64_t n_v, int sub_n, int sub_j,
+                           uint8_t* open_mask, int32_t* open_count, void* stream);
 
 /* open_mask[v*(d+1)+k] = 1 iff edge sigma_v \ sigma_v[k] has count < 2
  * (graph.py:127-128); open_count[v] = number of open edges of v. */

@@ -14,7 +14,8 @@ from .core import (TOL_VERTEX, TOL_DEGENERATE, HALFSPACE_SLACK, BoundaryRay, Mes
 from .raycast import (RayQuery, RaycastBatch, RaycastStats, initial_heuristic, project_t,
                       raycast_batch, raycast_incircle, search_direction, vertex_directions_batch)
 from .graph import (DESCENT_RETRIES, VerifyReport, brute_force_vertices, circumcenters, descent,
-                    descent_batch, edge_set, verify_mesh, voronoi_graph, voronoi_local)
+                    descent_batch, edge_set, set_sub_rounds, verify_mesh, voronoi_graph,
+                    voronoi_local)
 from .integrate_mc import (CellIntegrals, Integrand, MCResult, mc_areas_only, mc_cells,
                            mc_directions, mc_integrals_cells, mc_integrate_cell, mc_uniforms,
                            sample_unit_sphere, sphere_surface_area)
@@ -30,7 +31,7 @@ __all__ = [
     "edge_keys", "RayQuery", "RaycastStats", "RaycastBatch", "project_t", "initial_heuristic",
     "raycast_incircle", "raycast_batch", "search_direction", "vertex_directions_batch",
     "edge_set", "descent", "descent_batch", "voronoi_graph", "voronoi_local", "verify_mesh",
-    "VerifyReport",
+    "VerifyReport", "set_sub_rounds",
     "brute_force_vertices", "circumcenters", "DESCENT_RETRIES", "CellIntegrals", "Integrand",
     "MCResult", "sample_unit_sphere", "sphere_surface_area", "mc_areas_only", "mc_cells",
     "mc_directions", "mc_integrate_cell", "mc_integrals_cells", "mc_uniforms", "integrands",

@@ -15,7 +15,7 @@ import torch
 from ._build import LIB_PATH
 from .errors import DeviceUnavailable
 
-ABI_VERSION = 6  # vr_abi_version() of the library this package expects
+ABI_VERSION = 7  # vr_abi_version() of the library this package expects
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -95,6 +95,8 @@ _SIGNATURES = {
     "vr_trav_insert_vertices": [_vp, _int, _vp, _i64, ctypes.c_int32, ctypes.c_int32, _int, _vp],
     "vr_trav_rehash_edges": [_vp, _int, _vp, _vp, _vp, _i64, _vp],
     "vr_trav_open_edges": [_vp, _int, _vp, _i64, _vp, _vp, _vp],
+    "vr_trav_open_edges_sub": [_vp, _int, _vp, _i64, _int, _int, _vp, _vp, _vp],
+    "vr_trav_set_sub_rounds": [_i64, _int],
     "vr_trav_emit_rays": [_vp, _int, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "vr_trav_claim": [_vp, _int, _vp, _vp, _vp, _i64, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp],
     "vr_trav_finalize": [_vp, _vp, _int, _vp, _vp, _vp, _vp, _i64, ctypes.c_int32, _vp, _vp,

@@ -23,6 +23,9 @@
 #include "common.cuh"
 
 extern "C" {
+int vr_trav_open_edges_sub(const vr_traverse_tables* tab, int d, const int32_t* sigma,
+                           int64_t n_v, int sub_n, int sub_j, uint8_t* open_mask,
+                           int32_t* open_count, void* stream);
 int vr_trav_open_edges(const vr_traverse_tables* tab, int d, const int32_t* sigma, int64_t n_v,
                        uint8_t* open_mask, int32_t* open_count, void* stream);
 int vr_trav_emit_rays(const double* rec, int d, const int32_t* sigma, const double* r,
@@ -48,6 +51,17 @@ int vr_raycast_recheck(const double* rec, int64_t n_gen, int d, const double* ca
                        const int32_t* recheck_count, int64_t max_list, int32_t* out_idx,
                        double* out_t, double* out_rp, uint8_t* out_flag, void* stream);
 }
+
+// defaults measured on config 5 (N = 1e6, d = 8, 36.5 M vertices): 2 rounds for
+// levels of >= 8 M estimated rays cast 45.9 M instead of 56.6 M edges, 0.787 vs
+// 0.826 s; 4 / 8 rounds cast 42.1 / 40.4 M but their sparser batches screen
+// more pairs per ray (0.803 / 0.847 s)
+#ifndef VR_SUB_RAYS_DEFAULT
+#define VR_SUB_RAYS_DEFAULT 4000000
+#endif
+#ifndef VR_SUB_MAX_DEFAULT
+#define VR_SUB_MAX_DEFAULT 2
+#endif
 
 namespace {
 
@@ -173,10 +187,26 @@ extern "C" int vr_trav_level_workspace(int64_t n_v, int64_t n_rays, int64_t n_ge
   return VR_OK;
 }
 
+namespace {
+int level_open_sub(const vr_traverse_tables* tab, int d, const int32_t* frontier_sigma,
+                   int64_t n_v, int sub_n, int sub_j, uint8_t* open_mask, int32_t* open_count,
+                   int64_t* open_off, int64_t* n_rays_out, void* workspace,
+                   int64_t workspace_bytes, void* stream);
+}
+
 extern "C" int vr_trav_level_open(const vr_traverse_tables* tab, int d,
                                   const int32_t* frontier_sigma, int64_t n_v, uint8_t* open_mask,
                                   int32_t* open_count, int64_t* open_off, int64_t* n_rays_out,
                                   void* workspace, int64_t workspace_bytes, void* stream) {
+  return level_open_sub(tab, d, frontier_sigma, n_v, 1, 0, open_mask, open_count, open_off,
+                        n_rays_out, workspace, workspace_bytes, stream);
+}
+
+namespace {
+int level_open_sub(const vr_traverse_tables* tab, int d, const int32_t* frontier_sigma,
+                   int64_t n_v, int sub_n, int sub_j, uint8_t* open_mask, int32_t* open_count,
+                   int64_t* open_off, int64_t* n_rays_out, void* workspace,
+                   int64_t workspace_bytes, void* stream) {
   if (!tab || !frontier_sigma || !open_mask || !open_count || !open_off || !n_rays_out)
     return VR_EINVAL;
   *n_rays_out = 0;
@@ -185,7 +215,8 @@ extern "C" int vr_trav_level_open(const vr_traverse_tables* tab, int d,
   const size_t tmp = scan_tmp_bytes(n_v);
   if (!workspace || workspace_bytes < (int64_t)tmp) return VR_ECAPACITY;
   cudaStream_t st = as_stream(stream);
-  int s = vr_trav_open_edges(tab, d, frontier_sigma, n_v, open_mask, open_count, stream);
+  int s = vr_trav_open_edges_sub(tab, d, frontier_sigma, n_v, sub_n, sub_j, open_mask, open_count,
+                                 stream);
   if (s) return s;
   cudaError_t e = excl_scan(open_count, open_off, n_v, workspace, tmp, st);
   if (e != cudaSuccess) return fail(e);
@@ -198,6 +229,7 @@ extern "C" int vr_trav_level_open(const vr_traverse_tables* tab, int d,
   *n_rays_out = last[0] + cnt[0];
   return VR_OK;
 }
+}  // namespace
 
 extern "C" int vr_trav_level_cast(
     const vr_traverse_tables* tab, const double* rec, int64_t n_gen, int d, double sqmax,
@@ -350,6 +382,52 @@ int64_t small_rmax(int d);  // rays per level the persistent kernel takes
 
 namespace {
 
+// Sub-rounds of a large level.  A level-synchronous traversal casts one ray
+// per open edge of the frontier, so a new vertex adjacent to k frontier
+// vertices is found k times (config 5: 56.6 M rays for 36.5 M vertices); the
+// reference's one-vertex-at-a-time loop (graph.py:122-145) casts it once,
+// because the first discovery closes the other k - 1 edges (graph.py:115-120).
+// Splitting the frontier into sub_n interleaved sub-rounds (vertex v of the
+// frontier belongs to round v % sub_n; each round opens, casts, claims,
+// stores and bumps before the next one opens) recovers part of that: a ray
+// is skipped whenever an earlier round already found its far vertex.  The
+// vertex set, edge counts and boundary rays are those of the unsplit level.
+// A level of F frontier vertices is split so that a round casts about
+// VR_SUB_RAYS rays (estimated as F (d + 1) / 2), at most VR_SUB_MAX rounds.
+int64_t g_sub_rays = -1;  // vr_trav_set_sub_rounds overrides (-1: environment / default)
+int g_sub_max = -1;
+int64_t sub_target_rays() {
+  if (g_sub_rays >= 0) return g_sub_rays;
+  static const int64_t v = [] {
+    const char* e = std::getenv("VR_SUB_RAYS");
+    return e ? (int64_t)std::atoll(e) : (int64_t)VR_SUB_RAYS_DEFAULT;
+  }();
+  return v;
+}
+int sub_max_rounds() {
+  int m = g_sub_max;
+  if (m < 0) {
+    static const int v = [] {
+      const char* e = std::getenv("VR_SUB_MAX");
+      return e ? std::atoi(e) : VR_SUB_MAX_DEFAULT;
+    }();
+    m = v;
+  }
+  return m < 1 ? 1 : (m > 64 ? 64 : m);
+}
+int plan_sub_rounds(int64_t F, int d) {
+  const int64_t target = sub_target_rays();
+  if (target <= 0) return 1;
+  const int64_t est = F * (d + 1) / 2;
+  int64_t n = est / target;
+  if (n < 1) n = 1;
+  if (n > sub_max_rounds()) n = sub_max_rounds();
+  return (int)n;
+}
+// claim epoch of (level, sub-round): distinct from every level number the
+// other paths tag their claims with
+int32_t claim_epoch(int32_t level, int sub_j) { return 0x40000000 + level * 64 + sub_j; }
+
 // VR_SMALL_LEVELS=0 disables the persistent small-level kernel (A/B runs).
 bool small_mode() {
   const char* e = std::getenv("VR_SMALL_LEVELS");
@@ -398,6 +476,12 @@ int run_plan(int64_t F, int64_t R, int64_t n_gen, int d, RunPlan& p) {
 
 }  // namespace
 
+extern "C" int vr_trav_set_sub_rounds(int64_t rays_per_round, int max_rounds) {
+  g_sub_rays = rays_per_round;
+  g_sub_max = max_rounds;
+  return VR_OK;
+}
+
 extern "C" int vr_trav_run_workspace(int64_t n_frontier, int64_t n_rays, int64_t n_gen, int d,
                                      int64_t* bytes) {
   if (!bytes) return VR_EINVAL;
@@ -429,7 +513,7 @@ extern "C" int vr_trav_run(const vr_traverse_tables* tab, vr_trav_state* S, cons
     // stay small in one launch
     // (expected rays ~ F (d+1) / 2: about half the edges of a frontier
     // vertex are open; larger levels skip the attempt)
-    if (S->phase == 0 && S->level != host_level && small_mode() &&
+    if (S->phase == 0 && S->sub_j == 0 && S->level != host_level && small_mode() &&
         F * (d + 1) <= 2 * vr::small_rmax(d)) {
       int handled = 0;
       int32_t bail = 0;
@@ -460,14 +544,22 @@ extern "C" int vr_trav_run(const vr_traverse_tables* tab, vr_trav_state* S, cons
     int64_t* ooff = reinterpret_cast<int64_t*>(W + p0.o_off);
     int64_t R = S->pending_rays;
     if (S->phase == 0) {
-      s = vr_trav_level_open(tab, d, fs, F, mask, ocnt, ooff, &R, W + p0.o_scr,
-                             (int64_t)p0.scratch, stream);
+      if (S->sub_j == 0) {  // the level starts: its vertices go to ids f1 ..
+        S->nv = S->f1;
+        S->sub_n = plan_sub_rounds(F, d);
+      }
+      s = level_open_sub(tab, d, fs, F, S->sub_n, S->sub_j, mask, ocnt, ooff, &R, W + p0.o_scr,
+                         (int64_t)p0.scratch, stream);
       if (s) return s;
-      if (R == 0) {  // nothing open: the traversal ends here
-        level_new[S->level] = 0;
+      if (R == 0) {  // nothing open in this round
+        if (++S->sub_j < S->sub_n) continue;
+        S->sub_j = 0;
+        const bool grew = S->nv > S->f1;
         S->f0 = S->f1;
+        S->f1 = S->nv;
         S->level += 1;
-        S->need = VR_RUN_DONE;
+        if (grew) continue;
+        S->need = VR_RUN_DONE;  // nothing open in the whole level: the traversal ends here
         return VR_OK;
       }
       S->pending_rays = R;
@@ -514,7 +606,8 @@ extern "C" int vr_trav_run(const vr_traverse_tables* tab, vr_trav_state* S, cons
       }
       int64_t counts[5];
       s = vr_trav_level_cast(tab, rec, n_gen, d, sqmax, s32, ix, fs, fr, F, mask, ooff, R,
-                             S->level, rx, ru, reta, rpar, hidx, ht, hflag, rsig, slot, newf,
+                             claim_epoch(S->level, S->sub_j), rx, ru, reta, rpar, hidx, ht, hflag,
+                             rsig, slot, newf,
                              escf, noff, eoff, bad, work, counts, W + p.o_scr,
                              (int64_t)p.scratch, stream);
       if (s) return s;
@@ -536,7 +629,7 @@ extern "C" int vr_trav_run(const vr_traverse_tables* tab, vr_trav_state* S, cons
       S->need_amount = S->nb + S->n_esc;
       return VR_OK;
     }
-    s = vr_trav_finalize(tab, rec, d, rsig, slot, newf, noff, R, (int32_t)S->f1, S->vsig, S->vr,
+    s = vr_trav_finalize(tab, rec, d, rsig, slot, newf, noff, R, (int32_t)S->nv, S->vsig, S->vr,
                          bad + 1, 1, stream);
     if (s) return s;
     if (S->n_esc) {
@@ -545,13 +638,16 @@ extern "C" int vr_trav_run(const vr_traverse_tables* tab, vr_trav_state* S, cons
     }
     S->e_ub += (d + 1) * S->n_new;
     S->nb += S->n_esc;
-    S->nv = S->f1 + S->n_new;
-    level_new[S->level] = S->n_new;
+    S->nv += S->n_new;
+    level_new[S->level] += S->n_new;
     S->rays += R;
-    S->f0 = S->f1;
-    S->f1 = S->nv;
-    S->level += 1;
     S->phase = 0;
     S->pending_rays = 0;
+    if (++S->sub_j >= S->sub_n) {  // the level is complete
+      S->sub_j = 0;
+      S->f0 = S->f1;
+      S->f1 = S->nv;
+      S->level += 1;
+    }
   }
 }

@@ -47,7 +47,7 @@ int vr::hsweep_mode() {
   return e ? std::atoi(e) : 0;
 }
 
-extern "C" int vr_abi_version(void) { return 6; }
+extern "C" int vr_abi_version(void) { return 7; }
 
 extern "C" const char* vr_status_string(int status) {
   switch (status) {

@@ -145,10 +145,19 @@ __global__ void k_rehash_edges(Tables t, const int32_t* __restrict__ okeys,
                   [&](int64_t h) { t.ecount[h] = c; });
 }
 
+// (sub_n, sub_j): sub-rounds of a level -- only the frontier vertices with
+// v % sub_n == sub_j open their edges in this round (the others report none).
 template <int D>
 __device__ __forceinline__ void open_edges_one(Tables t, const int32_t* sigma, int64_t nv,
-                             uint8_t* open_mask, int32_t* open_count, int64_t v) {
+                             uint8_t* open_mask, int32_t* open_count, int64_t v,
+                             int sub_n = 1, int sub_j = 0) {
   if (v >= nv) return;
+  if (sub_n > 1 && (int)(v % sub_n) != sub_j) {
+#pragma unroll
+    for (int k = 0; k <= D; ++k) open_mask[v * (D + 1) + k] = 0;
+    open_count[v] = 0;
+    return;
+  }
   const int32_t* s = sigma + v * (D + 1);
   int cnt = 0;
 #pragma unroll 1
@@ -166,8 +175,10 @@ __device__ __forceinline__ void open_edges_one(Tables t, const int32_t* sigma, i
 
 template <int D>
 __global__ void k_open_edges(Tables t, const int32_t* __restrict__ sigma, int64_t nv,
-                             uint8_t* __restrict__ open_mask, int32_t* __restrict__ open_count) {
-  open_edges_one<D>(t, sigma, nv, open_mask, open_count, blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+                             uint8_t* __restrict__ open_mask, int32_t* __restrict__ open_count,
+                             int sub_n, int sub_j) {
+  open_edges_one<D>(t, sigma, nv, open_mask, open_count,
+                    blockIdx.x * (int64_t)blockDim.x + threadIdx.x, sub_n, sub_j);
 }
 
 // One thread per frontier vertex: LU of D (rows x_s - x_s0) once, then the

@@ -187,17 +187,24 @@ extern "C" int vr_trav_rehash_edges(const vr_traverse_tables* tab, int d, const 
   VR_RETURN_LAUNCH();
 }
 
-extern "C" int vr_trav_open_edges(const vr_traverse_tables* tab, int d, const int32_t* sigma,
-                                  int64_t n_v, uint8_t* open_mask, int32_t* open_count,
-                                  void* stream) {
-  if (!tab || !sigma || !open_mask || !open_count) return VR_EINVAL;
+extern "C" int vr_trav_open_edges_sub(const vr_traverse_tables* tab, int d, const int32_t* sigma,
+                                      int64_t n_v, int sub_n, int sub_j, uint8_t* open_mask,
+                                      int32_t* open_count, void* stream) {
+  if (!tab || !sigma || !open_mask || !open_count || sub_n < 1 || sub_j < 0 || sub_j >= sub_n)
+    return VR_EINVAL;
   if (n_v <= 0) return VR_OK;
   const Tables t = from(tab);
   VR_DISPATCH_D_ALL(d, {
     k_open_edges<D><<<nb(n_v, 128), 128, 0, as_stream(stream)>>>(t, sigma, n_v, open_mask,
-                                                                  open_count);
+                                                                  open_count, sub_n, sub_j);
   });
   VR_RETURN_LAUNCH();
+}
+
+extern "C" int vr_trav_open_edges(const vr_traverse_tables* tab, int d, const int32_t* sigma,
+                                  int64_t n_v, uint8_t* open_mask, int32_t* open_count,
+                                  void* stream) {
+  return vr_trav_open_edges_sub(tab, d, sigma, n_v, 1, 0, open_mask, open_count, stream);
 }
 
 extern "C" int vr_trav_emit_rays(const double* rec, int d, const int32_t* sigma, const double* r,

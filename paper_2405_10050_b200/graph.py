@@ -440,7 +440,8 @@ class _RunState(ctypes.Structure):  # vr_trav_state
                 ("n_new", ctypes.c_int64), ("n_esc", ctypes.c_int64),
                 ("n_degenerate", ctypes.c_int64), ("n_bad", ctypes.c_int64),
                 ("overflow", ctypes.c_int64), ("rays", ctypes.c_int64), ("need", ctypes.c_int32),
-                ("need_amount", ctypes.c_int64)]
+                ("need_amount", ctypes.c_int64), ("sub_n", ctypes.c_int32),
+                ("sub_j", ctypes.c_int32)]
 
 
 RUN_DONE, RUN_NEED_WS, RUN_NEED_V, RUN_NEED_E, RUN_NEED_B, RUN_ERROR = range(6)
@@ -852,6 +853,18 @@ def _sharding():
     if mode not in ("owner", "replicated"):
         raise ValueError(f"VR_SHARDING must be owner or replicated, got {mode!r}")
     return mode
+
+
+def set_sub_rounds(rays_per_round: int = -1, max_rounds: int = -1):
+    """Sub-rounds of large traversal levels (vr_trav_set_sub_rounds): a level
+    whose frontier would cast more than ``rays_per_round`` rays is cast in up
+    to ``max_rounds`` interleaved rounds, so that vertices found by an earlier
+    round close the edges later rounds would have cast again (the reference's
+    one-vertex-at-a-time loop never casts them, graph.py:115-128).  0 = never
+    split; -1, -1 = the library defaults (VR_SUB_RAYS / VR_SUB_MAX).  The mesh
+    (vertex set, edges, boundary rays) does not depend on the setting."""
+    _lib.check(_lib.lib().vr_trav_set_sub_rounds(int(rays_per_round), int(max_rounds)),
+               "vr_trav_set_sub_rounds")
 
 
 def voronoi_graph(ns: NodeSet, seed: int = 0, *, method: str = "incircle_heuristic",

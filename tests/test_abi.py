@@ -44,7 +44,7 @@ def test_library_is_sm100a(built_library):
 def test_loads_and_reports(built_library):
     from paper_2405_10050_b200 import _lib
     L = _lib.load_library()
-    assert L.vr_abi_version() == _lib.ABI_VERSION == 6
+    assert L.vr_abi_version() == _lib.ABI_VERSION == 7
     assert [L.vr_record_stride(d) for d in range(2, 9)] == [4, 4, 6, 6, 8, 8, 10]
     assert L.vr_record_stride(9) == 10 and L.vr_record_stride(16) == 18
     assert L.vr_record_stride(17) < 0

@@ -156,6 +156,66 @@ def test_config3_full_diagram():
     assert rep.passed and rep.vertices_total == ref["n_vertices"]
 
 
+@pytest.mark.parametrize("rounds", [2, 5, 64])
+def test_sub_rounds_same_mesh_fewer_rays(rounds):
+    """Large levels cast in interleaved sub-rounds (vr_trav_set_sub_rounds):
+    the mesh is that of the unsplit traversal (reference digests of config 1,
+    edge table, boundary multiset) and fewer edges are raycast, because a
+    vertex found by an earlier round closes the edges a later round would
+    have cast (graph.py:115-128)."""
+    gz = golden("mesh_config1.npz")
+    pts = np.random.default_rng(0).random((1000, 3))
+    ns = vb.build_node_set(pts)
+    old = os.environ.get("VR_SMALL_LEVELS")
+    os.environ["VR_SMALL_LEVELS"] = "0"  # the host level path is the one that splits
+    try:
+        vb.set_sub_rounds(0, 1)
+        st0 = vb.RaycastStats()
+        m0 = vb.voronoi_graph(ns, seed=0, stats=st0)
+        vb.set_sub_rounds(1, rounds)  # every level splits into `rounds` rounds
+        st1 = vb.RaycastStats()
+        m1 = vb.voronoi_graph(ns, seed=0, stats=st1)
+    finally:
+        vb.set_sub_rounds(-1, -1)
+        if old is None:
+            del os.environ["VR_SMALL_LEVELS"]
+        else:
+            os.environ["VR_SMALL_LEVELS"] = old
+    for m in (m0, m1):
+        a = m.arrays()
+        assert np.array_equal(sorted_rows(a["sigma"]), gz["sigma"])
+        assert np.array_equal(sorted_rows(a["boundary_sigma"]), gz["boundary_sigma"])
+        assert np.array_equal(a["edge_key"], gz["edge_key"])
+        assert np.array_equal(a["edge_count"], gz["edge_count"])
+    nv = gz["sigma"].shape[0]
+    assert st1.raycasts < st0.raycasts
+    if rounds == 64:  # close to the reference's sequential count (V - 1 + boundary rays)
+        assert st1.raycasts <= 1.2 * nv + 4
+    rep = vb.verify_mesh(m1, oracle=False)
+    assert rep.passed
+
+
+def test_sub_rounds_local_traversal_levels():
+    """L-hop traversal with sub-rounds: same vertex set and hop levels."""
+    pts = np.random.default_rng(5).random((20000, 6))
+    ns = vb.build_node_set(pts)
+    seeds = np.arange(0, 20000, 400)
+    try:
+        vb.set_sub_rounds(0, 1)
+        m0, l0 = vb.voronoi_local(ns, seeds, hops=3, return_levels=True)
+        vb.set_sub_rounds(20000, 4)
+        m1, l1 = vb.voronoi_local(ns, seeds, hops=3, return_levels=True)
+    finally:
+        vb.set_sub_rounds(-1, -1)
+    a0, a1 = m0.arrays(), m1.arrays()
+    o0, o1 = np.lexsort(a0["sigma"].T[::-1]), np.lexsort(a1["sigma"].T[::-1])
+    assert np.array_equal(a0["sigma"][o0], a1["sigma"][o1])
+    assert np.array_equal(np.asarray(l0)[o0], np.asarray(l1)[o1])
+    assert np.array_equal(a0["edge_key"], a1["edge_key"])
+    assert np.array_equal(a0["edge_count"], a1["edge_count"])
+    assert np.allclose(a0["r"][o0], a1["r"][o1], rtol=0, atol=1e-12)
+
+
 def test_verify_mesh_and_perturbation():
     pts = np.random.default_rng(1234).random((120, 2))
     mesh = vb.voronoi_graph(vb.build_node_set(pts), seed=0)
