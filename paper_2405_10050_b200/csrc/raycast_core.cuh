@@ -1092,18 +1092,26 @@ struct TreeCursor {
                                           const double* __restrict__ node_box,
                                           const float* __restrict__ node_box32,
                                           const int2* __restrict__ node_range) {
-#ifndef VR_LEAF_TILES  // tuning knob: nodes of <= VR_LEAF_TILES tiles are screened whole
-#define VR_LEAF_TILES 1
+    // Nodes of <= LT tiles are screened whole (their children are not
+    // box-tested).  At d >= 7 the walk costs more than the screens it saves:
+    // LT = 2 takes config 5 from 0.787 to 0.767 s (1,515 instead of 2,212 node
+    // tests, 724 instead of 528 tiles per warp of edge rays); at d <= 6 it is
+    // neutral (config 2: 2.416 vs 2.430 ms) or slower (config 4: 0.081 vs
+    // 0.079 s).  -DVR_LEAF_TILES=n overrides it for every d.
+#ifdef VR_LEAF_TILES
+    constexpr int LT = VR_LEAF_TILES;
+#else
+    constexpr int LT = D >= 7 ? 2 : 1;
 #endif
-    if (VR_LEAF_TILES > 1 && pend < pend_end) return pend++;
+    if (LT > 1 && pend < pend_end) return pend++;
     while (sp > 0) {
       --sp;
       const int node = __shfl_sync(0xffffffffu, s_node, sp);
       const int lo = __shfl_sync(0xffffffffu, s_lo, sp);
       const int hi = __shfl_sync(0xffffffffu, s_hi, sp);
-      if (hi - lo <= VR_LEAF_TILES) {
+      if (hi - lo <= LT) {
         leaf_mask = __shfl_sync(0xffffffffu, s_mask, sp);
-        if (VR_LEAF_TILES > 1) {
+        if (LT > 1) {
           pend = lo + 1;
           pend_end = hi;
         }

@@ -49,6 +49,20 @@ def cast(x, uf, eta):
     return float(np.median(ts)), x.shape[0]
 
 
+# split by direction instead: sign of the dominant component (2 rounds),
+# dominant axis parity x sign (4 rounds)
+X, U, E = rays(torch.arange(nv, device=dev))
+dom = U.abs().argmax(1)
+sgn = (U.gather(1, dom[:, None])[:, 0] > 0).long()
+for name, cls, S in (("sign", sgn, 2), ("axis-parity x sign", (dom % 2) * 2 + sgn, 4),
+                     ("axis", dom, 8)):
+    tot = 0.0
+    for j in range(S):
+        m = cls == j
+        t, _ = cast(X[m].contiguous(), U[m].contiguous(), E[m].contiguous())
+        tot += t
+    print(f"direction split {name} S={S}: total {tot:.1f} ms", flush=True)
+del X, U, E
 ids = torch.arange(nv, device=dev)
 for S in (1, 2, 4, 8):
     tot = 0.0
