@@ -317,9 +317,10 @@ def extra_configs(vb, torch, world, rank, cpu=True, passes=5):
     # ---- config 1: full diagram N=1000, d=3 ------------------------------
     pts1 = np.random.default_rng(0).random((1000, 3))
     ns1 = vb.build_node_set(pts1)
-    # a few ms of mostly host-side latency: 4x the passes, so that host
-    # scheduling noise (single passes of 5-10 ms) does not set the median
-    p1 = 4 * passes
+    # a few ms of mostly host-side latency: 12x the passes, so that a burst of
+    # host scheduling noise (one run had its first 13 passes at 4-60 ms, the
+    # rest at 3.1 ms) does not set the median
+    p1 = 12 * passes
     med, ts, (m1, info1) = _median_passes(
         lambda: vb.voronoi_graph(ns1, seed=0, return_info=True), p1, torch)
     c1 = {"vertices": info1["vertices"], "seconds": med, "passes_s": ts,
