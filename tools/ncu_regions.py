@@ -4,12 +4,45 @@ import csv
 import sys
 from collections import defaultdict
 
-REGIONS = [(88, 145, 'ray_setup'), (148, 197, 'set_best'), (200, 242, 'load_helpers'),
-           (252, 316, 'rare_block'), (333, 357, 'src_load'), (460, 487, 'store'),
-           (891, 916, 'box_test'), (980, 1039, 'seed32'), (1047, 1143, 'cursor'),
-           (1251, 1266, 'mma_instr'), (1276, 1313, 'mma_store'), (1319, 1342, 'mma_load/block'),
-           (1345, 1349, 'spread4'), (1351, 1371, 'screen_nohit'), (1372, 1418, 'screen_hit'),
-           (1530, 1712, 'kernel_main')]
+import os
+import re
+
+# region = [first line of the named function .. first line of the next one)
+ANCHORS = [("ray_setup", r"void ray_setup\("), ("set_best", r"void ray_set_best\("),
+           ("load_helpers", r"void load_rec\("), ("rare_block", r"void ray_rare_block\("),
+           ("ray_power", r"double ray_power\("), ("src_load", r"^struct SrcExplicit"),
+           ("philox/mc", r"void philox4x32_10\("), ("store", r"void ray_store\("),
+           ("screen_tile(other)", r"^struct WarpCounters"), ("box_test(other)", r"bool ray_needs_box\("),
+           ("box_test", r"bool ray_needs_box32_ch_d2\("), ("ray_needs", r"bool ray_needs\("),
+           ("seed64", r"void seed_tile\("), ("seed32", r"void seed_tile32\("),
+           ("cursor", r"^struct TreeCursor"), ("remap", r"int remap_max\(\)"),
+           ("mma_instr", r"void mma_tf32\("), ("mma_store", r"void mma_store_a\("),
+           ("mma_load/block", r"void mma_load_a\("), ("spread4", r"uint32_t spread4\("),
+           ("screen_nohit", r"void screen_tile_mma\("), ("screen_hit", r"Some pair passed: recompute"),
+           ("hsweep", r"k_raycast_hsweep"), ("kernel_main", r"\s+k_raycast_pruned\(Src src"),
+           ("coop", r"^constexpr int WIDE = 32")]
+
+
+def regions():
+    src = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2405_10050_b200",
+                       "csrc", "raycast_core.cuh")
+    lines = open(src).read().splitlines()
+    starts = []
+    for name, pat in ANCHORS:
+        rx = re.compile(pat)
+        for n, ln in enumerate(lines, 1):
+            if rx.search(ln):
+                starts.append((n, name))
+                break
+    starts.sort()
+    out = []
+    for k, (n, name) in enumerate(starts):
+        end = starts[k + 1][0] - 1 if k + 1 < len(starts) else len(lines)
+        out.append((n, end, name))
+    return out
+
+
+REGIONS = regions()
 
 
 def _int(v):
