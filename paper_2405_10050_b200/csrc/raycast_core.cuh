@@ -58,6 +58,7 @@ struct RayState {
   float bsl32;  // slack of the fp32 halfspace bound
   float del32;  // slack of the fp32 box distance (centre rounding)
   float rb32;   // (rho^2 + dlt) rounded up with the fp32 sum slack (+inf: none)
+  float rbd32;  // (sqrt(rb32) + sqrt(d) del32)^2 rounded up: rb32 with the del32 slack folded in
   float ctc;    // tensor-core screen constant: -(hi32 + tf32 error bound), tf32, rounded down
   int ib;       // current best (local candidate index), -1 = none
   int gk;       // local index of the reference generator g (never valid: u.x_g <= thr), -1 = unknown
@@ -139,6 +140,7 @@ __device__ __forceinline__ void ray_setup(RayState<D>& r, const double* __restri
   r.bsl32 = __double2float_ru((D + 4) * 2.384185791015625e-07 * sqrt((double)D) * fr.bnd32 + 1e-30);
   r.del32 = 0.0f;
   r.rb32 = CUDART_INF_F;
+  r.rbd32 = CUDART_INF_F;
   r.ctc = -1e20f;  // no sphere yet: every real candidate passes the tensor-core screen
   r.gk = -1;
 }
@@ -184,6 +186,16 @@ __device__ __forceinline__ void ray_set_best(RayState<D>& r, double t, double de
   // fp32 box test: |e32_k - e_k| <= 2^-22 (|z~|_inf + B); sum slack relative
   r.del32 = __double2float_ru(2.384185791015625e-07 * (ztmax + fr.bnd32));
   r.rb32 = __double2float_ru((rho2 + dlt) * (1.0 + (D + 4) * 1.1920928955078125e-07));
+  // The centre / half-extent box tests drop the per-dimension "- del32":
+  // with e'_k = max(|z_k - c_k| - h_k, 0) (no slack) and e_k >= max(e'_k -
+  // del32, 0), |e| >= |e'| - sqrt(d) del32, so |e'|^2 >= (sqrt(rb32) +
+  // sqrt(d) del32)^2 implies |e|^2 >= rb32: the folded test skips a subset of
+  // the boxes the per-dimension test skips (del32 ~ 2^-22 of the box scale).
+  {
+    const float sd = __double2float_ru(sqrt((double)D));
+    const float c = __fadd_ru(__fsqrt_ru(r.rb32), __fmul_ru(sd, r.del32));
+    r.rbd32 = __fmul_ru(c, c);
+  }
   // Tensor-core screen (screen_tile_mma): the same fp32 inputs rounded to
   // tf32 (relative error 2^-11 each, products exact in fp32) and summed by
   // the MMA: |f_tc - f_32| <= 2^-10 sum|z_k x_k| + 2^-11 |x|^2 + accumulation
@@ -879,11 +891,19 @@ __device__ __forceinline__ bool ray_needs_box32_ch(const RayState<D>& r,
     umax = fmaf(r.u32[k], v[k], umax);
     umax = fmaf(fabsf(r.u32[k]), v[D + k], umax);
     const float zc = -0.5f * r.z32[k];
+#ifdef VR_NO_FOLD_DEL
     const float e = fmaxf(fabsf(zc - v[k]) - v[D + k] - r.del32, 0.0f);
+#else
+    const float e = fmaxf(fabsf(zc - v[k]) - v[D + k], 0.0f);  // del32 folded into rbd32
+#endif
     d2 = fmaf(e, e, d2);
   }
   if (umax + r.bsl32 <= r.thr32) return false;  // behind the forward halfspace
+#ifdef VR_NO_FOLD_DEL
   return !(d2 >= r.rb32);                        // inside sphere + band (or no sphere)
+#else
+  return !(d2 >= r.rbd32);
+#endif
 }
 
 // ray_needs_box32_ch plus the sphere-distance term d2 (child ordering).
@@ -908,11 +928,19 @@ __device__ __forceinline__ bool ray_needs_box32_ch_d2(const RayState<D>& r,
     umax = fmaf(r.u32[k], v[k], umax);
     umax = fmaf(fabsf(r.u32[k]), v[D + k], umax);
     const float zc = -0.5f * r.z32[k];
+#ifdef VR_NO_FOLD_DEL
     const float e = fmaxf(fabsf(zc - v[k]) - v[D + k] - r.del32, 0.0f);
+#else
+    const float e = fmaxf(fabsf(zc - v[k]) - v[D + k], 0.0f);
+#endif
     d2 = fmaf(e, e, d2);
   }
   if (umax + r.bsl32 <= r.thr32) return false;
+#ifdef VR_NO_FOLD_DEL
   return !(d2 >= r.rb32);
+#else
+  return !(d2 >= r.rbd32);
+#endif
 }
 
 template <int D, bool F32, bool CH = false>
