@@ -16,6 +16,7 @@
 // The caller (DeviceTraversal.level) then grows the edge table if needed and
 // calls vr_trav_finalize / vr_trav_boundary as before.  Results are those of
 // the Python-driven level (the processing order is the same stable sort).
+#include <atomic>
 #include <cub/device/device_scan.cuh>
 
 #include <cstdlib>
@@ -394,10 +395,11 @@ namespace {
 // vertex set, edge counts and boundary rays are those of the unsplit level.
 // A level of F frontier vertices is split so that a round casts about
 // VR_SUB_RAYS rays (estimated as F (d + 1) / 2), at most VR_SUB_MAX rounds.
-int64_t g_sub_rays = -1;  // vr_trav_set_sub_rounds overrides (-1: environment / default)
-int g_sub_max = -1;
+std::atomic<int64_t> g_sub_rays{-1};  // vr_trav_set_sub_rounds overrides (-1: environment / default)
+std::atomic<int> g_sub_max{-1};
 int64_t sub_target_rays() {
-  if (g_sub_rays >= 0) return g_sub_rays;
+  const int64_t o = g_sub_rays.load(std::memory_order_relaxed);
+  if (o >= 0) return o;
   static const int64_t v = [] {
     const char* e = std::getenv("VR_SUB_RAYS");
     return e ? (int64_t)std::atoll(e) : (int64_t)VR_SUB_RAYS_DEFAULT;
@@ -405,7 +407,7 @@ int64_t sub_target_rays() {
   return v;
 }
 int sub_max_rounds() {
-  int m = g_sub_max;
+  int m = g_sub_max.load(std::memory_order_relaxed);
   if (m < 0) {
     static const int v = [] {
       const char* e = std::getenv("VR_SUB_MAX");
@@ -477,8 +479,8 @@ int run_plan(int64_t F, int64_t R, int64_t n_gen, int d, RunPlan& p) {
 }  // namespace
 
 extern "C" int vr_trav_set_sub_rounds(int64_t rays_per_round, int max_rounds) {
-  g_sub_rays = rays_per_round;
-  g_sub_max = max_rounds;
+  g_sub_rays.store(rays_per_round, std::memory_order_relaxed);
+  g_sub_max.store(max_rounds, std::memory_order_relaxed);
   return VR_OK;
 }
 
