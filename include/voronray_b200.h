@@ -433,7 +433,15 @@ typedef struct vr_traverse_tables {
   int64_t vcap;
   int32_t* ekeys;   /* ecap * d sorted eta keys                              */
   int32_t* estate;  /* ecap                                                  */
-  int32_t* ecount;  /* ecap: number of discovered incident vertices          */
+  int32_t* ecount;  /* ecap: number of discovered incident vertices.  The two
+                       arrays may be ONE array of 2 * ecap int32 holding
+                       (state, count) pairs -- pass ecount == estate + 1 -- so
+                       that a slot's state and counter share a 32-B sector (one
+                       random sector less per bump); every vr_trav_* call taking
+                       the tables (and the old-table arguments of
+                       vr_trav_rehash_edges) recognises the pair layout by that
+                       pointer relation.  vr_trav_published reads a plain state
+                       array (stride 1) only.                                */
   int64_t ecap;
   int32_t* overflow;/* 1 int32: set when a probe sequence exhausts a table   */
 } vr_traverse_tables;

@@ -380,7 +380,8 @@ int trav_run_small(const vr_traverse_tables* tab, vr_trav_state* S, const double
   cudaError_t e = cudaMemcpyAsync(B.S, S, sizeof(vr_trav_state), cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return vr_cuda_status(e);
   const Tables t{tab->vkeys, tab->vstate, tab->vval, tab->vlevel, tab->vcap,
-                 tab->ekeys, tab->estate, tab->ecount, tab->ecap, tab->overflow};
+                 tab->ekeys, tab->estate, tab->ecount, tab->ecap, tab->overflow,
+                 edge_stride(tab->estate, tab->ecount)};
   const PrunedIndex pi = pruned_index_from(ix, true);
   const Screen sc = make_screen(sqmax, s32, d);
   int s = VR_OK;

@@ -23,7 +23,19 @@ struct Tables {
   int32_t* ecount;
   int64_t ecap;
   int32_t* overflow;
+  // Stride (in int32) of the edge table's state / count arrays: 2 when they
+  // are interleaved as (state, count) pairs -- ecount == estate + 1, so a
+  // slot's state and counter share one 32-B sector and a bump costs one
+  // random sector less -- else 1 (two separate arrays).
+  int es = 1;
 };
+
+inline int edge_stride(const int32_t* estate, const int32_t* ecount) {
+  return ecount == estate + 1 ? 2 : 1;
+}
+__device__ __forceinline__ int edge_stride_dev(const int32_t* estate, const int32_t* ecount) {
+  return ecount == estate + 1 ? 2 : 1;
+}
 
 template <int KW>
 __device__ __forceinline__ uint64_t hash_key(const int32_t (&k)[KW]) {
@@ -51,12 +63,12 @@ __device__ __forceinline__ bool key_eq(const int32_t* slot, const int32_t (&k)[K
 template <int KW, class Init>
 __device__ int64_t table_insert(int32_t* keys, int32_t* state, int64_t cap,
                                 const int32_t (&k)[KW], bool& inserted, int32_t* overflow,
-                                Init init) {
+                                Init init, int ss = 1) {
   const uint64_t mask = (uint64_t)cap - 1;
   uint64_t h = hash_key<KW>(k) & mask;
   inserted = false;
   for (int64_t probe = 0; probe < cap; ++probe) {
-    dev_atomic st(state[h]);
+    dev_atomic st(state[(int64_t)ss * h]);
     int32_t s = st.load(cuda::memory_order_acquire);
     if (s == 0) {
       int32_t expect = 0;
@@ -81,11 +93,11 @@ __device__ int64_t table_insert(int32_t* keys, int32_t* state, int64_t cap,
 // Lookup only (no concurrent inserts in the same kernel).
 template <int KW>
 __device__ int64_t table_find(const int32_t* keys, const int32_t* state, int64_t cap,
-                              const int32_t (&k)[KW]) {
+                              const int32_t (&k)[KW], int ss = 1) {
   const uint64_t mask = (uint64_t)cap - 1;
   uint64_t h = hash_key<KW>(k) & mask;
   for (int64_t probe = 0; probe < cap; ++probe) {
-    const int32_t s = __ldcg(state + h);
+    const int32_t s = __ldcg(state + (int64_t)ss * h);
     if (s == 0) return -1;
     if (key_eq<KW>(keys + h * KW, k)) return (int64_t)h;
     h = (h + 1) & mask;
@@ -108,8 +120,8 @@ __device__ void bump_edges(const Tables& t, const int32_t (&sig)[D + 1]) {
     edge_of<D>(sig, k, e);
     bool ins;
     const int64_t h = table_insert<D>(t.ekeys, t.estate, t.ecap, e, ins, t.overflow,
-                                      [&](int64_t) {});
-    if (h >= 0) atomicAdd(&t.ecount[h], 1);
+                                      [&](int64_t) {}, t.es);
+    if (h >= 0) atomicAdd(&t.ecount[(int64_t)t.es * h], 1);
   }
 }
 
@@ -135,14 +147,15 @@ __global__ void k_rehash_edges(Tables t, const int32_t* __restrict__ okeys,
                                const int32_t* __restrict__ ostate,
                                const int32_t* __restrict__ ocount, int64_t ocap) {
   const int64_t h0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (h0 >= ocap || ostate[h0] != 2) return;
+  const int os = edge_stride_dev(ostate, ocount);
+  if (h0 >= ocap || ostate[(int64_t)os * h0] != 2) return;
   int32_t e[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) e[a] = okeys[h0 * D + a];
-  const int32_t c = ocount[h0];
+  const int32_t c = ocount[(int64_t)os * h0];
   bool ins;
   table_insert<D>(t.ekeys, t.estate, t.ecap, e, ins, t.overflow,
-                  [&](int64_t h) { t.ecount[h] = c; });
+                  [&](int64_t h) { t.ecount[(int64_t)t.es * h] = c; }, t.es);
 }
 
 // (sub_n, sub_j): sub-rounds of a level -- only the frontier vertices with
@@ -164,8 +177,8 @@ __device__ __forceinline__ void open_edges_one(Tables t, const int32_t* sigma, i
   for (int k = 0; k <= D; ++k) {
     int32_t e[D];
     edge_of<D>(s, k, e);
-    const int64_t h = table_find<D>(t.ekeys, t.estate, t.ecap, e);
-    const int c = h >= 0 ? __ldcg(t.ecount + h) : 0;
+    const int64_t h = table_find<D>(t.ekeys, t.estate, t.ecap, e, t.es);
+    const int c = h >= 0 ? __ldcg(t.ecount + (int64_t)t.es * h) : 0;
     const bool open = c < 2;
     open_mask[v * (D + 1) + k] = open ? 1 : 0;
     cnt += open;
@@ -322,8 +335,8 @@ __global__ void k_bump_keys(Tables t, const int32_t* __restrict__ keys, int64_t 
   for (int a = 0; a < D; ++a) e[a] = keys[k * D + a];
   bool ins;
   const int64_t h = table_insert<D>(t.ekeys, t.estate, t.ecap, e, ins, t.overflow,
-                                    [&](int64_t) {});
-  if (h >= 0) atomicAdd(&t.ecount[h], 1);
+                                    [&](int64_t) {}, t.es);
+  if (h >= 0) atomicAdd(&t.ecount[(int64_t)t.es * h], 1);
 }
 
 template <int D>
@@ -334,8 +347,8 @@ __global__ void k_edge_counts(Tables t, const int32_t* __restrict__ keys, int64_
   int32_t e[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) e[a] = keys[k * D + a];
-  const int64_t h = table_find<D>(t.ekeys, t.estate, t.ecap, e);
-  out[k] = h >= 0 ? __ldcg(t.ecount + h) : 0;
+  const int64_t h = table_find<D>(t.ekeys, t.estate, t.ecap, e, t.es);
+  out[k] = h >= 0 ? __ldcg(t.ecount + (int64_t)t.es * h) : 0;
 }
 
 template <int D>
@@ -455,11 +468,11 @@ template <int D>
 __global__ void k_edge_compact(Tables t, const int64_t* __restrict__ off,
                                int32_t* __restrict__ out_keys, int32_t* __restrict__ out_count) {
   const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (h >= t.ecap || t.estate[h] != 2) return;
+  if (h >= t.ecap || t.estate[(int64_t)t.es * h] != 2) return;
   const int64_t o = off[h];
 #pragma unroll
   for (int a = 0; a < D; ++a) out_keys[o * D + a] = t.ekeys[h * D + a];
-  out_count[o] = t.ecount[h];
+  out_count[o] = t.ecount[(int64_t)t.es * h];
 }
 
 __global__ void k_published(const int32_t* __restrict__ state, int64_t cap, int32_t* flag) {

@@ -26,7 +26,8 @@ inline unsigned nb(int64_t n, int nt = 256) { return (unsigned)((n + nt - 1) / n
 
 Tables from(const vr_traverse_tables* p) {
   return Tables{p->vkeys, p->vstate, p->vval, p->vlevel, p->vcap,
-                p->ekeys, p->estate, p->ecount, p->ecap, p->overflow};
+                p->ekeys, p->estate, p->ecount, p->ecap, p->overflow,
+                edge_stride(p->estate, p->ecount)};
 }
 
 bool pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
@@ -41,14 +42,14 @@ bool pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
 constexpr int EC_NT = 256, EC_PER = 16, EC_CHUNK = EC_NT * EC_PER;
 
 __global__ void __launch_bounds__(EC_NT) k_count_published(const int32_t* __restrict__ state,
-                                                           int64_t cap,
+                                                           int ss, int64_t cap,
                                                            int64_t* __restrict__ chunk_cnt) {
   const int64_t base = (int64_t)blockIdx.x * EC_CHUNK;
   int c = 0;
 #pragma unroll
   for (int i = 0; i < EC_PER; ++i) {
     const int64_t h = base + i * EC_NT + threadIdx.x;
-    c += (h < cap && state[h] == 2) ? 1 : 0;
+    c += (h < cap && state[(int64_t)ss * h] == 2) ? 1 : 0;
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(EC_NT) k_compact_published(Tables t,
 #pragma unroll
   for (int i = 0; i < EC_PER; ++i) {
     const int64_t h = base + i;
-    if (h < t.ecap && t.estate[h] == 2) m |= 1u << i;
+    if (h < t.ecap && t.estate[(int64_t)t.es * h] == 2) m |= 1u << i;
   }
   const int c = __popc(m);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -106,7 +107,7 @@ __global__ void k_gather_edges(Tables t, const int64_t* __restrict__ out_slot, i
     const int a = (int)(q - o * (D + 1));
     const int64_t h = out_slot[o];
     if (a < D) out_keys[o * D + a] = t.ekeys[h * D + a];
-    else out_count[o] = t.ecount[h];
+    else out_count[o] = t.ecount[(int64_t)t.es * h];
   }
 }
 
@@ -129,7 +130,9 @@ extern "C" int vr_trav_edges_count(const vr_traverse_tables* tab, int64_t* chunk
   cudaStream_t st = as_stream(stream);
   cudaError_t e = cudaMemsetAsync(chunk_off + nc, 0, sizeof(int64_t), st);
   if (e != cudaSuccess) return vr_cuda_status(e);
-  k_count_published<<<(unsigned)nc, EC_NT, 0, st>>>(tab->estate, tab->ecap, chunk_off);
+  k_count_published<<<(unsigned)nc, EC_NT, 0, st>>>(tab->estate,
+                                                    edge_stride(tab->estate, tab->ecount),
+                                                    tab->ecap, chunk_off);
   if ((e = cudaGetLastError()) != cudaSuccess) return vr_cuda_status(e);
   // in-place exclusive scan over nc + 1 entries: chunk_off[nc] = total
   if ((e = cub::DeviceScan::ExclusiveSum(workspace, tmp, chunk_off, chunk_off, (int)(nc + 1),

@@ -492,8 +492,11 @@ class DeviceTraversal:
 
     def _alloc_etable(self, cap):
         self.ekeys = torch.empty(cap * self.d, dtype=torch.int32, device=self.dev)
-        self.estate = torch.zeros(cap, dtype=torch.int32, device=self.dev)
-        self.ecount = torch.zeros(cap, dtype=torch.int32, device=self.dev)
+        # (state, count) pairs of the slots interleaved: ecount == estate + 1 tells
+        # the library, and a slot's state and counter share one 32-B sector
+        self.epairs = torch.zeros(2 * cap, dtype=torch.int32, device=self.dev)
+        self.estate = self.epairs[0::2]
+        self.ecount = self.epairs[1::2]
         self.ecap = cap
 
     def tables(self):

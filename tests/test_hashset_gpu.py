@@ -32,11 +32,14 @@ def _p(t):
 class Tabs:
     """Bare vertex / edge tables for dimension d (capacities powers of two)."""
 
-    def __init__(self, d, vcap, ecap):
+    def __init__(self, d, vcap, ecap, pairs=False):
         z = lambda n: torch.zeros(n, dtype=torch.int32, device=DEV)  # noqa: E731
         self.d = d
         self.vkeys, self.vstate, self.vval, self.vlevel = z(vcap * (d + 1)), z(vcap), z(vcap), z(vcap)
         self.ekeys, self.estate, self.ecount = z(ecap * d), z(ecap), z(ecap)
+        if pairs:  # (state, count) pairs in one array: ecount == estate + 1
+            self.epairs = z(2 * ecap)
+            self.estate, self.ecount = self.epairs[0::2], self.epairs[1::2]
         self.overflow = z(1)
         self.T = _Tables(_p(self.vkeys).value, _p(self.vstate).value, _p(self.vval).value,
                          _p(self.vlevel).value, vcap, _p(self.ekeys).value, _p(self.estate).value,
@@ -110,15 +113,16 @@ def test_claim_sigma_under_contention(d, vcap, copies):
         assert int(newf2.sum()) == len(fresh)
 
 
+@pytest.mark.parametrize("pairs", [False, True])
 @pytest.mark.parametrize("d,ecap", [(3, 1 << 14), (6, 1 << 14), (8, 1 << 13)])
-def test_bump_keys_counts_every_bump(d, ecap):
+def test_bump_keys_counts_every_bump(d, ecap, pairs):
     rng = np.random.default_rng(10 + d)
     k = int(0.9 * ecap)  # long probe chains
     keys = _distinct_sorted_rows(rng, k, d, 10 ** 6)
     mult = rng.integers(1, 40, k)
     which = np.repeat(np.arange(k), mult)
     rng.shuffle(which)
-    tb = Tabs(d, 1 << 10, ecap)
+    tb = Tabs(d, 1 << 10, ecap, pairs=pairs)
     out = tb.bump(torch.from_numpy(keys[which]).to(DEV))
     assert int(tb.overflow.item()) == 0
     assert np.array_equal(out, mult[which]), "lost or duplicated edge bumps"
