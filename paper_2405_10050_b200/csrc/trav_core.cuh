@@ -119,9 +119,12 @@ __device__ void bump_edges(const Tables& t, const int32_t (&sig)[D + 1]) {
     int32_t e[D];
     edge_of<D>(sig, k, e);
     bool ins;
+    // the inserting bump writes count = 1 before the slot is published (one
+    // plain store in the sector being written anyway); only a later bump of a
+    // published slot pays the atomic -- about half of all bumps
     const int64_t h = table_insert<D>(t.ekeys, t.estate, t.ecap, e, ins, t.overflow,
-                                      [&](int64_t) {}, t.es);
-    if (h >= 0) atomicAdd(&t.ecount[(int64_t)t.es * h], 1);
+                                      [&](int64_t hh) { t.ecount[(int64_t)t.es * hh] = 1; }, t.es);
+    if (h >= 0 && !ins) atomicAdd(&t.ecount[(int64_t)t.es * h], 1);
   }
 }
 
@@ -335,8 +338,8 @@ __global__ void k_bump_keys(Tables t, const int32_t* __restrict__ keys, int64_t 
   for (int a = 0; a < D; ++a) e[a] = keys[k * D + a];
   bool ins;
   const int64_t h = table_insert<D>(t.ekeys, t.estate, t.ecap, e, ins, t.overflow,
-                                    [&](int64_t) {}, t.es);
-  if (h >= 0) atomicAdd(&t.ecount[(int64_t)t.es * h], 1);
+                                    [&](int64_t hh) { t.ecount[(int64_t)t.es * hh] = 1; }, t.es);
+  if (h >= 0 && !ins) atomicAdd(&t.ecount[(int64_t)t.es * h], 1);
 }
 
 template <int D>
