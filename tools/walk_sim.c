@@ -99,8 +99,12 @@ static int need(const Tree* T, const Ray* r, int64_t node, double* lb, double* d
 
 static int sub_rows = 0;        /* 0: off; else rows per sub-box */
 static int64_t sub_needed = 0;  /* sub-boxes needed over the batch */
-void set_sub(int v) { sub_rows = v; sub_needed = 0; }
+static int64_t sub_needed_sph = 0;  /* same groups with bounding SPHERES (centroid, max distance):
+                                       the test |z - c| < rho + r is bilinear in (z, rho) x (c, r),
+                                       i.e. it could run on the tensor core */
+void set_sub(int v) { sub_rows = v; sub_needed = 0; sub_needed_sph = 0; }
 int64_t get_sub_needed(void) { return sub_needed; }
+int64_t get_sub_needed_sph(void) { return sub_needed_sph; }
 
 static void count_subs(const Tree* T, const Ray* r, int64_t tile) {
   const int d = T->d;
@@ -126,6 +130,31 @@ static void count_subs(const Tree* T, const Ray* r, int64_t tile) {
       um += r->u[k] * (r->u[k] > 0 ? hi[k] : lo[k]);
     }
     if (um > r->thr && dz < rho2) ++sub_needed;
+    /* bounding sphere of the same rows */
+    double c[16], rad2 = 0, cz = 0, uc = 0;
+    int cnt = 0;
+    for (int k = 0; k < d; ++k) c[k] = 0;
+    for (int j = s0; j < s0 + sub_rows; ++j) {
+      const double* y = T->rec + (tile * T->pt + j) * T->rs;
+      if (isinf(y[d])) continue;
+      ++cnt;
+      for (int k = 0; k < d; ++k) c[k] += y[k];
+    }
+    for (int k = 0; k < d; ++k) c[k] /= cnt;
+    for (int j = s0; j < s0 + sub_rows; ++j) {
+      const double* y = T->rec + (tile * T->pt + j) * T->rs;
+      if (isinf(y[d])) continue;
+      double q = 0;
+      for (int k = 0; k < d; ++k) q += (y[k] - c[k]) * (y[k] - c[k]);
+      rad2 = fmax(rad2, q);
+    }
+    for (int k = 0; k < d; ++k) {
+      double z = r->x[k] + (isfinite(r->tb) ? r->tb : 0) * r->u[k];
+      cz += (z - c[k]) * (z - c[k]);
+      uc += r->u[k] * c[k];
+    }
+    const double rad = sqrt(rad2);
+    if (uc + rad > r->thr && (!isfinite(rho2) || sqrt(cz) < sqrt(rho2) + rad)) ++sub_needed_sph;
   }
 }
 

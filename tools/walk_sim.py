@@ -113,6 +113,7 @@ def main(nray=int(os.environ.get("NRAY", "1500"))):
     names = {0: "start-tile child first", 1: "nearest (d2) first", 2: "lower bound first (DFS)",
              3: "best-first (LB heap)"}
     W.get_sub_needed.restype = ctypes.c_int64
+    W.get_sub_needed_sph.restype = ctypes.c_int64
     W.set_joint(0)
 
     def kd_within_tiles(rec, levels):
@@ -139,7 +140,8 @@ def main(nray=int(os.environ.get("NRAY", "1500"))):
             tl, ts, ag = run(0, "oracle", 1)
             print(f"{tag}: oracle seed, {sub}-row sub-boxes: tiles/ray {tl:.2f} -> pairs/ray "
                   f"{64 * tl:.0f}; needed sub-boxes/ray {W.get_sub_needed() / n:.2f} -> pairs/ray "
-                  f"{sub * W.get_sub_needed() / n:.0f}", flush=True)
+                  f"{sub * W.get_sub_needed() / n:.0f}; with bounding spheres "
+                  f"{W.get_sub_needed_sph() / n:.2f} -> {sub * W.get_sub_needed_sph() / n:.0f}", flush=True)
     rec = rec_orig
     W.set_sub(0)
     for seedmode in ("oracle", "own"):
