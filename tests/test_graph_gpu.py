@@ -195,6 +195,41 @@ def test_sub_rounds_same_mesh_fewer_rays(rounds):
     assert rep.passed
 
 
+@pytest.mark.parametrize("d", [2, 4, 7])
+def test_sub_rounds_fuzz(d, monkeypatch):
+    """Random inputs (uniform, Gaussian, clustered) at several sub-round
+    settings: the sorted vertex set, circumcentres, edge table and boundary
+    multiset equal the unsplit traversal's, and no setting casts more rays."""
+    monkeypatch.setenv("VR_SMALL_LEVELS", "0")
+    rng = np.random.default_rng(900 + d)
+    n = {2: 1500, 4: 600, 7: 120}[d]
+    cases = [rng.random((n, d)), rng.standard_normal((n, d)),
+             np.vstack([rng.normal(0.0, 0.05, (n // 2, d)), rng.random((n - n // 2, d))])]
+
+    def canon(mesh):
+        a = mesh.arrays()
+        o = np.lexsort(a["sigma"].T[::-1])
+        bk = np.hstack([a["boundary_sigma"].astype(np.float64), a["boundary_u"]])
+        ob = np.lexsort(bk.T[::-1])
+        return (a["sigma"][o], a["r"][o], a["edge_key"], a["edge_count"],
+                a["boundary_sigma"][ob], a["boundary_u"][ob])
+    try:
+        for pts in cases:
+            ns = vb.build_node_set(pts)
+            vb.set_sub_rounds(0, 1)
+            st0 = vb.RaycastStats()
+            ref = canon(vb.voronoi_graph(ns, seed=1, stats=st0))
+            for rays, mx in ((1, 2), (50, 3), (1, 17), (400, 64)):
+                vb.set_sub_rounds(rays, mx)
+                st = vb.RaycastStats()
+                got = canon(vb.voronoi_graph(ns, seed=1, stats=st))
+                for x, y in zip(ref, got):
+                    assert np.array_equal(x, y), (d, rays, mx)
+                assert st.raycasts <= st0.raycasts
+    finally:
+        vb.set_sub_rounds(-1, -1)
+
+
 def test_sub_rounds_local_traversal_levels():
     """L-hop traversal with sub-rounds: same vertex set and hop levels."""
     pts = np.random.default_rng(5).random((20000, 6))
